@@ -1,0 +1,247 @@
+/*
+ * fs4d.h — C ABI of libfs4d.so, the sm_100a implementation of the FE-4DGS
+ * per-frame render path (HexPlane+MLP deformation, tile rasterizer, and their
+ * analytic backward passes).
+ *
+ * The reference (`featsplat`, /root/reference/pkg/src/featsplat) is pure
+ * Python/NumPy and has no FFI; its "plugin boundary" is a set of Python
+ * functions.  Every entry point below replaces one of them and cites it:
+ *
+ *   fs4d_deform_fwd   <- deformation.deform_with_cache   deformation.py:105-136
+ *                        (hexplane.query_with_cache       hexplane.py:118-142,
+ *                         numerics.mlp_forward            numerics.py:56-75)
+ *   fs4d_deform_bwd   <- deformation.deform_backward     deformation.py:139-183
+ *                        (hexplane.query_backward         hexplane.py:145-187,
+ *                         numerics.mlp_backward           numerics.py:78-105)
+ *   fs4d_render_fwd   <- rasterizer.render               rasterizer.py:264-303
+ *                        (project :117-185, bin_tiles :188-207,
+ *                         _tile_alphas :215-234, _composite_weights :244-261)
+ *   fs4d_render_bwd   <- rasterizer.render_backward      rasterizer.py:320-452
+ *                        (gaussians.covariance_backward   gaussians.py:203-218)
+ *   fs4d_render_export_projected / fs4d_render_export_tiles
+ *                     <- rasterizer.project / bin_tiles results (ProjectedGaussians,
+ *                        per-tile lists) read back from a forward record.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers unless stated; all float data is fp32,
+ *    row-major in the reference's logical layout ([K,3] positions, [K,4]
+ *    (w,x,y,z) rotations, [H,W,C] images, [Ra,Rb,C] planes, [out,in] weights).
+ *  - Every call is stream-ordered, allocation-free and never synchronises the
+ *    device.  Host-detectable errors (bad configuration, skewed intrinsics,
+ *    record/snapshot mismatch, undersized workspace) are returned directly.
+ *    Device-detected errors (non-finite parameters, degenerate quaternions,
+ *    pair-buffer overflow) are written to the caller's device status block
+ *    (FS4D_STATUS_WORDS int32) and read by the host when it chooses to.
+ *  - Error codes mirror featsplat/errors.py:4-35 and the CLI exit codes.
+ */
+#ifndef FS4D_H_
+#define FS4D_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS4D_ABI_VERSION 1
+
+/* status / return codes (errors.py:4-35) */
+#define FS4D_OK 0
+#define FS4D_ERR_CONFIG 1        /* ConfigurationError                    */
+#define FS4D_ERR_DATA 2          /* DataError (e.g. skewed intrinsics)    */
+#define FS4D_ERR_NUMERIC 3       /* NumericalError (non-finite inputs)    */
+#define FS4D_ERR_CONTRACT 4      /* ContractViolation (stale record)      */
+#define FS4D_ERR_CAPACITY 5      /* pair buffer too small: grow + retry   */
+#define FS4D_ERR_DEGENERATE 6    /* DegenerateRotationError (|q|<1e-12)   */
+#define FS4D_ERR_CUDA 7          /* CUDA launch failure                   */
+
+/* device status block layout (int32 words) */
+#define FS4D_STATUS_WORDS 32
+#define FS4D_ST_CODE 0           /* first device error code (atomicCAS)       */
+#define FS4D_ST_BAD_FIELDS 1     /* bitmask of cloud fields with non-finite   */
+#define FS4D_ST_N_VISIBLE 2      /* kept Gaussians after culls (M)            */
+#define FS4D_ST_PAIRS_LO 3       /* total (tile, Gaussian) pairs, low word    */
+#define FS4D_ST_PAIRS_HI 4       /*                              high word    */
+#define FS4D_ST_BAD_INDEX 8      /* 8 words: first bad index per field        */
+#define FS4D_ST_DEGEN_INDEX 16   /* first degenerate-quaternion index         */
+
+/* cloud field ids (order of rasterizer.py:120-127 finite checks) */
+#define FS4D_FIELD_POSITIONS 0
+#define FS4D_FIELD_ROTATIONS 1
+#define FS4D_FIELD_LOG_SCALES 2
+#define FS4D_FIELD_OPACITY 3
+#define FS4D_FIELD_COLORS 4
+#define FS4D_FIELD_FEATURES 5
+#define FS4D_FIELD_SH 6
+
+#define FS4D_MAX_LEVELS 8
+#define FS4D_MAX_TRUNK 16
+#define FS4D_N_BRANCHES 4        /* position, rotation, scale, opacity (deformation.py:19) */
+
+/* GaussianCloud (gaussians.py:39-94) as SoA device arrays.  sh_rest is the
+ * build's SH extension ([K, (L+1)^2-1, 3], degree-0 term is colors_raw);
+ * NULL when sh_degree == 0. */
+typedef struct Fs4dCloud {
+  int64_t K;
+  int32_t D;          /* feature channels N */
+  int32_t sh_degree;  /* 0..3 */
+  float* positions;       /* [K,3] */
+  float* rotations;       /* [K,4] raw (w,x,y,z) */
+  float* log_scales;      /* [K,3] */
+  float* opacity_logits;  /* [K]   */
+  float* colors_raw;      /* [K,3] */
+  float* sh_rest;         /* [K,(L+1)^2-1,3] or NULL */
+  float* features;        /* [K,D] */
+} Fs4dCloud;
+
+/* CameraFrame intrinsics/extrinsics (gaussians.py:97-133) in float64. */
+typedef struct Fs4dCamera {
+  int32_t height, width;
+  double K[9];   /* 3x3 row-major */
+  double T[16];  /* 4x4 world->camera, row-major */
+} Fs4dCamera;
+
+/* RasterConfig (rasterizer.py:26-35). */
+typedef struct Fs4dRasterConfig {
+  int32_t tile;            /* only 16 is implemented on device */
+  int32_t with_features;
+  double z_near, lowpass, alpha_cap, alpha_skip, stop_transmittance;
+  double background[3];
+} Fs4dRasterConfig;
+
+/* Sizes a render record (workspace) is laid out for; passed unchanged to the
+ * forward and the backward call (the record's snapshot_len/height/width
+ * contract, rasterizer.py:330-331). */
+typedef struct Fs4dRecordInfo {
+  int64_t K;
+  int32_t height, width, D, sh_degree, tile, pad_;
+  int64_t pair_capacity;
+} Fs4dRecordInfo;
+
+/* RenderOutput images (rasterizer.py:95-100), all device, row-major. */
+typedef struct Fs4dImages {
+  float* color;      /* [H,W,3] */
+  float* depth;      /* [H,W]   */
+  float* feature;    /* [H,W,D] (D = 0 when with_features == 0) */
+  float* alpha;      /* [H,W]   */
+  int32_t* n_contrib;/* [H,W] live contributor count (RenderOutput.pixel_record), may be NULL */
+} Fs4dImages;
+
+/* Upstream image gradients for render_backward; NULL == zeros. */
+typedef struct Fs4dImageGrads {
+  const float* d_color;   /* [H,W,3] */
+  const float* d_depth;   /* [H,W]   */
+  const float* d_feature; /* [H,W,D] */
+  const float* d_alpha;   /* [H,W]   */
+} Fs4dImageGrads;
+
+/* ProjectedGaussians export (rasterizer.py:38-61), depth-sorted, M rows. */
+typedef struct Fs4dProjected {
+  float* mean2d;        /* [K,2]   */
+  float* cov2d;         /* [K,3]   (a, b, c) of the symmetric 2x2 */
+  float* conic;         /* [K,3]   */
+  float* view_depth;    /* [K]     */
+  float* radius;        /* [K]     */
+  float* color;         /* [K,3]   */
+  float* opacity;       /* [K]     */
+  int32_t* source_index;/* [K]     */
+  int32_t* tiles_touched;/*[K]     */
+} Fs4dProjected;
+
+/* HexPlaneField (hexplane.py:49-92). planes[l][p] is [res[l][p][0], res[l][p][1], channels]. */
+typedef struct Fs4dHexPlane {
+  int32_t levels, channels;
+  int32_t res[FS4D_MAX_LEVELS][6][2];
+  float* planes[FS4D_MAX_LEVELS][6];
+  double aabb[6];  /* lo xyz, hi xyz */
+} Fs4dHexPlane;
+
+/* LinearLayer (numerics.py:17-41): y = act(x W^T + b), W [out,in]. */
+typedef struct Fs4dLinear {
+  float* weight;
+  float* bias;
+  int32_t in_dim, out_dim, relu;
+} Fs4dLinear;
+
+/* DeformationNet (deformation.py:32-73).  Branch order: position, rotation,
+ * scale, opacity.  The same struct carries gradient buffers in deform_bwd. */
+typedef struct Fs4dDeformNet {
+  int32_t latent_dim, width, depth, feature_dim;
+  int32_t enable_grid, enable_feature_update;
+  Fs4dLinear trunk[FS4D_MAX_TRUNK];
+  Fs4dLinear ext[FS4D_N_BRANCHES][2];
+  Fs4dLinear head[FS4D_N_BRANCHES];
+  Fs4dLinear feat[2];
+} Fs4dDeformNet;
+
+/* ---- library info ---- */
+int fs4d_abi_version(void);
+const char* fs4d_last_error(void);          /* thread-local message of the last failing call */
+const char* fs4d_build_info(void);
+
+/* Initialise a device status block (FS4D_STATUS_WORDS int32) before a call:
+ * zero codes/counters, INT32_MAX in the first-index slots. */
+int fs4d_status_reset(int32_t* status, void* stream);
+
+/* ---- deformation ---- */
+/* Bytes of device scratch the deform calls need (packed weights + per-CTA
+ * weight-gradient partials for the backward). */
+size_t fs4d_deform_workspace_bytes(const Fs4dDeformNet* net, int64_t K);
+
+/* deform_with_cache: writes snapshot->{positions, rotations, log_scales,
+ * opacity_logits, features}; colors_raw / sh_rest are aliased by the caller
+ * (deformation.py:131), as are features when enable_feature_update == 0. */
+int fs4d_deform_fwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field,
+                    const Fs4dDeformNet* net, double t, Fs4dCloud* snapshot,
+                    void* workspace, size_t workspace_bytes,
+                    int32_t* status, void* stream);
+
+/* deform_backward: snapshot_grads carries dL/d{positions, rotations,
+ * log_scales, opacity_logits, features} of the snapshot.  Writes cloud_grads
+ * (positions incl. the grid term, others pass through), net_grads (weight /
+ * bias pointers of the struct, zeroed and accumulated) and plane_grads
+ * (shapes of field->planes, zeroed and accumulated; ignored when
+ * enable_grid == 0). */
+int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field,
+                    const Fs4dDeformNet* net, double t,
+                    const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads,
+                    Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads,
+                    void* workspace, size_t workspace_bytes,
+                    int32_t* status, void* stream);
+
+/* ---- rasterizer ---- */
+size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info);
+
+/* render: project -> depth sort -> tile binning -> per-tile blend.  The
+ * workspace becomes the RasterRecord replayed by fs4d_render_bwd. */
+int fs4d_render_fwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam,
+                    const Fs4dRasterConfig* cfg, const Fs4dRecordInfo* info,
+                    void* workspace, size_t workspace_bytes,
+                    Fs4dImages* out, int32_t* status, void* stream);
+
+/* render_backward: grads->{positions, rotations, log_scales, opacity_logits,
+ * colors_raw, sh_rest, features} are fully written (zeros for culled rows).
+ * viewspace_index / viewspace_norm get the first M entries (depth order). */
+int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam,
+                    const Fs4dRasterConfig* cfg, const Fs4dRecordInfo* info,
+                    void* workspace, size_t workspace_bytes,
+                    const Fs4dImageGrads* upstream, Fs4dCloud* grads,
+                    int32_t* viewspace_index, float* viewspace_norm,
+                    int32_t* status, void* stream);
+
+/* Read back a forward record: depth-sorted ProjectedGaussians (first M rows). */
+int fs4d_render_export_projected(const Fs4dRecordInfo* info, const void* workspace,
+                                 size_t workspace_bytes, Fs4dProjected* out,
+                                 void* stream);
+
+/* Read back tile lists: tile_ranges [n_tiles,2] (start,end) into pair_values
+ * [pairs] (depth rank of the Gaussian, i.e. row of the ProjectedGaussians). */
+int fs4d_render_export_tiles(const Fs4dRecordInfo* info, const void* workspace,
+                             size_t workspace_bytes, int32_t* tile_ranges,
+                             int32_t* pair_rows, int64_t max_pairs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FS4D_H_ */

@@ -1,0 +1,189 @@
+// extern "C" surface of libfs4d.so (declared in include/fs4d.h).
+#include <stdio.h>
+#include <string.h>
+
+#include "render_common.cuh"
+
+namespace fs4d {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(FS4D_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return FS4D_OK;
+}
+
+// defined in the kernel translation units
+int render_forward(const Fs4dCloud&, const Fs4dCamera&, const Fs4dRasterConfig&, const RenderLayout&, void*,
+                   Fs4dImages&, int32_t*, cudaStream_t);
+int render_backward(const Fs4dCloud&, const Fs4dCamera&, const Fs4dRasterConfig&, const RenderLayout&, void*,
+                    const Fs4dImageGrads&, Fs4dCloud&, int32_t*, float*, cudaStream_t);
+int render_export_projected(const RenderLayout&, void*, Fs4dProjected&, cudaStream_t);
+int render_export_tiles(const RenderLayout&, void*, int32_t*, int32_t*, int64_t, cudaStream_t);
+size_t deform_workspace_bytes(const Fs4dDeformNet& net, int64_t K, int* nparts_out);
+int deform_forward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, Fs4dCloud&, void*, size_t,
+                   cudaStream_t);
+int deform_backward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, const Fs4dCloud&, Fs4dCloud&,
+                    Fs4dDeformNet&, Fs4dHexPlane*, void*, size_t, cudaStream_t);
+
+static int check_cloud(const Fs4dCloud* c, bool need_colors) {
+  if (!c) return fail(FS4D_ERR_CONFIG, "null cloud");
+  if (c->K < 0 || c->K > 0x7FFFFFFF) return fail(FS4D_ERR_CONFIG, "cloud size out of range");
+  if (c->D < 0) return fail(FS4D_ERR_CONFIG, "negative feature dimension");
+  if (c->sh_degree < 0 || c->sh_degree > 3) return fail(FS4D_ERR_CONFIG, "sh_degree must be in [0, 3]");
+  if (c->K > 0) {
+    if (!c->positions || !c->rotations || !c->log_scales || !c->opacity_logits)
+      return fail(FS4D_ERR_CONFIG, "cloud pointer missing");
+    if (need_colors && !c->colors_raw) return fail(FS4D_ERR_CONFIG, "cloud colors missing");
+    if (c->D > 0 && !c->features) return fail(FS4D_ERR_CONFIG, "cloud features missing");
+    if (c->sh_degree > 0 && !c->sh_rest) return fail(FS4D_ERR_CONFIG, "sh_rest missing for sh_degree > 0");
+  }
+  return FS4D_OK;
+}
+
+static int check_camera(const Fs4dCamera* cam) {
+  if (!cam) return fail(FS4D_ERR_CONFIG, "null camera");
+  if (cam->height <= 0 || cam->width <= 0) return fail(FS4D_ERR_DATA, "image size must be positive");
+  if (!(cam->K[0] > 0) || !(cam->K[4] > 0)) return fail(FS4D_ERR_DATA, "intrinsics must have positive focal lengths");
+  // rasterizer.py:128-130
+  if (cam->K[1] > 1e-9 || cam->K[1] < -1e-9) return fail(FS4D_ERR_DATA, "intrinsics with skew are not supported");
+  return FS4D_OK;
+}
+
+static int check_record(const Fs4dRecordInfo* info, const Fs4dCloud* snap, const Fs4dCamera* cam,
+                        const Fs4dRasterConfig* cfg, size_t ws_bytes, const void* ws) {
+  if (!info || !cfg) return fail(FS4D_ERR_CONFIG, "null record info / config");
+  if (cfg->tile != kTile) return fail(FS4D_ERR_CONFIG, "only tile = 16 is implemented on device");
+  if (info->pair_capacity < 0) return fail(FS4D_ERR_CONFIG, "negative pair capacity");
+  if (info->pair_capacity > 0x7FFFFFFFll) return fail(FS4D_ERR_CONFIG, "pair capacity above 2^31");
+  // rasterizer.py:330-331 (stale record)
+  if (snap && info->K != snap->K) return fail(FS4D_ERR_CONTRACT, "record does not match this snapshot/frame");
+  if (cam && (info->height != cam->height || info->width != cam->width))
+    return fail(FS4D_ERR_CONTRACT, "record does not match this snapshot/frame");
+  if (snap && info->D != snap->D) return fail(FS4D_ERR_CONTRACT, "record feature dimension mismatch");
+  RenderLayout L = make_layout(*info);
+  if (!ws || ws_bytes < L.total) return fail(FS4D_ERR_CONFIG, "render workspace too small");
+  return FS4D_OK;
+}
+
+__global__ void k_status_reset(int32_t* st) {
+  int i = threadIdx.x;
+  if (i < FS4D_STATUS_WORDS)
+    st[i] = (i >= FS4D_ST_BAD_INDEX && i <= FS4D_ST_DEGEN_INDEX) ? 0x7FFFFFFF : 0;
+}
+
+}  // namespace fs4d
+
+using namespace fs4d;
+
+extern "C" {
+
+int fs4d_abi_version(void) { return FS4D_ABI_VERSION; }
+
+const char* fs4d_last_error(void) { return g_last_error.c_str(); }
+
+const char* fs4d_build_info(void) {
+  static char buf[256];
+  snprintf(buf, sizeof(buf), "libfs4d abi=%d arch=sm_100a cuda=%d.%d", FS4D_ABI_VERSION, CUDART_VERSION / 1000,
+           (CUDART_VERSION % 1000) / 10);
+  return buf;
+}
+
+int fs4d_status_reset(int32_t* status, void* stream) {
+  if (!status) return fail(FS4D_ERR_CONFIG, "null status block");
+  k_status_reset<<<1, FS4D_STATUS_WORDS, 0, (cudaStream_t)stream>>>(status);
+  return check_launch("status_reset");
+}
+
+size_t fs4d_deform_workspace_bytes(const Fs4dDeformNet* net, int64_t K) {
+  if (!net) return 0;
+  return deform_workspace_bytes(*net, K, nullptr);
+}
+
+int fs4d_deform_fwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net, double t,
+                    Fs4dCloud* snapshot, void* workspace, size_t workspace_bytes, int32_t* status, void* stream) {
+  (void)status;
+  int rc = check_cloud(cloud, false);
+  if (rc) return rc;
+  if (!field || !net || !snapshot) return fail(FS4D_ERR_CONFIG, "null deform argument");
+  if (snapshot->K != cloud->K) return fail(FS4D_ERR_CONFIG, "snapshot size mismatch");
+  return deform_forward(*cloud, *field, *net, t, *snapshot, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net, double t,
+                    const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads, Fs4dDeformNet* net_grads,
+                    Fs4dHexPlane* plane_grads, void* workspace, size_t workspace_bytes, int32_t* status,
+                    void* stream) {
+  (void)status;
+  int rc = check_cloud(cloud, false);
+  if (rc) return rc;
+  if (!field || !net || !snapshot_grads || !cloud_grads || !net_grads)
+    return fail(FS4D_ERR_CONFIG, "null deform_bwd argument");
+  if (snapshot_grads->K != cloud->K || cloud_grads->K != cloud->K)
+    return fail(FS4D_ERR_CONTRACT, "gradient rows do not match the cloud");
+  return deform_backward(*cloud, *field, *net, t, *snapshot_grads, *cloud_grads, *net_grads, plane_grads, workspace,
+                         workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info) {
+  if (!info) return 0;
+  return make_layout(*info).total;
+}
+
+int fs4d_render_fwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam, const Fs4dRasterConfig* cfg,
+                    const Fs4dRecordInfo* info, void* workspace, size_t workspace_bytes, Fs4dImages* out,
+                    int32_t* status, void* stream) {
+  int rc = check_cloud(snapshot, true);
+  if (rc) return rc;
+  if ((rc = check_camera(cam))) return rc;
+  if ((rc = check_record(info, snapshot, cam, cfg, workspace_bytes, workspace))) return rc;
+  if (!out || !out->color || !out->depth || !out->alpha) return fail(FS4D_ERR_CONFIG, "null output image");
+  if (cfg->with_features && snapshot->D > 0 && !out->feature) return fail(FS4D_ERR_CONFIG, "null feature image");
+  RenderLayout L = make_layout(*info);
+  return render_forward(*snapshot, *cam, *cfg, L, workspace, *out, status, (cudaStream_t)stream);
+}
+
+int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam, const Fs4dRasterConfig* cfg,
+                    const Fs4dRecordInfo* info, void* workspace, size_t workspace_bytes,
+                    const Fs4dImageGrads* upstream, Fs4dCloud* grads, int32_t* viewspace_index,
+                    float* viewspace_norm, int32_t* status, void* stream) {
+  (void)status;
+  int rc = check_cloud(snapshot, true);
+  if (rc) return rc;
+  if ((rc = check_camera(cam))) return rc;
+  if ((rc = check_record(info, snapshot, cam, cfg, workspace_bytes, workspace))) return rc;
+  if (!upstream || !grads || !viewspace_index || !viewspace_norm) return fail(FS4D_ERR_CONFIG, "null backward argument");
+  if (grads->K != snapshot->K || grads->D != snapshot->D || grads->sh_degree != snapshot->sh_degree)
+    return fail(FS4D_ERR_CONFIG, "gradient buffers do not match the snapshot");
+  if (cfg->with_features && snapshot->D > 64)
+    return fail(FS4D_ERR_CONFIG, "render backward supports at most 64 feature channels");
+  RenderLayout L = make_layout(*info);
+  return render_backward(*snapshot, *cam, *cfg, L, workspace, *upstream, *grads, viewspace_index, viewspace_norm,
+                         (cudaStream_t)stream);
+}
+
+int fs4d_render_export_projected(const Fs4dRecordInfo* info, const void* workspace, size_t workspace_bytes,
+                                 Fs4dProjected* out, void* stream) {
+  if (!info || !out) return fail(FS4D_ERR_CONFIG, "null export argument");
+  RenderLayout L = make_layout(*info);
+  if (!workspace || workspace_bytes < L.total) return fail(FS4D_ERR_CONFIG, "render workspace too small");
+  return render_export_projected(L, const_cast<void*>(workspace), *out, (cudaStream_t)stream);
+}
+
+int fs4d_render_export_tiles(const Fs4dRecordInfo* info, const void* workspace, size_t workspace_bytes,
+                             int32_t* tile_ranges, int32_t* pair_rows, int64_t max_pairs, void* stream) {
+  if (!info) return fail(FS4D_ERR_CONFIG, "null export argument");
+  RenderLayout L = make_layout(*info);
+  if (!workspace || workspace_bytes < L.total) return fail(FS4D_ERR_CONFIG, "render workspace too small");
+  return render_export_tiles(L, const_cast<void*>(workspace), tile_ranges, pair_rows, max_pairs, (cudaStream_t)stream);
+}
+
+}  // extern "C"

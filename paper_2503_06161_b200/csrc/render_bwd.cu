@@ -1,0 +1,468 @@
+// Backward rasterizer: per-tile back-to-front replay + projection chain.
+//
+// Reference: rasterizer.render_backward (rasterizer.py:320-452) and
+// gaussians.covariance_backward / rotmat_backward / normalize_backward
+// (gaussians.py:156-218).
+//   k_blend_bwd       tile loop  rasterizer.py:349-393  (fp32, warp butterfly
+//                     reduction + one coalesced red.global per warp/Gaussian)
+//   k_preprocess_bwd  projection chain rasterizer.py:395-451 (fp64)
+#include "render_common.cuh"
+#include "sh.cuh"
+
+namespace fs4d {
+
+struct BwdArgs {
+  int H, W, ntx, D, acc_stride, nvals;
+  float alpha_cap, alpha_skip, stop;
+  float bg0, bg1, bg2;
+  const uint2* ranges;
+  const uint32_t* pvals;
+  const float2* xy;
+  const float4* conic_o;
+  const int4* pix_rect;
+  const float4* rgbz;
+  const float* features;
+  const float* tfinal;
+  const int32_t* last;
+  const float* dC;
+  const float* dD;
+  const float* dF;
+  const float* dA;
+  float* accum;
+};
+
+// Reduce v[0..31] over the warp; afterwards lane L holds the warp sum of v[L].
+__device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane) {
+#pragma unroll
+  for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int k = 0; k < n / 2; ++k) {
+      float send = upper ? v[k] : v[k + n / 2];
+      float keep = upper ? v[k + n / 2] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+template <int DC>
+__global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
+  constexpr int B = DC >= 64 ? 128 : kTilePixels;  // Gaussians staged per batch
+  __shared__ float2 s_xy[B];
+  __shared__ float4 s_co[B];
+  __shared__ int4 s_pr[B];
+  __shared__ float4 s_rgbz[B];
+  __shared__ uint32_t s_g[B];
+  __shared__ __align__(16) float s_f[DC > 0 ? B * DC : 1];
+  __shared__ int s_maxlast;
+
+  const int tile = blockIdx.x;
+  const int tx = tile % a.ntx, ty = tile / a.ntx;
+  const int col = tx * kTile + (threadIdx.x & (kTile - 1));
+  const int row = ty * kTile + (threadIdx.x / kTile);
+  const int lane = threadIdx.x & 31;
+  const bool inside = col < a.W && row < a.H;
+  const uint2 rg = a.ranges[tile];
+  if (rg.y <= rg.x) return;
+  const int64_t pix = (int64_t)row * a.W + col;
+  const float fc = (float)col, fr = (float)row;
+
+  float T = 1.f, Tfin = 1.f;
+  int lastj = -1;
+  float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dd = 0.f, da = 0.f;
+  float df[DC > 0 ? DC : 1];
+#pragma unroll
+  for (int c = 0; c < (DC > 0 ? DC : 1); ++c) df[c] = 0.f;
+  if (inside) {
+    T = Tfin = a.tfinal[pix];
+    lastj = a.last[pix];
+    if (a.dC) { dc0 = a.dC[3 * pix]; dc1 = a.dC[3 * pix + 1]; dc2 = a.dC[3 * pix + 2]; }
+    if (a.dD) dd = a.dD[pix];
+    if (a.dA) da = a.dA[pix];
+    if (DC > 0 && a.dF) {
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        if (c < a.D) df[c] = a.dF[pix * a.D + c];
+    }
+  }
+  const float vpix = dc0 * a.bg0 + dc1 * a.bg1 + dc2 * a.bg2 - da;  // dL/dT_final
+  float suffix = 0.f;
+
+  if (threadIdx.x == 0) s_maxlast = -1;
+  __syncthreads();
+  atomicMax(&s_maxlast, lastj);
+  __syncthreads();
+  const int maxlast = s_maxlast;
+  if (maxlast < (int)rg.x) return;
+
+  const int nv = a.nvals;
+  const uint32_t hi = (uint32_t)(maxlast + 1) < rg.y ? (uint32_t)(maxlast + 1) : rg.y;
+  for (int64_t bend = hi; bend > (int64_t)rg.x; bend -= B) {
+    const int64_t bstart = bend - B > (int64_t)rg.x ? bend - B : (int64_t)rg.x;
+    const int cnt = (int)(bend - bstart);
+    __syncthreads();
+    if ((int)threadIdx.x < cnt) {
+      const uint32_t g = a.pvals[bstart + threadIdx.x];
+      s_g[threadIdx.x] = g;
+      s_xy[threadIdx.x] = a.xy[g];
+      s_co[threadIdx.x] = a.conic_o[g];
+      s_pr[threadIdx.x] = a.pix_rect[g];
+      s_rgbz[threadIdx.x] = a.rgbz[g];
+      if (DC > 0) {
+        const float* src = a.features + (int64_t)g * a.D;
+        float* dst = s_f + threadIdx.x * DC;
+        for (int c = 0; c < DC; ++c) dst[c] = c < a.D ? src[c] : 0.f;
+      }
+    }
+    __syncthreads();
+    for (int k = cnt - 1; k >= 0; --k) {
+      const int64_t j = bstart + k;
+      bool live = inside && j <= (int64_t)lastj;
+      float v[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = 0.f;
+      float vf[DC > 0 ? DC : 1];
+#pragma unroll
+      for (int c = 0; c < (DC > 0 ? DC : 1); ++c) vf[c] = 0.f;
+      if (live) {
+        const int4 pr = s_pr[k];
+        live = !(col < pr.x || col > pr.y || row < pr.z || row > pr.w);
+      }
+      float dx = 0.f, dy = 0.f, q = 0.f, gv = 0.f, araw = 0.f, al = 0.f;
+      float4 co = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live) {
+        const float2 m = s_xy[k];
+        co = s_co[k];
+        dx = fc - m.x;
+        dy = fr - m.y;
+        q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
+        live = q <= kQSkip;
+        if (live) {
+          gv = __expf(-0.5f * q);
+          araw = co.w * gv;
+          al = fminf(araw, a.alpha_cap);
+          live = al >= a.alpha_skip;
+        }
+      }
+      if (live) {
+        const float4 cz = s_rgbz[k];
+        const float om = 1.f - al;
+        const float Texc = T / om;
+        const float w = al * Texc;
+        float uval = cz.x * dc0 + cz.y * dc1 + cz.z * dc2 + cz.w * dd;
+        if (DC > 0) {
+          const float* f = s_f + k * DC;
+#pragma unroll
+          for (int c = 0; c < DC; ++c) {
+            uval += f[c] * df[c];
+            vf[c] = w * df[c];
+          }
+        }
+        const float dal = uval * Texc - (suffix + Tfin * vpix) / om;
+        suffix += w * uval;
+        T = Texc;
+        const float dar = araw < a.alpha_cap ? dal : 0.f;
+        const float dq = -0.5f * gv * dar * co.w;
+        v[0] = w * dc0;
+        v[1] = w * dc1;
+        v[2] = w * dc2;
+        v[3] = w * dd;
+        v[4] = dar * gv;
+        v[5] = dq * dx * dx;
+        v[6] = dq * dx * dy;
+        v[7] = dq * dy * dy;
+        v[8] = -2.f * dq * (co.x * dx + co.y * dy);
+        v[9] = -2.f * dq * (co.y * dx + co.z * dy);
+      }
+      if (!__any_sync(0xffffffffu, live)) continue;
+      float* dst = a.accum + (int64_t)s_g[k] * a.acc_stride;
+      // chunk 0: values 0..31 (10 fixed + first 22 feature channels)
+#pragma unroll
+      for (int c = 0; c < 22; ++c)
+        if (c < DC) v[10 + c] = vf[c];
+      {
+        float r = warp_transpose_reduce(v, lane);
+        if (lane < nv && r != 0.f) red_add(dst + lane, r);
+      }
+      // further chunks of 32 feature channels
+#pragma unroll
+      for (int base = 22; base < DC; base += 32) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = (base + c < DC) ? vf[base + c] : 0.f;
+        float r = warp_transpose_reduce(v, lane);
+        if (10 + base + lane < nv && r != 0.f) red_add(dst + 10 + base + lane, r);
+      }
+    }
+  }
+}
+
+struct PreBwdArgs {
+  Fs4dCloud c;  // snapshot
+  Fs4dCloud g;  // output grads (SoA, zero-initialised by the host driver)
+  double R[9], tv[3], campos[3];
+  double fx, fy, lowpass;
+  int H, W, D, acc_stride, sh_degree;
+  const uint32_t* order;
+  const uint32_t* counters;
+  const float* accum;
+  const uint32_t* clamp_mask;
+  int32_t* vs_index;
+  float* vs_norm;
+};
+
+__device__ __forceinline__ double sigmoid_db(double x) {
+  if (x >= 0) return 1.0 / (1.0 + exp(-x));
+  double e = exp(x);
+  return e / (1.0 + e);
+}
+
+// One thread per visible Gaussian (depth rank r).  fp64 throughout, mirroring
+// rasterizer.py:395-451 and gaussians.py:156-218.
+__global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (int64_t)a.counters[CNT_VISIBLE]) return;
+  const int64_t i = a.order[r];
+  const float* acc = a.accum + i * a.acc_stride;
+  const double dcol[3] = {acc[0], acc[1], acc[2]};
+  const double ddep = acc[3], dop = acc[4];
+  const double dk00 = acc[5], dk01 = acc[6], dk11 = acc[7];
+  const double dmx = acc[8], dmy = acc[9];
+
+  const float* P = a.c.positions + 3 * i;
+  const float* Q = a.c.rotations + 4 * i;
+  const float* LS = a.c.log_scales + 3 * i;
+  const double X = P[0], Y = P[1], Z = P[2];
+  const double* R = a.R;
+  const double x = R[0] * X + R[1] * Y + R[2] * Z + a.tv[0];
+  const double y = R[3] * X + R[4] * Y + R[5] * Z + a.tv[1];
+  const double z = R[6] * X + R[7] * Y + R[8] * Z + a.tv[2];
+
+  // covariance (gaussians.py:187-194)
+  const double q0 = Q[0], q1 = Q[1], q2 = Q[2], q3 = Q[3];
+  const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+  const double qu[4] = {q0 / qn, q1 / qn, q2 / qn, q3 / qn};
+  const double qw = qu[0], qx = qu[1], qy = qu[2], qz = qu[3];
+  double Rq[9];
+  Rq[0] = 1 - 2 * (qy * qy + qz * qz);
+  Rq[1] = 2 * (qx * qy - qw * qz);
+  Rq[2] = 2 * (qx * qz + qw * qy);
+  Rq[3] = 2 * (qx * qy + qw * qz);
+  Rq[4] = 1 - 2 * (qx * qx + qz * qz);
+  Rq[5] = 2 * (qy * qz - qw * qx);
+  Rq[6] = 2 * (qx * qz - qw * qy);
+  Rq[7] = 2 * (qy * qz + qw * qx);
+  Rq[8] = 1 - 2 * (qx * qx + qy * qy);
+  const double s[3] = {exp((double)LS[0]), exp((double)LS[1]), exp((double)LS[2])};
+  const double Dg[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+  double Sig[9];
+  for (int rr = 0; rr < 3; ++rr)
+    for (int cc = 0; cc < 3; ++cc)
+      Sig[3 * rr + cc] = (Rq[3 * rr] * s[0]) * (Rq[3 * cc] * s[0]) + (Rq[3 * rr + 1] * s[1]) * (Rq[3 * cc + 1] * s[1]) +
+                         (Rq[3 * rr + 2] * s[2]) * (Rq[3 * cc + 2] * s[2]);
+
+  // projection Jacobian and cov2d (rasterizer.py:141-152)
+  const double fx = a.fx, fy = a.fy;
+  const double j00 = fx / z, j02 = -fx * x / (z * z);
+  const double j11 = fy / z, j12 = -fy * y / (z * z);
+  double M[6];
+  for (int k = 0; k < 3; ++k) {
+    M[k] = j00 * R[k] + j02 * R[6 + k];
+    M[3 + k] = j11 * R[3 + k] + j12 * R[6 + k];
+  }
+  double MS[6];
+  for (int rr = 0; rr < 2; ++rr)
+    for (int k = 0; k < 3; ++k)
+      MS[3 * rr + k] = M[3 * rr] * Sig[k] + M[3 * rr + 1] * Sig[3 + k] + M[3 * rr + 2] * Sig[6 + k];
+  const double ca = MS[0] * M[0] + MS[1] * M[1] + MS[2] * M[2] + a.lowpass;
+  const double cb = MS[0] * M[3] + MS[1] * M[4] + MS[2] * M[5];
+  const double cc2 = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5] + a.lowpass;
+  const double det = ca * cc2 - cb * cb;
+  const double C00 = cc2 / det, C01 = -cb / det, C11 = ca / det;
+
+  // d_cov2d = -C dConic C  (rasterizer.py:396), dConic symmetric with dxy off-diagonal
+  // T1 = dConic C
+  const double t00 = dk00 * C00 + dk01 * C01, t01 = dk00 * C01 + dk01 * C11;
+  const double t10 = dk01 * C00 + dk11 * C01, t11 = dk01 * C01 + dk11 * C11;
+  const double g00 = -(C00 * t00 + C01 * t10), g01 = -(C00 * t01 + C01 * t11);
+  const double g10 = -(C01 * t00 + C11 * t10), g11 = -(C01 * t01 + C11 * t11);
+  const double G[4] = {g00, g01, g10, g11};
+  const double S2[4] = {2 * g00, g01 + g10, g10 + g01, 2 * g11};  // sym = G + G^T
+
+  // d_Mm = sym @ Mm @ Sigma ; d_sigma = Mm^T G Mm ; d_J = d_Mm @ R^T (rasterizer.py:412-415)
+  double dM[6];
+  for (int rr = 0; rr < 2; ++rr)
+    for (int k = 0; k < 3; ++k)
+      dM[3 * rr + k] = S2[2 * rr] * MS[k] + S2[2 * rr + 1] * MS[3 + k];
+  double dS[9];
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q)
+      dS[3 * p + q] = M[p] * (G[0] * M[q] + G[1] * M[3 + q]) + M[3 + p] * (G[2] * M[q] + G[3] * M[3 + q]);
+  double dJ[6];
+  for (int rr = 0; rr < 2; ++rr)
+    for (int k = 0; k < 3; ++k)
+      dJ[3 * rr + k] = dM[3 * rr] * R[3 * k] + dM[3 * rr + 1] * R[3 * k + 1] + dM[3 * rr + 2] * R[3 * k + 2];
+
+  // camera-space gradient (rasterizer.py:417-426)
+  const double z2 = z * z, z3 = z2 * z;
+  double dcam[3];
+  dcam[0] = dJ[2] * (-fx / z2) + dmx * fx / z;
+  dcam[1] = dJ[5] * (-fy / z2) + dmy * fy / z;
+  dcam[2] = dJ[0] * (-fx / z2) + dJ[2] * (2.0 * fx * x / z3) + dJ[4] * (-fy / z2) + dJ[5] * (2.0 * fy * y / z3) +
+            dmx * (-fx * x / z2) + dmy * (-fy * y / z2) + ddep;
+  double dpos[3];
+  for (int k = 0; k < 3; ++k) dpos[k] = dcam[0] * R[k] + dcam[1] * R[3 + k] + dcam[2] * R[6 + k];
+
+  // covariance_backward (gaussians.py:203-218)
+  double dR[9];
+  {
+    double SS[9];
+    for (int p = 0; p < 9; ++p) SS[p] = dS[p] + dS[3 * (p % 3) + p / 3];
+    for (int p = 0; p < 3; ++p)
+      for (int q = 0; q < 3; ++q)
+        dR[3 * p + q] = (SS[3 * p] * Rq[q] + SS[3 * p + 1] * Rq[3 + q] + SS[3 * p + 2] * Rq[6 + q]) * Dg[q];
+  }
+  double dls[3];
+  for (int k = 0; k < 3; ++k) {
+    double v = 0;
+    for (int p = 0; p < 3; ++p)
+      for (int q = 0; q < 3; ++q) v += Rq[3 * p + k] * dS[3 * p + q] * Rq[3 * q + k];
+    dls[k] = 2.0 * Dg[k] * v;
+  }
+  const double* g = dR;
+  double dqu[4];
+  dqu[0] = 2 * (-qz * g[1] + qy * g[2] + qz * g[3] - qx * g[5] - qy * g[6] + qx * g[7]);
+  dqu[1] = 2 * (qy * g[1] + qz * g[2] + qy * g[3] - 2 * qx * g[4] - qw * g[5] + qz * g[6] + qw * g[7] - 2 * qx * g[8]);
+  dqu[2] = 2 * (-2 * qy * g[0] + qx * g[1] + qw * g[2] + qx * g[3] + qz * g[5] - qw * g[6] + qz * g[7] - 2 * qy * g[8]);
+  dqu[3] = 2 * (-2 * qz * g[0] - qw * g[1] + qx * g[2] + qw * g[3] - 2 * qz * g[4] + qy * g[5] + qx * g[6] + qy * g[7]);
+  const double inner = dqu[0] * qu[0] + dqu[1] * qu[1] + dqu[2] * qu[2] + dqu[3] * qu[3];
+
+  // colour gate and SH (build extension)
+  const uint32_t gate = a.clamp_mask[i];
+  double dcg[3];
+  for (int k = 0; k < 3; ++k) dcg[k] = (gate >> k) & 1u ? dcol[k] : 0.0;
+  const int n_sh = (a.sh_degree + 1) * (a.sh_degree + 1) - 1;
+  if (n_sh > 0 && a.c.sh_rest) {
+    double vx = X - a.campos[0], vy = Y - a.campos[1], vz = Z - a.campos[2];
+    double dn = sqrt(vx * vx + vy * vy + vz * vz);
+    dn = dn > 0 ? dn : 1.0;
+    const double ux = vx / dn, uy = vy / dn, uz = vz / dn;
+    double Yb[15], dY[15][3];
+    int nb = sh_basis<double>(a.sh_degree, ux, uy, uz, Yb, dY);
+    const float* S = a.c.sh_rest + (int64_t)n_sh * 3 * i;
+    float* GS = a.g.sh_rest + (int64_t)n_sh * 3 * i;
+    double ddir[3] = {0, 0, 0};
+    for (int k = 0; k < nb; ++k) {
+      double gk = 0;
+      for (int c = 0; c < 3; ++c) {
+        GS[3 * k + c] = (float)(Yb[k] * dcg[c]);
+        gk += S[3 * k + c] * dcg[c];
+      }
+      ddir[0] += gk * dY[k][0];
+      ddir[1] += gk * dY[k][1];
+      ddir[2] += gk * dY[k][2];
+    }
+    const double dot = ddir[0] * ux + ddir[1] * uy + ddir[2] * uz;
+    dpos[0] += (ddir[0] - dot * ux) / dn;
+    dpos[1] += (ddir[1] - dot * uy) / dn;
+    dpos[2] += (ddir[2] - dot * uz) / dn;
+  }
+
+  const double o = sigmoid_db((double)a.c.opacity_logits[i]);
+  for (int k = 0; k < 3; ++k) {
+    a.g.positions[3 * i + k] = (float)dpos[k];
+    a.g.log_scales[3 * i + k] = (float)dls[k];
+    a.g.colors_raw[3 * i + k] = (float)dcg[k];
+  }
+  for (int k = 0; k < 4; ++k) a.g.rotations[4 * i + k] = (float)((dqu[k] - inner * qu[k]) / qn);
+  a.g.opacity_logits[i] = (float)(dop * o * (1.0 - o));
+  for (int c = 0; c < a.D; ++c) a.g.features[(int64_t)a.D * i + c] = acc[10 + c];
+  a.vs_index[r] = (int32_t)i;
+  a.vs_norm[r] = (float)hypot(dmx * 0.5 * a.W, dmy * 0.5 * a.H);
+}
+
+static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t s) {
+  switch (dc) {
+    case 0: k_blend_bwd<0><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 4: k_blend_bwd<4><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 8: k_blend_bwd<8><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 16: k_blend_bwd<16><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 32: k_blend_bwd<32><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    default: k_blend_bwd<64><<<ntiles, kTilePixels, 0, s>>>(a); break;
+  }
+}
+
+int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRasterConfig& cfg,
+                    const RenderLayout& L, void* ws, const Fs4dImageGrads& up, Fs4dCloud& grads,
+                    int32_t* vs_index, float* vs_norm, cudaStream_t s) {
+  const int64_t K = L.K;
+  const int D = cfg.with_features ? L.D : 0;
+  float* accum = at<float>(ws, L.accum);
+  cudaMemsetAsync(accum, 0, (size_t)K * L.acc_stride * 4, s);
+  // zero the outputs: culled rows keep zero gradients (rasterizer.py:432-441)
+  cudaMemsetAsync(grads.positions, 0, (size_t)K * 3 * 4, s);
+  cudaMemsetAsync(grads.rotations, 0, (size_t)K * 4 * 4, s);
+  cudaMemsetAsync(grads.log_scales, 0, (size_t)K * 3 * 4, s);
+  cudaMemsetAsync(grads.opacity_logits, 0, (size_t)K * 4, s);
+  cudaMemsetAsync(grads.colors_raw, 0, (size_t)K * 3 * 4, s);
+  if (grads.features && snap.D > 0) cudaMemsetAsync(grads.features, 0, (size_t)K * snap.D * 4, s);
+  const int n_sh = (snap.sh_degree + 1) * (snap.sh_degree + 1) - 1;
+  if (grads.sh_rest && n_sh > 0) cudaMemsetAsync(grads.sh_rest, 0, (size_t)K * n_sh * 3 * 4, s);
+
+  BwdArgs b;
+  b.H = L.H;
+  b.W = L.W;
+  b.ntx = L.ntx;
+  b.D = D;
+  b.acc_stride = L.acc_stride;
+  b.nvals = 10 + D;
+  b.alpha_cap = (float)cfg.alpha_cap;
+  b.alpha_skip = (float)cfg.alpha_skip;
+  b.stop = (float)cfg.stop_transmittance;
+  b.bg0 = (float)cfg.background[0];
+  b.bg1 = (float)cfg.background[1];
+  b.bg2 = (float)cfg.background[2];
+  b.ranges = at<uint2>(ws, L.ranges);
+  b.pvals = at<uint32_t>(ws, L.pair_final ? L.pvals1 : L.pvals0);
+  b.xy = at<float2>(ws, L.xy);
+  b.conic_o = at<float4>(ws, L.conic_o);
+  b.pix_rect = at<int4>(ws, L.pix_rect);
+  b.rgbz = at<float4>(ws, L.rgbz);
+  b.features = snap.features;
+  b.tfinal = at<float>(ws, L.tfinal);
+  b.last = at<int32_t>(ws, L.last);
+  b.dC = up.d_color;
+  b.dD = up.d_depth;
+  b.dF = D > 0 ? up.d_feature : nullptr;
+  b.dA = up.d_alpha;
+  b.accum = accum;
+  int dc = D <= 0 ? 0 : D <= 4 ? 4 : D <= 8 ? 8 : D <= 16 ? 16 : D <= 32 ? 32 : 64;
+  if (L.ntiles > 0) launch_blend_bwd(dc, L.ntiles, b, s);
+
+  PreBwdArgs p;
+  p.c = snap;
+  p.g = grads;
+  for (int r = 0; r < 3; ++r) {
+    for (int k = 0; k < 3; ++k) p.R[3 * r + k] = cam.T[4 * r + k];
+    p.tv[r] = cam.T[4 * r + 3];
+  }
+  for (int k = 0; k < 3; ++k) p.campos[k] = -(p.R[k] * p.tv[0] + p.R[3 + k] * p.tv[1] + p.R[6 + k] * p.tv[2]);
+  p.fx = cam.K[0];
+  p.fy = cam.K[4];
+  p.lowpass = cfg.lowpass;
+  p.H = L.H;
+  p.W = L.W;
+  p.D = D;
+  p.acc_stride = L.acc_stride;
+  p.sh_degree = snap.sh_degree;
+  p.order = at<uint32_t>(ws, L.depth_final ? L.dvals1 : L.dvals0);
+  p.counters = at<uint32_t>(ws, L.counters);
+  p.accum = accum;
+  p.clamp_mask = at<uint32_t>(ws, L.clamp_mask);
+  p.vs_index = vs_index;
+  p.vs_norm = vs_norm;
+  if (K > 0) k_preprocess_bwd<<<(unsigned)ceil_div(K, 128), 128, 0, s>>>(p);
+  return check_launch("render_bwd");
+}
+
+}  // namespace fs4d

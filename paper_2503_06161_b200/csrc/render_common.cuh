@@ -1,0 +1,100 @@
+// Render record layout shared by the forward and backward rasterizer passes.
+//
+// The record is the B200 counterpart of rasterizer.RasterRecord
+// (rasterizer.py:64-91): instead of per-tile [G,256] float64 alpha matrices
+// (15 GB at 200k Gaussians) it keeps O(K + pairs + pixels) state and the
+// backward pass recomputes alphas from the projected Gaussians.
+#pragma once
+#include "common.cuh"
+#include "scan_sort.cuh"
+
+namespace fs4d {
+
+constexpr int kTile = 16;
+constexpr int kTilePixels = kTile * kTile;
+constexpr float kQSkip = 11.0825270270270f;  // 2 ln 255 (rasterizer.py:212)
+
+struct RenderLayout {
+  int64_t K = 0, cap = 0;
+  int H = 0, W = 0, D = 0, ntx = 0, nty = 0, ntiles = 0, tile_bits = 0, acc_stride = 0;
+  int depth_final = 0, pair_final = 0;
+  // per Gaussian (source-indexed unless noted)
+  size_t xy, conic_o, pix_rect, tile_rect, rgbz, cov_r, z64, dkeys0, dkeys1, dvals0, dvals1,
+      tcount /*by rank*/, toff /*by rank*/, rank_of, clamp_mask;
+  // tiles / pairs / pixels
+  size_t ranges, pkeys0, pkeys1, pvals0, pvals1, tfinal, last;
+  // counters and scratch
+  size_t counters, scratch, scratch_bytes;
+  // backward accumulators [K, acc_stride]
+  size_t accum;
+  size_t total;
+};
+
+// counters (uint32 words at layout.counters)
+enum { CNT_VISIBLE = 0, CNT_PAIRS64 = 2 /* u64 at words 2..3 */, CNT_PAIRS_CLAMPED = 4, CNT_WORDS = 8 };
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
+  RenderLayout L;
+  L.K = info.K;
+  L.cap = info.pair_capacity;
+  L.H = info.height;
+  L.W = info.width;
+  L.D = info.D;
+  L.ntx = (int)ceil_div(L.W, kTile);
+  L.nty = (int)ceil_div(L.H, kTile);
+  L.ntiles = L.ntx * L.nty;
+  int bits = 0;
+  while ((1ll << bits) < (int64_t)L.ntiles) ++bits;
+  L.tile_bits = bits;
+  // depth sort: 32-bit keys in 8-bit passes -> 4 passes -> result in buffer 0
+  L.depth_final = (32 / kRadixBits) & 1;
+  L.pair_final = (int)(ceil_div(bits, kRadixBits) & 1);
+  L.acc_stride = (int)ceil_div(10 + L.D, 32) * 32;
+  const int64_t K = L.K > 0 ? L.K : 1;
+  const int64_t cap = L.cap > 0 ? L.cap : 1;
+  const int64_t npix = (int64_t)L.H * L.W > 0 ? (int64_t)L.H * L.W : 1;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.xy = take(K * 8);
+  L.conic_o = take(K * 16);
+  L.pix_rect = take(K * 16);
+  L.tile_rect = take(K * 16);
+  L.rgbz = take(K * 16);
+  L.cov_r = take(K * 16);
+  L.z64 = take(K * 8);
+  L.dkeys0 = take(K * 4);
+  L.dkeys1 = take(K * 4);
+  L.dvals0 = take(K * 4);
+  L.dvals1 = take(K * 4);
+  L.tcount = take(K * 4);
+  L.toff = take(K * 8);
+  L.rank_of = take(K * 4);
+  L.clamp_mask = take(K * 4);
+  L.ranges = take((size_t)(L.ntiles > 0 ? L.ntiles : 1) * 8);
+  L.pkeys0 = take(cap * 4);
+  L.pkeys1 = take(cap * 4);
+  L.pvals0 = take(cap * 4);
+  L.pvals1 = take(cap * 4);
+  L.tfinal = take(npix * 4);
+  L.last = take(npix * 4);
+  L.counters = take(CNT_WORDS * 4);
+  size_t s1 = scan_scratch_bytes(K), s2 = radix_scratch_bytes(K > cap ? K : cap);
+  L.scratch_bytes = s1 > s2 ? s1 : s2;
+  L.scratch = take(L.scratch_bytes);
+  L.accum = take((size_t)K * L.acc_stride * 4);
+  L.total = o;
+  return L;
+}
+
+template <typename T>
+__host__ __device__ inline T* at(void* base, size_t off) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + off);
+}
+
+}  // namespace fs4d

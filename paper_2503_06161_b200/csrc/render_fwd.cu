@@ -1,0 +1,592 @@
+// Forward rasterizer: project -> stable depth sort -> tile binning -> blend.
+//
+// Reference: rasterizer.render (rasterizer.py:264-303) and the functions it
+// calls.  Stage map:
+//   k_preprocess      project()            rasterizer.py:117-185 (fp64, per Gaussian)
+//   radix + tie fixup np.argsort(z, stable) rasterizer.py:163
+//   k_tile_count/scan/k_emit/radix/k_ranges   bin_tiles()  rasterizer.py:188-207
+//   k_blend           _tile_alphas + _composite_weights + tile matmuls
+//                                          rasterizer.py:215-261, 284-303
+#include "render_common.cuh"
+#include "sh.cuh"
+
+namespace fs4d {
+
+struct PreArgs {
+  Fs4dCloud c;
+  double R[9], tv[3], campos[3];
+  double fx, fy, cx, cy;
+  int H, W, ntx, nty;
+  double z_near, lowpass;
+  int with_features;
+  float2* xy;
+  float4* conic_o;
+  int4* pix_rect;
+  int4* tile_rect;
+  float4* rgbz;
+  float4* cov_r;
+  double* z64;
+  uint32_t* dkeys;
+  uint32_t* dvals;
+  uint32_t* clamp_mask;
+  uint32_t* counters;
+  int32_t* status;
+};
+
+__device__ __forceinline__ double sigmoid_d(double x) {
+  // gaussians.py:25-31 (sign-split stable form)
+  if (x >= 0) return 1.0 / (1.0 + exp(-x));
+  double e = exp(x);
+  return e / (1.0 + e);
+}
+
+__global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.c.K) return;
+  a.dvals[i] = (uint32_t)i;
+  a.dkeys[i] = 0xFFFFFFFFu;  // culled sentinel sorts last
+  a.tile_rect[i] = make_int4(0, -1, 0, -1);
+
+  // ---- finite checks, field order of rasterizer.py:120-127 ----
+  const float* P = a.c.positions + 3 * i;
+  const float* Q = a.c.rotations + 4 * i;
+  const float* LS = a.c.log_scales + 3 * i;
+  const float* CR = a.c.colors_raw + 3 * i;
+  float p0 = P[0], p1 = P[1], p2 = P[2];
+  float q0 = Q[0], q1 = Q[1], q2 = Q[2], q3 = Q[3];
+  float s0 = LS[0], s1 = LS[1], s2 = LS[2];
+  float ol = a.c.opacity_logits[i];
+  float cr0 = CR[0], cr1 = CR[1], cr2 = CR[2];
+  bool bad = false;
+  if (!(isfinite(p0) && isfinite(p1) && isfinite(p2))) { flag_bad_field(a.status, FS4D_FIELD_POSITIONS, i); bad = true; }
+  if (!(isfinite(q0) && isfinite(q1) && isfinite(q2) && isfinite(q3))) { flag_bad_field(a.status, FS4D_FIELD_ROTATIONS, i); bad = true; }
+  if (!(isfinite(s0) && isfinite(s1) && isfinite(s2))) { flag_bad_field(a.status, FS4D_FIELD_LOG_SCALES, i); bad = true; }
+  if (!isfinite(ol)) { flag_bad_field(a.status, FS4D_FIELD_OPACITY, i); bad = true; }
+  if (!(isfinite(cr0) && isfinite(cr1) && isfinite(cr2))) { flag_bad_field(a.status, FS4D_FIELD_COLORS, i); bad = true; }
+  {
+    const float* F = a.c.features + (int64_t)a.c.D * i;
+    bool fb = false;
+    for (int k = 0; k < a.c.D; ++k) fb |= !isfinite(F[k]);
+    if (fb) { flag_bad_field(a.status, FS4D_FIELD_FEATURES, i); bad = true; }
+  }
+  const int n_sh = (a.c.sh_degree + 1) * (a.c.sh_degree + 1) - 1;
+  if (n_sh > 0 && a.c.sh_rest) {
+    const float* S = a.c.sh_rest + (int64_t)n_sh * 3 * i;
+    bool sb = false;
+    for (int k = 0; k < n_sh * 3; ++k) sb |= !isfinite(S[k]);
+    if (sb) { flag_bad_field(a.status, FS4D_FIELD_SH, i); bad = true; }
+  }
+  if (bad) return;
+
+  // ---- camera space (rasterizer.py:131-140) ----
+  const double X = p0, Y = p1, Z = p2;
+  const double x = a.R[0] * X + a.R[1] * Y + a.R[2] * Z + a.tv[0];
+  const double y = a.R[3] * X + a.R[4] * Y + a.R[5] * Z + a.tv[1];
+  const double z = a.R[6] * X + a.R[7] * Y + a.R[8] * Z + a.tv[2];
+  if (!(z > a.z_near)) return;
+  const double u = a.fx * x / z + a.cx;
+  const double v = a.fy * y / z + a.cy;
+
+  // ---- 3-d covariance (gaussians.py:140-194) ----
+  const double qn = sqrt((double)q0 * q0 + (double)q1 * q1 + (double)q2 * q2 + (double)q3 * q3);
+  if (qn < 1e-12) {
+    if (a.status) {
+      atomicMin(&a.status[FS4D_ST_DEGEN_INDEX], (int32_t)i);
+      raise_status(a.status, FS4D_ERR_DEGENERATE);
+    }
+    return;
+  }
+  const double qw = q0 / qn, qx = q1 / qn, qy = q2 / qn, qz = q3 / qn;
+  double Rq[9];
+  Rq[0] = 1 - 2 * (qy * qy + qz * qz);
+  Rq[1] = 2 * (qx * qy - qw * qz);
+  Rq[2] = 2 * (qx * qz + qw * qy);
+  Rq[3] = 2 * (qx * qy + qw * qz);
+  Rq[4] = 1 - 2 * (qx * qx + qz * qz);
+  Rq[5] = 2 * (qy * qz - qw * qx);
+  Rq[6] = 2 * (qx * qz - qw * qy);
+  Rq[7] = 2 * (qy * qz + qw * qx);
+  Rq[8] = 1 - 2 * (qx * qx + qy * qy);
+  const double sc[3] = {exp((double)s0), exp((double)s1), exp((double)s2)};
+  double RS[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) RS[3 * r + k] = Rq[3 * r + k] * sc[k];
+  double Sig[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+      Sig[3 * r + cc] = RS[3 * r] * RS[3 * cc] + RS[3 * r + 1] * RS[3 * cc + 1] + RS[3 * r + 2] * RS[3 * cc + 2];
+
+  // ---- EWA projection (rasterizer.py:141-158) ----
+  const double j00 = a.fx / z, j02 = -a.fx * x / (z * z);
+  const double j11 = a.fy / z, j12 = -a.fy * y / (z * z);
+  double M[6];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    M[k] = j00 * a.R[k] + j02 * a.R[6 + k];
+    M[3 + k] = j11 * a.R[3 + k] + j12 * a.R[6 + k];
+  }
+  double MS[6];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      MS[3 * r + k] = M[3 * r] * Sig[k] + M[3 * r + 1] * Sig[3 + k] + M[3 * r + 2] * Sig[6 + k];
+  double ca = MS[0] * M[0] + MS[1] * M[1] + MS[2] * M[2];
+  double cb = MS[0] * M[3] + MS[1] * M[4] + MS[2] * M[5];
+  double cc = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5];
+  ca += a.lowpass;
+  cc += a.lowpass;
+  const double mid = 0.5 * (ca + cc);
+  const double det = ca * cc - cb * cb;
+  const double eig = mid + sqrt(fmax(mid * mid - det, 0.0));
+  const double radius = ceil(3.0 * sqrt(eig));
+
+  // ---- offscreen cull (rasterizer.py:160-162) ----
+  const bool on = (u + radius >= 0) && (u - radius <= a.W - 1) && (v + radius >= 0) && (v - radius <= a.H - 1);
+  if (!on) return;
+
+  // ---- kept: conic, activations, footprints ----
+  const double inv = 1.0 / det;
+  const double c00 = cc * inv, c01 = -cb * inv, c11 = ca * inv;
+  // rasterizer.py:165-171 divides each entry by det; match that rounding
+  const double c00r = cc / det, c01r = -cb / det, c11r = ca / det;
+  (void)c00; (void)c01; (void)c11;
+  const float opac = (float)sigmoid_d((double)ol);
+
+  double col[3] = {cr0, cr1, cr2};
+  if (n_sh > 0 && a.c.sh_rest) {
+    double dx = X - a.campos[0], dy = Y - a.campos[1], dz = Z - a.campos[2];
+    double dn = sqrt(dx * dx + dy * dy + dz * dz);
+    dn = dn > 0 ? dn : 1.0;
+    double Yb[15];
+    int nb = sh_basis<double>(a.c.sh_degree, dx / dn, dy / dn, dz / dn, Yb, nullptr);
+    const float* S = a.c.sh_rest + (int64_t)n_sh * 3 * i;
+    for (int k = 0; k < nb; ++k) {
+      col[0] += Yb[k] * S[3 * k + 0];
+      col[1] += Yb[k] * S[3 * k + 1];
+      col[2] += Yb[k] * S[3 * k + 2];
+    }
+  }
+  uint32_t gate = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (col[k] > 0.0 && col[k] < 1.0) gate |= 1u << k;
+    col[k] = fmin(fmax(col[k], 0.0), 1.0);
+  }
+  a.clamp_mask[i] = gate;
+
+  // pixel footprint |j - u| <= r  <=>  ceil(u - r) <= j <= floor(u + r)  (rasterizer.py:227)
+  int px0 = (int)fmax(ceil(u - radius), 0.0), px1 = (int)fmin(floor(u + radius), (double)(a.W - 1));
+  int py0 = (int)fmax(ceil(v - radius), 0.0), py1 = (int)fmin(floor(v + radius), (double)(a.H - 1));
+  // inclusive tile rectangle (rasterizer.py:198-201)
+  const int tx0 = (int)fmin(fmax(floor((u - radius) / kTile), 0.0), (double)(a.ntx - 1));
+  const int tx1 = (int)fmin(fmax(floor((u + radius) / kTile), 0.0), (double)(a.ntx - 1));
+  const int ty0 = (int)fmin(fmax(floor((v - radius) / kTile), 0.0), (double)(a.nty - 1));
+  const int ty1 = (int)fmin(fmax(floor((v + radius) / kTile), 0.0), (double)(a.nty - 1));
+
+  a.xy[i] = make_float2((float)u, (float)v);
+  a.conic_o[i] = make_float4((float)c00r, (float)c01r, (float)c11r, opac);
+  a.pix_rect[i] = make_int4(px0, px1, py0, py1);
+  a.tile_rect[i] = make_int4(tx0, tx1, ty0, ty1);
+  a.rgbz[i] = make_float4((float)col[0], (float)col[1], (float)col[2], (float)z);
+  a.cov_r[i] = make_float4((float)ca, (float)cb, (float)cc, (float)radius);
+  a.z64[i] = z;
+  a.dkeys[i] = __float_as_uint((float)z);  // z > 0: IEEE bits order as unsigned
+  atomicAdd(&a.counters[CNT_VISIBLE], 1u);
+}
+
+// Equal fp32 keys are re-ordered by the exact fp64 depth, ties by source
+// index, so the order equals np.argsort(z64, kind="stable") (rasterizer.py:163).
+__global__ void k_depth_tie_fixup(const uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                  const double* __restrict__ z64, int64_t K, const uint32_t* counters) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t M = counters[CNT_VISIBLE];
+  if (r >= M) return;
+  const uint32_t key = keys[r];
+  if (r > 0 && keys[r - 1] == key) return;        // not a run start
+  if (r + 1 >= M || keys[r + 1] != key) return;   // run of length 1
+  int64_t e = r + 1;
+  while (e < M && keys[e] == key) ++e;
+  for (int64_t a = r + 1; a < e; ++a) {  // insertion sort of the (tiny) run
+    uint32_t va = vals[a];
+    double za = z64[va];
+    int64_t b = a - 1;
+    while (b >= r) {
+      uint32_t vb = vals[b];
+      double zb = z64[vb];
+      if (zb < za || (zb == za && vb < va)) break;
+      vals[b + 1] = vb;
+      --b;
+    }
+    vals[b + 1] = va;
+  }
+}
+
+__global__ void k_tile_count(const uint32_t* __restrict__ order, const int4* __restrict__ tile_rect, int64_t K,
+                             const uint32_t* counters, uint32_t* __restrict__ tcount, int32_t* __restrict__ rank_of) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= K) return;
+  const uint32_t i = order[r];
+  rank_of[i] = (int32_t)r;
+  uint32_t n = 0;
+  if (r < (int64_t)counters[CNT_VISIBLE]) {
+    int4 t = tile_rect[i];
+    n = (uint32_t)((t.y - t.x + 1) * (t.w - t.z + 1));
+  }
+  tcount[r] = n;
+}
+
+__global__ void k_pairs_check(uint32_t* counters, int64_t cap, int32_t* status) {
+  uint64_t total = *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64);
+  uint32_t clamped = (uint32_t)(total < (uint64_t)cap ? total : (uint64_t)cap);
+  counters[CNT_PAIRS_CLAMPED] = clamped;
+  if (status) {
+    status[FS4D_ST_N_VISIBLE] = (int32_t)counters[CNT_VISIBLE];
+    status[FS4D_ST_PAIRS_LO] = (int32_t)(total & 0xFFFFFFFFu);
+    status[FS4D_ST_PAIRS_HI] = (int32_t)(total >> 32);
+    if (total > (uint64_t)cap) raise_status(status, FS4D_ERR_CAPACITY);
+  }
+}
+
+// one warp per Gaussian: lanes stride over its tile rectangle
+__global__ void k_emit_pairs(const uint32_t* __restrict__ order, const int4* __restrict__ tile_rect,
+                             const uint64_t* __restrict__ toff, const uint32_t* counters, int64_t cap, int ntx,
+                             uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= (int64_t)counters[CNT_VISIBLE]) return;
+  const uint32_t i = order[r];
+  const int4 t = tile_rect[i];
+  const int w = t.y - t.x + 1, h = t.w - t.z + 1;
+  const uint64_t base = toff[r];
+  for (int k = lane; k < w * h; k += 32) {
+    uint64_t o = base + (uint64_t)k;
+    if (o >= (uint64_t)cap) break;
+    int ty = t.z + k / w, tx = t.x + k % w;
+    pkeys[o] = (uint32_t)(ty * ntx + tx);
+    pvals[o] = i;
+  }
+}
+
+__global__ void k_tile_ranges(const uint32_t* __restrict__ pkeys, const uint32_t* counters, uint2* __restrict__ ranges) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = counters[CNT_PAIRS_CLAMPED];
+  if (p >= n) return;
+  const uint32_t t = pkeys[p];
+  if (p == 0 || pkeys[p - 1] != t) ranges[t].x = (uint32_t)p;
+  if (p == n - 1 || pkeys[p + 1] != t) ranges[t].y = (uint32_t)(p + 1);
+}
+
+struct BlendArgs {
+  int H, W, ntx, D, c0;
+  float alpha_cap, alpha_skip, stop;
+  float bg0, bg1, bg2;
+  const uint2* ranges;
+  const uint32_t* pvals;
+  const float2* xy;
+  const float4* conic_o;
+  const int4* pix_rect;
+  const float4* rgbz;
+  const float* features;  // [K, D] snapshot features
+  float* out_color;
+  float* out_depth;
+  float* out_feature;
+  float* out_alpha;
+  int32_t* out_ncontrib;
+  float* tfinal;
+  int32_t* last;
+};
+
+// One CTA per 16x16 tile, one pixel per thread, Gaussians staged through
+// shared memory in batches of 256 (front to back).  DC = feature channels
+// handled by this launch ([c0, c0+DC)); the first launch also composites
+// colour, depth and alpha.
+template <int DC>
+__global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
+  __shared__ float2 s_xy[kTilePixels];
+  __shared__ float4 s_co[kTilePixels];
+  __shared__ int4 s_pr[kTilePixels];
+  __shared__ float4 s_rgbz[kTilePixels];
+  __shared__ __align__(16) float s_f[DC > 0 ? kTilePixels * DC : 1];
+
+  const int tile = blockIdx.x;
+  const int tx = tile % a.ntx, ty = tile / a.ntx;
+  const int col = tx * kTile + (threadIdx.x & (kTile - 1));
+  const int row = ty * kTile + (threadIdx.x / kTile);
+  const bool inside = col < a.W && row < a.H;
+  const uint2 rg = a.ranges[tile];
+  const bool first = a.c0 == 0;
+  const float fc = (float)col, fr = (float)row;
+
+  float T = 1.f, acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f;
+  float accf[DC > 0 ? DC : 1];
+#pragma unroll
+  for (int c = 0; c < (DC > 0 ? DC : 1); ++c) accf[c] = 0.f;
+  int ncontrib = 0, last = -1;
+  bool done = !inside;
+  const int nf = DC > 0 ? min(DC, a.D - a.c0) : 0;
+  const bool vec_ok = DC >= 4 && nf == DC && (a.D & 3) == 0 && (a.c0 & 3) == 0;
+
+  for (uint32_t b = rg.x; b < rg.y; b += kTilePixels) {
+    if (__syncthreads_count(done) == kTilePixels) break;
+    const uint32_t j = b + threadIdx.x;
+    if (j < rg.y) {
+      const uint32_t g = a.pvals[j];
+      s_xy[threadIdx.x] = a.xy[g];
+      s_co[threadIdx.x] = a.conic_o[g];
+      s_pr[threadIdx.x] = a.pix_rect[g];
+      s_rgbz[threadIdx.x] = a.rgbz[g];
+      if (DC > 0) {
+        const float* src = a.features + (int64_t)g * a.D + a.c0;
+        float* dst = s_f + threadIdx.x * DC;
+        if (vec_ok) {
+#pragma unroll
+          for (int c = 0; c < DC; c += 4)
+            *reinterpret_cast<float4*>(dst + c) = __ldg(reinterpret_cast<const float4*>(src + c));
+        } else {
+          for (int c = 0; c < DC; ++c) dst[c] = c < nf ? src[c] : 0.f;
+        }
+      }
+    }
+    __syncthreads();
+    const int cnt = min((uint32_t)kTilePixels, rg.y - b);
+    if (!done) {
+      for (int k = 0; k < cnt; ++k) {
+        const int4 pr = s_pr[k];
+        if (col < pr.x || col > pr.y || row < pr.z || row > pr.w) continue;
+        const float2 m = s_xy[k];
+        const float4 co = s_co[k];
+        const float dx = fc - m.x, dy = fr - m.y;
+        const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
+        if (q > kQSkip) continue;
+        const float gv = __expf(-0.5f * q);
+        const float al = fminf(co.w * gv, a.alpha_cap);
+        if (al < a.alpha_skip) continue;
+        if (T < a.stop) { done = true; break; }
+        const float w = al * T;
+        if (first) {
+          const float4 cz = s_rgbz[k];
+          acc_r += w * cz.x;
+          acc_g += w * cz.y;
+          acc_b += w * cz.z;
+          acc_z += w * cz.w;
+        }
+        if (DC > 0) {
+          const float* f = s_f + k * DC;
+#pragma unroll
+          for (int c = 0; c < DC; c += 4) {
+            if (DC >= 4) {
+              const float4 fv = *reinterpret_cast<const float4*>(f + c);
+              accf[c] += w * fv.x;
+              accf[c + 1] += w * fv.y;
+              accf[c + 2] += w * fv.z;
+              accf[c + 3] += w * fv.w;
+            }
+          }
+        }
+        T *= (1.f - al);
+        ++ncontrib;
+        last = (int)(b + k);
+        if (T < a.stop) { done = true; break; }
+      }
+    }
+  }
+  if (!inside) return;
+  const int64_t pix = (int64_t)row * a.W + col;
+  if (first) {
+    a.out_color[3 * pix + 0] = acc_r + T * a.bg0;
+    a.out_color[3 * pix + 1] = acc_g + T * a.bg1;
+    a.out_color[3 * pix + 2] = acc_b + T * a.bg2;
+    a.out_depth[pix] = acc_z;
+    a.out_alpha[pix] = 1.f - T;
+    if (a.out_ncontrib) a.out_ncontrib[pix] = ncontrib;
+    a.tfinal[pix] = T;
+    a.last[pix] = last;
+  }
+  if (DC > 0) {
+    float* dst = a.out_feature + pix * a.D + a.c0;
+    if (vec_ok) {
+#pragma unroll
+      for (int c = 0; c < DC; c += 4)
+        *reinterpret_cast<float4*>(dst + c) = make_float4(accf[c], accf[c + 1], accf[c + 2], accf[c + 3]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        if (c < nf) dst[c] = accf[c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+static void launch_blend(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
+  switch (dc) {
+    case 0: k_blend<0><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 4: k_blend<4><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 8: k_blend<8><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 16: k_blend<16><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    default: k_blend<32><<<ntiles, kTilePixels, 0, s>>>(a); break;
+  }
+}
+
+int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRasterConfig& cfg,
+                   const RenderLayout& L, void* ws, Fs4dImages& out, int32_t* status, cudaStream_t s) {
+  const int64_t K = L.K;
+  uint32_t* counters = at<uint32_t>(ws, L.counters);
+  cudaMemsetAsync(counters, 0, CNT_WORDS * 4, s);
+  cudaMemsetAsync(at<uint2>(ws, L.ranges), 0, (size_t)L.ntiles * 8, s);
+
+  PreArgs p;
+  p.c = snap;
+  for (int r = 0; r < 3; ++r) {
+    for (int k = 0; k < 3; ++k) p.R[3 * r + k] = cam.T[4 * r + k];
+    p.tv[r] = cam.T[4 * r + 3];
+  }
+  for (int k = 0; k < 3; ++k)  // camera centre C = -R^T t
+    p.campos[k] = -(p.R[k] * p.tv[0] + p.R[3 + k] * p.tv[1] + p.R[6 + k] * p.tv[2]);
+  p.fx = cam.K[0];
+  p.fy = cam.K[4];
+  p.cx = cam.K[2];
+  p.cy = cam.K[5];
+  p.H = L.H;
+  p.W = L.W;
+  p.ntx = L.ntx;
+  p.nty = L.nty;
+  p.z_near = cfg.z_near;
+  p.lowpass = cfg.lowpass;
+  p.with_features = cfg.with_features;
+  p.xy = at<float2>(ws, L.xy);
+  p.conic_o = at<float4>(ws, L.conic_o);
+  p.pix_rect = at<int4>(ws, L.pix_rect);
+  p.tile_rect = at<int4>(ws, L.tile_rect);
+  p.rgbz = at<float4>(ws, L.rgbz);
+  p.cov_r = at<float4>(ws, L.cov_r);
+  p.z64 = at<double>(ws, L.z64);
+  p.dkeys = at<uint32_t>(ws, L.dkeys0);
+  p.dvals = at<uint32_t>(ws, L.dvals0);
+  p.clamp_mask = at<uint32_t>(ws, L.clamp_mask);
+  p.counters = counters;
+  p.status = status;
+  if (K > 0) k_preprocess<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(p);
+
+  // stable global depth order (culled rows carry key 0xFFFFFFFF and sort last)
+  uint32_t* dk[2] = {at<uint32_t>(ws, L.dkeys0), at<uint32_t>(ws, L.dkeys1)};
+  uint32_t* dv[2] = {at<uint32_t>(ws, L.dvals0), at<uint32_t>(ws, L.dvals1)};
+  void* scratch = at<void>(ws, L.scratch);
+  int df = radix_sort_pairs(dk, dv, K, nullptr, 0, 32, scratch, s);
+  if (K > 0) k_depth_tie_fixup<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dk[df], dv[df], p.z64, K, counters);
+  const uint32_t* order = dv[df];
+
+  // tile binning: count -> scan -> emit -> stable sort by tile -> ranges
+  uint32_t* tcount = at<uint32_t>(ws, L.tcount);
+  uint64_t* toff = at<uint64_t>(ws, L.toff);
+  if (K > 0)
+    k_tile_count<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, p.tile_rect, K, counters, tcount,
+                                                             at<int32_t>(ws, L.rank_of));
+  exclusive_scan_u32_to_u64(tcount, toff, K, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64), scratch, s);
+  k_pairs_check<<<1, 1, 0, s>>>(counters, L.cap, status);
+  uint32_t* pk[2] = {at<uint32_t>(ws, L.pkeys0), at<uint32_t>(ws, L.pkeys1)};
+  uint32_t* pv[2] = {at<uint32_t>(ws, L.pvals0), at<uint32_t>(ws, L.pvals1)};
+  if (K > 0)
+    k_emit_pairs<<<(unsigned)ceil_div(K * 32, 256), 256, 0, s>>>(order, p.tile_rect, toff, counters, L.cap, L.ntx,
+                                                                  pk[0], pv[0]);
+  int pf = radix_sort_pairs(pk, pv, L.cap, counters + CNT_PAIRS_CLAMPED, 0, L.tile_bits, scratch, s);
+  if (L.cap > 0)
+    k_tile_ranges<<<(unsigned)ceil_div(L.cap, 256), 256, 0, s>>>(pk[pf], counters, at<uint2>(ws, L.ranges));
+
+  // blend
+  BlendArgs b;
+  b.H = L.H;
+  b.W = L.W;
+  b.ntx = L.ntx;
+  b.D = cfg.with_features ? L.D : 0;
+  b.alpha_cap = (float)cfg.alpha_cap;
+  b.alpha_skip = (float)cfg.alpha_skip;
+  b.stop = (float)cfg.stop_transmittance;
+  b.bg0 = (float)cfg.background[0];
+  b.bg1 = (float)cfg.background[1];
+  b.bg2 = (float)cfg.background[2];
+  b.ranges = at<uint2>(ws, L.ranges);
+  b.pvals = pv[pf];
+  b.xy = p.xy;
+  b.conic_o = p.conic_o;
+  b.pix_rect = p.pix_rect;
+  b.rgbz = p.rgbz;
+  b.features = snap.features;
+  b.out_color = out.color;
+  b.out_depth = out.depth;
+  b.out_feature = out.feature;
+  b.out_alpha = out.alpha;
+  b.out_ncontrib = out.n_contrib;
+  b.tfinal = at<float>(ws, L.tfinal);
+  b.last = at<int32_t>(ws, L.last);
+  if (L.ntiles > 0) {
+    int c0 = 0;
+    do {
+      int rem = b.D - c0;
+      int dc = rem <= 0 ? 0 : rem <= 4 ? 4 : rem <= 8 ? 8 : rem <= 16 ? 16 : 32;
+      b.c0 = c0;
+      launch_blend(dc, L.ntiles, b, s);
+      c0 += dc;
+    } while (c0 < b.D);
+  }
+  return check_launch("render_fwd");
+}
+
+// ---------------------------------------------------------------------------
+// record export (ProjectedGaussians / tile lists)
+// ---------------------------------------------------------------------------
+__global__ void k_export_projected(const uint32_t* __restrict__ order, const uint32_t* counters, int64_t K,
+                                   const float2* xy, const float4* conic_o, const float4* rgbz, const float4* cov_r,
+                                   const int4* tile_rect, Fs4dProjected o) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (int64_t)counters[CNT_VISIBLE] || r >= K) return;
+  const uint32_t i = order[r];
+  const float2 m = xy[i];
+  const float4 co = conic_o[i], cz = rgbz[i], cv = cov_r[i];
+  if (o.mean2d) { o.mean2d[2 * r] = m.x; o.mean2d[2 * r + 1] = m.y; }
+  if (o.cov2d) { o.cov2d[3 * r] = cv.x; o.cov2d[3 * r + 1] = cv.y; o.cov2d[3 * r + 2] = cv.z; }
+  if (o.conic) { o.conic[3 * r] = co.x; o.conic[3 * r + 1] = co.y; o.conic[3 * r + 2] = co.z; }
+  if (o.view_depth) o.view_depth[r] = cz.w;
+  if (o.radius) o.radius[r] = cv.w;
+  if (o.color) { o.color[3 * r] = cz.x; o.color[3 * r + 1] = cz.y; o.color[3 * r + 2] = cz.z; }
+  if (o.opacity) o.opacity[r] = co.w;
+  if (o.source_index) o.source_index[r] = (int32_t)i;
+  if (o.tiles_touched) {
+    int4 t = tile_rect[i];
+    o.tiles_touched[r] = (t.y - t.x + 1) * (t.w - t.z + 1);
+  }
+}
+
+int render_export_projected(const RenderLayout& L, void* ws, Fs4dProjected& out, cudaStream_t s) {
+  uint32_t* dv = at<uint32_t>(ws, L.depth_final ? L.dvals1 : L.dvals0);
+  if (L.K > 0)
+    k_export_projected<<<(unsigned)ceil_div(L.K, 256), 256, 0, s>>>(
+        dv, at<uint32_t>(ws, L.counters), L.K, at<float2>(ws, L.xy), at<float4>(ws, L.conic_o),
+        at<float4>(ws, L.rgbz), at<float4>(ws, L.cov_r), at<int4>(ws, L.tile_rect), out);
+  return check_launch("render_export_projected");
+}
+
+__global__ void k_export_pairs(const uint32_t* __restrict__ pvals, const int32_t* __restrict__ rank_of,
+                               const uint32_t* counters, int32_t* out, int64_t max_pairs) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)counters[CNT_PAIRS_CLAMPED] || p >= max_pairs) return;
+  out[p] = rank_of[pvals[p]];
+}
+
+int render_export_tiles(const RenderLayout& L, void* ws, int32_t* ranges, int32_t* rows, int64_t max_pairs,
+                        cudaStream_t s) {
+  if (ranges) cudaMemcpyAsync(ranges, at<void>(ws, L.ranges), (size_t)L.ntiles * 8, cudaMemcpyDeviceToDevice, s);
+  if (rows && max_pairs > 0)
+    k_export_pairs<<<(unsigned)ceil_div(max_pairs, 256), 256, 0, s>>>(
+        at<uint32_t>(ws, L.pair_final ? L.pvals1 : L.pvals0), at<int32_t>(ws, L.rank_of),
+        at<uint32_t>(ws, L.counters), rows, max_pairs);
+  return check_launch("render_export_tiles");
+}
+
+}  // namespace fs4d

@@ -1,0 +1,427 @@
+"""Device-resident (torch CUDA) fast path over libfs4d.
+
+PyTorch is only the allocator/stream provider here: every op is one call into
+the C ABI (include/fs4d.h) on the current CUDA stream.  Objects:
+
+  DeviceCloud   GaussianCloud as fp32 SoA tensors (gaussians.py:39-94)
+  DeviceField   HexPlaneField planes + aabb (hexplane.py:49-92)
+  DeviceNet     DeformationNet weights (deformation.py:32-73)
+  Renderer      owns the render record (workspace) + status block and grows
+                the tile-pair capacity on overflow (no host sync in steady
+                state when check=False)
+
+The numpy-facing modules (rasterizer, deformation) wrap these to keep the
+reference API unchanged.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigurationError
+
+BRANCHES = ("position", "rotation", "scale", "opacity")
+BRANCH_DIMS = (3, 4, 3, 1)
+
+
+def _p(t):
+    """Device address of a tensor (None -> NULL), usable as a ctypes c_void_p
+    argument or struct field."""
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dev(x, device):
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32), device=device)
+
+
+class DeviceCloud:
+    """fp32 SoA cloud on the GPU. sh_rest is [K, (L+1)^2 - 1, 3] or None."""
+
+    FIELDS = ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features")
+
+    def __init__(self, positions, rotations, log_scales, opacity_logits, colors_raw, features,
+                 sh_rest=None):
+        self.positions = positions
+        self.rotations = rotations
+        self.log_scales = log_scales
+        self.opacity_logits = opacity_logits
+        self.colors_raw = colors_raw
+        self.features = features
+        self.sh_rest = sh_rest
+
+    def __len__(self):
+        return self.positions.shape[0]
+
+    @property
+    def feature_dim(self):
+        return self.features.shape[1]
+
+    @property
+    def sh_degree(self):
+        if self.sh_rest is None or self.sh_rest.shape[1] == 0:
+            return 0
+        return int(round(np.sqrt(self.sh_rest.shape[1] + 1))) - 1
+
+    @classmethod
+    def from_cloud(cls, cloud, device="cuda"):
+        sh = getattr(cloud, "sh_rest", None)
+        k = len(cloud)
+        return cls(_dev(cloud.positions, device).reshape(k, 3),
+                   _dev(cloud.rotations, device).reshape(k, 4),
+                   _dev(cloud.log_scales, device).reshape(k, 3),
+                   _dev(cloud.opacity_logits, device).reshape(k),
+                   _dev(cloud.colors_raw, device).reshape(k, 3),
+                   _dev(cloud.features, device).reshape(k, -1),
+                   None if sh is None else _dev(sh, device).reshape(k, -1, 3))
+
+    @classmethod
+    def empty(cls, k, d, sh_degree=0, device="cuda"):
+        f = dict(dtype=torch.float32, device=device)
+        n_sh = (sh_degree + 1) ** 2 - 1
+        return cls(torch.empty(k, 3, **f), torch.empty(k, 4, **f), torch.empty(k, 3, **f),
+                   torch.empty(k, **f), torch.empty(k, 3, **f), torch.empty(k, d, **f),
+                   torch.empty(k, n_sh, 3, **f) if n_sh > 0 else None)
+
+    def struct(self):
+        s = N.Cloud()
+        s.K = len(self)
+        s.D = self.feature_dim
+        s.sh_degree = self.sh_degree
+        for name in self.FIELDS:
+            setattr(s, name, _p(getattr(self, name)))
+        s.sh_rest = _p(self.sh_rest)
+        return s
+
+
+def camera_struct(K, T, height, width):
+    c = N.Camera()
+    c.height = int(height)
+    c.width = int(width)
+    c.K[:] = [float(v) for v in np.asarray(K, dtype=np.float64).reshape(9)]
+    c.T[:] = [float(v) for v in np.asarray(T, dtype=np.float64).reshape(16)]
+    return c
+
+
+def raster_struct(cfg):
+    r = N.RasterCfg()
+    r.tile = int(cfg.tile)
+    r.with_features = int(bool(cfg.with_features))
+    r.z_near = float(cfg.z_near)
+    r.lowpass = float(cfg.lowpass)
+    r.alpha_cap = float(cfg.alpha_cap)
+    r.alpha_skip = float(cfg.alpha_skip)
+    r.stop_transmittance = float(cfg.stop_transmittance)
+    bg = np.zeros(3) if cfg.background is None else np.asarray(cfg.background, dtype=np.float64)
+    r.background[:] = [float(v) for v in bg.reshape(3)]
+    return r
+
+
+class StatusBlock:
+    """Device int32[32] status words (FS4D_ST_*), reset before each call."""
+
+    def __init__(self, device="cuda"):
+        self.t = torch.zeros(N.STATUS_WORDS, dtype=torch.int32, device=device)
+
+    def reset(self):
+        N.check(N.load().fs4d_status_reset(_p(self.t), _stream()))
+
+    def read(self):
+        return self.t.cpu().numpy()
+
+    def raise_if_error(self):
+        st = self.read()
+        N.raise_device_status(st)
+        return st
+
+
+class DeviceField:
+    """HexPlane planes [levels][6] of [Ra, Rb, C] fp32 plus the aabb."""
+
+    def __init__(self, planes, aabb, channels):
+        self.planes = planes
+        self.aabb = np.asarray(aabb, dtype=np.float64).reshape(2, 3)
+        self.channels = int(channels)
+
+    @property
+    def levels(self):
+        return len(self.planes)
+
+    @property
+    def latent_dim(self):
+        return self.channels * self.levels
+
+    @classmethod
+    def from_field(cls, field, device="cuda"):
+        planes = [[_dev(p, device) for p in level] for level in field.planes]
+        return cls(planes, field.aabb, field.channels)
+
+    def zeros_like(self):
+        return DeviceField([[torch.zeros_like(p) for p in level] for level in self.planes],
+                           self.aabb, self.channels)
+
+    def struct(self):
+        h = N.HexPlane()
+        h.levels = self.levels
+        h.channels = self.channels
+        if self.levels > N.MAX_LEVELS:
+            raise ConfigurationError(f"at most {N.MAX_LEVELS} hexplane levels are supported")
+        for l, level in enumerate(self.planes):
+            for p, plane in enumerate(level):
+                h.res[l][p][0] = plane.shape[0]
+                h.res[l][p][1] = plane.shape[1]
+                h.planes[l][p] = plane.data_ptr()
+        h.aabb[:] = [float(v) for v in self.aabb.reshape(6)]
+        return h
+
+
+class DeviceNet:
+    """Deformation MLP weights ([out,in] fp32, exactly LinearLayer.weight)."""
+
+    def __init__(self, layers, latent_dim, width, depth, feature_dim, enable_grid=True,
+                 enable_feature_update=True):
+        # layers: dict stack-name -> list of (weight, bias, relu)
+        self.layers = layers
+        self.latent_dim = int(latent_dim)
+        self.width = int(width)
+        self.depth = int(depth)
+        self.feature_dim = int(feature_dim)
+        self.enable_grid = bool(enable_grid)
+        self.enable_feature_update = bool(enable_feature_update)
+
+    @staticmethod
+    def stack_names():
+        names = ["net.trunk"]
+        for b in BRANCHES:
+            names += [f"net.ext.{b}", f"net.head.{b}"]
+        return names + ["net.feat"]
+
+    @classmethod
+    def from_net(cls, net, device="cuda"):
+        layers = {}
+        for prefix, stack in net.stacks():
+            layers[prefix] = [(_dev(l.weight, device), _dev(l.bias, device),
+                               l.activation == "relu") for l in stack]
+        c = net.cfg
+        return cls(layers, net.latent_dim, c.width, c.depth, c.feature_dim, c.enable_grid,
+                   c.enable_feature_update)
+
+    def zeros_like(self):
+        layers = {k: [(torch.zeros_like(w), torch.zeros_like(b), r) for (w, b, r) in v]
+                  for k, v in self.layers.items()}
+        return DeviceNet(layers, self.latent_dim, self.width, self.depth, self.feature_dim,
+                         self.enable_grid, self.enable_feature_update)
+
+    def struct(self):
+        s = N.DeformNet()
+        s.latent_dim = self.latent_dim
+        s.width = self.width
+        s.depth = self.depth
+        s.feature_dim = self.feature_dim
+        s.enable_grid = int(self.enable_grid)
+        s.enable_feature_update = int(self.enable_feature_update)
+        if self.depth > N.MAX_TRUNK:
+            raise ConfigurationError(f"trunk depth above {N.MAX_TRUNK} is not supported")
+
+        def fill(dst, layer):
+            w, b, relu = layer
+            dst.weight = w.data_ptr()
+            dst.bias = b.data_ptr()
+            dst.out_dim, dst.in_dim = int(w.shape[0]), int(w.shape[1])
+            dst.relu = int(relu)
+
+        for i, layer in enumerate(self.layers["net.trunk"]):
+            fill(s.trunk[i], layer)
+        for bi, b in enumerate(BRANCHES):
+            for k in range(2):
+                fill(s.ext[bi][k], self.layers[f"net.ext.{b}"][k])
+            fill(s.head[bi], self.layers[f"net.head.{b}"][0])
+        for k in range(2):
+            fill(s.feat[k], self.layers["net.feat"][k])
+        return s
+
+
+class DeformEngine:
+    """Runs fs4d_deform_fwd / fs4d_deform_bwd with a cached workspace."""
+
+    def __init__(self, device="cuda"):
+        self.device = device
+        self.ws = None
+
+    def _workspace(self, net_s, k):
+        need = N.load().fs4d_deform_workspace_bytes(ctypes.byref(net_s), k)
+        if need == 0:
+            N.check(N.ERR_CONFIG)
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = torch.empty(int(need), dtype=torch.uint8, device=self.device)
+        return self.ws
+
+    def forward(self, cloud, field, net, t, out=None):
+        """Snapshot at time t (raw-space deltas; colours/SH aliased)."""
+        k = len(cloud)
+        if out is None:
+            out = DeviceCloud.empty(k, cloud.feature_dim, 0, self.device)
+        out.colors_raw = cloud.colors_raw
+        out.sh_rest = cloud.sh_rest
+        if not net.enable_feature_update:
+            out.features = cloud.features
+        cs, fs, ns, os_ = cloud.struct(), field.struct(), net.struct(), out.struct()
+        ws = self._workspace(ns, k)
+        N.check(N.load().fs4d_deform_fwd(ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns),
+                                         float(t), ctypes.byref(os_), _p(ws), ws.numel(), None,
+                                         _stream()))
+        return out
+
+    def backward(self, cloud, field, net, t, snap_grads):
+        """Returns (d_positions [K,3], net_grads DeviceNet, plane_grads DeviceField|None)."""
+        k = len(cloud)
+        gpos = torch.empty(k, 3, dtype=torch.float32, device=self.device)
+        ngrads = net.zeros_like()
+        pgrads = field.zeros_like() if net.enable_grid else None
+        cs, fs, ns = cloud.struct(), field.struct(), net.struct()
+        sgs, ngs = snap_grads.struct(), ngrads.struct()
+        cgs = N.Cloud()
+        cgs.K = k
+        cgs.positions = gpos.data_ptr()
+        pgs = pgrads.struct() if pgrads is not None else None
+        ws = self._workspace(ns, k)
+        N.check(N.load().fs4d_deform_bwd(ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns),
+                                         float(t), ctypes.byref(sgs), ctypes.byref(cgs),
+                                         ctypes.byref(ngs),
+                                         ctypes.byref(pgs) if pgs is not None else None,
+                                         _p(ws), ws.numel(), None, _stream()))
+        return gpos, ngrads, pgrads
+
+
+class RenderRecordDev:
+    """Device render record: workspace + the sizes it was laid out for."""
+
+    def __init__(self, info, ws, status):
+        self.info = info
+        self.ws = ws
+        self.status = status
+
+    @property
+    def n_visible(self):
+        return int(self.status.read()[N.ST_N_VISIBLE])
+
+    @property
+    def n_pairs(self):
+        st = self.status.read()
+        return (int(st[N.ST_PAIRS_HI]) << 32) | (int(st[N.ST_PAIRS_LO]) & 0xFFFFFFFF)
+
+
+class Renderer:
+    """Owns one reusable record; fs4d_render_fwd / fs4d_render_bwd."""
+
+    def __init__(self, device="cuda", pair_capacity=None):
+        self.device = device
+        self.cap = pair_capacity
+        self.ws = None
+        self.status = StatusBlock(device)
+        self.info = None
+
+    def _info(self, k, h, w, d, sh, cap):
+        i = N.RecordInfo()
+        i.K, i.height, i.width, i.D, i.sh_degree, i.tile, i.pair_capacity = k, h, w, d, sh, 16, cap
+        return i
+
+    def _prepare(self, k, h, w, d, sh, tile):
+        if tile != 16:
+            raise ConfigurationError("only tile = 16 is implemented on device")
+        if self.cap is None:
+            self.cap = max(1024, 8 * k)
+        info = self._info(k, h, w, d, sh, self.cap)
+        need = N.load().fs4d_render_workspace_bytes(ctypes.byref(info))
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = torch.empty(int(need), dtype=torch.uint8, device=self.device)
+        self.info = info
+        return info
+
+    def alloc_images(self, h, w, d):
+        f = dict(dtype=torch.float32, device=self.device)
+        return {"color": torch.empty(h, w, 3, **f), "depth": torch.empty(h, w, **f),
+                "feature": torch.empty(h, w, d, **f), "alpha": torch.empty(h, w, **f),
+                "n_contrib": torch.empty(h, w, dtype=torch.int32, device=self.device)}
+
+    def forward(self, cloud, K, T, height, width, cfg, images=None, check=True):
+        """Render one frame.  check=True reads the status block back (one
+        sync) and raises / grows the pair buffer; check=False keeps the call
+        fully asynchronous (caller checks self.status later)."""
+        k, d, sh = len(cloud), cloud.feature_dim, cloud.sh_degree
+        dout = d if cfg.with_features else 0
+        if images is None:
+            images = self.alloc_images(height, width, dout)
+        cs, cam, rc = cloud.struct(), camera_struct(K, T, height, width), raster_struct(cfg)
+        imgs = N.Images()
+        imgs.color, imgs.depth, imgs.alpha = (images["color"].data_ptr(), images["depth"].data_ptr(),
+                                              images["alpha"].data_ptr())
+        imgs.feature = images["feature"].data_ptr() if dout > 0 else None
+        imgs.n_contrib = images["n_contrib"].data_ptr() if images.get("n_contrib") is not None else None
+        for _attempt in range(4):
+            info = self._prepare(k, height, width, d, sh, cfg.tile)
+            self.status.reset()
+            N.check(N.load().fs4d_render_fwd(ctypes.byref(cs), ctypes.byref(cam), ctypes.byref(rc),
+                                             ctypes.byref(info), _p(self.ws), self.ws.numel(),
+                                             ctypes.byref(imgs), _p(self.status.t), _stream()))
+            if not check:
+                break
+            st = self.status.read()
+            if int(st[N.ST_CODE]) == N.ERR_CAPACITY:
+                pairs = (int(st[N.ST_PAIRS_HI]) << 32) | (int(st[N.ST_PAIRS_LO]) & 0xFFFFFFFF)
+                if pairs >= 2 ** 31:
+                    raise ConfigurationError("more than 2^31 tile pairs in one frame")
+                self.cap = int(pairs * 1.25) + 1024
+                continue
+            N.raise_device_status(st)
+            break
+        rec = RenderRecordDev(self.info, self.ws, self.status)
+        return images, rec
+
+    def backward(self, cloud, K, T, height, width, cfg, rec, d_color=None, d_depth=None,
+                 d_feature=None, d_alpha=None, grads=None):
+        k, d, sh = len(cloud), cloud.feature_dim, cloud.sh_degree
+        if grads is None:
+            grads = DeviceCloud.empty(k, d, sh, self.device)
+        vs_index = torch.empty(max(k, 1), dtype=torch.int32, device=self.device)
+        vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device)
+        cs, cam, rc, gs = cloud.struct(), camera_struct(K, T, height, width), raster_struct(cfg), grads.struct()
+        up = N.ImageGrads()
+        up.d_color, up.d_depth = _p(d_color), _p(d_depth)
+        up.d_feature, up.d_alpha = _p(d_feature), _p(d_alpha)
+        N.check(N.load().fs4d_render_bwd(ctypes.byref(cs), ctypes.byref(cam), ctypes.byref(rc),
+                                         ctypes.byref(rec.info), _p(rec.ws), rec.ws.numel(),
+                                         ctypes.byref(up), ctypes.byref(gs), _p(vs_index),
+                                         _p(vs_norm), None, _stream()))
+        return grads, vs_index, vs_norm
+
+    def export_projected(self, rec):
+        k = int(rec.info.K)
+        f = dict(dtype=torch.float32, device=self.device)
+        out = {"mean2d": torch.zeros(k, 2, **f), "cov2d": torch.zeros(k, 3, **f),
+               "conic": torch.zeros(k, 3, **f), "view_depth": torch.zeros(k, **f),
+               "radius": torch.zeros(k, **f), "color": torch.zeros(k, 3, **f),
+               "opacity": torch.zeros(k, **f),
+               "source_index": torch.zeros(k, dtype=torch.int32, device=self.device),
+               "tiles_touched": torch.zeros(k, dtype=torch.int32, device=self.device)}
+        p = N.Projected()
+        for name, t in out.items():
+            setattr(p, name, t.data_ptr() if t.numel() else None)
+        N.check(N.load().fs4d_render_export_projected(ctypes.byref(rec.info), _p(rec.ws),
+                                                      rec.ws.numel(), ctypes.byref(p), _stream()))
+        return out
+
+    def export_tiles(self, rec):
+        h, w = int(rec.info.height), int(rec.info.width)
+        ntiles = ((h + 15) // 16) * ((w + 15) // 16)
+        npairs = min(rec.n_pairs, int(rec.info.pair_capacity))
+        ranges = torch.zeros(ntiles, 2, dtype=torch.int32, device=self.device)
+        rows = torch.zeros(max(npairs, 1), dtype=torch.int32, device=self.device)
+        N.check(N.load().fs4d_render_export_tiles(ctypes.byref(rec.info), _p(rec.ws), rec.ws.numel(),
+                                                  _p(ranges), _p(rows), npairs, _stream()))
+        return ranges, rows[:npairs]

@@ -1,0 +1,78 @@
+"""HexPlane field container (hexplane.py:16-92 API).
+
+Planes are stored channel-last [Ra, Rb, C] float64 on the host like the
+reference; the query (bilinear gather + six-plane product) and its backward
+run inside libfs4d's deform kernels (csrc/deform.cu).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ConfigurationError
+
+PLANE_AXES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
+TIME_AXIS = 3
+
+
+@dataclass
+class HexPlaneConfig:
+    levels: tuple = (1, 2, 4, 8)
+    base_resolution: tuple = (64, 64, 64, 100)
+    out_dim: int = 64
+    feat_dim: int = 0
+    init_scale: float = 0.1
+
+    def channels_per_level(self):
+        if self.feat_dim > 0:
+            return self.feat_dim
+        n = len(self.levels)
+        if self.out_dim % n:
+            raise ConfigurationError(
+                f"out_dim {self.out_dim} not divisible by {n} levels; set feat_dim explicitly")
+        return self.out_dim // n
+
+
+def plane_shape(cfg, mult, axes):
+    """Spatial axes scale with the level multiplier, time does not (hexplane.py:41-46)."""
+    return tuple(cfg.base_resolution[a] * (1 if a == TIME_AXIS else mult) for a in axes)
+
+
+class HexPlaneField:
+    """Grids of every level plus the aabb normalising query positions."""
+
+    def __init__(self, cfg, aabb, rng, init="reference"):
+        self.cfg = cfg
+        self.aabb = np.asarray(aabb, dtype=np.float64)
+        if self.aabb.shape != (2, 3) or not np.all(self.aabb[1] > self.aabb[0]):
+            raise ConfigurationError("aabb must be [2, 3] with hi > lo")
+        self.channels = cfg.channels_per_level()
+        self.planes = []
+        for mult in cfg.levels:
+            level = []
+            for axes in PLANE_AXES:
+                ra, rb = plane_shape(cfg, mult, axes)
+                if min(ra, rb) < 2:
+                    raise ConfigurationError("plane resolutions must be >= 2")
+                shape = (ra, rb, self.channels)
+                if init == "reference":   # 1 +- init_scale (hexplane.py:65-66)
+                    level.append(1.0 + rng.uniform(-cfg.init_scale, cfg.init_scale, size=shape))
+                elif init == "uniform":   # BASELINE configs: U[0.1, 0.5]
+                    level.append(rng.uniform(0.1, 0.5, size=shape))
+                elif init == "zeros":
+                    level.append(np.zeros(shape))
+                else:
+                    raise ConfigurationError(f"unknown plane init {init!r}")
+            self.planes.append(level)
+
+    @property
+    def latent_dim(self):
+        return self.channels * len(self.cfg.levels)
+
+    def param_arrays(self):
+        return {f"grid.l{li}.p{pi}": plane
+                for li, level in enumerate(self.planes) for pi, plane in enumerate(level)}
+
+    def set_param(self, name, arr):
+        _, l, p = name.split(".")
+        self.planes[int(l[1:])][int(p[1:])] = arr

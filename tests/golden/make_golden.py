@@ -1,0 +1,183 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+    python tests/golden/make_golden.py
+It imports the reference package `featsplat` from /root/reference/pkg/src
+(read-only, unmodified), feeds it seeded fp32-representable inputs and
+stores inputs + reference outputs as .npz fixtures next to this script.  The
+GPU box has no /root/reference; tests read only these fixtures.
+"""
+
+import importlib
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def load_reference():
+    sys.path.insert(0, REF_SRC)
+    mods = {}
+    for m in ("gaussians", "rasterizer", "hexplane", "deformation", "numerics"):
+        mods[m] = importlib.import_module(f"featsplat.{m}")
+    return mods
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def cloud_arrays(rng, k, nf, op_range, depth_range, xy=0.9, ls_range=(0.08, 0.35)):
+    """conftest.random_cloud-style inputs (tests/conftest.py:17-27), rounded to fp32."""
+    pos = np.column_stack([rng.uniform(-xy, xy, k), rng.uniform(-xy, xy, k),
+                           rng.uniform(*depth_range, k)])
+    rot = rng.normal(size=(k, 4))
+    ls = np.log(rng.uniform(*ls_range, size=(k, 3)))
+    p = rng.uniform(*op_range, k)
+    return dict(positions=f32(pos), rotations=f32(rot), log_scales=f32(ls),
+                opacity_logits=f32(np.log(p) - np.log1p(-p)),
+                colors_raw=f32(rng.uniform(0.1, 0.9, size=(k, 3))),
+                features=f32(rng.normal(size=(k, nf))))
+
+
+def make_cloud(ref, arrs):
+    G = ref["gaussians"].GaussianCloud
+    return G(**{k: v.copy() for k, v in arrs.items()})
+
+
+def frame(ref, h, w, focal, T=None, time=0.0):
+    CF = ref["gaussians"].CameraFrame
+    return CF(K=np.array([[focal, 0, (w - 1) / 2], [0, focal, (h - 1) / 2], [0, 0, 1.0]]),
+              T=np.eye(4) if T is None else T, time=time, image=np.zeros((h, w, 3)),
+              depth=np.zeros((h, w)), mask=np.ones((h, w), dtype=bool))
+
+
+def rigid(rng, max_deg=5.0, max_t=0.1):
+    axis = rng.normal(size=3)
+    axis /= np.linalg.norm(axis)
+    ang = np.deg2rad(rng.uniform(-max_deg, max_deg))
+    Kx = np.array([[0, -axis[2], axis[1]], [axis[2], 0, -axis[0]], [-axis[1], axis[0], 0]])
+    R = np.eye(3) + np.sin(ang) * Kx + (1 - np.cos(ang)) * Kx @ Kx
+    T = np.eye(4)
+    T[:3, :3] = R
+    T[:3, 3] = rng.uniform(-max_t, max_t, 3)
+    return T
+
+
+def render_case(ref, name, seed, k, h, w, nf, focal, bg, rigid_T=False, op_range=(0.05, 0.98),
+                depth_range=(2.2, 3.8), with_backward=True, ls_range=(0.08, 0.35)):
+    R = ref["rasterizer"]
+    rng = np.random.default_rng(seed)
+    arrs = cloud_arrays(rng, k, nf, op_range, depth_range, ls_range=ls_range)
+    T = rigid(rng) if rigid_T else np.eye(4)
+    fr = frame(ref, h, w, focal, T)
+    cfg = R.RasterConfig(background=np.asarray(bg, dtype=np.float64))
+    cloud = make_cloud(ref, arrs)
+    out = R.render(cloud, fr, cfg)
+    proj = out.record.proj
+    tiles = R.bin_tiles(proj, h, w, cfg.tile)
+    ranges, rows = [], []
+    for row in tiles:
+        for cell in row:
+            ranges.append((len(rows), len(rows) + cell.size))
+            rows.extend(cell.tolist())
+    ncontrib = np.zeros((h, w), dtype=np.int64)
+    for tr in out.record.tiles:
+        _, contrib, _, _ = R._composite_weights(tr.alpha, cfg.stop_transmittance)
+        live = (contrib & (tr.alpha > 0)).sum(axis=0).reshape(tr.ys.size, tr.xs.size)
+        ncontrib[tr.y0:tr.y0 + tr.ys.size, tr.x0:tr.x0 + tr.xs.size] = live
+    data = dict(K=fr.K, T=fr.T, height=h, width=w, background=cfg.background,
+                color=out.color, depth=out.depth, feature=out.feature, alpha=out.alpha,
+                n_contrib=ncontrib, proj_mean2d=proj.mean2d, proj_radius=proj.radius,
+                proj_source_index=proj.source_index, proj_view_depth=proj.view_depth,
+                proj_conic=proj.conic, proj_cov2d=proj.cov2d, proj_color=proj.color,
+                proj_opacity=proj.opacity,
+                tile_ranges=np.asarray(ranges, dtype=np.int64).reshape(-1, 2),
+                tile_rows=np.asarray(rows, dtype=np.int64))
+    data.update({f"cloud_{k_}": v for k_, v in arrs.items()})
+    if with_backward:
+        ups = dict(color=f32(rng.normal(size=(h, w, 3))), depth=f32(rng.normal(size=(h, w)) * 0.3),
+                   feature=f32(rng.normal(size=(h, w, nf)) * 0.5),
+                   alpha=f32(rng.normal(size=(h, w)) * 0.5))
+        g = R.render_backward(cloud, fr, out, ups["color"], ups["depth"], ups["feature"], ups["alpha"])
+        data.update({f"up_{k_}": v for k_, v in ups.items()})
+        for f in ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features",
+                  "viewspace_index", "viewspace_norm"):
+            data[f"grad_{f}"] = getattr(g, f)
+    np.savez_compressed(os.path.join(OUT, f"render_{name}.npz"), **data)
+    print("render", name, "M =", len(proj), "pairs =", len(rows))
+
+
+def deform_case(ref, name, seed, k, nf, width, depth, levels, base, out_dim, randomize=True):
+    H, D, G = ref["hexplane"], ref["deformation"], ref["gaussians"]
+    rng = np.random.default_rng(seed)
+    arrs = cloud_arrays(rng, k, nf, (0.15, 0.3), (2.2, 3.8))
+    aabb = np.array([[-1.2, -1.2, 1.8], [1.2, 1.2, 4.2]])
+    field = H.HexPlaneField(H.HexPlaneConfig(levels=levels, base_resolution=base, out_dim=out_dim), aabb, rng)
+    net = D.DeformationNet(field.latent_dim, D.DeformationConfig(width=width, depth=depth, feature_dim=nf), rng)
+    for li, level in enumerate(field.planes):
+        for pi in range(len(level)):
+            field.planes[li][pi] = f32(0.8 + rng.normal(size=level[pi].shape) * 0.3) if randomize \
+                else f32(level[pi])
+    for prefix, stack in net.stacks():
+        for layer in stack:
+            layer.weight = f32(rng.normal(size=layer.weight.shape) * 0.2)
+            layer.bias = f32(rng.normal(size=layer.bias.shape) * 0.2)
+    cloud = G.GaussianCloud(**{k_: v.copy() for k_, v in arrs.items()})
+    t = 0.61
+    snap, cache = D.deform_with_cache(cloud, field, net, t)
+    ups = {n_: f32(rng.normal(size=np.shape(getattr(cloud, n_))))
+           for n_ in ("positions", "rotations", "log_scales", "opacity_logits", "features")}
+
+    class Gr:
+        pass
+
+    gr = Gr()
+    for n_, v in ups.items():
+        setattr(gr, n_, v)
+    cg, ng, pg = D.deform_backward(cloud, field, net, cache, gr)
+    data = {f"cloud_{k_}": v for k_, v in arrs.items()}
+    data.update(aabb=aabb, t=t, width=width, depth=depth, levels=np.asarray(levels),
+                base=np.asarray(base), out_dim=out_dim, feature_dim=nf)
+    for li, level in enumerate(field.planes):
+        for pi, pl in enumerate(level):
+            data[f"plane_{li}_{pi}"] = pl
+            data[f"gplane_{li}_{pi}"] = pg[li][pi]
+    for prefix, stack in net.stacks():
+        for i, layer in enumerate(stack):
+            data[f"w:{prefix}.{i}"] = layer.weight
+            data[f"b:{prefix}.{i}"] = layer.bias
+    for k_, v in ng.items():
+        data[f"g:{k_}"] = v
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        data[f"snap_{f}"] = getattr(snap, f)
+        data[f"up_{f}"] = ups[f]
+    data["cg_positions"] = cg["positions"]
+    data["latent"] = H.query(field, cloud.positions, t)
+    np.savez_compressed(os.path.join(OUT, f"deform_{name}.npz"), **data)
+    print("deform", name)
+
+
+def main():
+    ref = load_reference()
+    # the reference's own tiled-vs-naive scenes (test_rasterizer.py:168-183 sizes)
+    render_case(ref, "s0", 0, 50, 32, 32, 4, 1.1 * 32, (0.1, 0.2, 0.3))
+    render_case(ref, "s1", 1, 200, 64, 64, 16, 1.1 * 64, (0.1, 0.2, 0.3))
+    render_case(ref, "s2", 2, 120, 48, 48, 4, 1.1 * 48, (0.1, 0.2, 0.3))
+    render_case(ref, "s3", 3, 30, 33, 33, 16, 1.1 * 33, (0.1, 0.2, 0.3))
+    # non-square, ragged tiles, rigid non-identity view (SURVEY §4 coverage gap)
+    render_case(ref, "rigid", 7, 300, 40, 72, 8, 60.0, (0.0, 0.0, 0.0), rigid_T=True)
+    # configs[0]-shaped, reduced K (fits in a small fixture): 160x128, fx=150, D=8
+    render_case(ref, "cfg0", 11, 1500, 128, 160, 8, 150.0, (0.0, 0.0, 0.0),
+                depth_range=(2.0, 4.0), op_range=(0.05, 0.95), with_backward=True,
+                ls_range=(0.01, 0.05))
+    # reference test_deformation.make_parts shapes
+    deform_case(ref, "small", 5, 6, 5, 16, 3, (1, 2), (4, 4, 4, 3), 8)
+    deform_case(ref, "wide", 6, 64, 16, 64, 1, (1, 2), (8, 8, 8, 5), 64)
+
+
+if __name__ == "__main__":
+    main()

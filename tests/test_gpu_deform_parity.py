@@ -1,0 +1,140 @@
+"""GPU parity of the deformation path (fs4d_deform_fwd / fs4d_deform_bwd through
+deform / deform_with_cache / deform_backward) against golden vectors made by
+the reference, and against the oracle at the BASELINE configs[1] shapes.
+
+Tolerances (fp32 device vs fp64 reference): snapshot 1e-4 max-abs; gradients
+1e-4 relative to the gradient scale (max(1, max|ref|))."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cloud, has_gpu, load_golden, random_cloud_arrays
+from oracle import fs4d_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+
+
+def fs():
+    import paper_2503_06161_b200 as m
+    return m
+
+
+def build_parts(g):
+    m = fs()
+    levels = tuple(int(x) for x in g["levels"])
+    base = tuple(int(x) for x in g["base"])
+    cfg = m.HexPlaneConfig(levels=levels, base_resolution=base, out_dim=int(g["out_dim"]))
+    field = m.HexPlaneField(cfg, g["aabb"], np.random.default_rng(0))
+    for l in range(len(levels)):
+        for p in range(6):
+            field.planes[l][p] = g[f"plane_{l}_{p}"]
+    net = m.DeformationNet(field.latent_dim, m.DeformationConfig(width=int(g["width"]), depth=int(g["depth"]),
+                                                                 feature_dim=int(g["feature_dim"])),
+                           np.random.default_rng(0))
+    for prefix, st in net.stacks():
+        for i, layer in enumerate(st):
+            layer.weight = g[f"w:{prefix}.{i}"]
+            layer.bias = g[f"b:{prefix}.{i}"]
+    c = golden_cloud(g)
+    cloud = m.GaussianCloud(c.positions, c.rotations, c.log_scales, c.opacity_logits, c.colors_raw, c.features)
+    return cloud, field, net
+
+
+def close(a, b, what, rel=False):
+    tol = TOL * (max(1.0, np.abs(b).max()) if rel else 1.0)
+    err = np.abs(np.asarray(a) - np.asarray(b)).max(initial=0.0)
+    assert err < tol, (what, err, tol)
+
+
+@pytest.mark.parametrize("case", ["small", "wide"])
+def test_deform_matches_reference_golden(case):
+    g = load_golden("deform_" + case)
+    cloud, field, net = build_parts(g)
+    t = float(g["t"])
+    snap, cache = fs().deform_with_cache(cloud, field, net, t)
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        close(getattr(snap, f), g[f"snap_{f}"], f)
+    assert snap.colors_raw is cloud.colors_raw
+
+    class G:
+        pass
+
+    gr = G()
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        setattr(gr, f, g[f"up_{f}"])
+    cg, ng, pg = fs().deform_backward(cloud, field, net, cache, gr)
+    close(cg["positions"], g["cg_positions"], "cloud positions", rel=True)
+    assert cg["rotations"] is gr.rotations
+    for key in g:
+        if key.startswith("g:"):
+            close(ng[key[2:]], g[key], key, rel=True)
+    for l, level in enumerate(pg):
+        for p, arr in enumerate(level):
+            close(arr, g[f"gplane_{l}_{p}"], f"plane {l}/{p}", rel=True)
+
+
+def test_flags_grid_disabled_and_feature_update_disabled():
+    g = load_golden("deform_small")
+    cloud, field, net = build_parts(g)
+    net.cfg.enable_grid = False
+    snap = fs().deform(cloud, field, net, 0.5)
+    d = snap.positions - cloud.positions
+    assert np.allclose(d, d[0], atol=1e-6)
+    net.cfg.enable_grid = True
+    net.cfg.enable_feature_update = False
+    snap = fs().deform(cloud, field, net, 0.5)
+    assert snap.features is cloud.features
+
+
+def config1_parts(k=20000, seed=0):
+    """BASELINE configs[1] shapes: levels (1,2), base (64,64,64,25), 32 ch, planes U[0.1,0.5],
+    MLP width 64 depth 1 Xavier everywhere, D=16."""
+    m = fs()
+    rng = np.random.default_rng(seed)
+    a = random_cloud_arrays(rng, k, 16, depth_range=(3.0, 6.0), xy=1.0)
+    cloud = m.GaussianCloud(**{kk: v for kk, v in a.items() if kk != "sh_rest"})
+    field = m.HexPlaneField(m.HexPlaneConfig(levels=(1, 2), base_resolution=(64, 64, 64, 25), out_dim=64),
+                            m.scene_aabb(cloud), rng, init="uniform")
+    for level in field.planes:
+        for i in range(6):
+            level[i] = level[i].astype(np.float32).astype(np.float64)
+    net = m.DeformationNet(64, m.DeformationConfig(width=64, depth=1, feature_dim=16), rng, init="xavier",
+                           head_init="xavier")
+    for _, st in net.stacks():
+        for layer in st:
+            layer.weight = layer.weight.astype(np.float32).astype(np.float64)
+    return cloud, field, net
+
+
+def oracle_net(net):
+    return {p: [(l.weight, l.bias, l.activation == "relu") for l in st] for p, st in net.stacks()}
+
+
+def test_config1_shapes_forward_and_backward_vs_oracle():
+    cloud, field, net = config1_parts()
+    t = 0.37
+    snap, cache = fs().deform_with_cache(cloud, field, net, t)
+    osnap, ocache = O.deform(cloud, field.planes, field.aabb, oracle_net(net), t)
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        close(getattr(snap, f), osnap[f], f)
+    rng = np.random.default_rng(1)
+    ups = {f: rng.normal(size=np.shape(getattr(cloud, f))).astype(np.float32).astype(np.float64)
+           for f in ("positions", "rotations", "log_scales", "opacity_logits", "features")}
+    gr = type("G", (), ups)()
+    cg, ng, pg = fs().deform_backward(cloud, field, net, cache, gr)
+    ocg, ong, opg = O.deform_backward(cloud, field.planes, field.aabb, oracle_net(net), ocache, ups)
+    close(cg["positions"], ocg["positions"], "positions", rel=True)
+    for k in ong:
+        close(ng[k], ong[k], k, rel=True)
+    for l in range(2):
+        for p in range(6):
+            close(pg[l][p], opg[l][p], f"plane {l}/{p}", rel=True)

@@ -1,0 +1,191 @@
+"""GPU edge cases the reference tests (test_rasterizer.py) exercise: closed
+forms, culls, empty/ragged inputs, error taxonomy, capacity retry, and
+size-independent properties at BASELINE sizes."""
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu, pinhole, random_cloud_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+
+
+def fs():
+    import paper_2503_06161_b200 as m
+    return m
+
+
+def frame(size=None, h=None, w=None, focal=None, T=None):
+    h = h or size
+    w = w or size
+    focal = focal if focal is not None else 1.1 * w
+    return fs().CameraFrame(K=pinhole(h, w, focal), T=np.eye(4) if T is None else T, time=0.0,
+                            image=np.zeros((h, w, 3)), depth=np.zeros((h, w)), mask=np.ones((h, w), bool))
+
+
+def lone(position, opacity, color, scale=0.5, feature=None):
+    feature = np.zeros(2) if feature is None else feature
+    return fs().GaussianCloud(positions=np.asarray([position], float), rotations=np.array([[1.0, 0, 0, 0]]),
+                              log_scales=np.log(np.full((1, 3), scale)),
+                              opacity_logits=np.asarray([float(fs().logit(opacity))]),
+                              colors_raw=np.asarray([color], float), features=np.asarray([feature], float))
+
+
+def stack(*clouds):
+    return fs().GaussianCloud(*(np.concatenate([getattr(c, f) for c in clouds]) for f in
+                                ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw",
+                                 "features")))
+
+
+def test_on_axis_projection_closed_form():
+    f, d, s = 40.0, 4.0, 0.5
+    proj = fs().project(lone([0, 0, d], 0.5, [0.5] * 3, scale=s), frame(32, focal=f), fs().RasterConfig())
+    assert len(proj) == 1
+    np.testing.assert_allclose(proj.cov2d[0], (f * s / d) ** 2 * np.eye(2) + 0.3 * np.eye(2), rtol=1e-6)
+    np.testing.assert_allclose(proj.mean2d[0], [15.5, 15.5], atol=1e-5)
+
+
+def test_behind_camera_and_offscreen_culled():
+    assert len(fs().project(lone([0, 0, -2.0], 0.5, [0.5] * 3), frame(16), fs().RasterConfig())) == 0
+    assert len(fs().project(lone([50.0, 0, 2.0], 0.5, [0.5] * 3, scale=0.01), frame(16),
+                            fs().RasterConfig())) == 0
+
+
+def test_depth_sort_stable_with_ties():
+    cloud = stack(lone([0.3, 0, 3.0], 0.4, [0.9, 0.1, 0.1]), lone([-0.3, 0, 3.0], 0.4, [0.1, 0.9, 0.1]),
+                  lone([0.0, 0, 2.0], 0.4, [0.1, 0.1, 0.9]))
+    proj = fs().project(cloud, frame(32), fs().RasterConfig())
+    assert proj.source_index.tolist() == [2, 0, 1]
+
+
+def test_single_and_stacked_blend_closed_forms():
+    out = fs().render(lone([0, 0, 3.0], 0.6, [1.0, 0, 0], scale=0.8), frame(17),
+                      fs().RasterConfig(with_features=False))
+    np.testing.assert_allclose(out.color[8, 8], [0.6, 0, 0], atol=1e-6)
+    assert out.alpha[8, 8] == pytest.approx(0.6, abs=1e-6)
+    assert out.depth[8, 8] == pytest.approx(1.8, abs=1e-5)
+    c1, c2 = np.array([1.0, 0, 0]), np.array([0, 1.0, 0])
+    out = fs().render(stack(lone([0, 0, 2.0], 0.5, c1, 0.8), lone([0, 0, 4.0], 0.5, c2, 1.6)), frame(17),
+                      fs().RasterConfig(with_features=False))
+    np.testing.assert_allclose(out.color[8, 8], 0.5 * c1 + 0.25 * c2, atol=1e-6)
+    src, alphas, weights = out.pixel_record(8, 8)
+    assert src.tolist() == [0, 1]
+
+
+def test_background_and_feature_saturation():
+    bg = np.array([0.2, 0.4, 0.6])
+    out = fs().render(lone([0, 0, 3.0], 0.6, [1.0, 0, 0], scale=0.8), frame(17),
+                      fs().RasterConfig(background=bg, with_features=False))
+    np.testing.assert_allclose(out.color[8, 8], [0.6, 0, 0] + 0.4 * bg, atol=1e-6)
+    z = np.array([0.7, -1.3, 2.0])
+    parts = [lone([0, 0, 2.0 + 0.2 * i], 0.985, [0.5] * 3, scale=1.2, feature=z) for i in range(4)]
+    out = fs().render(stack(*parts), frame(17), fs().RasterConfig())
+    assert 1 - out.alpha[8, 8] < 1e-4
+    np.testing.assert_allclose(out.feature[8, 8], z, atol=1e-3)
+
+
+def test_empty_cloud_and_all_culled():
+    rng = np.random.default_rng(0)
+    a = random_cloud_arrays(rng, 0, 4)
+    out = fs().render(fs().GaussianCloud(**{k: v for k, v in a.items()}), frame(20), fs().RasterConfig())
+    assert np.all(out.alpha == 0) and np.all(out.color == 0)
+    a = random_cloud_arrays(rng, 50, 4)
+    a["positions"][:, 2] = -3.0
+    out = fs().render(fs().GaussianCloud(**{k: v for k, v in a.items()}), frame(20), fs().RasterConfig())
+    assert np.all(out.alpha == 0)
+    g = fs().render_backward(fs().GaussianCloud(**{k: v for k, v in a.items()}), frame(20), out,
+                             np.ones((20, 20, 3)))
+    assert np.all(g.positions == 0) and g.viewspace_index.size == 0
+
+
+def test_errors_map_to_reference_taxonomy():
+    c = lone([0, 0, 3.0], 0.5, [0.5] * 3)
+    c.positions[0, 1] = np.nan
+    with pytest.raises(fs().NumericalError, match="0"):
+        fs().render(c, frame(16), fs().RasterConfig())
+    c = lone([0, 0, 3.0], 0.5, [0.5] * 3)
+    c.rotations[:] = 0.0
+    with pytest.raises(fs().DegenerateRotationError):
+        fs().render(c, frame(16), fs().RasterConfig())
+    fr = frame(16)
+    fr.K[0, 1] = 0.5
+    with pytest.raises(fs().DataError):
+        fs().render(lone([0, 0, 3.0], 0.5, [0.5] * 3), fr, fs().RasterConfig())
+    rng = np.random.default_rng(3)
+    a = random_cloud_arrays(rng, 6, 4)
+    b = random_cloud_arrays(rng, 7, 4)
+    out = fs().render(fs().GaussianCloud(**a), frame(16), fs().RasterConfig())
+    with pytest.raises(fs().ContractViolation):
+        fs().render_backward(fs().GaussianCloud(**b), frame(16), out)
+
+
+def test_capacity_overflow_retries_without_changing_result():
+    from paper_2503_06161_b200.device import DeviceCloud, Renderer
+    rng = np.random.default_rng(5)
+    a = random_cloud_arrays(rng, 3000, 8, ls_range=(0.05, 0.2))
+    cloud = DeviceCloud.from_cloud(fs().GaussianCloud(**a))
+    K = pinhole(64, 96, 80.0)
+    cfg = fs().RasterConfig()
+    big = Renderer(pair_capacity=10_000_000)
+    ref, rec = big.forward(cloud, K, np.eye(4), 64, 96, cfg)
+    small = Renderer(pair_capacity=64)
+    got, rec2 = small.forward(cloud, K, np.eye(4), 64, 96, cfg)
+    assert small.cap > 64 and rec2.n_pairs == rec.n_pairs
+    for key in ("color", "feature", "alpha", "n_contrib"):
+        assert bool((ref[key] == got[key]).all())
+
+
+@pytest.mark.parametrize("nf", [0, 3, 13, 40])
+def test_feature_widths_and_ragged_sizes(nf):
+    """D = 0 (with_features off), odd D, D > 32 (chunked blend); 33x47 ragged tiles."""
+    from oracle import fs4d_oracle as O
+    rng = np.random.default_rng(nf)
+    a = random_cloud_arrays(rng, 400, nf, ls_range=(0.03, 0.15))
+    K = pinhole(33, 47, 40.0)
+    fr = fs().CameraFrame(K=K, T=np.eye(4), time=0.0, image=np.zeros((33, 47, 3)), depth=np.zeros((33, 47)),
+                          mask=np.ones((33, 47), bool))
+    cfg = fs().RasterConfig(with_features=nf != 13)
+    out = fs().render(fs().GaussianCloud(**a), fr, cfg)
+    ref = O.render(type("C", (), a)(), K, np.eye(4), 33, 47, O.RasterParams(with_features=cfg.with_features))
+    amb = O.pixel_decision_margins(ref, O.RasterParams()) < 1e-5
+    for key in ("color", "feature", "alpha", "depth"):
+        d = np.abs(getattr(out, key) - ref[key])
+        if d.size:
+            d = d.reshape(33, 47, -1).max(axis=2)
+            assert d[~amb].max() < 1e-4, key
+
+
+def test_size_independent_properties_at_config1_size():
+    """At the 640x512 / 200k headline size: linearity in a shared feature,
+    conservation (alpha + T = 1), colour bound, determinism of the device path."""
+    import torch
+    from paper_2503_06161_b200.device import DeviceCloud, Renderer
+    rng = np.random.default_rng(9)
+    k, h, w = 200_000, 512, 640
+    a = random_cloud_arrays(rng, k, 16, op_range=(0.05, 0.95), depth_range=(3.0, 6.0), xy=1.0,
+                            ls_range=(np.exp(-5.0), np.exp(-3.0)))
+    zstar = np.linspace(-1.0, 1.0, 16)
+    a["features"] = np.tile(zstar, (k, 1))
+    a["colors_raw"] = np.tile([0.25, 0.5, 0.75], (k, 1))
+    cloud = DeviceCloud.from_cloud(fs().GaussianCloud(**a))
+    r = Renderer()
+    K = pinhole(h, w, 560.0)
+    img, rec = r.forward(cloud, K, np.eye(4), h, w, fs().RasterConfig())
+    alpha = img["alpha"].cpu().numpy()
+    feat = img["feature"].cpu().numpy()
+    col = img["color"].cpu().numpy()
+    assert alpha.min() >= 0 and alpha.max() <= 1
+    np.testing.assert_allclose(feat, alpha[:, :, None] * zstar[None, None, :], atol=2e-5)
+    np.testing.assert_allclose(col, alpha[:, :, None] * np.array([0.25, 0.5, 0.75]), atol=2e-5)
+    img2, _ = r.forward(cloud, K, np.eye(4), h, w, fs().RasterConfig())
+    for key in img:
+        assert torch.equal(img[key], img2[key])
+    assert rec.n_visible > 0.95 * k

@@ -1,0 +1,204 @@
+"""GPU parity of the rasterizer (fs4d_render_fwd / fs4d_render_bwd through the
+featsplat-compatible API) against (a) golden vectors made by the reference
+itself and (b) the CPU float64 oracle on seeded scenes.
+
+Contract: inputs are fp32-representable; discrete outputs
+(visible set, depth order, radius, tile lists, per-pixel live-contributor
+counts) must match exactly wherever the reference's deciding quantity is not
+within a relative margin TAU of its flip point; continuous outputs must agree
+to ATOL_IMG max-abs on pixels untouched by an ambiguous decision; gradients to
+ATOL_GRAD relative to the gradient scale.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import (GOLDEN, golden_cloud, has_gpu, load_golden, pinhole, random_cloud_arrays,
+                      rigid_T)
+from oracle import fs4d_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TAU = 1e-5          # relative margin below which a discrete decision is "ambiguous"
+ATOL_IMG = 1e-4     # colour / depth / feature / alpha max-abs (fp32 vs fp64 reference)
+ATOL_GRAD = 1e-4    # gradients: max-abs <= ATOL_GRAD * max(1, max|ref|)
+
+RENDER_CASES = ["s0", "s1", "s2", "s3", "rigid", "cfg0"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+
+
+def fs():
+    import paper_2503_06161_b200 as m
+    return m
+
+
+def make_frame(K, T, h, w, time=0.0):
+    return fs().CameraFrame(K=K, T=T, time=time, image=np.zeros((h, w, 3)), depth=np.zeros((h, w)),
+                            mask=np.ones((h, w), dtype=bool))
+
+
+def make_cloud(arrs):
+    return fs().GaussianCloud(**{k: v for k, v in arrs.items()})
+
+
+def ambiguous_pixels(oracle_out, cfg, h, w):
+    """Pixels whose compositing met a decision within TAU, dilated by the
+    footprint of Gaussians with an ambiguous projection decision."""
+    amb = O.pixel_decision_margins(oracle_out, cfg) < TAU
+    proj = oracle_out["proj"]
+    pm = O.projection_margins(proj, h, w, cfg.tile, cfg)
+    for g in np.flatnonzero(pm < TAU):
+        u, v, r = proj["mean2d"][g, 0], proj["mean2d"][g, 1], proj["radius"][g]
+        x0, x1 = int(max(0, np.floor(u - r - 1))), int(min(w - 1, np.ceil(u + r + 1)))
+        y0, y1 = int(max(0, np.floor(v - r - 1))), int(min(h - 1, np.ceil(v + r + 1)))
+        amb[y0:y1 + 1, x0:x1 + 1] = True
+    return amb, pm < TAU
+
+
+def compare_render(out, ref_imgs, amb, n_contrib_ref):
+    ok = ~amb
+    for key in ("color", "depth", "feature", "alpha"):
+        a, b = getattr(out, key), ref_imgs[key]
+        if a.size == 0:
+            continue
+        diff = np.abs(a - b)
+        if diff.ndim == 3:
+            diff = diff.max(axis=2)
+        assert diff[ok].max(initial=0.0) < ATOL_IMG, (key, diff[ok].max())
+    assert np.array_equal(out.n_contrib[ok], n_contrib_ref[ok])
+
+
+@pytest.mark.parametrize("case", RENDER_CASES)
+def test_render_matches_reference_golden(case):
+    g = load_golden("render_" + case)
+    h, w = int(g["height"]), int(g["width"])
+    cloud = make_cloud({k: getattr(golden_cloud(g), k) for k in
+                        ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features")})
+    cfg = fs().RasterConfig(background=g["background"])
+    frame = make_frame(g["K"], g["T"], h, w)
+    out = fs().render(cloud, frame, cfg)
+    ocfg = O.RasterParams(background=g["background"])
+    oout = O.render(golden_cloud(g), g["K"], g["T"], h, w, ocfg)
+    amb, amb_g = ambiguous_pixels(oout, ocfg, h, w)
+    assert amb.mean() < 0.02
+    compare_render(out, {k: g[k] for k in ("color", "depth", "feature", "alpha")}, amb, g["n_contrib"])
+
+    # discrete projection / binning outputs, bit-exact (no ambiguous decisions in these scenes)
+    proj = out.record.proj
+    if not amb_g.any():
+        np.testing.assert_array_equal(proj.source_index, g["proj_source_index"])
+        np.testing.assert_array_equal(proj.radius, g["proj_radius"])
+        lists = out.record.tile_lists()
+        flat = [c for row in lists for c in row]
+        np.testing.assert_array_equal(np.concatenate(flat), g["tile_rows"])
+        np.testing.assert_array_equal([c.size for c in flat], g["tile_ranges"][:, 1] - g["tile_ranges"][:, 0])
+    np.testing.assert_allclose(proj.mean2d, g["proj_mean2d"], atol=1e-3)
+
+    # backward through render_backward
+    grads = fs().render_backward(cloud, frame, out, g["up_color"], g["up_depth"], g["up_feature"], g["up_alpha"])
+    if not amb.any():
+        for f in ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features",
+                  "viewspace_norm"):
+            ref = g[f"grad_{f}"]
+            tol = ATOL_GRAD * max(1.0, np.abs(ref).max())
+            assert np.abs(getattr(grads, f) - ref).max() < tol, (f, np.abs(getattr(grads, f) - ref).max(), tol)
+        np.testing.assert_array_equal(grads.viewspace_index, g["grad_viewspace_index"])
+
+
+def _scene(seed, k=10000, h=128, w=160, focal=150.0, nf=8, rigid=False, sh=0, ls=None, op=(0.05, 0.95)):
+    rng = np.random.default_rng(seed)
+    arrs = random_cloud_arrays(rng, k, nf, op_range=op, depth_range=(2.0, 4.0), xy=1.0,
+                               ls_range=(np.exp(-4.5), np.exp(-3.0)) if ls is None else ls, sh_degree=sh)
+    T = rigid_T(rng) if rigid else np.eye(4)
+    return arrs, pinhole(h, w, focal), T, h, w
+
+
+@pytest.mark.parametrize("seed,rigid,sh", [(0, False, 0), (1, False, 0), (2, True, 0), (3, True, 3),
+                                          (4, False, 3), (5, False, 1)])
+def test_config0_scene_matches_oracle(seed, rigid, sh):
+    """configs[0]-shaped scenes (10k Gaussians, 160x128, fx=150, D=8), incl. SH and rigid views."""
+    arrs, K, T, h, w = _scene(seed, rigid=rigid, sh=sh)
+    cloud = make_cloud(arrs)
+    ocloud = type("C", (), dict(arrs))()
+    cfg = fs().RasterConfig()
+    ocfg = O.RasterParams()
+    out = fs().render(cloud, make_frame(K, T, h, w), cfg)
+    oout = O.render(ocloud, K, T, h, w, ocfg)
+    amb, amb_g = ambiguous_pixels(oout, ocfg, h, w)
+    assert amb.mean() < 0.01, amb.mean()
+    compare_render(out, oout, amb, oout["n_contrib"])
+    proj = out.record.proj
+    keep = ~amb_g
+    if not amb_g.any():
+        np.testing.assert_array_equal(proj.source_index, oout["proj"]["source_index"])
+    np.testing.assert_array_equal(np.sort(proj.source_index), np.sort(oout["proj"]["source_index"]))
+    # radius is bit-exact for every non-ambiguous Gaussian
+    pos = {s: i for i, s in enumerate(proj.source_index)}
+    idx = np.array([pos[s] for s in oout["proj"]["source_index"]])
+    assert np.array_equal(proj.radius[idx][keep], oout["proj"]["radius"][keep])
+
+
+@pytest.mark.parametrize("seed,rigid,sh", [(10, False, 0), (11, True, 0), (12, False, 3)])
+def test_config0_backward_matches_oracle(seed, rigid, sh):
+    arrs, K, T, h, w = _scene(seed, k=3000, rigid=rigid, sh=sh)
+    rng = np.random.default_rng(seed + 100)
+    ups = dict(color=rng.normal(size=(h, w, 3)), depth=rng.normal(size=(h, w)) * 0.3,
+               feature=rng.normal(size=(h, w, 8)) * 0.5, alpha=rng.normal(size=(h, w)) * 0.5)
+    ups = {k: v.astype(np.float32).astype(np.float64) for k, v in ups.items()}
+    cloud = make_cloud(arrs)
+    frame = make_frame(K, T, h, w)
+    cfg = fs().RasterConfig()
+    out = fs().render(cloud, frame, cfg)
+    g = fs().render_backward(cloud, frame, out, ups["color"], ups["depth"], ups["feature"], ups["alpha"])
+    ocloud = type("C", (), dict(arrs))()
+    ocfg = O.RasterParams()
+    oout = O.render(ocloud, K, T, h, w, ocfg)
+    og = O.render_backward(ocloud, K, T, h, w, ocfg, oout, ups["color"], ups["depth"], ups["feature"], ups["alpha"])
+    amb, amb_g = ambiguous_pixels(oout, ocfg, h, w)
+    # Gaussians touching an ambiguous pixel are excluded (their sums include a flipped term)
+    bad = set()
+    for (ty, tx), (rows, xs, ys) in oout["tiles"].items():
+        if amb[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1].any():
+            bad.update(oout["proj"]["source_index"][rows].tolist())
+    keep = np.ones(len(arrs["positions"]), dtype=bool)
+    keep[list(bad)] = False
+    assert keep.mean() > 0.5
+    fields = ["positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features"]
+    if sh:
+        fields.append("sh_rest")
+    for f in fields:
+        a = np.asarray(getattr(g, f))[keep]
+        b = np.asarray(og[f])[keep]
+        tol = ATOL_GRAD * max(1.0, np.abs(b).max())
+        assert np.abs(a - b).max() < tol, (f, np.abs(a - b).max(), tol)
+
+
+def test_render_deterministic():
+    arrs, K, T, h, w = _scene(21, k=5000)
+    cloud = make_cloud(arrs)
+    frame = make_frame(K, T, h, w)
+    a = fs().render(cloud, frame, fs().RasterConfig())
+    b = fs().render(cloud, frame, fs().RasterConfig())
+    for f in ("color", "depth", "feature", "alpha", "n_contrib"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))
+
+
+def test_tile_lists_sorted_by_depth_and_cover_visible_set():
+    arrs, K, T, h, w = _scene(22, k=4000, rigid=True)
+    cloud = make_cloud(arrs)
+    out = fs().render(cloud, make_frame(K, T, h, w), fs().RasterConfig())
+    proj = out.record.proj
+    assert np.all(np.diff(proj.view_depth) >= 0)
+    union = set()
+    for row in out.record.tile_lists():
+        for cell in row:
+            assert np.all(np.diff(cell) > 0)      # rows are depth ranks: strictly increasing
+            union.update(cell.tolist())
+    assert union == set(range(len(proj)))
