@@ -1,0 +1,411 @@
+"""Benchmark: RGB+feature frames/s of the FE-4DGS per-frame render path
+(deform at time t + tile rasterizer) on BASELINE.json configs[1]
+(200k Gaussians, 640x512, fx=fy=560, SH3, D=16, HexPlane (1,2)x(64,64,64,25)x32,
+MLP width 64 depth 1, Xavier weights, planes U[0.1,0.5]).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one frame (fs4d_deform_fwd + fs4d_render_fwd) at a fresh t on every
+rank; ranks render disjoint timesteps (configs[2]'s frame sharding: weak
+scaling, no data-path collective).  Inputs are seeded synthetic stand-ins for
+EndoNeRF (no dataset access).  `--impl reference` times the reference
+algorithm's CPU implementation (the float64 oracle port in oracle/, since the
+Python reference cannot travel to the GPU box) on bounded samples of the same
+workload with all host cores.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_GAUSS, H, W, FOCAL, SH_DEG, D = 200_000, 512, 640, 560.0, 3, 16
+WORKLOAD = "configs[1]: EndoNeRF-shaped frame, 200k Gaussians, 640x512, fx=fy=560, SH3, D=16"
+METRIC = "RGB+feature frames/s per B200 at 640x512, 200k Gaussians, D=16; 1/2/4/8 GPU"
+PUBLISHED_FPS = None  # paper's 287.95 FPS is RTX 5090 / D=128 -> not the same metric
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def make_scene(seed=0):
+    """Seeded configs[1] scene."""
+    import paper_2503_06161_b200 as fs
+    rng = np.random.default_rng(seed)
+    k = K_GAUSS
+    q = rng.normal(size=(k, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    sh = rng.normal(0.0, 0.2, size=(k, 16, 3))
+    cloud = fs.GaussianCloud(
+        positions=f32(np.column_stack([rng.uniform(-1, 1, k), rng.uniform(-1, 1, k), rng.uniform(3, 6, k)])),
+        rotations=f32(q), log_scales=f32(rng.normal(-4.0, 0.5, size=(k, 3))),
+        opacity_logits=f32(rng.normal(0.0, 1.0, size=k)),
+        colors_raw=f32(sh[:, 0, :]), features=f32(rng.normal(size=(k, D))), sh_rest=f32(sh[:, 1:, :]))
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(64, 64, 64, 25), out_dim=64),
+                             fs.scene_aabb(cloud), rng, init="uniform")
+    for level in field.planes:
+        for i in range(6):
+            level[i] = f32(level[i])
+    net = fs.DeformationNet(64, fs.DeformationConfig(width=64, depth=1, feature_dim=D), rng, init="xavier",
+                            head_init="xavier")
+    for _, st in net.stacks():
+        for layer in st:
+            layer.weight = f32(layer.weight)
+    Kmat = np.array([[FOCAL, 0, (W - 1) / 2], [0, FOCAL, (H - 1) / 2], [0, 0, 1.0]])
+    return cloud, field, net, Kmat
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work
+# ---------------------------------------------------------------------------
+def plane_floats():
+    res = {1: (64, 64, 64, 25), 2: (128, 128, 128, 25)}
+    axes = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
+    return sum(res[m][a] * res[m][b] * 32 for m in (1, 2) for a, b in axes)
+
+
+MLP_PARAMS = 64 * 64 + 64 + 4 * (64 * 32 + 32 + 32 * 32 + 32) + (32 * 3 + 3 + 32 * 4 + 4 + 32 * 3 + 3 + 32 + 1) \
+    + 128 * 32 + 32 + 32 * D + D
+FRAME_BYTES = K_GAUSS * 4 * (11 + D + 3 * (SH_DEG + 1) ** 2) + 4 * plane_floats() + 4 * MLP_PARAMS \
+    + H * W * 4 * (3 + D + 1 + 1)
+MLP_FLOPS = 2 * 21344 * K_GAUSS
+
+
+def stage_bytes(stage, n_visible, n_pairs):
+    """Algorithmic HBM bytes of one launch of each stage (inputs read once + outputs written once)."""
+    k = K_GAUSS
+    if stage == "deform_fwd":   # cloud geometry+features in, snapshot out, planes + MLP once
+        return k * 4 * (11 + D) * 2 + 4 * plane_floats() + 4 * MLP_PARAMS
+    if stage == "preprocess":   # snapshot (incl. SH) in, 96 B projected record out
+        return k * 4 * (11 + D + 3 * (SH_DEG + 1) ** 2) + n_visible * 96
+    if stage == "blend":        # projected records + features of the visible set, image out
+        return n_visible * (8 + 16 + 16 + 16 + 4 * D) + n_pairs * 4 + H * W * 4 * (3 + 1 + D + 1)
+    if stage == "depth_sort":   # key+value in/out once
+        return k * 16
+    if stage == "binning":      # pairs written once (key+value), ranges
+        return n_pairs * 8 + k * 16
+    return 0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed helpers
+# ---------------------------------------------------------------------------
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def dist_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: reference algorithm (oracle port), bounded samples
+# ---------------------------------------------------------------------------
+CPU_SLICES = 32  # one sample = 1/32 of the Gaussians deformed + 1 of 32 tile rows composited (+ full projection)
+
+
+def _cpu_worker(args):
+    seed, band = args
+    import fs4d_cpu_state as S  # populated in the parent before fork
+    from oracle import fs4d_oracle as O
+    cloud, planes, aabb, onet, Kmat = S.scene
+    k = K_GAUSS
+    sl = slice((band % CPU_SLICES) * k // CPU_SLICES, (band % CPU_SLICES + 1) * k // CPU_SLICES)
+    part = type("C", (), {n: getattr(cloud, n)[sl] for n in
+                          ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features")})()
+    t0 = time.perf_counter()
+    O.deform(part, planes, aabb, onet, 0.37)
+    t_def = time.perf_counter() - t0
+    nty = -(-H // 16)
+    t0 = time.perf_counter()
+    O.render(cloud, Kmat, np.eye(4), H, W, O.RasterParams(), tile_rows=[band % nty], prepared=S.prepared)
+    t_band = time.perf_counter() - t0
+    # projection + binning of the whole frame is paid once per frame, compositing per tile row
+    return CPU_SLICES * t_def + S.t_project + nty * t_band
+
+
+def cpu_reference(steps, warmup, seed=0, procs=None):
+    """Reference CPU path on bounded samples with all host cores; returns dict."""
+    import multiprocessing as mp
+    import types
+    from oracle import fs4d_oracle as O
+    cloud, field, net, Kmat = make_scene(seed)
+    onet = {p: [(l.weight, l.bias, l.activation == "relu") for l in st] for p, st in net.stacks()}
+    t0 = time.perf_counter()
+    proj = O.project(cloud, Kmat, np.eye(4), H, W, O.RasterParams())
+    lists = O.bin_tiles(proj, H, W, 16)
+    t_proj = time.perf_counter() - t0
+    mod = types.ModuleType("fs4d_cpu_state")
+    mod.scene = (cloud, field.planes, field.aabb, onet, Kmat)
+    mod.t_project = t_proj
+    mod.prepared = (proj, lists)
+    sys.modules["fs4d_cpu_state"] = mod
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2 ** 30
+    procs = procs or max(1, min(ncores, int(mem_gb // 4), 32))
+    ctx = mp.get_context("fork")
+    vals = []
+    with ctx.Pool(procs, initializer=lambda: os.environ.update(OMP_NUM_THREADS="1")) as pool:
+        for step in range(warmup + steps):
+            jobs = [(seed, step * procs + j) for j in range(procs)]
+            ts = time.perf_counter()
+            frame_s = pool.map(_cpu_worker, jobs)
+            wall = time.perf_counter() - ts
+            if step >= warmup:
+                vals.append(sum(1.0 / f for f in frame_s))  # aggregate frames/s of P concurrent processes
+    return {"value": float(np.mean(vals)), "cores": procs, "host_cores": ncores,
+            "sample": f"per process per step: deform of 1/{CPU_SLICES} of the 200k Gaussians + "
+                      f"compositing of 1 of {-(-H // 16)} tile rows (+ the frame's fp64 projection+binning, timed once), extrapolated to one frame "
+                      f"(frame_s = {CPU_SLICES}*t_deform_slice + t_project + n_rows*t_band); "
+                      f"value = sum over {procs} concurrent processes of 1/frame_s",
+            "project_s": t_proj, "step_wall_s": wall}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def gpu_bench(args, rank, world, local):
+    import torch
+    import paper_2503_06161_b200 as fs
+    from paper_2503_06161_b200 import device as dv
+
+    torch.cuda.set_device(local)
+    cloud_np, field_np, net_np, Kmat = make_scene(0)
+    cloud = dv.DeviceCloud.from_cloud(cloud_np)
+    field = dv.DeviceField.from_field(field_np)
+    net = dv.DeviceNet.from_net(net_np)
+    cfg = fs.RasterConfig()
+    pipe = dv.FramePipeline(cloud, field, net, H, W, cfg)
+    T = np.eye(4)
+    # timesteps of configs[2]: t = k/155, sharded contiguously over ranks; cycled for K steps
+    ts = np.arange(156) / 155.0
+    mine = np.array_split(ts, world)[rank]
+    steps, warm = args.steps, args.warmup
+
+    # size the pair buffer once (host-synchronous check), then run fully async
+    pipe.run(float(mine[0]), Kmat, T, check=True)
+    torch.cuda.synchronize()
+    st = pipe.renderer.status.read()
+    n_vis = int(st[2])
+    n_pairs = (int(st[4]) << 32) | (int(st[3]) & 0xFFFFFFFF)
+    pipe.renderer.cap = int(n_pairs * 1.5) + 4096
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    for i in range(warm):
+        pipe.run(float(mine[i % len(mine)]), Kmat, T)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            ev[i][0].record(stream)
+            pipe.run(float(mine[i % len(mine)]), Kmat, T)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    st = pipe.renderer.status.read()
+    if int(st[0]) != 0:
+        raise RuntimeError(f"device status {st[:5]} during timed region")
+    ms_max = dist_max(ms, world)
+
+    # per-stage timing pass (events around each stage on the launching stream)
+    dv.profile_collect()
+    dv.profile_enable(True)
+    for i in range(steps):
+        flush.zero_()
+        pipe.run(float(mine[i % len(mine)]), Kmat, T)
+    torch.cuda.synchronize()
+    prof = dv.profile_collect()
+    dv.profile_enable(False)
+
+    # end-to-end through the public API with host buffers (pinned H2D + D2H every step)
+    host_in, host_out = pipe.pinned_host_buffers()
+    for i in range(warm):
+        pipe.run(float(mine[i % len(mine)]), Kmat, T, host_in=host_in, host_out=host_out)
+    torch.cuda.synchronize()
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    barrier(world)
+    for i in range(steps):
+        e2e_ev[i][0].record(stream)
+        pipe.run(float(mine[i % len(mine)]), Kmat, T, host_in=host_in, host_out=host_out)
+        e2e_ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = dist_max(sum(a.elapsed_time(b) for a, b in e2e_ev), world)
+    return dict(ms=ms_max, prof=prof, clocks=clk.summary(), n_vis=n_vis, n_pairs=n_pairs, e2e_ms=e2e_ms,
+                h2d=pipe.h2d_bytes(host_in), d2h=pipe.d2h_bytes(), steps=steps)
+
+
+def launches_per_frame(n_pairs_cap_bits=11):
+    deform = 2                        # pack + k_deform_fwd
+    sort_passes = 32 // 8
+    pair_passes = -(-n_pairs_cap_bits // 8)
+    render = 1 + 1 + 3 * sort_passes + 1 + 1 + 3 + 1 + 1 + 3 * pair_passes + 1 + 1  # status,pre,sort,fix,count,scan,check,emit,sort,ranges,blend
+    return deform + render
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = dist_setup(args.gpus)
+    base = {"metric": METRIC, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded stand-in for EndoNeRF, SURVEY §8(d); z~U[3,6])",
+            "config": {"workload": WORKLOAD, "frames_per_rank_step": 1, "timesteps": "t=k/155 sharded by rank",
+                       "parallelism": f"frame-sharded x{world}", "l2": "flushed (256 MB write) between steps"}}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference(args.steps, args.warmup)
+        line = dict(base)
+        line.update({"impl": "reference", "value": r["value"], "ms_per_step": 1000.0 / r["value"],
+                     "n_gpus": world,
+                     "cpu_baseline": {"value": r["value"], "unit": "frames/s", "cores": r["cores"],
+                                      "kind": "port", "sample": r["sample"]},
+                     "e2e": {"value": r["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                             "d2h_bytes_per_step": 0}})
+        line["config"] = dict(base["config"], cpu_impl="oracle/fs4d_oracle.py (float64 NumPy port of featsplat)")
+        print(json.dumps(line))
+        return
+
+    r = gpu_bench(args, rank, world, local)
+    hbm, tf, peak_src = peaks()
+    frames = world * r["steps"]
+    value = frames / (r["ms"] / 1000.0)
+    prof = r["prof"]
+    stage_ms = {s: (ms / c if c else 0.0) for s, (ms, c) in prof.items()}
+    fwd = {s: v for s, v in stage_ms.items() if s in ("deform_fwd", "preprocess", "depth_sort", "binning", "blend")}
+    top = max(fwd, key=fwd.get)
+    frame_ms = sum(fwd.values())
+    top_bytes = stage_bytes(top, r["n_vis"], r["n_pairs"])
+    achieved = top_bytes / (stage_ms[top] / 1000.0) / 1e9
+    line = dict(base)
+    line.update({
+        "value": value, "ms_per_step": r["ms"] / r["steps"],
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": top_bytes,
+                     "share_of_step": stage_ms[top] / frame_ms if frame_ms else None},
+        "roofline_frame": {"bytes_per_frame": FRAME_BYTES,
+                           "achieved_gbs": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9,
+                           "frac": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9 / hbm},
+        "stage_ms": {k: round(v, 4) for k, v in stage_ms.items() if v},
+        "mlp": {"flops_per_frame": MLP_FLOPS,
+                "tflops": MLP_FLOPS / (stage_ms["deform_fwd"] / 1000.0) / 1e12 if stage_ms["deform_fwd"] else None},
+        "work": {"visible": r["n_vis"], "pairs": r["n_pairs"]},
+        "clocks": r["clocks"],
+        "e2e": {"value": frames / (r["e2e_ms"] / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": r["h2d"],
+                "d2h_bytes_per_step": r["d2h"]},
+        "gpu_launches": launches_per_frame() * r["steps"],
+    })
+    if rank == 0 and world == 1 and not args.no_cpu:
+        c = cpu_reference(args.cpu_steps, 0)
+        line["cpu_baseline"] = {"value": c["value"], "unit": "frames/s", "cores": c["cores"], "kind": "port",
+                                "sample": c["sample"]}
+    if rank == 0:
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -184,6 +184,23 @@ const char* fs4d_build_info(void);
  * zero codes/counters, INT32_MAX in the first-index slots. */
 int fs4d_status_reset(int32_t* status, void* stream);
 
+/* ---- optional per-stage timing ----
+ * When enabled, every entry point brackets its stages with CUDA events
+ * recorded on the launching stream; collect() waits on them, returns the
+ * summed milliseconds and call counts per stage, and resets.  Disabled by
+ * default (no events are recorded). */
+#define FS4D_STAGE_DEFORM_FWD 0   /* weight pack + k_deform_fwd           */
+#define FS4D_STAGE_PREPROCESS 1   /* k_preprocess (projection, fp64)      */
+#define FS4D_STAGE_DEPTH_SORT 2   /* radix depth sort + tie fix-up        */
+#define FS4D_STAGE_BINNING 3      /* count, scan, emit, tile sort, ranges */
+#define FS4D_STAGE_BLEND 4        /* k_blend                              */
+#define FS4D_STAGE_BLEND_BWD 5    /* k_blend_bwd                          */
+#define FS4D_STAGE_PREPROCESS_BWD 6
+#define FS4D_STAGE_DEFORM_BWD 7
+#define FS4D_N_STAGES 8
+int fs4d_profile_enable(int on);
+int fs4d_profile_collect(double* ms_total, int64_t* calls, int32_t n_stages);
+
 /* ---- deformation ---- */
 /* Bytes of device scratch the deform calls need (packed weights + per-CTA
  * weight-gradient partials for the backward). */

@@ -256,19 +256,11 @@ def bin_tiles(proj, height, width, tile):
     a stable sort of (tile id) over rows emitted in depth order."""
     ntx, nty = -(-width // tile), -(-height // tile)
     tx0, tx1, ty0, ty1 = tile_rects(proj, height, width, tile)
-    rows, ids = [], []
-    for g in range(tx0.size):
-        tys = np.arange(ty0[g], ty1[g] + 1)
-        txs = np.arange(tx0[g], tx1[g] + 1)
-        tid = (tys[:, None] * ntx + txs[None, :]).ravel()
-        ids.append(tid)
-        rows.append(np.full(tid.size, g, dtype=np.int64))
-    if rows:
-        ids = np.concatenate(ids)
-        rows = np.concatenate(rows)
-    else:
-        ids = np.zeros(0, dtype=np.int64)
-        rows = np.zeros(0, dtype=np.int64)
+    span_x = tx1 - tx0 + 1
+    counts = span_x * (ty1 - ty0 + 1)
+    rows = np.repeat(np.arange(tx0.size, dtype=np.int64), counts)
+    local = np.arange(rows.size, dtype=np.int64) - np.repeat(np.cumsum(counts) - counts, counts)
+    ids = (ty0[rows] + local // span_x[rows]) * ntx + tx0[rows] + local % span_x[rows]
     perm = np.argsort(ids, kind="stable")
     ids, rows = ids[perm], rows[perm]
     bounds = np.searchsorted(ids, np.arange(ntx * nty + 1))
@@ -309,14 +301,18 @@ def transmittance(alpha, stop):
     return t_before, contrib, w, t_final
 
 
-def render(cloud, K, T, height, width, cfg, tile_rows=None):
+def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None):
     """Colour/depth/feature/alpha + per-pixel live-contributor counts.
 
     tile_rows: optional iterable of tile-row indices to composite (used by the
-    bounded CPU baseline); other pixels stay at background."""
-    proj = project(cloud, K, T, height, width, cfg)
+    bounded CPU baseline); other pixels stay at background.
+    prepared: optional (proj, lists) from project()/bin_tiles() to reuse."""
+    if prepared is None:
+        proj = project(cloud, K, T, height, width, cfg)
+        lists = bin_tiles(proj, height, width, cfg.tile)
+    else:
+        proj, lists = prepared
     tile = cfg.tile
-    lists = bin_tiles(proj, height, width, tile)
     n = proj["feature"].shape[1]
     color = np.zeros((height, width, 3))
     depth = np.zeros((height, width))
@@ -656,20 +652,26 @@ def deform_backward(cloud, planes, aabb, net, cache, grads, enable_grid=True,
 def projection_margins(proj, height, width, tile, cfg):
     """Relative distance of every discrete projection/binning decision of the
     *kept* Gaussians to its flip point: ceil argument vs integer, (u±r)/tile
-    vs integer, offscreen inequalities, depth gaps to depth neighbours."""
+    vs integer, offscreen inequalities, and the relative depth gap to the
+    depth-order neighbours (exact ties resolve by source index on both sides
+    and are not ambiguous).  The device evaluates these in fp64, so callers
+    compare them against an fp64-level threshold."""
     u, v, r = proj["mean2d"][:, 0], proj["mean2d"][:, 1], proj["radius"]
     src = proj["source_index"]
     pos_in_front = np.searchsorted(proj["front_index"], src)
     arg = proj["front_radius_arg"][pos_in_front]
-    frac = np.abs(arg - np.round(arg)) / np.maximum(np.abs(arg), 1.0)
-    m = frac
+    m = np.abs(arg - np.round(arg)) / np.maximum(np.abs(arg), 1.0)
     for e in ((u - r) / tile, (u + r) / tile, (v - r) / tile, (v + r) / tile):
         m = np.minimum(m, np.abs(e - np.round(e)) / np.maximum(np.abs(e), 1.0))
     for e in (u + r, (width - 1) - (u - r), v + r, (height - 1) - (v - r)):
         m = np.minimum(m, np.abs(e) / np.maximum(np.abs(u) + r + width, 1.0))
+    # pixel footprint bounds: |j - u| <= r decided per integer column/row
+    for e in (u - r, u + r, v - r, v + r):
+        m = np.minimum(m, np.abs(e - np.round(e)) / np.maximum(np.abs(e), 1.0))
     z = proj["view_depth"]
     if z.size > 1:
         gap = np.abs(np.diff(z)) / np.maximum(np.abs(z[1:]), 1e-12)
+        gap = np.where(gap == 0.0, np.inf, gap)
         gl = np.concatenate([[np.inf], gap])
         gr = np.concatenate([gap, [np.inf]])
         m = np.minimum(m, np.minimum(gl, gr))
@@ -677,8 +679,10 @@ def projection_margins(proj, height, width, tile, cfg):
 
 
 def pixel_decision_margins(out, cfg):
-    """Per pixel: the smallest relative margin of any alpha-skip, alpha-cap,
-    footprint, q-skip or stop decision met while compositing it."""
+    """Per pixel: the smallest relative margin of any fp32-evaluated blend
+    decision met while compositing it (alpha-skip, alpha-cap, q-skip, stop).
+    The square-footprint test is decided from fp64 integer bounds on device
+    and is covered by projection_margins."""
     proj = out["proj"]
     h, w = out["t_final"].shape
     margin = np.full((h, w), np.inf)
@@ -686,11 +690,8 @@ def pixel_decision_margins(out, cfg):
         alpha, g, a_raw, dx, dy, q, inside = tile_alpha(proj, rows, xs, ys, cfg)
         t_before, contrib, wts, t_final = transmittance(alpha, cfg.stop_transmittance)
         reach = t_before >= cfg.stop_transmittance * 0.5  # rows the traversal can see
-        r = proj["radius"][rows][:, None]
         mm = np.full(alpha.shape, np.inf)
-        near_fp = np.minimum(np.abs(np.abs(dx) - r), np.abs(np.abs(dy) - r)) / np.maximum(r, 1.0)
-        mm = np.minimum(mm, near_fp)
-        mm = np.minimum(mm, np.abs(q - Q_SKIP) / Q_SKIP)
+        mm = np.minimum(mm, np.where(inside | (q > Q_SKIP), np.abs(q - Q_SKIP) / Q_SKIP, np.inf))
         am = np.minimum(a_raw, cfg.alpha_cap)
         mm = np.minimum(mm, np.where(inside, np.abs(am - cfg.alpha_skip) / cfg.alpha_skip, np.inf))
         mm = np.minimum(mm, np.where(inside, np.abs(a_raw - cfg.alpha_cap) / cfg.alpha_cap, np.inf))

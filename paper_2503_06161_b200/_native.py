@@ -103,6 +103,9 @@ SIGNATURES = {
     "fs4d_last_error": (ctypes.c_char_p, []),
     "fs4d_build_info": (ctypes.c_char_p, []),
     "fs4d_status_reset": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "fs4d_profile_collect": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]),
     "fs4d_deform_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(DeformNet), ctypes.c_int64]),
     "fs4d_deform_fwd": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(HexPlane),
                                        ctypes.POINTER(DeformNet), ctypes.c_double,

@@ -2,6 +2,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <vector>
+
 #include "render_common.cuh"
 
 namespace fs4d {
@@ -19,6 +21,42 @@ int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FS4D_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return FS4D_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stage profiler: pairs of CUDA events per stage invocation
+// ---------------------------------------------------------------------------
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof_done;
+static ProfRec g_prof_open[FS4D_N_STAGES];
+static std::vector<cudaEvent_t> g_prof_pool;
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void profile_mark(int stage, bool begin, cudaStream_t s) {
+  if (!g_prof_on || stage < 0 || stage >= FS4D_N_STAGES) return;
+  if (begin) {
+    g_prof_open[stage].stage = stage;
+    g_prof_open[stage].a = prof_event();
+    cudaEventRecord(g_prof_open[stage].a, s);
+  } else {
+    g_prof_open[stage].b = prof_event();
+    cudaEventRecord(g_prof_open[stage].b, s);
+    g_prof_done.push_back(g_prof_open[stage]);
+  }
 }
 
 // defined in the kernel translation units
@@ -95,6 +133,31 @@ const char* fs4d_build_info(void) {
   snprintf(buf, sizeof(buf), "libfs4d abi=%d arch=sm_100a cuda=%d.%d", FS4D_ABI_VERSION, CUDART_VERSION / 1000,
            (CUDART_VERSION % 1000) / 10);
   return buf;
+}
+
+int fs4d_profile_enable(int on) {
+  g_prof_on = on != 0;
+  return FS4D_OK;
+}
+
+int fs4d_profile_collect(double* ms_total, int64_t* calls, int32_t n_stages) {
+  for (int i = 0; i < n_stages; ++i) {
+    if (ms_total) ms_total[i] = 0.0;
+    if (calls) calls[i] = 0;
+  }
+  for (const ProfRec& r : g_prof_done) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (r.stage < n_stages) {
+      if (ms_total) ms_total[r.stage] += ms;
+      if (calls) calls[r.stage] += 1;
+    }
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_done.clear();
+  return check_launch("profile_collect");
 }
 
 int fs4d_status_reset(int32_t* status, void* stream) {

@@ -17,6 +17,19 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int check_launch(const char* what);
 
+// optional stage timing (fs4d_profile_*): RAII bracket recording CUDA events
+void profile_mark(int stage, bool begin, cudaStream_t s);
+struct StageTimer {
+  int stage;
+  cudaStream_t s;
+  StageTimer(int st, cudaStream_t str) : stage(st), s(str) { profile_mark(stage, true, s); }
+  void stop() {
+    if (stage >= 0) profile_mark(stage, false, s);
+    stage = -1;
+  }
+  ~StageTimer() { stop(); }
+};
+
 // ---------------------------------------------------------------------------
 // device status block
 // ---------------------------------------------------------------------------

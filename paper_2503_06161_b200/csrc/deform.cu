@@ -47,7 +47,7 @@ struct FieldDesc {
   int res[FS4D_MAX_LEVELS][6][2];
   const float* planes[FS4D_MAX_LEVELS][6];
   float* gplanes[FS4D_MAX_LEVELS][6];
-  float lo[3], span[3];
+  double lo[3], span[3];
 };
 
 __constant__ int c_plane_axes[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};  // hexplane.py:16
@@ -143,7 +143,7 @@ __global__ void k_pack_weights(PackArgs a) {
 struct DefArgs {
   int64_t K;
   int TG;
-  float t;  // clipped time
+  double t;  // clipped time
   const float* pos;
   const float* rot;
   const float* ls;
@@ -240,13 +240,16 @@ __device__ __forceinline__ void dense_bwd_w(const LayerDesc& L, float* __restric
   }
 }
 
-// normalized coordinates (hexplane.py:84-92)
-__device__ __forceinline__ void norm_coords(const FieldDesc& f, const float* p, float t, float c[4], bool inside[3]) {
+// normalized coordinates (hexplane.py:84-92).  Evaluated in fp64 so the cell
+// choice (floor) and the strict `inside` test match the float64 reference; the
+// interpolation itself runs in fp32.
+__device__ __forceinline__ void norm_coords(const FieldDesc& f, const float* p, double t, double c[4],
+                                            bool inside[3]) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const float raw = (p[k] - f.lo[k]) / f.span[k];
-    inside[k] = raw > 0.f && raw < 1.f;
-    c[k] = fminf(fmaxf(raw, 0.f), 1.f);
+    const double raw = ((double)p[k] - f.lo[k]) / f.span[k];
+    inside[k] = raw > 0.0 && raw < 1.0;
+    c[k] = fmin(fmax(raw, 0.0), 1.0);
   }
   c[3] = t;
 }
@@ -258,21 +261,21 @@ struct Bilin {
 };
 
 // hexplane.py:95-110
-__device__ __forceinline__ Bilin bilinear_cell(int ra, int rb, int C, float ca, float cb) {
-  const float u = ca * (float)(ra - 1), v = cb * (float)(rb - 1);
-  int i0 = (int)floorf(u), j0 = (int)floorf(v);
+__device__ __forceinline__ Bilin bilinear_cell(int ra, int rb, int C, double ca, double cb) {
+  const double u = ca * (double)(ra - 1), v = cb * (double)(rb - 1);
+  int i0 = (int)floor(u), j0 = (int)floor(v);
   i0 = min(max(i0, 0), ra - 2);
   j0 = min(max(j0, 0), rb - 2);
   Bilin b;
   b.base = ((int64_t)i0 * rb + j0) * C;
   b.rowstride = rb * C;
-  b.fa = u - (float)i0;
-  b.fb = v - (float)j0;
+  b.fa = (float)(u - (double)i0);
+  b.fb = (float)(v - (double)j0);
   return b;
 }
 
 // Gather the latent of Gaussian g (one warp, lanes over channels) into lat[dim][TG].
-__device__ __forceinline__ void hexplane_gather(const FieldDesc& f, const float c[4], float* lat, int g, int TG,
+__device__ __forceinline__ void hexplane_gather(const FieldDesc& f, const double c[4], float* lat, int g, int TG,
                                                 int lane) {
   const int C = f.C;
   for (int l = 0; l < f.levels; ++l) {
@@ -382,7 +385,7 @@ __device__ void latent_tile(const DefArgs& a, const SmemPlan& sp, float* sm, int
   }
   for (int g = warp; g < TG; g += nw) {
     if (g < ng) {
-      float c[4];
+      double c[4];
       bool inside[3];
       norm_coords(a.field, a.pos + 3 * (g0 + g), a.t, c, inside);
       hexplane_gather(a.field, c, lat, g, TG, lane);
@@ -449,7 +452,7 @@ __device__ __forceinline__ float warp_transpose_reduce32(float (&v)[32], int lan
 __device__ void hexplane_backward_one(const DefArgs& a, const float* glat, int g, int TG, int64_t k, int lane) {
   const FieldDesc& f = a.field;
   const int C = f.C;
-  float c[4];
+  double c[4];
   bool inside[3];
   norm_coords(f, a.pos + 3 * k, a.t, c, inside);
   float dco[4] = {0.f, 0.f, 0.f, 0.f};
@@ -510,7 +513,7 @@ __device__ void hexplane_backward_one(const DefArgs& a, const float* glat, int g
     }
   }
   if (lane < 3) {
-    const float d = inside[lane] ? dco[lane] / f.span[lane] : 0.f;
+    const float d = inside[lane] ? (float)((double)dco[lane] / f.span[lane]) : 0.f;
     a.cg_pos[3 * k + lane] = a.g_pos[3 * k + lane] + d;
   }
 }
@@ -690,8 +693,8 @@ static int build_field_desc(const Fs4dHexPlane& h, const Fs4dDeformNet& n, Field
         return fail(FS4D_ERR_CONFIG, "plane resolutions must be >= 2");
     }
   for (int k = 0; k < 3; ++k) {
-    f.lo[k] = (float)h.aabb[k];
-    f.span[k] = (float)(h.aabb[3 + k] - h.aabb[k]);
+    f.lo[k] = h.aabb[k];
+    f.span[k] = h.aabb[3 + k] - h.aabb[k];
     if (n.enable_grid && !(h.aabb[3 + k] > h.aabb[k])) return fail(FS4D_ERR_CONFIG, "aabb must have hi > lo");
   }
   return FS4D_OK;
@@ -751,7 +754,7 @@ static int fill_args(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs
   const size_t need = deform_workspace_bytes(net, cloud.K, nullptr);
   if (!ws || ws_bytes < need) return fail(FS4D_ERR_CONFIG, "deform workspace too small");
   a.K = cloud.K;
-  a.t = (float)(t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t));  // hexplane.py:90
+  a.t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);  // hexplane.py:90
   a.pos = cloud.positions;
   a.rot = cloud.rotations;
   a.ls = cloud.log_scales;
@@ -777,6 +780,7 @@ int deform_forward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4d
   a.o_ls = snap.log_scales;
   a.o_op = snap.opacity_logits;
   a.o_feat = snap.features;
+  StageTimer st(FS4D_STAGE_DEFORM_FWD, s);
   pack_net(a.net, (float*)ws, s);
   cudaFuncSetAttribute(k_deform_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = ceil_div(cloud.K, a.TG);
@@ -808,6 +812,7 @@ int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4
                         (size_t)field.res[l][p][0] * field.res[l][p][1] * field.channels * 4, s);
       }
   }
+  StageTimer st(FS4D_STAGE_DEFORM_BWD, s);
   const int64_t ntiles = ceil_div(cloud.K, a.TG);
   const int grid = (int)(ntiles < kNumSMs * 2 ? (ntiles > 0 ? ntiles : 1) : kNumSMs * 2);
   cudaMemsetAsync(a.wpart, 0, (size_t)grid * a.net.packed_floats * 4, s);

@@ -437,7 +437,10 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   b.dA = up.d_alpha;
   b.accum = accum;
   int dc = D <= 0 ? 0 : D <= 4 ? 4 : D <= 8 ? 8 : D <= 16 ? 16 : D <= 32 ? 32 : 64;
-  if (L.ntiles > 0) launch_blend_bwd(dc, L.ntiles, b, s);
+  if (L.ntiles > 0) {
+    StageTimer st(FS4D_STAGE_BLEND_BWD, s);
+    launch_blend_bwd(dc, L.ntiles, b, s);
+  }
 
   PreBwdArgs p;
   p.c = snap;
@@ -461,7 +464,10 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   p.clamp_mask = at<uint32_t>(ws, L.clamp_mask);
   p.vs_index = vs_index;
   p.vs_norm = vs_norm;
-  if (K > 0) k_preprocess_bwd<<<(unsigned)ceil_div(K, 128), 128, 0, s>>>(p);
+  if (K > 0) {
+    StageTimer st(FS4D_STAGE_PREPROCESS_BWD, s);
+    k_preprocess_bwd<<<(unsigned)ceil_div(K, 128), 128, 0, s>>>(p);
+  }
   return check_launch("render_bwd");
 }
 

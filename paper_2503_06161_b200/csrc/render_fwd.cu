@@ -9,6 +9,7 @@
 //                                          rasterizer.py:215-261, 284-303
 #include "render_common.cuh"
 #include "sh.cuh"
+#include <new>
 
 namespace fs4d {
 
@@ -472,15 +473,23 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   p.clamp_mask = at<uint32_t>(ws, L.clamp_mask);
   p.counters = counters;
   p.status = status;
-  if (K > 0) k_preprocess<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(p);
+  {
+    StageTimer st(FS4D_STAGE_PREPROCESS, s);
+    if (K > 0) k_preprocess<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(p);
+  }
 
   // stable global depth order (culled rows carry key 0xFFFFFFFF and sort last)
   uint32_t* dk[2] = {at<uint32_t>(ws, L.dkeys0), at<uint32_t>(ws, L.dkeys1)};
   uint32_t* dv[2] = {at<uint32_t>(ws, L.dvals0), at<uint32_t>(ws, L.dvals1)};
   void* scratch = at<void>(ws, L.scratch);
-  int df = radix_sort_pairs(dk, dv, K, nullptr, 0, 32, scratch, s);
-  if (K > 0) k_depth_tie_fixup<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dk[df], dv[df], p.z64, K, counters);
+  int df;
+  {
+    StageTimer st(FS4D_STAGE_DEPTH_SORT, s);
+    df = radix_sort_pairs(dk, dv, K, nullptr, 0, 32, scratch, s);
+    if (K > 0) k_depth_tie_fixup<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dk[df], dv[df], p.z64, K, counters);
+  }
   const uint32_t* order = dv[df];
+  StageTimer st_bin(FS4D_STAGE_BINNING, s);
 
   // tile binning: count -> scan -> emit -> stable sort by tile -> ranges
   uint32_t* tcount = at<uint32_t>(ws, L.tcount);
@@ -498,6 +507,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   int pf = radix_sort_pairs(pk, pv, L.cap, counters + CNT_PAIRS_CLAMPED, 0, L.tile_bits, scratch, s);
   if (L.cap > 0)
     k_tile_ranges<<<(unsigned)ceil_div(L.cap, 256), 256, 0, s>>>(pk[pf], counters, at<uint2>(ws, L.ranges));
+  st_bin.stop();
 
   // blend
   BlendArgs b;
@@ -526,6 +536,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   b.tfinal = at<float>(ws, L.tfinal);
   b.last = at<int32_t>(ws, L.last);
   if (L.ntiles > 0) {
+    StageTimer st(FS4D_STAGE_BLEND, s);
     int c0 = 0;
     do {
       int rem = b.D - c0;

@@ -104,7 +104,8 @@ def deform_with_cache(cloud, field, net, t):
         log_scales=_host(snap.log_scales).reshape(k, 3),
         opacity_logits=_host(snap.opacity_logits).reshape(k),
         colors_raw=cloud.colors_raw,
-        features=_host(snap.features).reshape(k, -1) if net.cfg.enable_feature_update
+        features=_host(snap.features).reshape(k, np.shape(cloud.features)[1])
+        if net.cfg.enable_feature_update
         else cloud.features,
         sh_rest=getattr(cloud, "sh_rest", None),
     )

@@ -72,13 +72,14 @@ class DeviceCloud:
     def from_cloud(cls, cloud, device="cuda"):
         sh = getattr(cloud, "sh_rest", None)
         k = len(cloud)
+        d = int(np.shape(cloud.features)[1]) if np.ndim(cloud.features) == 2 else 0
         return cls(_dev(cloud.positions, device).reshape(k, 3),
                    _dev(cloud.rotations, device).reshape(k, 4),
                    _dev(cloud.log_scales, device).reshape(k, 3),
                    _dev(cloud.opacity_logits, device).reshape(k),
                    _dev(cloud.colors_raw, device).reshape(k, 3),
-                   _dev(cloud.features, device).reshape(k, -1),
-                   None if sh is None else _dev(sh, device).reshape(k, -1, 3))
+                   _dev(cloud.features, device).reshape(k, d),
+                   None if sh is None else _dev(sh, device).reshape(k, np.shape(sh)[1], 3))
 
     @classmethod
     def empty(cls, k, d, sh_degree=0, device="cuda"):
@@ -425,3 +426,65 @@ class Renderer:
         N.check(N.load().fs4d_render_export_tiles(ctypes.byref(rec.info), _p(rec.ws), rec.ws.numel(),
                                                   _p(ranges), _p(rows), npairs, _stream()))
         return ranges, rows[:npairs]
+
+
+STAGES = ("deform_fwd", "preprocess", "depth_sort", "binning", "blend", "blend_bwd",
+          "preprocess_bwd", "deform_bwd")
+
+
+def profile_enable(on=True):
+    N.load().fs4d_profile_enable(int(bool(on)))
+
+
+def profile_collect():
+    """{stage: (total_ms, calls)} for the stages recorded since the last collect."""
+    n = len(STAGES)
+    ms = (ctypes.c_double * n)()
+    calls = (ctypes.c_int64 * n)()
+    N.check(N.load().fs4d_profile_collect(ms, calls, n))
+    return {STAGES[i]: (ms[i], int(calls[i])) for i in range(n)}
+
+
+class FramePipeline:
+    """One deformed + rendered frame per call, the cli.render_frame path
+    (cli.py:58-61: model_snapshot -> render) with device-resident buffers.
+
+    run(t, K, T)                       everything already in HBM
+    run(t, K, T, host_in=..., host_out=...)  end-to-end: H2D of the canonical
+        cloud from pinned host memory, deform + render, D2H of the images.
+    """
+
+    def __init__(self, cloud, field, net, height, width, cfg, device="cuda"):
+        self.cloud, self.field, self.net = cloud, field, net
+        self.h, self.w, self.cfg = int(height), int(width), cfg
+        self.deformer = DeformEngine(device)
+        self.renderer = Renderer(device)
+        k, d = len(cloud), cloud.feature_dim
+        self.snap = DeviceCloud.empty(k, d, 0, device)
+        self.images = self.renderer.alloc_images(self.h, self.w, d if cfg.with_features else 0)
+
+    def pinned_host_buffers(self):
+        """Pinned host copies of the canonical cloud and the output images."""
+        host_in = {n: getattr(self.cloud, n).cpu().pin_memory() for n in DeviceCloud.FIELDS}
+        if self.cloud.sh_rest is not None:
+            host_in["sh_rest"] = self.cloud.sh_rest.cpu().pin_memory()
+        host_out = {n: torch.empty(t.shape, dtype=t.dtype).pin_memory() for n, t in self.images.items()}
+        return host_in, host_out
+
+    def h2d_bytes(self, host_in):
+        return sum(t.numel() * t.element_size() for t in host_in.values())
+
+    def d2h_bytes(self):
+        return sum(t.numel() * t.element_size() for n, t in self.images.items() if n != "n_contrib")
+
+    def run(self, t, K, T, host_in=None, host_out=None, check=False):
+        if host_in is not None:
+            for n, src in host_in.items():
+                getattr(self.cloud, n).copy_(src, non_blocking=True)
+        self.deformer.forward(self.cloud, self.field, self.net, t, out=self.snap)
+        self.renderer.forward(self.snap, K, T, self.h, self.w, self.cfg, images=self.images, check=check)
+        if host_out is not None:
+            for n, dst in host_out.items():
+                if n != "n_contrib":
+                    dst.copy_(self.images[n], non_blocking=True)
+        return self.images

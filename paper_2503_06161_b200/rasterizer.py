@@ -259,7 +259,7 @@ def render_backward(snapshot, frame, out, dL_dcolor=None, dL_ddepth=None, dL_dfe
         log_scales=_host(grads.log_scales).reshape(k, 3),
         opacity_logits=_host(grads.opacity_logits).reshape(k),
         colors_raw=_host(grads.colors_raw).reshape(k, 3),
-        features=_host(grads.features).reshape(k, -1),
+        features=_host(grads.features).reshape(k, np.shape(snapshot.features)[1]),
         viewspace_index=vs_index[:m].cpu().numpy().astype(np.int64),
         viewspace_norm=_host(vs_norm[:m]),
         sh_rest=None if sh is None else _host(grads.sh_rest).reshape(np.shape(sh)),

@@ -19,7 +19,8 @@ from oracle import fs4d_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-TAU = 1e-5          # relative margin below which a discrete decision is "ambiguous"
+TAU = 1e-5          # relative margin below which an fp32 blend decision is "ambiguous"
+TAU64 = 1e-9        # same for projection/binning decisions (evaluated in fp64 on device)
 ATOL_IMG = 1e-4     # colour / depth / feature / alpha max-abs (fp32 vs fp64 reference)
 ATOL_GRAD = 1e-4    # gradients: max-abs <= ATOL_GRAD * max(1, max|ref|)
 
@@ -54,12 +55,12 @@ def ambiguous_pixels(oracle_out, cfg, h, w):
     amb = O.pixel_decision_margins(oracle_out, cfg) < TAU
     proj = oracle_out["proj"]
     pm = O.projection_margins(proj, h, w, cfg.tile, cfg)
-    for g in np.flatnonzero(pm < TAU):
+    for g in np.flatnonzero(pm < TAU64):
         u, v, r = proj["mean2d"][g, 0], proj["mean2d"][g, 1], proj["radius"][g]
         x0, x1 = int(max(0, np.floor(u - r - 1))), int(min(w - 1, np.ceil(u + r + 1)))
         y0, y1 = int(max(0, np.floor(v - r - 1))), int(min(h - 1, np.ceil(v + r + 1)))
         amb[y0:y1 + 1, x0:x1 + 1] = True
-    return amb, pm < TAU
+    return amb, pm < TAU64
 
 
 def compare_render(out, ref_imgs, amb, n_contrib_ref):
