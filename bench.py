@@ -116,6 +116,18 @@ class ClockSampler:
         self.th = None
 
     def __enter__(self):
+        self.stop = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.th = threading.Thread(target=self._poll, daemon=True)
+            self.th.start()
+            return self
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
@@ -134,7 +146,24 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
+    def _poll(self):
+        nv = self.nv
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                "sw_power_cap": 0x4}
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                act = ["active" if rs & b else "not active" for b in bits.values()]
+                self.rows.append([str(sm), str(self.max_mhz), hex(rs)] + act)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def __exit__(self, *a):
+        self.stop = True
+        if self.th is not None and self.nv is not None:
+            self.th.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:

@@ -477,12 +477,54 @@ class FramePipeline:
     def d2h_bytes(self):
         return sum(t.numel() * t.element_size() for n, t in self.images.items() if n != "n_contrib")
 
+    def _bind(self):
+        """Build every ctypes argument once; steady-state frames then cost two
+        ABI calls (+ a status reset) of host time."""
+        lib = N.load()
+        self.snap.colors_raw = self.cloud.colors_raw
+        self.snap.sh_rest = self.cloud.sh_rest
+        if not self.net.enable_feature_update:
+            self.snap.features = self.cloud.features
+        c = dict(cloud=self.cloud.struct(), field=self.field.struct(), net=self.net.struct(),
+                 snap=self.snap.struct(), raster=raster_struct(self.cfg), imgs=N.Images())
+        ws = self.deformer._workspace(c["net"], len(self.cloud))
+        c["dws"], c["dws_n"] = ws.data_ptr(), ws.numel()
+        im = self.images
+        c["imgs"].color, c["imgs"].depth, c["imgs"].alpha = (im["color"].data_ptr(), im["depth"].data_ptr(),
+                                                             im["alpha"].data_ptr())
+        c["imgs"].feature = im["feature"].data_ptr() if im["feature"].numel() else None
+        c["imgs"].n_contrib = im["n_contrib"].data_ptr()
+        k, d, sh = len(self.snap), self.snap.feature_dim, self.snap.sh_degree
+        c["info"] = self.renderer._prepare(k, self.h, self.w, d, sh, self.cfg.tile)
+        c["rws"], c["rws_n"] = self.renderer.ws.data_ptr(), self.renderer.ws.numel()
+        c["status"] = self.renderer.status.t.data_ptr()
+        c["cap"] = self.renderer.cap
+        c["cam_key"] = None
+        self._c = c
+        self._lib = lib
+
     def run(self, t, K, T, host_in=None, host_out=None, check=False):
         if host_in is not None:
             for n, src in host_in.items():
                 getattr(self.cloud, n).copy_(src, non_blocking=True)
-        self.deformer.forward(self.cloud, self.field, self.net, t, out=self.snap)
-        self.renderer.forward(self.snap, K, T, self.h, self.w, self.cfg, images=self.images, check=check)
+        c = getattr(self, "_c", None)
+        if check or c is None or c["cap"] != self.renderer.cap:
+            # checked path: sizes / grows the pair buffer, raises device errors
+            self.deformer.forward(self.cloud, self.field, self.net, t, out=self.snap)
+            self.renderer.forward(self.snap, K, T, self.h, self.w, self.cfg, images=self.images, check=check)
+            self._bind()
+        else:
+            lib, s = self._lib, _stream()
+            key = (np.asarray(K, dtype=np.float64).tobytes(), np.asarray(T, dtype=np.float64).tobytes())
+            if key != c["cam_key"]:
+                c["cam"] = camera_struct(K, T, self.h, self.w)
+                c["cam_key"] = key
+            N.check(lib.fs4d_deform_fwd(ctypes.byref(c["cloud"]), ctypes.byref(c["field"]), ctypes.byref(c["net"]),
+                                        float(t), ctypes.byref(c["snap"]), c["dws"], c["dws_n"], None, s))
+            N.check(lib.fs4d_status_reset(c["status"], s))
+            N.check(lib.fs4d_render_fwd(ctypes.byref(c["snap"]), ctypes.byref(c["cam"]), ctypes.byref(c["raster"]),
+                                        ctypes.byref(c["info"]), c["rws"], c["rws_n"], ctypes.byref(c["imgs"]),
+                                        c["status"], s))
         if host_out is not None:
             for n, dst in host_out.items():
                 if n != "n_contrib":
