@@ -18,6 +18,7 @@
 // (reduced by a final kernel — deterministic, no atomics on weights), and
 // scatters plane gradients with coalesced red.global.add per corner.
 #include "common.cuh"
+#include <stdlib.h>
 #include <string.h>
 
 namespace fs4d {
@@ -431,149 +432,6 @@ __global__ void __launch_bounds__(kDefThreads) k_deform_fwd(DefArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// fast forward for the headline shape: width 64, latent 64 (2 levels x 32 ch),
-// feature dim DP <= 32.  One thread owns one Gaussian and keeps every
-// activation in registers; the whole packed weight blob (87 KB) is staged in
-// shared memory once per persistent CTA and read as warp-uniform float4
-// broadcasts (outer-product form: one LDS.128 feeds 4 independent FFMAs).
-// ---------------------------------------------------------------------------
-constexpr int kFastThreads = 256;
-
-template <int NIN, int NOUT, bool RELU>
-__device__ __forceinline__ void dense_regs(const float* __restrict__ Wt, const float* __restrict__ bias,
-                                           const float (&x)[NIN], float (&y)[NOUT]) {
-  // Wt: [NIN][NOUT] (NOUT multiple of 4, 16-byte aligned)
-#pragma unroll
-  for (int o = 0; o < NOUT; o += 4) {
-    const float4 b = *reinterpret_cast<const float4*>(bias + o);
-    y[o] = b.x;
-    y[o + 1] = b.y;
-    y[o + 2] = b.z;
-    y[o + 3] = b.w;
-  }
-#pragma unroll
-  for (int i = 0; i < NIN; ++i) {
-    const float xi = x[i];
-#pragma unroll
-    for (int o = 0; o < NOUT; o += 4) {
-      const float4 w = *reinterpret_cast<const float4*>(Wt + i * NOUT + o);
-      y[o] = fmaf(w.x, xi, y[o]);
-      y[o + 1] = fmaf(w.y, xi, y[o + 1]);
-      y[o + 2] = fmaf(w.z, xi, y[o + 2]);
-      y[o + 3] = fmaf(w.w, xi, y[o + 3]);
-    }
-  }
-  if (RELU) {
-#pragma unroll
-    for (int o = 0; o < NOUT; ++o) y[o] = fmaxf(y[o], 0.f);
-  }
-}
-
-template <int DP>
-__global__ void __launch_bounds__(kFastThreads, 1) k_deform_fwd_w64(DefArgs a) {
-  extern __shared__ __align__(16) float sm[];
-  const NetDesc& n = a.net;
-  float* wsm = sm;                                            // packed weights
-  float* lat = sm + ((n.packed_floats + 3) & ~3ll);           // [64][kFastThreads]
-  for (int64_t e = threadIdx.x; e < n.packed_floats / 4; e += blockDim.x)
-    reinterpret_cast<float4*>(wsm)[e] = __ldg(reinterpret_cast<const float4*>(a.blob) + e);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ntiles = ceil_div(a.K, kFastThreads);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t g0 = tile * kFastThreads;
-    __syncthreads();  // weights staged / previous tile's latent consumed
-    // HexPlane gather: warp w fills Gaussians [32w, 32w+32) of the tile
-    for (int j = 0; j < 32; ++j) {
-      const int g = warp * 32 + j;
-      const int64_t k = g0 + g;
-      if (k < a.K && n.enable_grid) {
-        double c[4];
-        bool inside[3];
-        norm_coords(a.field, a.pos + 3 * k, a.t, c, inside);
-        hexplane_gather(a.field, c, lat, g, kFastThreads, lane);
-      } else {
-        lat[lane * kFastThreads + g] = 0.f;
-        lat[(32 + lane) * kFastThreads + g] = 0.f;
-      }
-    }
-    __syncthreads();
-    const int64_t k = g0 + threadIdx.x;
-    float x[64], h[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) x[i] = lat[i * kFastThreads + threadIdx.x];
-    for (int l = 0; l < n.depth; ++l) {
-      const LayerDesc& L = n.layers[n.trunk0 + l];
-      dense_regs<64, 64, true>(wsm + L.off_w, wsm + L.off_b, x, h);
-#pragma unroll
-      for (int i = 0; i < 64; ++i) x[i] = h[i];
-    }
-    float ff[32];
-    {
-      const LayerDesc& F0 = n.layers[n.feat0];
-#pragma unroll
-      for (int o = 0; o < 32; ++o) ff[o] = wsm[F0.off_b + o];
-    }
-    const int hoff[4] = {0, 3, 7, 10};
-    float delta[12];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      float e1[32], e2[32];
-      const LayerDesc& E0 = n.layers[n.ext0 + 2 * b];
-      const LayerDesc& E1 = n.layers[n.ext0 + 2 * b + 1];
-      const LayerDesc& HD = n.layers[n.head0 + b];
-      dense_regs<64, 32, true>(wsm + E0.off_w, wsm + E0.off_b, x, e1);
-      dense_regs<32, 32, true>(wsm + E1.off_w, wsm + E1.off_b, e1, e2);
-      float d4[4];
-      dense_regs<32, 4, false>(wsm + HD.off_w, wsm + HD.off_b, e2, d4);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (hoff[b] + q < 11 && q < (b == 1 ? 4 : (b == 3 ? 1 : 3))) delta[hoff[b] + q] = d4[q];
-      // F_feat first layer consumes the concat slice of this branch (deformation.py:119-120)
-      const LayerDesc& F0 = n.layers[n.feat0];
-      const float* Wf = wsm + F0.off_w + b * 32 * 32;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float xi = e2[i];
-#pragma unroll
-        for (int o = 0; o < 32; o += 4) {
-          const float4 w = *reinterpret_cast<const float4*>(Wf + i * 32 + o);
-          ff[o] = fmaf(w.x, xi, ff[o]);
-          ff[o + 1] = fmaf(w.y, xi, ff[o + 1]);
-          ff[o + 2] = fmaf(w.z, xi, ff[o + 2]);
-          ff[o + 3] = fmaf(w.w, xi, ff[o + 3]);
-        }
-      }
-    }
-    if (k < a.K) {
-#pragma unroll
-      for (int q = 0; q < 3; ++q) a.o_pos[3 * k + q] = a.pos[3 * k + q] + delta[q];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) a.o_rot[4 * k + q] = a.rot[4 * k + q] + delta[3 + q];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) a.o_ls[3 * k + q] = a.ls[3 * k + q] + delta[7 + q];
-      a.o_op[k] = a.op[k] + delta[10];
-    }
-    if (n.enable_feat) {
-#pragma unroll
-      for (int o = 0; o < 32; ++o) ff[o] = fmaxf(ff[o], 0.f);
-      const LayerDesc& F1 = n.layers[n.feat0 + 1];
-      float dz[DP];
-      dense_regs<32, DP, false>(wsm + F1.off_w, wsm + F1.off_b, ff, dz);
-      if (k < a.K) {
-#pragma unroll
-        for (int c = 0; c < DP; ++c)
-          if (c < n.D) a.o_feat[(int64_t)n.D * k + c] = a.feat[(int64_t)n.D * k + c] + dz[c];
-      }
-    }
-  }
-}
-
-static bool fast_fwd_ok(const NetDesc& d, const FieldDesc& f) {
-  return d.width == 64 && d.L == 64 && (d.D == 4 || d.D == 8 || d.D == 16 || d.D == 32) &&
-         (!d.enable_grid || (f.levels == 2 && f.C == 32));
-}
-
-// ---------------------------------------------------------------------------
 // backward
 // ---------------------------------------------------------------------------
 // Reduce v[0..31] over the warp; afterwards lane L holds the warp sum of v[L].
@@ -866,13 +724,20 @@ static int pick_tg(const NetDesc& n, bool backward, size_t* smem_bytes) {
 
 static size_t blob_bytes(const NetDesc& d) { return align_up_sz((size_t)d.packed_floats * 4, 256); }
 
+bool tc_path_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f);
+size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K);
+int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
+                      Fs4dCloud& snap, void* ws, cudaStream_t s);
+
 size_t deform_workspace_bytes(const Fs4dDeformNet& net, int64_t K, int* nparts_out) {
   NetDesc d;
   if (build_net_desc(net, d) != FS4D_OK) return 0;
   int nparts = kNumSMs * 2;
   if (nparts_out) *nparts_out = nparts;
   (void)K;
-  return blob_bytes(d) + (size_t)nparts * d.packed_floats * 4 + 256;
+  const size_t generic = blob_bytes(d) + (size_t)nparts * d.packed_floats * 4 + 256;
+  const size_t tc = tc_workspace_bytes(net, K);
+  return generic > tc ? generic : tc;
 }
 
 
@@ -924,19 +789,8 @@ int deform_forward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4d
   a.o_op = snap.opacity_logits;
   a.o_feat = snap.features;
   StageTimer st(FS4D_STAGE_DEFORM_FWD, s);
+  if (tc_path_ok(net, field) && !getenv("FS4D_NO_TC")) return deform_forward_tc(cloud, field, net, t, snap, ws, s);
   pack_net(a.net, (float*)ws, s);
-  if (fast_fwd_ok(a.net, a.field)) {
-    const size_t fsmem = (size_t)(((a.net.packed_floats + 3) & ~3ll) + 64 * kFastThreads) * 4;
-    const int64_t nt = ceil_div(cloud.K, kFastThreads);
-    const int fgrid = (int)(nt < kNumSMs ? nt : kNumSMs);
-    const int dp = a.net.D <= 4 ? 4 : a.net.D <= 8 ? 8 : a.net.D <= 16 ? 16 : 32;
-#define FS4D_FAST(DPV)                                                                              \
-  cudaFuncSetAttribute(k_deform_fwd_w64<DPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem); \
-  k_deform_fwd_w64<DPV><<<fgrid, kFastThreads, fsmem, s>>>(a);
-    if (dp == 4) { FS4D_FAST(4) } else if (dp == 8) { FS4D_FAST(8) } else if (dp == 16) { FS4D_FAST(16) } else { FS4D_FAST(32) }
-#undef FS4D_FAST
-    return check_launch("deform_fwd_w64");
-  }
   cudaFuncSetAttribute(k_deform_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = ceil_div(cloud.K, a.TG);
   const int grid = (int)(ntiles < kNumSMs * 2 ? ntiles : kNumSMs * 2);

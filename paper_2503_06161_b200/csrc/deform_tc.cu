@@ -1,0 +1,600 @@
+// Deformation forward, fast path:  HexPlane gather kernel + tcgen05 MLP kernel.
+//
+//   k_hexplane_latent  hexplane.query_with_cache (hexplane.py:118-142): one
+//                      warp per 32 Gaussians; lanes first compute their own
+//                      Gaussian's 6*levels bilinear cells in fp64 (once, into
+//                      shared memory), then sweep the 32 Gaussians with lane =
+//                      channel so every corner fetch is a coalesced 128 B row.
+//   k_mlp_tc           every MLP stack of deformation.py:105-136 for a tile of
+//                      128 Gaussians on the 5th-gen tensor cores: operands in
+//                      shared memory (K-major, no-swizzle core-matrix layout),
+//                      fp32 accumulators in TMEM (tcgen05.mma kind::f16,
+//                      M=128), 3-term bf16 split (hi*hi + hi*lo + lo*hi, rel.
+//                      error ~1e-5) so fp32 parity holds; the epilogue of each
+//                      layer (tcgen05.ld -> bias -> ReLU -> split -> st.shared)
+//                      produces the next layer's A operand in place, and the
+//                      last epilogues add the raw-space deltas straight into
+//                      the snapshot (deformation.py:126-133).
+#include <cuda_bf16.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace fs4d {
+
+// ---------------------------------------------------------------------------
+// shared declarations with deform.cu
+// ---------------------------------------------------------------------------
+struct TcPlan {
+  int depth, D, DP, enable_feat, enable_grid;
+  int levels, C, L;
+  int res[FS4D_MAX_LEVELS][6][2];
+  const float* planes[FS4D_MAX_LEVELS][6];
+  double lo[3], span[3];
+  double t;
+  // packed blob offsets (bytes)
+  int off_trunk[FS4D_MAX_TRUNK], off_ext0, off_ext1[4], off_head[4], off_f1, off_f2;
+  int off_b_trunk[FS4D_MAX_TRUNK], off_b_ext0, off_b_ext1, off_b_head, off_b_f1, off_b_f2;
+  int blob_bytes;
+};
+
+constexpr int kTcRows = 128;       // M tile (TMEM lanes)
+constexpr int kTcThreads = 128;    // one thread per row
+constexpr int kTmemCols = 256;
+
+__constant__ int c_axes_tc[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};  // hexplane.py:16
+
+// ---------------------------------------------------------------------------
+// HexPlane latent
+// ---------------------------------------------------------------------------
+constexpr int kGatherWarps = 4;
+constexpr int kGatherMaxLevels = 4;
+
+__global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent(TcPlan p, int64_t K, const float* __restrict__ pos,
+                                                                         float* __restrict__ latent) {
+  __shared__ int s_base[kGatherWarps][kGatherMaxLevels * 6][32];
+  __shared__ float s_fa[kGatherWarps][kGatherMaxLevels * 6][32];
+  __shared__ float s_fb[kGatherWarps][kGatherMaxLevels * 6][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g0 = ((int64_t)blockIdx.x * kGatherWarps + warp) * 32;
+  if (g0 >= K) return;
+  const int L = p.L;
+  if (!p.enable_grid) {
+    for (int j = 0; j < 32 && g0 + j < K; ++j)
+      for (int c = lane; c < L; c += 32) latent[(g0 + j) * L + c] = 0.f;
+    return;
+  }
+  // lane j: bilinear cells of Gaussian g0 + j (fp64 coordinates, hexplane.py:84-110)
+  {
+    const int64_t k = g0 + lane;
+    double c[4] = {0.0, 0.0, 0.0, p.t};
+    if (k < K) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double raw = ((double)pos[3 * k + a] - p.lo[a]) / p.span[a];
+        c[a] = fmin(fmax(raw, 0.0), 1.0);
+      }
+    }
+    for (int l = 0; l < p.levels; ++l)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int ra = p.res[l][q][0], rb = p.res[l][q][1];
+        const double u = c[c_axes_tc[q][0]] * (ra - 1), v = c[c_axes_tc[q][1]] * (rb - 1);
+        int i0 = (int)floor(u), j0 = (int)floor(v);
+        i0 = min(max(i0, 0), ra - 2);
+        j0 = min(max(j0, 0), rb - 2);
+        s_base[warp][l * 6 + q][lane] = (i0 * rb + j0) * p.C;
+        s_fa[warp][l * 6 + q][lane] = (float)(u - i0);
+        s_fb[warp][l * 6 + q][lane] = (float)(v - j0);
+      }
+  }
+  __syncwarp();
+  const int C = p.C;
+  for (int j = 0; j < 32; ++j) {
+    const int64_t k = g0 + j;
+    if (k >= K) break;
+    for (int l = 0; l < p.levels; ++l) {
+      for (int ch = lane; ch < C; ch += 32) {
+        float prod = 1.f;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int rb = p.res[l][q][1];
+          const float* pl = p.planes[l][q] + s_base[warp][l * 6 + q][j] + ch;
+          const float fa = s_fa[warp][l * 6 + q][j], fb = s_fb[warp][l * 6 + q][j];
+          const float p00 = __ldg(pl), p01 = __ldg(pl + C);
+          const float p10 = __ldg(pl + rb * C), p11 = __ldg(pl + rb * C + C);
+          prod *= (1.f - fa) * (1.f - fb) * p00 + fa * (1.f - fb) * p10 + (1.f - fa) * fb * p01 + fa * fb * p11;
+        }
+        latent[k * L + l * C + ch] = prod;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// weight packing: fp32 [out,in] -> bf16 hi/lo K-major core-matrix operands
+// ---------------------------------------------------------------------------
+// Byte offset of element (r, k) in an operand block with KT columns:
+//   8-row x 16-byte core matrices; K chunks of 8 elements 128 B apart (LBO),
+//   8-row groups KT*16 B apart (SBO).
+__host__ __device__ inline int core_off(int r, int k, int KT) {
+  return (r >> 3) * (KT * 16) + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
+}
+
+struct TcSrc {
+  const float* w;  // [rows, in] row-major
+  int rows, in, row0;
+};
+struct TcOperand {
+  int N, KT, off, nsrc;
+  TcSrc src[4];
+};
+struct TcBias {
+  int n, off, nsrc;
+  const float* b[4];
+  int len[4], at[4];
+};
+struct TcPackArgs {
+  TcOperand op[FS4D_MAX_TRUNK + 12];
+  int nop;
+  TcBias bias[FS4D_MAX_TRUNK + 8];
+  int nbias;
+  uint8_t* blob;
+};
+
+__global__ void k_pack_tc(TcPackArgs a) {
+  const int o = blockIdx.y;
+  if (o < a.nop) {
+    const TcOperand& op = a.op[o];
+    __nv_bfloat16* hi = reinterpret_cast<__nv_bfloat16*>(a.blob + op.off);
+    __nv_bfloat16* lo = reinterpret_cast<__nv_bfloat16*>(a.blob + op.off + op.N * op.KT * 2);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < op.N * op.KT; e += gridDim.x * blockDim.x) {
+      const int r = e / op.KT, k = e % op.KT;
+      float v = 0.f;
+      for (int s = 0; s < op.nsrc; ++s) {
+        const TcSrc& S = op.src[s];
+        if (r >= S.row0 && r < S.row0 + S.rows && k < S.in) v = S.w[(r - S.row0) * S.in + k];
+      }
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+      const int off = core_off(r, k, op.KT) / 2;
+      hi[off] = h;
+      lo[off] = l;
+    }
+  } else {
+    const TcBias& b = a.bias[o - a.nop];
+    float* dst = reinterpret_cast<float*>(a.blob + b.off);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < b.n; e += gridDim.x * blockDim.x) {
+      float v = 0.f;
+      for (int s = 0; s < b.nsrc; ++s)
+        if (e >= b.at[s] && e < b.at[s] + b.len[s]) v = b.b[s][e - b.at[s]];
+      dst[e] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// K-major SWIZZLE_NONE shared-memory matrix descriptor (sm_100 version bit 46)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major, M = 128
+__device__ __forceinline__ uint32_t idesc_bf16(int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// A[M=128][KT] (hi block then lo block at +128*KT*2 bytes) times B[N][KT]
+// (hi, lo) into TMEM columns [col, col+N): hi*hi + hi*lo + lo*hi, K steps of 16.
+__device__ __forceinline__ void gemm_bf16x3(uint32_t tmem_d, uint32_t a_base, int a_kt, int a_k0, uint32_t b_base,
+                                            int b_kt, int N, int ksteps) {
+  const uint32_t id = idesc_bf16(N);
+  const uint32_t a_lo = a_base + kTcRows * a_kt * 2, b_lo = b_base + N * b_kt * 2;
+  const uint32_t a_sbo = a_kt * 16, b_sbo = b_kt * 16;
+#pragma unroll 1
+  for (int s = 0; s < ksteps; ++s) {
+    const uint32_t ak = (uint32_t)(((a_k0 >> 3) + 2 * s) * 128), bk = (uint32_t)(s * 256);
+    const uint64_t ah = sdesc(a_base + ak, 128, a_sbo), al = sdesc(a_lo + ak, 128, a_sbo);
+    const uint64_t bh = sdesc(b_base + bk, 128, b_sbo), bl = sdesc(b_lo + bk, 128, b_sbo);
+    mma_bf16(tmem_d, ah, bh, id, s > 0 ? 1u : 0u);
+    mma_bf16(tmem_d, ah, bl, id, 1u);
+    mma_bf16(tmem_d, al, bh, id, 1u);
+  }
+}
+
+// store 8 consecutive values (k0..k0+7) of row r into an A operand (hi, lo) with KT columns
+__device__ __forceinline__ void store_split8(uint8_t* a_base, int KT, int r, int k0, const float* v) {
+  __nv_bfloat16 h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    h[i] = __float2bfloat16_rn(v[i]);
+    l[i] = __float2bfloat16_rn(v[i] - __bfloat162float(h[i]));
+  }
+  const int off = core_off(r, k0, KT);
+  *reinterpret_cast<uint4*>(a_base + off) = *reinterpret_cast<const uint4*>(h);
+  *reinterpret_cast<uint4*>(a_base + kTcRows * KT * 2 + off) = *reinterpret_cast<const uint4*>(l);
+}
+
+struct TcArgs {
+  TcPlan p;
+  int64_t K;
+  const float* latent;
+  const uint8_t* blob;
+  const float* pos;
+  const float* rot;
+  const float* ls;
+  const float* op;
+  const float* feat;
+  float* o_pos;
+  float* o_rot;
+  float* o_ls;
+  float* o_op;
+  float* o_feat;
+};
+
+// one accumulator region [col, col+n) -> bias -> (relu) -> split -> A operand columns [k0, k0+n)
+__device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, int n, const float* bias, bool relu,
+                                                    uint8_t* a_base, int KT, int k0, int r) {
+  for (int c = 0; c < n; c += 16) {
+    float v[16];
+    tmem_ld16(tmem_row + col + c, v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] += bias[c + i];
+      if (relu) v[i] = fmaxf(v[i], 0.f);
+    }
+    store_split8(a_base, KT, r, k0 + c, v);
+    store_split8(a_base, KT, r, k0 + c + 8, v + 8);
+  }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_mlp_tc(TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base_sh;
+  const TcPlan& p = a.p;
+  uint8_t* W = smem;
+  const int wbytes = (p.blob_bytes + 1023) & ~1023;
+  uint8_t* X = smem + wbytes;            // [128 x 64] hi + lo   (32 KB)
+  uint8_t* E = X + kTcRows * 64 * 2 * 2;  // [128 x 128] hi + lo  (64 KB)
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
+  const uint32_t bar = smem_u32(&mbar);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t tmem_row = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's 32 lanes
+  const uint32_t sW = smem_u32(W), sX = smem_u32(X), sE = smem_u32(E);
+  const float* bias_f = reinterpret_cast<const float*>(W);
+  uint32_t phase = 0;
+  const int64_t ntiles = ceil_div(a.K, kTcRows);
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t k = tile * kTcRows + tid;
+    const bool valid = k < a.K;
+    // latent row -> X (A operand, KT = 64)
+    {
+      const float4* src = reinterpret_cast<const float4*>(a.latent + (valid ? k : 0) * 64);
+#pragma unroll
+      for (int c = 0; c < 64; c += 8) {
+        float v[8];
+        float4 x0 = valid ? __ldg(src + c / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 x1 = valid ? __ldg(src + c / 4 + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+        store_split8(X, 64, tid, c, v);
+      }
+    }
+    // trunk: 64 -> 64, ReLU (deformation.py:41-42)
+    for (int l = 0; l < p.depth; ++l) {
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        gemm_bf16x3(tmem, sX, 64, 0, sW + p.off_trunk[l], 64, 64, 4);
+        mma_commit(bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      tc_fence_after();
+      epilogue_to_operand(tmem_row, 0, 64, bias_f + p.off_b_trunk[l] / 4, true, X, 64, 0, tid);
+    }
+    // extractor layer 0 of all four branches as one N = 128 GEMM (deformation.py:46-49)
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      gemm_bf16x3(tmem, sX, 64, 0, sW + p.off_ext0, 64, 128, 4);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    epilogue_to_operand(tmem_row, 0, 128, bias_f + p.off_b_ext0 / 4, true, E, 128, 0, tid);
+    // extractor layer 1 per branch: A = E[:, 32b:32b+32]
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      for (int b = 0; b < 4; ++b) gemm_bf16x3(tmem + 32 * b, sE, 128, 32 * b, sW + p.off_ext1[b], 32, 32, 2);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // e2 of every branch = the F_feat concat [h_pos|h_rot|h_scale|h_opa] (deformation.py:119-120)
+    epilogue_to_operand(tmem_row, 0, 128, bias_f + p.off_b_ext1 / 4, true, E, 128, 0, tid);
+    // heads (N = 16 per branch) and F_feat layer 0 (K = 128, N = 32)
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      for (int b = 0; b < 4; ++b) gemm_bf16x3(tmem + 128 + 16 * b, sE, 128, 32 * b, sW + p.off_head[b], 32, 16, 2);
+      if (p.enable_feat) gemm_bf16x3(tmem + 192, sE, 128, 0, sW + p.off_f1, 128, 32, 8);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      const float* hb = bias_f + p.off_b_head / 4;
+      float d[64];
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        float v[16];
+        tmem_ld16(tmem_row + 128 + c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) d[c + i] = v[i] + hb[c + i];
+      }
+      if (valid) {  // raw-space deltas (deformation.py:126-133)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) a.o_pos[3 * k + q] = a.pos[3 * k + q] + d[q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a.o_rot[4 * k + q] = a.rot[4 * k + q] + d[16 + q];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) a.o_ls[3 * k + q] = a.ls[3 * k + q] + d[32 + q];
+        a.o_op[k] = a.op[k] + d[48];
+      }
+    }
+    if (p.enable_feat) {
+      epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, X, 32, 0, tid);
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        gemm_bf16x3(tmem, sX, 32, 0, sW + p.off_f2, 32, p.DP, 2);
+        mma_commit(bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      tc_fence_after();
+      const float* fb = bias_f + p.off_b_f2 / 4;
+      for (int c = 0; c < p.DP; c += 16) {
+        float v[16];
+        tmem_ld16(tmem_row + c, v);
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c + i < p.D) a.o_feat[(int64_t)p.D * k + c + i] = a.feat[(int64_t)p.D * k + c + i] + v[i] + fb[c + i];
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+bool tc_path_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f) {
+  if (n.width != 64 || n.latent_dim != 64 || n.feature_dim > 64 || n.depth < 1 || n.depth > FS4D_MAX_TRUNK)
+    return false;
+  if (n.enable_grid && !(f.levels * f.channels == 64 && f.levels <= kGatherMaxLevels)) return false;
+  return true;
+}
+
+static int build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p, TcPackArgs* pk) {
+  memset(&p, 0, sizeof(p));
+  p.depth = n.depth;
+  p.D = n.feature_dim;
+  p.DP = (n.feature_dim + 15) / 16 * 16;
+  if (p.DP == 0) p.DP = 16;
+  p.enable_feat = n.enable_feature_update;
+  p.enable_grid = n.enable_grid;
+  p.levels = f.levels;
+  p.C = f.channels;
+  p.L = 64;
+  for (int l = 0; l < FS4D_MAX_LEVELS; ++l)
+    for (int q = 0; q < 6; ++q) {
+      p.res[l][q][0] = f.res[l][q][0];
+      p.res[l][q][1] = f.res[l][q][1];
+      p.planes[l][q] = f.planes[l][q];
+    }
+  for (int a = 0; a < 3; ++a) {
+    p.lo[a] = f.aabb[a];
+    p.span[a] = f.aabb[3 + a] - f.aabb[a];
+  }
+  p.t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  int off = 0, nop = 0, nb = 0;
+  auto operand = [&](int N, int KT) {
+    int at = off;
+    off += N * KT * 2 * 2;
+    return at;
+  };
+  auto src = [](const Fs4dLinear& l, int row0) {
+    TcSrc s;
+    s.w = l.weight;
+    s.rows = l.out_dim;
+    s.in = l.in_dim;
+    s.row0 = row0;
+    return s;
+  };
+  for (int l = 0; l < n.depth; ++l) {
+    p.off_trunk[l] = operand(64, 64);
+    if (pk) pk->op[nop++] = TcOperand{64, 64, p.off_trunk[l], 1, {src(n.trunk[l], 0)}};
+  }
+  p.off_ext0 = operand(128, 64);
+  if (pk)
+    pk->op[nop++] = TcOperand{128, 64, p.off_ext0, 4,
+                              {src(n.ext[0][0], 0), src(n.ext[1][0], 32), src(n.ext[2][0], 64), src(n.ext[3][0], 96)}};
+  for (int b = 0; b < 4; ++b) {
+    p.off_ext1[b] = operand(32, 32);
+    if (pk) pk->op[nop++] = TcOperand{32, 32, p.off_ext1[b], 1, {src(n.ext[b][1], 0)}};
+  }
+  for (int b = 0; b < 4; ++b) {
+    p.off_head[b] = operand(16, 32);
+    if (pk) pk->op[nop++] = TcOperand{16, 32, p.off_head[b], 1, {src(n.head[b], 0)}};
+  }
+  p.off_f1 = operand(32, 128);
+  if (pk) pk->op[nop++] = TcOperand{32, 128, p.off_f1, 1, {src(n.feat[0], 0)}};
+  p.off_f2 = operand(p.DP, 32);
+  if (pk) pk->op[nop++] = TcOperand{p.DP, 32, p.off_f2, 1, {src(n.feat[1], 0)}};
+  auto bias = [&](int len) {
+    int at = off;
+    off += (len * 4 + 15) / 16 * 16;
+    return at;
+  };
+  for (int l = 0; l < n.depth; ++l) {
+    p.off_b_trunk[l] = bias(64);
+    if (pk) pk->bias[nb++] = TcBias{64, p.off_b_trunk[l], 1, {n.trunk[l].bias}, {64}, {0}};
+  }
+  p.off_b_ext0 = bias(128);
+  if (pk)
+    pk->bias[nb++] = TcBias{128, p.off_b_ext0, 4, {n.ext[0][0].bias, n.ext[1][0].bias, n.ext[2][0].bias, n.ext[3][0].bias},
+                            {32, 32, 32, 32}, {0, 32, 64, 96}};
+  p.off_b_ext1 = bias(128);
+  if (pk)
+    pk->bias[nb++] = TcBias{128, p.off_b_ext1, 4, {n.ext[0][1].bias, n.ext[1][1].bias, n.ext[2][1].bias, n.ext[3][1].bias},
+                            {32, 32, 32, 32}, {0, 32, 64, 96}};
+  p.off_b_head = bias(64);
+  if (pk)
+    pk->bias[nb++] = TcBias{64, p.off_b_head, 4, {n.head[0].bias, n.head[1].bias, n.head[2].bias, n.head[3].bias},
+                            {3, 4, 3, 1}, {0, 16, 32, 48}};
+  p.off_b_f1 = bias(32);
+  if (pk) pk->bias[nb++] = TcBias{32, p.off_b_f1, 1, {n.feat[0].bias}, {32}, {0}};
+  p.off_b_f2 = bias(p.DP);
+  if (pk) pk->bias[nb++] = TcBias{p.DP, p.off_b_f2, 1, {n.feat[1].bias}, {p.D}, {0}};
+  p.blob_bytes = (off + 15) / 16 * 16;
+  if (pk) {
+    pk->nop = nop;
+    pk->nbias = nb;
+  }
+  // shared memory: weights + X + E must fit
+  const int smem = ((p.blob_bytes + 1023) & ~1023) + kTcRows * 64 * 4 + kTcRows * 128 * 4;
+  if (smem > 227 * 1024) return fail(FS4D_ERR_CONFIG, "tcgen05 MLP weights exceed shared memory");
+  return FS4D_OK;
+}
+
+size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K) {
+  Fs4dHexPlane f;
+  memset(&f, 0, sizeof(f));
+  TcPlan p;
+  build_plan(n, f, 0.0, p, nullptr);
+  return (size_t)((p.blob_bytes + 255) / 256 * 256) + (size_t)K * 64 * 4 + 256;
+}
+
+int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
+                      Fs4dCloud& snap, void* ws, cudaStream_t s) {
+  TcPlan p;
+  static TcPackArgs pk;  // large: keep off the stack (host-side, filled per call)
+  int rc = build_plan(net, field, t, p, &pk);
+  if (rc) return rc;
+  uint8_t* blob = (uint8_t*)ws;
+  float* latent = (float*)((char*)ws + (p.blob_bytes + 255) / 256 * 256);
+  pk.blob = blob;
+  k_pack_tc<<<dim3(4, pk.nop + pk.nbias), 256, 0, s>>>(pk);
+  const int64_t K = cloud.K;
+  if (K == 0) return check_launch("deform_tc_pack");
+  k_hexplane_latent<<<(unsigned)ceil_div(K, kGatherWarps * 32), kGatherWarps * 32, 0, s>>>(p, K, cloud.positions,
+                                                                                           latent);
+  TcArgs a;
+  a.p = p;
+  a.K = K;
+  a.latent = latent;
+  a.blob = blob;
+  a.pos = cloud.positions;
+  a.rot = cloud.rotations;
+  a.ls = cloud.log_scales;
+  a.op = cloud.opacity_logits;
+  a.feat = cloud.features;
+  a.o_pos = snap.positions;
+  a.o_rot = snap.rotations;
+  a.o_ls = snap.log_scales;
+  a.o_op = snap.opacity_logits;
+  a.o_feat = snap.features;
+  const int smem = ((p.blob_bytes + 1023) & ~1023) + kTcRows * 64 * 4 + kTcRows * 128 * 4;
+  cudaFuncSetAttribute(k_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int64_t ntiles = ceil_div(K, kTcRows);
+  const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
+  k_mlp_tc<<<grid, kTcThreads, smem, s>>>(a);
+  return check_launch("deform_tc");
+}
+
+}  // namespace fs4d
