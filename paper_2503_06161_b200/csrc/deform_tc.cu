@@ -39,7 +39,7 @@ struct TcPlan {
 };
 
 constexpr int kTcRows = 128;       // M tile (TMEM lanes)
-constexpr int kTcThreads = 128;    // one thread per row
+constexpr int kTcThreads = 256;    // two threads per row (column halves)
 constexpr int kTmemCols = 256;
 
 __constant__ int c_axes_tc[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};  // hexplane.py:16
@@ -107,6 +107,71 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent(TcPlan p,
         }
         latent[k * L + l * C + ch] = prod;
       }
+    }
+  }
+}
+
+// 32-channel planes: lane = (Gaussian j%4, channel quad) so one warp
+// instruction fetches four corner rows as float4 (4 x 128 B) and interpolates
+// 4 channels per lane; 8x fewer load/FMA instructions than lane = channel.
+template <int LEVELS>
+__global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPlan p, int64_t K,
+                                                                             const float* __restrict__ pos,
+                                                                             float* __restrict__ latent) {
+  __shared__ int s_base[kGatherWarps][LEVELS * 6][32];
+  __shared__ float2 s_f[kGatherWarps][LEVELS * 6][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g0 = ((int64_t)blockIdx.x * kGatherWarps + warp) * 32;
+  if (g0 >= K) return;
+  {
+    const int64_t k = g0 + lane;
+    double c[4] = {0.0, 0.0, 0.0, p.t};
+    if (k < K) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double raw = ((double)pos[3 * k + a] - p.lo[a]) / p.span[a];
+        c[a] = fmin(fmax(raw, 0.0), 1.0);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < LEVELS; ++l)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int ra = p.res[l][q][0], rb = p.res[l][q][1];
+        const double u = c[c_axes_tc[q][0]] * (ra - 1), v = c[c_axes_tc[q][1]] * (rb - 1);
+        int i0 = (int)floor(u), j0 = (int)floor(v);
+        i0 = min(max(i0, 0), ra - 2);
+        j0 = min(max(j0, 0), rb - 2);
+        s_base[warp][l * 6 + q][lane] = (i0 * rb + j0) * 32;
+        s_f[warp][l * 6 + q][lane] = make_float2((float)(u - i0), (float)(v - j0));
+      }
+  }
+  __syncwarp();
+  const int sub = lane >> 3, ch = (lane & 7) * 4;
+  for (int j0 = 0; j0 < 32; j0 += 4) {
+    const int j = j0 + sub;
+    const int64_t k = g0 + j;
+#pragma unroll
+    for (int l = 0; l < LEVELS; ++l) {
+      float4 prod = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int rs = p.res[l][q][1] * 32;
+        const float* pl = p.planes[l][q] + s_base[warp][l * 6 + q][j] + ch;
+        const float2 f = s_f[warp][l * 6 + q][j];
+        const float w00 = (1.f - f.x) * (1.f - f.y), w10 = f.x * (1.f - f.y);
+        const float w01 = (1.f - f.x) * f.y, w11 = f.x * f.y;
+        const float4 a = __ldg(reinterpret_cast<const float4*>(pl));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(pl + 32));
+        const float4 c = __ldg(reinterpret_cast<const float4*>(pl + rs));
+        const float4 d = __ldg(reinterpret_cast<const float4*>(pl + rs + 32));
+        // hexplane.py:105-106 order: (1-fa)(1-fb)p00 + fa(1-fb)p10 + (1-fa)fb p01 + fa fb p11
+        prod.x *= w00 * a.x + w10 * c.x + w01 * b.x + w11 * d.x;
+        prod.y *= w00 * a.y + w10 * c.y + w01 * b.y + w11 * d.y;
+        prod.z *= w00 * a.z + w10 * c.z + w01 * b.z + w11 * d.z;
+        prod.w *= w00 * a.w + w10 * c.w + w01 * b.w + w11 * d.w;
+      }
+      if (k < K) *reinterpret_cast<float4*>(latent + k * 64 + l * 32 + ch) = prod;
     }
   }
 }
@@ -231,19 +296,41 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // A[M=128][KT] (hi block then lo block at +128*KT*2 bytes) times B[N][KT]
 // (hi, lo) into TMEM columns [col, col+N): hi*hi + hi*lo + lo*hi, K steps of 16.
+// A columns [a_k0, a_k0 + 16*ksteps) against B columns [b_k0, ...); the first
+// MMA overwrites the accumulator unless `accumulate` is set.
 __device__ __forceinline__ void gemm_bf16x3(uint32_t tmem_d, uint32_t a_base, int a_kt, int a_k0, uint32_t b_base,
-                                            int b_kt, int N, int ksteps) {
+                                            int b_kt, int b_k0, int N, int ksteps, bool accumulate) {
   const uint32_t id = idesc_bf16(N);
   const uint32_t a_lo = a_base + kTcRows * a_kt * 2, b_lo = b_base + N * b_kt * 2;
   const uint32_t a_sbo = a_kt * 16, b_sbo = b_kt * 16;
 #pragma unroll 1
   for (int s = 0; s < ksteps; ++s) {
-    const uint32_t ak = (uint32_t)(((a_k0 >> 3) + 2 * s) * 128), bk = (uint32_t)(s * 256);
+    const uint32_t ak = (uint32_t)(((a_k0 >> 3) + 2 * s) * 128), bk = (uint32_t)(((b_k0 >> 3) + 2 * s) * 128);
     const uint64_t ah = sdesc(a_base + ak, 128, a_sbo), al = sdesc(a_lo + ak, 128, a_sbo);
     const uint64_t bh = sdesc(b_base + bk, 128, b_sbo), bl = sdesc(b_lo + bk, 128, b_sbo);
-    mma_bf16(tmem_d, ah, bh, id, s > 0 ? 1u : 0u);
+    mma_bf16(tmem_d, ah, bh, id, (s > 0 || accumulate) ? 1u : 0u);
     mma_bf16(tmem_d, ah, bl, id, 1u);
     mma_bf16(tmem_d, al, bh, id, 1u);
   }
@@ -279,19 +366,20 @@ struct TcArgs {
   float* o_feat;
 };
 
-// one accumulator region [col, col+n) -> bias -> (relu) -> split -> A operand columns [k0, k0+n)
+// one accumulator region [col, col+n) -> bias -> (relu) -> split -> A operand
+// columns [k0, k0+n).  Two threads share a row: `half` takes the even or odd
+// 8-column chunks.
 __device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, int n, const float* bias, bool relu,
-                                                    uint8_t* a_base, int KT, int k0, int r) {
-  for (int c = 0; c < n; c += 16) {
-    float v[16];
-    tmem_ld16(tmem_row + col + c, v);
+                                                    uint8_t* a_base, int KT, int k0, int r, int half) {
+  for (int c = 8 * half; c < n; c += 16) {
+    float v[8];
+    tmem_ld8(tmem_row + col + c, v);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 8; ++i) {
       v[i] += bias[c + i];
       if (relu) v[i] = fmaxf(v[i], 0.f);
     }
     store_split8(a_base, KT, r, k0 + c, v);
-    store_split8(a_base, KT, r, k0 + c + 8, v + 8);
   }
 }
 
@@ -305,6 +393,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mlp_tc(TcArgs a) {
   uint8_t* X = smem + wbytes;            // [128 x 64] hi + lo   (32 KB)
   uint8_t* E = X + kTcRows * 64 * 2 * 2;  // [128 x 128] hi + lo  (64 KB)
   const int tid = threadIdx.x, warp = tid >> 5;
+  // two threads per TMEM lane / tile row: warps w and w+4 share lanes 32(w%4)..
+  const int row = tid & (kTcRows - 1), half = tid / kTcRows;
 
   for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
@@ -322,123 +412,130 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mlp_tc(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t tmem_row = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's 32 lanes
+  const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's 32 lanes
   const uint32_t sW = smem_u32(W), sX = smem_u32(X), sE = smem_u32(E);
   const float* bias_f = reinterpret_cast<const float*>(W);
   uint32_t phase = 0;
   const int64_t ntiles = ceil_div(a.K, kTcRows);
 
+  // the next tile's latent rows are prefetched into registers while the
+  // current tile runs its GEMM chain
+  float4 lat[8];  // this thread's half of its row: latent columns [32*half, 32*half+32)
+  auto load_latent = [&](int64_t t) {
+    const int64_t kk = t * kTcRows + row;
+    const float4* src = reinterpret_cast<const float4*>(a.latent + (kk < a.K ? kk : 0) * 64 + 32 * half);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) lat[c] = (t < ntiles && kk < a.K) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  load_latent(blockIdx.x);
+  // All warps reach each issue point; thread 0 issues after the fence/barrier
+  // so that every st.shared of the A operand is visible to the async proxy.
+#define TC_SYNC_ISSUE() \
+  fence_async_smem();   \
+  tc_fence_before();    \
+  __syncthreads();      \
+  if (tid == 0) tc_fence_after();
+
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t k = tile * kTcRows + tid;
+    const int64_t k = tile * kTcRows + row;
     const bool valid = k < a.K;
     // latent row -> X (A operand, KT = 64)
-    {
-      const float4* src = reinterpret_cast<const float4*>(a.latent + (valid ? k : 0) * 64);
 #pragma unroll
-      for (int c = 0; c < 64; c += 8) {
-        float v[8];
-        float4 x0 = valid ? __ldg(src + c / 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 x1 = valid ? __ldg(src + c / 4 + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-        store_split8(X, 64, tid, c, v);
-      }
+    for (int c = 0; c < 8; c += 2) {
+      float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
+      store_split8(X, 64, row, 32 * half + 4 * c, v);
     }
-    // trunk: 64 -> 64, ReLU (deformation.py:41-42)
+    load_latent(tile + gridDim.x);
+    // trunk: 64 -> 64, ReLU (deformation.py:41-42); accumulators in TMEM cols [128, 192)
     for (int l = 0; l < p.depth; ++l) {
-      fence_async_smem();
-      tc_fence_before();
-      __syncthreads();
+      TC_SYNC_ISSUE();
       if (tid == 0) {
-        tc_fence_after();
-        gemm_bf16x3(tmem, sX, 64, 0, sW + p.off_trunk[l], 64, 64, 4);
+        gemm_bf16x3(tmem + 128, sX, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
         mma_commit(bar);
       }
       mbar_wait(bar, phase);
       phase ^= 1;
       tc_fence_after();
-      epilogue_to_operand(tmem_row, 0, 64, bias_f + p.off_b_trunk[l] / 4, true, X, 64, 0, tid);
-    }
-    // extractor layer 0 of all four branches as one N = 128 GEMM (deformation.py:46-49)
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      gemm_bf16x3(tmem, sX, 64, 0, sW + p.off_ext0, 64, 128, 4);
-      mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    epilogue_to_operand(tmem_row, 0, 128, bias_f + p.off_b_ext0 / 4, true, E, 128, 0, tid);
-    // extractor layer 1 per branch: A = E[:, 32b:32b+32]
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      for (int b = 0; b < 4; ++b) gemm_bf16x3(tmem + 32 * b, sE, 128, 32 * b, sW + p.off_ext1[b], 32, 32, 2);
-      mma_commit(bar);
+      const float* tb = bias_f + p.off_b_trunk[l] / 4;
+      if (l + 1 < p.depth) {
+        epilogue_to_operand(tmem_row, 128, 64, tb, true, X, 64, 0, row, half);
+      } else {
+        // last trunk layer: each 16-column chunk of the hidden state feeds one
+        // K step of the fused extractor-0 GEMM (N = 128, deformation.py:46-49)
+        for (int c = 0; c < 64; c += 16) {
+          epilogue_to_operand(tmem_row, 128 + c, 16, tb + c, true, X, 64, c, row, half);
+          TC_SYNC_ISSUE();
+          if (tid == 0) gemm_bf16x3(tmem, sX, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
+        }
+        if (tid == 0) mma_commit(bar);
+      }
     }
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    // e2 of every branch = the F_feat concat [h_pos|h_rot|h_scale|h_opa] (deformation.py:119-120)
-    epilogue_to_operand(tmem_row, 0, 128, bias_f + p.off_b_ext1 / 4, true, E, 128, 0, tid);
-    // heads (N = 16 per branch) and F_feat layer 0 (K = 128, N = 32)
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      for (int b = 0; b < 4; ++b) gemm_bf16x3(tmem + 128 + 16 * b, sE, 128, 32 * b, sW + p.off_head[b], 32, 16, 2);
-      if (p.enable_feat) gemm_bf16x3(tmem + 192, sE, 128, 0, sW + p.off_f1, 128, 32, 8);
-      mma_commit(bar);
+    // extractor-0 epilogue per branch -> E[:, 32b:32b+32], then that branch's
+    // extractor-1 GEMM runs while the next branch's epilogue proceeds
+    for (int b = 0; b < 4; ++b) {
+      epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext0 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
+      TC_SYNC_ISSUE();
+      if (tid == 0) gemm_bf16x3(tmem + 32 * b, sE, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
     }
+    if (tid == 0) mma_commit(bar);
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // e2 of every branch = the F_feat concat [h_pos|h_rot|h_scale|h_opa]
+    // (deformation.py:119-120): per branch, the head GEMM (N = 16) and that
+    // branch's K slice of F_feat layer 0 (N = 32) are issued as soon as it lands
+    for (int b = 0; b < 4; ++b) {
+      epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext1 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
+      TC_SYNC_ISSUE();
+      if (tid == 0) {
+        gemm_bf16x3(tmem + 128 + 16 * b, sE, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
+        if (p.enable_feat) gemm_bf16x3(tmem + 192, sE, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
+      }
+    }
+    if (tid == 0) mma_commit(bar);
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
     {
+      // raw-space deltas (deformation.py:126-133); half 0: position + rotation
+      // heads, half 1: scale + opacity heads (head b lives in cols 128 + 16b)
       const float* hb = bias_f + p.off_b_head / 4;
-      float d[64];
+      float d0[4], d1[4];
+      tmem_ld4(tmem_row + 128 + 32 * half, d0);
+      tmem_ld4(tmem_row + 144 + 32 * half, d1);
+      if (valid) {
+        if (half == 0) {
 #pragma unroll
-      for (int c = 0; c < 64; c += 16) {
-        float v[16];
-        tmem_ld16(tmem_row + 128 + c, v);
+          for (int q = 0; q < 3; ++q) a.o_pos[3 * k + q] = a.pos[3 * k + q] + d0[q] + hb[q];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) d[c + i] = v[i] + hb[c + i];
-      }
-      if (valid) {  // raw-space deltas (deformation.py:126-133)
+          for (int q = 0; q < 4; ++q) a.o_rot[4 * k + q] = a.rot[4 * k + q] + d1[q] + hb[16 + q];
+        } else {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) a.o_pos[3 * k + q] = a.pos[3 * k + q] + d[q];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) a.o_rot[4 * k + q] = a.rot[4 * k + q] + d[16 + q];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) a.o_ls[3 * k + q] = a.ls[3 * k + q] + d[32 + q];
-        a.o_op[k] = a.op[k] + d[48];
+          for (int q = 0; q < 3; ++q) a.o_ls[3 * k + q] = a.ls[3 * k + q] + d0[q] + hb[32 + q];
+          a.o_op[k] = a.op[k] + d1[0] + hb[48];
+        }
       }
     }
     if (p.enable_feat) {
-      epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, X, 32, 0, tid);
-      fence_async_smem();
-      tc_fence_before();
-      __syncthreads();
+      epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, X, 32, 0, row, half);
+      TC_SYNC_ISSUE();
       if (tid == 0) {
-        tc_fence_after();
-        gemm_bf16x3(tmem, sX, 32, 0, sW + p.off_f2, 32, p.DP, 2);
+        gemm_bf16x3(tmem, sX, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
         mma_commit(bar);
       }
       mbar_wait(bar, phase);
       phase ^= 1;
       tc_fence_after();
       const float* fb = bias_f + p.off_b_f2 / 4;
-      for (int c = 0; c < p.DP; c += 16) {
-        float v[16];
-        tmem_ld16(tmem_row + c, v);
+      for (int c = 8 * half; c < p.DP; c += 16) {
+        float v[8];
+        tmem_ld8(tmem_row + c, v);
         if (valid) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
+          for (int i = 0; i < 8; ++i)
             if (c + i < p.D) a.o_feat[(int64_t)p.D * k + c + i] = a.feat[(int64_t)p.D * k + c + i] + v[i] + fb[c + i];
         }
       }
@@ -572,8 +669,11 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   k_pack_tc<<<dim3(4, pk.nop + pk.nbias), 256, 0, s>>>(pk);
   const int64_t K = cloud.K;
   if (K == 0) return check_launch("deform_tc_pack");
-  k_hexplane_latent<<<(unsigned)ceil_div(K, kGatherWarps * 32), kGatherWarps * 32, 0, s>>>(p, K, cloud.positions,
-                                                                                           latent);
+  const unsigned gblocks = (unsigned)ceil_div(K, kGatherWarps * 32);
+  if (p.enable_grid && p.C == 32 && p.levels == 2)
+    k_hexplane_latent_c32<2><<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
+  else
+    k_hexplane_latent<<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
   TcArgs a;
   a.p = p;
   a.K = K;

@@ -322,6 +322,9 @@ __global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
   const uint2 rg = a.ranges[tile];
   const bool first = a.c0 == 0;
   const float fc = (float)col, fr = (float)row;
+  const int lane = threadIdx.x & 31;
+  const int wrow0 = ty * kTile + (threadIdx.x >> 5) * 2;  // this warp's two pixel rows
+  const int tcol0 = tx * kTile;
 
   float T = 1.f, acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f;
   float accf[DC > 0 ? DC : 1];
@@ -355,44 +358,67 @@ __global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
     }
     __syncthreads();
     const int cnt = min((uint32_t)kTilePixels, rg.y - b);
-    if (!done) {
-      for (int k = 0; k < cnt; ++k) {
-        const int4 pr = s_pr[k];
-        if (col < pr.x || col > pr.y || row < pr.z || row > pr.w) continue;
-        const float2 m = s_xy[k];
-        const float4 co = s_co[k];
-        const float dx = fc - m.x, dy = fr - m.y;
-        const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
-        if (q > kQSkip) continue;
-        const float gv = __expf(-0.5f * q);
-        const float al = fminf(co.w * gv, a.alpha_cap);
-        if (al < a.alpha_skip) continue;
-        if (T < a.stop) { done = true; break; }
-        const float w = al * T;
-        if (first) {
-          const float4 cz = s_rgbz[k];
-          acc_r += w * cz.x;
-          acc_g += w * cz.y;
-          acc_b += w * cz.z;
-          acc_z += w * cz.w;
-        }
-        if (DC > 0) {
-          const float* f = s_f + k * DC;
+    // warp-level culling: one ballot per 32 staged Gaussians keeps those whose
+    // pixel footprint touches this warp's two pixel rows; the per-thread loop
+    // then walks only the set bits, in depth order
+    unsigned wmask[kTilePixels / 32];
 #pragma unroll
-          for (int c = 0; c < DC; c += 4) {
-            if (DC >= 4) {
-              const float4 fv = *reinterpret_cast<const float4*>(f + c);
+    for (int m = 0; m < kTilePixels / 32; ++m) {
+      const int kk = m * 32 + lane;
+      bool hit = false;
+      if (kk < cnt) {
+        const int4 pr = s_pr[kk];
+        hit = pr.w >= wrow0 && pr.z <= wrow0 + 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
+      }
+      wmask[m] = __ballot_sync(0xffffffffu, hit);
+    }
+    if (!done) {
+#pragma unroll 1
+      for (int m = 0; m < kTilePixels / 32 && !done; ++m) {
+        unsigned bits = wmask[m];
+        while (bits) {
+          const int k = m * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int4 pr = s_pr[k];
+          if (col < pr.x || col > pr.y || row < pr.z || row > pr.w) continue;
+          const float2 mm = s_xy[k];
+          const float4 co = s_co[k];
+          const float dx = fc - mm.x, dy = fr - mm.y;
+          const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
+          if (q > kQSkip) continue;
+          const float gv = __expf(-0.5f * q);
+          const float al = fminf(co.w * gv, a.alpha_cap);
+          if (al < a.alpha_skip) continue;
+          if (T < a.stop) {
+            done = true;
+            break;
+          }
+          const float w = al * T;
+          if (first) {
+            const float4 cz = s_rgbz[k];
+            acc_r += w * cz.x;
+            acc_g += w * cz.y;
+            acc_b += w * cz.z;
+            acc_z += w * cz.w;
+          }
+          if (DC > 0) {
+#pragma unroll
+            for (int c = 0; c < DC; c += 4) {
+              const float4 fv = *reinterpret_cast<const float4*>(&s_f[k * DC + c]);
               accf[c] += w * fv.x;
               accf[c + 1] += w * fv.y;
               accf[c + 2] += w * fv.z;
               accf[c + 3] += w * fv.w;
             }
           }
+          T *= (1.f - al);
+          ++ncontrib;
+          last = (int)(b + k);
+          if (T < a.stop) {
+            done = true;
+            break;
+          }
         }
-        T *= (1.f - al);
-        ++ncontrib;
-        last = (int)(b + k);
-        if (T < a.stop) { done = true; break; }
       }
     }
   }
