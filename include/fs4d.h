@@ -224,8 +224,23 @@ int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field,
                     const Fs4dDeformNet* net, double t,
                     const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads,
                     Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads,
+                    int32_t accumulate,
                     void* workspace, size_t workspace_bytes,
                     int32_t* status, void* stream);
+/* accumulate != 0 adds into every output instead of overwriting it (gradient
+ * accumulation over the (view, t) pairs of a training step).  Non-NULL
+ * cloud_grads fields other than positions receive the pass-through snapshot
+ * gradients (deformation.py:178-181; colours/SH bypass the deformation,
+ * training.py:518). */
+
+/* Fused L1 photometric + feature loss and its upstream gradients
+ * (training.py:302-338 with an all-ones mask, semantic.py:171-181 at render
+ * resolution): dC = w_rgb*sign(C-Ct)/(3HW), dF = w_feat*sign(F-Ft)/(HW); the
+ * weighted loss is atomically added to *loss (device double). */
+int fs4d_l1_loss_grad(const float* color, const float* color_target, const float* feature,
+                      const float* feature_target, int32_t height, int32_t width, int32_t D,
+                      double w_rgb, double w_feat, float* d_color, float* d_feature, double* loss,
+                      void* stream);
 
 /* ---- rasterizer ---- */
 size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info);

@@ -115,8 +115,13 @@ SIGNATURES = {
                                        ctypes.POINTER(DeformNet), ctypes.c_double,
                                        ctypes.POINTER(Cloud), ctypes.POINTER(Cloud),
                                        ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane),
-                                       ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
-                                       ctypes.c_void_p]),
+                                       ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_l1_loss_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p]),
     "fs4d_render_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(RecordInfo)]),
     "fs4d_render_fwd": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(Camera),
                                        ctypes.POINTER(RasterCfg), ctypes.POINTER(RecordInfo),

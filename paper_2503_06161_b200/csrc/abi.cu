@@ -70,7 +70,9 @@ size_t deform_workspace_bytes(const Fs4dDeformNet& net, int64_t K, int* nparts_o
 int deform_forward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, Fs4dCloud&, void*, size_t,
                    cudaStream_t);
 int deform_backward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, const Fs4dCloud&, Fs4dCloud&,
-                    Fs4dDeformNet&, Fs4dHexPlane*, void*, size_t, cudaStream_t);
+                    Fs4dDeformNet&, Fs4dHexPlane*, int, void*, size_t, cudaStream_t);
+int l1_loss_grad(const float*, const float*, const float*, const float*, int, int, int, double, double, float*, float*,
+                 double*, cudaStream_t);
 
 static int check_cloud(const Fs4dCloud* c, bool need_colors) {
   if (!c) return fail(FS4D_ERR_CONFIG, "null cloud");
@@ -183,8 +185,8 @@ int fs4d_deform_fwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4
 
 int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net, double t,
                     const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads, Fs4dDeformNet* net_grads,
-                    Fs4dHexPlane* plane_grads, void* workspace, size_t workspace_bytes, int32_t* status,
-                    void* stream) {
+                    Fs4dHexPlane* plane_grads, int32_t accumulate, void* workspace, size_t workspace_bytes,
+                    int32_t* status, void* stream) {
   (void)status;
   int rc = check_cloud(cloud, false);
   if (rc) return rc;
@@ -192,8 +194,18 @@ int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4
     return fail(FS4D_ERR_CONFIG, "null deform_bwd argument");
   if (snapshot_grads->K != cloud->K || cloud_grads->K != cloud->K)
     return fail(FS4D_ERR_CONTRACT, "gradient rows do not match the cloud");
-  return deform_backward(*cloud, *field, *net, t, *snapshot_grads, *cloud_grads, *net_grads, plane_grads, workspace,
-                         workspace_bytes, (cudaStream_t)stream);
+  return deform_backward(*cloud, *field, *net, t, *snapshot_grads, *cloud_grads, *net_grads, plane_grads, accumulate,
+                         workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int fs4d_l1_loss_grad(const float* color, const float* color_target, const float* feature,
+                      const float* feature_target, int32_t height, int32_t width, int32_t D, double w_rgb,
+                      double w_feat, float* d_color, float* d_feature, double* loss, void* stream) {
+  if (!color || !color_target || !d_color || height <= 0 || width <= 0 || D < 0)
+    return fail(FS4D_ERR_CONFIG, "bad l1 loss arguments");
+  if (D > 0 && (!feature || !feature_target || !d_feature)) return fail(FS4D_ERR_CONFIG, "feature buffers missing");
+  return l1_loss_grad(color, color_target, feature, feature_target, height, width, D, w_rgb, w_feat, d_color,
+                      d_feature, loss, (cudaStream_t)stream);
 }
 
 size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info) {

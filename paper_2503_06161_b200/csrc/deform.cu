@@ -162,6 +162,7 @@ struct DefArgs {
   const float* g_op;
   const float* g_feat;
   float* cg_pos;
+  int accumulate;
   float* wpart;  // [gridDim.x][packed_floats] per-CTA weight-gradient partials
   NetDesc net;
   FieldDesc field;
@@ -515,7 +516,7 @@ __device__ void hexplane_backward_one(const DefArgs& a, const float* glat, int g
   }
   if (lane < 3) {
     const float d = inside[lane] ? (float)((double)dco[lane] / f.span[lane]) : 0.f;
-    a.cg_pos[3 * k + lane] = a.g_pos[3 * k + lane] + d;
+    a.cg_pos[3 * k + lane] = (a.accumulate ? a.cg_pos[3 * k + lane] : 0.f) + a.g_pos[3 * k + lane] + d;
   }
 }
 
@@ -636,7 +637,8 @@ __global__ void __launch_bounds__(kDefThreads) k_deform_bwd(DefArgs a) {
     if (n.enable_grid) {
       for (int g = warp; g < ng; g += nw) hexplane_backward_one(a, gcur, g, TG, g0 + g, lane);
     } else {
-      for (int idx = threadIdx.x; idx < 3 * ng; idx += blockDim.x) a.cg_pos[3 * g0 + idx] = a.g_pos[3 * g0 + idx];
+      for (int idx = threadIdx.x; idx < 3 * ng; idx += blockDim.x)
+        a.cg_pos[3 * g0 + idx] = (a.accumulate ? a.cg_pos[3 * g0 + idx] : 0.f) + a.g_pos[3 * g0 + idx];
     }
     __syncthreads();
   }
@@ -649,6 +651,7 @@ struct ReduceArgs {
   float* gb[kMaxLayers];
   int n_layers;
   int nparts;
+  int accumulate;
   int64_t packed_floats;
   const float* wpart;
 };
@@ -670,8 +673,25 @@ __global__ void k_reduce_wgrads(ReduceArgs a) {
     }
     float s = 0.f;
     for (int p = 0; p < a.nparts; ++p) s += a.wpart[(int64_t)p * a.packed_floats + src];
-    *dst = s;
+    *dst = a.accumulate ? *dst + s : s;
   }
+}
+
+// cloud gradients that pass straight through the deformation
+// (deformation.py:178-181: rotations, log-scales, opacity logits, features;
+// colours and SH bypass it, training.py:518)
+struct PassArgs {
+  const float* src[6];
+  float* dst[6];
+  int64_t n[6];
+  int accumulate;
+};
+
+__global__ void k_grad_passthrough(PassArgs a) {
+  const int f = blockIdx.y;
+  if (!a.src[f] || !a.dst[f]) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.n[f]; e += (int64_t)gridDim.x * blockDim.x)
+    a.dst[f][e] = a.accumulate ? a.dst[f][e] + a.src[f][e] : a.src[f][e];
 }
 
 // ---------------------------------------------------------------------------
@@ -799,8 +819,8 @@ int deform_forward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4d
 }
 
 int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
-                    const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng, Fs4dHexPlane* pg, void* ws,
-                    size_t ws_bytes, cudaStream_t s) {
+                    const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng, Fs4dHexPlane* pg, int accumulate,
+                    void* ws, size_t ws_bytes, cudaStream_t s) {
   DefArgs a;
   memset(&a, 0, sizeof(a));
   size_t smem = 0;
@@ -812,16 +832,32 @@ int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4
   a.g_op = sg.opacity_logits;
   a.g_feat = sg.features;
   a.cg_pos = cg.positions;
+  a.accumulate = accumulate;
   if (net.enable_grid) {
     if (!pg) return fail(FS4D_ERR_CONFIG, "plane gradient buffers required when the grid is enabled");
     for (int l = 0; l < field.levels; ++l)
       for (int p = 0; p < 6; ++p) {
         a.field.gplanes[l][p] = pg->planes[l][p];
-        cudaMemsetAsync(pg->planes[l][p], 0,
-                        (size_t)field.res[l][p][0] * field.res[l][p][1] * field.channels * 4, s);
+        if (!accumulate)
+          cudaMemsetAsync(pg->planes[l][p], 0,
+                          (size_t)field.res[l][p][0] * field.res[l][p][1] * field.channels * 4, s);
       }
   }
   StageTimer st(FS4D_STAGE_DEFORM_BWD, s);
+  {
+    const int n_sh = (sg.sh_degree + 1) * (sg.sh_degree + 1) - 1;
+    PassArgs pa;
+    const float* srcs[6] = {sg.rotations, sg.log_scales, sg.opacity_logits, sg.colors_raw, sg.sh_rest, sg.features};
+    float* dsts[6] = {cg.rotations, cg.log_scales, cg.opacity_logits, cg.colors_raw, cg.sh_rest, cg.features};
+    const int64_t ns[6] = {cloud.K * 4, cloud.K * 3, cloud.K, cloud.K * 3, cloud.K * n_sh * 3, cloud.K * cloud.D};
+    for (int f = 0; f < 6; ++f) {
+      pa.src[f] = ns[f] > 0 ? srcs[f] : nullptr;
+      pa.dst[f] = ns[f] > 0 ? dsts[f] : nullptr;
+      pa.n[f] = ns[f];
+    }
+    pa.accumulate = accumulate;
+    k_grad_passthrough<<<dim3(64, 6), 256, 0, s>>>(pa);
+  }
   const int64_t ntiles = ceil_div(cloud.K, a.TG);
   const int grid = (int)(ntiles < kNumSMs * 2 ? (ntiles > 0 ? ntiles : 1) : kNumSMs * 2);
   cudaMemsetAsync(a.wpart, 0, (size_t)grid * a.net.packed_floats * 4, s);
@@ -851,6 +887,7 @@ int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4
   }
   ra.n_layers = d.n_layers;
   ra.nparts = grid;
+  ra.accumulate = accumulate;
   ra.packed_floats = d.packed_floats;
   ra.wpart = a.wpart;
   dim3 rg(16, d.n_layers);

@@ -278,25 +278,34 @@ class DeformEngine:
                                          _stream()))
         return out
 
-    def backward(self, cloud, field, net, t, snap_grads):
-        """Returns (d_positions [K,3], net_grads DeviceNet, plane_grads DeviceField|None)."""
+    def backward(self, cloud, field, net, t, snap_grads, cloud_grads=None, net_grads=None,
+                 plane_grads=None, accumulate=False):
+        """deform_backward on device.  Without output buffers: returns
+        (d_positions [K,3], net_grads DeviceNet, plane_grads DeviceField|None).
+        With a DeviceCloud `cloud_grads` (+ net/plane grads) every cloud
+        gradient is written (or added, accumulate=True) and the buffers are
+        returned."""
         k = len(cloud)
-        gpos = torch.empty(k, 3, dtype=torch.float32, device=self.device)
-        ngrads = net.zeros_like()
-        pgrads = field.zeros_like() if net.enable_grid else None
+        ngrads = net_grads if net_grads is not None else net.zeros_like()
+        pgrads = plane_grads if plane_grads is not None else (field.zeros_like() if net.enable_grid else None)
         cs, fs, ns = cloud.struct(), field.struct(), net.struct()
         sgs, ngs = snap_grads.struct(), ngrads.struct()
-        cgs = N.Cloud()
-        cgs.K = k
-        cgs.positions = gpos.data_ptr()
+        if cloud_grads is None:
+            gpos = torch.empty(k, 3, dtype=torch.float32, device=self.device)
+            cgs = N.Cloud()
+            cgs.K = k
+            cgs.positions = gpos.data_ptr()
+        else:
+            gpos = cloud_grads.positions
+            cgs = cloud_grads.struct()
         pgs = pgrads.struct() if pgrads is not None else None
         ws = self._workspace(ns, k)
         N.check(N.load().fs4d_deform_bwd(ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns),
                                          float(t), ctypes.byref(sgs), ctypes.byref(cgs),
                                          ctypes.byref(ngs),
                                          ctypes.byref(pgs) if pgs is not None else None,
-                                         _p(ws), ws.numel(), None, _stream()))
-        return gpos, ngrads, pgrads
+                                         int(bool(accumulate)), _p(ws), ws.numel(), None, _stream()))
+        return (cloud_grads if cloud_grads is not None else gpos), ngrads, pgrads
 
 
 class RenderRecordDev:
