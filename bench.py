@@ -357,11 +357,67 @@ def gpu_bench(args, rank, world, local):
                 h2d=pipe.h2d_bytes(host_in), d2h=pipe.d2h_bytes(), steps=steps)
 
 
-def launches_per_frame(n_pairs_cap_bits=11):
-    deform = 2                        # pack + k_deform_fwd
-    sort_passes = 32 // 8
-    pair_passes = -(-n_pairs_cap_bits // 8)
-    render = 1 + 1 + 3 * sort_passes + 1 + 1 + 3 + 1 + 1 + 3 * pair_passes + 1 + 1  # status,pre,sort,fix,count,scan,check,emit,sort,ranges,blend
+def train_bench(args, rank, world, local):
+    """configs[4]: 8 (view, t) pairs per GPU, L1 RGB + L1 feature, backward
+    through rasterizer and deformation, one flat-gradient all-reduce."""
+    import torch
+    import paper_2503_06161_b200 as fs
+    from paper_2503_06161_b200 import device as dv
+    from paper_2503_06161_b200.train import TrainStep
+
+    torch.cuda.set_device(local)
+    cloud_np, field_np, net_np, Kmat = make_scene(0)
+    step = TrainStep(dv.DeviceCloud.from_cloud(cloud_np), dv.DeviceField.from_field(field_np),
+                     dv.DeviceNet.from_net(net_np), H, W, fs.RasterConfig(), world=world)
+    rng = np.random.default_rng(100 + rank)
+    pairs = 8
+
+    def rigid():
+        axis = rng.normal(size=3)
+        axis /= np.linalg.norm(axis)
+        ang = np.deg2rad(rng.uniform(-5, 5))
+        Kx = np.array([[0, -axis[2], axis[1]], [axis[2], 0, -axis[0]], [-axis[1], axis[0], 0]])
+        T = np.eye(4)
+        T[:3, :3] = np.eye(3) + np.sin(ang) * Kx + (1 - np.cos(ang)) * Kx @ Kx
+        T[:3, 3] = rng.uniform(-0.1, 0.1, 3)
+        return T
+
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(rank)
+    batch = [(float(rng.uniform()), Kmat, rigid(),
+              torch.rand(H, W, 3, device="cuda", generator=gen),
+              torch.randn(H, W, D, device="cuda", generator=gen)) for _ in range(pairs)]
+    step.run(batch, check=True)  # sizes the pair buffer
+    for _ in range(args.warmup):
+        step.run(batch)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(args.steps):
+        step.run(batch)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = dist_max(a.elapsed_time(b), world)
+    dv.profile_collect()
+    dv.profile_enable(True)
+    step.run(batch)
+    torch.cuda.synchronize()
+    prof = dv.profile_collect()
+    dv.profile_enable(False)
+    return dict(ms=ms, prof=prof, loss=float(step.loss.item()), grad_floats=step.grads.numel, pairs=pairs)
+
+
+def launches_per_frame(tile_bits=11):
+    """libfs4d kernels per frame: deform (pack, HexPlane latent, tcgen05 MLP) and
+    render (status reset, preprocess, 3 kernels per radix pass, tie fix-up,
+    tile count, 3-kernel scan, pair check, emit, tile ranges, blend)."""
+    deform = 3
+    sort_passes = -(-32 // 11)
+    pair_passes = -(-tile_bits // 11)
+    render = 1 + 1 + 3 * sort_passes + 1 + 1 + 3 + 1 + 1 + 3 * pair_passes + 1 + 1
     return deform + render
 
 
@@ -373,6 +429,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="render", choices=["render", "train"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -398,6 +455,20 @@ def main():
         print(json.dumps(line))
         return
 
+    if args.workload == "train":
+        r = train_bench(args, rank, world, local)
+        if rank == 0:
+            line = dict(base)
+            line.update({"metric": "configs[4] training steps/s (8 (view,t) pairs per GPU, fwd+bwd+allreduce)",
+                         "unit": "steps/s", "value": world * args.steps / (r["ms"] / 1000.0) / world,
+                         "ms_per_step": r["ms"] / args.steps,
+                         "frames_per_s": world * r["pairs"] * args.steps / (r["ms"] / 1000.0),
+                         "stage_ms_per_step": {s: round(ms, 4) for s, (ms, c) in r["prof"].items() if c},
+                         "allreduce_floats": r["grad_floats"], "loss": r["loss"]})
+            line["config"] = dict(base["config"], workload="configs[4]: configs[1] scene, 8 (view,t) pairs/GPU, "
+                                                           "L1 RGB + L1 feature", parallelism=f"dp{world}")
+            print(json.dumps(line))
+        return
     r = gpu_bench(args, rank, world, local)
     hbm, tf, peak_src = peaks()
     frames = world * r["steps"]

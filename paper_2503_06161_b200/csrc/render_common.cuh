@@ -48,9 +48,9 @@ inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
   int bits = 0;
   while ((1ll << bits) < (int64_t)L.ntiles) ++bits;
   L.tile_bits = bits;
-  // depth sort: 32-bit keys in 8-bit passes -> 4 passes -> result in buffer 0
-  L.depth_final = (32 / kRadixBits) & 1;
-  L.pair_final = (int)(ceil_div(bits, kRadixBits) & 1);
+  // ping-pong parity after the radix passes (32-bit depth keys, tile-id keys)
+  L.depth_final = (int)(ceil_div(32, kMaxRadixBits) & 1);
+  L.pair_final = (int)(ceil_div(bits, kMaxRadixBits) & 1);
   L.acc_stride = (int)ceil_div(10 + L.D, 32) * 32;
   const int64_t K = L.K > 0 ? L.K : 1;
   const int64_t cap = L.cap > 0 ? L.cap : 1;

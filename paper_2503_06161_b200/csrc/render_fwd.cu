@@ -253,23 +253,47 @@ __global__ void k_pairs_check(uint32_t* counters, int64_t cap, int32_t* status) 
   }
 }
 
-// one warp per Gaussian: lanes stride over its tile rectangle
+// one thread per Gaussian (depth rank r); rectangles larger than 16 tiles are
+// emitted cooperatively by the whole warp so one huge footprint does not
+// serialise a lane
 __global__ void k_emit_pairs(const uint32_t* __restrict__ order, const int4* __restrict__ tile_rect,
                              const uint64_t* __restrict__ toff, const uint32_t* counters, int64_t cap, int ntx,
                              uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  if (r >= (int64_t)counters[CNT_VISIBLE]) return;
-  const uint32_t i = order[r];
-  const int4 t = tile_rect[i];
-  const int w = t.y - t.x + 1, h = t.w - t.z + 1;
-  const uint64_t base = toff[r];
-  for (int k = lane; k < w * h; k += 32) {
-    uint64_t o = base + (uint64_t)k;
-    if (o >= (uint64_t)cap) break;
-    int ty = t.z + k / w, tx = t.x + k % w;
-    pkeys[o] = (uint32_t)(ty * ntx + tx);
-    pvals[o] = i;
+  const int64_t M = counters[CNT_VISIBLE];
+  uint32_t i = 0;
+  int4 t = make_int4(0, -1, 0, -1);
+  uint64_t base = 0;
+  if (r < M) {
+    i = order[r];
+    t = tile_rect[i];
+    base = toff[r];
+  }
+  const int w = t.y - t.x + 1, area = w * (t.w - t.z + 1);
+  const bool big = r < M && area > 16;
+  if (r < M && !big) {
+    for (int k = 0; k < area; ++k) {
+      const uint64_t o = base + (uint64_t)k;
+      if (o >= (uint64_t)cap) break;
+      pkeys[o] = (uint32_t)((t.z + k / w) * ntx + t.x + k % w);
+      pvals[o] = i;
+    }
+  }
+  unsigned todo = __ballot_sync(0xffffffffu, big);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t gi = __shfl_sync(0xffffffffu, i, src);
+    const int tx0 = __shfl_sync(0xffffffffu, t.x, src), tz0 = __shfl_sync(0xffffffffu, t.z, src);
+    const int gw = __shfl_sync(0xffffffffu, w, src), ga = __shfl_sync(0xffffffffu, area, src);
+    const uint64_t gb = __shfl_sync(0xffffffffu, base, src);
+    for (int k = lane; k < ga; k += 32) {
+      const uint64_t o = gb + (uint64_t)k;
+      if (o >= (uint64_t)cap) break;
+      pkeys[o] = (uint32_t)((tz0 + k / gw) * ntx + tx0 + k % gw);
+      pvals[o] = gi;
+    }
   }
 }
 
@@ -528,7 +552,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   uint32_t* pk[2] = {at<uint32_t>(ws, L.pkeys0), at<uint32_t>(ws, L.pkeys1)};
   uint32_t* pv[2] = {at<uint32_t>(ws, L.pvals0), at<uint32_t>(ws, L.pvals1)};
   if (K > 0)
-    k_emit_pairs<<<(unsigned)ceil_div(K * 32, 256), 256, 0, s>>>(order, p.tile_rect, toff, counters, L.cap, L.ntx,
+    k_emit_pairs<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, p.tile_rect, toff, counters, L.cap, L.ntx,
                                                                   pk[0], pv[0]);
   int pf = radix_sort_pairs(pk, pv, L.cap, counters + CNT_PAIRS_CLAMPED, 0, L.tile_bits, scratch, s);
   if (L.cap > 0)

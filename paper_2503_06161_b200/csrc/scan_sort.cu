@@ -128,8 +128,9 @@ void exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, int64_t cap, c
 // ---------------------------------------------------------------------------
 __global__ void k_radix_hist(const uint32_t* __restrict__ keys, int64_t cap, const uint32_t* n_dev,
                              int shift, int nbits, uint32_t* __restrict__ hist, int nblocks) {
-  __shared__ uint32_t h[kRadix];
-  for (int d = threadIdx.x; d < kRadix; d += blockDim.x) h[d] = 0;
+  __shared__ uint32_t h[kMaxRadix];
+  const int radix = 1 << nbits;
+  for (int d = threadIdx.x; d < radix; d += blockDim.x) h[d] = 0;
   __syncthreads();
   const int64_t n = live_count(n_dev, cap);
   const int64_t base = (int64_t)blockIdx.x * kSortChunk;
@@ -142,7 +143,7 @@ __global__ void k_radix_hist(const uint32_t* __restrict__ keys, int64_t cap, con
     }
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kRadix; d += blockDim.x) hist[(int64_t)d * nblocks + blockIdx.x] = h[d];
+  for (int d = threadIdx.x; d < radix; d += blockDim.x) hist[(int64_t)d * nblocks + blockIdx.x] = h[d];
 }
 
 // one block per digit: exclusive scan over blocks, digit total out
@@ -168,22 +169,37 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int64_t cap,
     const uint32_t* n_dev, int shift, int nbits, const uint32_t* __restrict__ hist,
     const uint32_t* __restrict__ totals, int nblocks) {
-  __shared__ uint32_t digit_base[kRadix];
-  __shared__ uint32_t warp_cnt[kSortWarps][kRadix];
+  // dynamic: digit_base[radix] + warp_cnt[kSortWarps][radix]
+  extern __shared__ uint32_t rs_smem[];
   __shared__ uint32_t scan_tmp[32];
+  const int radix = 1 << nbits;
+  uint32_t* digit_base = rs_smem;
+  uint32_t* warp_cnt = rs_smem + radix;  // [warp * radix + d]
   const int64_t n = live_count(n_dev, cap);
   const int64_t base = (int64_t)blockIdx.x * kSortChunk;
   if (base >= n) return;  // uniform per block
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t mask = (1u << nbits) - 1u;
 
-  // global base per digit = exclusive scan of totals + this block's offset
+  // global base per digit = exclusive scan of totals + this block's offset;
+  // thread t owns digits [t*per, t*per + per)
   {
-    uint32_t t = threadIdx.x < kRadix ? totals[threadIdx.x] : 0u;
-    uint32_t e = block_exclusive_scan<uint32_t>(t, scan_tmp, nullptr);
-    if (threadIdx.x < kRadix) digit_base[threadIdx.x] = e + hist[(int64_t)threadIdx.x * nblocks + blockIdx.x];
+    const int per = (radix + kSortThreads - 1) / kSortThreads;
+    uint32_t loc = 0;
+    for (int q = 0; q < per; ++q) {
+      const int d = threadIdx.x * per + q;
+      if (d < radix) loc += totals[d];
+    }
+    uint32_t e = block_exclusive_scan<uint32_t>(loc, scan_tmp, nullptr);
+    for (int q = 0; q < per; ++q) {
+      const int d = threadIdx.x * per + q;
+      if (d < radix) {
+        digit_base[d] = e + hist[(int64_t)d * nblocks + blockIdx.x];
+        e += totals[d];
+      }
+    }
   }
-  for (int d = threadIdx.x; d < kSortWarps * kRadix; d += blockDim.x) (&warp_cnt[0][0])[d] = 0;
+  for (int d = threadIdx.x; d < kSortWarps * radix; d += blockDim.x) warp_cnt[d] = 0;
   __syncthreads();
 
   // warp w ranks its contiguous sub-chunk in order, 32 items per round
@@ -199,9 +215,9 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
     uint32_t d = (key >> shift) & mask;
     unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
     uint32_t rank = 0;
-    if (valid) rank = warp_cnt[warp][d] + __popc(peers & lt);
+    if (valid) rank = warp_cnt[warp * radix + d] + __popc(peers & lt);
     __syncwarp();
-    if (valid && (peers & lt) == 0) warp_cnt[warp][d] += __popc(peers);
+    if (valid && (peers & lt) == 0) warp_cnt[warp * radix + d] += __popc(peers);
     __syncwarp();
     k_reg[r] = key;
     v_reg[r] = val;
@@ -209,12 +225,12 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
   }
   __syncthreads();
   // exclusive scan across warps per digit
-  for (int d = threadIdx.x; d < kRadix; d += blockDim.x) {
+  for (int d = threadIdx.x; d < radix; d += blockDim.x) {
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) {
-      uint32_t c = warp_cnt[w][d];
-      warp_cnt[w][d] = run;
+      uint32_t c = warp_cnt[w * radix + d];
+      warp_cnt[w * radix + d] = run;
       run += c;
     }
   }
@@ -223,7 +239,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
   for (int r = 0; r < kSortIPT; ++r) {
     if (r_reg[r] == 0xFFFFFFFFu) continue;
     uint32_t d = (k_reg[r] >> shift) & mask;
-    uint32_t pos = digit_base[d] + warp_cnt[warp][d] + r_reg[r];
+    uint32_t pos = digit_base[d] + warp_cnt[warp * radix + d] + r_reg[r];
     keys_out[pos] = k_reg[r];
     vals_out[pos] = v_reg[r];
   }
@@ -231,25 +247,40 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(
 
 size_t radix_scratch_bytes(int64_t cap) {
   int64_t nb = ceil_div(cap > 0 ? cap : 1, kSortChunk);
-  return (size_t)(nb * kRadix + kRadix) * sizeof(uint32_t) + 256;
+  return (size_t)(nb * kMaxRadix + kMaxRadix) * sizeof(uint32_t) + 256;
 }
 
+// Digits of at most kMaxRadixBits, passes balanced: 32 bits -> 11+11+10,
+// 11 tile bits (1280 tiles) -> one pass.
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
                      int begin_bit, int end_bit, void* scratch, cudaStream_t stream) {
   int cur = 0;
   if (cap <= 0 || end_bit <= begin_bit) return cur;
   int nb = (int)ceil_div(cap, kSortChunk);
   uint32_t* hist = (uint32_t*)scratch;
-  uint32_t* totals = hist + (int64_t)nb * kRadix;
-  for (int shift = begin_bit; shift < end_bit; shift += kRadixBits) {
-    int nbits = end_bit - shift < kRadixBits ? end_bit - shift : kRadixBits;
+  uint32_t* totals = hist + (int64_t)nb * kMaxRadix;
+  const int bits = end_bit - begin_bit;
+  const int passes = (bits + kMaxRadixBits - 1) / kMaxRadixBits;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((kSortWarps + 1) * kMaxRadix * sizeof(uint32_t)));
+    attr_set = true;
+  }
+  int shift = begin_bit;
+  for (int p = 0; p < passes; ++p) {
+    const int nbits = (bits - (shift - begin_bit) + (passes - p) - 1) / (passes - p);
+    const int radix = 1 << nbits;
     k_radix_hist<<<nb, kSortThreads, 0, stream>>>(keys[cur], cap, n_dev, shift, nbits, hist, nb);
-    k_radix_scan_digit<<<kRadix, 256, 0, stream>>>(hist, nb, totals);
-    k_radix_scatter<<<nb, kSortThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1],
-                                                     cap, n_dev, shift, nbits, hist, totals, nb);
+    k_radix_scan_digit<<<radix, 256, 0, stream>>>(hist, nb, totals);
+    k_radix_scatter<<<nb, kSortThreads, (kSortWarps + 1) * radix * sizeof(uint32_t), stream>>>(
+        keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], cap, n_dev, shift, nbits, hist, totals, nb);
     cur ^= 1;
+    shift += nbits;
   }
   return cur;
 }
+
+int radix_passes(int bits) { return (bits + kMaxRadixBits - 1) / kMaxRadixBits; }
 
 }  // namespace fs4d

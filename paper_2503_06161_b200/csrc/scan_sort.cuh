@@ -17,10 +17,10 @@ constexpr int kScanChunk = kScanThreads * kScanIPT;
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortIPT = 8;
+constexpr int kSortIPT = 4;
 constexpr int kSortChunk = kSortThreads * kSortIPT;
-constexpr int kRadixBits = 8;
-constexpr int kRadix = 1 << kRadixBits;
+constexpr int kMaxRadixBits = 11;
+constexpr int kMaxRadix = 1 << kMaxRadixBits;
 
 size_t scan_scratch_bytes(int64_t cap);
 // out[i] = sum_{j<i} in[j] for i < n; *total = sum of all n.  n = min(*n_dev, cap)
@@ -34,5 +34,7 @@ size_t radix_scratch_bytes(int64_t cap);
 // between buffer 0 and 1; returns the index holding the result.
 int radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t cap, const uint32_t* n_dev,
                      int begin_bit, int end_bit, void* scratch, cudaStream_t stream);
+// number of passes (and so ping-pong flips) radix_sort_pairs makes over `bits` key bits
+int radix_passes(int bits);
 
 }  // namespace fs4d
