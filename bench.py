@@ -410,15 +410,11 @@ def train_bench(args, rank, world, local):
     return dict(ms=ms, prof=prof, loss=float(step.loss.item()), grad_floats=step.grads.numel, pairs=pairs)
 
 
-def launches_per_frame(tile_bits=11):
+def launches_per_frame():
     """libfs4d kernels per frame: deform (pack, HexPlane latent, tcgen05 MLP) and
-    render (status reset, preprocess, 3 kernels per radix pass, tie fix-up,
-    tile count, 3-kernel scan, pair check, emit, tile ranges, blend)."""
-    deform = 3
-    sort_passes = -(-32 // 11)
-    pair_passes = -(-tile_bits // 11)
-    render = 1 + 1 + 3 * sort_passes + 1 + 1 + 3 + 1 + 1 + 3 * pair_passes + 1 + 1
-    return deform + render
+    render (status reset, preprocess, tile histogram, 3-kernel scan, pair
+    check, partition, per-tile sort, blend)."""
+    return 3 + (1 + 1 + 1 + 3 + 1 + 1 + 1 + 1)
 
 
 def main():

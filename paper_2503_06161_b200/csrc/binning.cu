@@ -1,0 +1,303 @@
+// Tile binning without a global sort (bin_tiles, rasterizer.py:188-207, and the
+// stable depth argsort it relies on, rasterizer.py:163).
+//
+//   k_tile_hist       per-tile pair counts (block-aggregated in shared memory)
+//   scan              tile offsets (device-wide exclusive scan)
+//   k_emit_partition  every (tile, Gaussian) pair lands in its tile's segment;
+//                     block-level reservation, order inside a segment arbitrary
+//   k_tile_sort       one CTA per tile sorts its segment by (fp32 depth bits,
+//                     exact fp64 depth on ties, source index) — the reference's
+//                     stable float64 argsort order — with a bitonic network in
+//                     shared memory (global memory for oversized tiles) and
+//                     writes the tile range and the sorted source indices.
+#include "render_common.cuh"
+
+namespace fs4d {
+
+constexpr int kHistMaxTiles = 6144;   // shared-memory histogram capacity (24 KB)
+constexpr int kSortSmemKeys = 8192;   // per-tile keys sorted in shared memory (64 KB)
+constexpr int kTileSortThreads = 512;
+
+__device__ __forceinline__ bool rect_valid(const int4& t) { return t.y >= t.x && t.w >= t.z; }
+
+__global__ void __launch_bounds__(256) k_tile_hist(const int4* __restrict__ tile_rect, const uint32_t* __restrict__ dkeys,
+                                                   int64_t K, int ntx, int ntiles, uint32_t* __restrict__ tcnt) {
+  __shared__ uint32_t h[kHistMaxTiles];
+  const bool smem = ntiles <= kHistMaxTiles;
+  if (smem)
+    for (int b = threadIdx.x; b < ntiles; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < K && dkeys[i] != 0xFFFFFFFFu) {
+    const int4 t = tile_rect[i];
+    for (int ty = t.z; ty <= t.w; ++ty)
+      for (int tx = t.x; tx <= t.y; ++tx) {
+        const int b = ty * ntx + tx;
+        if (smem) atomicAdd(&h[b], 1u);
+        else atomicAdd(&tcnt[b], 1u);
+      }
+  }
+  __syncthreads();
+  if (smem)
+    for (int b = threadIdx.x; b < ntiles; b += blockDim.x)
+      if (h[b]) atomicAdd(&tcnt[b], h[b]);
+}
+
+// key = fp32 depth bits (positive floats order as unsigned) << 32 | source index
+__global__ void __launch_bounds__(256) k_emit_partition(const int4* __restrict__ tile_rect,
+                                                        const uint32_t* __restrict__ dkeys, int64_t K, int ntx,
+                                                        int ntiles, const uint64_t* __restrict__ toff,
+                                                        uint32_t* __restrict__ tcur, int64_t cap,
+                                                        unsigned long long* __restrict__ pkey) {
+  __shared__ uint32_t cnt[kHistMaxTiles];
+  __shared__ uint32_t base[kHistMaxTiles];
+  const bool smem = ntiles <= kHistMaxTiles;
+  if (smem)
+    for (int b = threadIdx.x; b < ntiles; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool kept = i < K && dkeys[i] != 0xFFFFFFFFu;
+  int4 t = make_int4(0, -1, 0, -1);
+  if (kept) t = tile_rect[i];
+  if (smem && kept)
+    for (int ty = t.z; ty <= t.w; ++ty)
+      for (int tx = t.x; tx <= t.y; ++tx) atomicAdd(&cnt[ty * ntx + tx], 1u);
+  __syncthreads();
+  if (smem)
+    for (int b = threadIdx.x; b < ntiles; b += blockDim.x) {
+      const uint32_t c = cnt[b];
+      base[b] = c ? atomicAdd(&tcur[b], c) : 0u;  // reserve this block's slice of the segment
+      cnt[b] = 0;
+    }
+  __syncthreads();
+  if (!kept) return;
+  const unsigned long long key = ((unsigned long long)dkeys[i] << 32) | (unsigned long long)i;
+  for (int ty = t.z; ty <= t.w; ++ty)
+    for (int tx = t.x; tx <= t.y; ++tx) {
+      const int b = ty * ntx + tx;
+      const uint32_t local = smem ? base[b] + atomicAdd(&cnt[b], 1u) : atomicAdd(&tcur[b], 1u);
+      const uint64_t o = toff[b] + local;
+      if (o < (uint64_t)cap) pkey[o] = key;
+    }
+}
+
+// (depth bits, exact fp64 depth, source index) ordering
+__device__ __forceinline__ bool key_less(unsigned long long a, unsigned long long b, const double* __restrict__ z64) {
+  const uint32_t ha = (uint32_t)(a >> 32), hb = (uint32_t)(b >> 32);
+  if (ha != hb) return ha < hb;
+  const uint32_t ia = (uint32_t)a, ib = (uint32_t)b;
+  if (ia == ib) return false;
+  if (ha == 0xFFFFFFFFu) return ia < ib;  // padding
+  const double za = z64[ia], zb = z64[ib];
+  if (za != zb) return za < zb;
+  return ia < ib;
+}
+
+// Bitonic sort of keys[0..n) (virtual +inf padding to a power of two) with
+// the all-ascending formulation: every compare-exchange moves the smaller key
+// to the lower index, so virtual elements never move into [0, n).
+__device__ void bitonic_sort(unsigned long long* keys, int n, const double* __restrict__ z64) {
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int k = 2; k <= p2; k <<= 1) {
+    // first step of the merge: compare i with its mirror in the k-block
+    for (int q = threadIdx.x; q < p2 / 2; q += blockDim.x) {
+      const int blk = q / (k / 2), off = q % (k / 2);
+      const int lo = blk * k + off, hi = blk * k + k - 1 - off;
+      if (hi < n) {
+        const unsigned long long a = keys[lo], b = keys[hi];
+        if (key_less(b, a, z64)) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+    }
+    __syncthreads();
+    for (int j = k / 4; j >= 1; j >>= 1) {
+      for (int q = threadIdx.x; q < p2 / 2; q += blockDim.x) {
+        const int lo = (q / j) * 2 * j + (q % j), hi = lo + j;
+        if (hi < n) {
+          const unsigned long long a = keys[lo], b = keys[hi];
+          if (key_less(b, a, z64)) {
+            keys[lo] = b;
+            keys[hi] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+constexpr int kTileSortWarps = kTileSortThreads / 32;
+constexpr int kTileSortIPT = kSortSmemKeys / kTileSortThreads;  // 16 items per thread
+
+// CTA-wide stable LSD radix sort of up to kSortSmemKeys (depth bits, source
+// index) pairs held in registers ("striped": lane l of warp w owns items
+// w*32*IPT + r*32 + l), 8-bit digits, shared memory only for counters and the
+// exchange buffer.  Then equal-depth-bit runs (rare) are re-ordered by the
+// exact fp64 depth and the source index.
+__device__ void cta_radix_sort_tile(const unsigned long long* __restrict__ src, int n, const double* __restrict__ z64,
+                                    uint32_t* __restrict__ out_vals, unsigned long long* xbuf, uint32_t* wcnt,
+                                    uint32_t* dbase) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  // R rounds of 32 items per warp cover n (R <= kTileSortIPT, uniform per CTA)
+  const int R = (n + kTileSortThreads - 1) / kTileSortThreads;
+  uint32_t key[kTileSortIPT], val[kTileSortIPT];
+#pragma unroll
+  for (int r = 0; r < kTileSortIPT; ++r) {
+    const int q = warp * 32 * R + r * 32 + lane;
+    const unsigned long long kv = (r < R && q < n) ? src[q] : 0xFFFFFFFFFFFFFFFFull;
+    key[r] = (uint32_t)(kv >> 32);
+    val[r] = (uint32_t)kv;
+  }
+  for (int shift = 0; shift < 32; shift += 8) {
+    for (int d = threadIdx.x; d < kTileSortWarps * 256; d += blockDim.x) wcnt[d] = 0;
+    __syncthreads();
+    uint32_t rank[kTileSortIPT];
+#pragma unroll
+    for (int r = 0; r < kTileSortIPT; ++r) {
+      if (r >= R) break;
+      const uint32_t d = (key[r] >> shift) & 0xFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      rank[r] = wcnt[warp * 256 + d] + __popc(peers & lt);
+      __syncwarp();
+      if ((peers & lt) == 0) wcnt[warp * 256 + d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // digit totals -> exclusive digit bases; per-digit warp prefixes in place
+    if (threadIdx.x < 256) {
+      const int d = threadIdx.x;
+      uint32_t run = 0;
+#pragma unroll
+      for (int w = 0; w < kTileSortWarps; ++w) {
+        const uint32_t c = wcnt[w * 256 + d];
+        wcnt[w * 256 + d] = run;
+        run += c;
+      }
+      dbase[d] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of 256 digit totals by one warp
+      uint32_t v[8], s = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        v[q] = dbase[lane * 8 + q];
+        s += v[q];
+      }
+      uint32_t incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t run = incl - s;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        dbase[lane * 8 + q] = run;
+        run += v[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kTileSortIPT; ++r) {
+      if (r >= R) break;
+      const uint32_t d = (key[r] >> shift) & 0xFFu;
+      const uint32_t pos = dbase[d] + wcnt[warp * 256 + d] + rank[r];
+      xbuf[pos] = ((unsigned long long)key[r] << 32) | val[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kTileSortIPT; ++r) {
+      if (r >= R) break;
+      const unsigned long long kv = xbuf[warp * 32 * R + r * 32 + lane];
+      key[r] = (uint32_t)(kv >> 32);
+      val[r] = (uint32_t)kv;
+    }
+  }
+  // xbuf holds the sorted sequence; fix equal-depth-bit runs, then emit
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    const uint32_t k = (uint32_t)(xbuf[q] >> 32);
+    const bool start = (q == 0 || (uint32_t)(xbuf[q - 1] >> 32) != k) && q + 1 < n && (uint32_t)(xbuf[q + 1] >> 32) == k;
+    if (!start) continue;
+    int e = q + 1;
+    while (e < n && (uint32_t)(xbuf[e] >> 32) == k) ++e;
+    for (int a = q + 1; a < e; ++a) {
+      const unsigned long long ka = xbuf[a];
+      int b = a - 1;
+      while (b >= q && key_less(ka, xbuf[b], z64)) {
+        xbuf[b + 1] = xbuf[b];
+        --b;
+      }
+      xbuf[b + 1] = ka;
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < n; q += blockDim.x) out_vals[q] = (uint32_t)xbuf[q];
+}
+
+__global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long long* __restrict__ pkey,
+                                                                const uint64_t* __restrict__ toff,
+                                                                const uint32_t* __restrict__ tcnt, int ntiles,
+                                                                int64_t cap, const double* __restrict__ z64,
+                                                                uint32_t* __restrict__ pvals, uint2* __restrict__ ranges) {
+  extern __shared__ unsigned long long s_keys[];  // kSortSmemKeys exchange buffer (dynamic, 64 KB)
+  __shared__ uint32_t wcnt[kTileSortWarps * 256];
+  __shared__ uint32_t dbase[256];
+  const int tile = blockIdx.x;
+  const uint64_t off = toff[tile];
+  uint64_t end = off + tcnt[tile];
+  if (end > (uint64_t)cap) end = (uint64_t)cap;  // overflow frame: status already raised
+  const int n = off < end ? (int)(end - off) : 0;
+  if (threadIdx.x == 0) ranges[tile] = make_uint2((uint32_t)off, (uint32_t)(off + n));
+  if (n == 0) return;
+  unsigned long long* keys = pkey + off;
+  if (n <= kSortSmemKeys) {
+    cta_radix_sort_tile(keys, n, z64, pvals + off, s_keys, wcnt, dbase);
+  } else {
+    bitonic_sort(keys, n, z64);  // oversized tile: in place in global memory (L2-resident)
+    for (int q = threadIdx.x; q < n; q += blockDim.x) pvals[off + q] = (uint32_t)keys[q];
+  }
+}
+
+__global__ void k_pairs_check2(uint32_t* counters, int64_t cap, int32_t* status) {
+  const uint64_t total = *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64);
+  counters[CNT_PAIRS_CLAMPED] = (uint32_t)(total < (uint64_t)cap ? total : (uint64_t)cap);
+  if (status) {
+    status[FS4D_ST_N_VISIBLE] = (int32_t)counters[CNT_VISIBLE];
+    status[FS4D_ST_PAIRS_LO] = (int32_t)(total & 0xFFFFFFFFu);
+    status[FS4D_ST_PAIRS_HI] = (int32_t)(total >> 32);
+    if (total > (uint64_t)cap) raise_status(status, FS4D_ERR_CAPACITY);
+  }
+}
+
+// host: the whole binning stage (counts -> offsets -> partition -> per-tile sort)
+void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, const uint32_t* dkeys,
+                      const double* z64, uint32_t* counters, int32_t* status, cudaStream_t s) {
+  const int64_t K = L.K;
+  uint32_t* tcnt = at<uint32_t>(ws, L.tcnt);
+  uint32_t* tcur = at<uint32_t>(ws, L.tcur);
+  uint64_t* toff = at<uint64_t>(ws, L.toff64);
+  cudaMemsetAsync(tcnt, 0, (size_t)L.ntiles * 4, s);
+  cudaMemsetAsync(tcur, 0, (size_t)L.ntiles * 4, s);
+  const unsigned gb = (unsigned)ceil_div(K > 0 ? K : 1, 256);
+  if (K > 0) k_tile_hist<<<gb, 256, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles, tcnt);
+  exclusive_scan_u32_to_u64(tcnt, toff, L.ntiles, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64),
+                            at<void>(ws, L.scratch), s);
+  k_pairs_check2<<<1, 1, 0, s>>>(counters, L.cap, status);
+  unsigned long long* pkey = at<unsigned long long>(ws, L.pkey64);
+  if (K > 0) k_emit_partition<<<gb, 256, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles, toff, tcur, L.cap, pkey);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmemKeys * 8);
+    attr = true;
+  }
+  if (L.ntiles > 0)
+    k_tile_sort<<<L.ntiles, kTileSortThreads, kSortSmemKeys * 8, s>>>(pkey, toff, tcnt, L.ntiles, L.cap, z64,
+                                                                     at<uint32_t>(ws, L.pvals0),
+                                                                     at<uint2>(ws, L.ranges));
+}
+
+}  // namespace fs4d

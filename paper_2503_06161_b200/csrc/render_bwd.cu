@@ -423,7 +423,7 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   b.bg1 = (float)cfg.background[1];
   b.bg2 = (float)cfg.background[2];
   b.ranges = at<uint2>(ws, L.ranges);
-  b.pvals = at<uint32_t>(ws, L.pair_final ? L.pvals1 : L.pvals0);
+  b.pvals = at<uint32_t>(ws, L.pvals0);
   b.xy = at<float2>(ws, L.xy);
   b.conic_o = at<float4>(ws, L.conic_o);
   b.pix_rect = at<int4>(ws, L.pix_rect);
@@ -458,7 +458,7 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   p.D = D;
   p.acc_stride = L.acc_stride;
   p.sh_degree = snap.sh_degree;
-  p.order = at<uint32_t>(ws, L.depth_final ? L.dvals1 : L.dvals0);
+  p.order = depth_order(L, ws, s);  // viewspace statistics are reported in depth order
   p.counters = at<uint32_t>(ws, L.counters);
   p.accum = accum;
   p.clamp_mask = at<uint32_t>(ws, L.clamp_mask);

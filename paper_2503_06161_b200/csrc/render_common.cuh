@@ -17,12 +17,16 @@ constexpr float kQSkip = 11.0825270270270f;  // 2 ln 255 (rasterizer.py:212)
 struct RenderLayout {
   int64_t K = 0, cap = 0;
   int H = 0, W = 0, D = 0, ntx = 0, nty = 0, ntiles = 0, tile_bits = 0, acc_stride = 0;
-  int depth_final = 0, pair_final = 0;
-  // per Gaussian (source-indexed unless noted)
-  size_t xy, conic_o, pix_rect, tile_rect, rgbz, cov_r, z64, dkeys0, dkeys1, dvals0, dvals1,
-      tcount /*by rank*/, toff /*by rank*/, rank_of, clamp_mask;
-  // tiles / pairs / pixels
-  size_t ranges, pkeys0, pkeys1, pvals0, pvals1, tfinal, last;
+  int depth_final = 0;
+  // per Gaussian (source-indexed): projected record, fp64 depth, depth-sort
+  // keys/values (the global order is only materialised for export/backward)
+  size_t xy, conic_o, pix_rect, tile_rect, rgbz, cov_r, z64, dkeys0, dkeys1, dvals0, dvals1, rank_of, clamp_mask;
+  // tiles: counts, append cursors, segment offsets, [start, end) ranges
+  size_t tcnt, tcur, toff64, ranges;
+  // pairs: 64-bit (depth bits, source index) keys and the sorted source indices
+  size_t pkey64, pvals0;
+  // pixels
+  size_t tfinal, last;
   // counters and scratch
   size_t counters, scratch, scratch_bytes;
   // backward accumulators [K, acc_stride]
@@ -48,9 +52,8 @@ inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
   int bits = 0;
   while ((1ll << bits) < (int64_t)L.ntiles) ++bits;
   L.tile_bits = bits;
-  // ping-pong parity after the radix passes (32-bit depth keys, tile-id keys)
+  // ping-pong parity after the radix passes over 32-bit depth keys
   L.depth_final = (int)(ceil_div(32, kMaxRadixBits) & 1);
-  L.pair_final = (int)(ceil_div(bits, kMaxRadixBits) & 1);
   L.acc_stride = (int)ceil_div(10 + L.D, 32) * 32;
   const int64_t K = L.K > 0 ? L.K : 1;
   const int64_t cap = L.cap > 0 ? L.cap : 1;
@@ -72,19 +75,19 @@ inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
   L.dkeys1 = take(K * 4);
   L.dvals0 = take(K * 4);
   L.dvals1 = take(K * 4);
-  L.tcount = take(K * 4);
-  L.toff = take(K * 8);
   L.rank_of = take(K * 4);
   L.clamp_mask = take(K * 4);
-  L.ranges = take((size_t)(L.ntiles > 0 ? L.ntiles : 1) * 8);
-  L.pkeys0 = take(cap * 4);
-  L.pkeys1 = take(cap * 4);
+  const int64_t nt = L.ntiles > 0 ? L.ntiles : 1;
+  L.tcnt = take(nt * 4);
+  L.tcur = take(nt * 4);
+  L.toff64 = take(nt * 8);
+  L.ranges = take(nt * 8);
+  L.pkey64 = take(cap * 8);
   L.pvals0 = take(cap * 4);
-  L.pvals1 = take(cap * 4);
   L.tfinal = take(npix * 4);
   L.last = take(npix * 4);
   L.counters = take(CNT_WORDS * 4);
-  size_t s1 = scan_scratch_bytes(K), s2 = radix_scratch_bytes(K > cap ? K : cap);
+  size_t s1 = scan_scratch_bytes(K > nt ? K : nt), s2 = radix_scratch_bytes(K);
   L.scratch_bytes = s1 > s2 ? s1 : s2;
   L.scratch = take(L.scratch_bytes);
   L.accum = take((size_t)K * L.acc_stride * 4);
@@ -96,5 +99,11 @@ template <typename T>
 __host__ __device__ inline T* at(void* base, size_t off) {
   return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + off);
 }
+
+// binning.cu: per-tile pair segments sorted by (depth, index) -> ranges + pvals0
+void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, const uint32_t* dkeys,
+                      const double* z64, uint32_t* counters, int32_t* status, cudaStream_t s);
+// render_fwd.cu: global stable depth order of the visible set (export / backward)
+const uint32_t* depth_order(const RenderLayout& L, void* ws, cudaStream_t s);
 
 }  // namespace fs4d

@@ -227,85 +227,6 @@ __global__ void k_depth_tie_fixup(const uint32_t* __restrict__ keys, uint32_t* _
   }
 }
 
-__global__ void k_tile_count(const uint32_t* __restrict__ order, const int4* __restrict__ tile_rect, int64_t K,
-                             const uint32_t* counters, uint32_t* __restrict__ tcount, int32_t* __restrict__ rank_of) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= K) return;
-  const uint32_t i = order[r];
-  rank_of[i] = (int32_t)r;
-  uint32_t n = 0;
-  if (r < (int64_t)counters[CNT_VISIBLE]) {
-    int4 t = tile_rect[i];
-    n = (uint32_t)((t.y - t.x + 1) * (t.w - t.z + 1));
-  }
-  tcount[r] = n;
-}
-
-__global__ void k_pairs_check(uint32_t* counters, int64_t cap, int32_t* status) {
-  uint64_t total = *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64);
-  uint32_t clamped = (uint32_t)(total < (uint64_t)cap ? total : (uint64_t)cap);
-  counters[CNT_PAIRS_CLAMPED] = clamped;
-  if (status) {
-    status[FS4D_ST_N_VISIBLE] = (int32_t)counters[CNT_VISIBLE];
-    status[FS4D_ST_PAIRS_LO] = (int32_t)(total & 0xFFFFFFFFu);
-    status[FS4D_ST_PAIRS_HI] = (int32_t)(total >> 32);
-    if (total > (uint64_t)cap) raise_status(status, FS4D_ERR_CAPACITY);
-  }
-}
-
-// one thread per Gaussian (depth rank r); rectangles larger than 16 tiles are
-// emitted cooperatively by the whole warp so one huge footprint does not
-// serialise a lane
-__global__ void k_emit_pairs(const uint32_t* __restrict__ order, const int4* __restrict__ tile_rect,
-                             const uint64_t* __restrict__ toff, const uint32_t* counters, int64_t cap, int ntx,
-                             uint32_t* __restrict__ pkeys, uint32_t* __restrict__ pvals) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int64_t M = counters[CNT_VISIBLE];
-  uint32_t i = 0;
-  int4 t = make_int4(0, -1, 0, -1);
-  uint64_t base = 0;
-  if (r < M) {
-    i = order[r];
-    t = tile_rect[i];
-    base = toff[r];
-  }
-  const int w = t.y - t.x + 1, area = w * (t.w - t.z + 1);
-  const bool big = r < M && area > 16;
-  if (r < M && !big) {
-    for (int k = 0; k < area; ++k) {
-      const uint64_t o = base + (uint64_t)k;
-      if (o >= (uint64_t)cap) break;
-      pkeys[o] = (uint32_t)((t.z + k / w) * ntx + t.x + k % w);
-      pvals[o] = i;
-    }
-  }
-  unsigned todo = __ballot_sync(0xffffffffu, big);
-  while (todo) {
-    const int src = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const uint32_t gi = __shfl_sync(0xffffffffu, i, src);
-    const int tx0 = __shfl_sync(0xffffffffu, t.x, src), tz0 = __shfl_sync(0xffffffffu, t.z, src);
-    const int gw = __shfl_sync(0xffffffffu, w, src), ga = __shfl_sync(0xffffffffu, area, src);
-    const uint64_t gb = __shfl_sync(0xffffffffu, base, src);
-    for (int k = lane; k < ga; k += 32) {
-      const uint64_t o = gb + (uint64_t)k;
-      if (o >= (uint64_t)cap) break;
-      pkeys[o] = (uint32_t)((tz0 + k / gw) * ntx + tx0 + k % gw);
-      pvals[o] = gi;
-    }
-  }
-}
-
-__global__ void k_tile_ranges(const uint32_t* __restrict__ pkeys, const uint32_t* counters, uint2* __restrict__ ranges) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = counters[CNT_PAIRS_CLAMPED];
-  if (p >= n) return;
-  const uint32_t t = pkeys[p];
-  if (p == 0 || pkeys[p - 1] != t) ranges[t].x = (uint32_t)p;
-  if (p == n - 1 || pkeys[p + 1] != t) ranges[t].y = (uint32_t)(p + 1);
-}
-
 struct BlendArgs {
   int H, W, ntx, D, c0;
   float alpha_cap, alpha_skip, stop;
@@ -528,36 +449,11 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
     if (K > 0) k_preprocess<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(p);
   }
 
-  // stable global depth order (culled rows carry key 0xFFFFFFFF and sort last)
-  uint32_t* dk[2] = {at<uint32_t>(ws, L.dkeys0), at<uint32_t>(ws, L.dkeys1)};
-  uint32_t* dv[2] = {at<uint32_t>(ws, L.dvals0), at<uint32_t>(ws, L.dvals1)};
-  void* scratch = at<void>(ws, L.scratch);
-  int df;
+  // tile binning + per-tile depth order (no global sort on the frame path)
   {
-    StageTimer st(FS4D_STAGE_DEPTH_SORT, s);
-    df = radix_sort_pairs(dk, dv, K, nullptr, 0, 32, scratch, s);
-    if (K > 0) k_depth_tie_fixup<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dk[df], dv[df], p.z64, K, counters);
+    StageTimer st(FS4D_STAGE_BINNING, s);
+    bin_tiles_device(L, ws, p.tile_rect, p.dkeys, p.z64, counters, status, s);
   }
-  const uint32_t* order = dv[df];
-  StageTimer st_bin(FS4D_STAGE_BINNING, s);
-
-  // tile binning: count -> scan -> emit -> stable sort by tile -> ranges
-  uint32_t* tcount = at<uint32_t>(ws, L.tcount);
-  uint64_t* toff = at<uint64_t>(ws, L.toff);
-  if (K > 0)
-    k_tile_count<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, p.tile_rect, K, counters, tcount,
-                                                             at<int32_t>(ws, L.rank_of));
-  exclusive_scan_u32_to_u64(tcount, toff, K, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64), scratch, s);
-  k_pairs_check<<<1, 1, 0, s>>>(counters, L.cap, status);
-  uint32_t* pk[2] = {at<uint32_t>(ws, L.pkeys0), at<uint32_t>(ws, L.pkeys1)};
-  uint32_t* pv[2] = {at<uint32_t>(ws, L.pvals0), at<uint32_t>(ws, L.pvals1)};
-  if (K > 0)
-    k_emit_pairs<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(order, p.tile_rect, toff, counters, L.cap, L.ntx,
-                                                                  pk[0], pv[0]);
-  int pf = radix_sort_pairs(pk, pv, L.cap, counters + CNT_PAIRS_CLAMPED, 0, L.tile_bits, scratch, s);
-  if (L.cap > 0)
-    k_tile_ranges<<<(unsigned)ceil_div(L.cap, 256), 256, 0, s>>>(pk[pf], counters, at<uint2>(ws, L.ranges));
-  st_bin.stop();
 
   // blend
   BlendArgs b;
@@ -572,7 +468,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   b.bg1 = (float)cfg.background[1];
   b.bg2 = (float)cfg.background[2];
   b.ranges = at<uint2>(ws, L.ranges);
-  b.pvals = pv[pf];
+  b.pvals = at<uint32_t>(ws, L.pvals0);
   b.xy = p.xy;
   b.conic_o = p.conic_o;
   b.pix_rect = p.pix_rect;
@@ -624,8 +520,36 @@ __global__ void k_export_projected(const uint32_t* __restrict__ order, const uin
   }
 }
 
+// Global stable depth order of the visible set (np.argsort(z, stable),
+// rasterizer.py:163) for the record's consumers that need it
+// (ProjectedGaussians export, viewspace statistics of the backward):
+// radix sort of the fp32 depth bits + fp64 tie fix-up + inverse permutation.
+// Idempotent: re-sorting an already sorted sequence is stable.
+__global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t K, int32_t* __restrict__ rank_of) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < K) rank_of[order[r]] = (int32_t)r;
+}
+
+const uint32_t* depth_order(const RenderLayout& L, void* ws, cudaStream_t s) {
+  const int64_t K = L.K;
+  uint32_t* dk[2] = {at<uint32_t>(ws, L.dkeys0), at<uint32_t>(ws, L.dkeys1)};
+  uint32_t* dv[2] = {at<uint32_t>(ws, L.dvals0), at<uint32_t>(ws, L.dvals1)};
+  StageTimer st(FS4D_STAGE_DEPTH_SORT, s);
+  const int df = radix_sort_pairs(dk, dv, K, nullptr, 0, 32, at<void>(ws, L.scratch), s);
+  if (df != 0 && K > 0) {  // keep the sorted sequence in buffer 0 so repeated calls are stable
+    cudaMemcpyAsync(dk[0], dk[1], (size_t)K * 4, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(dv[0], dv[1], (size_t)K * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  if (K > 0) {
+    k_depth_tie_fixup<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dk[0], dv[0], at<double>(ws, L.z64), K,
+                                                                 at<uint32_t>(ws, L.counters));
+    k_rank_of<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dv[0], K, at<int32_t>(ws, L.rank_of));
+  }
+  return dv[0];
+}
+
 int render_export_projected(const RenderLayout& L, void* ws, Fs4dProjected& out, cudaStream_t s) {
-  uint32_t* dv = at<uint32_t>(ws, L.depth_final ? L.dvals1 : L.dvals0);
+  const uint32_t* dv = depth_order(L, ws, s);
   if (L.K > 0)
     k_export_projected<<<(unsigned)ceil_div(L.K, 256), 256, 0, s>>>(
         dv, at<uint32_t>(ws, L.counters), L.K, at<float2>(ws, L.xy), at<float4>(ws, L.conic_o),
@@ -643,10 +567,11 @@ __global__ void k_export_pairs(const uint32_t* __restrict__ pvals, const int32_t
 int render_export_tiles(const RenderLayout& L, void* ws, int32_t* ranges, int32_t* rows, int64_t max_pairs,
                         cudaStream_t s) {
   if (ranges) cudaMemcpyAsync(ranges, at<void>(ws, L.ranges), (size_t)L.ntiles * 8, cudaMemcpyDeviceToDevice, s);
-  if (rows && max_pairs > 0)
+  if (rows && max_pairs > 0) {
+    depth_order(L, ws, s);  // rank_of
     k_export_pairs<<<(unsigned)ceil_div(max_pairs, 256), 256, 0, s>>>(
-        at<uint32_t>(ws, L.pair_final ? L.pvals1 : L.pvals0), at<int32_t>(ws, L.rank_of),
-        at<uint32_t>(ws, L.counters), rows, max_pairs);
+        at<uint32_t>(ws, L.pvals0), at<int32_t>(ws, L.rank_of), at<uint32_t>(ws, L.counters), rows, max_pairs);
+  }
   return check_launch("render_export_tiles");
 }
 

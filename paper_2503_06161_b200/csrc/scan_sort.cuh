@@ -17,9 +17,9 @@ constexpr int kScanChunk = kScanThreads * kScanIPT;
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortIPT = 4;
+constexpr int kSortIPT = 8;
 constexpr int kSortChunk = kSortThreads * kSortIPT;
-constexpr int kMaxRadixBits = 11;
+constexpr int kMaxRadixBits = 8;  // measured: 11-bit digits cost more per pass than they save in passes
 constexpr int kMaxRadix = 1 << kMaxRadixBits;
 
 size_t scan_scratch_bytes(int64_t cap);
