@@ -539,3 +539,56 @@ class FramePipeline:
                 if n != "n_contrib":
                     dst.copy_(self.images[n], non_blocking=True)
         return self.images
+
+
+class StreamedFrames:
+    """End-to-end frame stream from host buffers with copy/compute overlap.
+
+    Two FramePipeline replicas (own device cloud copy, render record and
+    images) alternate over two CUDA streams, so frame i+1's host->device copy
+    of the canonical cloud and frame i-1's device->host copy of the images run
+    on the copy engines while frame i computes.  Every frame still performs
+    its full H2D and D2H.
+    """
+
+    def __init__(self, cloud, field, net, height, width, cfg, device="cuda"):
+        self.pipes = []
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(2)]
+        for p in range(2):
+            c = cloud if p == 0 else DeviceCloud(*(getattr(cloud, n).clone() for n in DeviceCloud.FIELDS),
+                                                 sh_rest=None if cloud.sh_rest is None else cloud.sh_rest.clone())
+            self.pipes.append(FramePipeline(c, field, net, height, width, cfg, device))
+        self.host_in, out0 = self.pipes[0].pinned_host_buffers()
+        _, out1 = self.pipes[1].pinned_host_buffers()
+        self.host_out = [out0, out1]
+
+    def warm(self, t, K, T):
+        for p, pipe in enumerate(self.pipes):
+            with torch.cuda.stream(self.streams[p]):
+                pipe.run(t, K, T, check=True)
+                pipe.run(t, K, T, host_in=self.host_in, host_out=self.host_out[p])
+        torch.cuda.synchronize()
+
+    def run(self, ts, K, T):
+        """Enqueue one frame per t; returns (start_event, end_event) on the
+        current stream bracketing the whole stream of frames."""
+        cur = torch.cuda.current_stream()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(cur)
+        for s in self.streams:
+            s.wait_event(start)
+        for i, t in enumerate(ts):
+            p = i % 2
+            with torch.cuda.stream(self.streams[p]):
+                self.pipes[p].run(float(t), K, T, host_in=self.host_in, host_out=self.host_out[p])
+        for s in self.streams:
+            cur.wait_stream(s)
+        end.record(cur)
+        return start, end
+
+    def h2d_bytes(self):
+        return self.pipes[0].h2d_bytes(self.host_in)
+
+    def d2h_bytes(self):
+        return self.pipes[0].d2h_bytes()
