@@ -383,24 +383,43 @@ __device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, 
   }
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) k_mlp_tc(TcArgs a) {
+// ---------------------------------------------------------------------------
+// warp-specialised variant: warps 0-7 run the epilogues (two threads per TMEM
+// lane), warp 8 only issues MMAs.  Epilogue threads never block on each other:
+// after each operand chunk they arrive on `opbar` (count 256) and move on;
+// the MMA warp waits on it, issues, and commits to `accbar`, which the
+// epilogue threads wait on only when they need the accumulators.  The cloud
+// rows a tile updates are prefetched at its start.
+// ---------------------------------------------------------------------------
+constexpr int kTcEpiThreads = 256;
+constexpr int kTcWsThreads = kTcEpiThreads + 32;
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar;
+  // one operand barrier per hand-off slot of a tile (a thread may run ahead by
+  // one slot, so slots must not share a barrier); parity = tile iteration
+  constexpr int kSlots = FS4D_MAX_TRUNK + 16;
+  __shared__ __align__(8) uint64_t accbar_s, opbar_s[kSlots];
   __shared__ uint32_t tmem_base_sh;
   const TcPlan& p = a.p;
   uint8_t* W = smem;
   const int wbytes = (p.blob_bytes + 1023) & ~1023;
-  uint8_t* X = smem + wbytes;            // [128 x 64] hi + lo   (32 KB)
+  uint8_t* X = smem + wbytes;             // [128 x 64] hi + lo   (32 KB)
   uint8_t* E = X + kTcRows * 64 * 2 * 2;  // [128 x 128] hi + lo  (64 KB)
   const int tid = threadIdx.x, warp = tid >> 5;
-  // two threads per TMEM lane / tile row: warps w and w+4 share lanes 32(w%4)..
-  const int row = tid & (kTcRows - 1), half = tid / kTcRows;
+  const bool mma_warp = warp == kTcEpiThreads / 32;
 
   for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
-  const uint32_t bar = smem_u32(&mbar);
+  const uint32_t accbar = smem_u32(&accbar_s), opbar = smem_u32(&opbar_s[0]);
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(accbar));
+    for (int j = 0; j < kSlots; ++j)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(opbar + 8 * j), "r"(kTcEpiThreads));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -412,137 +431,185 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_mlp_tc(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's 32 lanes
   const uint32_t sW = smem_u32(W), sX = smem_u32(X), sE = smem_u32(E);
-  const float* bias_f = reinterpret_cast<const float*>(W);
-  uint32_t phase = 0;
   const int64_t ntiles = ceil_div(a.K, kTcRows);
 
-  // the next tile's latent rows are prefetched into registers while the
-  // current tile runs its GEMM chain
-  float4 lat[8];  // this thread's half of its row: latent columns [32*half, 32*half+32)
-  auto load_latent = [&](int64_t t) {
-    const int64_t kk = t * kTcRows + row;
-    const float4* src = reinterpret_cast<const float4*>(a.latent + (kk < a.K ? kk : 0) * 64 + 32 * half);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) lat[c] = (t < ntiles && kk < a.K) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-  };
-  load_latent(blockIdx.x);
-  // All warps reach each issue point; thread 0 issues after the fence/barrier
-  // so that every st.shared of the A operand is visible to the async proxy.
-#define TC_SYNC_ISSUE() \
-  fence_async_smem();   \
-  tc_fence_before();    \
-  __syncthreads();      \
-  if (tid == 0) tc_fence_after();
-
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t k = tile * kTcRows + row;
-    const bool valid = k < a.K;
-    // latent row -> X (A operand, KT = 64)
-#pragma unroll
-    for (int c = 0; c < 8; c += 2) {
-      float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
-      store_split8(X, 64, row, 32 * half + 4 * c, v);
-    }
-    load_latent(tile + gridDim.x);
-    // trunk: 64 -> 64, ReLU (deformation.py:41-42); accumulators in TMEM cols [128, 192)
-    for (int l = 0; l < p.depth; ++l) {
-      TC_SYNC_ISSUE();
-      if (tid == 0) {
-        gemm_bf16x3(tmem + 128, sX, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
-        mma_commit(bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1;
+  if (mma_warp) {
+    // ------------------------------------------------------------ MMA issuer
+    uint32_t iter = 0;
+    int slot = 0;
+    auto wait_op = [&]() {
+      mbar_wait(opbar + 8 * slot, iter & 1);
+      ++slot;
       tc_fence_after();
-      const float* tb = bias_f + p.off_b_trunk[l] / 4;
-      if (l + 1 < p.depth) {
-        epilogue_to_operand(tmem_row, 128, 64, tb, true, X, 64, 0, row, half);
-      } else {
-        // last trunk layer: each 16-column chunk of the hidden state feeds one
-        // K step of the fused extractor-0 GEMM (N = 128, deformation.py:46-49)
-        for (int c = 0; c < 64; c += 16) {
-          epilogue_to_operand(tmem_row, 128 + c, 16, tb + c, true, X, 64, c, row, half);
-          TC_SYNC_ISSUE();
-          if (tid == 0) gemm_bf16x3(tmem, sX, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
+    };
+    const bool leader = (tid & 31) == 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
+      slot = 0;
+      for (int l = 0; l < p.depth; ++l) {
+        wait_op();  // X holds the latent / previous trunk output
+        if (leader) {
+          gemm_bf16x3(tmem + 128, sX, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
+          mma_commit(accbar);
         }
-        if (tid == 0) mma_commit(bar);
+        __syncwarp();
       }
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    // extractor-0 epilogue per branch -> E[:, 32b:32b+32], then that branch's
-    // extractor-1 GEMM runs while the next branch's epilogue proceeds
-    for (int b = 0; b < 4; ++b) {
-      epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext0 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
-      TC_SYNC_ISSUE();
-      if (tid == 0) gemm_bf16x3(tmem + 32 * b, sE, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
-    }
-    if (tid == 0) mma_commit(bar);
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    // e2 of every branch = the F_feat concat [h_pos|h_rot|h_scale|h_opa]
-    // (deformation.py:119-120): per branch, the head GEMM (N = 16) and that
-    // branch's K slice of F_feat layer 0 (N = 32) are issued as soon as it lands
-    for (int b = 0; b < 4; ++b) {
-      epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext1 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
-      TC_SYNC_ISSUE();
-      if (tid == 0) {
-        gemm_bf16x3(tmem + 128 + 16 * b, sE, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
-        if (p.enable_feat) gemm_bf16x3(tmem + 192, sE, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
+      for (int c = 0; c < 64; c += 16) {  // hidden chunk c -> extractor-0 K step
+        wait_op();
+        if (leader) gemm_bf16x3(tmem, sX, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
+        __syncwarp();
       }
+      if (leader) mma_commit(accbar);
+      for (int b = 0; b < 4; ++b) {  // e1 of branch b -> extractor-1
+        wait_op();
+        if (leader) gemm_bf16x3(tmem + 32 * b, sE, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
+        __syncwarp();
+      }
+      if (leader) mma_commit(accbar);
+      for (int b = 0; b < 4; ++b) {  // e2 of branch b -> head b and F_feat layer-0 K slice
+        wait_op();
+        if (leader) {
+          gemm_bf16x3(tmem + 128 + 16 * b, sE, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
+          if (p.enable_feat) gemm_bf16x3(tmem + 192, sE, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
+        }
+        __syncwarp();
+      }
+      if (leader) mma_commit(accbar);
+      if (p.enable_feat) {
+        wait_op();  // FF in X
+        if (leader) {
+          gemm_bf16x3(tmem, sX, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
+          mma_commit(accbar);
+        }
+        __syncwarp();
+      }
+      wait_op();  // tile finished: TMEM and X free for the next tile
     }
-    if (tid == 0) mma_commit(bar);
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    {
-      // raw-space deltas (deformation.py:126-133); half 0: position + rotation
-      // heads, half 1: scale + opacity heads (head b lives in cols 128 + 16b)
-      const float* hb = bias_f + p.off_b_head / 4;
-      float d0[4], d1[4];
-      tmem_ld4(tmem_row + 128 + 32 * half, d0);
-      tmem_ld4(tmem_row + 144 + 32 * half, d1);
+  } else {
+    // ------------------------------------------------------------ epilogues
+    const int row = tid & (kTcRows - 1), half = tid / kTcRows;
+    const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float* bias_f = reinterpret_cast<const float*>(W);
+    uint32_t ph = 0;
+    auto wait_acc = [&]() {
+      mbar_wait(accbar, ph);
+      ph ^= 1;
+      tc_fence_after();
+    };
+    int slot = 0;
+    auto signal = [&]() {
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(opbar + 8 * slot);
+      ++slot;
+    };
+    float4 lat[8];
+    auto load_latent = [&](int64_t t) {
+      const int64_t kk = t * kTcRows + row;
+      const float4* src = reinterpret_cast<const float4*>(a.latent + (kk < a.K ? kk : 0) * 64 + 32 * half);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) lat[c] = (t < ntiles && kk < a.K) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    load_latent(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      slot = 0;
+      const int64_t k = tile * kTcRows + row;
+      const bool valid = k < a.K;
+      // prefetch the cloud values this thread updates at the end of the tile
+      float cv[7];
+      float fv[16];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) cv[q] = 0.f;
       if (valid) {
         if (half == 0) {
 #pragma unroll
-          for (int q = 0; q < 3; ++q) a.o_pos[3 * k + q] = a.pos[3 * k + q] + d0[q] + hb[q];
+          for (int q = 0; q < 3; ++q) cv[q] = a.pos[3 * k + q];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a.o_rot[4 * k + q] = a.rot[4 * k + q] + d1[q] + hb[16 + q];
+          for (int q = 0; q < 4; ++q) cv[3 + q] = a.rot[4 * k + q];
         } else {
 #pragma unroll
-          for (int q = 0; q < 3; ++q) a.o_ls[3 * k + q] = a.ls[3 * k + q] + d0[q] + hb[32 + q];
-          a.o_op[k] = a.op[k] + d1[0] + hb[48];
+          for (int q = 0; q < 3; ++q) cv[q] = a.ls[3 * k + q];
+          cv[3] = a.op[k];
         }
       }
-    }
-    if (p.enable_feat) {
-      epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, X, 32, 0, row, half);
-      TC_SYNC_ISSUE();
-      if (tid == 0) {
-        gemm_bf16x3(tmem, sX, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
-        mma_commit(bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      tc_fence_after();
-      const float* fb = bias_f + p.off_b_f2 / 4;
-      for (int c = 8 * half; c < p.DP; c += 16) {
-        float v[8];
-        tmem_ld8(tmem_row + c, v);
-        if (valid) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (c + i < p.D) a.o_feat[(int64_t)p.D * k + c + i] = a.feat[(int64_t)p.D * k + c + i] + v[i] + fb[c + i];
+      for (int q = 0; q < 16; ++q) {
+        const int c = 8 * half + 16 * (q / 8) + (q % 8);
+        fv[q] = (valid && p.enable_feat && c < p.D && p.DP <= 32) ? a.feat[(int64_t)p.D * k + c] : 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) {
+        float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
+        store_split8(X, 64, row, 32 * half + 4 * c, v);
+      }
+      load_latent(tile + gridDim.x);
+      signal();
+      for (int l = 0; l < p.depth; ++l) {
+        wait_acc();
+        const float* tb = bias_f + p.off_b_trunk[l] / 4;
+        if (l + 1 < p.depth) {
+          epilogue_to_operand(tmem_row, 128, 64, tb, true, X, 64, 0, row, half);
+          signal();
+        } else {
+          for (int c = 0; c < 64; c += 16) {
+            epilogue_to_operand(tmem_row, 128 + c, 16, tb + c, true, X, 64, c, row, half);
+            signal();
+          }
         }
       }
+      wait_acc();
+      for (int b = 0; b < 4; ++b) {
+        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext0 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
+        signal();
+      }
+      wait_acc();
+      for (int b = 0; b < 4; ++b) {
+        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext1 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
+        signal();
+      }
+      wait_acc();
+      {
+        const float* hb = bias_f + p.off_b_head / 4;
+        float d0[4], d1[4];
+        tmem_ld4(tmem_row + 128 + 32 * half, d0);
+        tmem_ld4(tmem_row + 144 + 32 * half, d1);
+        if (valid) {
+          if (half == 0) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) a.o_pos[3 * k + q] = cv[q] + d0[q] + hb[q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a.o_rot[4 * k + q] = cv[3 + q] + d1[q] + hb[16 + q];
+          } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) a.o_ls[3 * k + q] = cv[q] + d0[q] + hb[32 + q];
+            a.o_op[k] = cv[3] + d1[0] + hb[48];
+          }
+        }
+      }
+      if (p.enable_feat) {
+        epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, X, 32, 0, row, half);
+        signal();
+        wait_acc();
+        const float* fb = bias_f + p.off_b_f2 / 4;
+        for (int c = 8 * half, q0 = 0; c < p.DP; c += 16, q0 += 8) {
+          float v[8];
+          tmem_ld8(tmem_row + c, v);
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (c + i < p.D) {
+                const float base = p.DP <= 32 ? fv[(q0 + i) & 15] : a.feat[(int64_t)p.D * k + c + i];
+                a.o_feat[(int64_t)p.D * k + c + i] = base + v[i] + fb[c + i];
+              }
+            }
+          }
+        }
+      }
+      signal();  // tile done
     }
-    tc_fence_before();
-    __syncthreads();
   }
+  tc_fence_before();
+  __syncthreads();
   tc_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
@@ -690,10 +757,10 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   a.o_op = snap.opacity_logits;
   a.o_feat = snap.features;
   const int smem = ((p.blob_bytes + 1023) & ~1023) + kTcRows * 64 * 4 + kTcRows * 128 * 4;
-  cudaFuncSetAttribute(k_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_mlp_tc_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int64_t ntiles = ceil_div(K, kTcRows);
   const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
-  k_mlp_tc<<<grid, kTcThreads, smem, s>>>(a);
+  k_mlp_tc_ws<<<grid, kTcWsThreads, smem, s>>>(a);
   return check_launch("deform_tc");
 }
 
