@@ -16,6 +16,7 @@
 //                      last epilogues add the raw-space deltas straight into
 //                      the snapshot (deformation.py:126-133).
 #include <cuda_bf16.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -398,28 +399,112 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-__global__ void __launch_bounds__(kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
+constexpr int kTcProducerThreads = 128;  // fused variant: 4 HexPlane producer warps
+constexpr int kTcFusedThreads = kTcWsThreads + kTcProducerThreads;
+
+// Producer warp pw of the fused kernel: gathers the latent of tile rows
+// [32 pw, 32 pw + 32) straight into the bf16 hi/lo A operand Xs.  Lane j first
+// selects its own Gaussian's 12 bilinear cells in fp64 (hexplane.py:84-110)
+// and keeps them in registers; then, four Gaussians per step, lanes
+// (Gaussian j%4, channel quad) fetch float4 corner rows (hexplane.py:118-142).
+__device__ __forceinline__ void produce_latent(const TcArgs& a, int64_t tile, uint8_t* Xs, int pw, int lane) {
+  const TcPlan& p = a.p;
+  const int r0 = pw * 32;
+  const int64_t kl = tile * kTcRows + r0 + lane;
+  int base[12];
+  float fa[12], fb[12];
+  {
+    double c[4] = {0.0, 0.0, 0.0, p.t};
+    if (kl < a.K) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) c[q] = fmin(fmax(((double)a.pos[3 * kl + q] - p.lo[q]) / p.span[q], 0.0), 1.0);
+    }
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int ra = p.res[l][q][0], rb = p.res[l][q][1];
+        const double u = c[c_axes_tc[q][0]] * (ra - 1), v = c[c_axes_tc[q][1]] * (rb - 1);
+        int i0 = (int)floor(u), j0 = (int)floor(v);
+        i0 = min(max(i0, 0), ra - 2);
+        j0 = min(max(j0, 0), rb - 2);
+        base[l * 6 + q] = (i0 * rb + j0) * 32;
+        fa[l * 6 + q] = (float)(u - i0);
+        fb[l * 6 + q] = (float)(v - j0);
+      }
+  }
+  const int sub = lane >> 3, ch = (lane & 7) * 4;
+  for (int j0 = 0; j0 < 32; j0 += 4) {
+    const int j = j0 + sub, row = r0 + j;
+    const bool ok = p.enable_grid && tile * kTcRows + row < a.K;
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      float4 prod = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int idx = l * 6 + q;
+        const int b = __shfl_sync(0xffffffffu, base[idx], j);
+        const float f0 = __shfl_sync(0xffffffffu, fa[idx], j), f1 = __shfl_sync(0xffffffffu, fb[idx], j);
+        if (ok) {
+          const int rs = p.res[l][q][1] * 32;
+          const float* pl = p.planes[l][q] + b + ch;
+          const float w00 = (1.f - f0) * (1.f - f1), w10 = f0 * (1.f - f1), w01 = (1.f - f0) * f1, w11 = f0 * f1;
+          const float4 c00 = __ldg(reinterpret_cast<const float4*>(pl));
+          const float4 c01 = __ldg(reinterpret_cast<const float4*>(pl + 32));
+          const float4 c10 = __ldg(reinterpret_cast<const float4*>(pl + rs));
+          const float4 c11 = __ldg(reinterpret_cast<const float4*>(pl + rs + 32));
+          prod.x *= w00 * c00.x + w10 * c10.x + w01 * c01.x + w11 * c11.x;
+          prod.y *= w00 * c00.y + w10 * c10.y + w01 * c01.y + w11 * c11.y;
+          prod.z *= w00 * c00.z + w10 * c10.z + w01 * c01.z + w11 * c11.z;
+          prod.w *= w00 * c00.w + w10 * c10.w + w01 * c01.w + w11 * c11.w;
+        }
+      }
+      if (!ok) prod = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float v[4] = {prod.x, prod.y, prod.z, prod.w};
+      __nv_bfloat16 h[4], lo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        h[i] = __float2bfloat16_rn(v[i]);
+        lo[i] = __float2bfloat16_rn(v[i] - __bfloat162float(h[i]));
+      }
+      const int off = core_off(row, l * 32 + ch, 64);
+      *reinterpret_cast<uint2*>(Xs + off) = *reinterpret_cast<const uint2*>(h);
+      *reinterpret_cast<uint2*>(Xs + kTcRows * 64 * 2 + off) = *reinterpret_cast<const uint2*>(lo);
+    }
+  }
+}
+
+template <bool FUSED>
+__global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // one operand barrier per hand-off slot of a tile (a thread may run ahead by
   // one slot, so slots must not share a barrier); parity = tile iteration
   constexpr int kSlots = FS4D_MAX_TRUNK + 16;
-  __shared__ __align__(8) uint64_t accbar_s, opbar_s[kSlots];
+  __shared__ __align__(8) uint64_t accbar_s, opbar_s[kSlots], xfull_s[2], xempty_s[2];
   __shared__ uint32_t tmem_base_sh;
   const TcPlan& p = a.p;
   uint8_t* W = smem;
   const int wbytes = (p.blob_bytes + 1023) & ~1023;
-  uint8_t* X = smem + wbytes;             // [128 x 64] hi + lo   (32 KB)
-  uint8_t* E = X + kTcRows * 64 * 2 * 2;  // [128 x 128] hi + lo  (64 KB)
+  // X: [128 x 64] hi + lo (32 KB) -- two of them in the fused kernel (the
+  // producers fill tile i+1's while tile i runs); E: [128 x 128] hi + lo (64 KB)
+  uint8_t* Xb[2] = {smem + wbytes, smem + wbytes + (FUSED ? kTcRows * 64 * 4 : 0)};
+  uint8_t* E = Xb[1] + kTcRows * 64 * 4;
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool mma_warp = warp == kTcEpiThreads / 32;
+  const bool producer = FUSED && warp > kTcEpiThreads / 32;
 
   for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
   const uint32_t accbar = smem_u32(&accbar_s), opbar = smem_u32(&opbar_s[0]);
+  const uint32_t xfull = smem_u32(&xfull_s[0]), xempty = smem_u32(&xempty_s[0]);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(accbar));
     for (int j = 0; j < kSlots; ++j)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(opbar + 8 * j), "r"(kTcEpiThreads));
+    for (int j = 0; j < 2; ++j) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(xfull + 8 * j), "r"(kTcProducerThreads));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(xempty + 8 * j));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -431,10 +516,20 @@ __global__ void __launch_bounds__(kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t sW = smem_u32(W), sX = smem_u32(X), sE = smem_u32(E);
+  const uint32_t sW = smem_u32(W), sE = smem_u32(E);
   const int64_t ntiles = ceil_div(a.K, kTcRows);
 
-  if (mma_warp) {
+  if (producer) {
+    // ------------------------------------------------------------ producers
+    uint32_t iter = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
+      const int s = iter & 1;
+      if (iter >= 2) mbar_wait(xempty + 8 * s, ((iter >> 1) - 1) & 1);
+      produce_latent(a, tile, Xb[s], warp - kTcEpiThreads / 32 - 1, tid & 31);
+      fence_async_smem();
+      mbar_arrive(xfull + 8 * s);
+    }
+  } else if (mma_warp) {
     // ------------------------------------------------------------ MMA issuer
     uint32_t iter = 0;
     int slot = 0;
@@ -446,8 +541,15 @@ __global__ void __launch_bounds__(kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
     const bool leader = (tid & 31) == 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
       slot = 0;
+      const int s = FUSED ? (iter & 1) : 0;
+      const uint32_t sX = smem_u32(Xb[s]);
       for (int l = 0; l < p.depth; ++l) {
-        wait_op();  // X holds the latent / previous trunk output
+        if (FUSED && l == 0) {  // producers filled X with the latent
+          mbar_wait(xfull + 8 * s, (iter >> 1) & 1);
+          tc_fence_after();
+        } else {
+          wait_op();  // X holds the latent / previous trunk output
+        }
         if (leader) {
           gemm_bf16x3(tmem + 128, sX, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
           mma_commit(accbar);
@@ -484,6 +586,8 @@ __global__ void __launch_bounds__(kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
         __syncwarp();
       }
       wait_op();  // tile finished: TMEM and X free for the next tile
+      if (FUSED && leader) mbar_arrive(xempty + 8 * s);
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ epilogues
@@ -505,14 +609,17 @@ __global__ void __launch_bounds__(kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
     };
     float4 lat[8];
     auto load_latent = [&](int64_t t) {
+      if (FUSED) return;
       const int64_t kk = t * kTcRows + row;
       const float4* src = reinterpret_cast<const float4*>(a.latent + (kk < a.K ? kk : 0) * 64 + 32 * half);
 #pragma unroll
       for (int c = 0; c < 8; ++c) lat[c] = (t < ntiles && kk < a.K) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     };
     load_latent(blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t iter = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
       slot = 0;
+      uint8_t* X = Xb[FUSED ? (iter & 1) : 0];
       const int64_t k = tile * kTcRows + row;
       const bool valid = k < a.K;
       // prefetch the cloud values this thread updates at the end of the tile
@@ -537,13 +644,15 @@ __global__ void __launch_bounds__(kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
         const int c = 8 * half + 16 * (q / 8) + (q % 8);
         fv[q] = (valid && p.enable_feat && c < p.D && p.DP <= 32) ? a.feat[(int64_t)p.D * k + c] : 0.f;
       }
+      if (!FUSED) {
 #pragma unroll
-      for (int c = 0; c < 8; c += 2) {
-        float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
-        store_split8(X, 64, row, 32 * half + 4 * c, v);
+        for (int c = 0; c < 8; c += 2) {
+          float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
+          store_split8(X, 64, row, 32 * half + 4 * c, v);
+        }
+        load_latent(tile + gridDim.x);
+        signal();
       }
-      load_latent(tile + gridDim.x);
-      signal();
       for (int l = 0; l < p.depth; ++l) {
         wait_acc();
         const float* tb = bias_f + p.off_b_trunk[l] / 4;
@@ -736,11 +845,19 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   k_pack_tc<<<dim3(4, pk.nop + pk.nbias), 256, 0, s>>>(pk);
   const int64_t K = cloud.K;
   if (K == 0) return check_launch("deform_tc_pack");
+  // The fused variant (HexPlane gather as 4 producer warps inside the MLP
+  // kernel, latent never leaves shared memory) is correct but measured slower
+  // on B200 (355 vs 228 us at configs[1]): 4 producer warps per SM expose far
+  // less memory-level parallelism than the stand-alone gather at full
+  // occupancy.  It stays opt-in (FS4D_FUSED_GATHER=1).
+  const bool fused = getenv("FS4D_FUSED_GATHER") && (!p.enable_grid || (p.C == 32 && p.levels == 2));
   const unsigned gblocks = (unsigned)ceil_div(K, kGatherWarps * 32);
-  if (p.enable_grid && p.C == 32 && p.levels == 2)
-    k_hexplane_latent_c32<2><<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
-  else
-    k_hexplane_latent<<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
+  if (!fused) {
+    if (p.enable_grid && p.C == 32 && p.levels == 2)
+      k_hexplane_latent_c32<2><<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
+    else
+      k_hexplane_latent<<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
+  }
   TcArgs a;
   a.p = p;
   a.K = K;
@@ -756,11 +873,16 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   a.o_ls = snap.log_scales;
   a.o_op = snap.opacity_logits;
   a.o_feat = snap.features;
-  const int smem = ((p.blob_bytes + 1023) & ~1023) + kTcRows * 64 * 4 + kTcRows * 128 * 4;
-  cudaFuncSetAttribute(k_mlp_tc_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = ((p.blob_bytes + 1023) & ~1023) + kTcRows * 64 * 4 * (fused ? 2 : 1) + kTcRows * 128 * 4;
   const int64_t ntiles = ceil_div(K, kTcRows);
   const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
-  k_mlp_tc_ws<<<grid, kTcWsThreads, smem, s>>>(a);
+  if (fused) {
+    cudaFuncSetAttribute(k_mlp_tc_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mlp_tc_ws<true><<<grid, kTcFusedThreads, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_mlp_tc_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mlp_tc_ws<false><<<grid, kTcWsThreads, smem, s>>>(a);
+  }
   return check_launch("deform_tc");
 }
 
