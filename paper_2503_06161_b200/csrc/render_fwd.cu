@@ -7,9 +7,10 @@
 //   k_tile_count/scan/k_emit/radix/k_ranges   bin_tiles()  rasterizer.py:188-207
 //   k_blend           _tile_alphas + _composite_weights + tile matmuls
 //                                          rasterizer.py:215-261, 284-303
+#include <stdlib.h>
+
 #include "render_common.cuh"
 #include "sh.cuh"
-#include <new>
 
 namespace fs4d {
 
@@ -251,24 +252,29 @@ struct BlendArgs {
 // shared memory in batches of 256 (front to back).  DC = feature channels
 // handled by this launch ([c0, c0+DC)); the first launch also composites
 // colour, depth and alpha.
-template <int DC>
-__global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
-  __shared__ float2 s_xy[kTilePixels];
-  __shared__ float4 s_co[kTilePixels];
-  __shared__ int4 s_pr[kTilePixels];
-  __shared__ float4 s_rgbz[kTilePixels];
-  __shared__ __align__(16) float s_f[DC > 0 ? kTilePixels * DC : 1];
+// SUB > 1 splits a tile's rows over SUB CTAs (each streams the whole depth-
+// ordered list but composites 16/SUB rows): shorter critical path for the
+// densest tiles, sharper warp-row culling.
+template <int DC, int SUB>
+__global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
+  constexpr int NT = kTilePixels / SUB;  // threads = pixels = Gaussians per batch
+  __shared__ float2 s_xy[NT];
+  __shared__ float4 s_co[NT];
+  __shared__ int4 s_pr[NT];
+  __shared__ float4 s_rgbz[NT];
+  __shared__ __align__(16) float s_f[DC > 0 ? NT * DC : 1];
 
-  const int tile = blockIdx.x;
+  const int tile = blockIdx.x / SUB, sub = blockIdx.x % SUB;
   const int tx = tile % a.ntx, ty = tile / a.ntx;
+  const int row0 = ty * kTile + sub * (kTile / SUB);
   const int col = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int row = ty * kTile + (threadIdx.x / kTile);
+  const int row = row0 + (threadIdx.x / kTile);
   const bool inside = col < a.W && row < a.H;
   const uint2 rg = a.ranges[tile];
   const bool first = a.c0 == 0;
   const float fc = (float)col, fr = (float)row;
   const int lane = threadIdx.x & 31;
-  const int wrow0 = ty * kTile + (threadIdx.x >> 5) * 2;  // this warp's two pixel rows
+  const int wrow0 = row0 + (threadIdx.x >> 5) * 2;  // this warp's two pixel rows
   const int tcol0 = tx * kTile;
 
   float T = 1.f, acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f;
@@ -280,8 +286,8 @@ __global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
   const int nf = DC > 0 ? min(DC, a.D - a.c0) : 0;
   const bool vec_ok = DC >= 4 && nf == DC && (a.D & 3) == 0 && (a.c0 & 3) == 0;
 
-  for (uint32_t b = rg.x; b < rg.y; b += kTilePixels) {
-    if (__syncthreads_count(done) == kTilePixels) break;
+  for (uint32_t b = rg.x; b < rg.y; b += NT) {
+    if (__syncthreads_count(done) == NT) break;
     const uint32_t j = b + threadIdx.x;
     if (j < rg.y) {
       const uint32_t g = a.pvals[j];
@@ -302,13 +308,13 @@ __global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
       }
     }
     __syncthreads();
-    const int cnt = min((uint32_t)kTilePixels, rg.y - b);
+    const int cnt = min((uint32_t)NT, rg.y - b);
     // warp-level culling: one ballot per 32 staged Gaussians keeps those whose
     // pixel footprint touches this warp's two pixel rows; the per-thread loop
     // then walks only the set bits, in depth order
-    unsigned wmask[kTilePixels / 32];
+    unsigned wmask[NT / 32];
 #pragma unroll
-    for (int m = 0; m < kTilePixels / 32; ++m) {
+    for (int m = 0; m < NT / 32; ++m) {
       const int kk = m * 32 + lane;
       bool hit = false;
       if (kk < cnt) {
@@ -319,7 +325,7 @@ __global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
     }
     if (!done) {
 #pragma unroll 1
-      for (int m = 0; m < kTilePixels / 32 && !done; ++m) {
+      for (int m = 0; m < NT / 32 && !done; ++m) {
         unsigned bits = wmask[m];
         while (bits) {
           const int k = m * 32 + __ffs(bits) - 1;
@@ -396,14 +402,23 @@ __global__ void __launch_bounds__(kTilePixels) k_blend(BlendArgs a) {
 // ---------------------------------------------------------------------------
 // host driver
 // ---------------------------------------------------------------------------
-static void launch_blend(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
+template <int SUB>
+static void launch_blend_sub(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
+  const int grid = ntiles * SUB, nt = kTilePixels / SUB;
   switch (dc) {
-    case 0: k_blend<0><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    case 4: k_blend<4><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    case 8: k_blend<8><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    case 16: k_blend<16><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    default: k_blend<32><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    case 0: k_blend<0, SUB><<<grid, nt, 0, s>>>(a); break;
+    case 4: k_blend<4, SUB><<<grid, nt, 0, s>>>(a); break;
+    case 8: k_blend<8, SUB><<<grid, nt, 0, s>>>(a); break;
+    case 16: k_blend<16, SUB><<<grid, nt, 0, s>>>(a); break;
+    default: k_blend<32, SUB><<<grid, nt, 0, s>>>(a); break;
   }
+}
+
+static void launch_blend(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
+  static const int sub = getenv("FS4D_BLEND_SUB") ? atoi(getenv("FS4D_BLEND_SUB")) : 2;
+  if (sub == 4) launch_blend_sub<4>(dc, ntiles, a, s);
+  else if (sub == 1) launch_blend_sub<1>(dc, ntiles, a, s);
+  else launch_blend_sub<2>(dc, ntiles, a, s);
 }
 
 int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRasterConfig& cfg,
