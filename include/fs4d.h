@@ -206,11 +206,21 @@ int fs4d_profile_collect(double* ms_total, int64_t* calls, int32_t n_stages);
  * weight-gradient partials for the backward). */
 size_t fs4d_deform_workspace_bytes(const Fs4dDeformNet* net, int64_t K);
 
-/* deform_with_cache: writes snapshot->{positions, rotations, log_scales,
- * opacity_logits, features}; colors_raw / sh_rest are aliased by the caller
- * (deformation.py:131), as are features when enable_feature_update == 0. */
+/* Bytes of the activation cache deform_with_cache keeps for deform_backward
+ * (deformation.py:105-136 returns it as `cache`): per 128 Gaussians the
+ * tensor-core operand images of latent, hidden, e1, e2 and F_feat's hidden
+ * layer.  0 when the net shape is outside the tensor-core backward (the
+ * backward then recomputes the forward and needs no cache). */
+size_t fs4d_deform_cache_bytes(const Fs4dDeformNet* net, const Fs4dHexPlane* field, int64_t K);
+
+/* deform / deform_with_cache: writes snapshot->{positions, rotations,
+ * log_scales, opacity_logits, features}; colors_raw / sh_rest are aliased by
+ * the caller (deformation.py:131), as are features when
+ * enable_feature_update == 0.  cache == NULL is `deform` (no cache); a cache
+ * of fs4d_deform_cache_bytes() bytes is `deform_with_cache`. */
 int fs4d_deform_fwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field,
                     const Fs4dDeformNet* net, double t, Fs4dCloud* snapshot,
+                    void* cache, size_t cache_bytes,
                     void* workspace, size_t workspace_bytes,
                     int32_t* status, void* stream);
 
@@ -219,9 +229,13 @@ int fs4d_deform_fwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field,
  * (positions incl. the grid term, others pass through), net_grads (weight /
  * bias pointers of the struct, zeroed and accumulated) and plane_grads
  * (shapes of field->planes, zeroed and accumulated; ignored when
- * enable_grid == 0). */
+ * enable_grid == 0).  `cache` is the deform_with_cache cache of the same
+ * (cloud, t) -- a mismatch raises FS4D_ERR_CONTRACT in the status block -- or
+ * NULL, in which case the forward is recomputed (deformation.py:139 takes the
+ * cache; the recompute path serves callers that kept none). */
 int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field,
                     const Fs4dDeformNet* net, double t,
+                    const void* cache, size_t cache_bytes,
                     const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads,
                     Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads,
                     int32_t accumulate,

@@ -607,6 +607,32 @@ def deform(cloud, planes, aabb, net, t, enable_grid=True, enable_feature_update=
     return snap, cache
 
 
+def relu_gate_margins(net, cache):
+    """Per Gaussian, the smallest relative margin of any ReLU gate
+    (numerics.py:72, 99: pre > 0) in the deformation MLP:
+    |pre| / (sum_i |W_oi x_i| + |b_o|).  A gate inside the device's
+    product-rounding band (tensor-core bf16x3 operands carry ~2^-17 relative
+    error) may resolve either way; its Gaussian is 'ambiguous' under the
+    parity contract."""
+    def stack(layers, rec, m):
+        for (W, b, relu), (x, pre) in zip(layers, rec):
+            if not relu:
+                continue
+            scale = np.abs(x) @ np.abs(np.asarray(W, dtype=np.float64)).T + np.abs(np.asarray(b, dtype=np.float64))
+            m = np.minimum(m, (np.abs(pre) / np.maximum(scale, 1e-300)).min(axis=1))
+        return m
+
+    k = cache["trunk"][0][0].shape[0]
+    m = stack(net["net.trunk"], cache["trunk"], np.full(k, np.inf))
+    for name in BRANCHES:
+        erec, hrec = cache["branch"][name]
+        m = stack(net[f"net.ext.{name}"], erec, m)
+        m = stack(net[f"net.head.{name}"], hrec, m)
+    if cache["feat"] is not None:
+        m = stack(net["net.feat"], cache["feat"], m)
+    return m
+
+
 def deform_backward(cloud, planes, aabb, net, cache, grads, enable_grid=True,
                     enable_feature_update=True):
     """deformation.py:139-183.  grads: dict with positions, rotations,

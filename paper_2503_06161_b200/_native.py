@@ -107,12 +107,16 @@ SIGNATURES = {
     "fs4d_profile_collect": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]),
     "fs4d_deform_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(DeformNet), ctypes.c_int64]),
+    "fs4d_deform_cache_bytes": (ctypes.c_size_t, [ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane),
+                                                  ctypes.c_int64]),
     "fs4d_deform_fwd": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(HexPlane),
                                        ctypes.POINTER(DeformNet), ctypes.c_double,
                                        ctypes.POINTER(Cloud), ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p, ctypes.c_void_p]),
     "fs4d_deform_bwd": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(HexPlane),
                                        ctypes.POINTER(DeformNet), ctypes.c_double,
+                                       ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.POINTER(Cloud), ctypes.POINTER(Cloud),
                                        ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane),
                                        ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,

@@ -67,10 +67,12 @@ int render_backward(const Fs4dCloud&, const Fs4dCamera&, const Fs4dRasterConfig&
 int render_export_projected(const RenderLayout&, void*, Fs4dProjected&, cudaStream_t);
 int render_export_tiles(const RenderLayout&, void*, int32_t*, int32_t*, int64_t, cudaStream_t);
 size_t deform_workspace_bytes(const Fs4dDeformNet& net, int64_t K, int* nparts_out);
+size_t deform_cache_bytes(const Fs4dDeformNet& net, const Fs4dHexPlane& field, int64_t K);
 int deform_forward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, Fs4dCloud&, void*, size_t,
-                   cudaStream_t);
-int deform_backward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, const Fs4dCloud&, Fs4dCloud&,
-                    Fs4dDeformNet&, Fs4dHexPlane*, int, void*, size_t, cudaStream_t);
+                   void*, size_t, cudaStream_t);
+int deform_backward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, const void*, size_t,
+                    const Fs4dCloud&, Fs4dCloud&, Fs4dDeformNet&, Fs4dHexPlane*, int, void*, size_t, int32_t*,
+                    cudaStream_t);
 int l1_loss_grad(const float*, const float*, const float*, const float*, int, int, int, double, double, float*, float*,
                  double*, cudaStream_t);
 
@@ -173,29 +175,35 @@ size_t fs4d_deform_workspace_bytes(const Fs4dDeformNet* net, int64_t K) {
   return deform_workspace_bytes(*net, K, nullptr);
 }
 
+size_t fs4d_deform_cache_bytes(const Fs4dDeformNet* net, const Fs4dHexPlane* field, int64_t K) {
+  if (!net || !field || K < 0) return 0;
+  return deform_cache_bytes(*net, *field, K);
+}
+
 int fs4d_deform_fwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net, double t,
-                    Fs4dCloud* snapshot, void* workspace, size_t workspace_bytes, int32_t* status, void* stream) {
+                    Fs4dCloud* snapshot, void* cache, size_t cache_bytes, void* workspace, size_t workspace_bytes,
+                    int32_t* status, void* stream) {
   (void)status;
   int rc = check_cloud(cloud, false);
   if (rc) return rc;
   if (!field || !net || !snapshot) return fail(FS4D_ERR_CONFIG, "null deform argument");
   if (snapshot->K != cloud->K) return fail(FS4D_ERR_CONFIG, "snapshot size mismatch");
-  return deform_forward(*cloud, *field, *net, t, *snapshot, workspace, workspace_bytes, (cudaStream_t)stream);
+  return deform_forward(*cloud, *field, *net, t, *snapshot, cache, cache_bytes, workspace, workspace_bytes,
+                        (cudaStream_t)stream);
 }
 
 int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net, double t,
-                    const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads, Fs4dDeformNet* net_grads,
-                    Fs4dHexPlane* plane_grads, int32_t accumulate, void* workspace, size_t workspace_bytes,
-                    int32_t* status, void* stream) {
-  (void)status;
+                    const void* cache, size_t cache_bytes, const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads,
+                    Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads, int32_t accumulate, void* workspace,
+                    size_t workspace_bytes, int32_t* status, void* stream) {
   int rc = check_cloud(cloud, false);
   if (rc) return rc;
   if (!field || !net || !snapshot_grads || !cloud_grads || !net_grads)
     return fail(FS4D_ERR_CONFIG, "null deform_bwd argument");
   if (snapshot_grads->K != cloud->K || cloud_grads->K != cloud->K)
     return fail(FS4D_ERR_CONTRACT, "gradient rows do not match the cloud");
-  return deform_backward(*cloud, *field, *net, t, *snapshot_grads, *cloud_grads, *net_grads, plane_grads, accumulate,
-                         workspace, workspace_bytes, (cudaStream_t)stream);
+  return deform_backward(*cloud, *field, *net, t, cache, cache_bytes, *snapshot_grads, *cloud_grads, *net_grads,
+                         plane_grads, accumulate, workspace, workspace_bytes, status, (cudaStream_t)stream);
 }
 
 int fs4d_l1_loss_grad(const float* color, const float* color_target, const float* feature,

@@ -205,6 +205,30 @@ __device__ __forceinline__ void dense_fwd(const LayerDesc& L, const float* __res
 // gx[i][g] (+)= sum_o W[o][i] gy[o][g]   (W^T gy; gy padding rows must be 0)
 __device__ __forceinline__ void dense_bwd_x(const LayerDesc& L, const float* __restrict__ blob, const float* gy,
                                             float* gx, int TG, bool accumulate) {
+  // one thread = one Gaussian x 4 input channels: 4 independent FMA chains fed
+  // by a warp-uniform float4 of the original [out,in] weight row
+  if ((L.in & 3) == 0) {
+    const int nib = L.in >> 2;
+    for (int idx = threadIdx.x; idx < nib * TG; idx += blockDim.x) {
+      const int g = idx % TG, i0 = (idx / TG) * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (accumulate) acc = make_float4(gx[i0 * TG + g], gx[(i0 + 1) * TG + g], gx[(i0 + 2) * TG + g], gx[(i0 + 3) * TG + g]);
+      const float* w = L.w + i0;
+      for (int o = 0; o < L.out; ++o) {
+        const float gv = gy[o * TG + g];
+        const float4 wv = __ldg(reinterpret_cast<const float4*>(w + (int64_t)o * L.in));
+        acc.x = fmaf(wv.x, gv, acc.x);
+        acc.y = fmaf(wv.y, gv, acc.y);
+        acc.z = fmaf(wv.z, gv, acc.z);
+        acc.w = fmaf(wv.w, gv, acc.w);
+      }
+      gx[i0 * TG + g] = acc.x;
+      gx[(i0 + 1) * TG + g] = acc.y;
+      gx[(i0 + 2) * TG + g] = acc.z;
+      gx[(i0 + 3) * TG + g] = acc.w;
+    }
+    return;
+  }
   const float* Wt = blob + L.off_w;
   for (int idx = threadIdx.x; idx < L.in * TG; idx += blockDim.x) {
     const int g = idx % TG, i = idx / TG;
@@ -226,13 +250,33 @@ __device__ __forceinline__ void dense_bwd_w(const LayerDesc& L, float* __restric
                                             const float* x, int TG, int ng) {
   float* Wt = part + L.off_w;
   float* bias = part + L.off_b;
-  for (int idx = threadIdx.x; idx < L.in * L.out; idx += blockDim.x) {
-    const int o = idx % L.out, i = idx / L.out;
-    const float* gyo = gy + o * TG;
-    const float* xi = x + i * TG;
-    float acc = 0.f;
-    for (int g = 0; g < ng; ++g) acc = fmaf(gyo[g], xi[g], acc);
-    Wt[(int64_t)i * L.out_pad + o] += acc;
+  // 4 (out) x 4 (in) register tile per thread: 16 independent accumulators,
+  // 8 shared loads per 16 FMA (gy padding rows are zero, x rows >= in masked)
+  const int nob = L.out_pad >> 2, nib = (L.in + 3) >> 2;
+  for (int idx = threadIdx.x; idx < nob * nib; idx += blockDim.x) {
+    const int o0 = (idx % nob) * 4, i0 = (idx / nob) * 4;
+    float acc[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[q][r] = 0.f;
+    const bool full_i = i0 + 4 <= L.in;
+    for (int g = 0; g < ng; ++g) {
+      float gv[4], xv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) gv[q] = gy[(o0 + q) * TG + g];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) xv[r] = (full_i || i0 + r < L.in) ? x[(i0 + r) * TG + g] : 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[q][r] = fmaf(gv[q], xv[r], acc[q][r]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (o0 + q < L.out && i0 + r < L.in) Wt[(int64_t)(i0 + r) * L.out_pad + o0 + q] += acc[q][r];
   }
   for (int o = threadIdx.x; o < L.out; o += blockDim.x) {
     const float* gyo = gy + o * TG;
@@ -747,7 +791,20 @@ static size_t blob_bytes(const NetDesc& d) { return align_up_sz((size_t)d.packed
 bool tc_path_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f);
 size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K);
 int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
-                      Fs4dCloud& snap, void* ws, cudaStream_t s);
+                      Fs4dCloud& snap, void* ws, uint8_t* cache, cudaStream_t s);
+bool tc_bwd_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f);
+size_t tc_cache_bytes(const Fs4dDeformNet& n, const Fs4dHexPlane& f, int64_t K);
+int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
+                       const uint8_t* cache, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
+                       Fs4dHexPlane* pg, int accumulate, void* ws, int32_t* status, cudaStream_t s);
+
+static bool tc_enabled() { return !getenv("FS4D_NO_TC"); }
+
+// activation cache of deform_with_cache: 0 when the tensor-core backward does
+// not cover this net (the backward then recomputes the forward itself)
+size_t deform_cache_bytes(const Fs4dDeformNet& net, const Fs4dHexPlane& field, int64_t K) {
+  return tc_enabled() ? tc_cache_bytes(net, field, K) : 0;
+}
 
 size_t deform_workspace_bytes(const Fs4dDeformNet& net, int64_t K, int* nparts_out) {
   NetDesc d;
@@ -796,7 +853,7 @@ static int fill_args(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs
 }
 
 int deform_forward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
-                   Fs4dCloud& snap, void* ws, size_t ws_bytes, cudaStream_t s) {
+                   Fs4dCloud& snap, void* cache, size_t cache_bytes, void* ws, size_t ws_bytes, cudaStream_t s) {
   DefArgs a;
   memset(&a, 0, sizeof(a));
   size_t smem = 0;
@@ -809,7 +866,10 @@ int deform_forward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4d
   a.o_op = snap.opacity_logits;
   a.o_feat = snap.features;
   StageTimer st(FS4D_STAGE_DEFORM_FWD, s);
-  if (tc_path_ok(net, field) && !getenv("FS4D_NO_TC")) return deform_forward_tc(cloud, field, net, t, snap, ws, s);
+  const size_t cneed = deform_cache_bytes(net, field, cloud.K);
+  if (cache && cneed && cache_bytes < cneed) return fail(FS4D_ERR_CONFIG, "deform cache too small");
+  if (tc_path_ok(net, field) && tc_enabled())
+    return deform_forward_tc(cloud, field, net, t, snap, ws, cneed ? (uint8_t*)cache : nullptr, s);
   pack_net(a.net, (float*)ws, s);
   cudaFuncSetAttribute(k_deform_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t ntiles = ceil_div(cloud.K, a.TG);
@@ -819,8 +879,8 @@ int deform_forward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4d
 }
 
 int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
-                    const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng, Fs4dHexPlane* pg, int accumulate,
-                    void* ws, size_t ws_bytes, cudaStream_t s) {
+                    const void* cache, size_t cache_bytes, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
+                    Fs4dHexPlane* pg, int accumulate, void* ws, size_t ws_bytes, int32_t* status, cudaStream_t s) {
   DefArgs a;
   memset(&a, 0, sizeof(a));
   size_t smem = 0;
@@ -856,7 +916,12 @@ int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4
       pa.n[f] = ns[f];
     }
     pa.accumulate = accumulate;
-    k_grad_passthrough<<<dim3(64, 6), 256, 0, s>>>(pa);
+    k_grad_passthrough<<<dim3(kNumSMs * 2, 6), 256, 0, s>>>(pa);
+  }
+  const size_t cneed = deform_cache_bytes(net, field, cloud.K);
+  if (cache && cneed) {
+    if (cache_bytes < cneed) return fail(FS4D_ERR_CONFIG, "deform cache too small");
+    return deform_backward_tc(cloud, field, net, t, (const uint8_t*)cache, sg, cg, ng, pg, accumulate, ws, status, s);
   }
   const int64_t ntiles = ceil_div(cloud.K, a.TG);
   const int grid = (int)(ntiles < kNumSMs * 2 ? (ntiles > 0 ? ntiles : 1) : kNumSMs * 2);

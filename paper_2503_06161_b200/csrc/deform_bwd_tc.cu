@@ -1,0 +1,567 @@
+// Deformation backward, fast path (deformation.deform_backward,
+// deformation.py:139-183; numerics.mlp_backward, numerics.py:78-105;
+// hexplane.query_backward, hexplane.py:145-187).
+//
+//   k_mlp_bwd_tc     one persistent CTA per SM walks tiles of 128 Gaussians.
+//                    The activations come from the deform_with_cache images
+//                    (cp.async.bulk straight into shared memory); every
+//                    input-gradient GEMM (dX = dY * W) and weight-gradient
+//                    GEMM (dW^T += X^T * dY, K = the tile's Gaussians) runs on
+//                    tcgen05 with the 3-term bf16 split.  The weight gradients
+//                    of all 15 layers stay resident in TMEM (384 fp32 columns)
+//                    for the CTA's whole tile range; the bias gradient of a
+//                    layer rides its weight-gradient MMA as the cached
+//                    constant-1 input column (lane `in`), except the heads and
+//                    F_feat layer 0 (whose inputs fill all 128 lanes), which
+//                    are reduced by the epilogue warps.  Epilogue warps (two
+//                    threads per Gaussian) apply the ReLU masks, split the
+//                    gradients into the next GEMM's operand image and write
+//                    dL/dlatent [K, 64].
+//   k_reduce_tc_wgrads  sums the per-CTA partials into the [out, in] / [out]
+//                    gradient buffers of DeformationNet.param_arrays().
+//   k_hexplane_bwd   plane scatter + position gradient from dL/dlatent.
+#include <stdlib.h>
+#include <string.h>
+
+#include "tc_common.cuh"
+
+namespace fs4d {
+
+__constant__ int c_axes_bwd[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};  // hexplane.py:16
+
+constexpr int kBwdEpiThreads = 256;
+constexpr int kBwdThreads = kBwdEpiThreads + 32;
+constexpr int kBwdTmemCols = 512;
+
+// TMEM columns: resident weight-gradient accumulators, then per-tile scratch
+constexpr int kDwTrunk = 0, kDwExt0 = 64, kDwExt1 = 192, kDwHead = 320, kDwF1 = 336, kDwF2 = 368;
+constexpr int kScr = kDwCols;  // 128 scratch columns
+
+// shared-memory regions after the weight blob (bytes).  Phase F (F_feat and
+// heads), phase B (branches, one at a time) and the trunk phase reuse space.
+constexpr int kRE2 = 0, kRFF = 65536, kRGZ = 86016, kRGD = 94208, kRGFF = 102400;
+constexpr int kRHid = 0, kRE1 = 36864, kRGE2 = 57344, kRGE1 = 73728;
+constexpr int kRLat = 36864, kRGH = 73728;
+constexpr int kRBytes = 118784 + 2048;  // + slack for M = 128 MN-major reads of narrower images
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+// ReLU gate of 16 consecutive columns c0.. of row r: bit i set iff value > 0
+__device__ __forceinline__ uint32_t relu_bits16(const uint8_t* img, int KT, int r, int c0) {
+  const uint4 a = *reinterpret_cast<const uint4*>(img + core_off(r, c0, KT));
+  const uint4 b = *reinterpret_cast<const uint4*>(img + core_off(r, c0 + 8, KT));
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t lo = w[i] & 0xFFFFu, hi = w[i] >> 16;
+    if (lo != 0 && !(lo & 0x8000u)) m |= 1u << (2 * i);
+    if (hi != 0 && !(hi & 0x8000u)) m |= 1u << (2 * i + 1);
+  }
+  return m;
+}
+
+// warp sum of v[i] for every i, added into shared accumulators by lane 0
+template <int N>
+__device__ __forceinline__ void warp_sum_to_smem(const float* v, float* dst, int lane) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    float s = v[i];
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) atomicAdd(dst + i, s);
+  }
+}
+
+struct BwdArgs {
+  TcPlan p;
+  int64_t K;
+  const uint8_t* blob;
+  const uint8_t* cache;
+  const float* g_pos;
+  const float* g_rot;
+  const float* g_ls;
+  const float* g_op;
+  const float* g_feat;
+  float* dlat;   // [K, 64]
+  float* wpart;  // [grid][kPartStride]
+  int32_t* status;
+};
+
+__global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t accbar_s, ldbar_s;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float sbias[64];  // head biases [0, 16), F_feat layer-0 biases [16, 48)
+  const TcPlan& p = a.p;
+  const int wbytes = (p.blob_bytes + 1023) & ~1023;
+  uint8_t* W = smem;
+  uint8_t* R = smem + wbytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool issuer = tid == kBwdEpiThreads;
+  const bool epi = tid < kBwdEpiThreads;
+
+  for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
+  if (tid < 64) sbias[tid] = 0.f;
+  const uint32_t accbar = smem_u32(&accbar_s), ldbar = smem_u32(&ldbar_s);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(accbar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ldbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const CacheHeader* h = reinterpret_cast<const CacheHeader*>(a.cache);
+    if (blockIdx.x == 0 && (h->magic != kCacheMagic || h->K != a.K || h->t != p.t))
+      raise_status(a.status, FS4D_ERR_CONTRACT);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kBwdTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t sW = smem_u32(W), sR = smem_u32(R);
+  auto sync_all = [&]() {
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  };
+
+  // operand views that do not depend on the tile
+  const TcOpnd wF2 = opnd_mn(sW + p.off_f2, p.DP, 32, 0);  // N = 32 inputs, K = D outputs
+  const int row = tid & (kTcRows - 1), half = (tid >> 7) & 1;
+  const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+
+  const int64_t ntiles = ceil_div(a.K, kTcRows);
+  bool first = true;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint8_t* ct = a.cache + kCacheHeader + tile * (int64_t)kCacheTileBytes;
+    const int64_t k = tile * kTcRows + row;
+    const bool valid = k < a.K;
+    const bool acc = !first;
+    // ------------------------------------------------ phase F: F_feat + heads
+    if (issuer) {
+      mbar_expect_tx(ldbar, 65536 + 20480);
+      bulk_g2s(sR + kRE2, ct + kCacheE2, 65536, ldbar);
+      bulk_g2s(sR + kRFF, ct + kCacheFF, 20480, ldbar);
+    }
+    if (epi) {
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = 8 * half + i;
+        v[i] = (valid && c < p.D) ? a.g_feat[(int64_t)p.D * k + c] : 0.f;
+      }
+      store_split8(R + kRGZ, 16, row, 8 * half, v);
+      // delta gradients in head order: position 3, rotation 4, scale 3, opacity 1
+      if (half == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) v[i] = valid ? a.g_pos[3 * k + i] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[3 + i] = valid ? a.g_rot[4 * k + i] : 0.f;
+        v[7] = valid ? a.g_ls[3 * k] : 0.f;
+      } else {
+        v[0] = valid ? a.g_ls[3 * k + 1] : 0.f;
+        v[1] = valid ? a.g_ls[3 * k + 2] : 0.f;
+        v[2] = valid ? a.g_op[k] : 0.f;
+#pragma unroll
+        for (int i = 3; i < 8; ++i) v[i] = 0.f;
+      }
+      store_split8(R + kRGD, 16, row, 8 * half, v);
+      warp_sum_to_smem<8>(v, sbias + 8 * half, lane);
+    }
+    sync_all();
+    if (issuer) {
+      mbar_wait(ldbar, 0);
+      tc_fence_after();
+      // dL/dFF = dL/dz * W_f2 (numerics.py:102), dW_f2^T += FF^T dL/dz
+      gemm3(tmem + kScr, opnd_k(sR + kRGZ, 128, 16, 0), wF2, 32, 1, false);
+      gemm3(tmem + kDwF2, opnd_mn(sR + kRFF, 128, kCacheKtFF, 0), opnd_mn(sR + kRGZ, 128, 16, 0), p.DP, 8, acc);
+      mma_commit(accbar);
+    }
+    uint64_t m2 = 0;  // ReLU gates of this thread's E2 columns: bit 16b+i = column 32b + 16 half + i
+    if (epi) {
+      mbar_wait(accbar, 0);
+      tc_fence_after();
+      mbar_wait(ldbar, 0);
+      float g[16];
+      tmem_ld16(tmem_row + kScr + 16 * half, g);
+      const uint32_t mf = relu_bits16(R + kRFF, kCacheKtFF, row, 16 * half);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (!((mf >> i) & 1u)) g[i] = 0.f;
+      store_split8(R + kRGFF, 32, row, 16 * half, g);
+      store_split8(R + kRGFF, 32, row, 16 * half + 8, g + 8);
+      warp_sum_to_smem<16>(g, sbias + 16 + 16 * half, lane);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        m2 |= (uint64_t)relu_bits16(R + kRE2, kCacheKtE2, row, 32 * b + 16 * half) << (16 * b);
+    }
+    sync_all();
+    auto issue_ge2 = [&](int b) {
+      // dL/de2_b = dL/dFF * W_f1[:, 32b:32b+32] + dL/ddelta_b * W_head_b (deformation.py:157-177)
+      gemm3(tmem + kScr, opnd_k(sR + kRGFF, 128, 32, 0), opnd_mn(sW + p.off_f1, 32, 128, 32 * b), 32, 2, false);
+      gemm3(tmem + kScr, opnd_k(sR + kRGD, 128, 16, 0), opnd_mn(sW + p.off_headT[b], 16, 32, 0), 32, 1, true);
+    };
+    if (issuer) {
+      const TcOpnd e2 = opnd_mn(sR + kRE2, 128, kCacheKtE2, 0);
+      gemm3(tmem + kDwF1, e2, opnd_mn(sR + kRGFF, 128, 32, 0), 32, 8, acc);
+      gemm3(tmem + kDwHead, e2, opnd_mn(sR + kRGD, 128, 16, 0), 16, 8, acc);
+      issue_ge2(0);
+      mma_commit(accbar);
+      mbar_wait(accbar, 1);  // E2 no longer read: load the hidden layer and branch 0's e1
+      mbar_expect_tx(ldbar, 36864 + kCacheE1Bytes);
+      bulk_g2s(sR + kRHid, ct + kCacheHid, 36864, ldbar);
+      bulk_g2s(sR + kRE1, ct + kCacheE1, kCacheE1Bytes, ldbar);
+    }
+    auto epi_ge2 = [&](int b) {
+      float g[16];
+      tmem_ld16(tmem_row + kScr + 16 * half, g);
+      const uint32_t m = (uint32_t)(m2 >> (16 * b)) & 0xFFFFu;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (!((m >> i) & 1u)) g[i] = 0.f;
+      store_split8(R + kRGE2, 32, row, 16 * half, g);
+      store_split8(R + kRGE2, 32, row, 16 * half + 8, g + 8);
+    };
+    if (epi) {
+      mbar_wait(accbar, 1);
+      tc_fence_after();
+      epi_ge2(0);
+    }
+    sync_all();
+    // ------------------------------------------------ phase B: one branch at a time
+    for (int b = 0; b < 4; ++b) {
+      if (issuer) {
+        mbar_wait(ldbar, (1 + b) & 1);
+        tc_fence_after();
+        // dL/de1_b = dL/de2_b * W_ext1_b; dW_ext1_b^T += e1_b^T dL/de2_b
+        gemm3(tmem + kScr + 32, opnd_k(sR + kRGE2, 128, 32, 0), opnd_mn(sW + p.off_ext1[b], 32, 32, 0), 32, 2, false);
+        gemm3(tmem + kDwExt1 + 32 * b, opnd_mn(sR + kRE1, 128, kCacheKtE1, 0), opnd_mn(sR + kRGE2, 128, 32, 0), 32, 8,
+              acc);
+        if (b < 3) issue_ge2(b + 1);
+        mma_commit(accbar);
+      }
+      if (epi) {
+        mbar_wait(accbar, (2 + b) & 1);
+        tc_fence_after();
+        mbar_wait(ldbar, (1 + b) & 1);
+        float g[16];
+        tmem_ld16(tmem_row + kScr + 32 + 16 * half, g);
+        const uint32_t m = relu_bits16(R + kRE1, kCacheKtE1, row, 16 * half);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (!((m >> i) & 1u)) g[i] = 0.f;
+        store_split8(R + kRGE1, 32, row, 16 * half, g);
+        store_split8(R + kRGE1, 32, row, 16 * half + 8, g + 8);
+        if (b < 3) epi_ge2(b + 1);
+      }
+      sync_all();
+      if (issuer) {
+        // dL/dhidden += dL/de1_b * W_ext0_b; dW_ext0_b^T += hidden^T dL/de1_b
+        gemm3(tmem + kScr + 64, opnd_k(sR + kRGE1, 128, 32, 0), opnd_mn(sW + p.off_ext0, 128, 64, 0, 32 * b), 64, 2,
+              b > 0);
+        gemm3(tmem + kDwExt0 + 32 * b, opnd_mn(sR + kRHid, 128, kCacheKtHid, 0), opnd_mn(sR + kRGE1, 128, 32, 0), 32,
+              8, acc);
+        if (b < 3) {
+          mbar_expect_tx(ldbar, kCacheE1Bytes);
+          bulk_g2s(sR + kRE1, ct + kCacheE1 + (b + 1) * kCacheE1Bytes, kCacheE1Bytes, ldbar);
+        }
+      }
+    }
+    // ------------------------------------------------ trunk
+    if (issuer) {
+      mma_commit(accbar);
+      mbar_wait(accbar, 0);
+      mbar_expect_tx(ldbar, 36864);
+      bulk_g2s(sR + kRLat, ct + kCacheLat, 36864, ldbar);
+    }
+    if (epi) {
+      mbar_wait(accbar, 0);
+      tc_fence_after();
+      const uint32_t m0 = relu_bits16(R + kRHid, kCacheKtHid, row, 32 * half);
+      const uint32_t m1 = relu_bits16(R + kRHid, kCacheKtHid, row, 32 * half + 16);
+      float g[16];
+      tmem_ld16(tmem_row + kScr + 64 + 32 * half, g);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (!((m0 >> i) & 1u)) g[i] = 0.f;
+      store_split8(R + kRGH, 64, row, 32 * half, g);
+      store_split8(R + kRGH, 64, row, 32 * half + 8, g + 8);
+      tmem_ld16(tmem_row + kScr + 64 + 32 * half + 16, g);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (!((m1 >> i) & 1u)) g[i] = 0.f;
+      store_split8(R + kRGH, 64, row, 32 * half + 16, g);
+      store_split8(R + kRGH, 64, row, 32 * half + 24, g + 8);
+    }
+    sync_all();
+    if (issuer) {
+      mbar_wait(ldbar, 1);
+      tc_fence_after();
+      // dL/dlatent = dL/dh0 * W_trunk; dW_trunk^T += latent^T dL/dh0
+      gemm3(tmem + kScr, opnd_k(sR + kRGH, 128, 64, 0), opnd_mn(sW + p.off_trunk[0], 64, 64, 0), 64, 4, false);
+      gemm3(tmem + kDwTrunk, opnd_mn(sR + kRLat, 128, kCacheKtLat, 0), opnd_mn(sR + kRGH, 128, 64, 0), 64, 8, acc);
+      mma_commit(accbar);
+    }
+    if (epi) {
+      mbar_wait(accbar, 1);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float g[16];
+        tmem_ld16(tmem_row + kScr + 32 * half + 16 * h, g);
+        if (valid) {
+          float4* dst = reinterpret_cast<float4*>(a.dlat + k * 64 + 32 * half + 16 * h);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+        }
+      }
+    }
+    sync_all();
+    first = false;
+  }
+  // resident weight gradients -> this CTA's partial, [column][lane]
+  if (epi) {
+    float* part = a.wpart + (int64_t)blockIdx.x * kPartStride;
+    for (int c = (kDwCols / 2) * half; c < (kDwCols / 2) * (half + 1); c += 16) {
+      float v[16];
+      tmem_ld16(tmem_row + c, v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) part[(c + i) * kTcRows + row] = v[i];
+    }
+    if (tid < 48) part[kDwCols * kTcRows + tid] = sbias[tid];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kBwdTmemCols));
+}
+
+// ---------------------------------------------------------------------------
+// partial reduction into DeformationNet gradient buffers
+// ---------------------------------------------------------------------------
+struct DwMap {
+  float* gw;  // [out, in]
+  float* gb;  // [out]
+  int out, in, col0, lane0, bias_lane, bias_tail;
+};
+constexpr int kNumDwMaps = 15;
+struct DwReduceArgs {
+  DwMap m[kNumDwMaps];
+  const float* wpart;
+  int nparts;
+  int accumulate;
+};
+
+__global__ void k_reduce_tc_wgrads(DwReduceArgs a) {
+  const DwMap& m = a.m[blockIdx.y];
+  const int nw = m.out * m.in;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nw + m.out; e += gridDim.x * blockDim.x) {
+    int src;
+    float* dst;
+    if (e < nw) {
+      const int o = e / m.in, i = e % m.in;
+      src = (m.col0 + o) * kTcRows + m.lane0 + i;
+      dst = m.gw + e;
+    } else {
+      const int o = e - nw;
+      src = m.bias_lane >= 0 ? (m.col0 + o) * kTcRows + m.bias_lane : kDwCols * kTcRows + m.bias_tail + o;
+      dst = m.gb + o;
+    }
+    float s = 0.f;
+    for (int q = 0; q < a.nparts; ++q) s += a.wpart[(int64_t)q * kPartStride + src];
+    *dst = a.accumulate ? *dst + s : s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// HexPlane backward (hexplane.py:145-187): one warp per Gaussian, lanes over
+// channels; prefix/suffix products, 4-corner scatter, bilinear derivatives.
+// ---------------------------------------------------------------------------
+struct HexBwdArgs {
+  TcPlan p;
+  int64_t K;
+  const float* pos;
+  const float* dlat;
+  const float* g_pos;
+  float* cg_pos;
+  float* gplanes[FS4D_MAX_LEVELS][6];
+  int accumulate;
+};
+
+constexpr int kHexBwdWarps = 8;
+
+__global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a) {
+  const TcPlan& p = a.p;
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * kHexBwdWarps + (threadIdx.x >> 5);
+  if (k >= a.K) return;
+  const int C = p.C;
+  double c[4] = {0.0, 0.0, 0.0, p.t};
+  bool inside[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double raw = ((double)a.pos[3 * k + q] - p.lo[q]) / p.span[q];
+    inside[q] = raw > 0.0 && raw < 1.0;
+    c[q] = fmin(fmax(raw, 0.0), 1.0);
+  }
+  float dco[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int l = 0; l < p.levels; ++l) {
+    int base[6], rs[6];
+    float fa[6], fb[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int ra = p.res[l][q][0], rb = p.res[l][q][1];
+      const double u = c[c_axes_bwd[q][0]] * (ra - 1), v = c[c_axes_bwd[q][1]] * (rb - 1);
+      int i0 = (int)floor(u), j0 = (int)floor(v);
+      i0 = min(max(i0, 0), ra - 2);
+      j0 = min(max(j0, 0), rb - 2);
+      base[q] = (i0 * rb + j0) * C;
+      rs[q] = rb * C;
+      fa[q] = (float)(u - i0);
+      fb[q] = (float)(v - j0);
+    }
+    float sa[6], sb[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sa[q] = sb[q] = 0.f;
+    for (int ch = lane; ch < C; ch += 32) {
+      float s[6], d_a[6], d_b[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const float* pl = p.planes[l][q] + base[q] + ch;
+        const float p00 = __ldg(pl), p01 = __ldg(pl + C), p10 = __ldg(pl + rs[q]), p11 = __ldg(pl + rs[q] + C);
+        s[q] = (1.f - fa[q]) * (1.f - fb[q]) * p00 + fa[q] * (1.f - fb[q]) * p10 + (1.f - fa[q]) * fb[q] * p01 +
+               fa[q] * fb[q] * p11;
+        d_a[q] = (1.f - fb[q]) * (p10 - p00) + fb[q] * (p11 - p01);
+        d_b[q] = (1.f - fa[q]) * (p01 - p00) + fa[q] * (p11 - p10);
+      }
+      float pre[6], suf[6];
+      pre[0] = 1.f;
+#pragma unroll
+      for (int q = 1; q < 6; ++q) pre[q] = pre[q - 1] * s[q - 1];
+      suf[5] = 1.f;
+#pragma unroll
+      for (int q = 4; q >= 0; --q) suf[q] = suf[q + 1] * s[q + 1];
+      const float up = a.dlat[k * 64 + l * C + ch];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const float coef = up * pre[q] * suf[q];
+        if (coef != 0.f) {
+          float* gp = a.gplanes[l][q] + base[q] + ch;
+          red_add(gp, coef * (1.f - fa[q]) * (1.f - fb[q]));
+          red_add(gp + rs[q], coef * fa[q] * (1.f - fb[q]));
+          red_add(gp + C, coef * (1.f - fa[q]) * fb[q]);
+          red_add(gp + rs[q] + C, coef * fa[q] * fb[q]);
+        }
+        sa[q] += coef * d_a[q];
+        sb[q] += coef * d_b[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        sa[q] += __shfl_xor_sync(0xffffffffu, sa[q], off);
+        sb[q] += __shfl_xor_sync(0xffffffffu, sb[q], off);
+      }
+      dco[c_axes_bwd[q][0]] += sa[q] * (float)(p.res[l][q][0] - 1);
+      dco[c_axes_bwd[q][1]] += sb[q] * (float)(p.res[l][q][1] - 1);
+    }
+  }
+  if (lane < 3) {
+    const float d = inside[lane] ? (float)((double)dco[lane] / p.span[lane]) : 0.f;
+    a.cg_pos[3 * k + lane] = (a.accumulate ? a.cg_pos[3 * k + lane] : 0.f) + a.g_pos[3 * k + lane] + d;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host driver (after deform_backward's pass-through and plane-gradient reset)
+// ---------------------------------------------------------------------------
+int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
+                       const uint8_t* cache, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
+                       Fs4dHexPlane* pg, int accumulate, void* ws, int32_t* status, cudaStream_t s) {
+  TcPlan p;
+  uint8_t* blob = (uint8_t*)ws;
+  int rc = tc_pack(net, field, t, p, blob, s);
+  if (rc) return rc;
+  const int64_t K = cloud.K;
+  char* base = (char*)ws + (p.blob_bytes + 255) / 256 * 256;
+  float* dlat = (float*)base;
+  float* wpart = (float*)(base + ((size_t)K * 64 * 4 + 255) / 256 * 256);
+  const int64_t ntiles = ceil_div(K, kTcRows);
+  const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
+  if (K > 0) {
+    BwdArgs a;
+    a.p = p;
+    a.K = K;
+    a.blob = blob;
+    a.cache = cache;
+    a.g_pos = sg.positions;
+    a.g_rot = sg.rotations;
+    a.g_ls = sg.log_scales;
+    a.g_op = sg.opacity_logits;
+    a.g_feat = sg.features;
+    a.dlat = dlat;
+    a.wpart = wpart;
+    a.status = status;
+    const int smem = ((p.blob_bytes + 1023) & ~1023) + kRBytes;
+    if (smem > 227 * 1024) return fail(FS4D_ERR_CONFIG, "tcgen05 backward exceeds shared memory");
+    cudaFuncSetAttribute(k_mlp_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mlp_bwd_tc<<<grid, kBwdThreads, smem, s>>>(a);
+
+    HexBwdArgs h;
+    h.p = p;
+    h.K = K;
+    h.pos = cloud.positions;
+    h.dlat = dlat;
+    h.g_pos = sg.positions;
+    h.cg_pos = cg.positions;
+    for (int l = 0; l < FS4D_MAX_LEVELS; ++l)
+      for (int q = 0; q < 6; ++q) h.gplanes[l][q] = l < field.levels ? pg->planes[l][q] : nullptr;
+    h.accumulate = accumulate;
+    k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
+  }
+  DwReduceArgs r;
+  memset(&r, 0, sizeof(r));
+  int n = 0;
+  auto map = [&](Fs4dLinear& g, int col0, int lane0, int bias_lane, int bias_tail) {
+    DwMap& m = r.m[n++];
+    m.gw = g.weight;
+    m.gb = g.bias;
+    m.out = g.out_dim;
+    m.in = g.in_dim;
+    m.col0 = col0;
+    m.lane0 = lane0;
+    m.bias_lane = bias_lane;
+    m.bias_tail = bias_tail;
+  };
+  const int hoff[4] = {0, 3, 7, 10};
+  map(ng.trunk[0], kDwTrunk, 0, 64, 0);
+  for (int b = 0; b < 4; ++b) map(ng.ext[b][0], kDwExt0 + 32 * b, 0, 64, 0);
+  for (int b = 0; b < 4; ++b) map(ng.ext[b][1], kDwExt1 + 32 * b, 0, 32, 0);
+  for (int b = 0; b < 4; ++b) map(ng.head[b], kDwHead + hoff[b], 32 * b, -1, hoff[b]);
+  map(ng.feat[0], kDwF1, 0, -1, 16);
+  map(ng.feat[1], kDwF2, 0, 32, 0);
+  for (int i = 0; i < n; ++i)
+    if (!r.m[i].gw || !r.m[i].gb) return fail(FS4D_ERR_CONFIG, "missing net gradient buffer");
+  r.wpart = wpart;
+  r.nparts = K > 0 ? grid : 0;
+  r.accumulate = accumulate;
+  k_reduce_tc_wgrads<<<dim3(8, n), 256, 0, s>>>(r);
+  return check_launch("deform_bwd_tc");
+}
+
+}  // namespace fs4d

@@ -19,29 +19,9 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include "common.cuh"
+#include "tc_common.cuh"
 
 namespace fs4d {
-
-// ---------------------------------------------------------------------------
-// shared declarations with deform.cu
-// ---------------------------------------------------------------------------
-struct TcPlan {
-  int depth, D, DP, enable_feat, enable_grid;
-  int levels, C, L;
-  int res[FS4D_MAX_LEVELS][6][2];
-  const float* planes[FS4D_MAX_LEVELS][6];
-  double lo[3], span[3];
-  double t;
-  // packed blob offsets (bytes)
-  int off_trunk[FS4D_MAX_TRUNK], off_ext0, off_ext1[4], off_head[4], off_f1, off_f2;
-  int off_b_trunk[FS4D_MAX_TRUNK], off_b_ext0, off_b_ext1, off_b_head, off_b_f1, off_b_f2;
-  int blob_bytes;
-};
-
-constexpr int kTcRows = 128;       // M tile (TMEM lanes)
-constexpr int kTcThreads = 256;    // two threads per row (column halves)
-constexpr int kTmemCols = 256;
 
 __constant__ int c_axes_tc[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};  // hexplane.py:16
 
@@ -180,13 +160,6 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPla
 // ---------------------------------------------------------------------------
 // weight packing: fp32 [out,in] -> bf16 hi/lo K-major core-matrix operands
 // ---------------------------------------------------------------------------
-// Byte offset of element (r, k) in an operand block with KT columns:
-//   8-row x 16-byte core matrices; K chunks of 8 elements 128 B apart (LBO),
-//   8-row groups KT*16 B apart (SBO).
-__host__ __device__ inline int core_off(int r, int k, int KT) {
-  return (r >> 3) * (KT * 16) + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
-}
-
 struct TcSrc {
   const float* w;  // [rows, in] row-major
   int rows, in, row0;
@@ -239,117 +212,6 @@ __global__ void k_pack_tc(TcPackArgs a) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// tcgen05 helpers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// K-major SWIZZLE_NONE shared-memory matrix descriptor (sm_100 version bit 46)
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
-
-// kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major, M = 128
-__device__ __forceinline__ uint32_t idesc_bf16(int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTcRows >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
-      "r"(phase)
-      : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-  uint32_t r[8];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
-  uint32_t r[4];
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// A[M=128][KT] (hi block then lo block at +128*KT*2 bytes) times B[N][KT]
-// (hi, lo) into TMEM columns [col, col+N): hi*hi + hi*lo + lo*hi, K steps of 16.
-// A columns [a_k0, a_k0 + 16*ksteps) against B columns [b_k0, ...); the first
-// MMA overwrites the accumulator unless `accumulate` is set.
-__device__ __forceinline__ void gemm_bf16x3(uint32_t tmem_d, uint32_t a_base, int a_kt, int a_k0, uint32_t b_base,
-                                            int b_kt, int b_k0, int N, int ksteps, bool accumulate) {
-  const uint32_t id = idesc_bf16(N);
-  const uint32_t a_lo = a_base + kTcRows * a_kt * 2, b_lo = b_base + N * b_kt * 2;
-  const uint32_t a_sbo = a_kt * 16, b_sbo = b_kt * 16;
-#pragma unroll 1
-  for (int s = 0; s < ksteps; ++s) {
-    const uint32_t ak = (uint32_t)(((a_k0 >> 3) + 2 * s) * 128), bk = (uint32_t)(((b_k0 >> 3) + 2 * s) * 128);
-    const uint64_t ah = sdesc(a_base + ak, 128, a_sbo), al = sdesc(a_lo + ak, 128, a_sbo);
-    const uint64_t bh = sdesc(b_base + bk, 128, b_sbo), bl = sdesc(b_lo + bk, 128, b_sbo);
-    mma_bf16(tmem_d, ah, bh, id, (s > 0 || accumulate) ? 1u : 0u);
-    mma_bf16(tmem_d, ah, bl, id, 1u);
-    mma_bf16(tmem_d, al, bh, id, 1u);
-  }
-}
-
-// store 8 consecutive values (k0..k0+7) of row r into an A operand (hi, lo) with KT columns
-__device__ __forceinline__ void store_split8(uint8_t* a_base, int KT, int r, int k0, const float* v) {
-  __nv_bfloat16 h[8], l[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    h[i] = __float2bfloat16_rn(v[i]);
-    l[i] = __float2bfloat16_rn(v[i] - __bfloat162float(h[i]));
-  }
-  const int off = core_off(r, k0, KT);
-  *reinterpret_cast<uint4*>(a_base + off) = *reinterpret_cast<const uint4*>(h);
-  *reinterpret_cast<uint4*>(a_base + kTcRows * KT * 2 + off) = *reinterpret_cast<const uint4*>(l);
-}
-
 struct TcArgs {
   TcPlan p;
   int64_t K;
@@ -365,13 +227,31 @@ struct TcArgs {
   float* o_ls;
   float* o_op;
   float* o_feat;
+  uint8_t* cache;  // deform_with_cache activation images (tc_common.cuh), or null
 };
+
+// the same 8 values into a cached row image in global memory
+__device__ __forceinline__ void cache_split8(uint8_t* img, int KT, int r, int k0, const float* v) {
+  uint4 h, l;
+  split8(v, h, l);
+  const int off = core_off(r, k0, KT);
+  *reinterpret_cast<uint4*>(img + off) = h;
+  *reinterpret_cast<uint4*>(img + kTcRows * KT * 2 + off) = l;
+}
+
+// the bias column block (1, 0, ..., 0) at column `at` of a cached image
+__device__ __forceinline__ void cache_ones(uint8_t* img, int KT, int r, int at) {
+  const int off = core_off(r, at, KT);
+  *reinterpret_cast<uint4*>(img + off) = make_uint4(0x3F80u, 0u, 0u, 0u);
+  *reinterpret_cast<uint4*>(img + kTcRows * KT * 2 + off) = make_uint4(0u, 0u, 0u, 0u);
+}
 
 // one accumulator region [col, col+n) -> bias -> (relu) -> split -> A operand
 // columns [k0, k0+n).  Two threads share a row: `half` takes the even or odd
 // 8-column chunks.
 __device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, int n, const float* bias, bool relu,
-                                                    uint8_t* a_base, int KT, int k0, int r, int half) {
+                                                    uint8_t* a_base, int KT, int k0, int r, int half,
+                                                    uint8_t* cimg = nullptr, int cKT = 0, int ck0 = 0) {
   for (int c = 8 * half; c < n; c += 16) {
     float v[8];
     tmem_ld8(tmem_row + col + c, v);
@@ -381,6 +261,7 @@ __device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, 
       if (relu) v[i] = fmaxf(v[i], 0.f);
     }
     store_split8(a_base, KT, r, k0 + c, v);
+    if (cimg) cache_split8(cimg, cKT, r, ck0 + c, v);
   }
 }
 
@@ -395,9 +276,6 @@ __device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, 
 constexpr int kTcEpiThreads = 256;
 constexpr int kTcWsThreads = kTcEpiThreads + 32;
 
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
 
 constexpr int kTcProducerThreads = 128;  // fused variant: 4 HexPlane producer warps
 constexpr int kTcFusedThreads = kTcWsThreads + kTcProducerThreads;
@@ -474,7 +352,7 @@ __device__ __forceinline__ void produce_latent(const TcArgs& a, int64_t tile, ui
   }
 }
 
-template <bool FUSED>
+template <bool FUSED, bool CACHE>
 __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   // one operand barrier per hand-off slot of a tile (a thread may run ahead by
@@ -484,7 +362,7 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
   __shared__ uint32_t tmem_base_sh;
   const TcPlan& p = a.p;
   uint8_t* W = smem;
-  const int wbytes = (p.blob_bytes + 1023) & ~1023;
+  const int wbytes = (p.fwd_bytes + 1023) & ~1023;
   // X: [128 x 64] hi + lo (32 KB) -- two of them in the fused kernel (the
   // producers fill tile i+1's while tile i runs); E: [128 x 128] hi + lo (64 KB)
   uint8_t* Xb[2] = {smem + wbytes, smem + wbytes + (FUSED ? kTcRows * 64 * 4 : 0)};
@@ -493,7 +371,13 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
   const bool mma_warp = warp == kTcEpiThreads / 32;
   const bool producer = FUSED && warp > kTcEpiThreads / 32;
 
-  for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
+  if (CACHE && blockIdx.x == 0 && tid == 0) {
+    CacheHeader* h = reinterpret_cast<CacheHeader*>(a.cache);
+    h->magic = kCacheMagic;
+    h->K = a.K;
+    h->t = p.t;
+  }
+  for (int e = tid; e < p.fwd_bytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
   const uint32_t accbar = smem_u32(&accbar_s), opbar = smem_u32(&opbar_s[0]);
   const uint32_t xfull = smem_u32(&xfull_s[0]), xempty = smem_u32(&xempty_s[0]);
@@ -644,11 +528,23 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
         const int c = 8 * half + 16 * (q / 8) + (q % 8);
         fv[q] = (valid && p.enable_feat && c < p.D && p.DP <= 32) ? a.feat[(int64_t)p.D * k + c] : 0.f;
       }
+      uint8_t* ct = CACHE ? a.cache + kCacheHeader + tile * (int64_t)kCacheTileBytes : nullptr;
+      if (CACHE) {
+        if (half == 0) {
+          cache_ones(ct + kCacheLat, kCacheKtLat, row, 64);
+          cache_ones(ct + kCacheHid, kCacheKtHid, row, 64);
+          cache_ones(ct + kCacheFF, kCacheKtFF, row, 32);
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) cache_ones(ct + kCacheE1 + b * kCacheE1Bytes, kCacheKtE1, row, 32);
+        }
+      }
       if (!FUSED) {
 #pragma unroll
         for (int c = 0; c < 8; c += 2) {
           float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
           store_split8(X, 64, row, 32 * half + 4 * c, v);
+          if (CACHE) cache_split8(ct + kCacheLat, kCacheKtLat, row, 32 * half + 4 * c, v);
         }
         load_latent(tile + gridDim.x);
         signal();
@@ -661,19 +557,22 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
           signal();
         } else {
           for (int c = 0; c < 64; c += 16) {
-            epilogue_to_operand(tmem_row, 128 + c, 16, tb + c, true, X, 64, c, row, half);
+            epilogue_to_operand(tmem_row, 128 + c, 16, tb + c, true, X, 64, c, row, half,
+                                CACHE ? ct + kCacheHid : nullptr, kCacheKtHid, c);
             signal();
           }
         }
       }
       wait_acc();
       for (int b = 0; b < 4; ++b) {
-        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext0 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
+        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext0 / 4 + 32 * b, true, E, 128, 32 * b, row, half,
+                            CACHE ? ct + kCacheE1 + b * kCacheE1Bytes : nullptr, kCacheKtE1, 0);
         signal();
       }
       wait_acc();
       for (int b = 0; b < 4; ++b) {
-        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext1 / 4 + 32 * b, true, E, 128, 32 * b, row, half);
+        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext1 / 4 + 32 * b, true, E, 128, 32 * b, row, half,
+                            CACHE ? ct + kCacheE2 : nullptr, kCacheKtE2, 32 * b);
         signal();
       }
       wait_acc();
@@ -696,7 +595,8 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
         }
       }
       if (p.enable_feat) {
-        epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, X, 32, 0, row, half);
+        epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, X, 32, 0, row, half,
+                            CACHE ? ct + kCacheFF : nullptr, kCacheKtFF, 0);
         signal();
         wait_acc();
         const float* fb = bias_f + p.off_b_f2 / 4;
@@ -814,15 +714,46 @@ static int build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, T
   if (pk) pk->bias[nb++] = TcBias{32, p.off_b_f1, 1, {n.feat[0].bias}, {32}, {0}};
   p.off_b_f2 = bias(p.DP);
   if (pk) pk->bias[nb++] = TcBias{p.DP, p.off_b_f2, 1, {n.feat[1].bias}, {p.D}, {0}};
+  // backward-only images after everything the forward kernel stages
+  p.fwd_bytes = (off + 15) / 16 * 16;
+  off = p.fwd_bytes;
+  const int hoff[4] = {0, 3, 7, 10};
+  for (int b = 0; b < 4; ++b) {
+    p.off_headT[b] = operand(16, 32);
+    if (pk) pk->op[nop++] = TcOperand{16, 32, p.off_headT[b], 1, {src(n.head[b], hoff[b])}};
+  }
   p.blob_bytes = (off + 15) / 16 * 16;
   if (pk) {
     pk->nop = nop;
     pk->nbias = nb;
   }
   // shared memory: weights + X + E must fit
-  const int smem = ((p.blob_bytes + 1023) & ~1023) + kTcRows * 64 * 4 + kTcRows * 128 * 4;
+  const int smem = ((p.fwd_bytes + 1023) & ~1023) + kTcRows * 64 * 4 + kTcRows * 128 * 4;
   if (smem > 227 * 1024) return fail(FS4D_ERR_CONFIG, "tcgen05 MLP weights exceed shared memory");
   return FS4D_OK;
+}
+
+int tc_build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p) {
+  return build_plan(n, f, t, p, nullptr);
+}
+
+int tc_pack(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p, uint8_t* blob, cudaStream_t s) {
+  static TcPackArgs pk;  // large: keep off the stack (host-side, filled per call)
+  int rc = build_plan(n, f, t, p, &pk);
+  if (rc) return rc;
+  pk.blob = blob;
+  k_pack_tc<<<dim3(4, pk.nop + pk.nbias), 256, 0, s>>>(pk);
+  return check_launch("deform_tc_pack");
+}
+
+bool tc_bwd_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f) {
+  return tc_path_ok(n, f) && n.depth == 1 && n.enable_grid && n.enable_feature_update && n.feature_dim > 0 &&
+         n.feature_dim <= 16 && f.levels * f.channels == 64;
+}
+
+size_t tc_cache_bytes(const Fs4dDeformNet& n, const Fs4dHexPlane& f, int64_t K) {
+  if (!tc_bwd_ok(n, f)) return 0;
+  return (size_t)kCacheHeader + (size_t)ceil_div(K, kTcRows) * kCacheTileBytes;
 }
 
 size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K) {
@@ -830,27 +761,25 @@ size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K) {
   memset(&f, 0, sizeof(f));
   TcPlan p;
   build_plan(n, f, 0.0, p, nullptr);
-  return (size_t)((p.blob_bytes + 255) / 256 * 256) + (size_t)K * 64 * 4 + 256;
+  // forward: latent [K, 64]; backward: d_latent [K, 64] + one weight-gradient partial per SM
+  return (size_t)((p.blob_bytes + 255) / 256 * 256) + (size_t)K * 64 * 4 + (size_t)kNumSMs * kPartStride * 4 + 512;
 }
 
 int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
-                      Fs4dCloud& snap, void* ws, cudaStream_t s) {
+                      Fs4dCloud& snap, void* ws, uint8_t* cache, cudaStream_t s) {
   TcPlan p;
-  static TcPackArgs pk;  // large: keep off the stack (host-side, filled per call)
-  int rc = build_plan(net, field, t, p, &pk);
-  if (rc) return rc;
   uint8_t* blob = (uint8_t*)ws;
+  int rc = tc_pack(net, field, t, p, blob, s);
+  if (rc) return rc;
   float* latent = (float*)((char*)ws + (p.blob_bytes + 255) / 256 * 256);
-  pk.blob = blob;
-  k_pack_tc<<<dim3(4, pk.nop + pk.nbias), 256, 0, s>>>(pk);
   const int64_t K = cloud.K;
-  if (K == 0) return check_launch("deform_tc_pack");
+  if (K == 0) return FS4D_OK;
   // The fused variant (HexPlane gather as 4 producer warps inside the MLP
   // kernel, latent never leaves shared memory) is correct but measured slower
   // on B200 (355 vs 228 us at configs[1]): 4 producer warps per SM expose far
   // less memory-level parallelism than the stand-alone gather at full
   // occupancy.  It stays opt-in (FS4D_FUSED_GATHER=1).
-  const bool fused = getenv("FS4D_FUSED_GATHER") && (!p.enable_grid || (p.C == 32 && p.levels == 2));
+  const bool fused = !cache && getenv("FS4D_FUSED_GATHER") && (!p.enable_grid || (p.C == 32 && p.levels == 2));
   const unsigned gblocks = (unsigned)ceil_div(K, kGatherWarps * 32);
   if (!fused) {
     if (p.enable_grid && p.C == 32 && p.levels == 2)
@@ -873,15 +802,19 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   a.o_ls = snap.log_scales;
   a.o_op = snap.opacity_logits;
   a.o_feat = snap.features;
-  const int smem = ((p.blob_bytes + 1023) & ~1023) + kTcRows * 64 * 4 * (fused ? 2 : 1) + kTcRows * 128 * 4;
+  a.cache = cache;
+  const int smem = ((p.fwd_bytes + 1023) & ~1023) + kTcRows * 64 * 4 * (fused ? 2 : 1) + kTcRows * 128 * 4;
   const int64_t ntiles = ceil_div(K, kTcRows);
   const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
   if (fused) {
-    cudaFuncSetAttribute(k_mlp_tc_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_mlp_tc_ws<true><<<grid, kTcFusedThreads, smem, s>>>(a);
+    cudaFuncSetAttribute(k_mlp_tc_ws<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mlp_tc_ws<true, false><<<grid, kTcFusedThreads, smem, s>>>(a);
+  } else if (cache) {
+    cudaFuncSetAttribute(k_mlp_tc_ws<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mlp_tc_ws<false, true><<<grid, kTcWsThreads, smem, s>>>(a);
   } else {
-    cudaFuncSetAttribute(k_mlp_tc_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_mlp_tc_ws<false><<<grid, kTcWsThreads, smem, s>>>(a);
+    cudaFuncSetAttribute(k_mlp_tc_ws<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mlp_tc_ws<false, false><<<grid, kTcWsThreads, smem, s>>>(a);
   }
   return check_launch("deform_tc");
 }

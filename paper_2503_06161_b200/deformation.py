@@ -85,18 +85,26 @@ def _host(t):
 
 
 def deform(cloud, field, net, t):
-    snapshot, _ = deform_with_cache(cloud, field, net, t)
+    snapshot, _ = _deform(cloud, field, net, t, False)
     return snapshot
 
 
 def deform_with_cache(cloud, field, net, t):
     """Snapshot of the cloud at time t plus the backward record
     (deformation.py:105-136)."""
+    return _deform(cloud, field, net, t, True)
+
+
+def _deform(cloud, field, net, t, want_cache):
     if net.cfg.enable_grid and net.latent_dim != field.latent_dim:
         raise ConfigurationError(
             f"input dim {field.latent_dim} does not match first layer in_dim {net.latent_dim}")
     dc, df, dn = _device_parts(cloud, field, net)
-    snap = _engine().forward(dc, df, dn, t)
+    dcache = None
+    if want_cache:
+        snap, dcache = _engine().forward(dc, df, dn, t, with_cache=True)
+    else:
+        snap = _engine().forward(dc, df, dn, t)
     k = len(cloud)
     snapshot = GaussianCloud(
         positions=_host(snap.positions).reshape(k, 3),
@@ -110,7 +118,7 @@ def deform_with_cache(cloud, field, net, t):
         sh_rest=getattr(cloud, "sh_rest", None),
     )
     cache = {"k": k, "t": float(t), "query": None if not net.cfg.enable_grid else "device",
-             "feat": "device" if net.cfg.enable_feature_update else None}
+             "feat": "device" if net.cfg.enable_feature_update else None, "device": dcache}
     return snapshot, cache
 
 
@@ -134,7 +142,7 @@ def deform_backward(cloud, field, net, cache, grads):
     feats = up("features", (k, d)) if net.cfg.enable_feature_update else torch.zeros(k, d, **f32)
     sg = DeviceCloud(up("positions", (k, 3)), up("rotations", (k, 4)), up("log_scales", (k, 3)),
                      up("opacity_logits", (k,)), torch.zeros(k, 3, **f32), feats)
-    gpos, ngrads, pgrads = _engine().backward(dc, df, dn, cache["t"], sg)
+    gpos, ngrads, pgrads = _engine().backward(dc, df, dn, cache["t"], sg, cache=cache.get("device"))
 
     cloud_grads = {
         "positions": _host(gpos).reshape(k, 3),

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import ConfigurationError
+from .errors import ConfigurationError, ContractViolation
 
 BRANCHES = ("position", "rotation", "scale", "opacity")
 BRANCH_DIMS = (3, 4, 3, 1)
@@ -247,12 +247,32 @@ class DeviceNet:
         return s
 
 
+class DeformCache:
+    """Device counterpart of deform_with_cache's `cache` (deformation.py:105):
+    the tensor-core operand images of every MLP activation, written by
+    DeformEngine.forward(with_cache=...) and read by DeformEngine.backward.
+    Empty (0 bytes) when the net is outside the tensor-core backward, whose
+    fallback recomputes the forward."""
+
+    def __init__(self, nbytes, device):
+        self.buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+        self.nbytes = int(nbytes)
+        self.t = None
+        self.k = None
+
+    def ptr(self):
+        return self.buf.data_ptr() if self.nbytes else None
+
+
 class DeformEngine:
     """Runs fs4d_deform_fwd / fs4d_deform_bwd with a cached workspace."""
 
     def __init__(self, device="cuda"):
         self.device = device
         self.ws = None
+
+    def cache_bytes(self, net, field, k):
+        return int(N.load().fs4d_deform_cache_bytes(ctypes.byref(net.struct()), ctypes.byref(field.struct()), k))
 
     def _workspace(self, net_s, k):
         need = N.load().fs4d_deform_workspace_bytes(ctypes.byref(net_s), k)
@@ -262,9 +282,19 @@ class DeformEngine:
             self.ws = torch.empty(int(need), dtype=torch.uint8, device=self.device)
         return self.ws
 
-    def forward(self, cloud, field, net, t, out=None):
-        """Snapshot at time t (raw-space deltas; colours/SH aliased)."""
+    def forward(self, cloud, field, net, t, out=None, with_cache=None):
+        """Snapshot at time t (raw-space deltas; colours/SH aliased).
+        with_cache=True (or a DeformCache to reuse) is deform_with_cache:
+        returns (snapshot, cache)."""
         k = len(cloud)
+        cache = None
+        if with_cache is not None and with_cache is not False:
+            need = self.cache_bytes(net, field, k)
+            cache = with_cache if isinstance(with_cache, DeformCache) else None
+            if cache is None or cache.buf.numel() < need:
+                cache = DeformCache(need, self.device)
+            cache.nbytes = need
+            cache.t, cache.k = float(t), k
         if out is None:
             out = DeviceCloud.empty(k, cloud.feature_dim, 0, self.device)
         out.colors_raw = cloud.colors_raw
@@ -273,13 +303,14 @@ class DeformEngine:
             out.features = cloud.features
         cs, fs, ns, os_ = cloud.struct(), field.struct(), net.struct(), out.struct()
         ws = self._workspace(ns, k)
+        cptr, cbytes = (cache.ptr(), cache.nbytes) if cache is not None else (None, 0)
         N.check(N.load().fs4d_deform_fwd(ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns),
-                                         float(t), ctypes.byref(os_), _p(ws), ws.numel(), None,
-                                         _stream()))
-        return out
+                                         float(t), ctypes.byref(os_), cptr, cbytes, _p(ws), ws.numel(),
+                                         None, _stream()))
+        return (out, cache) if cache is not None else out
 
     def backward(self, cloud, field, net, t, snap_grads, cloud_grads=None, net_grads=None,
-                 plane_grads=None, accumulate=False):
+                 plane_grads=None, accumulate=False, cache=None):
         """deform_backward on device.  Without output buffers: returns
         (d_positions [K,3], net_grads DeviceNet, plane_grads DeviceField|None).
         With a DeviceCloud `cloud_grads` (+ net/plane grads) every cloud
@@ -300,8 +331,11 @@ class DeformEngine:
             cgs = cloud_grads.struct()
         pgs = pgrads.struct() if pgrads is not None else None
         ws = self._workspace(ns, k)
+        if cache is not None and (cache.k != k or cache.t != float(t)):
+            raise ContractViolation("deform cache was made for another (cloud, t)")
+        cptr, cbytes = (cache.ptr(), cache.nbytes) if cache is not None else (None, 0)
         N.check(N.load().fs4d_deform_bwd(ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns),
-                                         float(t), ctypes.byref(sgs), ctypes.byref(cgs),
+                                         float(t), cptr, cbytes, ctypes.byref(sgs), ctypes.byref(cgs),
                                          ctypes.byref(ngs),
                                          ctypes.byref(pgs) if pgs is not None else None,
                                          int(bool(accumulate)), _p(ws), ws.numel(), None, _stream()))
@@ -529,7 +563,7 @@ class FramePipeline:
                 c["cam"] = camera_struct(K, T, self.h, self.w)
                 c["cam_key"] = key
             N.check(lib.fs4d_deform_fwd(ctypes.byref(c["cloud"]), ctypes.byref(c["field"]), ctypes.byref(c["net"]),
-                                        float(t), ctypes.byref(c["snap"]), c["dws"], c["dws_n"], None, s))
+                                        float(t), ctypes.byref(c["snap"]), None, 0, c["dws"], c["dws_n"], None, s))
             N.check(lib.fs4d_status_reset(c["status"], s))
             N.check(lib.fs4d_render_fwd(ctypes.byref(c["snap"]), ctypes.byref(c["cam"]), ctypes.byref(c["raster"]),
                                         ctypes.byref(c["info"]), c["rws"], c["rws_n"], ctypes.byref(c["imgs"]),

@@ -50,6 +50,7 @@ class TrainStep:
         self.d_color = torch.empty(self.h, self.w, 3, **f)
         self.d_feature = torch.empty(self.h, self.w, dout, **f)
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+        self.cache = None  # deform_with_cache activations, reused pair to pair
 
     def run(self, batch, check=False):
         """batch: list of (t, K, T, target_rgb [H,W,3] cuda, target_feat [H,W,D] cuda).
@@ -60,7 +61,8 @@ class TrainStep:
         self.loss.zero_()
         dout = self.d_feature.shape[2]
         for i, (t, K, T, tgt_rgb, tgt_feat) in enumerate(batch):
-            self.deformer.forward(self.cloud, self.field, self.net, t, out=self.snap)
+            _, self.cache = self.deformer.forward(self.cloud, self.field, self.net, t, out=self.snap,
+                                                  with_cache=self.cache or True)
             imgs, rec = self.renderer.forward(self.snap, K, T, self.h, self.w, self.cfg, images=self.images,
                                               check=check)
             N.check(lib.fs4d_l1_loss_grad(_p(imgs["color"]), _p(tgt_rgb), _p(imgs["feature"]) if dout else None,
@@ -72,7 +74,7 @@ class TrainStep:
             self.deformer.backward(self.cloud, self.field, self.net, t, self.snap_grads,
                                    cloud_grads=self.cloud_grads, net_grads=self.net_grads,
                                    plane_grads=self.plane_grads if self.net.enable_grid else None,
-                                   accumulate=i > 0)
+                                   accumulate=i > 0, cache=self.cache)
         self.grads.allreduce_sum(self.group)
         if self.world > 1:
             import torch.distributed as dist
