@@ -487,6 +487,197 @@ __global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a
   }
 }
 
+// 32-channel, 2-level planes (configs[1..4]).  One warp per 32 Gaussians:
+// lane j first selects Gaussian j's 12 bilinear cells in fp64 (kept in
+// registers, fetched by shuffle), then four Gaussians at a time lanes
+// (Gaussian, channel quad) fetch float4 corner rows.  The three time planes
+// of a level share one t row pair for every Gaussian, so their scatter is
+// reduced per CTA in shared memory over the spatial index only ([Ra][32]
+// per plane, the (1-fb, fb) split applied once at the flush); the spatial
+// planes scatter with red.global.add.v4.f32.
+constexpr int kHexC32Warps = 8;
+struct HexC32Args {
+  HexBwdArgs h;
+  int toff[2][3];  // shared-memory offsets (floats) of the time-plane accumulators
+  int tfloats;
+};
+
+__device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 || q == 5; }
+
+__global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC32Args A) {
+  extern __shared__ float tacc[];
+  const HexBwdArgs& a = A.h;
+  const TcPlan& p = a.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < A.tfloats; i += blockDim.x) tacc[i] = 0.f;
+  __syncthreads();
+  // the shared t cell of each level (hexplane.py:95-110 on the time axis)
+  int tj0[2];
+  float tfb[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    const int rt = p.res[l][2][1];
+    const double v = p.t * (rt - 1);
+    int j0 = (int)floor(v);
+    j0 = min(max(j0, 0), rt - 2);
+    tj0[l] = j0;
+    tfb[l] = (float)(v - j0);
+  }
+  const int sub = lane >> 3, ch = (lane & 7) * 4;
+  const int64_t nchunks = ceil_div(a.K, 32);
+  for (int64_t chunk = (int64_t)blockIdx.x * kHexC32Warps + warp; chunk < nchunks;
+       chunk += (int64_t)gridDim.x * kHexC32Warps) {
+    const int64_t g0 = chunk * 32;
+    // lane j: cells of Gaussian g0 + j (fp64 coordinates, hexplane.py:84-110)
+    int cell[12];  // spatial planes: element offset of corner 00; time planes: i0
+    float fa[12], fb[12];
+    uint32_t inside = 0;
+    {
+      const int64_t kl = g0 + lane;
+      double c[4] = {0.0, 0.0, 0.0, p.t};
+      if (kl < a.K) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const double raw = ((double)a.pos[3 * kl + q] - p.lo[q]) / p.span[q];
+          if (raw > 0.0 && raw < 1.0) inside |= 1u << q;
+          c[q] = fmin(fmax(raw, 0.0), 1.0);
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < 2; ++l)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int ra = p.res[l][q][0], rb = p.res[l][q][1];
+          const double u = c[c_axes_bwd[q][0]] * (ra - 1), v = c[c_axes_bwd[q][1]] * (rb - 1);
+          int i0 = (int)floor(u), j0 = (int)floor(v);
+          i0 = min(max(i0, 0), ra - 2);
+          j0 = min(max(j0, 0), rb - 2);
+          cell[l * 6 + q] = is_time_plane(q) ? i0 : (i0 * rb + j0) * 32;
+          fa[l * 6 + q] = (float)(u - i0);
+          fb[l * 6 + q] = (float)(v - j0);
+        }
+    }
+    for (int jj = 0; jj < 32; jj += 4) {
+      const int j = jj + sub;
+      const int64_t k = g0 + j;
+      const bool ok = k < a.K;
+      float dco[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        float4 s[6], da[6], db[6];
+        float w_a[6], w_b[6];
+        int cb[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int idx = l * 6 + q;
+          const int rb = p.res[l][q][1];
+          const int cj = __shfl_sync(0xffffffffu, cell[idx], j);
+          w_a[q] = __shfl_sync(0xffffffffu, fa[idx], j);
+          w_b[q] = __shfl_sync(0xffffffffu, fb[idx], j);
+          cb[q] = cj;
+          const int base = is_time_plane(q) ? (cj * rb + tj0[l]) * 32 : cj;
+          const int rs = rb * 32;
+          float4 c00 = make_float4(0.f, 0.f, 0.f, 0.f), c01 = c00, c10 = c00, c11 = c00;
+          if (ok) {
+            const float* pl = p.planes[l][q] + base + ch;
+            c00 = __ldg(reinterpret_cast<const float4*>(pl));
+            c01 = __ldg(reinterpret_cast<const float4*>(pl + 32));
+            c10 = __ldg(reinterpret_cast<const float4*>(pl + rs));
+            c11 = __ldg(reinterpret_cast<const float4*>(pl + rs + 32));
+          }
+          const float f0 = w_a[q], f1 = w_b[q];
+          const float w00 = (1.f - f0) * (1.f - f1), w10 = f0 * (1.f - f1), w01 = (1.f - f0) * f1, w11 = f0 * f1;
+          s[q] = make_float4(w00 * c00.x + w10 * c10.x + w01 * c01.x + w11 * c11.x,
+                             w00 * c00.y + w10 * c10.y + w01 * c01.y + w11 * c11.y,
+                             w00 * c00.z + w10 * c10.z + w01 * c01.z + w11 * c11.z,
+                             w00 * c00.w + w10 * c10.w + w01 * c01.w + w11 * c11.w);
+          // hexplane.py:179-183 bilinear derivatives along a and b
+          da[q] = make_float4((1.f - f1) * (c10.x - c00.x) + f1 * (c11.x - c01.x),
+                              (1.f - f1) * (c10.y - c00.y) + f1 * (c11.y - c01.y),
+                              (1.f - f1) * (c10.z - c00.z) + f1 * (c11.z - c01.z),
+                              (1.f - f1) * (c10.w - c00.w) + f1 * (c11.w - c01.w));
+          db[q] = make_float4((1.f - f0) * (c01.x - c00.x) + f0 * (c11.x - c10.x),
+                              (1.f - f0) * (c01.y - c00.y) + f0 * (c11.y - c10.y),
+                              (1.f - f0) * (c01.z - c00.z) + f0 * (c11.z - c10.z),
+                              (1.f - f0) * (c01.w - c00.w) + f0 * (c11.w - c10.w));
+        }
+        if (!ok) continue;
+        const float4 up = *reinterpret_cast<const float4*>(a.dlat + k * 64 + l * 32 + ch);
+        // product of the other five planes via prefix / suffix (hexplane.py:131-139)
+        float4 pre[6], suf[6];
+        pre[0] = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+        for (int q = 1; q < 6; ++q)
+          pre[q] = make_float4(pre[q - 1].x * s[q - 1].x, pre[q - 1].y * s[q - 1].y, pre[q - 1].z * s[q - 1].z,
+                               pre[q - 1].w * s[q - 1].w);
+        suf[5] = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+        for (int q = 4; q >= 0; --q)
+          suf[q] = make_float4(suf[q + 1].x * s[q + 1].x, suf[q + 1].y * s[q + 1].y, suf[q + 1].z * s[q + 1].z,
+                               suf[q + 1].w * s[q + 1].w);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const float4 cf = make_float4(up.x * pre[q].x * suf[q].x, up.y * pre[q].y * suf[q].y,
+                                        up.z * pre[q].z * suf[q].z, up.w * pre[q].w * suf[q].w);
+          const float f0 = w_a[q], f1 = w_b[q];
+          if (is_time_plane(q)) {
+            float* acc = tacc + A.toff[l][q == 2 ? 0 : (q == 4 ? 1 : 2)] + cb[q] * 32 + ch;
+            atomicAdd(acc + 0, cf.x * (1.f - f0));
+            atomicAdd(acc + 1, cf.y * (1.f - f0));
+            atomicAdd(acc + 2, cf.z * (1.f - f0));
+            atomicAdd(acc + 3, cf.w * (1.f - f0));
+            atomicAdd(acc + 32, cf.x * f0);
+            atomicAdd(acc + 33, cf.y * f0);
+            atomicAdd(acc + 34, cf.z * f0);
+            atomicAdd(acc + 35, cf.w * f0);
+          } else {
+            const int rs = p.res[l][q][1] * 32;
+            float* gp = a.gplanes[l][q] + cb[q] + ch;
+            const float w00 = (1.f - f0) * (1.f - f1), w10 = f0 * (1.f - f1), w01 = (1.f - f0) * f1, w11 = f0 * f1;
+            red_add_v4(gp, cf.x * w00, cf.y * w00, cf.z * w00, cf.w * w00);
+            red_add_v4(gp + rs, cf.x * w10, cf.y * w10, cf.z * w10, cf.w * w10);
+            red_add_v4(gp + 32, cf.x * w01, cf.y * w01, cf.z * w01, cf.w * w01);
+            red_add_v4(gp + rs + 32, cf.x * w11, cf.y * w11, cf.z * w11, cf.w * w11);
+          }
+          const float sa = cf.x * da[q].x + cf.y * da[q].y + cf.z * da[q].z + cf.w * da[q].w;
+          const float sb = cf.x * db[q].x + cf.y * db[q].y + cf.z * db[q].z + cf.w * db[q].w;
+          dco[c_axes_bwd[q][0]] += sa * (float)(p.res[l][q][0] - 1);
+          if (c_axes_bwd[q][1] < 3) dco[c_axes_bwd[q][1]] += sb * (float)(p.res[l][q][1] - 1);
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) dco[q] += __shfl_xor_sync(0xffffffffu, dco[q], off);
+      const uint32_t ins = __shfl_sync(0xffffffffu, inside, j);
+      if (ok && (lane & 7) < 3) {
+        const int q = lane & 7;
+        const float dq = q == 0 ? dco[0] : (q == 1 ? dco[1] : dco[2]);
+        const float d = ((ins >> q) & 1u) ? (float)((double)dq / p.span[q]) : 0.f;
+        a.cg_pos[3 * k + q] = (a.accumulate ? a.cg_pos[3 * k + q] : 0.f) + a.g_pos[3 * k + q] + d;
+      }
+    }
+  }
+  __syncthreads();
+  // flush the time planes: row i0 of the spatial axis, t rows j0 / j0 + 1
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int qi = 0; qi < 3; ++qi) {
+      const int q = qi == 0 ? 2 : (qi == 1 ? 4 : 5);
+      const int ra = p.res[l][q][0], rb = p.res[l][q][1];
+      float* gp = a.gplanes[l][q];
+      const float* acc = tacc + A.toff[l][qi];
+      for (int e = threadIdx.x; e < ra * 32; e += blockDim.x) {
+        const float v = acc[e];
+        if (v == 0.f) continue;
+        const int i = e >> 5, c = e & 31;
+        red_add(gp + (i * rb + tj0[l]) * 32 + c, v * (1.f - tfb[l]));
+        red_add(gp + (i * rb + tj0[l] + 1) * 32 + c, v * tfb[l]);
+      }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host driver (after deform_backward's pass-through and plane-gradient reset)
 // ---------------------------------------------------------------------------
@@ -532,7 +723,23 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
     for (int l = 0; l < FS4D_MAX_LEVELS; ++l)
       for (int q = 0; q < 6; ++q) h.gplanes[l][q] = l < field.levels ? pg->planes[l][q] : nullptr;
     h.accumulate = accumulate;
-    k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
+    HexC32Args hc;
+    hc.h = h;
+    int tf = 0;
+    for (int l = 0; l < 2 && p.levels == 2; ++l)
+      for (int qi = 0; qi < 3; ++qi) {
+        hc.toff[l][qi] = tf;
+        tf += p.res[l][qi == 0 ? 2 : (qi == 1 ? 4 : 5)][0] * 32;
+      }
+    hc.tfloats = tf;
+    if (p.C == 32 && p.levels == 2 && tf * 4 <= 100 * 1024 && !getenv("FS4D_HEX_BWD_GENERIC")) {
+      cudaFuncSetAttribute(k_hexplane_bwd_c32, cudaFuncAttributeMaxDynamicSharedMemorySize, tf * 4);
+      const int64_t nblk = ceil_div(ceil_div(K, 32), kHexC32Warps);
+      const int grid = (int)(nblk < 2 * kNumSMs ? nblk : 2 * kNumSMs);
+      k_hexplane_bwd_c32<<<grid, kHexC32Warps * 32, tf * 4, s>>>(hc);
+    } else {
+      k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
+    }
   }
   DwReduceArgs r;
   memset(&r, 0, sizeof(r));

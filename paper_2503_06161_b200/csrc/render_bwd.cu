@@ -6,6 +6,8 @@
 //   k_blend_bwd       tile loop  rasterizer.py:349-393  (fp32, warp butterfly
 //                     reduction + one coalesced red.global per warp/Gaussian)
 //   k_preprocess_bwd  projection chain rasterizer.py:395-451 (fp64)
+#include <stdlib.h>
+
 #include "render_common.cuh"
 #include "sh.cuh"
 
@@ -95,6 +97,9 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
   __syncthreads();
   const int maxlast = s_maxlast;
   if (maxlast < (int)rg.x) return;
+  const int wlast = __reduce_max_sync(0xffffffffu, lastj);
+  const int wrow0 = ty * kTile + (threadIdx.x >> 5) * 2;  // this warp's two pixel rows
+  const int tcol0 = tx * kTile;
 
   const int nv = a.nvals;
   const uint32_t hi = (uint32_t)(maxlast + 1) < rg.y ? (uint32_t)(maxlast + 1) : rg.y;
@@ -116,7 +121,25 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
       }
     }
     __syncthreads();
-    for (int k = cnt - 1; k >= 0; --k) {
+    // warp-level culling (as in k_blend): keep the staged Gaussians whose
+    // pixel rectangle meets this warp's two pixel rows and that lie at or
+    // before the warp's last contributor, then walk them back to front
+#pragma unroll 1
+    for (int m = (cnt - 1) / 32; m >= 0; --m) {
+     unsigned bits;
+     {
+      const int kk = m * 32 + lane;
+      bool hit = false;
+      if (kk < cnt && bstart + kk <= (int64_t)wlast) {
+        const int4 pr = s_pr[kk];
+        hit = pr.w >= wrow0 && pr.z <= wrow0 + 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
+      }
+      bits = __ballot_sync(0xffffffffu, hit);
+     }
+     while (bits) {
+      const int bit = 31 - __clz(bits);
+      bits &= ~(1u << bit);
+      const int k = m * 32 + bit;
       const int64_t j = bstart + k;
       bool live = inside && j <= (int64_t)lastj;
       float v[32];
@@ -192,6 +215,175 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
         for (int c = 0; c < 32; ++c) v[c] = (base + c < DC) ? vf[base + c] : 0.f;
         float r = warp_transpose_reduce(v, lane);
         if (10 + base + lane < nv && r != 0.f) red_add(dst + 10 + base + lane, r);
+      }
+     }
+    }
+  }
+}
+
+// Same replay with PX vertically adjacent pixels per thread (256/PX threads
+// per tile, a warp covers 2*PX pixel rows).  The per-Gaussian warp reduction
+// -- the kernel's dominant cost -- is then shared by PX times as many pixels.
+template <int DC, int PX>
+__global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
+  constexpr int NT = kTilePixels / PX;
+  constexpr int B = NT;  // Gaussians staged per batch
+  constexpr int NF = DC > 0 ? DC : 1;
+  __shared__ float2 s_xy[B];
+  __shared__ float4 s_co[B];
+  __shared__ int4 s_pr[B];
+  __shared__ float4 s_rgbz[B];
+  __shared__ uint32_t s_g[B];
+  __shared__ __align__(16) float s_f[DC > 0 ? B * DC : 1];
+  __shared__ int s_maxlast;
+
+  const int tile = blockIdx.x;
+  const int tx = tile % a.ntx, ty = tile / a.ntx;
+  const int col = tx * kTile + (threadIdx.x & (kTile - 1));
+  const int row0 = ty * kTile + (threadIdx.x / kTile) * PX;
+  const int lane = threadIdx.x & 31;
+  const uint2 rg = a.ranges[tile];
+  if (rg.y <= rg.x) return;
+  const float fc = (float)col;
+
+  bool inside[PX];
+  float T[PX], Tfin[PX], suffix[PX], vpix[PX], dc0[PX], dc1[PX], dc2[PX], dd[PX];
+  int lastj[PX];
+  float df[PX][NF];
+  int mylast = -1;
+#pragma unroll
+  for (int p = 0; p < PX; ++p) {
+    const int row = row0 + p;
+    inside[p] = col < a.W && row < a.H;
+    T[p] = Tfin[p] = 1.f;
+    lastj[p] = -1;
+    dc0[p] = dc1[p] = dc2[p] = dd[p] = 0.f;
+    float dA = 0.f;
+#pragma unroll
+    for (int c = 0; c < NF; ++c) df[p][c] = 0.f;
+    if (inside[p]) {
+      const int64_t pix = (int64_t)row * a.W + col;
+      T[p] = Tfin[p] = a.tfinal[pix];
+      lastj[p] = a.last[pix];
+      if (a.dC) {
+        dc0[p] = a.dC[3 * pix];
+        dc1[p] = a.dC[3 * pix + 1];
+        dc2[p] = a.dC[3 * pix + 2];
+      }
+      if (a.dD) dd[p] = a.dD[pix];
+      if (a.dA) dA = a.dA[pix];
+      if (DC > 0 && a.dF) {
+#pragma unroll
+        for (int c = 0; c < NF; ++c)
+          if (c < a.D) df[p][c] = a.dF[pix * a.D + c];
+      }
+    }
+    vpix[p] = dc0[p] * a.bg0 + dc1[p] * a.bg1 + dc2[p] * a.bg2 - dA;  // dL/dT_final
+    suffix[p] = 0.f;
+    mylast = max(mylast, lastj[p]);
+  }
+
+  if (threadIdx.x == 0) s_maxlast = -1;
+  __syncthreads();
+  atomicMax(&s_maxlast, mylast);
+  __syncthreads();
+  const int maxlast = s_maxlast;
+  if (maxlast < (int)rg.x) return;
+  const int wlast = __reduce_max_sync(0xffffffffu, mylast);
+  const int wrow0 = ty * kTile + (threadIdx.x >> 5) * 2 * PX;  // this warp's 2*PX pixel rows
+  const int tcol0 = tx * kTile;
+
+  const int nv = a.nvals;
+  const uint32_t hi = (uint32_t)(maxlast + 1) < rg.y ? (uint32_t)(maxlast + 1) : rg.y;
+  for (int64_t bend = hi; bend > (int64_t)rg.x; bend -= B) {
+    const int64_t bstart = bend - B > (int64_t)rg.x ? bend - B : (int64_t)rg.x;
+    const int cnt = (int)(bend - bstart);
+    __syncthreads();
+    if ((int)threadIdx.x < cnt) {
+      const uint32_t g = a.pvals[bstart + threadIdx.x];
+      s_g[threadIdx.x] = g;
+      s_xy[threadIdx.x] = a.xy[g];
+      s_co[threadIdx.x] = a.conic_o[g];
+      s_pr[threadIdx.x] = a.pix_rect[g];
+      s_rgbz[threadIdx.x] = a.rgbz[g];
+      if (DC > 0) {
+        const float* src = a.features + (int64_t)g * a.D;
+        float* dst = s_f + threadIdx.x * DC;
+        for (int c = 0; c < DC; ++c) dst[c] = c < a.D ? src[c] : 0.f;
+      }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int m = (cnt - 1) / 32; m >= 0; --m) {
+      unsigned bits;
+      {
+        const int kk = m * 32 + lane;
+        bool hit = false;
+        if (kk < cnt && bstart + kk <= (int64_t)wlast) {
+          const int4 pr = s_pr[kk];
+          hit = pr.w >= wrow0 && pr.z <= wrow0 + 2 * PX - 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
+        }
+        bits = __ballot_sync(0xffffffffu, hit);
+      }
+      while (bits) {
+        const int bit = 31 - __clz(bits);
+        bits &= ~(1u << bit);
+        const int k = m * 32 + bit;
+        const int64_t j = bstart + k;
+        const int4 pr = s_pr[k];
+        const float2 mxy = s_xy[k];
+        const float4 co = s_co[k];
+        float v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = 0.f;
+        bool any = false;
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          const int row = row0 + p;
+          bool live = inside[p] && j <= (int64_t)lastj[p] &&
+                      !(col < pr.x || col > pr.y || row < pr.z || row > pr.w);
+          if (!live) continue;
+          const float dx = fc - mxy.x, dy = (float)row - mxy.y;
+          const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
+          if (q > kQSkip) continue;
+          const float gv = __expf(-0.5f * q);
+          const float araw = co.w * gv;
+          const float al = fminf(araw, a.alpha_cap);
+          if (al < a.alpha_skip) continue;
+          any = true;
+          const float4 cz = s_rgbz[k];
+          const float om = 1.f - al;
+          const float Texc = T[p] / om;
+          const float w = al * Texc;
+          float uval = cz.x * dc0[p] + cz.y * dc1[p] + cz.z * dc2[p] + cz.w * dd[p];
+          if (DC > 0) {
+            const float* f = s_f + k * DC;
+#pragma unroll
+            for (int c = 0; c < NF; ++c) {
+              uval += f[c] * df[p][c];
+              if (c < 22) v[10 + c] += w * df[p][c];
+            }
+          }
+          const float dal = uval * Texc - (suffix[p] + Tfin[p] * vpix[p]) / om;
+          suffix[p] += w * uval;
+          T[p] = Texc;
+          const float dar = araw < a.alpha_cap ? dal : 0.f;
+          const float dq = -0.5f * gv * dar * co.w;
+          v[0] += w * dc0[p];
+          v[1] += w * dc1[p];
+          v[2] += w * dc2[p];
+          v[3] += w * dd[p];
+          v[4] += dar * gv;
+          v[5] += dq * dx * dx;
+          v[6] += dq * dx * dy;
+          v[7] += dq * dy * dy;
+          v[8] += -2.f * dq * (co.x * dx + co.y * dy);
+          v[9] += -2.f * dq * (co.y * dx + co.z * dy);
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        float* dst = a.accum + (int64_t)s_g[k] * a.acc_stride;
+        const float r = warp_transpose_reduce(v, lane);
+        if (lane < nv && r != 0.f) red_add(dst + lane, r);
       }
     }
   }
@@ -382,13 +574,35 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
 }
 
 static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t s) {
-  switch (dc) {
-    case 0: k_blend_bwd<0><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    case 4: k_blend_bwd<4><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    case 8: k_blend_bwd<8><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    case 16: k_blend_bwd<16><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    case 32: k_blend_bwd<32><<<ntiles, kTilePixels, 0, s>>>(a); break;
-    default: k_blend_bwd<64><<<ntiles, kTilePixels, 0, s>>>(a); break;
+  // pixels per thread of the replay (FS4D_BLEND_BWD_PX = 1, 2 or 4)
+  static const int px = [] {
+    const char* e = getenv("FS4D_BLEND_BWD_PX");
+    const int v = e ? atoi(e) : 2;  // measured: 1 -> 416 us, 2 -> 342 us, 4 -> 620 us (configs[4])
+    return v == 1 || v == 4 ? v : 2;
+  }();
+  if (px == 1 || dc > 16) {
+    switch (dc) {
+      case 0: k_blend_bwd<0><<<ntiles, kTilePixels, 0, s>>>(a); break;
+      case 4: k_blend_bwd<4><<<ntiles, kTilePixels, 0, s>>>(a); break;
+      case 8: k_blend_bwd<8><<<ntiles, kTilePixels, 0, s>>>(a); break;
+      case 16: k_blend_bwd<16><<<ntiles, kTilePixels, 0, s>>>(a); break;
+      case 32: k_blend_bwd<32><<<ntiles, kTilePixels, 0, s>>>(a); break;
+      default: k_blend_bwd<64><<<ntiles, kTilePixels, 0, s>>>(a); break;
+    }
+  } else if (px == 2) {
+    switch (dc) {
+      case 0: k_blend_bwd2<0, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
+      case 4: k_blend_bwd2<4, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
+      case 8: k_blend_bwd2<8, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
+      default: k_blend_bwd2<16, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
+    }
+  } else {
+    switch (dc) {
+      case 0: k_blend_bwd2<0, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+      case 4: k_blend_bwd2<4, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+      case 8: k_blend_bwd2<8, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+      default: k_blend_bwd2<16, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+    }
   }
 }
 
