@@ -256,6 +256,94 @@ int fs4d_l1_loss_grad(const float* color, const float* color_target, const float
                       double w_rgb, double w_feat, float* d_color, float* d_feature, double* loss,
                       void* stream);
 
+/* ---- training-step glue ---- */
+
+/* Masked photometric L1 (training.py:300-338 _photometric_terms /
+ * _photometric_grads): rgb = sum|C-I|[mask]/n_rgb with n_rgb = 3*count(mask);
+ * depth = sum|D-Dt|[dmask]/n_d with dmask = mask & (alpha >= 0.5);
+ * dC = lambda_rgb*sign(C-I)*mask/n_rgb, dD = lambda_depth*sign(D-Dt)*dmask/n_d
+ * (zero when the count is zero).  mask (uint8 [H,W]) may be NULL (all ones);
+ * depth/depth_target/alpha/d_depth may be NULL (no depth term).  terms[4]
+ * (device double, may be NULL) receives {rgb, depth, n_rgb, n_d}; *loss (may
+ * be NULL) += lambda_rgb*rgb + lambda_depth*depth.  workspace:
+ * fs4d_photometric_workspace_bytes(H, W). */
+size_t fs4d_photometric_workspace_bytes(int32_t height, int32_t width);
+int fs4d_photometric_loss_grad(const float* color, const float* image, const uint8_t* mask,
+                               const float* depth, const float* depth_target, const float* alpha,
+                               int32_t height, int32_t width, double lambda_rgb, double lambda_depth,
+                               float* d_color, float* d_depth, double* terms, double* loss,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
+/* Generic L1 (semantic.py:171-181 feature_loss / feature_loss_backward):
+ * *loss += scale * sum|pred - target|; grad = scale * sign(pred - target)
+ * (either output may be NULL).  feature_loss is scale = 1/(H*W). */
+int fs4d_l1(const float* pred, const float* target, int64_t n, double scale, float* grad,
+            double* loss, void* stream);
+
+/* Adam over a flat parameter buffer (numerics.py:119-159 AdamState /
+ * adam_step, applied per parameter array as training.py:431-442 does).
+ * Every segment is one reference parameter array: [offset, offset+count) of
+ * params/grads/m/v, its learning rate (lr_at_step of its schedule,
+ * numerics.py:189-199, computed by the host) and eps (training.py:46-47).
+ * step_counts[i] (device int32) is segment i's AdamState.step_count; it is
+ * incremented by the call.  A non-finite gradient anywhere aborts the whole
+ * step before any parameter or moment is touched (numerics.py:149-153):
+ * status[FS4D_ST_ADAM_BAD_SEG] gets the first bad segment,
+ * status[FS4D_ST_ADAM_BAD_COUNT] the number of non-finite entries, and the
+ * status code FS4D_ERR_NUMERIC. */
+#define FS4D_MAX_ADAM_SEGMENTS 128
+#define FS4D_ST_ADAM_BAD_SEG 17
+#define FS4D_ST_ADAM_BAD_COUNT 18
+typedef struct Fs4dAdamSegment {
+  int64_t offset, count;
+  double lr, eps, beta1, beta2;
+} Fs4dAdamSegment;
+int fs4d_adam_step(float* params, const float* grads, float* m, float* v, int32_t* step_counts,
+                   const Fs4dAdamSegment* segments /* host array */, int32_t n_segments,
+                   int32_t* status, void* stream);
+
+/* HexPlane total-variation regulariser (hexplane.py:190-222): with tv = sum
+ * over planes of mean squared axis-adjacent differences, *loss (may be NULL)
+ * += scale * tv and grads (same shapes as field, may be NULL) receive
+ * d(scale * tv)/d(plane), overwritten or (accumulate != 0) added -- so the
+ * TV term folds into the plane-gradient segment of the flat buffer before
+ * the all-reduce, in one pass over the planes. */
+int fs4d_tv_loss_grad(const Fs4dHexPlane* field, Fs4dHexPlane* grads, double scale,
+                      int32_t accumulate, double* loss, void* stream);
+
+/* Corner-aligned bilinear resize of [hi,wi,C] to [ho,wo,C]
+ * (semantic.py:82-102) and its adjoint (semantic.py:105-123, computed as a
+ * deterministic two-pass gather instead of np.add.at).  The adjoint needs
+ * fs4d_resize_workspace_bytes(ho, wi, C) of scratch. */
+int fs4d_resize_bilinear(const float* in, int32_t hi, int32_t wi, int32_t C, float* out, int32_t ho,
+                         int32_t wo, void* stream);
+size_t fs4d_resize_workspace_bytes(int32_t ho, int32_t wi, int32_t C);
+int fs4d_resize_bilinear_backward(const float* d_out, int32_t ho, int32_t wo, int32_t C, float* d_in,
+                                  int32_t hi, int32_t wi, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
+/* PointwiseDecoder (semantic.py:126-168): out[ho,wo,Ct] = resize(rendered
+ * [hi,wi,N]) @ W^T + b with W [Ct,N]; `resized` [ho,wo,N] (the cache) may be
+ * NULL.  Backward: d_weight [Ct,N], d_bias [Ct], d_rendered [hi,wi,N] from
+ * d_out and the cache; partial sums are reduced in a fixed order (bitwise
+ * deterministic).  The fused loss variant computes the decoder output, the
+ * feature L1 against `teacher` (semantic.py:171-181, scaled by lambda) and
+ * the whole backward in one pass without writing the decoded map:
+ *   *loss += lambda * sum|dec - teacher| / (ho*wo). */
+size_t fs4d_decoder_workspace_bytes(int32_t hi, int32_t wi, int32_t N, int32_t ho, int32_t wo, int32_t Ct);
+int fs4d_decode_features(const float* rendered, int32_t hi, int32_t wi, int32_t N, const float* weight,
+                         const float* bias, int32_t Ct, int32_t ho, int32_t wo, float* out, float* resized,
+                         void* stream);
+int fs4d_decode_features_backward(const float* d_out, const float* resized, const float* weight, int32_t hi,
+                                  int32_t wi, int32_t N, int32_t Ct, int32_t ho, int32_t wo,
+                                  float* d_rendered, float* d_weight, float* d_bias, int32_t accumulate,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+int fs4d_decoder_feature_loss(const float* rendered, int32_t hi, int32_t wi, int32_t N, const float* weight,
+                              const float* bias, int32_t Ct, const float* teacher, int32_t ho, int32_t wo,
+                              double lambda, float* d_rendered, float* d_weight, float* d_bias,
+                              int32_t accumulate, double* loss, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
 /* ---- rasterizer ---- */
 size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info);
 

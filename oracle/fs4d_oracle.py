@@ -728,3 +728,128 @@ def pixel_decision_margins(out, cfg):
         sl = (slice(ys[0], ys[-1] + 1), slice(xs[0], xs[-1] + 1))
         margin[sl] = mm.min(axis=0).reshape(ys.size, xs.size) if rows.size else np.inf
     return margin
+
+
+# ---------------------------------------------------------------------------
+# training-step glue
+# ---------------------------------------------------------------------------
+def adam_update(param, grad, m, v, step_count, lr, eps, beta1=0.9, beta2=0.999):
+    """numerics.py:137-159: returns (new_param, new_m, new_v, new_step_count);
+    raises OracleError('numeric') on a non-finite gradient before touching
+    anything, 'config' on a non-positive learning rate."""
+    if not lr > 0.0:
+        raise OracleError("config", f"learning rate must be positive, got {lr}")
+    grad = np.asarray(grad, dtype=np.float64)
+    if not np.all(np.isfinite(grad)):
+        raise OracleError("numeric", f"non-finite gradient ({int(np.sum(~np.isfinite(grad)))}/{grad.size} entries)")
+    step = step_count + 1
+    m_new = beta1 * m + (1.0 - beta1) * grad
+    v_new = beta2 * v + (1.0 - beta2) * grad * grad
+    corr_m = m_new / (1.0 - beta1 ** step)
+    corr_v = v_new / (1.0 - beta2 ** step)
+    return param - lr * corr_m / (np.sqrt(corr_v) + eps), m_new, v_new, step
+
+
+def learning_rate(lr_init, lr_final, max_steps, t, delay_mult=1.0, delay_steps=0):
+    """numerics.py:189-199 (log-linear interpolation + optional sine ramp)."""
+    frac = min(t, max_steps) / max_steps
+    lr = np.exp((1.0 - frac) * np.log(lr_init) + frac * np.log(lr_final)) if lr_init != lr_final else lr_init
+    if delay_steps > 0:
+        ramp = min(max(t / delay_steps, 0.0), 1.0)
+        lr = lr * (delay_mult + (1.0 - delay_mult) * np.sin(0.5 * np.pi * ramp))
+    return float(lr)
+
+
+def total_variation(planes, scale=1.0):
+    """hexplane.py:190-222: (sum over planes of mean squared axis-adjacent
+    differences, d(scale*tv)/d(plane) per plane)."""
+    total = 0.0
+    grads = []
+    for level in planes:
+        lg = []
+        for p in level:
+            p = np.asarray(p, dtype=np.float64)
+            ra, rb, c = p.shape
+            n = ((ra - 1) * rb + ra * (rb - 1)) * c
+            fa = np.diff(p, axis=0)  # p[a+1]-p[a]
+            fb = np.diff(p, axis=1)
+            total += (np.sum(fa ** 2) + np.sum(fb ** 2)) / n
+            g = np.zeros_like(p)
+            k = 2.0 * scale / n
+            g[1:] += k * fa
+            g[:-1] -= k * fa
+            g[:, 1:] += k * fb
+            g[:, :-1] -= k * fb
+            lg.append(g)
+        grads.append(lg)
+    return total, grads
+
+
+def _resize_axis(n_in, n_out):
+    """semantic.py:82-90: corner-aligned source index and weight per output."""
+    pos = np.full(1, 0.5 * (n_in - 1)) if n_out == 1 else np.arange(n_out) * (n_in - 1) / (n_out - 1)
+    lo = np.clip(np.floor(pos).astype(np.int64), 0, max(n_in - 2, 0))
+    return lo, np.minimum(lo + 1, n_in - 1), pos - lo
+
+
+def resize_matrix(n_in, n_out):
+    """Dense [n_out, n_in] interpolation matrix of one axis (so resize and
+    its adjoint are A·X·Bᵀ and Aᵀ·G·B — an independent restatement of
+    semantic.py:93-123)."""
+    lo, hi, f = _resize_axis(n_in, n_out)
+    A = np.zeros((n_out, n_in))
+    np.add.at(A, (np.arange(n_out), lo), 1.0 - f)
+    np.add.at(A, (np.arange(n_out), hi), f)
+    return A
+
+
+def resize(img, out_hw):
+    img = np.asarray(img, dtype=np.float64)
+    Ay = resize_matrix(img.shape[0], out_hw[0])
+    Ax = resize_matrix(img.shape[1], out_hw[1])
+    return np.einsum("yi,ijc,xj->yxc", Ay, img, Ax)
+
+
+def resize_adjoint(d_out, in_hw):
+    d_out = np.asarray(d_out, dtype=np.float64)
+    Ay = resize_matrix(in_hw[0], d_out.shape[0])
+    Ax = resize_matrix(in_hw[1], d_out.shape[1])
+    return np.einsum("yi,yxc,xj->ijc", Ay, d_out, Ax)
+
+
+def decoder_forward(weight, bias, rendered, out_hw):
+    """semantic.py:150-158."""
+    r = resize(rendered, out_hw)
+    return r @ np.asarray(weight).T + bias, r
+
+
+def decoder_backward(weight, resized, in_hw, d_out):
+    """semantic.py:161-168: (d_rendered, d_weight, d_bias)."""
+    d_out = np.asarray(d_out, dtype=np.float64)
+    d_bias = d_out.reshape(-1, d_out.shape[2]).sum(axis=0)
+    d_weight = d_out.reshape(-1, d_out.shape[2]).T @ resized.reshape(-1, resized.shape[2])
+    return resize_adjoint(d_out @ np.asarray(weight), in_hw), d_weight, d_bias
+
+
+def l1_mean_pixels(pred, gt):
+    """semantic.py:171-181: (sum|pred-gt|/(H*W), sign(pred-gt)/(H*W))."""
+    d = np.asarray(pred, dtype=np.float64) - np.asarray(gt, dtype=np.float64)
+    hw = d.shape[0] * d.shape[1]
+    return float(np.abs(d).sum() / hw), np.sign(d) / hw
+
+
+def photometric(color, image, mask, depth, depth_target, alpha, lambda_rgb=1.0, lambda_depth=1.0):
+    """training.py:300-338: (rgb, depth_term, dC, dD) with dmask = mask & alpha>=0.5."""
+    mask = np.ones(color.shape[:2], bool) if mask is None else np.asarray(mask, bool)
+    n_rgb = 3 * int(mask.sum())
+    diff = np.asarray(color, np.float64) - image
+    rgb = float(np.abs(diff)[mask].sum() / n_rgb) if n_rgb else 0.0
+    dC = lambda_rgb * np.sign(diff) * mask[:, :, None] / n_rgb if n_rgb else np.zeros_like(diff)
+    if depth is None:
+        return rgb, 0.0, dC, None
+    dmask = mask & (np.asarray(alpha) >= 0.5)
+    n_d = int(dmask.sum())
+    dd = np.asarray(depth, np.float64) - depth_target
+    dterm = float(np.abs(dd)[dmask].sum() / n_d) if n_d else 0.0
+    dD = lambda_depth * np.sign(dd) * dmask / n_d if n_d else np.zeros_like(dd)
+    return rgb, dterm, dC, dD

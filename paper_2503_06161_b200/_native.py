@@ -20,6 +20,8 @@ OK, ERR_CONFIG, ERR_DATA, ERR_NUMERIC, ERR_CONTRACT, ERR_CAPACITY, ERR_DEGENERAT
 STATUS_WORDS = 32
 ST_CODE, ST_BAD_FIELDS, ST_N_VISIBLE, ST_PAIRS_LO, ST_PAIRS_HI = 0, 1, 2, 3, 4
 ST_BAD_INDEX, ST_DEGEN_INDEX = 8, 16
+ST_ADAM_BAD_SEG, ST_ADAM_BAD_COUNT = 17, 18
+MAX_ADAM_SEGMENTS = 128
 
 FIELD_NAMES = ("positions", "rotations", "log_scales", "opacity_logits",
                "colors_raw", "features", "sh_rest")
@@ -97,6 +99,13 @@ class DeformNet(ctypes.Structure):
                 ("head", Linear * N_BRANCHES), ("feat", Linear * 2)]
 
 
+class AdamSegment(ctypes.Structure):
+    _fields_ = [("offset", ctypes.c_int64), ("count", ctypes.c_int64), ("lr", ctypes.c_double),
+                ("eps", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double)]
+
+
+_V, _I32, _I64, _D, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+
 # symbol -> (restype, argtypes); every entry point declared in include/fs4d.h
 SIGNATURES = {
     "fs4d_abi_version": (ctypes.c_int, []),
@@ -126,6 +135,21 @@ SIGNATURES = {
                                          ctypes.c_int32, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p]),
+    "fs4d_photometric_workspace_bytes": (_SZ, [_I32, _I32]),
+    "fs4d_photometric_loss_grad": (ctypes.c_int, [_V, _V, _V, _V, _V, _V, _I32, _I32, _D, _D, _V, _V, _V,
+                                                  _V, _V, _SZ, _V]),
+    "fs4d_l1": (ctypes.c_int, [_V, _V, _I64, _D, _V, _V, _V]),
+    "fs4d_adam_step": (ctypes.c_int, [_V, _V, _V, _V, _V, ctypes.POINTER(AdamSegment), _I32, _V, _V]),
+    "fs4d_tv_loss_grad": (ctypes.c_int, [ctypes.POINTER(HexPlane), ctypes.POINTER(HexPlane), _D, _I32, _V, _V]),
+    "fs4d_resize_bilinear": (ctypes.c_int, [_V, _I32, _I32, _I32, _V, _I32, _I32, _V]),
+    "fs4d_resize_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
+    "fs4d_resize_bilinear_backward": (ctypes.c_int, [_V, _I32, _I32, _I32, _V, _I32, _I32, _V, _SZ, _V]),
+    "fs4d_decoder_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I32, _I32, _I32]),
+    "fs4d_decode_features": (ctypes.c_int, [_V, _I32, _I32, _I32, _V, _V, _I32, _I32, _I32, _V, _V, _V]),
+    "fs4d_decode_features_backward": (ctypes.c_int, [_V, _V, _V, _I32, _I32, _I32, _I32, _I32, _I32, _V, _V, _V,
+                                                     _I32, _V, _SZ, _V]),
+    "fs4d_decoder_feature_loss": (ctypes.c_int, [_V, _I32, _I32, _I32, _V, _V, _I32, _V, _I32, _I32, _D, _V, _V,
+                                                 _V, _I32, _V, _V, _SZ, _V]),
     "fs4d_render_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(RecordInfo)]),
     "fs4d_render_fwd": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(Camera),
                                        ctypes.POINTER(RasterCfg), ctypes.POINTER(RecordInfo),

@@ -76,6 +76,23 @@ int deform_backward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&,
 int l1_loss_grad(const float*, const float*, const float*, const float*, int, int, int, double, double, float*, float*,
                  double*, cudaStream_t);
 
+size_t photometric_workspace_bytes(int, int);
+int photometric_loss_grad(const float*, const float*, const uint8_t*, const float*, const float*, const float*, int,
+                          int, double, double, float*, float*, double*, double*, void*, cudaStream_t);
+int l1(const float*, const float*, int64_t, double, float*, double*, cudaStream_t);
+int adam_step(float*, const float*, float*, float*, int32_t*, const Fs4dAdamSegment*, int, int32_t*, cudaStream_t);
+int tv_loss_grad(const Fs4dHexPlane&, Fs4dHexPlane*, double, int, double*, cudaStream_t);
+int resize_bilinear(const float*, int, int, int, float*, int, int, cudaStream_t);
+size_t resize_workspace_bytes(int, int, int);
+int resize_bilinear_backward(const float*, int, int, int, float*, int, int, float*, cudaStream_t);
+size_t decoder_workspace_bytes(int, int, int, int, int, int);
+int decode_features(const float*, int, int, int, const float*, const float*, int, int, int, float*, float*,
+                    cudaStream_t);
+int decode_features_backward(const float*, const float*, const float*, int, int, int, int, int, int, float*, float*,
+                             float*, int, void*, size_t, cudaStream_t);
+int decoder_feature_loss(const float*, int, int, int, const float*, const float*, int, const float*, int, int, double,
+                         float*, float*, float*, int, double*, void*, size_t, cudaStream_t);
+
 static int check_cloud(const Fs4dCloud* c, bool need_colors) {
   if (!c) return fail(FS4D_ERR_CONFIG, "null cloud");
   if (c->K < 0 || c->K > 0x7FFFFFFF) return fail(FS4D_ERR_CONFIG, "cloud size out of range");
@@ -119,7 +136,7 @@ static int check_record(const Fs4dRecordInfo* info, const Fs4dCloud* snap, const
 __global__ void k_status_reset(int32_t* st) {
   int i = threadIdx.x;
   if (i < FS4D_STATUS_WORDS)
-    st[i] = (i >= FS4D_ST_BAD_INDEX && i <= FS4D_ST_DEGEN_INDEX) ? 0x7FFFFFFF : 0;
+    st[i] = (i >= FS4D_ST_BAD_INDEX && i <= FS4D_ST_ADAM_BAD_SEG) ? 0x7FFFFFFF : 0;
 }
 
 }  // namespace fs4d
@@ -214,6 +231,122 @@ int fs4d_l1_loss_grad(const float* color, const float* color_target, const float
   if (D > 0 && (!feature || !feature_target || !d_feature)) return fail(FS4D_ERR_CONFIG, "feature buffers missing");
   return l1_loss_grad(color, color_target, feature, feature_target, height, width, D, w_rgb, w_feat, d_color,
                       d_feature, loss, (cudaStream_t)stream);
+}
+
+size_t fs4d_photometric_workspace_bytes(int32_t height, int32_t width) {
+  return photometric_workspace_bytes(height, width);
+}
+
+int fs4d_photometric_loss_grad(const float* color, const float* image, const uint8_t* mask, const float* depth,
+                               const float* depth_target, const float* alpha, int32_t height, int32_t width,
+                               double lambda_rgb, double lambda_depth, float* d_color, float* d_depth, double* terms,
+                               double* loss, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!color || !image || !d_color || height <= 0 || width <= 0)
+    return fail(FS4D_ERR_CONFIG, "bad photometric loss arguments");
+  const bool with_depth = depth != nullptr;
+  if (with_depth && (!depth_target || !alpha || !d_depth))
+    return fail(FS4D_ERR_CONFIG, "depth term needs depth, depth_target, alpha and d_depth");
+  if (!workspace || workspace_bytes < photometric_workspace_bytes(height, width))
+    return fail(FS4D_ERR_CONFIG, "photometric workspace too small");
+  return photometric_loss_grad(color, image, mask, depth, depth_target, alpha, height, width, lambda_rgb,
+                               lambda_depth, d_color, with_depth ? d_depth : nullptr, terms, loss, workspace,
+                               (cudaStream_t)stream);
+}
+
+int fs4d_l1(const float* pred, const float* target, int64_t n, double scale, float* grad, double* loss,
+            void* stream) {
+  if (n < 0 || (n > 0 && (!pred || !target))) return fail(FS4D_ERR_CONFIG, "bad l1 arguments");
+  return l1(pred, target, n, scale, grad, loss, (cudaStream_t)stream);
+}
+
+int fs4d_adam_step(float* params, const float* grads, float* m, float* v, int32_t* step_counts,
+                   const Fs4dAdamSegment* segments, int32_t n_segments, int32_t* status, void* stream) {
+  if (n_segments < 0 || n_segments > FS4D_MAX_ADAM_SEGMENTS)
+    return fail(FS4D_ERR_CONFIG, "adam segment count out of range");
+  if (n_segments == 0) return FS4D_OK;
+  if (!params || !grads || !m || !v || !step_counts || !segments || !status)
+    return fail(FS4D_ERR_CONFIG, "null adam argument");
+  for (int i = 0; i < n_segments; ++i) {
+    const Fs4dAdamSegment& g = segments[i];
+    // numerics.py:143-144: a non-positive learning rate is a configuration error
+    if (!(g.lr > 0.0)) return fail(FS4D_ERR_CONFIG, "learning rate must be positive, got " + std::to_string(g.lr));
+    if (g.offset < 0 || g.count < 0) return fail(FS4D_ERR_CONFIG, "bad adam segment bounds");
+    if (!(g.beta1 >= 0.0 && g.beta1 < 1.0) || !(g.beta2 >= 0.0 && g.beta2 < 1.0) || !(g.eps >= 0.0))
+      return fail(FS4D_ERR_CONFIG, "bad adam hyper-parameters");
+  }
+  return adam_step(params, grads, m, v, step_counts, segments, n_segments, status, (cudaStream_t)stream);
+}
+
+static int check_field(const Fs4dHexPlane* f) {
+  if (!f) return fail(FS4D_ERR_CONFIG, "null field");
+  if (f->levels < 0 || f->levels > FS4D_MAX_LEVELS || f->channels <= 0)
+    return fail(FS4D_ERR_CONFIG, "bad field levels / channels");
+  for (int l = 0; l < f->levels; ++l)
+    for (int q = 0; q < 6; ++q)
+      if (!f->planes[l][q] || f->res[l][q][0] < 1 || f->res[l][q][1] < 1)
+        return fail(FS4D_ERR_CONFIG, "bad plane pointer / resolution");
+  return FS4D_OK;
+}
+
+int fs4d_tv_loss_grad(const Fs4dHexPlane* field, Fs4dHexPlane* grads, double scale, int32_t accumulate, double* loss,
+                      void* stream) {
+  if (int rc = check_field(field)) return rc;
+  if (grads) {
+    if (grads->levels != field->levels) return fail(FS4D_ERR_CONFIG, "gradient field level mismatch");
+    for (int l = 0; l < field->levels; ++l)
+      for (int q = 0; q < 6; ++q)
+        if (!grads->planes[l][q]) return fail(FS4D_ERR_CONFIG, "null plane gradient");
+  }
+  return tv_loss_grad(*field, grads, scale, accumulate, loss, (cudaStream_t)stream);
+}
+
+int fs4d_resize_bilinear(const float* in, int32_t hi, int32_t wi, int32_t C, float* out, int32_t ho, int32_t wo,
+                         void* stream) {
+  if (hi <= 0 || wi <= 0 || C <= 0 || ho <= 0 || wo <= 0 || !in || !out)
+    return fail(FS4D_ERR_CONFIG, "bad resize arguments");
+  return resize_bilinear(in, hi, wi, C, out, ho, wo, (cudaStream_t)stream);
+}
+
+size_t fs4d_resize_workspace_bytes(int32_t ho, int32_t wi, int32_t C) { return resize_workspace_bytes(ho, wi, C); }
+
+int fs4d_resize_bilinear_backward(const float* d_out, int32_t ho, int32_t wo, int32_t C, float* d_in, int32_t hi,
+                                  int32_t wi, void* workspace, size_t workspace_bytes, void* stream) {
+  if (hi <= 0 || wi <= 0 || C <= 0 || ho <= 0 || wo <= 0 || !d_out || !d_in)
+    return fail(FS4D_ERR_CONFIG, "bad resize arguments");
+  if (!workspace || workspace_bytes < resize_workspace_bytes(ho, wi, C))
+    return fail(FS4D_ERR_CONFIG, "resize workspace too small");
+  return resize_bilinear_backward(d_out, ho, wo, C, d_in, hi, wi, (float*)workspace, (cudaStream_t)stream);
+}
+
+size_t fs4d_decoder_workspace_bytes(int32_t hi, int32_t wi, int32_t N, int32_t ho, int32_t wo, int32_t Ct) {
+  return decoder_workspace_bytes(hi, wi, N, ho, wo, Ct);
+}
+
+int fs4d_decode_features(const float* rendered, int32_t hi, int32_t wi, int32_t N, const float* weight,
+                         const float* bias, int32_t Ct, int32_t ho, int32_t wo, float* out, float* resized,
+                         void* stream) {
+  if (!rendered || !weight || !bias || !out) return fail(FS4D_ERR_CONFIG, "null decoder argument");
+  return decode_features(rendered, hi, wi, N, weight, bias, Ct, ho, wo, out, resized, (cudaStream_t)stream);
+}
+
+int fs4d_decode_features_backward(const float* d_out, const float* resized, const float* weight, int32_t hi,
+                                  int32_t wi, int32_t N, int32_t Ct, int32_t ho, int32_t wo, float* d_rendered,
+                                  float* d_weight, float* d_bias, int32_t accumulate, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if (!d_out || !resized || !weight || !d_rendered || !d_weight || !d_bias)
+    return fail(FS4D_ERR_CONFIG, "null decoder backward argument");
+  return decode_features_backward(d_out, resized, weight, hi, wi, N, Ct, ho, wo, d_rendered, d_weight, d_bias,
+                                  accumulate, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int fs4d_decoder_feature_loss(const float* rendered, int32_t hi, int32_t wi, int32_t N, const float* weight,
+                              const float* bias, int32_t Ct, const float* teacher, int32_t ho, int32_t wo,
+                              double lambda, float* d_rendered, float* d_weight, float* d_bias, int32_t accumulate,
+                              double* loss, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!rendered || !weight || !bias || !teacher || !d_rendered || !d_weight || !d_bias)
+    return fail(FS4D_ERR_CONFIG, "null decoder loss argument");
+  return decoder_feature_loss(rendered, hi, wi, N, weight, bias, Ct, teacher, ho, wo, lambda, d_rendered, d_weight,
+                              d_bias, accumulate, loss, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info) {

@@ -626,3 +626,23 @@ class StreamedFrames:
 
     def d2h_bytes(self):
         return self.pipes[0].d2h_bytes()
+
+
+# ---------------------------------------------------------------------------
+# numpy <-> device helpers for the reference-shaped wrappers
+# ---------------------------------------------------------------------------
+def as_device(x, device="cuda"):
+    """(fp32 contiguous CUDA tensor, came_from_host).  torch CUDA fp32 tensors
+    pass through without a copy (the zero-copy fast path); anything else is a
+    host array (the reference's float64 NumPy) rounded to fp32 and uploaded."""
+    if isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32:
+        return x.contiguous(), False
+    if isinstance(x, torch.Tensor):
+        return x.detach().to(device=device, dtype=torch.float32).contiguous(), True
+    return _dev(x, device), True
+
+
+def to_host(t, like_host):
+    """Back to float64 NumPy when the caller passed host arrays (reference API);
+    otherwise the device tensor itself."""
+    return t.detach().cpu().numpy().astype(np.float64) if like_host else t

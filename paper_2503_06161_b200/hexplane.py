@@ -76,3 +76,49 @@ class HexPlaneField:
     def set_param(self, name, arr):
         _, l, p = name.split(".")
         self.planes[int(l[1:])][int(p[1:])] = arr
+
+
+# ---------------------------------------------------------------------------
+# total-variation regulariser (hexplane.py:190-222), on device
+# ---------------------------------------------------------------------------
+def tv_loss_grad_device(field, grads=None, scale=1.0, accumulate=False, loss=None):
+    """fs4d_tv_loss_grad on a DeviceField: adds scale * tv to `loss` (device
+    float64 [1], optional) and writes / accumulates d(scale*tv)/d(plane) into
+    `grads` (DeviceField, optional), in one pass."""
+    import ctypes
+
+    from . import _native as N
+    from .device import _p, _stream
+
+    fs = field.struct()
+    gs = grads.struct() if grads is not None else None
+    N.check(N.load().fs4d_tv_loss_grad(ctypes.byref(fs), ctypes.byref(gs) if gs is not None else None,
+                                       float(scale), int(bool(accumulate)), _p(loss), _stream()))
+
+
+def _device_field(field):
+    from .device import DeviceField
+    if isinstance(field, DeviceField):
+        return field, False
+    return DeviceField.from_field(field), True
+
+
+def tv_loss(field):
+    """Mean squared difference of axis-adjacent cells, summed over planes
+    (hexplane.py:190-196)."""
+    import torch
+
+    dev, _ = _device_field(field)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    tv_loss_grad_device(dev, None, 1.0, False, loss)
+    return float(loss.item())
+
+
+def tv_backward(field, scale=1.0):
+    """d(scale * tv_loss)/d(plane) for every plane (hexplane.py:207-222)."""
+    dev, host = _device_field(field)
+    grads = dev.zeros_like()
+    tv_loss_grad_device(dev, grads, scale, False, None)
+    if not host:
+        return grads.planes
+    return [[p.cpu().numpy().astype(np.float64) for p in level] for level in grads.planes]

@@ -1,0 +1,90 @@
+"""Adam over device parameters (numerics.py:119-199, training.py:46-47,
+365-376, 431-442) -- SURVEY §8(f) row 1.
+
+* ``FlatAdam`` is the training path: every parameter array of the model is a
+  segment of ONE flat fp32 buffer (the same layout as the all-reduced
+  gradient buffer, parallel.FlatGrads), so the whole optimizer step is two
+  kernel launches (non-finite check + update) for all ~50 arrays, each
+  segment with its own learning rate, eps and Adam step count exactly as the
+  reference keeps one AdamState per array.
+* ``numerics.adam_step`` (reference signature) runs the same kernel on a
+  single array.
+
+The learning-rate schedule itself is host scalar arithmetic
+(``numerics.lr_at_step``), evaluated once per step per group.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import StatusBlock, _p, _stream
+from .errors import ConfigurationError, NumericalError
+
+GAUSSIAN_ADAM_EPS = 1e-15  # training.py:46
+NETWORK_ADAM_EPS = 1e-8    # training.py:47
+
+
+def adam_eps(name):
+    """training.py:366-367: dotted names (grid./net./decoder.) are network params."""
+    return GAUSSIAN_ADAM_EPS if "." not in name else NETWORK_ADAM_EPS
+
+
+def schedule_key(name):
+    """training.py:370-377."""
+    for prefix in ("grid", "net", "decoder"):
+        if name.startswith(prefix + "."):
+            return prefix
+    return name
+
+
+class FlatAdam:
+    """Multi-tensor Adam over a flat fp32 parameter buffer.
+
+    specs: [(name, shape)] in buffer order (parallel.gradient_specs layout).
+    params: the flat fp32 CUDA parameter buffer (updated in place).
+    """
+
+    def __init__(self, specs, params, beta1=0.9, beta2=0.999, eps_of=adam_eps):
+        self.specs = [(n, tuple(int(s) for s in sh)) for n, sh in specs]
+        if len(self.specs) > N.MAX_ADAM_SEGMENTS:
+            raise ConfigurationError(f"at most {N.MAX_ADAM_SEGMENTS} parameter arrays per Adam call")
+        self.params = params
+        self.m = torch.zeros_like(params)
+        self.v = torch.zeros_like(params)
+        self.steps = torch.zeros(len(self.specs), dtype=torch.int32, device=params.device)
+        self.status = StatusBlock(params.device)
+        self.status.reset()
+        self.segs = (N.AdamSegment * max(len(self.specs), 1))()
+        off = 0
+        for i, (name, shape) in enumerate(self.specs):
+            n = int(np.prod(shape)) if shape else 1
+            s = self.segs[i]
+            s.offset, s.count = off, n
+            s.eps, s.beta1, s.beta2 = float(eps_of(name)), float(beta1), float(beta2)
+            s.lr = 1.0
+            off += n
+        if off != params.numel():
+            raise ConfigurationError(f"Adam specs cover {off} floats, buffer has {params.numel()}")
+        self.names = [n for n, _ in self.specs]
+
+    def step(self, grads, lrs):
+        """grads: flat fp32 CUDA buffer of the same layout; lrs: name -> lr or
+        schedule-key -> lr.  Stream-ordered; check() reads the status."""
+        for i, name in enumerate(self.names):
+            lr = lrs[name] if name in lrs else lrs[schedule_key(name)]
+            self.segs[i].lr = float(lr)
+        N.check(N.load().fs4d_adam_step(_p(self.params), _p(grads), _p(self.m), _p(self.v), _p(self.steps),
+                                        self.segs, len(self.names), _p(self.status.t), _stream()))
+
+    def check(self):
+        """Raise NumericalError (numerics.py:149-153) if a step saw a non-finite gradient."""
+        st = self.status.read()
+        if int(st[N.ST_CODE]) != 0:
+            seg = int(st[N.ST_ADAM_BAD_SEG])
+            name, shape = self.specs[seg] if 0 <= seg < len(self.specs) else ("?", ())
+            self.status.reset()
+            raise NumericalError(f"param {name}: non-finite gradient ({int(st[N.ST_ADAM_BAD_COUNT])} entries) "
+                                 f"for param of shape {shape}")

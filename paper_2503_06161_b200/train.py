@@ -1,82 +1,211 @@
-"""Data-parallel training step of the render path on device (configs[4]).
+"""Data-parallel training step of the render path on device (configs[4], and
+the reference's fine-stage iteration training.py:489-535 when the decoder /
+TV / optimizer options are on).
 
 Per rank: a batch of (view, t) pairs; for each pair
-    fs4d_deform_fwd -> fs4d_render_fwd -> fs4d_l1_loss_grad (L1 RGB + L1
-    feature, training.py:302-338 / semantic.py:171-181 normalisations)
+    fs4d_deform_fwd -> fs4d_render_fwd -> loss + upstream image gradients
     -> fs4d_render_bwd -> fs4d_deform_bwd (accumulating into the flat buffer)
-then ONE all-reduce (SUM) of the flat gradient buffer; the mean over pairs
-and ranks is folded into the loss weights.  The optimizer step is the next
-row; this module stops at the reduced gradients.
+then the HexPlane TV term (hexplane.py:190-222) is folded into the plane
+gradients, ONE all-reduce (SUM) of the flat gradient buffer runs, and --
+with an optimizer attached -- one multi-segment Adam launch
+(numerics.py:137-159) updates every parameter array with its own schedule
+(training.py:156-170, 365-376, 431-442).  The mean over pairs and ranks is
+folded into the loss weights, so the collective is a plain SUM.
+
+Loss modes:
+  "raw"     configs[4]: L1 RGB / (3HW) + L1 raw D-channel feature / (HW) at
+            render resolution (fused kernel fs4d_l1_loss_grad).
+  "decoder" the reference's fine stage: masked photometric L1 (+ depth L1)
+            (training.py:300-338) and the pointwise-decoder feature loss
+            against a teacher map (training.py:497-505) in one fused kernel.
 """
 
 import ctypes
 
+import numpy as np
 import torch
 
 from . import _native as N
 from .device import DeformEngine, DeviceCloud, DeviceField, DeviceNet, Renderer, _p, _stream
+from .hexplane import tv_loss_grad_device
+from .numerics import lr_at_step
+from .optim import FlatAdam
 from .parallel import FlatGrads, gradient_specs
+from .semantic import DecoderLoss
+
+
+def photometric_loss_grad(color, image, mask, depth, depth_target, alpha, lambda_rgb, lambda_depth, d_color,
+                          d_depth=None, terms=None, loss=None, workspace=None):
+    """Masked photometric L1 + depth L1 and their gradients (training.py:300-338)
+    on device.  Returns the device float64 terms tensor {rgb, depth, n_rgb, n_d}."""
+    lib = N.load()
+    h, w = int(color.shape[0]), int(color.shape[1])
+    if terms is None:
+        terms = torch.zeros(4, dtype=torch.float64, device=color.device)
+    need = int(lib.fs4d_photometric_workspace_bytes(h, w))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=color.device)
+    N.check(lib.fs4d_photometric_loss_grad(_p(color), _p(image), _p(mask), _p(depth), _p(depth_target), _p(alpha),
+                                           h, w, float(lambda_rgb), float(lambda_depth), _p(d_color), _p(d_depth),
+                                           _p(terms), _p(loss), _p(workspace), workspace.numel(), _stream()))
+    return terms
+
+
+def _net_layer_specs(net):
+    specs = []
+    for prefix, stack in net.layers.items():
+        for i, (wt, b, _) in enumerate(stack):
+            specs += [(f"{prefix}.{i}.weight", tuple(wt.shape)), (f"{prefix}.{i}.bias", tuple(b.shape))]
+    return specs
 
 
 class TrainStep:
-    def __init__(self, cloud, field, net, height, width, cfg, world=1, group=None, device="cuda"):
+    def __init__(self, cloud, field, net, height, width, cfg, world=1, group=None, device="cuda",
+                 loss_mode="raw", lambda_rgb=1.0, lambda_depth=0.0, lambda_feat=1.0, lambda_tv=0.0,
+                 decoder=None):
         self.cloud, self.field, self.net = cloud, field, net
         self.h, self.w, self.cfg = int(height), int(width), cfg
         self.world, self.group = int(world), group
+        self.device = device
+        if loss_mode not in ("raw", "decoder"):
+            raise ValueError(f"unknown loss mode {loss_mode!r}")
+        self.loss_mode = loss_mode
+        self.lambda_rgb, self.lambda_depth = float(lambda_rgb), float(lambda_depth)
+        self.lambda_feat, self.lambda_tv = float(lambda_feat), float(lambda_tv)
+        self.decoder = decoder  # (weight [Ct,N], bias [Ct]) CUDA tensors for loss_mode="decoder"
         self.deformer = DeformEngine(device)
         self.renderer = Renderer(device)
         k, d, sh = len(cloud), cloud.feature_dim, cloud.sh_degree
-        layer_shapes = []
-        for prefix, stack in net.layers.items():
-            for i, (wt, b, _) in enumerate(stack):
-                layer_shapes += [(f"{prefix}.{i}.weight", tuple(wt.shape)), (f"{prefix}.{i}.bias", tuple(b.shape))]
         plane_shapes = [[tuple(p.shape) for p in level] for level in field.planes]
-        self.grads = FlatGrads(gradient_specs(k, d, sh, plane_shapes, layer_shapes), device)
-        g = self.grads
-        self.cloud_grads = DeviceCloud(g["positions"], g["rotations"], g["log_scales"], g["opacity_logits"],
-                                       g["colors_raw"], g["features"], g.views.get("sh_rest"))
-        self.plane_grads = DeviceField([[g[f"grid.l{l}.p{p}"] for p in range(len(level))]
-                                        for l, level in enumerate(field.planes)], field.aabb, field.channels)
-        self.net_grads = DeviceNet({prefix: [(g[f"{prefix}.{i}.weight"], g[f"{prefix}.{i}.bias"], relu)
-                                             for i, (_, _, relu) in enumerate(stack)]
-                                    for prefix, stack in net.layers.items()},
-                                   net.latent_dim, net.width, net.depth, net.feature_dim, net.enable_grid,
-                                   net.enable_feature_update)
+        specs = gradient_specs(k, d, sh, plane_shapes, _net_layer_specs(net))
+        if decoder is not None:
+            specs += [("decoder.weight", tuple(decoder[0].shape)), ("decoder.bias", tuple(decoder[1].shape))]
+        self.specs = specs
+        self.grads = FlatGrads(specs, device)
+        self.cloud_grads, self.plane_grads, self.net_grads = self._bind(self.grads)
         self.snap = DeviceCloud.empty(k, d, 0, device)
         self.snap_grads = DeviceCloud.empty(k, d, sh, device)
         dout = d if cfg.with_features else 0
         self.images = self.renderer.alloc_images(self.h, self.w, dout)
         f = dict(dtype=torch.float32, device=device)
         self.d_color = torch.empty(self.h, self.w, 3, **f)
+        self.d_depth = torch.empty(self.h, self.w, **f)
         self.d_feature = torch.empty(self.h, self.w, dout, **f)
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
         self.cache = None  # deform_with_cache activations, reused pair to pair
+        self.decoder_loss = DecoderLoss(device)
+        self.photo_ws = None
+        self.params = None
+        self.optimizer = None
+        self.schedules = None
+        self.iteration = 0
+
+    def _bind(self, flat):
+        """DeviceCloud / DeviceField / DeviceNet views into a flat buffer."""
+        g = flat
+        cloud = DeviceCloud(g["positions"], g["rotations"], g["log_scales"], g["opacity_logits"], g["colors_raw"],
+                            g["features"], g.views.get("sh_rest"))
+        planes = DeviceField([[g[f"grid.l{l}.p{p}"] for p in range(len(level))]
+                              for l, level in enumerate(self.field.planes)], self.field.aabb, self.field.channels)
+        net = DeviceNet({prefix: [(g[f"{prefix}.{i}.weight"], g[f"{prefix}.{i}.bias"], relu)
+                                  for i, (_, _, relu) in enumerate(stack)]
+                         for prefix, stack in self.net.layers.items()},
+                        self.net.latent_dim, self.net.width, self.net.depth, self.net.feature_dim,
+                        self.net.enable_grid, self.net.enable_feature_update)
+        return cloud, planes, net
+
+    def attach_optimizer(self, schedules):
+        """Move every parameter into ONE flat fp32 buffer (same layout as the
+        gradients) and attach a multi-segment Adam.  schedules: schedule key
+        (positions, rotations, log_scales, opacity_logits, colors_raw,
+        features, grid, net, decoder -- TrainConfig.schedules(),
+        training.py:156-170) -> numerics.LrSchedule.  sh_rest uses the
+        colors_raw schedule."""
+        params = FlatGrads(self.specs, self.device)
+        cloud, field, net = self._bind(params)
+        for name in DeviceCloud.FIELDS + ("sh_rest",):
+            src = getattr(self.cloud, name)
+            if src is not None and getattr(cloud, name) is not None:
+                getattr(cloud, name).copy_(src)
+        for l, level in enumerate(self.field.planes):
+            for p, plane in enumerate(level):
+                field.planes[l][p].copy_(plane)
+        for prefix, stack in self.net.layers.items():
+            for i, (wt, b, _) in enumerate(stack):
+                net.layers[prefix][i][0].copy_(wt)
+                net.layers[prefix][i][1].copy_(b)
+        if self.decoder is not None:
+            params["decoder.weight"].copy_(self.decoder[0])
+            params["decoder.bias"].copy_(self.decoder[1])
+            self.decoder = (params["decoder.weight"], params["decoder.bias"])
+        self.cloud, self.field, self.net = cloud, field, net
+        self.params = params
+        self.schedules = dict(schedules)
+        self.schedules.setdefault("sh_rest", self.schedules.get("colors_raw"))
+        self.optimizer = FlatAdam(self.specs, params.buffer)
+        return self
+
+    def current_lrs(self):
+        return {k: lr_at_step(s, self.iteration) for k, s in self.schedules.items() if s is not None}
 
     def run(self, batch, check=False):
-        """batch: list of (t, K, T, target_rgb [H,W,3] cuda, target_feat [H,W,D] cuda).
-        Returns the device loss (mean over pairs and ranks after the reduce)."""
+        """batch: list of (t, K, T, target_rgb [H,W,3], target_feat) CUDA
+        tensors; loss_mode "decoder" additionally takes optional
+        (mask uint8 [H,W] | None, target_depth [H,W] | None) as items 5-6 and
+        target_feat is the teacher map [ho,wo,Ct].  Returns the device loss
+        (mean over pairs and ranks after the reduce)."""
         lib = N.load()
         n = len(batch) * self.world
         w = 1.0 / n
         self.loss.zero_()
         dout = self.d_feature.shape[2]
-        for i, (t, K, T, tgt_rgb, tgt_feat) in enumerate(batch):
+        for i, item in enumerate(batch):
+            t, K, T, tgt_rgb, tgt_feat = item[:5]
             _, self.cache = self.deformer.forward(self.cloud, self.field, self.net, t, out=self.snap,
                                                   with_cache=self.cache or True)
             imgs, rec = self.renderer.forward(self.snap, K, T, self.h, self.w, self.cfg, images=self.images,
                                               check=check)
-            N.check(lib.fs4d_l1_loss_grad(_p(imgs["color"]), _p(tgt_rgb), _p(imgs["feature"]) if dout else None,
-                                          _p(tgt_feat) if dout else None, self.h, self.w, dout, w, w,
-                                          _p(self.d_color), _p(self.d_feature) if dout else None,
-                                          _p(self.loss), _stream()))
+            d_depth = None
+            if self.loss_mode == "raw":
+                N.check(lib.fs4d_l1_loss_grad(_p(imgs["color"]), _p(tgt_rgb), _p(imgs["feature"]) if dout else None,
+                                              _p(tgt_feat) if dout else None, self.h, self.w, dout,
+                                              w * self.lambda_rgb, w * self.lambda_feat, _p(self.d_color),
+                                              _p(self.d_feature) if dout else None, _p(self.loss), _stream()))
+            else:
+                mask = item[5] if len(item) > 5 else None
+                tgt_depth = item[6] if len(item) > 6 else None
+                if tgt_depth is not None:
+                    d_depth = self.d_depth
+                if self.photo_ws is None:
+                    self.photo_ws = torch.empty(int(lib.fs4d_photometric_workspace_bytes(self.h, self.w)),
+                                                dtype=torch.uint8, device=self.device)
+                photometric_loss_grad(imgs["color"], tgt_rgb, mask, imgs["depth"] if d_depth is not None else None,
+                                      tgt_depth, imgs["alpha"], w * self.lambda_rgb, w * self.lambda_depth,
+                                      self.d_color, d_depth, loss=self.loss, workspace=self.photo_ws)
+                if dout and tgt_feat is not None and self.decoder is not None:
+                    dw = self.grads["decoder.weight"]
+                    db = self.grads["decoder.bias"]
+                    self.decoder_loss(self.decoder[0], self.decoder[1], imgs["feature"], tgt_feat,
+                                      w * self.lambda_feat, self.d_feature, dw, db, self.loss, accumulate=i > 0)
+                elif dout:
+                    self.d_feature.zero_()
             self.renderer.backward(self.snap, K, T, self.h, self.w, self.cfg, rec, d_color=self.d_color,
-                                   d_feature=self.d_feature if dout else None, grads=self.snap_grads)
+                                   d_depth=d_depth, d_feature=self.d_feature if dout else None,
+                                   grads=self.snap_grads)
             self.deformer.backward(self.cloud, self.field, self.net, t, self.snap_grads,
                                    cloud_grads=self.cloud_grads, net_grads=self.net_grads,
                                    plane_grads=self.plane_grads if self.net.enable_grid else None,
                                    accumulate=i > 0, cache=self.cache)
+        if self.lambda_tv > 0 and self.net.enable_grid:
+            # d(lambda_tv * tv)/d(plane) once per iteration (training.py:523-529); 1/world per rank
+            tv_loss_grad_device(self.field, self.plane_grads, self.lambda_tv / self.world, True, self.loss)
         self.grads.allreduce_sum(self.group)
         if self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(self.loss, op=dist.ReduceOp.SUM, group=self.group)
+        if self.optimizer is not None:
+            self.optimizer.step(self.grads.buffer, self.current_lrs())
+            if check:
+                self.optimizer.check()
+            self.iteration += 1
         return self.loss

@@ -21,7 +21,7 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 def load_reference():
     sys.path.insert(0, REF_SRC)
     mods = {}
-    for m in ("gaussians", "rasterizer", "hexplane", "deformation", "numerics"):
+    for m in ("gaussians", "rasterizer", "hexplane", "deformation", "numerics", "semantic", "training"):
         mods[m] = importlib.import_module(f"featsplat.{m}")
     return mods
 
@@ -161,8 +161,97 @@ def deform_case(ref, name, seed, k, nf, width, depth, levels, base, out_dim, ran
     print("deform", name)
 
 
+def train_ops_case(ref, seed=21):
+    """Adam (3 steps, both eps), LR schedules, HexPlane TV, bilinear resize
+    and adjoint, pointwise decoder fwd/bwd, feature L1 and the masked
+    photometric grads -- all from the reference's own functions."""
+    Nm, H, S, T = ref["numerics"], ref["hexplane"], ref["semantic"], ref["training"]
+    rng = np.random.default_rng(seed)
+    data = {}
+    # Adam: numerics.py:137-159, three consecutive steps
+    for tag, eps in (("g", 1e-15), ("n", 1e-8)):
+        p = f32(rng.normal(size=(37, 5)))
+        st = Nm.AdamState.for_param(p, eps=eps)
+        data[f"adam_{tag}_p0"] = p
+        for i in range(3):
+            gr = f32(rng.normal(size=p.shape) * (10.0 ** rng.uniform(-6, 1)))
+            if i == 1:
+                gr[0, 0] = 0.0
+            data[f"adam_{tag}_g{i}"] = gr
+            p = Nm.adam_step(p, gr, st, 1e-3 * (i + 1))
+            data[f"adam_{tag}_p{i + 1}"] = p
+            data[f"adam_{tag}_m{i + 1}"] = st.m
+            data[f"adam_{tag}_v{i + 1}"] = st.v
+    # schedules: numerics.py:189-199
+    steps = np.array([0, 1, 7, 500, 14000, 20000, 30000])
+    data["lr_steps"] = steps
+    data["lr_decay"] = np.array([Nm.lr_at_step(Nm.LrSchedule(1.6e-4, 1.6e-6, 20000), int(t)) for t in steps])
+    data["lr_delay"] = np.array([Nm.lr_at_step(Nm.LrSchedule(1.6e-3, 1.6e-4, 20000, 0.01, 500), int(t))
+                                 for t in steps])
+    # TV: hexplane.py:190-222
+    field = H.HexPlaneField(H.HexPlaneConfig(levels=(1, 2), base_resolution=(6, 5, 4, 3), out_dim=8),
+                            np.array([[-1.0, -1, -1], [1, 1, 1]]), rng)
+    for li, level in enumerate(field.planes):
+        for pi in range(len(level)):
+            field.planes[li][pi] = f32(rng.normal(size=level[pi].shape))
+            data[f"tv_plane_{li}_{pi}"] = field.planes[li][pi]
+    data["tv_loss"] = H.tv_loss(field)
+    tg = H.tv_backward(field, 0.37)
+    for li, level in enumerate(tg):
+        for pi, g in enumerate(level):
+            data[f"tv_grad_{li}_{pi}"] = g
+    # resize (semantic.py:93-123): down, up, ragged, single-row/column
+    for i, (hin, win, hout, wout) in enumerate(((12, 16, 5, 7), (5, 7, 12, 17), (9, 1, 4, 3), (1, 6, 1, 1))):
+        img = f32(rng.normal(size=(hin, win, 3)))
+        dout = f32(rng.normal(size=(hout, wout, 3)))
+        data[f"rs{i}_in"], data[f"rs{i}_dout"] = img, dout
+        data[f"rs{i}_out"] = S.resize_bilinear(img, (hout, wout))
+        data[f"rs{i}_din"] = S.resize_bilinear_backward(dout, (hin, win))
+    # decoder + feature loss (semantic.py:126-181), rendered N=6 -> teacher Ct=10
+    dec = S.PointwiseDecoder.create(10, 6, rng)
+    dec.weight = f32(dec.weight)
+    dec.bias = f32(rng.normal(size=10) * 0.1)
+    rendered = f32(rng.normal(size=(20, 24, 6)))
+    teacher = f32(rng.normal(size=(9, 11, 10)))
+    out, cache = S.decode_features_with_cache(dec, rendered, teacher.shape[:2])
+    d_dec = 0.7 * S.feature_loss_backward(out, teacher)
+    dr, dw, db = S.decode_features_backward(dec, cache, d_dec)
+    data.update(dec_w=dec.weight, dec_b=dec.bias, dec_rendered=rendered, dec_teacher=teacher, dec_out=out,
+                dec_loss=S.feature_loss(out, teacher), dec_d_rendered=dr, dec_dw=dw, dec_db=db)
+    # masked photometric terms (training.py:300-338)
+    h, w = 14, 18
+
+    class Out:
+        pass
+
+    class Fr:
+        pass
+
+    o, fr = Out(), Fr()
+    o.color = f32(rng.uniform(size=(h, w, 3)))
+    o.depth = f32(rng.uniform(1, 3, size=(h, w)))
+    o.alpha = f32(rng.uniform(size=(h, w)))
+    fr.image = f32(rng.uniform(size=(h, w, 3)))
+    fr.depth = f32(rng.uniform(1, 3, size=(h, w)))
+    fr.mask = rng.uniform(size=(h, w)) > 0.3
+
+    class Cfg:
+        lambda_rgb = 0.8
+        lambda_depth = 0.3
+
+    rgb, depth, dC, dD = T._photometric_grads(o, fr, Cfg)
+    data.update(ph_color=o.color, ph_depth=o.depth, ph_alpha=o.alpha, ph_image=fr.image, ph_depth_t=fr.depth,
+                ph_mask=fr.mask, ph_rgb=rgb, ph_dterm=depth, ph_dC=dC, ph_dD=dD)
+    np.savez_compressed(os.path.join(OUT, "train_ops.npz"), **data)
+    print("train_ops")
+
+
 def main():
     ref = load_reference()
+    if len(sys.argv) > 1 and sys.argv[1] == "train_ops":
+        train_ops_case(ref)
+        return
+    train_ops_case(ref)
     # the reference's own tiled-vs-naive scenes (test_rasterizer.py:168-183 sizes)
     render_case(ref, "s0", 0, 50, 32, 32, 4, 1.1 * 32, (0.1, 0.2, 0.3))
     render_case(ref, "s1", 1, 200, 64, 64, 16, 1.1 * 64, (0.1, 0.2, 0.3))

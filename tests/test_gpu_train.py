@@ -110,3 +110,130 @@ def test_train_step_matches_oracle_chain():
         # check is relative to each tensor's scale (stricter than 1e-4 absolute)
         tol = max(1e-3 * np.abs(ref).max(), 1e-12)
         assert np.abs(got - ref).max() < tol, (key, np.abs(got - ref).max(), tol)
+
+
+def test_fine_stage_step_decoder_tv_adam_matches_oracle():
+    """The reference's fine-stage iteration (training.py:489-535) on device:
+    masked photometric + depth L1, pointwise-decoder feature loss against a
+    half-resolution teacher, HexPlane TV, flat all-reduce buffer, then the
+    multi-segment Adam step -- against the float64 oracle chained the same
+    way (the Adam update is checked on the device's own gradients)."""
+    import torch
+    import paper_2503_06161_b200 as fs
+    from paper_2503_06161_b200 import device as dv
+    from paper_2503_06161_b200.numerics import LrSchedule
+    from paper_2503_06161_b200.optim import adam_eps, schedule_key
+    from paper_2503_06161_b200.train import TrainStep
+
+    rng = np.random.default_rng(7)
+    k, h, w, d, ct = 2000, 64, 80, 8, 12
+    ho, wo = 32, 40
+    a = random_cloud_arrays(rng, k, d, op_range=(0.05, 0.9), depth_range=(2.0, 4.0), xy=1.0,
+                            ls_range=(np.exp(-4.0), np.exp(-2.8)), sh_degree=1)
+    cloud = fs.GaussianCloud(**a)
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(8, 8, 8, 4), out_dim=32),
+                             fs.scene_aabb(cloud), rng, init="uniform")
+    for level in field.planes:
+        for i in range(6):
+            level[i] = (level[i] * 2.0).astype(np.float32).astype(np.float64)
+    net = fs.DeformationNet(32, fs.DeformationConfig(width=64, depth=1, feature_dim=d), rng, init="xavier",
+                            head_init="xavier")
+    for _, st in net.stacks():
+        for layer in st:
+            layer.weight = layer.weight.astype(np.float32).astype(np.float64)
+    onet = {p: [(l.weight, l.bias, l.activation == "relu") for l in st] for p, st in net.stacks()}
+    dec_w = rng.uniform(-1, 1, size=(ct, d)).astype(np.float32).astype(np.float64)
+    dec_b = (rng.normal(size=ct) * 0.1).astype(np.float32).astype(np.float64)
+    K = pinhole(h, w, 60.0)
+    lam_rgb, lam_d, lam_f, lam_tv = 1.0, 0.2, 0.7, 0.05
+    cfg = O.RasterParams()
+    pairs = []
+    for t, T in ((0.3, np.eye(4)), (0.8, rigid_T(rng))):
+        snap, cache = O.deform(_C(**a), field.planes, field.aabb, onet, t)
+        snap_obj = _C(**snap, sh_rest=a["sh_rest"])
+        out = O.render(snap_obj, K, T, h, w, cfg)
+        assert np.abs(out["alpha"] - 0.5).min() > 1e-6  # no ambiguous depth-mask pixel
+        sgn = lambda shape: np.where(rng.random(shape) < 0.5, -1.0, 1.0)  # noqa: E731
+        tgt_rgb = (out["color"] - 0.25 * sgn((h, w, 3))).astype(np.float32)
+        tgt_depth = (out["depth"] - 0.3 * sgn((h, w))).astype(np.float32)
+        mask = rng.random((h, w)) > 0.2
+        dec, _ = O.decoder_forward(dec_w, dec_b, out["feature"], (ho, wo))
+        teacher = (dec - 0.5 * sgn((ho, wo, ct))).astype(np.float32)
+        pairs.append((t, T, snap_obj, cache, out, tgt_rgb, tgt_depth, mask, teacher))
+
+    # ---- device step ----
+    f = dict(device="cuda")
+    dec_dev = (torch.tensor(dec_w, dtype=torch.float32, **f), torch.tensor(dec_b, dtype=torch.float32, **f))
+    step = TrainStep(dv.DeviceCloud.from_cloud(cloud), dv.DeviceField.from_field(field), dv.DeviceNet.from_net(net),
+                     h, w, fs.RasterConfig(), loss_mode="decoder", lambda_rgb=lam_rgb, lambda_depth=lam_d,
+                     lambda_feat=lam_f, lambda_tv=lam_tv, decoder=dec_dev)
+    schedules = {"positions": LrSchedule(1.6e-4, 1.6e-6, 100), "rotations": LrSchedule.constant(1e-3),
+                 "log_scales": LrSchedule.constant(5e-3), "opacity_logits": LrSchedule.constant(5e-2),
+                 "colors_raw": LrSchedule.constant(2.5e-3), "features": LrSchedule.constant(2.5e-3),
+                 "grid": LrSchedule(1.6e-3, 1.6e-5, 100), "net": LrSchedule(1.6e-4, 1.6e-6, 100, 0.01, 10),
+                 "decoder": LrSchedule.constant(1e-3)}
+    step.attach_optimizer(schedules)
+    p0 = step.params.buffer.clone()
+    batch = [(t, K, T, torch.as_tensor(tr, **f), torch.as_tensor(te, **f), torch.as_tensor(m, **f),
+              torch.as_tensor(td, **f)) for (t, T, _, _, _, tr, td, m, te) in pairs]
+    loss = float(step.run(batch, check=True).item())
+    torch.cuda.synchronize()
+
+    # ---- oracle chain ----
+    wp = 1.0 / len(pairs)
+    acc, loss_ref = {}, 0.0
+    bad = np.zeros(k, dtype=bool)
+    for (t, T, snap_obj, cache, out, tr, td, m, te) in pairs:
+        rgb, dterm, gC, gD = O.photometric(out["color"], tr, m, out["depth"], td, out["alpha"], wp * lam_rgb,
+                                           wp * lam_d)
+        dec, resized = O.decoder_forward(dec_w, dec_b, out["feature"], (ho, wo))
+        fl, d_dec = O.l1_mean_pixels(dec, te)
+        gF, dW, dB = O.decoder_backward(dec_w, resized, (h, w), wp * lam_f * d_dec)
+        loss_ref += wp * (lam_rgb * rgb + lam_d * dterm + lam_f * fl)
+        g = O.render_backward(snap_obj, K, T, h, w, cfg, out, gC, gD, gF, None)
+        cg, ng, pg = O.deform_backward(_C(**a), field.planes, field.aabb, onet, cache, g)
+        contrib = {"positions": cg["positions"], "rotations": g["rotations"], "log_scales": g["log_scales"],
+                   "opacity_logits": g["opacity_logits"], "colors_raw": g["colors_raw"],
+                   "sh_rest": g["sh_rest"], "features": g["features"], "decoder.weight": dW, "decoder.bias": dB}
+        contrib.update(ng)
+        for l, level in enumerate(pg):
+            for p, arr in enumerate(level):
+                contrib[f"grid.l{l}.p{p}"] = arr
+        for key, v in contrib.items():
+            acc[key] = acc.get(key, 0.0) + v
+        amb = O.pixel_decision_margins(out, cfg) < 1e-5
+        for (ty, tx), (rows, xs, ys) in out["tiles"].items():
+            if amb[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1].any():
+                bad[out["proj"]["source_index"][rows]] = True
+    tv, tv_g = O.total_variation(field.planes, lam_tv)
+    loss_ref += lam_tv * tv
+    for l, level in enumerate(tv_g):
+        for p, arr in enumerate(level):
+            acc[f"grid.l{l}.p{p}"] = acc[f"grid.l{l}.p{p}"] + arr
+
+    assert abs(loss - loss_ref) < 1e-5 * max(1.0, abs(loss_ref)), (loss, loss_ref)
+    keep = ~bad
+    assert keep.mean() > 0.5
+    for key, ref in acc.items():
+        got = step.grads[key].cpu().numpy().astype(np.float64).reshape(np.shape(ref))
+        if np.shape(ref)[0] == k and key in ("positions", "rotations", "log_scales", "opacity_logits",
+                                               "colors_raw", "sh_rest", "features"):
+            got, ref = got[keep], np.asarray(ref)[keep]
+        tol = max(1e-3 * np.abs(ref).max(), 1e-12)
+        assert np.abs(got - ref).max() < tol, (key, np.abs(got - ref).max(), tol)
+
+    # ---- Adam on the device's own gradients (stage injection) ----
+    p1 = step.params.buffer.cpu().numpy().astype(np.float64)
+    g0 = step.grads.buffer.cpu().numpy().astype(np.float64)
+    p0 = p0.cpu().numpy().astype(np.float64)
+    off = 0
+    lrs = {key: s.lr_init for key, s in schedules.items()}  # iteration 0: lr_at_step(s, 0) == lr_init
+    lrs["net"] = schedules["net"].lr_init * schedules["net"].delay_mult
+    for name, shape in step.specs:
+        n = int(np.prod(shape))
+        lr = lrs["colors_raw"] if name == "sh_rest" else lrs[schedule_key(name)]
+        ref, _, _, _ = O.adam_update(p0[off:off + n], g0[off:off + n], 0.0, 0.0, 0, lr, adam_eps(name))
+        got = p1[off:off + n]
+        assert np.abs(got - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max()), name
+        off += n
+    assert step.iteration == 1
