@@ -45,9 +45,11 @@ class FlatAdam:
 
     specs: [(name, shape)] in buffer order (parallel.gradient_specs layout).
     params: the flat fp32 CUDA parameter buffer (updated in place).
+    offsets: start of each array in the buffer (FlatGrads.offsets, which pads
+    every array to 64 bytes); contiguous when None.
     """
 
-    def __init__(self, specs, params, beta1=0.9, beta2=0.999, eps_of=adam_eps):
+    def __init__(self, specs, params, beta1=0.9, beta2=0.999, eps_of=adam_eps, offsets=None):
         self.specs = [(n, tuple(int(s) for s in sh)) for n, sh in specs]
         if len(self.specs) > N.MAX_ADAM_SEGMENTS:
             raise ConfigurationError(f"at most {N.MAX_ADAM_SEGMENTS} parameter arrays per Adam call")
@@ -61,13 +63,15 @@ class FlatAdam:
         off = 0
         for i, (name, shape) in enumerate(self.specs):
             n = int(np.prod(shape)) if shape else 1
+            if offsets is not None:
+                off = int(offsets[i])
             s = self.segs[i]
             s.offset, s.count = off, n
             s.eps, s.beta1, s.beta2 = float(eps_of(name)), float(beta1), float(beta2)
             s.lr = 1.0
             off += n
-        if off != params.numel():
-            raise ConfigurationError(f"Adam specs cover {off} floats, buffer has {params.numel()}")
+            if off > params.numel():
+                raise ConfigurationError(f"Adam segment {name} ends at {off}, buffer has {params.numel()}")
         self.names = [n for n, _ in self.specs]
 
     def step(self, grads, lrs):

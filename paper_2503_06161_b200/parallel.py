@@ -43,18 +43,24 @@ def shard_timesteps(n_frames, world, rank):
 
 
 class FlatGrads:
-    """One contiguous fp32 buffer with named, shaped views."""
+    """One contiguous fp32 buffer with named, shaped views.  Every view starts
+    on a 64-byte boundary (`align` floats) so the kernels' vector loads see
+    aligned arrays when parameters live in the buffer; the zero padding
+    between views rides along in the all-reduce."""
 
-    def __init__(self, specs, device="cuda"):
+    def __init__(self, specs, device="cuda", align=16):
         self.specs = [(name, tuple(int(s) for s in shape)) for name, shape in specs]
-        sizes = [int(np.prod(shape)) if len(shape) else 1 for _, shape in self.specs]
-        self.numel = int(sum(sizes))
+        self.sizes = [int(np.prod(shape)) if len(shape) else 1 for _, shape in self.specs]
+        self.offsets = []
+        off = 0
+        for n in self.sizes:
+            self.offsets.append(off)
+            off += -(-n // align) * align
+        self.numel = int(off)
         self.buffer = torch.zeros(self.numel, dtype=torch.float32, device=device)
         self.views = {}
-        off = 0
-        for (name, shape), n in zip(self.specs, sizes):
-            self.views[name] = self.buffer[off:off + n].view(shape)
-            off += n
+        for (name, shape), o, n in zip(self.specs, self.offsets, self.sizes):
+            self.views[name] = self.buffer[o:o + n].view(shape)
 
     def __getitem__(self, name):
         return self.views[name]

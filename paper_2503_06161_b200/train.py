@@ -142,7 +142,7 @@ class TrainStep:
         self.params = params
         self.schedules = dict(schedules)
         self.schedules.setdefault("sh_rest", self.schedules.get("colors_raw"))
-        self.optimizer = FlatAdam(self.specs, params.buffer)
+        self.optimizer = FlatAdam(self.specs, params.buffer, offsets=params.offsets)
         return self
 
     def current_lrs(self):

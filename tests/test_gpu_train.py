@@ -226,14 +226,12 @@ def test_fine_stage_step_decoder_tv_adam_matches_oracle():
     p1 = step.params.buffer.cpu().numpy().astype(np.float64)
     g0 = step.grads.buffer.cpu().numpy().astype(np.float64)
     p0 = p0.cpu().numpy().astype(np.float64)
-    off = 0
     lrs = {key: s.lr_init for key, s in schedules.items()}  # iteration 0: lr_at_step(s, 0) == lr_init
     lrs["net"] = schedules["net"].lr_init * schedules["net"].delay_mult
-    for name, shape in step.specs:
+    for (name, shape), off in zip(step.specs, step.params.offsets):
         n = int(np.prod(shape))
         lr = lrs["colors_raw"] if name == "sh_rest" else lrs[schedule_key(name)]
         ref, _, _, _ = O.adam_update(p0[off:off + n], g0[off:off + n], 0.0, 0.0, 0, lr, adam_eps(name))
         got = p1[off:off + n]
         assert np.abs(got - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max()), name
-        off += n
     assert step.iteration == 1

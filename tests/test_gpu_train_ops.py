@@ -162,7 +162,7 @@ def test_tv_accumulates_into_gradient_buffer():
     tv_loss_grad_device(dev, grads, 0.25, True, loss)
     ref_loss, ref_g = O.total_variation([[p.astype(np.float32).astype(np.float64) for p in lv] for lv in planes],
                                         0.25)
-    assert float(loss.item()) == pytest.approx(ref_loss, rel=1e-6)
+    assert float(loss.item()) == pytest.approx(0.25 * ref_loss, rel=1e-6)  # loss += scale * tv
     for p in range(6):
         close(grads.planes[0][p].cpu().numpy(), base[0][p] + ref_g[0][p], 1e-6, f"plane {p}")
 
