@@ -689,7 +689,7 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
   int rc = tc_pack(net, field, t, p, blob, s);
   if (rc) return rc;
   const int64_t K = cloud.K;
-  char* base = (char*)ws + (p.blob_bytes + 255) / 256 * 256;
+  char* base = (char*)ws + p.ws_bytes;
   float* dlat = (float*)base;
   float* wpart = (float*)(base + ((size_t)K * 64 * 4 + 255) / 256 * 256);
   const int64_t ntiles = ceil_div(K, kTcRows);

@@ -157,6 +157,91 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPla
   }
 }
 
+// Same gather, with the three time planes of each level read as 1-D lerps of
+// the per-frame time rows (k_pack_tc): 2 corner rows instead of 4 for half
+// of the planes, and those rows (72 KB at configs[1]) stay L1/L2-hot.  The
+// kernel is bound by L2->SM bytes, so this halves the time planes' share.
+template <int LEVELS>
+__global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPlan p, int64_t K,
+                                                                              const float* __restrict__ pos,
+                                                                              const float* __restrict__ rows,
+                                                                              float* __restrict__ latent) {
+  __shared__ int s_base[kGatherWarps][LEVELS * 6][32];
+  __shared__ float2 s_f[kGatherWarps][LEVELS * 6][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g0 = ((int64_t)blockIdx.x * kGatherWarps + warp) * 32;
+  if (g0 >= K) return;
+  {
+    const int64_t k = g0 + lane;
+    double c[3] = {0.0, 0.0, 0.0};
+    if (k < K) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double raw = ((double)pos[3 * k + a] - p.lo[a]) / p.span[a];
+        c[a] = fmin(fmax(raw, 0.0), 1.0);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < LEVELS; ++l)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int ra = p.res[l][q][0], rb = p.res[l][q][1];
+        const double u = c[c_axes_tc[q][0]] * (ra - 1);
+        int i0 = (int)floor(u);
+        i0 = min(max(i0, 0), ra - 2);
+        if (q == 2 || q == 4 || q == 5) {
+          s_base[warp][l * 6 + q][lane] = i0 * 32;
+          s_f[warp][l * 6 + q][lane] = make_float2((float)(u - i0), 0.f);
+        } else {
+          const double v = c[c_axes_tc[q][1]] * (rb - 1);
+          int j0 = (int)floor(v);
+          j0 = min(max(j0, 0), rb - 2);
+          s_base[warp][l * 6 + q][lane] = (i0 * rb + j0) * 32;
+          s_f[warp][l * 6 + q][lane] = make_float2((float)(u - i0), (float)(v - j0));
+        }
+      }
+  }
+  __syncwarp();
+  const int sub = lane >> 3, ch = (lane & 7) * 4;
+  for (int j0 = 0; j0 < 32; j0 += 4) {
+    const int j = j0 + sub;
+    const int64_t k = g0 + j;
+#pragma unroll
+    for (int l = 0; l < LEVELS; ++l) {
+      float4 prod = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const float2 f = s_f[warp][l * 6 + q][j];
+        if (q == 2 || q == 4 || q == 5) {
+          const int tq = q == 2 ? 0 : (q == 4 ? 1 : 2);
+          const float* rp = rows + p.row_off[l][tq] + s_base[warp][l * 6 + q][j] + ch;
+          const float4 a = __ldg(reinterpret_cast<const float4*>(rp));
+          const float4 c = __ldg(reinterpret_cast<const float4*>(rp + 32));
+          const float wa = 1.f - f.x;
+          prod.x *= wa * a.x + f.x * c.x;
+          prod.y *= wa * a.y + f.x * c.y;
+          prod.z *= wa * a.z + f.x * c.z;
+          prod.w *= wa * a.w + f.x * c.w;
+        } else {
+          const int rs = p.res[l][q][1] * 32;
+          const float* pl = p.planes[l][q] + s_base[warp][l * 6 + q][j] + ch;
+          const float w00 = (1.f - f.x) * (1.f - f.y), w10 = f.x * (1.f - f.y);
+          const float w01 = (1.f - f.x) * f.y, w11 = f.x * f.y;
+          const float4 a = __ldg(reinterpret_cast<const float4*>(pl));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(pl + 32));
+          const float4 c = __ldg(reinterpret_cast<const float4*>(pl + rs));
+          const float4 d = __ldg(reinterpret_cast<const float4*>(pl + rs + 32));
+          prod.x *= w00 * a.x + w10 * c.x + w01 * b.x + w11 * d.x;
+          prod.y *= w00 * a.y + w10 * c.y + w01 * b.y + w11 * d.y;
+          prod.z *= w00 * a.z + w10 * c.z + w01 * b.z + w11 * d.z;
+          prod.w *= w00 * a.w + w10 * c.w + w01 * b.w + w11 * d.w;
+        }
+      }
+      if (k < K) *reinterpret_cast<float4*>(latent + k * 64 + l * 32 + ch) = prod;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // weight packing: fp32 [out,in] -> bf16 hi/lo K-major core-matrix operands
 // ---------------------------------------------------------------------------
@@ -173,13 +258,26 @@ struct TcBias {
   const float* b[4];
   int len[4], at[4];
 };
+struct TcRowOp {
+  const float* plane;  // [Ra, Rb, 32]
+  int Ra, Rb, j0, off; // off: float offset into the rows region
+  float fb;
+};
 struct TcPackArgs {
   TcOperand op[FS4D_MAX_TRUNK + 12];
   int nop;
   TcBias bias[FS4D_MAX_TRUNK + 8];
   int nbias;
+  TcRowOp row[FS4D_MAX_LEVELS * 3];
+  int nrow;
+  float* rows;
   uint8_t* blob;
 };
+
+// reserved for the time rows in every blob (fixed so workspace sizing does
+// not depend on the field): sum over levels of 3 * Ra * 32 floats
+constexpr int kTimeRowBytes = 256 * 1024;
+constexpr int kTimeQ[3] = {2, 4, 5};  // planes (x,t), (y,t), (z,t) of PLANE_AXES
 
 __global__ void k_pack_tc(TcPackArgs a) {
   const int o = blockIdx.y;
@@ -199,6 +297,14 @@ __global__ void k_pack_tc(TcPackArgs a) {
       const int off = core_off(r, k, op.KT) / 2;
       hi[off] = h;
       lo[off] = l;
+    }
+  } else if (o >= a.nop + a.nbias) {
+    const TcRowOp& r = a.row[o - a.nop - a.nbias];
+    float* dst = a.rows + r.off;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < r.Ra * 32; e += gridDim.x * blockDim.x) {
+      const int i = e >> 5, c = e & 31;
+      const float* src = r.plane + ((int64_t)i * r.Rb + r.j0) * 32 + c;
+      dst[e] = (1.f - r.fb) * src[0] + r.fb * src[32];
     }
   } else {
     const TcBias& b = a.bias[o - a.nop];
@@ -723,9 +829,30 @@ static int build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, T
     if (pk) pk->op[nop++] = TcOperand{16, 32, p.off_headT[b], 1, {src(n.head[b], hoff[b])}};
   }
   p.blob_bytes = (off + 15) / 16 * 16;
+  p.off_rows = (p.blob_bytes + 255) / 256 * 256;
+  p.ws_bytes = p.off_rows + kTimeRowBytes;
+  // time rows (only for the 32-channel gather; Rb >= 2 guaranteed by the field)
+  int nrow = 0, rfl = 0;
+  p.rows_ok = n.enable_grid && f.channels == 32 && f.levels == 2;
+  for (int l = 0; p.rows_ok && l < f.levels; ++l)
+    for (int tq = 0; tq < 3; ++tq) {
+      const int q = kTimeQ[tq], Ra = f.res[l][q][0], Rb = f.res[l][q][1];
+      if ((rfl + Ra * 32) * 4 > kTimeRowBytes || Rb < 2) {
+        p.rows_ok = 0;
+        break;
+      }
+      const double v = p.t * (Rb - 1);  // hexplane.py:99-101 on the time axis
+      int j0 = (int)floor(v);
+      j0 = j0 < 0 ? 0 : (j0 > Rb - 2 ? Rb - 2 : j0);
+      p.row_off[l][tq] = rfl;
+      if (pk) pk->row[nrow++] = TcRowOp{f.planes[l][q], Ra, Rb, j0, rfl, (float)(v - j0)};
+      rfl += Ra * 32;
+    }
+  if (!p.rows_ok) nrow = 0;
   if (pk) {
     pk->nop = nop;
     pk->nbias = nb;
+    pk->nrow = nrow;
   }
   // shared memory: weights + X + E must fit
   const int smem = ((p.fwd_bytes + 1023) & ~1023) + kTcRows * 64 * 4 + kTcRows * 128 * 4;
@@ -742,7 +869,8 @@ int tc_pack(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p, 
   int rc = build_plan(n, f, t, p, &pk);
   if (rc) return rc;
   pk.blob = blob;
-  k_pack_tc<<<dim3(4, pk.nop + pk.nbias), 256, 0, s>>>(pk);
+  pk.rows = reinterpret_cast<float*>(blob + p.off_rows);
+  k_pack_tc<<<dim3(4, pk.nop + pk.nbias + pk.nrow), 256, 0, s>>>(pk);
   return check_launch("deform_tc_pack");
 }
 
@@ -762,7 +890,7 @@ size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K) {
   TcPlan p;
   build_plan(n, f, 0.0, p, nullptr);
   // forward: latent [K, 64]; backward: d_latent [K, 64] + one weight-gradient partial per SM
-  return (size_t)((p.blob_bytes + 255) / 256 * 256) + (size_t)K * 64 * 4 + (size_t)kNumSMs * kPartStride * 4 + 512;
+  return (size_t)p.ws_bytes + (size_t)K * 64 * 4 + (size_t)kNumSMs * kPartStride * 4 + 512;
 }
 
 int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
@@ -771,7 +899,7 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   uint8_t* blob = (uint8_t*)ws;
   int rc = tc_pack(net, field, t, p, blob, s);
   if (rc) return rc;
-  float* latent = (float*)((char*)ws + (p.blob_bytes + 255) / 256 * 256);
+  float* latent = (float*)((char*)ws + p.ws_bytes);
   const int64_t K = cloud.K;
   if (K == 0) return FS4D_OK;
   // The fused variant (HexPlane gather as 4 producer warps inside the MLP
@@ -782,7 +910,10 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   const bool fused = !cache && getenv("FS4D_FUSED_GATHER") && (!p.enable_grid || (p.C == 32 && p.levels == 2));
   const unsigned gblocks = (unsigned)ceil_div(K, kGatherWarps * 32);
   if (!fused) {
-    if (p.enable_grid && p.C == 32 && p.levels == 2)
+    if (p.rows_ok && !getenv("FS4D_NO_TIME_ROWS"))
+      k_hexplane_latent_c32t<2><<<gblocks, kGatherWarps * 32, 0, s>>>(
+          p, K, cloud.positions, reinterpret_cast<const float*>(blob + p.off_rows), latent);
+    else if (p.enable_grid && p.C == 32 && p.levels == 2)
       k_hexplane_latent_c32<2><<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
     else
       k_hexplane_latent<<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);

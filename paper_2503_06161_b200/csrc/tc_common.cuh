@@ -30,7 +30,12 @@ struct TcPlan {
   int off_trunk[FS4D_MAX_TRUNK], off_ext0, off_ext1[4], off_head[4], off_f1, off_f2;
   int off_headT[4];  // head b weights placed at rows hoff[b].. of a 16-row image (backward)
   int off_b_trunk[FS4D_MAX_TRUNK], off_b_ext0, off_b_ext1, off_b_head, off_b_f1, off_b_f2;
-  int blob_bytes;  // whole blob (pack target)
+  // per-frame time rows of the (x,t),(y,t),(z,t) planes (all Gaussians share
+  // t, so those bilinear lookups collapse to 1-D lerps between two rows of
+  // R[i] = (1-fb) P[i][j0] + fb P[i][j0+1]); float offsets from off_rows
+  int rows_ok, off_rows, row_off[FS4D_MAX_LEVELS][3];
+  int blob_bytes;  // packed weights (what the kernels stage in shared memory)
+  int ws_bytes;    // blob + time rows: start of the next workspace region (256-aligned)
   int fwd_bytes;   // prefix the forward kernel stages in shared memory
 };
 
