@@ -706,17 +706,31 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
         signal();
         wait_acc();
         const float* fb = bias_f + p.off_b_f2 / 4;
-        for (int c = 8 * half, q0 = 0; c < p.DP; c += 16, q0 += 8) {
+        // the first two 16-column chunks use the prefetched fv[] with static
+        // indices (no local-memory array); wider feature maps re-read the cloud
+#pragma unroll
+        for (int qc = 0; qc < 2; ++qc) {
+          const int c = 8 * half + 16 * qc;
+          if (c >= p.DP) break;
           float v[8];
           tmem_ld8(tmem_row + c, v);
           if (valid) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               if (c + i < p.D) {
-                const float base = p.DP <= 32 ? fv[(q0 + i) & 15] : a.feat[(int64_t)p.D * k + c + i];
+                const float base = p.DP <= 32 ? fv[8 * qc + i] : a.feat[(int64_t)p.D * k + c + i];
                 a.o_feat[(int64_t)p.D * k + c + i] = base + v[i] + fb[c + i];
               }
             }
+          }
+        }
+        for (int c = 8 * half + 32; c < p.DP; c += 16) {
+          float v[8];
+          tmem_ld8(tmem_row + c, v);
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (c + i < p.D) a.o_feat[(int64_t)p.D * k + c + i] = a.feat[(int64_t)p.D * k + c + i] + v[i] + fb[c + i];
           }
         }
       }

@@ -262,7 +262,11 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   __shared__ float4 s_co[NT];
   __shared__ int4 s_pr[NT];
   __shared__ float4 s_rgbz[NT];
-  __shared__ __align__(16) float s_f[DC > 0 ? NT * DC : 1];
+  // features channel-quad-major [DC/4][NT] float4: conflict-free staging
+  // stores, broadcast reads in the compositing loop
+  __shared__ __align__(16) float4 s_f4[DC > 0 ? NT * DC / 4 : 1];
+  // per-warp ballot masks of the staged batch (shared, not a local array)
+  __shared__ unsigned s_mask[NT / 32][NT / 32];
 
   const int tile = blockIdx.x / SUB, sub = blockIdx.x % SUB;
   const int tx = tile % a.ntx, ty = tile / a.ntx;
@@ -277,10 +281,13 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   const int wrow0 = row0 + (threadIdx.x >> 5) * 2;  // this warp's two pixel rows
   const int tcol0 = tx * kTile;
 
-  float T = 1.f, acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f;
-  float accf[DC > 0 ? DC : 1];
+  // accumulators as float2 pairs: every update is one FFMA2 (two fp32 FMAs,
+  // bit-identical to the scalar FMAs) -- halves the blend's FMA issue slots
+  float T = 1.f;
+  float2 acc_rg = make_float2(0.f, 0.f), acc_bz = make_float2(0.f, 0.f);
+  float2 accf2[DC > 0 ? DC / 2 : 1];
 #pragma unroll
-  for (int c = 0; c < (DC > 0 ? DC : 1); ++c) accf[c] = 0.f;
+  for (int c = 0; c < (DC > 0 ? DC / 2 : 1); ++c) accf2[c] = make_float2(0.f, 0.f);
   int ncontrib = 0, last = -1;
   bool done = !inside;
   const int nf = DC > 0 ? min(DC, a.D - a.c0) : 0;
@@ -297,13 +304,15 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
       s_rgbz[threadIdx.x] = a.rgbz[g];
       if (DC > 0) {
         const float* src = a.features + (int64_t)g * a.D + a.c0;
-        float* dst = s_f + threadIdx.x * DC;
         if (vec_ok) {
 #pragma unroll
-          for (int c = 0; c < DC; c += 4)
-            *reinterpret_cast<float4*>(dst + c) = __ldg(reinterpret_cast<const float4*>(src + c));
+          for (int c = 0; c < DC; c += 4) s_f4[(c / 4) * NT + threadIdx.x] = __ldg(reinterpret_cast<const float4*>(src + c));
         } else {
-          for (int c = 0; c < DC; ++c) dst[c] = c < nf ? src[c] : 0.f;
+          for (int c = 0; c < DC; c += 4) {
+            float v[4];
+            for (int i = 0; i < 4; ++i) v[i] = c + i < nf ? src[c + i] : 0.f;
+            s_f4[(c / 4) * NT + threadIdx.x] = make_float4(v[0], v[1], v[2], v[3]);
+          }
         }
       }
     }
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
     // warp-level culling: one ballot per 32 staged Gaussians keeps those whose
     // pixel footprint touches this warp's two pixel rows; the per-thread loop
     // then walks only the set bits, in depth order
-    unsigned wmask[NT / 32];
+    const int wid = threadIdx.x >> 5;
 #pragma unroll
     for (int m = 0; m < NT / 32; ++m) {
       const int kk = m * 32 + lane;
@@ -321,54 +330,72 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
         const int4 pr = s_pr[kk];
         hit = pr.w >= wrow0 && pr.z <= wrow0 + 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
       }
-      wmask[m] = __ballot_sync(0xffffffffu, hit);
+      const unsigned msk = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) s_mask[wid][m] = msk;
     }
+    __syncwarp();
     if (!done) {
 #pragma unroll 1
       for (int m = 0; m < NT / 32 && !done; ++m) {
-        unsigned bits = wmask[m];
+        unsigned bits = s_mask[wid][m];
+        // groups of BK Gaussians: the alphas of a group are independent of T
+        // (instruction-level parallelism across the smem loads and ex2), only
+        // the compositing below is a serial chain -- same decisions, same order
+        constexpr int BK = 4;
         while (bits) {
-          const int k = m * 32 + __ffs(bits) - 1;
-          bits &= bits - 1;
-          const int4 pr = s_pr[k];
-          if (col < pr.x || col > pr.y || row < pr.z || row > pr.w) continue;
-          const float2 mm = s_xy[k];
-          const float4 co = s_co[k];
-          const float dx = fc - mm.x, dy = fr - mm.y;
-          const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
-          if (q > kQSkip) continue;
-          const float gv = __expf(-0.5f * q);
-          const float al = fminf(co.w * gv, a.alpha_cap);
-          if (al < a.alpha_skip) continue;
-          if (T < a.stop) {
-            done = true;
-            break;
-          }
-          const float w = al * T;
-          if (first) {
-            const float4 cz = s_rgbz[k];
-            acc_r += w * cz.x;
-            acc_g += w * cz.y;
-            acc_b += w * cz.z;
-            acc_z += w * cz.w;
-          }
-          if (DC > 0) {
+          int kk[BK];
+          float alv[BK];
+          bool live[BK];
 #pragma unroll
-            for (int c = 0; c < DC; c += 4) {
-              const float4 fv = *reinterpret_cast<const float4*>(&s_f[k * DC + c]);
-              accf[c] += w * fv.x;
-              accf[c + 1] += w * fv.y;
-              accf[c + 2] += w * fv.z;
-              accf[c + 3] += w * fv.w;
+          for (int j = 0; j < BK; ++j) {
+            kk[j] = bits ? m * 32 + __ffs(bits) - 1 : 0;
+            live[j] = bits != 0;
+            bits &= bits - 1;
+          }
+#pragma unroll
+          for (int j = 0; j < BK; ++j) {
+            const int k = kk[j];
+            const int4 pr = s_pr[k];
+            const float2 mm = s_xy[k];
+            const float4 co = s_co[k];
+            const float dx = fc - mm.x, dy = fr - mm.y;
+            const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
+            const float gv = __expf(-0.5f * q);
+            const float al = fminf(co.w * gv, a.alpha_cap);
+            live[j] = live[j] && !(col < pr.x || col > pr.y || row < pr.z || row > pr.w) && !(q > kQSkip) &&
+                      !(al < a.alpha_skip);
+            alv[j] = al;
+          }
+#pragma unroll
+          for (int j = 0; j < BK; ++j) {
+            if (!live[j] || done) continue;
+            if (T < a.stop) {
+              done = true;
+              continue;
             }
+            const int k = kk[j];
+            const float al = alv[j];
+            const float w = al * T;
+            const float2 w2 = make_float2(w, w);
+            if (first) {
+              const float4 cz = s_rgbz[k];
+              acc_rg = __ffma2_rn(w2, make_float2(cz.x, cz.y), acc_rg);
+              acc_bz = __ffma2_rn(w2, make_float2(cz.z, cz.w), acc_bz);
+            }
+            if (DC > 0) {
+#pragma unroll
+              for (int c = 0; c < DC; c += 4) {
+                const float4 fv = s_f4[(c / 4) * NT + k];
+                accf2[c / 2] = __ffma2_rn(w2, make_float2(fv.x, fv.y), accf2[c / 2]);
+                accf2[c / 2 + 1] = __ffma2_rn(w2, make_float2(fv.z, fv.w), accf2[c / 2 + 1]);
+              }
+            }
+            T *= (1.f - al);
+            ++ncontrib;
+            last = (int)(b + k);
+            if (T < a.stop) done = true;
           }
-          T *= (1.f - al);
-          ++ncontrib;
-          last = (int)(b + k);
-          if (T < a.stop) {
-            done = true;
-            break;
-          }
+          if (done) break;
         }
       }
     }
@@ -376,10 +403,10 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   if (!inside) return;
   const int64_t pix = (int64_t)row * a.W + col;
   if (first) {
-    a.out_color[3 * pix + 0] = acc_r + T * a.bg0;
-    a.out_color[3 * pix + 1] = acc_g + T * a.bg1;
-    a.out_color[3 * pix + 2] = acc_b + T * a.bg2;
-    a.out_depth[pix] = acc_z;
+    a.out_color[3 * pix + 0] = acc_rg.x + T * a.bg0;
+    a.out_color[3 * pix + 1] = acc_rg.y + T * a.bg1;
+    a.out_color[3 * pix + 2] = acc_bz.x + T * a.bg2;
+    a.out_depth[pix] = acc_bz.y;
     a.out_alpha[pix] = 1.f - T;
     if (a.out_ncontrib) a.out_ncontrib[pix] = ncontrib;
     a.tfinal[pix] = T;
@@ -390,11 +417,12 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
     if (vec_ok) {
 #pragma unroll
       for (int c = 0; c < DC; c += 4)
-        *reinterpret_cast<float4*>(dst + c) = make_float4(accf[c], accf[c + 1], accf[c + 2], accf[c + 3]);
+        *reinterpret_cast<float4*>(dst + c) =
+            make_float4(accf2[c / 2].x, accf2[c / 2].y, accf2[c / 2 + 1].x, accf2[c / 2 + 1].y);
     } else {
 #pragma unroll
       for (int c = 0; c < DC; ++c)
-        if (c < nf) dst[c] = accf[c];
+        if (c < nf) dst[c] = (c & 1) ? accf2[c / 2].y : accf2[c / 2].x;
     }
   }
 }
