@@ -371,6 +371,39 @@ __device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, 
   }
 }
 
+// NCH 8-column TMEM chunks at taddr0 + 16 i (one thread's half of a stage),
+// all issued before a single tcgen05.wait::ld: one TMEM round trip per stage
+// instead of one per chunk.  The empty asm ties keep every use after the wait.
+template <int NCH>
+__device__ __forceinline__ void tmem_ld_batch(uint32_t taddr0, float (&v)[NCH][8]) {
+  uint32_t r[NCH][8];
+#pragma unroll
+  for (int i = 0; i < NCH; ++i)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[i][0]), "=r"(r[i][1]), "=r"(r[i][2]), "=r"(r[i][3]), "=r"(r[i][4]), "=r"(r[i][5]),
+                   "=r"(r[i][6]), "=r"(r[i][7])
+                 : "r"(taddr0 + 16u * i));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    asm volatile("" : "+r"(r[i][0]), "+r"(r[i][1]), "+r"(r[i][2]), "+r"(r[i][3]), "+r"(r[i][4]), "+r"(r[i][5]),
+                 "+r"(r[i][6]), "+r"(r[i][7]));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[i][j] = __uint_as_float(r[i][j]);
+  }
+}
+
+// bias -> relu -> bf16 hi/lo of one loaded chunk into an A operand (+ optional cached image)
+__device__ __forceinline__ void chunk_to_operand(float (&v)[8], const float* bias, uint8_t* a_base, int KT, int k0,
+                                                 int r, uint8_t* cimg = nullptr, int cKT = 0, int ck0 = 0) {
+  const float4 b0 = *reinterpret_cast<const float4*>(bias), b1 = *reinterpret_cast<const float4*>(bias + 4);
+  const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};  // 32-byte aligned bias chunk
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i] + bv[i], 0.f);
+  store_split8(a_base, KT, r, k0, v);
+  if (cimg) cache_split8(cimg, cKT, r, ck0, v);
+}
+
 // ---------------------------------------------------------------------------
 // warp-specialised variant: warps 0-7 run the epilogues (two threads per TMEM
 // lane), warp 8 only issues MMAs.  Epilogue threads never block on each other:
@@ -458,6 +491,20 @@ __device__ __forceinline__ void produce_latent(const TcArgs& a, int64_t tile, ui
   }
 }
 
+#ifdef FS4D_MLP_TRACE
+// debug timeline of CTA 0 (tools/mlp_trace.sh): clock64 << 4 | event
+// (MMA warp: 1 operand ready, 2 commit; epilogue thread 0: 3 acc ready, 4 signal)
+__device__ long long g_mlp_trace[2][512];
+__device__ int g_mlp_n[2];
+#define MLP_TRACE(who, ev)                                                           \
+  if (blockIdx.x == 0) {                                                             \
+    const int i_ = g_mlp_n[who]++;                                                   \
+    if (i_ < 512) g_mlp_trace[who][i_] = ((long long)clock64() << 4) | (ev);         \
+  }
+#else
+#define MLP_TRACE(who, ev)
+#endif
+
 template <bool FUSED, bool CACHE>
 __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_mlp_tc_ws(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -521,14 +568,21 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
     }
   } else if (mma_warp) {
     // ------------------------------------------------------------ MMA issuer
+    // the whole warp runs the issue code (uniform descriptors); an elected
+    // lane issues each tcgen05.mma / commit
     uint32_t iter = 0;
     int slot = 0;
+    const bool leader = (tid & 31) == 0;
     auto wait_op = [&]() {
       mbar_wait(opbar + 8 * slot, iter & 1);
       ++slot;
       tc_fence_after();
+      if (leader) MLP_TRACE(0, 1);
     };
-    const bool leader = (tid & 31) == 0;
+    auto commit = [&]() {
+      mma_commit_w(accbar);
+      if (leader) MLP_TRACE(0, 2);
+    };
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
       slot = 0;
       const int s = FUSED ? (iter & 1) : 0;
@@ -540,40 +594,29 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
         } else {
           wait_op();  // X holds the latent / previous trunk output
         }
-        if (leader) {
-          gemm_bf16x3(tmem + 128, sX, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
-          mma_commit(accbar);
-        }
-        __syncwarp();
+        gemm_bf16x3_w(tmem + 128, sX, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
+        commit();
       }
       for (int c = 0; c < 64; c += 16) {  // hidden chunk c -> extractor-0 K step
         wait_op();
-        if (leader) gemm_bf16x3(tmem, sX, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
-        __syncwarp();
+        gemm_bf16x3_w(tmem, sX, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
       }
-      if (leader) mma_commit(accbar);
+      commit();
       for (int b = 0; b < 4; ++b) {  // e1 of branch b -> extractor-1
         wait_op();
-        if (leader) gemm_bf16x3(tmem + 32 * b, sE, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
-        __syncwarp();
+        gemm_bf16x3_w(tmem + 32 * b, sE, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
       }
-      if (leader) mma_commit(accbar);
+      commit();
       for (int b = 0; b < 4; ++b) {  // e2 of branch b -> head b and F_feat layer-0 K slice
         wait_op();
-        if (leader) {
-          gemm_bf16x3(tmem + 128 + 16 * b, sE, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
-          if (p.enable_feat) gemm_bf16x3(tmem + 192, sE, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
-        }
-        __syncwarp();
+        gemm_bf16x3_w(tmem + 128 + 16 * b, sE, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
+        if (p.enable_feat) gemm_bf16x3_w(tmem + 192, sE, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
       }
-      if (leader) mma_commit(accbar);
+      commit();
       if (p.enable_feat) {
         wait_op();  // FF in X
-        if (leader) {
-          gemm_bf16x3(tmem, sX, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
-          mma_commit(accbar);
-        }
-        __syncwarp();
+        gemm_bf16x3_w(tmem, sX, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
+        commit();
       }
       wait_op();  // tile finished: TMEM and X free for the next tile
       if (FUSED && leader) mbar_arrive(xempty + 8 * s);
@@ -589,6 +632,7 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
       mbar_wait(accbar, ph);
       ph ^= 1;
       tc_fence_after();
+      if (tid == 0) MLP_TRACE(1, 3);
     };
     int slot = 0;
     auto signal = [&]() {
@@ -596,6 +640,7 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
       tc_fence_before();
       mbar_arrive(opbar + 8 * slot);
       ++slot;
+      if (tid == 0) MLP_TRACE(1, 4);
     };
     float4 lat[8];
     auto load_latent = [&](int64_t t) {
@@ -662,24 +707,46 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
           epilogue_to_operand(tmem_row, 128, 64, tb, true, X, 64, 0, row, half);
           signal();
         } else {
-          for (int c = 0; c < 64; c += 16) {
-            epilogue_to_operand(tmem_row, 128 + c, 16, tb + c, true, X, 64, c, row, half,
-                                CACHE ? ct + kCacheHid : nullptr, kCacheKtHid, c);
+          float v[4][8];
+          tmem_ld_batch<4>(tmem_row + 128 + 8 * half, v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int c = 16 * i + 8 * half;
+            chunk_to_operand(v[i], tb + c, X, 64, c, row, CACHE ? ct + kCacheHid : nullptr, kCacheKtHid, c);
             signal();
           }
         }
       }
-      wait_acc();
-      for (int b = 0; b < 4; ++b) {
-        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext0 / 4 + 32 * b, true, E, 128, 32 * b, row, half,
-                            CACHE ? ct + kCacheE1 + b * kCacheE1Bytes : nullptr, kCacheKtE1, 0);
-        signal();
+      {
+        wait_acc();
+        float v[8][8];
+        tmem_ld_batch<8>(tmem_row + 8 * half, v);
+        const float* eb = bias_f + p.off_b_ext0 / 4;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int c = 32 * b + 16 * i + 8 * half;
+            chunk_to_operand(v[2 * b + i], eb + c, E, 128, c, row, CACHE ? ct + kCacheE1 + b * kCacheE1Bytes : nullptr,
+                             kCacheKtE1, c - 32 * b);
+          }
+          signal();
+        }
       }
-      wait_acc();
-      for (int b = 0; b < 4; ++b) {
-        epilogue_to_operand(tmem_row, 32 * b, 32, bias_f + p.off_b_ext1 / 4 + 32 * b, true, E, 128, 32 * b, row, half,
-                            CACHE ? ct + kCacheE2 : nullptr, kCacheKtE2, 32 * b);
-        signal();
+      {
+        wait_acc();
+        float v[8][8];
+        tmem_ld_batch<8>(tmem_row + 8 * half, v);
+        const float* eb = bias_f + p.off_b_ext1 / 4;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int c = 32 * b + 16 * i + 8 * half;
+            chunk_to_operand(v[2 * b + i], eb + c, E, 128, c, row, CACHE ? ct + kCacheE2 : nullptr, kCacheKtE2, c);
+          }
+          signal();
+        }
       }
       wait_acc();
       {
@@ -874,6 +941,17 @@ static int build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, T
   return FS4D_OK;
 }
 
+#ifdef FS4D_MLP_TRACE
+extern "C" int fs4d_debug_mlp_trace(long long* out, int* n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_mlp_trace, sizeof(long long) * 1024);
+  cudaMemcpyFromSymbol(n, g_mlp_n, sizeof(int) * 2);
+  int z[2] = {0, 0};
+  cudaMemcpyToSymbol(g_mlp_n, z, sizeof(z));
+  return 0;
+}
+#endif
+
 int tc_build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p) {
   return build_plan(n, f, t, p, nullptr);
 }
@@ -958,6 +1036,10 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
     cudaFuncSetAttribute(k_mlp_tc_ws<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mlp_tc_ws<false, true><<<grid, kTcWsThreads, smem, s>>>(a);
   } else {
+    // (a two-slot variant -- two tiles in flight per SM, branch-wise
+    // extractors, one epilogue thread per row -- was measured slower on B200,
+    // 220 vs 179 us at configs[1]: the chain is bound by epilogue issue, not
+    // by MMA latency, and halving the threads per tile lengthens it.)
     cudaFuncSetAttribute(k_mlp_tc_ws<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mlp_tc_ws<false, false><<<grid, kTcWsThreads, smem, s>>>(a);
   }

@@ -75,6 +75,25 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// Warp-wide variants: every lane executes the call with identical (uniform)
+// descriptors and one elected lane issues -- the descriptor arithmetic then
+// stays on the uniform datapath instead of going through one divergent lane
+// (measured ~90 cycles per MMA issue that way).
+__device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit_w(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -148,6 +167,23 @@ __device__ __forceinline__ void gemm_bf16x3(uint32_t tmem_d, uint32_t a_base, in
   }
 }
 
+// warp-wide gemm_bf16x3 (all 32 lanes call it; one elected lane issues)
+__device__ __forceinline__ void gemm_bf16x3_w(uint32_t tmem_d, uint32_t a_base, int a_kt, int a_k0, uint32_t b_base,
+                                              int b_kt, int b_k0, int N, int ksteps, bool accumulate) {
+  const uint32_t id = idesc_bf16(N);
+  const uint32_t a_lo = a_base + kTcRows * a_kt * 2, b_lo = b_base + N * b_kt * 2;
+  const uint32_t a_sbo = a_kt * 16, b_sbo = b_kt * 16;
+#pragma unroll
+  for (int s = 0; s < ksteps; ++s) {
+    const uint32_t ak = (uint32_t)(((a_k0 >> 3) + 2 * s) * 128), bk = (uint32_t)(((b_k0 >> 3) + 2 * s) * 128);
+    const uint64_t ah = sdesc(a_base + ak, 128, a_sbo), al = sdesc(a_lo + ak, 128, a_sbo);
+    const uint64_t bh = sdesc(b_base + bk, 128, b_sbo), bl = sdesc(b_lo + bk, 128, b_sbo);
+    mma_bf16_w(tmem_d, ah, bh, id, (s > 0 || accumulate) ? 1u : 0u);
+    mma_bf16_w(tmem_d, ah, bl, id, 1u);
+    mma_bf16_w(tmem_d, al, bh, id, 1u);
+  }
+}
+
 // General operand view of a row image for the backward GEMMs.
 struct TcOpnd {
   uint32_t base;   // shared address of the first core matrix used (hi block)
@@ -181,15 +217,25 @@ __device__ __forceinline__ void gemm3(uint32_t tmem_d, const TcOpnd& A, const Tc
   }
 }
 
+// v = hi + lo with hi = bf16_rn(v), lo = bf16_rn(v - hi) (v - hi is exact in
+// fp32).  Pairs go through cvt.rn.bf16x2.f32 (one packed convert per two
+// values); bit-identical to per-element __float2bfloat16_rn.
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo_elem, float hi_elem) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
+  return d;
+}
+
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
-  __nv_bfloat16 h[8], l[8];
+  uint32_t h[4], l[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    h[i] = __float2bfloat16_rn(v[i]);
-    l[i] = __float2bfloat16_rn(v[i] - __bfloat162float(h[i]));
+  for (int i = 0; i < 4; ++i) {
+    h[i] = cvt_bf16x2(v[2 * i], v[2 * i + 1]);
+    const float h0 = __uint_as_float(h[i] << 16), h1 = __uint_as_float(h[i] & 0xFFFF0000u);
+    l[i] = cvt_bf16x2(v[2 * i] - h0, v[2 * i + 1] - h1);
   }
-  hi = *reinterpret_cast<const uint4*>(h);
-  lo = *reinterpret_cast<const uint4*>(l);
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 // store 8 consecutive values (k0..k0+7) of row r into an A operand (hi, lo) with KT columns
