@@ -344,6 +344,43 @@ int fs4d_decoder_feature_loss(const float* rendered, int32_t hi, int32_t wi, int
                               int32_t accumulate, double* loss, void* workspace, size_t workspace_bytes,
                               void* stream);
 
+/* ---- adaptive density control (gaussians.py:309-425) ---- */
+/* DensityControlConfig (gaussians.py:330-334) plus the scene extent. */
+typedef struct Fs4dDensityConfig {
+  double grad_threshold, percent_dense, prune_opacity, split_factor, extent;
+} Fs4dDensityConfig;
+
+/* ViewspaceGradStats.add (gaussians.py:319-321): accum[idx[i]] += norms[i],
+ * count[idx[i]] += 1 for i < n (n = min(n, *n_dev) when n_dev != NULL; the
+ * indices of one render_backward are distinct).  accum / count are float64. */
+int fs4d_grad_stats_add(double* accum, double* count, const int32_t* indices, const float* norms, int64_t n,
+                        const int32_t* n_dev, void* stream);
+
+/* densify_and_prune (gaussians.py:349-405) / prune_only (gaussians.py:408-417)
+ * as stream compaction.  Step 1 classifies every row in fp64 and builds the
+ * reference's output row order ([kept | clones | split children set 0 | set
+ * 1]); counts (device int32[4]) = {n_keep, n_clone, n_split, n_out}.  The
+ * caller reads the counts, draws the split samples exactly as the reference
+ * does (rng.standard_normal((n_split, 3)) twice -> float64 [2, n_split, 3]) and
+ * runs step 2, which writes the new cloud (out->K >= n_out rows), the grad
+ * stats (zeroed for densify, compacted for prune_only) and any per-row extra
+ * arrays (Adam moments: copied for kept rows, zero for new rows,
+ * gaussians.py:336-346).  capacity bounds n_out (CAPACITY status if above). */
+size_t fs4d_density_workspace_bytes(int64_t K, int64_t capacity);
+int fs4d_density_classify(const Fs4dCloud* cloud, const double* accum, const double* count,
+                          const Fs4dDensityConfig* cfg, int32_t prune_only, int64_t capacity, int32_t* counts,
+                          void* workspace, size_t workspace_bytes, int32_t* status, void* stream);
+int fs4d_density_apply(const Fs4dCloud* cloud, const double* split_normals, const Fs4dDensityConfig* cfg,
+                       int64_t capacity, int32_t n_keep, int32_t n_clone, int32_t n_split, Fs4dCloud* out,
+                       const double* stats_accum_in, const double* stats_count_in, double* stats_accum_out,
+                       double* stats_count_out, int32_t stats_reset, int32_t n_extra,
+                       const float* const* extra_in /* host array of device pointers */,
+                       float* const* extra_out, const int32_t* extra_width /* host */,
+                       void* workspace, size_t workspace_bytes, int32_t* status, void* stream);
+
+/* reset_opacity (gaussians.py:420-425): logit(min(sigmoid(x), cap)) in place. */
+int fs4d_reset_opacity(float* opacity_logits, int64_t K, double cap, void* stream);
+
 /* ---- rasterizer ---- */
 size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info);
 

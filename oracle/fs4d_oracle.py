@@ -853,3 +853,48 @@ def photometric(color, image, mask, depth, depth_target, alpha, lambda_rgb=1.0, 
     dterm = float(np.abs(dd)[dmask].sum() / n_d) if n_d else 0.0
     dD = lambda_depth * np.sign(dd) * dmask / n_d if n_d else np.zeros_like(dd)
     return rgb, dterm, dC, dD
+
+
+def density_control(cloud, accum, count, grad_threshold, percent_dense, prune_opacity, split_factor, extent,
+                    normals=None, prune_only=False, extras=()):
+    """gaussians.py:349-417 restated: returns (new arrays dict, new accum, new
+    count, new extras, counts dict).  normals: [2, n_split, 3] samples (the
+    reference draws rng.standard_normal((n_split, 3)) twice)."""
+    fields = ["positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features"]
+    if getattr(cloud, "sh_rest", None) is not None:
+        fields.append("sh_rest")
+    arrs = {f: np.asarray(getattr(cloud, f), dtype=np.float64) for f in fields}
+    prune = sigmoid(arrs["opacity_logits"]) < prune_opacity
+    k = len(prune)
+    if prune_only:
+        keep = ~prune
+        out = {f: a[keep] for f, a in arrs.items()}
+        return out, accum[keep], count[keep], [e[keep] for e in extras], {"keep": int(keep.sum())}
+    avg = accum / np.maximum(count, 1.0)
+    high = avg >= grad_threshold
+    small = np.exp(arrs["log_scales"]).max(axis=1) <= percent_dense * extent
+    clone = high & small & ~prune
+    split = high & ~small & ~prune
+    keep = ~(prune | (high & ~small))
+    ci, si = np.nonzero(clone)[0], np.nonzero(split)[0]
+    parts = {f: [a[keep], a[ci]] for f, a in arrs.items()}
+    if si.size:
+        q = arrs["rotations"][si]
+        q = q / np.linalg.norm(q, axis=1, keepdims=True)
+        R = rotation_from_unit_quats(q)
+        s = np.exp(arrs["log_scales"][si])
+        for j in range(2):
+            off = np.einsum("kij,kj->ki", R, normals[j] * s)
+            for f, a in arrs.items():
+                rows = a[si].copy()
+                if f == "positions":
+                    rows = rows + off
+                elif f == "log_scales":
+                    rows = rows - np.log(split_factor)
+                parts[f].append(rows)
+    out = {f: np.concatenate(p, axis=0) for f, p in parts.items()}
+    n_new = len(out["positions"]) - int(keep.sum())
+    new_extras = [np.concatenate([e[keep], np.zeros((n_new,) + e.shape[1:])]) for e in extras]
+    n = len(out["positions"])
+    return out, np.zeros(n), np.zeros(n), new_extras, {"keep": int(keep.sum()), "clone": int(ci.size),
+                                                       "split": int(si.size), "pruned": int(prune.sum())}

@@ -106,6 +106,12 @@ class AdamSegment(ctypes.Structure):
 
 _V, _I32, _I64, _D, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
 
+class DensityConfig(ctypes.Structure):
+    _fields_ = [("grad_threshold", ctypes.c_double), ("percent_dense", ctypes.c_double),
+                ("prune_opacity", ctypes.c_double), ("split_factor", ctypes.c_double),
+                ("extent", ctypes.c_double)]
+
+
 # symbol -> (restype, argtypes); every entry point declared in include/fs4d.h
 SIGNATURES = {
     "fs4d_abi_version": (ctypes.c_int, []),
@@ -150,6 +156,15 @@ SIGNATURES = {
                                                      _I32, _V, _SZ, _V]),
     "fs4d_decoder_feature_loss": (ctypes.c_int, [_V, _I32, _I32, _I32, _V, _V, _I32, _V, _I32, _I32, _D, _V, _V,
                                                  _V, _I32, _V, _V, _SZ, _V]),
+    "fs4d_grad_stats_add": (ctypes.c_int, [_V, _V, _V, _V, _I64, _V, _V]),
+    "fs4d_density_workspace_bytes": (_SZ, [_I64, _I64]),
+    "fs4d_density_classify": (ctypes.c_int, [ctypes.POINTER(Cloud), _V, _V, ctypes.POINTER(DensityConfig), _I32,
+                                             _I64, _V, _V, _SZ, _V, _V]),
+    "fs4d_density_apply": (ctypes.c_int, [ctypes.POINTER(Cloud), _V, ctypes.POINTER(DensityConfig), _I64, _I32,
+                                          _I32, _I32, ctypes.POINTER(Cloud), _V, _V, _V, _V, _I32, _I32,
+                                          ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                          ctypes.POINTER(ctypes.c_int32), _V, _SZ, _V, _V]),
+    "fs4d_reset_opacity": (ctypes.c_int, [_V, _I64, _D, _V]),
     "fs4d_render_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(RecordInfo)]),
     "fs4d_render_fwd": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(Camera),
                                        ctypes.POINTER(RasterCfg), ctypes.POINTER(RecordInfo),

@@ -93,6 +93,15 @@ int decode_features_backward(const float*, const float*, const float*, int, int,
 int decoder_feature_loss(const float*, int, int, int, const float*, const float*, int, const float*, int, int, double,
                          float*, float*, float*, int, double*, void*, size_t, cudaStream_t);
 
+size_t density_workspace_bytes(int64_t, int64_t);
+int stats_add(double*, double*, const int32_t*, const float*, int64_t, const int32_t*, cudaStream_t);
+int density_classify(const Fs4dCloud&, const double*, const double*, const Fs4dDensityConfig&, int, int64_t,
+                     int32_t*, void*, size_t, int32_t*, cudaStream_t);
+int density_apply(const Fs4dCloud&, const double*, const Fs4dDensityConfig&, int64_t, int32_t, int32_t, int32_t,
+                  Fs4dCloud&, const double*, const double*, double*, double*, int, int, const float* const*,
+                  float* const*, const int32_t*, void*, size_t, int32_t*, cudaStream_t);
+int reset_opacity(float*, int64_t, double, cudaStream_t);
+
 static int check_cloud(const Fs4dCloud* c, bool need_colors) {
   if (!c) return fail(FS4D_ERR_CONFIG, "null cloud");
   if (c->K < 0 || c->K > 0x7FFFFFFF) return fail(FS4D_ERR_CONFIG, "cloud size out of range");
@@ -347,6 +356,60 @@ int fs4d_decoder_feature_loss(const float* rendered, int32_t hi, int32_t wi, int
     return fail(FS4D_ERR_CONFIG, "null decoder loss argument");
   return decoder_feature_loss(rendered, hi, wi, N, weight, bias, Ct, teacher, ho, wo, lambda, d_rendered, d_weight,
                               d_bias, accumulate, loss, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int fs4d_grad_stats_add(double* accum, double* count, const int32_t* indices, const float* norms, int64_t n,
+                        const int32_t* n_dev, void* stream) {
+  if (n < 0 || (n > 0 && (!accum || !count || !indices || !norms))) return fail(FS4D_ERR_CONFIG, "bad stats arguments");
+  return stats_add(accum, count, indices, norms, n, n_dev, (cudaStream_t)stream);
+}
+
+size_t fs4d_density_workspace_bytes(int64_t K, int64_t capacity) {
+  if (K < 0 || capacity < 0) return 0;
+  return density_workspace_bytes(K, capacity);
+}
+
+static int check_density_cfg(const Fs4dDensityConfig* cfg) {
+  if (!cfg) return fail(FS4D_ERR_CONFIG, "null density config");
+  if (!(cfg->split_factor > 0.0) || !(cfg->extent >= 0.0)) return fail(FS4D_ERR_CONFIG, "bad density config");
+  return FS4D_OK;
+}
+
+int fs4d_density_classify(const Fs4dCloud* cloud, const double* accum, const double* count,
+                          const Fs4dDensityConfig* cfg, int32_t prune_only, int64_t capacity, int32_t* counts,
+                          void* workspace, size_t workspace_bytes, int32_t* status, void* stream) {
+  if (int rc = check_cloud(cloud, true)) return rc;
+  if (int rc = check_density_cfg(cfg)) return rc;
+  if (cloud->K > 0 && (!accum || !count) && !prune_only) return fail(FS4D_ERR_CONFIG, "grad stats missing");
+  if (capacity > 0x7FFFFFFFll) return fail(FS4D_ERR_CONFIG, "density capacity above 2^31");
+  if (!status) return fail(FS4D_ERR_CONFIG, "null status block");
+  return density_classify(*cloud, accum, count, *cfg, prune_only, capacity, counts, workspace, workspace_bytes,
+                          status, (cudaStream_t)stream);
+}
+
+int fs4d_density_apply(const Fs4dCloud* cloud, const double* split_normals, const Fs4dDensityConfig* cfg,
+                       int64_t capacity, int32_t n_keep, int32_t n_clone, int32_t n_split, Fs4dCloud* out,
+                       const double* stats_accum_in, const double* stats_count_in, double* stats_accum_out,
+                       double* stats_count_out, int32_t stats_reset, int32_t n_extra, const float* const* extra_in,
+                       float* const* extra_out, const int32_t* extra_width, void* workspace, size_t workspace_bytes,
+                       int32_t* status, void* stream) {
+  if (int rc = check_cloud(cloud, true)) return rc;
+  if (int rc = check_cloud(out, true)) return rc;
+  if (int rc = check_density_cfg(cfg)) return rc;
+  if (out->D != cloud->D || out->sh_degree != cloud->sh_degree) return fail(FS4D_ERR_CONFIG, "output cloud shape");
+  if (n_keep < 0 || n_clone < 0 || n_split < 0) return fail(FS4D_ERR_CONFIG, "negative density counts");
+  if (stats_accum_out && (!stats_count_out || (!stats_reset && (!stats_accum_in || !stats_count_in))))
+    return fail(FS4D_ERR_CONFIG, "grad stats arrays missing");
+  if (n_extra > 0 && (!extra_in || !extra_out || !extra_width)) return fail(FS4D_ERR_CONFIG, "extra arrays missing");
+  return density_apply(*cloud, split_normals, *cfg, capacity, n_keep, n_clone, n_split, *out, stats_accum_in,
+                       stats_count_in, stats_accum_out, stats_count_out, stats_reset, n_extra, extra_in, extra_out,
+                       extra_width, workspace, workspace_bytes, status, (cudaStream_t)stream);
+}
+
+int fs4d_reset_opacity(float* opacity_logits, int64_t K, double cap, void* stream) {
+  if (!(cap > 0.0 && cap < 1.0)) return fail(FS4D_ERR_CONFIG, "opacity cap must lie in (0, 1)");
+  if (K < 0 || (K > 0 && !opacity_logits)) return fail(FS4D_ERR_CONFIG, "bad reset_opacity arguments");
+  return reset_opacity(opacity_logits, K, cap, (cudaStream_t)stream);
 }
 
 size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info) {

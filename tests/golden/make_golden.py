@@ -246,12 +246,67 @@ def train_ops_case(ref, seed=21):
     print("train_ops")
 
 
+def density_case(ref, seed=31):
+    """densify_and_prune (clone + split + prune, with Adam states), then
+    prune_only and reset_opacity, from the reference itself.  The split
+    samples are recorded by replaying the same seeded generator."""
+    G, Nm = ref["gaussians"], ref["numerics"]
+    rng = np.random.default_rng(seed)
+    k, nf = 400, 5
+    arrs = cloud_arrays(rng, k, nf, (0.001, 0.9), (2.2, 3.8), ls_range=(0.002, 0.2))
+    cloud = G.GaussianCloud(**{k_: v.copy() for k_, v in arrs.items()})
+    stats = G.ViewspaceGradStats.zeros(k)
+    idx = rng.integers(0, k, size=1500)
+    norms = f32(rng.exponential(3e-4, size=1500))
+    for i0 in range(0, 1500, 300):  # renders: distinct indices per call
+        ii, pos = np.unique(idx[i0:i0 + 300], return_index=True)
+        stats.add(ii, norms[i0:i0 + 300][pos])
+    data = {f"cloud_{k_}": v for k_, v in arrs.items()}
+    data.update(stats_accum=stats.accum.copy(), stats_count=stats.count.copy())
+    adam = {}
+    for name, arr in cloud.param_arrays().items():
+        st = Nm.AdamState.for_param(arr)
+        st.m = f32(rng.normal(size=arr.shape))
+        st.v = f32(rng.uniform(size=arr.shape))
+        adam[name] = st
+        data[f"adam_{name}_m"], data[f"adam_{name}_v"] = st.m, st.v
+    cfg = G.DensityControlConfig(grad_threshold=2e-4, percent_dense=0.05, prune_opacity=0.02, split_factor=1.6)
+    extent = 1.3
+    seed2 = 77
+    split_rng = np.random.default_rng(seed2)
+    rep = G.densify_and_prune(cloud, stats, 5, cfg, extent, split_rng, adam_states=adam)
+    data.update(cfg=np.array([cfg.grad_threshold, cfg.percent_dense, cfg.prune_opacity, cfg.split_factor, extent]),
+                split_seed=seed2, report=np.array([rep["cloned"], rep["split"], rep["pruned"], rep["count"]]))
+    for name, arr in cloud.param_arrays().items():
+        data[f"out_{name}"] = arr
+        data[f"out_adam_{name}_m"], data[f"out_adam_{name}_v"] = adam[name].m, adam[name].v
+    data.update(out_accum=stats.accum, out_count=stats.count)
+    # prune_only on the densified cloud with fresh stats, then reset_opacity
+    stats2 = G.ViewspaceGradStats(accum=f32(rng.uniform(size=len(cloud))), count=np.floor(rng.uniform(0, 5, len(cloud))))
+    data.update(po_accum=stats2.accum.copy(), po_count=stats2.count.copy())
+    cloud.opacity_logits = f32(cloud.opacity_logits)
+    data["po_in_opacity"] = cloud.opacity_logits.copy()
+    n_pruned = G.prune_only(cloud, stats2, cfg)
+    data.update(po_pruned=n_pruned, po_out_accum=stats2.accum, po_out_count=stats2.count,
+                po_out_positions=cloud.positions)
+    cloud.opacity_logits = f32(cloud.opacity_logits)
+    data["ro_in"] = cloud.opacity_logits.copy()
+    G.reset_opacity(cloud, 0.01)
+    data["ro_out"] = cloud.opacity_logits
+    np.savez_compressed(os.path.join(OUT, "density.npz"), **data)
+    print("density", rep)
+
+
 def main():
     ref = load_reference()
     if len(sys.argv) > 1 and sys.argv[1] == "train_ops":
         train_ops_case(ref)
         return
+    if len(sys.argv) > 1 and sys.argv[1] == "density":
+        density_case(ref)
+        return
     train_ops_case(ref)
+    density_case(ref)
     # the reference's own tiled-vs-naive scenes (test_rasterizer.py:168-183 sizes)
     render_case(ref, "s0", 0, 50, 32, 32, 4, 1.1 * 32, (0.1, 0.2, 0.3))
     render_case(ref, "s1", 1, 200, 64, 64, 16, 1.1 * 64, (0.1, 0.2, 0.3))
