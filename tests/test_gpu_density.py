@@ -77,7 +77,8 @@ def test_device_density_full_size_matches_oracle():
     rng = np.random.default_rng(9)
     k = 200_000
     a = random_cloud_arrays(rng, k, 16, op_range=(0.001, 0.9), ls_range=(0.002, 0.2), sh_degree=3)
-    cloud = DeviceCloud.from_cloud(type("C", (), a)())
+    import paper_2503_06161_b200 as fs
+    cloud = DeviceCloud.from_cloud(fs.GaussianCloud(**a))
     acc = rng.exponential(3e-4, size=k)
     cnt = np.floor(rng.uniform(0, 4, size=k))
     stats = dn.ViewspaceGradStats(torch.tensor(acc, device="cuda"), torch.tensor(cnt, device="cuda"))
@@ -86,7 +87,7 @@ def test_device_density_full_size_matches_oracle():
     out, st, outs, rep = dn.DeviceDensity().run(cloud, stats, cfg, 1.3, np.random.default_rng(5), False,
                                                  [torch.tensor(e, device="cuda") for e in ex])
     zrng = np.random.default_rng(5)
-    ref_cloud = type("C", (), dict(a))()
+    ref_cloud = fs.GaussianCloud(**a)
     ro, racc, rcnt, rex, rc = O.density_control(ref_cloud, acc, cnt, 2e-4, 0.05, 0.02, 1.6, 1.3,
                                                 np.stack([zrng.standard_normal((rep["split"], 3)) for _ in range(2)]),
                                                 extras=[e.astype(np.float64) for e in ex])
