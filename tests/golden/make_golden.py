@@ -297,8 +297,43 @@ def density_case(ref, seed=31):
     print("density", rep)
 
 
+def checkpoint_case(ref, seed=41):
+    """An FS4C container written by the reference's own entry writer
+    (training.py:599-628, the code save_checkpoint runs), plus its entries."""
+    import io
+    import struct
+    T = ref["training"]
+    rng = np.random.default_rng(seed)
+    entries = {
+        "meta.config": b"[train]\nseed = 3\n",
+        "meta.iteration": 7,
+        "meta.extent": 1.25,
+        "meta.aabb": rng.normal(size=(2, 3)),
+        "stats.accum": rng.uniform(size=11),
+        "cloud.positions": rng.normal(size=(11, 3)),
+        "cloud.opacity_logits": rng.normal(size=11),
+        "grid.l0.p2": rng.normal(size=(4, 3, 2)),
+        "net.trunk.0.weight": rng.normal(size=(5, 4)),
+        "adam.positions.step": 3,
+        "labels": np.arange(6, dtype=np.int64).reshape(2, 3),
+    }
+    buf = io.BytesIO()
+    buf.write(T.CHECKPOINT_MAGIC)
+    buf.write(struct.pack("<IQ", T.CHECKPOINT_VERSION, len(entries)))
+    for name in sorted(entries):
+        T._write_entry(buf, name, entries[name])
+    with open(os.path.join(OUT, "checkpoint.fs4c"), "wb") as fh:
+        fh.write(buf.getvalue())
+    back = T.load_entries(os.path.join(OUT, "checkpoint.fs4c"))
+    assert sorted(back) == sorted(entries)
+    print("checkpoint", len(buf.getvalue()), "bytes")
+
+
 def main():
     ref = load_reference()
+    if len(sys.argv) > 1 and sys.argv[1] == "checkpoint":
+        checkpoint_case(ref)
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "train_ops":
         train_ops_case(ref)
         return
@@ -307,6 +342,7 @@ def main():
         return
     train_ops_case(ref)
     density_case(ref)
+    checkpoint_case(ref)
     # the reference's own tiled-vs-naive scenes (test_rasterizer.py:168-183 sizes)
     render_case(ref, "s0", 0, 50, 32, 32, 4, 1.1 * 32, (0.1, 0.2, 0.3))
     render_case(ref, "s1", 1, 200, 64, 64, 16, 1.1 * 64, (0.1, 0.2, 0.3))

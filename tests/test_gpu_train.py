@@ -235,3 +235,52 @@ def test_fine_stage_step_decoder_tv_adam_matches_oracle():
         got = p1[off:off + n]
         assert np.abs(got - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max()), name
     assert step.iteration == 1
+
+
+def test_checkpoint_round_trip_of_device_training_state(tmp_path):
+    """save_train_state -> load_train_state into a fresh TrainStep restores
+    parameters, Adam moments and step counts exactly; the next step of both
+    agrees up to the backward's atomic-order noise (training.py:569-706
+    semantics on device buffers)."""
+    import torch
+    import paper_2503_06161_b200 as fs
+    from paper_2503_06161_b200 import checkpoint as ck
+    from paper_2503_06161_b200 import device as dv
+    from paper_2503_06161_b200.numerics import LrSchedule
+    from paper_2503_06161_b200.train import TrainStep
+
+    rng = np.random.default_rng(3)
+    k, h, w, d = 800, 32, 48, 8
+    a = random_cloud_arrays(rng, k, d, depth_range=(2.0, 4.0), xy=1.0)
+    cloud = fs.GaussianCloud(**a)
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(8, 8, 8, 4), out_dim=64),
+                             fs.scene_aabb(cloud), rng, init="uniform")
+    net = fs.DeformationNet(64, fs.DeformationConfig(width=64, depth=1, feature_dim=d), rng, init="xavier",
+                            head_init="xavier")
+    K = pinhole(h, w, 40.0)
+    sched = {n: LrSchedule.constant(1e-3) for n in ("positions", "rotations", "log_scales", "opacity_logits",
+                                                     "colors_raw", "features", "grid", "net")}
+
+    def make():
+        s = TrainStep(dv.DeviceCloud.from_cloud(cloud), dv.DeviceField.from_field(field), dv.DeviceNet.from_net(net),
+                      h, w, fs.RasterConfig())
+        return s.attach_optimizer(sched)
+
+    batch = [(0.4, K, np.eye(4), torch.rand(h, w, 3, device="cuda"), torch.randn(h, w, d, device="cuda"))]
+    s1 = make()
+    for _ in range(2):
+        s1.run(batch, check=True)
+    p = str(tmp_path / "state.fs4c")
+    ck.save_train_state(s1, p, meta={"meta.extent": 1.5})
+    e = ck.load_entries(p)
+    assert e["meta.iteration"] == 2 and e["adam.positions.step"] == 2 and e["cloud.positions"].dtype == np.float64
+    s2 = make()
+    ck.load_train_state(s2, p)
+    assert torch.equal(s1.params.buffer, s2.params.buffer)
+    assert torch.equal(s1.optimizer.m, s2.optimizer.m) and torch.equal(s1.optimizer.v, s2.optimizer.v)
+    assert torch.equal(s1.optimizer.steps, s2.optimizer.steps) and s2.iteration == 2
+    s1.run(batch, check=True)
+    s2.run(batch, check=True)
+    torch.cuda.synchronize()
+    diff = (s1.params.buffer - s2.params.buffer).abs().max().item()
+    assert diff < 1e-6, diff  # atomics in the backward: last-bit differences only
