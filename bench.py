@@ -80,11 +80,21 @@ FRAME_BYTES = K_GAUSS * 4 * (11 + D + 3 * (SH_DEG + 1) ** 2) + 4 * plane_floats(
 MLP_FLOPS = 2 * 21344 * K_GAUSS
 
 
+# stage (library profiler id) -> the single kernel it times (traffic lookup)
+STAGE_KERNEL = {"deform_gather": "k_hexplane_latent_c32t", "deform_mlp": "k_mlp_tc_ws", "preprocess": "k_preprocess",
+                "blend": "k_blend"}
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r1_traffic.json")
+
+
 def stage_bytes(stage, n_visible, n_pairs):
     """Algorithmic HBM bytes of one launch of each stage (inputs read once + outputs written once)."""
     k = K_GAUSS
     if stage == "deform_fwd":   # cloud geometry+features in, snapshot out, planes + MLP once
         return k * 4 * (11 + D) * 2 + 4 * plane_floats() + 4 * MLP_PARAMS
+    if stage == "deform_gather":  # positions in, planes once, latent [K, 64] out
+        return k * 4 * 3 + 4 * plane_floats() + k * 4 * 64
+    if stage == "deform_mlp":   # latent + cloud geometry/features in, snapshot out, MLP once
+        return k * 4 * 64 + k * 4 * (11 + D) * 2 + 4 * MLP_PARAMS
     if stage == "preprocess":   # snapshot (incl. SH) in, 96 B projected record out
         return k * 4 * (11 + D + 3 * (SH_DEG + 1) ** 2) + n_visible * 96
     if stage == "blend":        # projected records + features of the visible set, image out
@@ -374,8 +384,30 @@ def train_bench(args, rank, world, local):
 
     torch.cuda.set_device(local)
     cloud_np, field_np, net_np, Kmat = make_scene(0)
-    step = TrainStep(dv.DeviceCloud.from_cloud(cloud_np), dv.DeviceField.from_field(field_np),
-                     dv.DeviceNet.from_net(net_np), H, W, fs.RasterConfig(), world=world)
+    fine = args.workload == "fine"
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(rank)
+    if fine:
+        # the reference's fine-stage iteration (training.py:489-535) with its
+        # TrainConfig defaults (training.py:53-83): masked RGB L1 + depth L1,
+        # pointwise decoder against a 16-channel teacher at 1/4 resolution,
+        # HexPlane TV, then Adam on every parameter array
+        from paper_2503_06161_b200.numerics import LrSchedule
+        ct = 16
+        dec_w = (torch.rand(ct, D, device="cuda", generator=gen) * 2 - 1) * float(np.sqrt(6.0 / D))
+        dec = (dec_w, torch.zeros(ct, device="cuda"))
+        step = TrainStep(dv.DeviceCloud.from_cloud(cloud_np), dv.DeviceField.from_field(field_np),
+                         dv.DeviceNet.from_net(net_np), H, W, fs.RasterConfig(), world=world, loss_mode="decoder",
+                         lambda_rgb=1.0, lambda_depth=0.01, lambda_feat=1.0, lambda_tv=0.03, decoder=dec)
+        step.attach_optimizer({
+            "positions": LrSchedule(1.6e-4, 1.6e-6, 7000), "rotations": LrSchedule.constant(1e-3),
+            "log_scales": LrSchedule.constant(5e-3), "opacity_logits": LrSchedule.constant(5e-2),
+            "colors_raw": LrSchedule.constant(2.5e-3), "features": LrSchedule.constant(2.5e-3),
+            "grid": LrSchedule(3.2e-3, 3.2e-6, 7000), "net": LrSchedule(1.6e-4, 1.6e-7, 7000, 0.01, 0),
+            "decoder": LrSchedule.constant(1e-3)})
+    else:
+        step = TrainStep(dv.DeviceCloud.from_cloud(cloud_np), dv.DeviceField.from_field(field_np),
+                         dv.DeviceNet.from_net(net_np), H, W, fs.RasterConfig(), world=world)
     rng = np.random.default_rng(100 + rank)
     pairs = 8
 
@@ -389,11 +421,16 @@ def train_bench(args, rank, world, local):
         T[:3, 3] = rng.uniform(-0.1, 0.1, 3)
         return T
 
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(rank)
-    batch = [(float(rng.uniform()), Kmat, rigid(),
-              torch.rand(H, W, 3, device="cuda", generator=gen),
-              torch.randn(H, W, D, device="cuda", generator=gen)) for _ in range(pairs)]
+    if fine:
+        batch = [(float(rng.uniform()), Kmat, rigid(),
+                  torch.rand(H, W, 3, device="cuda", generator=gen),
+                  torch.randn(H // 4, W // 4, 16, device="cuda", generator=gen),
+                  (torch.rand(H, W, device="cuda", generator=gen) > 0.05).to(torch.uint8),
+                  torch.rand(H, W, device="cuda", generator=gen) * 3 + 3) for _ in range(pairs)]
+    else:
+        batch = [(float(rng.uniform()), Kmat, rigid(),
+                  torch.rand(H, W, 3, device="cuda", generator=gen),
+                  torch.randn(H, W, D, device="cuda", generator=gen)) for _ in range(pairs)]
     step.run(batch, check=True)  # sizes the pair buffer
     for _ in range(args.warmup):
         step.run(batch)
@@ -432,7 +469,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", default="render", choices=["render", "train"])
+    ap.add_argument("--workload", default="render", choices=["render", "train", "fine"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -458,11 +495,15 @@ def main():
         print(json.dumps(line))
         return
 
-    if args.workload == "train":
+    if args.workload in ("train", "fine"):
         r = train_bench(args, rank, world, local)
         if rank == 0:
             line = dict(base)
-            line.update({"metric": "configs[4] training steps/s (8 (view,t) pairs per GPU, fwd+bwd+allreduce)",
+            metric = "configs[4] training steps/s (8 (view,t) pairs per GPU, fwd+bwd+allreduce)"
+            if args.workload == "fine":
+                metric = ("fine-stage training steps/s (configs[4] scene, 8 pairs/GPU, masked RGB+depth L1, decoder "
+                          "feature loss, TV, all-reduce, Adam)")
+            line.update({"metric": metric,
                          "unit": "steps/s", "value": world * args.steps / (r["ms"] / 1000.0) / world,
                          "ms_per_step": r["ms"] / args.steps,
                          "frames_per_s": world * r["pairs"] * args.steps / (r["ms"] / 1000.0),
@@ -470,6 +511,9 @@ def main():
                          "allreduce_floats": r["grad_floats"], "loss": r["loss"]})
             line["config"] = dict(base["config"], workload="configs[4]: configs[1] scene, 8 (view,t) pairs/GPU, "
                                                            "L1 RGB + L1 feature", parallelism=f"dp{world}")
+            if args.workload == "fine":
+                line["config"]["workload"] = ("reference fine-stage iteration (training.py:489-535) on the configs[1] "
+                                              "scene: 8 pairs/GPU, teacher 16ch at 160x128, TrainConfig defaults")
             print(json.dumps(line))
         return
     r = gpu_bench(args, rank, world, local)
@@ -479,23 +523,39 @@ def main():
     prof = r["prof"]
     stage_ms = {s: (ms / c if c else 0.0) for s, (ms, c) in prof.items()}
     fwd = {s: v for s, v in stage_ms.items() if s in ("deform_fwd", "preprocess", "depth_sort", "binning", "blend")}
-    top = max(fwd, key=fwd.get)
     frame_ms = sum(fwd.values())
+    # dominant single kernel (binning is a chain of small kernels, excluded)
+    single = {s: stage_ms[s] for s in STAGE_KERNEL if stage_ms.get(s)}
+    top = max(single, key=single.get)
     top_bytes = stage_bytes(top, r["n_vis"], r["n_pairs"])
     achieved = top_bytes / (stage_ms[top] / 1000.0) / 1e9
+    traffic, traffic_src = None, None
+    try:
+        with open(TRAFFIC_JSON) as fh:
+            t = json.load(fh)[STAGE_KERNEL[top]]
+        traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+        traffic_src = f"{os.path.basename(TRAFFIC_JSON)}: ncu --set full of {t['kernel'].split('(')[0]} (one launch)"
+    except Exception:
+        pass
+    kernels = {s: {"ms": round(stage_ms[s], 4), "algorithmic_bytes": stage_bytes(s, r["n_vis"], r["n_pairs"]),
+                   "achieved_gbs": stage_bytes(s, r["n_vis"], r["n_pairs"]) / (stage_ms[s] / 1000.0) / 1e9}
+               for s in single}
     line = dict(base)
     line.update({
         "value": value, "ms_per_step": r["ms"] / r["steps"],
-        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": top_bytes,
+        "roofline": {"bound": "hbm", "kernel": STAGE_KERNEL[top], "stage": top, "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": top_bytes,
                      "share_of_step": stage_ms[top] / frame_ms if frame_ms else None},
+        "kernels": kernels,
         "roofline_frame": {"bytes_per_frame": FRAME_BYTES,
                            "achieved_gbs": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9,
                            "frac": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9 / hbm},
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items() if v},
-        "mlp": {"flops_per_frame": MLP_FLOPS,
-                "tflops": MLP_FLOPS / (stage_ms["deform_fwd"] / 1000.0) / 1e12 if stage_ms["deform_fwd"] else None},
+        "mlp": {"flops_per_frame": MLP_FLOPS, "kernel": "k_mlp_tc_ws (bf16x3 on tcgen05: 3x these flops issued)",
+                "tflops": MLP_FLOPS / (stage_ms["deform_mlp"] / 1000.0) / 1e12 if stage_ms.get("deform_mlp") else None,
+                "peak_bf16_tflops": tf, "frac_of_bf16_peak_issued": 3 * MLP_FLOPS / (stage_ms["deform_mlp"] / 1000.0)
+                / 1e12 / tf if stage_ms.get("deform_mlp") else None},
         "work": {"visible": r["n_vis"], "pairs": r["n_pairs"]},
         "clocks": r["clocks"],
         "e2e": {"value": frames / (r["e2e_ms"] / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": r["h2d"],

@@ -197,7 +197,9 @@ int fs4d_status_reset(int32_t* status, void* stream);
 #define FS4D_STAGE_BLEND_BWD 5    /* k_blend_bwd                          */
 #define FS4D_STAGE_PREPROCESS_BWD 6
 #define FS4D_STAGE_DEFORM_BWD 7
-#define FS4D_N_STAGES 8
+#define FS4D_STAGE_DEFORM_GATHER 8 /* HexPlane latent gather (inside DEFORM_FWD) */
+#define FS4D_STAGE_DEFORM_MLP 9    /* tcgen05 MLP + delta apply (inside DEFORM_FWD) */
+#define FS4D_N_STAGES 10
 int fs4d_profile_enable(int on);
 int fs4d_profile_collect(double* ms_total, int64_t* calls, int32_t n_stages);
 

@@ -1001,6 +1001,7 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   // occupancy.  It stays opt-in (FS4D_FUSED_GATHER=1).
   const bool fused = !cache && getenv("FS4D_FUSED_GATHER") && (!p.enable_grid || (p.C == 32 && p.levels == 2));
   const unsigned gblocks = (unsigned)ceil_div(K, kGatherWarps * 32);
+  StageTimer st_gather(fused ? -1 : FS4D_STAGE_DEFORM_GATHER, s);
   if (!fused) {
     if (p.rows_ok && !getenv("FS4D_NO_TIME_ROWS"))
       k_hexplane_latent_c32t<2><<<gblocks, kGatherWarps * 32, 0, s>>>(
@@ -1010,6 +1011,8 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
     else
       k_hexplane_latent<<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, cloud.positions, latent);
   }
+  st_gather.stop();
+  StageTimer st_mlp(FS4D_STAGE_DEFORM_MLP, s);
   TcArgs a;
   a.p = p;
   a.K = K;

@@ -472,7 +472,7 @@ class Renderer:
 
 
 STAGES = ("deform_fwd", "preprocess", "depth_sort", "binning", "blend", "blend_bwd",
-          "preprocess_bwd", "deform_bwd")
+          "preprocess_bwd", "deform_bwd", "deform_gather", "deform_mlp")
 
 
 def profile_enable(on=True):
