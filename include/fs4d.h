@@ -22,6 +22,20 @@
  *                     <- rasterizer.project / bin_tiles results (ProjectedGaussians,
  *                        per-tile lists) read back from a forward record.
  *
+ * and the callers either side of the path:
+ *   fs4d_l1_loss_grad / fs4d_photometric_loss_grad / fs4d_l1
+ *                     <- training._photometric_terms/_grads training.py:300-338,
+ *                        semantic.feature_loss(_backward) semantic.py:171-181
+ *   fs4d_adam_step    <- numerics.adam_step numerics.py:137-159 (per array,
+ *                        training.py:431-442), all arrays in one launch
+ *   fs4d_tv_loss_grad <- hexplane.tv_loss / tv_backward hexplane.py:190-222
+ *   fs4d_resize_bilinear(_backward) <- semantic.resize_bilinear(_backward) semantic.py:82-123
+ *   fs4d_decode_features(_backward) / fs4d_decoder_feature_loss
+ *                     <- semantic.decode_features_with_cache / _backward semantic.py:145-168
+ *   fs4d_grad_stats_add / fs4d_density_classify / fs4d_density_apply / fs4d_reset_opacity
+ *                     <- gaussians.ViewspaceGradStats.add, densify_and_prune,
+ *                        prune_only, reset_opacity gaussians.py:309-425
+ *
  * Conventions
  *  - All pointers are DEVICE pointers unless stated; all float data is fp32,
  *    row-major in the reference's logical layout ([K,3] positions, [K,4]
