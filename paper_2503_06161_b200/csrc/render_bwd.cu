@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
         if (kk < cnt && bstart + kk <= (int64_t)wlast) {
           const int4 pr = s_pr[kk];
           hit = pr.w >= wrow0 && pr.z <= wrow0 + 2 * PX - 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
+          if (hit) hit = strip_hits<2 * PX>(pr, s_xy[kk], s_co[kk], wrow0, tcol0, a.alpha_skip);
         }
         bits = __ballot_sync(0xffffffffu, hit);
       }

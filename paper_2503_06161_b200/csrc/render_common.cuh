@@ -39,6 +39,38 @@ enum { CNT_VISIBLE = 0, CNT_PAIRS64 = 2 /* u64 at words 2..3 */, CNT_PAIRS_CLAMP
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Conservative warp-level cull: can any pixel of the NR-row strip [r0, r0+NR) x
+// [c0, c0+15] pass the per-pixel tests (inside pix_rect, q <= 2 ln 255,
+// o exp(-q/2) >= alpha_skip)?  Row by row, q(dx) is a parabola with minimum
+// (c - b^2/a) dy^2 at dx* = -b dy / a, so the admissible columns are
+// mu_x + dx* +- sqrt((Q - q_min)/a) with Q = min(2 ln 255, 2 ln(o/skip)).
+// Q gets a 1e-3 relative and the column interval a 0.02 pixel margin, far
+// above the fp32 rounding of either side, so no Gaussian the exact per-pixel
+// test accepts is ever culled: the pixel decisions stay exactly k_blend's.
+template <int NR>
+__device__ __forceinline__ bool strip_hits(const int4& pr, const float2& mm, const float4& co, int r0, int c0,
+                                           float alpha_skip) {
+  if (co.w < alpha_skip) return false;
+  const float Q = fminf(kQSkip, 2.f * __logf(co.w / alpha_skip)) * 1.001f + 1e-3f;
+  const float inv_a = 1.f / co.x, schur = co.z - co.y * co.y * inv_a;
+  const float xlo = (float)max(c0, pr.x) - 0.02f, xhi = (float)min(c0 + kTile - 1, pr.y) + 0.02f;
+  bool hit = false;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int row = r0 + r;
+    if (row < pr.z || row > pr.w) continue;
+    const float dy = (float)row - mm.y;
+    const float qmin = schur * dy * dy;
+    if (qmin > Q) continue;
+    const float h = sqrtf((Q - qmin) * inv_a) + 0.02f;
+    const float xc = mm.x - co.y * dy * inv_a;
+    const float lo = fmaxf(xc - h, xlo), hi = fminf(xc + h, xhi);
+    hit |= ceilf(lo) <= floorf(hi);
+  }
+  return hit;
+}
+
+
 inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
   RenderLayout L;
   L.K = info.K;

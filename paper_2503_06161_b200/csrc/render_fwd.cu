@@ -274,36 +274,6 @@ extern "C" int fs4d_debug_blend_trace(unsigned long long* out) {
 }
 #endif
 
-// Conservative warp-level cull: can any pixel of the 2-row strip [r0, r0+1] x
-// [c0, c0+15] pass the per-pixel tests (inside pix_rect, q <= 2 ln 255,
-// o exp(-q/2) >= alpha_skip)?  Row by row, q(dx) is a parabola with minimum
-// (c - b^2/a) dy^2 at dx* = -b dy / a, so the admissible columns are
-// mu_x + dx* +- sqrt((Q - q_min)/a) with Q = min(2 ln 255, 2 ln(o/skip)).
-// Q gets a 1e-3 relative and the column interval a 0.02 pixel margin, far
-// above the fp32 rounding of either side, so no Gaussian the exact per-pixel
-// test accepts is ever culled: the pixel decisions stay exactly k_blend's.
-__device__ __forceinline__ bool strip_hits(const int4& pr, const float2& mm, const float4& co, int r0, int c0,
-                                           float alpha_skip) {
-  if (co.w < alpha_skip) return false;
-  const float Q = fminf(kQSkip, 2.f * __logf(co.w / alpha_skip)) * 1.001f + 1e-3f;
-  const float inv_a = 1.f / co.x, schur = co.z - co.y * co.y * inv_a;
-  const float xlo = (float)max(c0, pr.x) - 0.02f, xhi = (float)min(c0 + kTile - 1, pr.y) + 0.02f;
-  bool hit = false;
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int row = r0 + r;
-    if (row < pr.z || row > pr.w) continue;
-    const float dy = (float)row - mm.y;
-    const float qmin = schur * dy * dy;
-    if (qmin > Q) continue;
-    const float h = sqrtf((Q - qmin) * inv_a) + 0.02f;
-    const float xc = mm.x - co.y * dy * inv_a;
-    const float lo = fmaxf(xc - h, xlo), hi = fminf(xc + h, xhi);
-    hit |= ceilf(lo) <= floorf(hi);
-  }
-  return hit;
-}
-
 template <int DC, int SUB>
 __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
 #ifdef FS4D_BLEND_TRACE
@@ -385,7 +355,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
       if (kk < cnt) {
         const int4 pr = s_pr[kk];
         hit = pr.w >= wrow0 && pr.z <= wrow0 + 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
-        if (hit) hit = strip_hits(pr, s_xy[kk], s_co[kk], wrow0, tcol0, a.alpha_skip);
+        if (hit) hit = strip_hits<2>(pr, s_xy[kk], s_co[kk], wrow0, tcol0, a.alpha_skip);
       }
       const unsigned msk = __ballot_sync(0xffffffffu, hit);
       if (lane == 0) s_mask[wid][m] = msk;
