@@ -300,6 +300,8 @@ def gpu_bench(args, rank, world, local):
     cloud_np, field_np, net_np, Kmat = make_scene(0)
     cloud = dv.DeviceCloud.from_cloud(cloud_np)
     field = dv.DeviceField.from_field(field_np)
+    if os.environ.get("FS4D_LOCALITY", "0") == "1":
+        field = field.with_order(dv.locality_order(cloud.positions, field.aabb))
     net = dv.DeviceNet.from_net(net_np)
     cfg = fs.RasterConfig()
     pipe = dv.FramePipeline(cloud, field, net, H, W, cfg)

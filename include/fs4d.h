@@ -169,6 +169,13 @@ typedef struct Fs4dHexPlane {
   int32_t res[FS4D_MAX_LEVELS][6][2];
   float* planes[FS4D_MAX_LEVELS][6];
   double aabb[6];  /* lo xyz, hi xyz */
+  /* Optional order in which the plane gathers / scatters visit the K
+   * Gaussians (a permutation of [0, K), e.g. fs4d_locality_order), or NULL
+   * for index order.  Every Gaussian's latent is computed independently, so
+   * any permutation gives identical results (the backward's float atomics
+   * are unordered either way); a spatially coherent one turns most corner-
+   * row fetches into L1 hits. */
+  const int32_t* order;
 } Fs4dHexPlane;
 
 /* LinearLayer (numerics.py:17-41): y = act(x W^T + b), W [out,in]. */
@@ -216,6 +223,15 @@ int fs4d_status_reset(int32_t* status, void* stream);
 #define FS4D_N_STAGES 10
 int fs4d_profile_enable(int on);
 int fs4d_profile_collect(double* ms_total, int64_t* calls, int32_t n_stages);
+
+/* Spatially coherent visiting order of a cloud for Fs4dHexPlane.order:
+ * Gaussians sorted by the 30-bit Morton code of their position normalised
+ * by aabb (lo xyz, hi xyz) and clipped to it, ties by index (stable radix
+ * sort).  A model-load-time permutation: it never changes results, only
+ * cache locality, so it may be reused while positions drift. */
+size_t fs4d_locality_order_workspace_bytes(int64_t K);
+int fs4d_locality_order(const float* positions, int64_t K, const double* aabb, int32_t* order,
+                        void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- deformation ---- */
 /* Bytes of device scratch the deform calls need (packed weights + per-CTA

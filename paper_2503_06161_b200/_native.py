@@ -83,7 +83,7 @@ class HexPlane(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("channels", ctypes.c_int32),
                 ("res", ((ctypes.c_int32 * 2) * 6) * MAX_LEVELS),
                 ("planes", (ctypes.c_void_p * 6) * MAX_LEVELS),
-                ("aabb", ctypes.c_double * 6)]
+                ("aabb", ctypes.c_double * 6), ("order", ctypes.c_void_p)]
 
 
 class Linear(ctypes.Structure):
@@ -165,6 +165,8 @@ SIGNATURES = {
                                           ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
                                           ctypes.POINTER(ctypes.c_int32), _V, _SZ, _V, _V]),
     "fs4d_reset_opacity": (ctypes.c_int, [_V, _I64, _D, _V]),
+    "fs4d_locality_order_workspace_bytes": (_SZ, [_I64]),
+    "fs4d_locality_order": (ctypes.c_int, [_V, _I64, ctypes.POINTER(ctypes.c_double), _V, _V, _SZ, _V]),
     "fs4d_render_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(RecordInfo)]),
     "fs4d_render_fwd": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(Camera),
                                        ctypes.POINTER(RasterCfg), ctypes.POINTER(RecordInfo),

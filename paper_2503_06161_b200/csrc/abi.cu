@@ -102,6 +102,9 @@ int density_apply(const Fs4dCloud&, const double*, const Fs4dDensityConfig&, int
                   float* const*, const int32_t*, void*, size_t, int32_t*, cudaStream_t);
 int reset_opacity(float*, int64_t, double, cudaStream_t);
 
+size_t locality_order_workspace_bytes(int64_t);
+int locality_order(const float*, int64_t, const double*, int32_t*, void*, size_t, cudaStream_t);
+
 static int check_cloud(const Fs4dCloud* c, bool need_colors) {
   if (!c) return fail(FS4D_ERR_CONFIG, "null cloud");
   if (c->K < 0 || c->K > 0x7FFFFFFF) return fail(FS4D_ERR_CONFIG, "cloud size out of range");
@@ -410,6 +413,15 @@ int fs4d_reset_opacity(float* opacity_logits, int64_t K, double cap, void* strea
   if (!(cap > 0.0 && cap < 1.0)) return fail(FS4D_ERR_CONFIG, "opacity cap must lie in (0, 1)");
   if (K < 0 || (K > 0 && !opacity_logits)) return fail(FS4D_ERR_CONFIG, "bad reset_opacity arguments");
   return reset_opacity(opacity_logits, K, cap, (cudaStream_t)stream);
+}
+
+size_t fs4d_locality_order_workspace_bytes(int64_t K) { return K < 0 ? 0 : locality_order_workspace_bytes(K); }
+
+int fs4d_locality_order(const float* positions, int64_t K, const double* aabb, int32_t* order, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  if (K < 0 || K > 0x7FFFFFFF || !aabb || (K > 0 && (!positions || !order)))
+    return fail(FS4D_ERR_CONFIG, "bad locality order arguments");
+  return locality_order(positions, K, aabb, order, workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t fs4d_render_workspace_bytes(const Fs4dRecordInfo* info) {

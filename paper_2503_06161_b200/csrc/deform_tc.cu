@@ -171,8 +171,10 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPl
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t g0 = ((int64_t)blockIdx.x * kGatherWarps + warp) * 32;
   if (g0 >= K) return;
+  // slot g0 + lane visits Gaussian kg (the optional locality order)
+  const int64_t kg = g0 + lane < K ? (p.order ? (int64_t)p.order[g0 + lane] : g0 + lane) : K;
   {
-    const int64_t k = g0 + lane;
+    const int64_t k = kg;
     double c[3] = {0.0, 0.0, 0.0};
     if (k < K) {
 #pragma unroll
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPl
   const int sub = lane >> 3, ch = (lane & 7) * 4;
   for (int j0 = 0; j0 < 32; j0 += 4) {
     const int j = j0 + sub;
-    const int64_t k = g0 + j;
+    const int64_t k = __shfl_sync(0xffffffffu, kg, j);
 #pragma unroll
     for (int l = 0; l < LEVELS; ++l) {
       float4 prod = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -841,6 +843,7 @@ static int build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, T
     p.lo[a] = f.aabb[a];
     p.span[a] = f.aabb[3 + a] - f.aabb[a];
   }
+  p.order = f.order;
   p.t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
   int off = 0, nop = 0, nb = 0;
   auto operand = [&](int N, int KT) {

@@ -24,6 +24,7 @@ struct TcPlan {
   int levels, C, L;
   int res[FS4D_MAX_LEVELS][6][2];
   const float* planes[FS4D_MAX_LEVELS][6];
+  const int32_t* order;  // optional Gaussian visiting order (Fs4dHexPlane.order)
   double lo[3], span[3];
   double t;
   // packed blob offsets (bytes)

@@ -144,10 +144,11 @@ class StatusBlock:
 class DeviceField:
     """HexPlane planes [levels][6] of [Ra, Rb, C] fp32 plus the aabb."""
 
-    def __init__(self, planes, aabb, channels):
+    def __init__(self, planes, aabb, channels, order=None):
         self.planes = planes
         self.aabb = np.asarray(aabb, dtype=np.float64).reshape(2, 3)
         self.channels = int(channels)
+        self.order = order  # optional int32 [K] Gaussian visiting order (locality_order)
 
     @property
     def levels(self):
@@ -178,7 +179,12 @@ class DeviceField:
                 h.res[l][p][1] = plane.shape[1]
                 h.planes[l][p] = plane.data_ptr()
         h.aabb[:] = [float(v) for v in self.aabb.reshape(6)]
+        h.order = _p(self.order)
         return h
+
+    def with_order(self, order):
+        """Same planes, visited in `order` (results are identical)."""
+        return DeviceField(self.planes, self.aabb, self.channels, order)
 
 
 class DeviceNet:
@@ -245,6 +251,19 @@ class DeviceNet:
         for k in range(2):
             fill(s.feat[k], self.layers["net.feat"][k])
         return s
+
+
+def locality_order(positions, aabb, device="cuda"):
+    """fs4d_locality_order: int32 [K] Morton order of `positions` ([K,3] fp32
+    CUDA) inside `aabb` -- a model-load-time permutation for
+    DeviceField.order (never changes results, only cache locality)."""
+    lib = N.load()
+    k = int(positions.shape[0])
+    order = torch.empty(max(k, 1), dtype=torch.int32, device=device)
+    ws = torch.empty(max(int(lib.fs4d_locality_order_workspace_bytes(k)), 1), dtype=torch.uint8, device=device)
+    box = (ctypes.c_double * 6)(*[float(v) for v in np.asarray(aabb, dtype=np.float64).reshape(6)])
+    N.check(lib.fs4d_locality_order(_p(positions), k, box, _p(order), _p(ws), ws.numel(), _stream()))
+    return order[:k]
 
 
 class DeformCache:
