@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
   uint8_t* W = smem;
   uint8_t* R = smem + wbytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool issuer = tid == kBwdEpiThreads;
+  // the MMA warp runs the issue code warp-wide (uniform descriptors, one
+  // elected lane issues); TMA bulk copies stay single-lane
+  const bool issuer = warp == kBwdEpiThreads / 32;
   const bool epi = tid < kBwdEpiThreads;
 
   for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
@@ -153,9 +155,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
     const bool acc = !first;
     // ------------------------------------------------ phase F: F_feat + heads
     if (issuer) {
-      mbar_expect_tx(ldbar, 65536 + 20480);
-      bulk_g2s(sR + kRE2, ct + kCacheE2, 65536, ldbar);
-      bulk_g2s(sR + kRFF, ct + kCacheFF, 20480, ldbar);
+      if (lane == 0) mbar_expect_tx(ldbar, 65536 + 20480);
+      if (lane == 0) bulk_g2s(sR + kRE2, ct + kCacheE2, 65536, ldbar);
+      if (lane == 0) bulk_g2s(sR + kRFF, ct + kCacheFF, 20480, ldbar);
     }
     if (epi) {
       float v[8];
@@ -187,9 +189,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
       mbar_wait(ldbar, 0);
       tc_fence_after();
       // dL/dFF = dL/dz * W_f2 (numerics.py:102), dW_f2^T += FF^T dL/dz
-      gemm3(tmem + kScr, opnd_k(sR + kRGZ, 128, 16, 0), wF2, 32, 1, false);
-      gemm3(tmem + kDwF2, opnd_mn(sR + kRFF, 128, kCacheKtFF, 0), opnd_mn(sR + kRGZ, 128, 16, 0), p.DP, 8, acc);
-      mma_commit(accbar);
+      gemm3_w(tmem + kScr, opnd_k(sR + kRGZ, 128, 16, 0), wF2, 32, 1, false);
+      gemm3_w(tmem + kDwF2, opnd_mn(sR + kRFF, 128, kCacheKtFF, 0), opnd_mn(sR + kRGZ, 128, 16, 0), p.DP, 8, acc);
+      mma_commit_w(accbar);
     }
     uint64_t m2 = 0;  // ReLU gates of this thread's E2 columns: bit 16b+i = column 32b + 16 half + i
     if (epi) {
@@ -212,19 +214,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
     sync_all();
     auto issue_ge2 = [&](int b) {
       // dL/de2_b = dL/dFF * W_f1[:, 32b:32b+32] + dL/ddelta_b * W_head_b (deformation.py:157-177)
-      gemm3(tmem + kScr, opnd_k(sR + kRGFF, 128, 32, 0), opnd_mn(sW + p.off_f1, 32, 128, 32 * b), 32, 2, false);
-      gemm3(tmem + kScr, opnd_k(sR + kRGD, 128, 16, 0), opnd_mn(sW + p.off_headT[b], 16, 32, 0), 32, 1, true);
+      gemm3_w(tmem + kScr, opnd_k(sR + kRGFF, 128, 32, 0), opnd_mn(sW + p.off_f1, 32, 128, 32 * b), 32, 2, false);
+      gemm3_w(tmem + kScr, opnd_k(sR + kRGD, 128, 16, 0), opnd_mn(sW + p.off_headT[b], 16, 32, 0), 32, 1, true);
     };
     if (issuer) {
       const TcOpnd e2 = opnd_mn(sR + kRE2, 128, kCacheKtE2, 0);
-      gemm3(tmem + kDwF1, e2, opnd_mn(sR + kRGFF, 128, 32, 0), 32, 8, acc);
-      gemm3(tmem + kDwHead, e2, opnd_mn(sR + kRGD, 128, 16, 0), 16, 8, acc);
+      gemm3_w(tmem + kDwF1, e2, opnd_mn(sR + kRGFF, 128, 32, 0), 32, 8, acc);
+      gemm3_w(tmem + kDwHead, e2, opnd_mn(sR + kRGD, 128, 16, 0), 16, 8, acc);
       issue_ge2(0);
-      mma_commit(accbar);
+      mma_commit_w(accbar);
       mbar_wait(accbar, 1);  // E2 no longer read: load the hidden layer and branch 0's e1
-      mbar_expect_tx(ldbar, 36864 + kCacheE1Bytes);
-      bulk_g2s(sR + kRHid, ct + kCacheHid, 36864, ldbar);
-      bulk_g2s(sR + kRE1, ct + kCacheE1, kCacheE1Bytes, ldbar);
+      if (lane == 0) mbar_expect_tx(ldbar, 36864 + kCacheE1Bytes);
+      if (lane == 0) bulk_g2s(sR + kRHid, ct + kCacheHid, 36864, ldbar);
+      if (lane == 0) bulk_g2s(sR + kRE1, ct + kCacheE1, kCacheE1Bytes, ldbar);
     }
     auto epi_ge2 = [&](int b) {
       float g[16];
@@ -248,11 +250,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
         mbar_wait(ldbar, (1 + b) & 1);
         tc_fence_after();
         // dL/de1_b = dL/de2_b * W_ext1_b; dW_ext1_b^T += e1_b^T dL/de2_b
-        gemm3(tmem + kScr + 32, opnd_k(sR + kRGE2, 128, 32, 0), opnd_mn(sW + p.off_ext1[b], 32, 32, 0), 32, 2, false);
-        gemm3(tmem + kDwExt1 + 32 * b, opnd_mn(sR + kRE1, 128, kCacheKtE1, 0), opnd_mn(sR + kRGE2, 128, 32, 0), 32, 8,
+        gemm3_w(tmem + kScr + 32, opnd_k(sR + kRGE2, 128, 32, 0), opnd_mn(sW + p.off_ext1[b], 32, 32, 0), 32, 2, false);
+        gemm3_w(tmem + kDwExt1 + 32 * b, opnd_mn(sR + kRE1, 128, kCacheKtE1, 0), opnd_mn(sR + kRGE2, 128, 32, 0), 32, 8,
               acc);
         if (b < 3) issue_ge2(b + 1);
-        mma_commit(accbar);
+        mma_commit_w(accbar);
       }
       if (epi) {
         mbar_wait(accbar, (2 + b) & 1);
@@ -271,22 +273,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
       sync_all();
       if (issuer) {
         // dL/dhidden += dL/de1_b * W_ext0_b; dW_ext0_b^T += hidden^T dL/de1_b
-        gemm3(tmem + kScr + 64, opnd_k(sR + kRGE1, 128, 32, 0), opnd_mn(sW + p.off_ext0, 128, 64, 0, 32 * b), 64, 2,
+        gemm3_w(tmem + kScr + 64, opnd_k(sR + kRGE1, 128, 32, 0), opnd_mn(sW + p.off_ext0, 128, 64, 0, 32 * b), 64, 2,
               b > 0);
-        gemm3(tmem + kDwExt0 + 32 * b, opnd_mn(sR + kRHid, 128, kCacheKtHid, 0), opnd_mn(sR + kRGE1, 128, 32, 0), 32,
+        gemm3_w(tmem + kDwExt0 + 32 * b, opnd_mn(sR + kRHid, 128, kCacheKtHid, 0), opnd_mn(sR + kRGE1, 128, 32, 0), 32,
               8, acc);
         if (b < 3) {
-          mbar_expect_tx(ldbar, kCacheE1Bytes);
-          bulk_g2s(sR + kRE1, ct + kCacheE1 + (b + 1) * kCacheE1Bytes, kCacheE1Bytes, ldbar);
+          if (lane == 0) mbar_expect_tx(ldbar, kCacheE1Bytes);
+          if (lane == 0) bulk_g2s(sR + kRE1, ct + kCacheE1 + (b + 1) * kCacheE1Bytes, kCacheE1Bytes, ldbar);
         }
       }
     }
     // ------------------------------------------------ trunk
     if (issuer) {
-      mma_commit(accbar);
+      mma_commit_w(accbar);
       mbar_wait(accbar, 0);
-      mbar_expect_tx(ldbar, 36864);
-      bulk_g2s(sR + kRLat, ct + kCacheLat, 36864, ldbar);
+      if (lane == 0) mbar_expect_tx(ldbar, 36864);
+      if (lane == 0) bulk_g2s(sR + kRLat, ct + kCacheLat, 36864, ldbar);
     }
     if (epi) {
       mbar_wait(accbar, 0);
@@ -312,9 +314,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
       mbar_wait(ldbar, 1);
       tc_fence_after();
       // dL/dlatent = dL/dh0 * W_trunk; dW_trunk^T += latent^T dL/dh0
-      gemm3(tmem + kScr, opnd_k(sR + kRGH, 128, 64, 0), opnd_mn(sW + p.off_trunk[0], 64, 64, 0), 64, 4, false);
-      gemm3(tmem + kDwTrunk, opnd_mn(sR + kRLat, 128, kCacheKtLat, 0), opnd_mn(sR + kRGH, 128, 64, 0), 64, 8, acc);
-      mma_commit(accbar);
+      gemm3_w(tmem + kScr, opnd_k(sR + kRGH, 128, 64, 0), opnd_mn(sW + p.off_trunk[0], 64, 64, 0), 64, 4, false);
+      gemm3_w(tmem + kDwTrunk, opnd_mn(sR + kRLat, 128, kCacheKtLat, 0), opnd_mn(sR + kRGH, 128, 64, 0), 64, 8, acc);
+      mma_commit_w(accbar);
     }
     if (epi) {
       mbar_wait(accbar, 1);

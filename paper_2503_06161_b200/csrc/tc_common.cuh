@@ -218,6 +218,21 @@ __device__ __forceinline__ void gemm3(uint32_t tmem_d, const TcOpnd& A, const Tc
   }
 }
 
+// warp-wide gemm3 (all 32 lanes call it; one elected lane issues)
+__device__ __forceinline__ void gemm3_w(uint32_t tmem_d, const TcOpnd& A, const TcOpnd& B, int N, int ksteps,
+                                      bool accumulate) {
+  const uint32_t id = idesc_bf16(N, A.mn, B.mn);
+#pragma unroll
+  for (int s = 0; s < ksteps; ++s) {
+    const uint32_t ao = A.base + s * A.kstep, bo = B.base + s * B.kstep;
+    const uint64_t ah = sdesc(ao, A.lbo, A.sbo), al = sdesc(ao + A.lo, A.lbo, A.sbo);
+    const uint64_t bh = sdesc(bo, B.lbo, B.sbo), bl = sdesc(bo + B.lo, B.lbo, B.sbo);
+    mma_bf16_w(tmem_d, ah, bh, id, (s > 0 || accumulate) ? 1u : 0u);
+    mma_bf16_w(tmem_d, ah, bl, id, 1u);
+    mma_bf16_w(tmem_d, al, bh, id, 1u);
+  }
+}
+
 // v = hi + lo with hi = bf16_rn(v), lo = bf16_rn(v - hi) (v - hi is exact in
 // fp32).  Pairs go through cvt.rn.bf16x2.f32 (one packed convert per two
 // values); bit-identical to per-element __float2bfloat16_rn.
