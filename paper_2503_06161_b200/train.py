@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import DeformEngine, DeviceCloud, DeviceField, DeviceNet, Renderer, _p, _stream
+from .device import DeformEngine, DeviceCloud, DeviceField, DeviceNet, Renderer, _p, _stream, locality_order
 from .hexplane import tv_loss_grad_device
 from .numerics import lr_at_step
 from .optim import FlatAdam
@@ -62,7 +62,7 @@ def _net_layer_specs(net):
 class TrainStep:
     def __init__(self, cloud, field, net, height, width, cfg, world=1, group=None, device="cuda",
                  loss_mode="raw", lambda_rgb=1.0, lambda_depth=0.0, lambda_feat=1.0, lambda_tv=0.0,
-                 decoder=None):
+                 decoder=None, locality=None):
         self.cloud, self.field, self.net = cloud, field, net
         self.h, self.w, self.cfg = int(height), int(width), cfg
         self.world, self.group = int(world), group
@@ -70,6 +70,8 @@ class TrainStep:
         if loss_mode not in ("raw", "decoder"):
             raise ValueError(f"unknown loss mode {loss_mode!r}")
         self.loss_mode = loss_mode
+        import os
+        self.locality = (os.environ.get("FS4D_TRAIN_LOCALITY", "0") == "1") if locality is None else bool(locality)
         self.lambda_rgb, self.lambda_depth = float(lambda_rgb), float(lambda_depth)
         self.lambda_feat, self.lambda_tv = float(lambda_feat), float(lambda_tv)
         self.decoder = decoder  # (weight [Ct,N], bias [Ct]) CUDA tensors for loss_mode="decoder"
@@ -159,9 +161,14 @@ class TrainStep:
         w = 1.0 / n
         self.loss.zero_()
         dout = self.d_feature.shape[2]
+        field = self.field
+        if self.locality:
+            # Morton visiting order of this step's canonical positions for the
+            # HexPlane gather / scatter (identical results, coherent caches)
+            field = field.with_order(locality_order(self.cloud.positions, field.aabb, self.device))
         for i, item in enumerate(batch):
             t, K, T, tgt_rgb, tgt_feat = item[:5]
-            _, self.cache = self.deformer.forward(self.cloud, self.field, self.net, t, out=self.snap,
+            _, self.cache = self.deformer.forward(self.cloud, field, self.net, t, out=self.snap,
                                                   with_cache=self.cache or True)
             imgs, rec = self.renderer.forward(self.snap, K, T, self.h, self.w, self.cfg, images=self.images,
                                               check=check)
@@ -192,7 +199,7 @@ class TrainStep:
             self.renderer.backward(self.snap, K, T, self.h, self.w, self.cfg, rec, d_color=self.d_color,
                                    d_depth=d_depth, d_feature=self.d_feature if dout else None,
                                    grads=self.snap_grads)
-            self.deformer.backward(self.cloud, self.field, self.net, t, self.snap_grads,
+            self.deformer.backward(self.cloud, field, self.net, t, self.snap_grads,
                                    cloud_grads=self.cloud_grads, net_grads=self.net_grads,
                                    plane_grads=self.plane_grads if self.net.enable_grid else None,
                                    accumulate=i > 0, cache=self.cache)
