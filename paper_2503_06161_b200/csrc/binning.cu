@@ -16,7 +16,10 @@ namespace fs4d {
 
 constexpr int kHistMaxTiles = 6144;   // shared-memory histogram capacity (24 KB)
 constexpr int kSortSmemKeys = 8192;   // per-tile keys sorted in shared memory (64 KB)
-constexpr int kTileSortThreads = 512;
+#ifndef FS4D_TILE_SORT_THREADS
+#define FS4D_TILE_SORT_THREADS 512
+#endif
+constexpr int kTileSortThreads = FS4D_TILE_SORT_THREADS;
 
 __device__ __forceinline__ bool rect_valid(const int4& t) { return t.y >= t.x && t.w >= t.z; }
 
