@@ -376,7 +376,7 @@ __device__ __forceinline__ void epilogue_to_operand(uint32_t tmem_row, int col, 
 // NCH 8-column TMEM chunks at taddr0 + 16 i (one thread's half of a stage),
 // all issued before a single tcgen05.wait::ld: one TMEM round trip per stage
 // instead of one per chunk.  The empty asm ties keep every use after the wait.
-template <int NCH>
+template <int NCH, int STRIDE = 16>
 __device__ __forceinline__ void tmem_ld_batch(uint32_t taddr0, float (&v)[NCH][8]) {
   uint32_t r[NCH][8];
 #pragma unroll
@@ -384,7 +384,7 @@ __device__ __forceinline__ void tmem_ld_batch(uint32_t taddr0, float (&v)[NCH][8
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[i][0]), "=r"(r[i][1]), "=r"(r[i][2]), "=r"(r[i][3]), "=r"(r[i][4]), "=r"(r[i][5]),
                    "=r"(r[i][6]), "=r"(r[i][7])
-                 : "r"(taddr0 + 16u * i));
+                 : "r"(taddr0 + (uint32_t)STRIDE * i));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < NCH; ++i) {
@@ -1046,6 +1046,9 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
     // extractors, one epilogue thread per row -- was measured slower on B200,
     // 220 vs 179 us at configs[1]: the chain is bound by epilogue issue, not
     // by MMA latency, and halving the threads per tile lengthens it.)
+    // (a variant with four epilogue threads per row, 16 epilogue warps, was
+    // measured equal -- 95.6 vs 95.1 us -- so the epilogue is not starved of
+    // warps either; kept out.)
     cudaFuncSetAttribute(k_mlp_tc_ws<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mlp_tc_ws<false, false><<<grid, kTcWsThreads, smem, s>>>(a);
   }
