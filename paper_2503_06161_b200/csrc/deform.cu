@@ -728,14 +728,38 @@ struct PassArgs {
   const float* src[6];
   float* dst[6];
   int64_t n[6];
+  int64_t block_start[7];  // blocks of kPassChunk elements per field, prefix sums
   int accumulate;
 };
+constexpr int kPassChunk = 256 * 16;  // elements per block (16 per thread)
 
-__global__ void k_grad_passthrough(PassArgs a) {
-  const int f = blockIdx.y;
-  if (!a.src[f] || !a.dst[f]) return;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.n[f]; e += (int64_t)gridDim.x * blockDim.x)
-    a.dst[f][e] = a.accumulate ? a.dst[f][e] + a.src[f][e] : a.src[f][e];
+// Pass-through cloud gradients (deformation.py:178-181; colours / SH bypass
+// the deformation, training.py:518): every field's elements split into
+// equal chunks of one flat block index space, float4 accesses when aligned.
+__global__ void __launch_bounds__(256) k_grad_passthrough(PassArgs a) {
+  int f = 0;
+  while (f < 5 && (int64_t)blockIdx.x >= a.block_start[f + 1]) ++f;
+  const int64_t lo = ((int64_t)blockIdx.x - a.block_start[f]) * kPassChunk;
+  const int64_t hi = min(lo + kPassChunk, a.n[f]);
+  const float* src = a.src[f];
+  float* dst = a.dst[f];
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (vec && hi - lo == kPassChunk) {
+    const float4* s4 = reinterpret_cast<const float4*>(src + lo);
+    float4* d4 = reinterpret_cast<float4*>(dst + lo);
+#pragma unroll
+    for (int r = 0; r < kPassChunk / 4 / 256; ++r) {
+      const int e = r * 256 + threadIdx.x;
+      float4 v = __ldg(s4 + e);
+      if (a.accumulate) {
+        const float4 o = d4[e];
+        v = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+      }
+      d4[e] = v;
+    }
+    return;
+  }
+  for (int64_t e = lo + threadIdx.x; e < hi; e += 256) dst[e] = a.accumulate ? dst[e] + src[e] : src[e];
 }
 
 // ---------------------------------------------------------------------------
@@ -910,13 +934,18 @@ int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4
     const float* srcs[6] = {sg.rotations, sg.log_scales, sg.opacity_logits, sg.colors_raw, sg.sh_rest, sg.features};
     float* dsts[6] = {cg.rotations, cg.log_scales, cg.opacity_logits, cg.colors_raw, cg.sh_rest, cg.features};
     const int64_t ns[6] = {cloud.K * 4, cloud.K * 3, cloud.K, cloud.K * 3, cloud.K * n_sh * 3, cloud.K * cloud.D};
+    int64_t blocks = 0;
     for (int f = 0; f < 6; ++f) {
-      pa.src[f] = ns[f] > 0 ? srcs[f] : nullptr;
-      pa.dst[f] = ns[f] > 0 ? dsts[f] : nullptr;
-      pa.n[f] = ns[f];
+      const bool on = ns[f] > 0 && srcs[f] && dsts[f];
+      pa.src[f] = on ? srcs[f] : nullptr;
+      pa.dst[f] = on ? dsts[f] : nullptr;
+      pa.n[f] = on ? ns[f] : 0;
+      pa.block_start[f] = blocks;
+      blocks += ceil_div(pa.n[f], kPassChunk);
     }
+    pa.block_start[6] = blocks;
     pa.accumulate = accumulate;
-    k_grad_passthrough<<<dim3(kNumSMs * 2, 6), 256, 0, s>>>(pa);
+    if (blocks > 0) k_grad_passthrough<<<(unsigned)blocks, 256, 0, s>>>(pa);
   }
   const size_t cneed = deform_cache_bytes(net, field, cloud.K);
   if (cache && cneed) {
