@@ -425,7 +425,9 @@ int fs4d_render_fwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam,
 
 /* render_backward: grads->{positions, rotations, log_scales, opacity_logits,
  * colors_raw, sh_rest, features} are fully written (zeros for culled rows).
- * viewspace_index / viewspace_norm get the first M entries (depth order). */
+ * viewspace_index / viewspace_norm get the first M entries (depth order); when
+ * both are NULL the depth order is not materialised (no global sort) and the
+ * rows are visited in source order. */
 int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam,
                     const Fs4dRasterConfig* cfg, const Fs4dRecordInfo* info,
                     void* workspace, size_t workspace_bytes,

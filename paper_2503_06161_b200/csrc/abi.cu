@@ -451,7 +451,9 @@ int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam, const Fs4d
   if (rc) return rc;
   if ((rc = check_camera(cam))) return rc;
   if ((rc = check_record(info, snapshot, cam, cfg, workspace_bytes, workspace))) return rc;
-  if (!upstream || !grads || !viewspace_index || !viewspace_norm) return fail(FS4D_ERR_CONFIG, "null backward argument");
+  if (!upstream || !grads) return fail(FS4D_ERR_CONFIG, "null backward argument");
+  if (!viewspace_index != !viewspace_norm)
+    return fail(FS4D_ERR_CONFIG, "viewspace_index and viewspace_norm are both given or both NULL");
   if (grads->K != snapshot->K || grads->D != snapshot->D || grads->sh_degree != snapshot->sh_degree)
     return fail(FS4D_ERR_CONFIG, "gradient buffers do not match the snapshot");
   if (cfg->with_features && snapshot->D > 64)

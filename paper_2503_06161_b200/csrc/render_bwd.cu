@@ -396,7 +396,8 @@ struct PreBwdArgs {
   double R[9], tv[3], campos[3];
   double fx, fy, lowpass;
   int H, W, D, acc_stride, sh_degree;
-  const uint32_t* order;
+  const uint32_t* order;      // depth order (viewspace outputs in depth order), or null: source order
+  const int4* tile_rect;      // culled rows: (0, -1, 0, -1) (source-order mode zeroes their gradients)
   const uint32_t* counters;
   const float* accum;
   const uint32_t* clamp_mask;
@@ -414,8 +415,25 @@ __device__ __forceinline__ double sigmoid_db(double x) {
 // rasterizer.py:395-451 and gaussians.py:156-218.
 __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= (int64_t)a.counters[CNT_VISIBLE]) return;
-  const int64_t i = a.order[r];
+  int64_t i;
+  if (a.order) {
+    if (r >= (int64_t)a.counters[CNT_VISIBLE]) return;
+    i = a.order[r];
+  } else {  // source order, no viewspace outputs: culled rows get their zero gradients here
+    if (r >= a.c.K) return;
+    i = r;
+    const int4 t = a.tile_rect[i];
+    if (t.y < t.x) {
+      for (int k = 0; k < 3; ++k) a.g.positions[3 * i + k] = a.g.log_scales[3 * i + k] = a.g.colors_raw[3 * i + k] = 0.f;
+      for (int k = 0; k < 4; ++k) a.g.rotations[4 * i + k] = 0.f;
+      a.g.opacity_logits[i] = 0.f;
+      for (int c = 0; c < a.c.D; ++c) a.g.features[(int64_t)a.c.D * i + c] = 0.f;
+      const int nsh = ((a.sh_degree + 1) * (a.sh_degree + 1) - 1) * 3;
+      if (a.g.sh_rest)
+        for (int c = 0; c < nsh; ++c) a.g.sh_rest[(int64_t)nsh * i + c] = 0.f;
+      return;
+    }
+  }
   const float* acc = a.accum + i * a.acc_stride;
   const double dcol[3] = {acc[0], acc[1], acc[2]};
   const double ddep = acc[3], dop = acc[4];
@@ -570,8 +588,8 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
   for (int k = 0; k < 4; ++k) a.g.rotations[4 * i + k] = (float)((dqu[k] - inner * qu[k]) / qn);
   a.g.opacity_logits[i] = (float)(dop * o * (1.0 - o));
   for (int c = 0; c < a.D; ++c) a.g.features[(int64_t)a.D * i + c] = acc[10 + c];
-  a.vs_index[r] = (int32_t)i;
-  a.vs_norm[r] = (float)hypot(dmx * 0.5 * a.W, dmy * 0.5 * a.H);
+  if (a.vs_index) a.vs_index[r] = (int32_t)i;
+  if (a.vs_norm) a.vs_norm[r] = (float)hypot(dmx * 0.5 * a.W, dmy * 0.5 * a.H);
 }
 
 static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t s) {
@@ -614,6 +632,13 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   const int D = cfg.with_features ? L.D : 0;
   float* accum = at<float>(ws, L.accum);
   cudaMemsetAsync(accum, 0, (size_t)K * L.acc_stride * 4, s);
+  // Viewspace outputs requested: visit the visible rows in depth order (the
+  // order ProjectedGaussians reports them in) and zero the culled rows up
+  // front.  Not requested (training): source order, no global depth sort,
+  // the kernel writes the culled rows' zeros itself.
+  const bool depth_ordered = vs_index || vs_norm;
+  const int n_sh = (snap.sh_degree + 1) * (snap.sh_degree + 1) - 1;
+  if (depth_ordered) {
   // zero the outputs: culled rows keep zero gradients (rasterizer.py:432-441)
   cudaMemsetAsync(grads.positions, 0, (size_t)K * 3 * 4, s);
   cudaMemsetAsync(grads.rotations, 0, (size_t)K * 4 * 4, s);
@@ -621,8 +646,8 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   cudaMemsetAsync(grads.opacity_logits, 0, (size_t)K * 4, s);
   cudaMemsetAsync(grads.colors_raw, 0, (size_t)K * 3 * 4, s);
   if (grads.features && snap.D > 0) cudaMemsetAsync(grads.features, 0, (size_t)K * snap.D * 4, s);
-  const int n_sh = (snap.sh_degree + 1) * (snap.sh_degree + 1) - 1;
   if (grads.sh_rest && n_sh > 0) cudaMemsetAsync(grads.sh_rest, 0, (size_t)K * n_sh * 3 * 4, s);
+  }
 
   BwdArgs b;
   b.H = L.H;
@@ -673,7 +698,8 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   p.D = D;
   p.acc_stride = L.acc_stride;
   p.sh_degree = snap.sh_degree;
-  p.order = depth_order(L, ws, s);  // viewspace statistics are reported in depth order
+  p.order = depth_ordered ? depth_order(L, ws, s) : nullptr;  // viewspace statistics come in depth order
+  p.tile_rect = at<int4>(ws, L.tile_rect);
   p.counters = at<uint32_t>(ws, L.counters);
   p.accum = accum;
   p.clamp_mask = at<uint32_t>(ws, L.clamp_mask);

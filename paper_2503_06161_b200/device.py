@@ -447,12 +447,15 @@ class Renderer:
         return images, rec
 
     def backward(self, cloud, K, T, height, width, cfg, rec, d_color=None, d_depth=None,
-                 d_feature=None, d_alpha=None, grads=None):
+                 d_feature=None, d_alpha=None, grads=None, viewspace=True):
+        """render_backward on device.  viewspace=False skips the viewspace
+        outputs (and with them the global depth sort they are ordered by);
+        returns None for both then."""
         k, d, sh = len(cloud), cloud.feature_dim, cloud.sh_degree
         if grads is None:
             grads = DeviceCloud.empty(k, d, sh, self.device)
-        vs_index = torch.empty(max(k, 1), dtype=torch.int32, device=self.device)
-        vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device)
+        vs_index = torch.empty(max(k, 1), dtype=torch.int32, device=self.device) if viewspace else None
+        vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device) if viewspace else None
         cs, cam, rc, gs = cloud.struct(), camera_struct(K, T, height, width), raster_struct(cfg), grads.struct()
         up = N.ImageGrads()
         up.d_color, up.d_depth = _p(d_color), _p(d_depth)

@@ -198,7 +198,7 @@ class TrainStep:
                     self.d_feature.zero_()
             self.renderer.backward(self.snap, K, T, self.h, self.w, self.cfg, rec, d_color=self.d_color,
                                    d_depth=d_depth, d_feature=self.d_feature if dout else None,
-                                   grads=self.snap_grads)
+                                   grads=self.snap_grads, viewspace=False)
             self.deformer.backward(self.cloud, field, self.net, t, self.snap_grads,
                                    cloud_grads=self.cloud_grads, net_grads=self.net_grads,
                                    plane_grads=self.plane_grads if self.net.enable_grid else None,
