@@ -500,19 +500,23 @@ __global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a
 constexpr int kHexC32Warps = 8;
 struct HexC32Args {
   HexBwdArgs h;
-  int toff[2][3];  // shared-memory offsets (floats) of the time-plane accumulators
+  int toff[2][3];  // offsets (floats) of the time-plane accumulators inside a CTA's partial
   int tfloats;
+  float* tpart;    // [grid][tfloats] per-CTA time-plane partials (global, zeroed by the host)
 };
 
 __device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 || q == 5; }
 
+// Time planes: every Gaussian of a frame hits the same t row pair, so their
+// gradients collapse onto Ra spatial rows per plane.  They accumulate with
+// fire-and-forget red.global.add.v4 into a per-CTA partial (no cross-CTA
+// contention; a shared-memory float atomic is a CAS loop on sm_100), reduced
+// by k_time_partials afterwards.
 __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC32Args A) {
-  extern __shared__ float tacc[];
   const HexBwdArgs& a = A.h;
   const TcPlan& p = a.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < A.tfloats; i += blockDim.x) tacc[i] = 0.f;
-  __syncthreads();
+  float* tacc = A.tpart + (int64_t)blockIdx.x * A.tfloats;
   // the shared t cell of each level (hexplane.py:95-110 on the time axis)
   int tj0[2];
   float tfb[2];
@@ -624,14 +628,9 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC3
           const float f0 = w_a[q], f1 = w_b[q];
           if (is_time_plane(q)) {
             float* acc = tacc + A.toff[l][q == 2 ? 0 : (q == 4 ? 1 : 2)] + cb[q] * 32 + ch;
-            atomicAdd(acc + 0, cf.x * (1.f - f0));
-            atomicAdd(acc + 1, cf.y * (1.f - f0));
-            atomicAdd(acc + 2, cf.z * (1.f - f0));
-            atomicAdd(acc + 3, cf.w * (1.f - f0));
-            atomicAdd(acc + 32, cf.x * f0);
-            atomicAdd(acc + 33, cf.y * f0);
-            atomicAdd(acc + 34, cf.z * f0);
-            atomicAdd(acc + 35, cf.w * f0);
+            const float g0 = 1.f - f0;
+            red_add_v4(acc, cf.x * g0, cf.y * g0, cf.z * g0, cf.w * g0);
+            red_add_v4(acc + 32, cf.x * f0, cf.y * f0, cf.z * f0, cf.w * f0);
           } else {
             const int rs = p.res[l][q][1] * 32;
             float* gp = a.gplanes[l][q] + cb[q] + ch;
@@ -660,24 +659,32 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC3
       }
     }
   }
-  __syncthreads();
-  // flush the time planes: row i0 of the spatial axis, t rows j0 / j0 + 1
-#pragma unroll
-  for (int l = 0; l < 2; ++l)
-#pragma unroll
-    for (int qi = 0; qi < 3; ++qi) {
-      const int q = qi == 0 ? 2 : (qi == 1 ? 4 : 5);
-      const int ra = p.res[l][q][0], rb = p.res[l][q][1];
-      float* gp = a.gplanes[l][q];
-      const float* acc = tacc + A.toff[l][qi];
-      for (int e = threadIdx.x; e < ra * 32; e += blockDim.x) {
-        const float v = acc[e];
-        if (v == 0.f) continue;
-        const int i = e >> 5, c = e & 31;
-        red_add(gp + (i * rb + tj0[l]) * 32 + c, v * (1.f - tfb[l]));
-        red_add(gp + (i * rb + tj0[l] + 1) * 32 + c, v * tfb[l]);
-      }
-    }
+
+}
+
+// Sum the per-CTA time-plane partials (fixed order) and spread each spatial
+// row onto the t rows j0 / j0 + 1 with the frame's t weights (hexplane.py:95-110).
+struct TimeReduceArgs {
+  const float* tpart;
+  int nparts, tfloats;
+  int toff[2][3], ra[2][3], rb[2][3], tj0[2];
+  float tfb[2];
+  float* gp[2][3];
+};
+__global__ void __launch_bounds__(256) k_time_partials(TimeReduceArgs a) {
+  const int e = blockIdx.x * 256 + threadIdx.x;
+  if (e >= a.tfloats) return;
+  int l = 0, t = 0;
+  for (int ll = 0; ll < 2; ++ll)
+    for (int tt = 0; tt < 3; ++tt)
+      if (e >= a.toff[ll][tt]) l = ll, t = tt;
+  float v = 0.f;
+  for (int q = 0; q < a.nparts; ++q) v += a.tpart[(int64_t)q * a.tfloats + e];
+  if (v == 0.f) return;
+  const int loc = e - a.toff[l][t], i = loc >> 5, c = loc & 31, rb = a.rb[l][t];
+  float* g = a.gp[l][t];
+  g[(i * rb + a.tj0[l]) * 32 + c] += v * (1.f - a.tfb[l]);
+  g[(i * rb + a.tj0[l] + 1) * 32 + c] += v * a.tfb[l];
 }
 
 // ---------------------------------------------------------------------------
@@ -734,11 +741,32 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
         tf += p.res[l][qi == 0 ? 2 : (qi == 1 ? 4 : 5)][0] * 32;
       }
     hc.tfloats = tf;
-    if (p.C == 32 && p.levels == 2 && tf * 4 <= 100 * 1024 && !getenv("FS4D_HEX_BWD_GENERIC")) {
-      cudaFuncSetAttribute(k_hexplane_bwd_c32, cudaFuncAttributeMaxDynamicSharedMemorySize, tf * 4);
+    hc.tpart = wpart + (size_t)kNumSMs * kPartStride + 128;
+    if (p.C == 32 && p.levels == 2 && tf <= kTimePartFloats && !getenv("FS4D_HEX_BWD_GENERIC")) {
       const int64_t nblk = ceil_div(ceil_div(K, 32), kHexC32Warps);
-      const int grid = (int)(nblk < 2 * kNumSMs ? nblk : 2 * kNumSMs);
-      k_hexplane_bwd_c32<<<grid, kHexC32Warps * 32, tf * 4, s>>>(hc);
+      const int grid = (int)(nblk < kTimeParts ? nblk : kTimeParts);
+      cudaMemsetAsync(hc.tpart, 0, (size_t)grid * tf * 4, s);
+      k_hexplane_bwd_c32<<<grid, kHexC32Warps * 32, 0, s>>>(hc);
+      TimeReduceArgs tr;
+      tr.tpart = hc.tpart;
+      tr.nparts = grid;
+      tr.tfloats = tf;
+      for (int l = 0; l < 2; ++l) {
+        const int rt = p.res[l][2][1];
+        const double v = p.t * (rt - 1);
+        int j0 = (int)floor(v);
+        j0 = j0 < 0 ? 0 : (j0 > rt - 2 ? rt - 2 : j0);
+        tr.tj0[l] = j0;
+        tr.tfb[l] = (float)(v - j0);
+        for (int qi = 0; qi < 3; ++qi) {
+          const int q = qi == 0 ? 2 : (qi == 1 ? 4 : 5);
+          tr.toff[l][qi] = hc.toff[l][qi];
+          tr.ra[l][qi] = p.res[l][q][0];
+          tr.rb[l][qi] = p.res[l][q][1];
+          tr.gp[l][qi] = h.gplanes[l][q];
+        }
+      }
+      k_time_partials<<<(unsigned)ceil_div(tf, 256), 256, 0, s>>>(tr);
     } else {
       k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
     }

@@ -985,7 +985,8 @@ size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K) {
   TcPlan p;
   build_plan(n, f, 0.0, p, nullptr);
   // forward: latent [K, 64]; backward: d_latent [K, 64] + one weight-gradient partial per SM
-  return (size_t)p.ws_bytes + (size_t)K * 64 * 4 + (size_t)kNumSMs * kPartStride * 4 + 512;
+  return (size_t)p.ws_bytes + (size_t)K * 64 * 4 + (size_t)kNumSMs * kPartStride * 4 + 512 +
+         (size_t)kTimeParts * kTimePartFloats * 4;
 }
 
 int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,

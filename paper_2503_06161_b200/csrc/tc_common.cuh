@@ -291,6 +291,9 @@ constexpr uint32_t kCacheMagic = 0xF54DCAC1u;
 // (fp32, lane = input channel), plus 48 bias sums kept in shared memory; one
 // partial per CTA, [column][lane] then the bias tail.
 constexpr int kDwCols = 384;
+// per-CTA time-plane gradient partials of the HexPlane backward (deform_bwd_tc.cu)
+constexpr int kTimeParts = 2 * 148;
+constexpr int kTimePartFloats = 256 * 1024 / 4;  // upper bound of sum_l 3 * Ra * 32 (= kTimeRowBytes / 4)
 constexpr int kPartStride = kDwCols * kTcRows + 64;
 
 bool tc_path_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f);
