@@ -221,3 +221,35 @@ def test_cache_from_another_time_is_a_contract_violation():
            ("positions", "rotations", "log_scales", "opacity_logits", "features")}
     with pytest.raises(ContractViolation):
         fs().deform_backward(cloud, field, net, bad, type("G", (), ups)())
+
+
+def test_locality_order_is_a_permutation_and_changes_nothing():
+    """fs4d_locality_order (Morton order of the canonical positions) is a
+    permutation of [0, K); deforming with it (Fs4dHexPlane.order) gives
+    bit-identical snapshots, since every Gaussian's latent is computed
+    independently."""
+    import torch
+    import paper_2503_06161_b200 as fs
+    from paper_2503_06161_b200 import device as dv
+
+    rng = np.random.default_rng(17)
+    k = 20_000
+    a = random_cloud_arrays(rng, k, 16, depth_range=(2.0, 4.0), xy=1.0)
+    cloud = fs.GaussianCloud(**a)
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(16, 16, 16, 5), out_dim=64),
+                             fs.scene_aabb(cloud), rng, init="uniform")
+    net = fs.DeformationNet(64, fs.DeformationConfig(width=64, depth=1, feature_dim=16), rng, init="xavier",
+                            head_init="xavier")
+    c, f, n = dv.DeviceCloud.from_cloud(cloud), dv.DeviceField.from_field(field), dv.DeviceNet.from_net(net)
+    order = dv.locality_order(c.positions, f.aabb)
+    o = order.cpu().numpy()
+    np.testing.assert_array_equal(np.sort(o), np.arange(k))
+    # Morton order: consecutive Gaussians are spatially close on average
+    p = a["positions"]
+    assert np.linalg.norm(np.diff(p[o], axis=0), axis=1).mean() < 0.2 * np.linalg.norm(np.diff(p, axis=0), axis=1).mean()
+    e = dv.DeformEngine()
+    s0 = e.forward(c, f, n, 0.43)
+    s1 = e.forward(c, f.with_order(order), n, 0.43)
+    torch.cuda.synchronize()
+    for name in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        assert torch.equal(getattr(s0, name), getattr(s1, name)), name
