@@ -189,3 +189,40 @@ def test_size_independent_properties_at_config1_size():
     for key in img:
         assert torch.equal(img[key], img2[key])
     assert rec.n_visible > 0.95 * k
+
+
+def test_size_independent_properties_at_config3_size():
+    """configs[3] (SCARED-shaped): 500k Gaussians, 1280x1024, fx=fy=1100, SH3,
+    D=32 -- long tile lists and the 32-channel feature registers.  Linearity
+    in a shared feature and colour, conservation, determinism, and the pair
+    count / visible set of the device binning against the float64 oracle's
+    projection + binning of the same scene."""
+    import torch
+    from oracle import fs4d_oracle as O
+    from paper_2503_06161_b200.device import DeviceCloud, Renderer
+    rng = np.random.default_rng(13)
+    k, h, w, d = 500_000, 1024, 1280, 32
+    a = random_cloud_arrays(rng, k, d, op_range=(0.05, 0.95), depth_range=(3.0, 6.0), xy=1.0,
+                            ls_range=(np.exp(-5.0), np.exp(-3.0)), sh_degree=3)
+    zstar = np.linspace(-1.0, 1.0, d)
+    a["features"] = np.tile(zstar, (k, 1))
+    a["colors_raw"] = np.tile([0.25, 0.5, 0.75], (k, 1))
+    a["sh_rest"] = np.zeros_like(a["sh_rest"])  # colour = clip(DC) everywhere -> linearity holds
+    cloud_np = fs().GaussianCloud(**a)
+    cloud = DeviceCloud.from_cloud(cloud_np)
+    r = Renderer()
+    K = pinhole(h, w, 1100.0)
+    img, rec = r.forward(cloud, K, np.eye(4), h, w, fs().RasterConfig())
+    alpha = img["alpha"].cpu().numpy()
+    assert alpha.min() >= 0 and alpha.max() <= 1
+    np.testing.assert_allclose(img["feature"].cpu().numpy(), alpha[:, :, None] * zstar[None, None, :], atol=3e-5)
+    np.testing.assert_allclose(img["color"].cpu().numpy(), alpha[:, :, None] * np.array([0.25, 0.5, 0.75]),
+                               atol=3e-5)
+    img2, _ = r.forward(cloud, K, np.eye(4), h, w, fs().RasterConfig())
+    for key in img:
+        assert torch.equal(img[key], img2[key])
+    proj = O.project(cloud_np, K, np.eye(4), h, w, O.RasterParams())
+    lists = O.bin_tiles(proj, h, w, 16)
+    n_pairs = sum(c.size for row in lists for c in row)
+    assert rec.n_visible == len(proj["source_index"])
+    assert rec.n_pairs == n_pairs
