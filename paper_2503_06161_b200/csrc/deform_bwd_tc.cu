@@ -519,7 +519,6 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC3
   float* tacc = A.tpart + (int64_t)blockIdx.x * A.tfloats;
   // the shared t cell of each level (hexplane.py:95-110 on the time axis)
   int tj0[2];
-  float tfb[2];
 #pragma unroll
   for (int l = 0; l < 2; ++l) {
     const int rt = p.res[l][2][1];
@@ -527,7 +526,6 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC3
     int j0 = (int)floor(v);
     j0 = min(max(j0, 0), rt - 2);
     tj0[l] = j0;
-    tfb[l] = (float)(v - j0);
   }
   const int sub = lane >> 3, ch = (lane & 7) * 4;
   const int64_t nchunks = ceil_div(a.K, 32);

@@ -965,7 +965,7 @@ int tc_pack(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p, 
   if (rc) return rc;
   pk.blob = blob;
   pk.rows = reinterpret_cast<float*>(blob + p.off_rows);
-  k_pack_tc<<<dim3(4, pk.nop + pk.nbias + pk.nrow), 256, 0, s>>>(pk);
+  k_pack_tc<<<dim3(16, pk.nop + pk.nbias + pk.nrow), 256, 0, s>>>(pk);
   return check_launch("deform_tc_pack");
 }
 
