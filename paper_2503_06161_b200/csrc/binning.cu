@@ -1,7 +1,7 @@
 // Tile binning without a global sort (bin_tiles, rasterizer.py:188-207, and the
 // stable depth argsort it relies on, rasterizer.py:163).
 //
-//   k_tile_hist       per-tile pair counts (block-aggregated in shared memory)
+//   (per-tile pair counts: fused into k_preprocess, render_fwd.cu)
 //   scan              tile offsets (device-wide exclusive scan)
 //   k_emit_partition  every (tile, Gaussian) pair lands in its tile's segment;
 //                     block-level reservation, order inside a segment arbitrary
@@ -22,29 +22,6 @@ constexpr int kSortSmemKeys = 8192;   // per-tile keys sorted in shared memory (
 constexpr int kTileSortThreads = FS4D_TILE_SORT_THREADS;
 
 __device__ __forceinline__ bool rect_valid(const int4& t) { return t.y >= t.x && t.w >= t.z; }
-
-__global__ void __launch_bounds__(256) k_tile_hist(const int4* __restrict__ tile_rect, const uint32_t* __restrict__ dkeys,
-                                                   int64_t K, int ntx, int ntiles, uint32_t* __restrict__ tcnt) {
-  __shared__ uint32_t h[kHistMaxTiles];
-  const bool smem = ntiles <= kHistMaxTiles;
-  if (smem)
-    for (int b = threadIdx.x; b < ntiles; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < K && dkeys[i] != 0xFFFFFFFFu) {
-    const int4 t = tile_rect[i];
-    for (int ty = t.z; ty <= t.w; ++ty)
-      for (int tx = t.x; tx <= t.y; ++tx) {
-        const int b = ty * ntx + tx;
-        if (smem) atomicAdd(&h[b], 1u);
-        else atomicAdd(&tcnt[b], 1u);
-      }
-  }
-  __syncthreads();
-  if (smem)
-    for (int b = threadIdx.x; b < ntiles; b += blockDim.x)
-      if (h[b]) atomicAdd(&tcnt[b], h[b]);
-}
 
 // key = fp32 depth bits (positive floats order as unsigned) << 32 | source index
 __global__ void __launch_bounds__(256) k_emit_partition(const int4* __restrict__ tile_rect,
@@ -283,10 +260,8 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
   uint32_t* tcnt = at<uint32_t>(ws, L.tcnt);
   uint32_t* tcur = at<uint32_t>(ws, L.tcur);
   uint64_t* toff = at<uint64_t>(ws, L.toff64);
-  cudaMemsetAsync(tcnt, 0, (size_t)L.ntiles * 4, s);
-  cudaMemsetAsync(tcur, 0, (size_t)L.ntiles * 4, s);
+  // tcnt / tcur / ranges were zeroed and tcnt filled by k_preprocess's fused histogram
   const unsigned gb = (unsigned)ceil_div(K > 0 ? K : 1, 256);
-  if (K > 0) k_tile_hist<<<gb, 256, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles, tcnt);
   exclusive_scan_u32_to_u64(tcnt, toff, L.ntiles, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64),
                             at<void>(ws, L.scratch), s);
   k_pairs_check2<<<1, 1, 0, s>>>(counters, L.cap, status);

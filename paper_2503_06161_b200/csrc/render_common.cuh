@@ -12,6 +12,7 @@ namespace fs4d {
 
 constexpr int kTile = 16;
 constexpr int kTilePixels = kTile * kTile;
+constexpr int kHistTilesSmem = 6144;  // per-block shared histogram capacity (24 KB)
 constexpr float kQSkip = 11.0825270270270f;  // 2 ln 255 (rasterizer.py:212)
 
 struct RenderLayout {

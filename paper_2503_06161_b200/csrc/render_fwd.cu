@@ -32,6 +32,7 @@ struct PreArgs {
   uint32_t* dvals;
   uint32_t* clamp_mask;
   uint32_t* counters;
+  uint32_t* tcnt;  // per-tile pair counts (zeroed by the host), filled by the fused histogram
   int32_t* status;
 };
 
@@ -42,9 +43,10 @@ __device__ __forceinline__ double sigmoid_d(double x) {
   return e / (1.0 + e);
 }
 
-__global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.c.K) return;
+// One Gaussian of k_preprocess; returns its inclusive tile rectangle
+// ((0, -1, 0, -1) when culled / out of range).
+__device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i) {
+  if (i >= a.c.K) return make_int4(0, -1, 0, -1);
   a.dvals[i] = (uint32_t)i;
   a.dkeys[i] = 0xFFFFFFFFu;  // culled sentinel sorts last
   a.tile_rect[i] = make_int4(0, -1, 0, -1);
@@ -78,14 +80,14 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
     for (int k = 0; k < n_sh * 3; ++k) sb |= !isfinite(S[k]);
     if (sb) { flag_bad_field(a.status, FS4D_FIELD_SH, i); bad = true; }
   }
-  if (bad) return;
+  if (bad) return make_int4(0, -1, 0, -1);
 
   // ---- camera space (rasterizer.py:131-140) ----
   const double X = p0, Y = p1, Z = p2;
   const double x = a.R[0] * X + a.R[1] * Y + a.R[2] * Z + a.tv[0];
   const double y = a.R[3] * X + a.R[4] * Y + a.R[5] * Z + a.tv[1];
   const double z = a.R[6] * X + a.R[7] * Y + a.R[8] * Z + a.tv[2];
-  if (!(z > a.z_near)) return;
+  if (!(z > a.z_near)) return make_int4(0, -1, 0, -1);
   const double u = a.fx * x / z + a.cx;
   const double v = a.fy * y / z + a.cy;
 
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
       atomicMin(&a.status[FS4D_ST_DEGEN_INDEX], (int32_t)i);
       raise_status(a.status, FS4D_ERR_DEGENERATE);
     }
-    return;
+    return make_int4(0, -1, 0, -1);
   }
   const double qw = q0 / qn, qx = q1 / qn, qy = q2 / qn, qz = q3 / qn;
   double Rq[9];
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
 
   // ---- offscreen cull (rasterizer.py:160-162) ----
   const bool on = (u + radius >= 0) && (u - radius <= a.W - 1) && (v + radius >= 0) && (v - radius <= a.H - 1);
-  if (!on) return;
+  if (!on) return make_int4(0, -1, 0, -1);
 
   // ---- kept: conic, activations, footprints ----
   const double inv = 1.0 / det;
@@ -199,6 +201,29 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
   a.z64[i] = z;
   a.dkeys[i] = __float_as_uint((float)z);  // z > 0: IEEE bits order as unsigned
   atomicAdd(&a.counters[CNT_VISIBLE], 1u);
+  return make_int4(tx0, tx1, ty0, ty1);
+}
+
+// Projection of every Gaussian (preprocess_one) fused with the per-tile pair
+// histogram bin_tiles needs (rasterizer.py:188-207): block-aggregated in
+// shared memory, one global atomic per (block, touched tile).
+__global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
+  __shared__ uint32_t h[kHistTilesSmem];
+  const bool smem = a.ntx * a.nty <= kHistTilesSmem;
+  if (smem)
+    for (int b = threadIdx.x; b < a.ntx * a.nty; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int4 t = preprocess_one(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  for (int ty = t.z; ty <= t.w; ++ty)
+    for (int tx = t.x; tx <= t.y; ++tx) {
+      const int b = ty * a.ntx + tx;
+      if (smem) atomicAdd(&h[b], 1u);
+      else atomicAdd(&a.tcnt[b], 1u);
+    }
+  __syncthreads();
+  if (smem)
+    for (int b = threadIdx.x; b < a.ntx * a.nty; b += blockDim.x)
+      if (h[b]) atomicAdd(&a.tcnt[b], h[b]);
 }
 
 // Equal fp32 keys are re-ordered by the exact fp64 depth, ties by source
@@ -685,7 +710,8 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   const int64_t K = L.K;
   uint32_t* counters = at<uint32_t>(ws, L.counters);
   cudaMemsetAsync(counters, 0, CNT_WORDS * 4, s);
-  cudaMemsetAsync(at<uint2>(ws, L.ranges), 0, (size_t)L.ntiles * 8, s);
+  // tile counts, append cursors, offsets and ranges are contiguous: one memset
+  cudaMemsetAsync(at<char>(ws, L.tcnt), 0, L.ranges + (size_t)L.ntiles * 8 - L.tcnt, s);
 
   PreArgs p;
   p.c = snap;
@@ -717,6 +743,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   p.dvals = at<uint32_t>(ws, L.dvals0);
   p.clamp_mask = at<uint32_t>(ws, L.clamp_mask);
   p.counters = counters;
+  p.tcnt = at<uint32_t>(ws, L.tcnt);
   p.status = status;
   {
     StageTimer st(FS4D_STAGE_PREPROCESS, s);
