@@ -458,9 +458,9 @@ def train_bench(args, rank, world, local):
 
 def launches_per_frame():
     """libfs4d kernels per frame: deform (pack, HexPlane latent, tcgen05 MLP) and
-    render (status reset, preprocess + fused tile histogram, 3-kernel scan,
-    pair check, partition, per-tile sort, blend)."""
-    return 3 + (1 + 1 + 3 + 1 + 1 + 1 + 1)
+    render (status reset, preprocess + fused tile histogram, single-block tile
+    scan + pair check, partition, per-tile sort, blend)."""
+    return 3 + (1 + 1 + 1 + 1 + 1 + 1)
 
 
 def main():

@@ -242,6 +242,59 @@ __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long lo
   }
 }
 
+// Tile offsets for up to a few tens of thousands of tiles in ONE block:
+// exclusive scan of the per-tile counts (u64 offsets), the pair total, and
+// the capacity check -- one launch instead of a 3-kernel device scan + check.
+constexpr int kTileScanThreads = 1024;
+__global__ void __launch_bounds__(kTileScanThreads) k_tile_scan_check(const uint32_t* __restrict__ tcnt, int ntiles,
+                                                                      uint64_t* __restrict__ toff, uint32_t* counters,
+                                                                      int64_t cap, int32_t* status) {
+  __shared__ uint64_t wsum[kTileScanThreads / 32];
+  const int per = (ntiles + kTileScanThreads - 1) / kTileScanThreads;
+  const int b0 = threadIdx.x * per;
+  uint64_t local = 0;
+  for (int q = 0; q < per; ++q)
+    if (b0 + q < ntiles) local += tcnt[b0 + q];
+  // block-wide exclusive scan of the per-thread sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = wsum[lane];
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    wsum[lane] = wi - w;  // exclusive warp bases
+  }
+  __syncthreads();
+  uint64_t run = wsum[warp] + incl - local;
+  for (int q = 0; q < per; ++q)
+    if (b0 + q < ntiles) {
+      toff[b0 + q] = run;
+      run += tcnt[b0 + q];
+    }
+  if (threadIdx.x == kTileScanThreads - 1) {
+    const uint64_t total = run;
+    *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64) = total;
+    counters[CNT_PAIRS_CLAMPED] = (uint32_t)(total < (uint64_t)cap ? total : (uint64_t)cap);
+    if (status) {
+      status[FS4D_ST_N_VISIBLE] = (int32_t)counters[CNT_VISIBLE];
+      status[FS4D_ST_PAIRS_LO] = (int32_t)(total & 0xFFFFFFFFu);
+      status[FS4D_ST_PAIRS_HI] = (int32_t)(total >> 32);
+      if (total > (uint64_t)cap) raise_status(status, FS4D_ERR_CAPACITY);
+    }
+  }
+}
+
 __global__ void k_pairs_check2(uint32_t* counters, int64_t cap, int32_t* status) {
   const uint64_t total = *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64);
   counters[CNT_PAIRS_CLAMPED] = (uint32_t)(total < (uint64_t)cap ? total : (uint64_t)cap);
@@ -262,9 +315,13 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
   uint64_t* toff = at<uint64_t>(ws, L.toff64);
   // tcnt / tcur / ranges were zeroed and tcnt filled by k_preprocess's fused histogram
   const unsigned gb = (unsigned)ceil_div(K > 0 ? K : 1, 256);
-  exclusive_scan_u32_to_u64(tcnt, toff, L.ntiles, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64),
-                            at<void>(ws, L.scratch), s);
-  k_pairs_check2<<<1, 1, 0, s>>>(counters, L.cap, status);
+  if (L.ntiles <= 64 * kTileScanThreads) {
+    k_tile_scan_check<<<1, kTileScanThreads, 0, s>>>(tcnt, L.ntiles, toff, counters, L.cap, status);
+  } else {
+    exclusive_scan_u32_to_u64(tcnt, toff, L.ntiles, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64),
+                              at<void>(ws, L.scratch), s);
+    k_pairs_check2<<<1, 1, 0, s>>>(counters, L.cap, status);
+  }
   unsigned long long* pkey = at<unsigned long long>(ws, L.pkey64);
   if (K > 0) k_emit_partition<<<gb, 256, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles, toff, tcur, L.cap, pkey);
   static bool attr = false;
