@@ -152,17 +152,17 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
         const int4 pr = s_pr[k];
         live = !(col < pr.x || col > pr.y || row < pr.z || row > pr.w);
       }
-      float dx = 0.f, dy = 0.f, q = 0.f, gv = 0.f, araw = 0.f, al = 0.f;
+      float dx = 0.f, dy = 0.f, gv = 0.f, araw = 0.f, al = 0.f;
       float4 co = make_float4(0.f, 0.f, 0.f, 0.f);
       if (live) {
         const float2 m = s_xy[k];
         co = s_co[k];
         dx = fc - m.x;
         dy = fr - m.y;
-        q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
-        live = q <= kQSkip;
+        const float pw = gauss_power(scaled_conic(co), dx, dy);  // same scaling as the forward's staging
+        live = !(pw < kPowSkip);
         if (live) {
-          gv = __expf(-0.5f * q);
+          gv = fast_exp2(pw);
           araw = co.w * gv;
           al = fminf(araw, a.alpha_cap);
           live = al >= a.alpha_skip;
@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
   constexpr int NF = DC > 0 ? DC : 1;
   __shared__ float2 s_xy[B];
   __shared__ float4 s_co[B];
+  __shared__ float4 s_cs[B];  // scaled conic (gauss_power), same evaluation as the forward
   __shared__ int4 s_pr[B];
   __shared__ float4 s_rgbz[B];
   __shared__ uint32_t s_g[B];
@@ -303,7 +304,9 @@ __global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
       const uint32_t g = a.pvals[bstart + threadIdx.x];
       s_g[threadIdx.x] = g;
       s_xy[threadIdx.x] = a.xy[g];
-      s_co[threadIdx.x] = a.conic_o[g];
+      const float4 cog = a.conic_o[g];
+      s_co[threadIdx.x] = cog;
+      s_cs[threadIdx.x] = scaled_conic(cog);
       s_pr[threadIdx.x] = a.pix_rect[g];
       s_rgbz[threadIdx.x] = a.rgbz[g];
       if (DC > 0) {
@@ -345,9 +348,9 @@ __global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
                       !(col < pr.x || col > pr.y || row < pr.z || row > pr.w);
           if (!live) continue;
           const float dx = fc - mxy.x, dy = (float)row - mxy.y;
-          const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
-          if (q > kQSkip) continue;
-          const float gv = __expf(-0.5f * q);
+          const float pw = gauss_power(s_cs[k], dx, dy);
+          if (pw < kPowSkip) continue;
+          const float gv = fast_exp2(pw);
           const float araw = co.w * gv;
           const float al = fminf(araw, a.alpha_cap);
           if (al < a.alpha_skip) continue;

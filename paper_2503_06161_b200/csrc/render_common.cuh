@@ -15,6 +15,28 @@ constexpr int kTilePixels = kTile * kTile;
 constexpr int kHistTilesSmem = 6144;  // per-block shared histogram capacity (24 KB)
 constexpr float kQSkip = 11.0825270270270f;  // 2 ln 255 (rasterizer.py:212)
 
+// The forward blend and the backward replay evaluate a Gaussian at a pixel the
+// same way: exp(-q/2) = 2^power with power = a' dx^2 + b' dx dy + c' dy^2 for
+// the conic pre-scaled once per staged Gaussian (a' = -log2(e)/2 a, b' =
+// -log2(e) b, c' = -log2(e)/2 c), and q > 2 ln 255 <=> power < kPowSkip.
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kPowSkip = -0.5f * kLog2e * kQSkip;
+__device__ __forceinline__ float4 scaled_conic(const float4& co) {
+  return make_float4(-0.5f * kLog2e * co.x, -kLog2e * co.y, -0.5f * kLog2e * co.z, co.w);
+}
+// back to (a, b, c, opacity) up to a few ulps -- for the conservative strip cull only
+__device__ __forceinline__ float4 unscaled_conic(const float4& cs) {
+  return make_float4(cs.x * (-2.f / kLog2e), cs.y * (-1.f / kLog2e), cs.z * (-2.f / kLog2e), cs.w);
+}
+__device__ __forceinline__ float gauss_power(const float4& cs, float dx, float dy) {
+  return cs.x * dx * dx + cs.y * dx * dy + cs.z * dy * dy;
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 struct RenderLayout {
   int64_t K = 0, cap = 0;
   int H = 0, W = 0, D = 0, ntx = 0, nty = 0, ntiles = 0, tile_bits = 0, acc_stride = 0;

@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
 #endif
   constexpr int NT = kTilePixels / SUB;  // threads = pixels = Gaussians per batch
   __shared__ float2 s_xy[NT];
-  __shared__ float4 s_co[NT];
+  __shared__ float4 s_cs[NT];  // scaled conic (gauss_power)
   __shared__ int4 s_pr[NT];
   __shared__ float4 s_rgbz[NT];
   // features channel-quad-major [DC/4][NT] float4: conflict-free staging
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
     if (j < rg.y) {
       const uint32_t g = a.pvals[j];
       s_xy[threadIdx.x] = a.xy[g];
-      s_co[threadIdx.x] = a.conic_o[g];
+      s_cs[threadIdx.x] = scaled_conic(a.conic_o[g]);
       s_pr[threadIdx.x] = a.pix_rect[g];
       s_rgbz[threadIdx.x] = a.rgbz[g];
       if (DC > 0) {
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
       if (kk < cnt) {
         const int4 pr = s_pr[kk];
         hit = pr.w >= wrow0 && pr.z <= wrow0 + 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
-        if (hit) hit = strip_hits<2>(pr, s_xy[kk], s_co[kk], wrow0, tcol0, a.alpha_skip);
+        if (hit) hit = strip_hits<2>(pr, s_xy[kk], unscaled_conic(s_cs[kk]), wrow0, tcol0, a.alpha_skip);
       }
       const unsigned msk = __ballot_sync(0xffffffffu, hit);
       if (lane == 0) s_mask[wid][m] = msk;
@@ -409,12 +409,11 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
             const int k = kk[j];
             const int4 pr = s_pr[k];
             const float2 mm = s_xy[k];
-            const float4 co = s_co[k];
+            const float4 cs = s_cs[k];
             const float dx = fc - mm.x, dy = fr - mm.y;
-            const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
-            const float gv = __expf(-0.5f * q);
-            const float al = fminf(co.w * gv, a.alpha_cap);
-            live[j] = live[j] && !(col < pr.x || col > pr.y || row < pr.z || row > pr.w) && !(q > kQSkip) &&
+            const float pw = gauss_power(cs, dx, dy);
+            const float al = fminf(cs.w * fast_exp2(pw), a.alpha_cap);
+            live[j] = live[j] && !(col < pr.x || col > pr.y || row < pr.z || row > pr.w) && !(pw < kPowSkip) &&
                       !(al < a.alpha_skip);
             alv[j] = al;
           }
@@ -488,182 +487,6 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   }
 }
 
-// Two horizontally adjacent pixels per thread (cols 2c, 2c+1): every staged
-// Gaussian's shared-memory loads, ballot bookkeeping and loop overhead are
-// paid once for two pixels, and the two compositing chains are independent
-// (ILP).  A warp covers 4 rows x 16 columns; SUB CTAs split a tile's rows.
-// Per-pixel decisions and their order are exactly k_blend's.
-template <int DC, int SUB>
-__global__ void __launch_bounds__(kTilePixels / 2 / SUB) k_blend_px2(BlendArgs a) {
-  constexpr int NT = kTilePixels / 2 / SUB;  // threads = Gaussians per batch
-  constexpr int NW = NT / 32;
-  __shared__ float2 s_xy[NT];
-  __shared__ float4 s_co[NT];
-  __shared__ int4 s_pr[NT];
-  __shared__ float4 s_rgbz[NT];
-  __shared__ __align__(16) float4 s_f4[DC > 0 ? NT * DC / 4 : 1];
-  __shared__ unsigned s_mask[NW][NT / 32];
-
-  const int tile = blockIdx.x / SUB, sub = blockIdx.x % SUB;
-  const int tx = tile % a.ntx, ty = tile / a.ntx;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int row0 = ty * kTile + sub * (kTile / SUB);
-  const int wrow0 = row0 + wid * 4;              // this warp's four pixel rows
-  const int row = wrow0 + (lane >> 3);
-  const int col = tx * kTile + 2 * (lane & 7);   // and col + 1
-  const bool in0 = col < a.W && row < a.H, in1 = col + 1 < a.W && row < a.H;
-  const uint2 rg = a.ranges[tile];
-  const bool first = a.c0 == 0;
-  const float fc = (float)col, fr = (float)row;
-  const int tcol0 = tx * kTile;
-
-  float T[2] = {1.f, 1.f};
-  float2 acc_rg[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  float2 acc_bz[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  float2 accf2[2][DC > 0 ? DC / 2 : 1];
-#pragma unroll
-  for (int p = 0; p < 2; ++p)
-#pragma unroll
-    for (int c = 0; c < (DC > 0 ? DC / 2 : 1); ++c) accf2[p][c] = make_float2(0.f, 0.f);
-  int ncontrib[2] = {0, 0}, last[2] = {-1, -1};
-  bool done[2] = {!in0, !in1};
-  const int nf = DC > 0 ? min(DC, a.D - a.c0) : 0;
-  const bool vec_ok = DC >= 4 && nf == DC && (a.D & 3) == 0 && (a.c0 & 3) == 0;
-
-  for (uint32_t b = rg.x; b < rg.y; b += NT) {
-    if (__syncthreads_count(done[0] && done[1]) == NT) break;
-    const uint32_t j = b + threadIdx.x;
-    if (j < rg.y) {
-      const uint32_t g = a.pvals[j];
-      s_xy[threadIdx.x] = a.xy[g];
-      s_co[threadIdx.x] = a.conic_o[g];
-      s_pr[threadIdx.x] = a.pix_rect[g];
-      s_rgbz[threadIdx.x] = a.rgbz[g];
-      if (DC > 0) {
-        const float* src = a.features + (int64_t)g * a.D + a.c0;
-        if (vec_ok) {
-#pragma unroll
-          for (int c = 0; c < DC; c += 4) s_f4[(c / 4) * NT + threadIdx.x] = __ldg(reinterpret_cast<const float4*>(src + c));
-        } else {
-          for (int c = 0; c < DC; c += 4) {
-            float v[4];
-            for (int i = 0; i < 4; ++i) v[i] = c + i < nf ? src[c + i] : 0.f;
-            s_f4[(c / 4) * NT + threadIdx.x] = make_float4(v[0], v[1], v[2], v[3]);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    const int cnt = min((uint32_t)NT, rg.y - b);
-#pragma unroll
-    for (int m = 0; m < NT / 32; ++m) {
-      const int kk = m * 32 + lane;
-      bool hit = false;
-      if (kk < cnt) {
-        const int4 pr = s_pr[kk];
-        hit = pr.w >= wrow0 && pr.z <= wrow0 + 3 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
-      }
-      const unsigned msk = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) s_mask[wid][m] = msk;
-    }
-    __syncwarp();
-    if (!(done[0] && done[1])) {
-#pragma unroll 1
-      for (int m = 0; m < NT / 32 && !(done[0] && done[1]); ++m) {
-        unsigned bits = s_mask[wid][m];
-        constexpr int BK = 2;
-        while (bits) {
-          int kk[BK];
-          float alv[BK][2];
-          bool live[BK][2];
-#pragma unroll
-          for (int jj = 0; jj < BK; ++jj) {
-            kk[jj] = bits ? m * 32 + __ffs(bits) - 1 : 0;
-            const bool any = bits != 0;
-            bits &= bits - 1;
-            const int k = kk[jj];
-            const int4 pr = s_pr[k];
-            const float2 mm = s_xy[k];
-            const float4 co = s_co[k];
-            const float dy = fr - mm.y;
-            const bool rok = any && row >= pr.z && row <= pr.w;
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-              const float dx = fc + (float)p - mm.x;
-              const float q = co.x * dx * dx + 2.f * co.y * dx * dy + co.z * dy * dy;
-              const float al = fminf(co.w * __expf(-0.5f * q), a.alpha_cap);
-              live[jj][p] = rok && col + p >= pr.x && col + p <= pr.y && !(q > kQSkip) && !(al < a.alpha_skip);
-              alv[jj][p] = al;
-            }
-          }
-#pragma unroll
-          for (int jj = 0; jj < BK; ++jj) {
-            const int k = kk[jj];
-            float4 cz = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (first) cz = s_rgbz[k];
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-              if (!live[jj][p] || done[p]) continue;
-              if (T[p] < a.stop) {
-                done[p] = true;
-                continue;
-              }
-              const float al = alv[jj][p];
-              const float w = al * T[p];
-              const float2 w2 = make_float2(w, w);
-              if (first) {
-                acc_rg[p] = __ffma2_rn(w2, make_float2(cz.x, cz.y), acc_rg[p]);
-                acc_bz[p] = __ffma2_rn(w2, make_float2(cz.z, cz.w), acc_bz[p]);
-              }
-              if (DC > 0) {
-#pragma unroll
-                for (int c = 0; c < DC; c += 4) {
-                  const float4 fv = s_f4[(c / 4) * NT + k];
-                  accf2[p][c / 2] = __ffma2_rn(w2, make_float2(fv.x, fv.y), accf2[p][c / 2]);
-                  accf2[p][c / 2 + 1] = __ffma2_rn(w2, make_float2(fv.z, fv.w), accf2[p][c / 2 + 1]);
-                }
-              }
-              T[p] *= (1.f - al);
-              ++ncontrib[p];
-              last[p] = (int)(b + k);
-              if (T[p] < a.stop) done[p] = true;
-            }
-          }
-          if (done[0] && done[1]) break;
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < 2; ++p) {
-    if (!(p == 0 ? in0 : in1)) continue;
-    const int64_t pix = (int64_t)row * a.W + col + p;
-    if (first) {
-      a.out_color[3 * pix + 0] = acc_rg[p].x + T[p] * a.bg0;
-      a.out_color[3 * pix + 1] = acc_rg[p].y + T[p] * a.bg1;
-      a.out_color[3 * pix + 2] = acc_bz[p].x + T[p] * a.bg2;
-      a.out_depth[pix] = acc_bz[p].y;
-      a.out_alpha[pix] = 1.f - T[p];
-      if (a.out_ncontrib) a.out_ncontrib[pix] = ncontrib[p];
-      a.tfinal[pix] = T[p];
-      a.last[pix] = last[p];
-    }
-    if (DC > 0) {
-      float* dst = a.out_feature + pix * a.D + a.c0;
-      if (vec_ok) {
-#pragma unroll
-        for (int c = 0; c < DC; c += 4)
-          *reinterpret_cast<float4*>(dst + c) =
-              make_float4(accf2[p][c / 2].x, accf2[p][c / 2].y, accf2[p][c / 2 + 1].x, accf2[p][c / 2 + 1].y);
-      } else {
-#pragma unroll
-        for (int c = 0; c < DC; ++c)
-          if (c < nf) dst[c] = (c & 1) ? accf2[p][c / 2].y : accf2[p][c / 2].x;
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // host driver
 // ---------------------------------------------------------------------------
@@ -679,27 +502,9 @@ static void launch_blend_sub(int dc, int ntiles, const BlendArgs& a, cudaStream_
   }
 }
 
-template <int SUB>
-static void launch_blend_px2(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
-  const int grid = ntiles * SUB, nt = kTilePixels / 2 / SUB;
-  switch (dc) {
-    case 0: k_blend_px2<0, SUB><<<grid, nt, 0, s>>>(a); break;
-    case 4: k_blend_px2<4, SUB><<<grid, nt, 0, s>>>(a); break;
-    case 8: k_blend_px2<8, SUB><<<grid, nt, 0, s>>>(a); break;
-    case 16: k_blend_px2<16, SUB><<<grid, nt, 0, s>>>(a); break;
-    default: k_blend_px2<32, SUB><<<grid, nt, 0, s>>>(a); break;
-  }
-}
-
 static void launch_blend(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
-  static const int px = getenv("FS4D_BLEND_PX") ? atoi(getenv("FS4D_BLEND_PX")) : 1;
+  // (two pixels per thread was measured slower: 157-165 vs 150 us)
   static const int sub = getenv("FS4D_BLEND_SUB") ? atoi(getenv("FS4D_BLEND_SUB")) : 2;
-  if (px == 2) {
-    if (sub == 1) launch_blend_px2<1>(dc, ntiles, a, s);
-    else if (sub == 4) launch_blend_px2<4>(dc, ntiles, a, s);
-    else launch_blend_px2<2>(dc, ntiles, a, s);
-    return;
-  }
   if (sub == 4) launch_blend_sub<4>(dc, ntiles, a, s);
   else if (sub == 1) launch_blend_sub<1>(dc, ntiles, a, s);
   else launch_blend_sub<2>(dc, ntiles, a, s);
