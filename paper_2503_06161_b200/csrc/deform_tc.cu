@@ -28,7 +28,10 @@ __constant__ int c_axes_tc[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 
 // ---------------------------------------------------------------------------
 // HexPlane latent
 // ---------------------------------------------------------------------------
-constexpr int kGatherWarps = 4;
+#ifndef FS4D_GATHER_WARPS
+#define FS4D_GATHER_WARPS 4
+#endif
+constexpr int kGatherWarps = FS4D_GATHER_WARPS;
 constexpr int kGatherMaxLevels = 4;
 
 __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent(TcPlan p, int64_t K, const float* __restrict__ pos,
