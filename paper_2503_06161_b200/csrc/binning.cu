@@ -222,11 +222,12 @@ __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long lo
                                                                 const uint64_t* __restrict__ toff,
                                                                 const uint32_t* __restrict__ tcnt, int ntiles,
                                                                 int64_t cap, const double* __restrict__ z64,
-                                                                uint32_t* __restrict__ pvals, uint2* __restrict__ ranges) {
+                                                                uint32_t* __restrict__ pvals, uint2* __restrict__ ranges,
+                                                                const int32_t* __restrict__ tperm) {
   extern __shared__ unsigned long long s_keys[];  // kSortSmemKeys exchange buffer (dynamic, 64 KB)
   __shared__ uint32_t wcnt[kTileSortWarps * 256];
   __shared__ uint32_t dbase[256];
-  const int tile = blockIdx.x;
+  const int tile = tperm ? tperm[blockIdx.x] : blockIdx.x;
   const uint64_t off = toff[tile];
   uint64_t end = off + tcnt[tile];
   if (end > (uint64_t)cap) end = (uint64_t)cap;  // overflow frame: status already raised
@@ -248,8 +249,10 @@ __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long lo
 constexpr int kTileScanThreads = 1024;
 __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan_check(const uint32_t* __restrict__ tcnt, int ntiles,
                                                                       uint64_t* __restrict__ toff, uint32_t* counters,
-                                                                      int64_t cap, int32_t* status) {
+                                                                      int64_t cap, int32_t* status,
+                                                                      int32_t* __restrict__ tperm) {
   __shared__ uint64_t wsum[kTileScanThreads / 32];
+  __shared__ uint32_t bcnt[33], bcur[33];
   const int per = (ntiles + kTileScanThreads - 1) / kTileScanThreads;
   const int b0 = threadIdx.x * per;
   uint64_t local = 0;
@@ -282,6 +285,26 @@ __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan_check(const uint
       toff[b0 + q] = run;
       run += tcnt[b0 + q];
     }
+  // launch order for the per-tile kernels: tiles by decreasing count (log2
+  // buckets, arbitrary order inside a bucket) so the longest tiles start in
+  // the first wave instead of the tail -- the order never affects results
+  if (tperm) {
+    if (threadIdx.x < 33) bcnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int q = 0; q < per; ++q)
+      if (b0 + q < ntiles) atomicAdd(&bcnt[32 - __clz(tcnt[b0 + q])], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t r = 0;
+      for (int b = 32; b >= 0; --b) {
+        bcur[b] = r;
+        r += bcnt[b];
+      }
+    }
+    __syncthreads();
+    for (int q = 0; q < per; ++q)
+      if (b0 + q < ntiles) tperm[atomicAdd(&bcur[32 - __clz(tcnt[b0 + q])], 1u)] = b0 + q;
+  }
   if (threadIdx.x == kTileScanThreads - 1) {
     const uint64_t total = run;
     *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64) = total;
@@ -316,7 +339,8 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
   // tcnt / tcur / ranges were zeroed and tcnt filled by k_preprocess's fused histogram
   const unsigned gb = (unsigned)ceil_div(K > 0 ? K : 1, 256);
   if (L.ntiles <= 64 * kTileScanThreads) {
-    k_tile_scan_check<<<1, kTileScanThreads, 0, s>>>(tcnt, L.ntiles, toff, counters, L.cap, status);
+    k_tile_scan_check<<<1, kTileScanThreads, 0, s>>>(tcnt, L.ntiles, toff, counters, L.cap, status,
+                                                      at<int32_t>(ws, L.tperm));
   } else {
     exclusive_scan_u32_to_u64(tcnt, toff, L.ntiles, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64),
                               at<void>(ws, L.scratch), s);
@@ -332,7 +356,10 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
   if (L.ntiles > 0)
     k_tile_sort<<<L.ntiles, kTileSortThreads, kSortSmemKeys * 8, s>>>(pkey, toff, tcnt, L.ntiles, L.cap, z64,
                                                                      at<uint32_t>(ws, L.pvals0),
-                                                                     at<uint2>(ws, L.ranges));
+                                                                     at<uint2>(ws, L.ranges),
+                                                                     L.ntiles <= 64 * kTileScanThreads
+                                                                         ? at<int32_t>(ws, L.tperm)
+                                                                         : nullptr);
 }
 
 }  // namespace fs4d

@@ -18,6 +18,7 @@ struct BwdArgs {
   float alpha_cap, alpha_skip, stop;
   float bg0, bg1, bg2;
   const uint2* ranges;
+  const int32_t* tperm;  // tiles by decreasing pair count (from the forward record), or null
   const uint32_t* pvals;
   const float2* xy;
   const float4* conic_o;
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
   __shared__ __align__(16) float s_f[DC > 0 ? B * DC : 1];
   __shared__ int s_maxlast;
 
-  const int tile = blockIdx.x;
+  const int tile = a.tperm ? a.tperm[blockIdx.x] : blockIdx.x;
   const int tx = tile % a.ntx, ty = tile / a.ntx;
   const int col = tx * kTile + (threadIdx.x & (kTile - 1));
   const int row = ty * kTile + (threadIdx.x / kTile);
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
   __shared__ __align__(16) float s_f[DC > 0 ? B * DC : 1];
   __shared__ int s_maxlast;
 
-  const int tile = blockIdx.x;
+  const int tile = a.tperm ? a.tperm[blockIdx.x] : blockIdx.x;
   const int tx = tile % a.ntx, ty = tile / a.ntx;
   const int col = tx * kTile + (threadIdx.x & (kTile - 1));
   const int row0 = ty * kTile + (threadIdx.x / kTile) * PX;
@@ -666,6 +667,7 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   b.bg1 = (float)cfg.background[1];
   b.bg2 = (float)cfg.background[2];
   b.ranges = at<uint2>(ws, L.ranges);
+  b.tperm = L.ntiles <= 65536 ? at<int32_t>(ws, L.tperm) : nullptr;
   b.pvals = at<uint32_t>(ws, L.pvals0);
   b.xy = at<float2>(ws, L.xy);
   b.conic_o = at<float4>(ws, L.conic_o);

@@ -45,7 +45,7 @@ struct RenderLayout {
   // keys/values (the global order is only materialised for export/backward)
   size_t xy, conic_o, pix_rect, tile_rect, rgbz, cov_r, z64, dkeys0, dkeys1, dvals0, dvals1, rank_of, clamp_mask;
   // tiles: counts, append cursors, segment offsets, [start, end) ranges
-  size_t tcnt, tcur, toff64, ranges;
+  size_t tcnt, tcur, toff64, ranges, tperm;
   // pairs: 64-bit (depth bits, source index) keys and the sorted source indices
   size_t pkey64, pvals0;
   // pixels
@@ -137,6 +137,7 @@ inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
   L.tcur = take(nt * 4);
   L.toff64 = take(nt * 8);
   L.ranges = take(nt * 8);
+  L.tperm = take(nt * 4);  // tiles by decreasing pair count (CTA launch order)
   L.pkey64 = take(cap * 8);
   L.pvals0 = take(cap * 4);
   L.tfinal = take(npix * 4);

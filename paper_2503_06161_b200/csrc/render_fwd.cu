@@ -258,6 +258,7 @@ struct BlendArgs {
   float alpha_cap, alpha_skip, stop;
   float bg0, bg1, bg2;
   const uint2* ranges;
+  const int32_t* tperm;  // tiles by decreasing pair count (launch order), or null
   const uint32_t* pvals;
   const float2* xy;
   const float4* conic_o;
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   // per-warp ballot masks of the staged batch (shared, not a local array)
   __shared__ unsigned s_mask[NT / 32][NT / 32];
 
-  const int tile = blockIdx.x / SUB, sub = blockIdx.x % SUB;
+  const int tile = a.tperm ? a.tperm[blockIdx.x / SUB] : blockIdx.x / SUB, sub = blockIdx.x % SUB;
   const int tx = tile % a.ntx, ty = tile / a.ntx;
   const int row0 = ty * kTile + sub * (kTile / SUB);
   const int col = tx * kTile + (threadIdx.x & (kTile - 1));
@@ -574,6 +575,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   b.bg1 = (float)cfg.background[1];
   b.bg2 = (float)cfg.background[2];
   b.ranges = at<uint2>(ws, L.ranges);
+  b.tperm = L.ntiles <= 65536 ? at<int32_t>(ws, L.tperm) : nullptr;  // written by k_tile_scan_check
   b.pvals = at<uint32_t>(ws, L.pvals0);
   b.xy = p.xy;
   b.conic_o = p.conic_o;
