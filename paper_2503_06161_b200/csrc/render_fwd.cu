@@ -45,7 +45,7 @@ __device__ __forceinline__ double sigmoid_d(double x) {
 
 // One Gaussian of k_preprocess; returns its inclusive tile rectangle
 // ((0, -1, 0, -1) when culled / out of range).
-__device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i) {
+__device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i, const float* __restrict__ sh_row) {
   if (i >= a.c.K) return make_int4(0, -1, 0, -1);
   a.dvals[i] = (uint32_t)i;
   a.dkeys[i] = 0xFFFFFFFFu;  // culled sentinel sorts last
@@ -70,12 +70,19 @@ __device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i) {
   {
     const float* F = a.c.features + (int64_t)a.c.D * i;
     bool fb = false;
-    for (int k = 0; k < a.c.D; ++k) fb |= !isfinite(F[k]);
+    if ((a.c.D & 3) == 0 && (reinterpret_cast<uintptr_t>(a.c.features) & 15) == 0) {
+      for (int k = 0; k < a.c.D; k += 4) {  // one 16 B load per 4 channels
+        const float4 f = __ldg(reinterpret_cast<const float4*>(F + k));
+        fb |= !(isfinite(f.x) && isfinite(f.y) && isfinite(f.z) && isfinite(f.w));
+      }
+    } else {
+      for (int k = 0; k < a.c.D; ++k) fb |= !isfinite(F[k]);
+    }
     if (fb) { flag_bad_field(a.status, FS4D_FIELD_FEATURES, i); bad = true; }
   }
   const int n_sh = (a.c.sh_degree + 1) * (a.c.sh_degree + 1) - 1;
   if (n_sh > 0 && a.c.sh_rest) {
-    const float* S = a.c.sh_rest + (int64_t)n_sh * 3 * i;
+    const float* S = sh_row;  // this Gaussian's SH row, staged in shared memory by its warp
     bool sb = false;
     for (int k = 0; k < n_sh * 3; ++k) sb |= !isfinite(S[k]);
     if (sb) { flag_bad_field(a.status, FS4D_FIELD_SH, i); bad = true; }
@@ -168,7 +175,7 @@ __device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i) {
     dn = dn > 0 ? dn : 1.0;
     double Yb[15];
     int nb = sh_basis<double>(a.c.sh_degree, dx / dn, dy / dn, dz / dn, Yb, nullptr);
-    const float* S = a.c.sh_rest + (int64_t)n_sh * 3 * i;
+    const float* S = sh_row;
     for (int k = 0; k < nb; ++k) {
       col[0] += Yb[k] * S[3 * k + 0];
       col[1] += Yb[k] * S[3 * k + 1];
@@ -207,13 +214,35 @@ __device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i) {
 // Projection of every Gaussian (preprocess_one) fused with the per-tile pair
 // histogram bin_tiles needs (rasterizer.py:188-207): block-aggregated in
 // shared memory, one global atomic per (block, touched tile).
+// The warp's 32 SH rows ([K, n_sh, 3], 180 B each at SH3) are copied into
+// shared memory with coalesced 16 B loads first (a thread reading its own
+// row 180 B apart from its neighbours' was the kernel's load-issue cost).
 __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
+  extern __shared__ float4 s_sh4[];  // [8 warps][32 rows * n_sh * 3 floats]
   __shared__ uint32_t h[kHistTilesSmem];
   const bool smem = a.ntx * a.nty <= kHistTilesSmem;
   if (smem)
     for (int b = threadIdx.x; b < a.ntx * a.nty; b += blockDim.x) h[b] = 0;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rowf = ((a.c.sh_degree + 1) * (a.c.sh_degree + 1) - 1) * 3;
+  float* wsh = reinterpret_cast<float*>(s_sh4) + warp * 32 * rowf;
+  if (rowf > 0 && a.c.sh_rest) {
+    const int64_t g0 = i - lane;
+    const int64_t nrows = min((int64_t)32, a.c.K - g0);
+    const float* src = a.c.sh_rest + g0 * rowf;
+    const int64_t nf = nrows * rowf;
+    if (nrows == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      // 32 rows of any width are a multiple of 16 B in total
+      for (int e = lane; e < nf / 4; e += 32)
+        reinterpret_cast<float4*>(wsh)[e] = __ldg(reinterpret_cast<const float4*>(src) + e);
+      for (int e = (int)(nf / 4) * 4 + lane; e < nf; e += 32) wsh[e] = src[e];
+    } else {
+      for (int e = lane; e < nf; e += 32) wsh[e] = src[e];
+    }
+  }
   __syncthreads();
-  const int4 t = preprocess_one(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int4 t = preprocess_one(a, i, wsh + lane * rowf);
   for (int ty = t.z; ty <= t.w; ++ty)
     for (int tx = t.x; tx <= t.y; ++tx) {
       const int b = ty * a.ntx + tx;
@@ -553,7 +582,13 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   p.status = status;
   {
     StageTimer st(FS4D_STAGE_PREPROCESS, s);
-    if (K > 0) k_preprocess<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(p);
+    const size_t sh_smem = (size_t)8 * 32 * (((snap.sh_degree + 1) * (snap.sh_degree + 1) - 1) * 3) * 4;
+    static size_t sh_attr = 0;
+    if (sh_smem > sh_attr) {
+      cudaFuncSetAttribute(k_preprocess, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_smem);
+      sh_attr = sh_smem;
+    }
+    if (K > 0) k_preprocess<<<(unsigned)ceil_div(K, 256), 256, sh_smem, s>>>(p);
   }
 
   // tile binning + per-tile depth order (no global sort on the frame path)
