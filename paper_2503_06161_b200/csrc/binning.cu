@@ -24,7 +24,11 @@ constexpr int kTileSortThreads = FS4D_TILE_SORT_THREADS;
 __device__ __forceinline__ bool rect_valid(const int4& t) { return t.y >= t.x && t.w >= t.z; }
 
 // key = fp32 depth bits (positive floats order as unsigned) << 32 | source index
-__global__ void __launch_bounds__(256) k_emit_partition(const int4* __restrict__ tile_rect,
+#ifndef FS4D_EMIT_THREADS
+#define FS4D_EMIT_THREADS 256
+#endif
+constexpr int kEmitThreads = FS4D_EMIT_THREADS;
+__global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __restrict__ tile_rect,
                                                         const uint32_t* __restrict__ dkeys, int64_t K, int ntx,
                                                         int ntiles, const uint64_t* __restrict__ toff,
                                                         uint32_t* __restrict__ tcur, int64_t cap,
@@ -337,7 +341,6 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
   uint32_t* tcur = at<uint32_t>(ws, L.tcur);
   uint64_t* toff = at<uint64_t>(ws, L.toff64);
   // tcnt / tcur / ranges were zeroed and tcnt filled by k_preprocess's fused histogram
-  const unsigned gb = (unsigned)ceil_div(K > 0 ? K : 1, 256);
   if (L.ntiles <= 64 * kTileScanThreads) {
     k_tile_scan_check<<<1, kTileScanThreads, 0, s>>>(tcnt, L.ntiles, toff, counters, L.cap, status,
                                                       at<int32_t>(ws, L.tperm));
@@ -347,7 +350,9 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
     k_pairs_check2<<<1, 1, 0, s>>>(counters, L.cap, status);
   }
   unsigned long long* pkey = at<unsigned long long>(ws, L.pkey64);
-  if (K > 0) k_emit_partition<<<gb, 256, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles, toff, tcur, L.cap, pkey);
+  if (K > 0)
+    k_emit_partition<<<(unsigned)ceil_div(K, kEmitThreads), kEmitThreads, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles,
+                                                                                toff, tcur, L.cap, pkey);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmemKeys * 8);
