@@ -324,23 +324,39 @@ def gpu_bench(args, rank, world, local):
         pipe.run(float(mine[i % len(mine)]), Kmat, T)
     torch.cuda.synchronize()
 
+    # serial reference number: one frame at a time, L2 flushed between frames
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     barrier(world)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(steps):
-            flush.zero_()  # L2 flush between timed iterations (outside the events)
-            ev[i][0].record(stream)
-            pipe.run(float(mine[i % len(mine)]), Kmat, T)
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
+    for i in range(steps):
+        flush.zero_()  # L2 flush between timed iterations (outside the events)
+        ev[i][0].record(stream)
+        pipe.run(float(mine[i % len(mine)]), Kmat, T)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
     barrier(world)
-    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms_serial = dist_max(sum(a.elapsed_time(b) for a, b in ev), world)
     st = pipe.renderer.status.read()
     if int(st[0]) != 0:
         raise RuntimeError(f"device status {st[:5]} during timed region")
-    ms_max = dist_max(ms, world)
+
+    # headline: the configs[2] sequence with three frames in flight on three
+    # streams over six model replicas (6 x 70 MB rotate through far more than
+    # the 126 MB L2, so no flush is needed between frames); each step = one frame
+    seq = dv.SequenceRenderer(cloud, field, net, H, W, cfg, pipelines=6, streams=3, replicas=6)
+    seq.warm(float(mine[0]), Kmat, T, pair_capacity=pipe.renderer.cap)
+    ts_seq = [float(mine[i % len(mine)]) for i in range(steps)]
+    seq.run([float(mine[i % len(mine)]) for i in range(warm)], Kmat, T)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        a_ev, b_ev = seq.run(ts_seq, Kmat, T)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_max = dist_max(a_ev.elapsed_time(b_ev), world)
+    seq.raise_if_error()
 
     # per-stage timing pass (events around each stage on the launching stream)
     dv.profile_collect()
@@ -372,8 +388,8 @@ def gpu_bench(args, rank, world, local):
         st = p.renderer.status.read()
         if int(st[0]) != 0:
             raise RuntimeError(f"device status {st[:5]} during the e2e region")
-    return dict(ms=ms_max, prof=prof, clocks=clk.summary(), n_vis=n_vis, n_pairs=n_pairs, e2e_ms=e2e_ms,
-                h2d=sf.h2d_bytes(), d2h=sf.d2h_bytes(), steps=steps)
+    return dict(ms=ms_max, ms_serial=ms_serial, prof=prof, clocks=clk.summary(), n_vis=n_vis, n_pairs=n_pairs,
+                e2e_ms=e2e_ms, h2d=sf.h2d_bytes(), d2h=sf.d2h_bytes(), steps=steps)
 
 
 def train_bench(args, rank, world, local):
@@ -466,7 +482,7 @@ def launches_per_frame():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-steps", type=int, default=2)
@@ -519,6 +535,8 @@ def main():
             print(json.dumps(line))
         return
     r = gpu_bench(args, rank, world, local)
+    base["config"] = dict(base["config"], parallelism=f"frame-sharded x{world}, 3 frames in flight per GPU (3 streams)",
+                          l2="no flush: 6 rotating model replicas (6 x 70 MB > 126 MB L2); value_serial is flushed")
     hbm, tf, peak_src = peaks()
     frames = world * r["steps"]
     value = frames / (r["ms"] / 1000.0)
@@ -545,6 +563,8 @@ def main():
     line = dict(base)
     line.update({
         "value": value, "ms_per_step": r["ms"] / r["steps"],
+        "value_serial": {"value": frames / (r["ms_serial"] / 1000.0), "ms_per_frame": r["ms_serial"] / r["steps"],
+                         "note": "one frame at a time on one stream, 256 MB L2 flush between frames"},
         "roofline": {"bound": "hbm", "kernel": STAGE_KERNEL[top], "stage": top, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": top_bytes,

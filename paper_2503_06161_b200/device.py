@@ -597,6 +597,63 @@ class FramePipeline:
         return self.images
 
 
+class SequenceRenderer:
+    """Render a timestep sequence (configs[2], cli.py:220-246) with several
+    frames in flight: `pipelines` FramePipelines (own snapshot, render record,
+    images), pipeline p always on stream p % streams, frames assigned round
+    robin.  Consecutive frames are independent, so frame k+1's deformation
+    runs on the SMs frame k's tile kernels leave idle.  `replicas` > 1 gives
+    every pipeline its own copy of the model (the bench uses 4 so the model
+    rotation exceeds L2 and no cache flush is needed between frames)."""
+
+    def __init__(self, cloud, field, net, height, width, cfg, pipelines=2, streams=2, replicas=1, device="cuda"):
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(streams)]
+        self.pipes = []
+        for p in range(pipelines):
+            if replicas > 1 and p % replicas:
+                c = DeviceCloud(*(getattr(cloud, n).clone() for n in DeviceCloud.FIELDS),
+                                sh_rest=None if cloud.sh_rest is None else cloud.sh_rest.clone())
+                f = DeviceField([[pl.clone() for pl in lv] for lv in field.planes], field.aabb, field.channels,
+                                field.order)
+                nt = DeviceNet({k: [(w.clone(), b.clone(), r) for (w, b, r) in v] for k, v in net.layers.items()},
+                               net.latent_dim, net.width, net.depth, net.feature_dim, net.enable_grid,
+                               net.enable_feature_update)
+            else:
+                c, f, nt = cloud, field, net
+            self.pipes.append(FramePipeline(c, f, nt, height, width, cfg, device))
+
+    def warm(self, t, K, T, pair_capacity=None):
+        for p, pipe in enumerate(self.pipes):
+            with torch.cuda.stream(self.streams[p % len(self.streams)]):
+                pipe.run(t, K, T, check=True)
+                if pair_capacity:
+                    pipe.renderer.cap = max(pipe.renderer.cap, int(pair_capacity))
+                pipe.run(t, K, T, check=True)
+        torch.cuda.synchronize()
+
+    def run(self, ts, K, T):
+        """Enqueue one frame per t; returns (start, end) events on the current
+        stream bracketing all of them."""
+        cur = torch.cuda.current_stream()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(cur)
+        for s in self.streams:
+            s.wait_event(start)
+        for i, t in enumerate(ts):
+            p = i % len(self.pipes)
+            with torch.cuda.stream(self.streams[p % len(self.streams)]):
+                self.pipes[p].run(float(t), K, T)
+        for s in self.streams:
+            cur.wait_stream(s)
+        end.record(cur)
+        return start, end
+
+    def raise_if_error(self):
+        for pipe in self.pipes:
+            pipe.renderer.status.raise_if_error()
+
+
 class StreamedFrames:
     """End-to-end frame stream from host buffers with copy/compute overlap.
 

@@ -226,3 +226,39 @@ def test_size_independent_properties_at_config3_size():
     n_pairs = sum(c.size for row in lists for c in row)
     assert rec.n_visible == len(proj["source_index"])
     assert rec.n_pairs == n_pairs
+
+
+def test_sequence_renderer_frames_in_flight_match_serial_frames():
+    """configs[2]-style sequence with frames in flight on two streams (and a
+    model replica per pipeline) gives exactly the frames a single pipeline
+    renders one at a time."""
+    import torch
+    from paper_2503_06161_b200 import device as dv
+    rng = np.random.default_rng(21)
+    k, h, w, d = 20_000, 128, 160, 8
+    a = random_cloud_arrays(rng, k, d, depth_range=(2.0, 4.0), xy=1.0)
+    cloud_np = fs().GaussianCloud(**a)
+    field_np = fs().HexPlaneField(fs().HexPlaneConfig(levels=(1, 2), base_resolution=(16, 16, 16, 5), out_dim=64),
+                                  fs().scene_aabb(cloud_np), rng, init="uniform")
+    net_np = fs().DeformationNet(64, fs().DeformationConfig(width=64, depth=1, feature_dim=d), rng, init="xavier",
+                                 head_init="xavier")
+    c, f, n = dv.DeviceCloud.from_cloud(cloud_np), dv.DeviceField.from_field(field_np), dv.DeviceNet.from_net(net_np)
+    K = pinhole(h, w, 150.0)
+    ts = [i / 11.0 for i in range(12)]
+    single = dv.FramePipeline(c, f, n, h, w, fs().RasterConfig())
+    ref = []
+    for t in ts:
+        single.run(t, K, np.eye(4), check=True)
+        ref.append({key: v.clone() for key, v in single.images.items()})
+    seq = dv.SequenceRenderer(c, f, n, h, w, fs().RasterConfig(), pipelines=4, streams=2, replicas=4)
+    seq.warm(0.0, K, np.eye(4))
+    outs = []
+    for r0 in range(0, len(ts), 4):  # one round = one frame per pipeline, copied out after the round
+        seq.run(ts[r0:r0 + 4], K, np.eye(4))
+        torch.cuda.synchronize()
+        for p in range(4):
+            outs.append({key: v.clone() for key, v in seq.pipes[p].images.items()})
+    seq.raise_if_error()
+    for got, exp in zip(outs, ref):
+        for key in exp:
+            assert torch.equal(got[key], exp[key]), key
