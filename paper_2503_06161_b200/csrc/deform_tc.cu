@@ -1038,7 +1038,8 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   a.cache = cache;
   const int smem = ((p.fwd_bytes + 1023) & ~1023) + kTcRows * 64 * 4 * (fused ? 2 : 1) + kTcRows * 128 * 4;
   const int64_t ntiles = ceil_div(K, kTcRows);
-  const int grid = (int)(ntiles < kNumSMs ? ntiles : kNumSMs);
+  static const int grid_cap = getenv("FS4D_MLP_GRID") ? atoi(getenv("FS4D_MLP_GRID")) : kNumSMs;
+  const int grid = (int)(ntiles < grid_cap ? ntiles : grid_cap);
   if (fused) {
     cudaFuncSetAttribute(k_mlp_tc_ws<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mlp_tc_ws<true, false><<<grid, kTcFusedThreads, smem, s>>>(a);
