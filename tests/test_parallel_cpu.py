@@ -84,3 +84,33 @@ def test_flat_grad_allreduce_world2_gloo():
             np.testing.assert_allclose(v, (1 + 2) / 2.0)   # mean of the two ranks' contributions
     all_ts = res[0][2] + res[1][2]
     np.testing.assert_allclose(all_ts, sequence_timesteps(156))
+
+
+def _bench_worker(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        import bench
+        # every rank times its own frames; the job time is the slowest rank's
+        ms = bench.dist_max(10.0 + 5.0 * rank, world)
+        bench.barrier(world)
+        lo, hi = shard_range(156, world, rank)
+        q.put((rank, ms, hi - lo))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_max_over_ranks_world2_gloo():
+    """bench.py's N>1 plumbing: the timed region is the max over ranks and the
+    156 configs[2] timesteps split 78 / 78."""
+    world = 2
+    port = 29500 + (os.getpid() % 1000) + 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[1] for r in res] == [15.0, 15.0]
+    assert sum(r[2] for r in res) == 156 and res[0][2] == 78
