@@ -417,8 +417,11 @@ __device__ __forceinline__ double sigmoid_db(double x) {
 
 // One thread per visible Gaussian (depth rank r).  fp64 throughout, mirroring
 // rasterizer.py:395-451 and gaussians.py:156-218.
-__global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// One visible Gaussian (depth rank r) or, in source-order mode, row r.
+// sh_in / sh_out: this Gaussian's SH row and SH-gradient row -- global
+// memory in depth-order mode, the warp's shared-memory staging rows in
+// source-order mode (the kernel moves them with coalesced loads / stores).
+__device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t r, const float* sh_in, float* sh_out) {
   int64_t i;
   if (a.order) {
     if (r >= (int64_t)a.counters[CNT_VISIBLE]) return;
@@ -433,8 +436,8 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
       a.g.opacity_logits[i] = 0.f;
       for (int c = 0; c < a.c.D; ++c) a.g.features[(int64_t)a.c.D * i + c] = 0.f;
       const int nsh = ((a.sh_degree + 1) * (a.sh_degree + 1) - 1) * 3;
-      if (a.g.sh_rest)
-        for (int c = 0; c < nsh; ++c) a.g.sh_rest[(int64_t)nsh * i + c] = 0.f;
+      if (sh_out)
+        for (int c = 0; c < nsh; ++c) sh_out[c] = 0.f;
       return;
     }
   }
@@ -564,8 +567,8 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
     const double ux = vx / dn, uy = vy / dn, uz = vz / dn;
     double Yb[15], dY[15][3];
     int nb = sh_basis<double>(a.sh_degree, ux, uy, uz, Yb, dY);
-    const float* S = a.c.sh_rest + (int64_t)n_sh * 3 * i;
-    float* GS = a.g.sh_rest + (int64_t)n_sh * 3 * i;
+    const float* S = sh_in;
+    float* GS = sh_out;
     double ddir[3] = {0, 0, 0};
     for (int k = 0; k < nb; ++k) {
       double gk = 0;
@@ -594,6 +597,42 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
   for (int c = 0; c < a.D; ++c) a.g.features[(int64_t)a.D * i + c] = acc[10 + c];
   if (a.vs_index) a.vs_index[r] = (int32_t)i;
   if (a.vs_norm) a.vs_norm[r] = (float)hypot(dmx * 0.5 * a.W, dmy * 0.5 * a.H);
+}
+
+__global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
+  extern __shared__ float s_sh[];  // source-order mode: [4 warps][2][32 rows * n_sh * 3]
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int rowf = ((a.sh_degree + 1) * (a.sh_degree + 1) - 1) * 3;
+  const bool staged = !a.order && rowf > 0 && a.c.sh_rest && a.g.sh_rest;
+  if (!staged) {
+    const int64_t i = a.order ? (r < (int64_t)a.counters[CNT_VISIBLE] ? a.order[r] : 0) : r;
+    preprocess_bwd_one(a, r, rowf > 0 && a.c.sh_rest ? a.c.sh_rest + (int64_t)rowf * i : nullptr,
+                       rowf > 0 && a.g.sh_rest ? a.g.sh_rest + (int64_t)rowf * i : nullptr);
+    return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* win = s_sh + warp * 2 * 32 * rowf;
+  float* wout = win + 32 * rowf;
+  const int64_t g0 = r - lane;
+  const int64_t nrows = g0 < a.c.K ? min((int64_t)32, a.c.K - g0) : 0;
+  const int64_t nf = nrows * rowf;
+  const float* src = a.c.sh_rest + g0 * rowf;
+  float* dst = a.g.sh_rest + g0 * rowf;
+  const bool vec = nrows == 32 && ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (vec) {
+    for (int e = lane; e < nf / 4; e += 32)
+      reinterpret_cast<float4*>(win)[e] = __ldg(reinterpret_cast<const float4*>(src) + e);
+  } else {
+    for (int e = lane; e < nf; e += 32) win[e] = src[e];
+  }
+  __syncwarp();
+  preprocess_bwd_one(a, r, win + lane * rowf, wout + lane * rowf);
+  __syncwarp();
+  if (vec) {
+    for (int e = lane; e < nf / 4; e += 32) reinterpret_cast<float4*>(dst)[e] = reinterpret_cast<const float4*>(wout)[e];
+  } else {
+    for (int e = lane; e < nf; e += 32) dst[e] = wout[e];
+  }
 }
 
 static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t s) {
@@ -712,7 +751,13 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   p.vs_norm = vs_norm;
   if (K > 0) {
     StageTimer st(FS4D_STAGE_PREPROCESS_BWD, s);
-    k_preprocess_bwd<<<(unsigned)ceil_div(K, 128), 128, 0, s>>>(p);
+    const size_t sh_smem = p.order ? 0 : (size_t)4 * 2 * 32 * (size_t)(n_sh * 3) * 4;
+    static size_t sh_attr = 0;
+    if (sh_smem > sh_attr) {
+      cudaFuncSetAttribute(k_preprocess_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_smem);
+      sh_attr = sh_smem;
+    }
+    k_preprocess_bwd<<<(unsigned)ceil_div(K, 128), 128, sh_smem, s>>>(p);
   }
   return check_launch("render_bwd");
 }
