@@ -550,14 +550,15 @@ def main():
     top = max(single, key=single.get)
     top_bytes = stage_bytes(top, r["n_vis"], r["n_pairs"])
     achieved = top_bytes / (stage_ms[top] / 1000.0) / 1e9
-    traffic, traffic_src = None, None
+    traffic, traffic_src, utilisation = None, None, None
     try:
         with open(TRAFFIC_JSON) as fh:
             t = json.load(fh)[STAGE_KERNEL[top]]
         traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
         traffic_src = f"{os.path.basename(TRAFFIC_JSON)}: ncu --set full of {t['kernel'].split('(')[0]} (one launch)"
+        utilisation = t.get("utilisation")
     except Exception:
-        pass
+        utilisation = None
     kernels = {s: {"ms": round(stage_ms[s], 4), "algorithmic_bytes": stage_bytes(s, r["n_vis"], r["n_pairs"]),
                    "achieved_gbs": stage_bytes(s, r["n_vis"], r["n_pairs"]) / (stage_ms[s] / 1000.0) / 1e9}
                for s in single}
@@ -569,7 +570,10 @@ def main():
         "roofline": {"bound": "hbm", "kernel": STAGE_KERNEL[top], "stage": top, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": top_bytes,
-                     "share_of_step": stage_ms[top] / frame_ms if frame_ms else None},
+                     "share_of_step": stage_ms[top] / frame_ms if frame_ms else None,
+                     # the kernel is issue/latency bound, not HBM bound: SM-side utilisation of the
+                     # same ncu capture (percent of B200 peak)
+                     "sm_utilisation_pct": utilisation},
         "kernels": kernels,
         "roofline_frame": {"bytes_per_frame": FRAME_BYTES,
                            "achieved_gbs": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9,

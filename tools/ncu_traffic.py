@@ -26,9 +26,17 @@ def one(path):
 
     name = v[h.index("Kernel Name")]
     base = name.split("(")[0].split("<")[0].replace("void ", "").replace("fs4d::", "").strip()
+    pct = {k: get(m) for k, m in (
+        ("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        ("fma_pipe_pct", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+        ("tensor_pipe_pct", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+        ("fp64_pipe_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+        ("sm_throughput_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+        ("mem_throughput_pct", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"),
+        ("warps_active_pct", "sm__warps_active.avg.pct_of_peak_sustained_active"))}
     return base, {"kernel": name[:100], "dram_read_bytes": get("dram__bytes_read.sum"),
                   "dram_write_bytes": get("dram__bytes_write.sum"), "duration_s": get("gpu__time_duration.sum"),
-                  "source": path.split("/")[-1]}
+                  "utilisation": pct, "source": path.split("/")[-1]}
 
 
 def main():
