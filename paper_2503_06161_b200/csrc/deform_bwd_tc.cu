@@ -512,7 +512,7 @@ __device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 |
 // fire-and-forget red.global.add.v4 into a per-CTA partial (no cross-CTA
 // contention; a shared-memory float atomic is a CAS loop on sm_100), reduced
 // by k_time_partials afterwards.
-__global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC32Args A) {
+__global__ void __launch_bounds__(kHexC32Warps * 32, 1) k_hexplane_bwd_c32(HexC32Args A) {
   const HexBwdArgs& a = A.h;
   const TcPlan& p = a.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -566,6 +566,18 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC3
       const int64_t k = g0 + j;
       const bool ok = k < a.K;
       float dco[3] = {0.f, 0.f, 0.f};
+      // issue this Gaussian's upstream latent gradient and position-gradient
+      // loads before the plane gathers so their latency overlaps them
+      float4 up_l[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+      float gpos_in = 0.f, cpos_in = 0.f;
+      if (ok) {
+        up_l[0] = __ldg(reinterpret_cast<const float4*>(a.dlat + k * 64 + ch));
+        up_l[1] = __ldg(reinterpret_cast<const float4*>(a.dlat + k * 64 + 32 + ch));
+        if ((lane & 7) < 3) {
+          gpos_in = a.g_pos[3 * k + (lane & 7)];
+          if (a.accumulate) cpos_in = a.cg_pos[3 * k + (lane & 7)];
+        }
+      }
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
         float4 s[6], da[6], db[6];
@@ -606,7 +618,7 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC3
                               (1.f - f0) * (c01.w - c00.w) + f0 * (c11.w - c10.w));
         }
         if (!ok) continue;
-        const float4 up = *reinterpret_cast<const float4*>(a.dlat + k * 64 + l * 32 + ch);
+        const float4 up = up_l[l];
         // product of the other five planes via prefix / suffix (hexplane.py:131-139)
         float4 pre[6], suf[6];
         pre[0] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -653,7 +665,7 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 2) k_hexplane_bwd_c32(HexC3
         const int q = lane & 7;
         const float dq = q == 0 ? dco[0] : (q == 1 ? dco[1] : dco[2]);
         const float d = ((ins >> q) & 1u) ? (float)((double)dq / p.span[q]) : 0.f;
-        a.cg_pos[3 * k + q] = (a.accumulate ? a.cg_pos[3 * k + q] : 0.f) + a.g_pos[3 * k + q] + d;
+        a.cg_pos[3 * k + q] = cpos_in + gpos_in + d;
       }
     }
   }
@@ -742,7 +754,7 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
     hc.tpart = wpart + (size_t)kNumSMs * kPartStride + 128;
     if (p.C == 32 && p.levels == 2 && tf <= kTimePartFloats && !getenv("FS4D_HEX_BWD_GENERIC")) {
       const int64_t nblk = ceil_div(ceil_div(K, 32), kHexC32Warps);
-      const int grid = (int)(nblk < kTimeParts ? nblk : kTimeParts);
+      const int grid = (int)(nblk < kNumSMs ? nblk : kNumSMs);  // one 256-thread CTA per SM (242 registers)
       cudaMemsetAsync(hc.tpart, 0, (size_t)grid * tf * 4, s);
       k_hexplane_bwd_c32<<<grid, kHexC32Warps * 32, 0, s>>>(hc);
       TimeReduceArgs tr;
