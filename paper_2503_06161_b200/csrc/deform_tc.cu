@@ -160,6 +160,9 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPla
   }
 }
 
+#ifndef PLANE_LD
+#define PLANE_LD __ldg
+#endif
 // Same gather, with the three time planes of each level read as 1-D lerps of
 // the per-frame time rows (k_pack_tc): 2 corner rows instead of 4 for half
 // of the planes, and those rows (72 KB at configs[1]) stay L1/L2-hot.  The
@@ -232,10 +235,10 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPl
           const float* pl = p.planes[l][q] + s_base[warp][l * 6 + q][j] + ch;
           const float w00 = (1.f - f.x) * (1.f - f.y), w10 = f.x * (1.f - f.y);
           const float w01 = (1.f - f.x) * f.y, w11 = f.x * f.y;
-          const float4 a = __ldg(reinterpret_cast<const float4*>(pl));
-          const float4 b = __ldg(reinterpret_cast<const float4*>(pl + 32));
-          const float4 c = __ldg(reinterpret_cast<const float4*>(pl + rs));
-          const float4 d = __ldg(reinterpret_cast<const float4*>(pl + rs + 32));
+          const float4 a = PLANE_LD(reinterpret_cast<const float4*>(pl));
+          const float4 b = PLANE_LD(reinterpret_cast<const float4*>(pl + 32));
+          const float4 c = PLANE_LD(reinterpret_cast<const float4*>(pl + rs));
+          const float4 d = PLANE_LD(reinterpret_cast<const float4*>(pl + rs + 32));
           prod.x *= w00 * a.x + w10 * c.x + w01 * b.x + w11 * d.x;
           prod.y *= w00 * a.y + w10 * c.y + w01 * b.y + w11 * d.y;
           prod.z *= w00 * a.z + w10 * c.z + w01 * b.z + w11 * d.z;
