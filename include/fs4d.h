@@ -384,7 +384,9 @@ typedef struct Fs4dDensityConfig {
 
 /* ViewspaceGradStats.add (gaussians.py:319-321): accum[idx[i]] += norms[i],
  * count[idx[i]] += 1 for i < n (n = min(n, *n_dev) when n_dev != NULL; the
- * indices of one render_backward are distinct).  accum / count are float64. */
+ * indices of one render_backward are distinct).  indices NULL: norms is the
+ * dense per-Gaussian form of fs4d_render_bwd ([K], negative = culled, skipped).
+ * accum / count are float64. */
 int fs4d_grad_stats_add(double* accum, double* count, const int32_t* indices, const float* norms, int64_t n,
                         const int32_t* n_dev, void* stream);
 
@@ -425,9 +427,10 @@ int fs4d_render_fwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam,
 
 /* render_backward: grads->{positions, rotations, log_scales, opacity_logits,
  * colors_raw, sh_rest, features} are fully written (zeros for culled rows).
- * viewspace_index / viewspace_norm get the first M entries (depth order); when
- * both are NULL the depth order is not materialised (no global sort) and the
- * rows are visited in source order. */
+ * viewspace_index / viewspace_norm get the first M entries (depth order).
+ * With viewspace_index NULL the depth order is not materialised (no global
+ * sort), rows are visited in source order, and a non-NULL viewspace_norm is
+ * written densely per Gaussian ([K], -1 for culled rows). */
 int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam,
                     const Fs4dRasterConfig* cfg, const Fs4dRecordInfo* info,
                     void* workspace, size_t workspace_bytes,

@@ -363,7 +363,7 @@ int fs4d_decoder_feature_loss(const float* rendered, int32_t hi, int32_t wi, int
 
 int fs4d_grad_stats_add(double* accum, double* count, const int32_t* indices, const float* norms, int64_t n,
                         const int32_t* n_dev, void* stream) {
-  if (n < 0 || (n > 0 && (!accum || !count || !indices || !norms))) return fail(FS4D_ERR_CONFIG, "bad stats arguments");
+  if (n < 0 || (n > 0 && (!accum || !count || !norms))) return fail(FS4D_ERR_CONFIG, "bad stats arguments");
   return stats_add(accum, count, indices, norms, n, n_dev, (cudaStream_t)stream);
 }
 
@@ -452,8 +452,7 @@ int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam, const Fs4d
   if ((rc = check_camera(cam))) return rc;
   if ((rc = check_record(info, snapshot, cam, cfg, workspace_bytes, workspace))) return rc;
   if (!upstream || !grads) return fail(FS4D_ERR_CONFIG, "null backward argument");
-  if (!viewspace_index != !viewspace_norm)
-    return fail(FS4D_ERR_CONFIG, "viewspace_index and viewspace_norm are both given or both NULL");
+  if (viewspace_index && !viewspace_norm) return fail(FS4D_ERR_CONFIG, "viewspace_index without viewspace_norm");
   if (grads->K != snapshot->K || grads->D != snapshot->D || grads->sh_degree != snapshot->sh_degree)
     return fail(FS4D_ERR_CONFIG, "gradient buffers do not match the snapshot");
   if (cfg->with_features && snapshot->D > 64)

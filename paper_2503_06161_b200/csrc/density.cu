@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(kT) k_stats_add(double* __restrict__ accum, do
                                                   int64_t n, const int32_t* __restrict__ n_dev) {
   const int64_t m = n_dev ? min((int64_t)*n_dev, n) : n;
   for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < m; i += (int64_t)gridDim.x * kT) {
-    const int32_t g = idx[i];
+    if (!idx && norms[i] < 0.f) continue;  // dense form: culled Gaussian
+    const int64_t g = idx ? (int64_t)idx[i] : i;
     accum[g] += (double)norms[i];
     count[g] += 1.0;
   }

@@ -438,6 +438,7 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
       const int nsh = ((a.sh_degree + 1) * (a.sh_degree + 1) - 1) * 3;
       if (sh_out)
         for (int c = 0; c < nsh; ++c) sh_out[c] = 0.f;
+      if (a.vs_norm) a.vs_norm[i] = -1.f;  // dense source-indexed norms: culled
       return;
     }
   }
@@ -596,7 +597,8 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
   a.g.opacity_logits[i] = (float)(dop * o * (1.0 - o));
   for (int c = 0; c < a.D; ++c) a.g.features[(int64_t)a.D * i + c] = acc[10 + c];
   if (a.vs_index) a.vs_index[r] = (int32_t)i;
-  if (a.vs_norm) a.vs_norm[r] = (float)hypot(dmx * 0.5 * a.W, dmy * 0.5 * a.H);
+  // depth-ordered: entry r of the visible list; source order: dense per Gaussian
+  if (a.vs_norm) a.vs_norm[a.order ? r : i] = (float)hypot(dmx * 0.5 * a.W, dmy * 0.5 * a.H);
 }
 
 __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
@@ -679,7 +681,7 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   // order ProjectedGaussians reports them in) and zero the culled rows up
   // front.  Not requested (training): source order, no global depth sort,
   // the kernel writes the culled rows' zeros itself.
-  const bool depth_ordered = vs_index || vs_norm;
+  const bool depth_ordered = vs_index != nullptr;
   const int n_sh = (snap.sh_degree + 1) * (snap.sh_degree + 1) - 1;
   if (depth_ordered) {
   // zero the outputs: culled rows keep zero gradients (rasterizer.py:432-441)

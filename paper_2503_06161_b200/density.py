@@ -60,6 +60,13 @@ class ViewspaceGradStats:
             np.add.at(self.accum, indices, norms)
             np.add.at(self.count, indices, 1.0)
 
+    def add_dense(self, norms):
+        """Accumulate render_backward's dense per-Gaussian norms (negative =
+        culled) -- the source-order form the training step produces."""
+        nrm = norms.to(torch.float32).contiguous()
+        N.check(N.load().fs4d_grad_stats_add(_p(self.accum), _p(self.count), None, _p(nrm), nrm.numel(), None,
+                                             _stream()))
+
     def averages(self):
         if isinstance(self.accum, torch.Tensor):
             return self.accum / torch.clamp(self.count, min=1.0)

@@ -448,14 +448,20 @@ class Renderer:
 
     def backward(self, cloud, K, T, height, width, cfg, rec, d_color=None, d_depth=None,
                  d_feature=None, d_alpha=None, grads=None, viewspace=True):
-        """render_backward on device.  viewspace=False skips the viewspace
-        outputs (and with them the global depth sort they are ordered by);
-        returns None for both then."""
+        """render_backward on device.  viewspace=True: depth-ordered
+        (index, norm) pairs like SnapshotGrads; False: none (and no global
+        depth sort); "dense": norms per Gaussian ([K], -1 for culled, no depth
+        sort) for ViewspaceGradStats.add_dense; a tensor: dense norms into it."""
         k, d, sh = len(cloud), cloud.feature_dim, cloud.sh_degree
         if grads is None:
             grads = DeviceCloud.empty(k, d, sh, self.device)
-        vs_index = torch.empty(max(k, 1), dtype=torch.int32, device=self.device) if viewspace else None
-        vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device) if viewspace else None
+        dense = isinstance(viewspace, torch.Tensor) or viewspace == "dense"
+        vs_index = torch.empty(max(k, 1), dtype=torch.int32, device=self.device) \
+            if (viewspace is True) else None
+        if isinstance(viewspace, torch.Tensor):
+            vs_norm = viewspace
+        else:
+            vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device) if viewspace else None
         cs, cam, rc, gs = cloud.struct(), camera_struct(K, T, height, width), raster_struct(cfg), grads.struct()
         up = N.ImageGrads()
         up.d_color, up.d_depth = _p(d_color), _p(d_depth)
@@ -464,6 +470,8 @@ class Renderer:
                                          ctypes.byref(rec.info), _p(rec.ws), rec.ws.numel(),
                                          ctypes.byref(up), ctypes.byref(gs), _p(vs_index),
                                          _p(vs_norm), None, _stream()))
+        if dense:
+            return grads, None, vs_norm
         return grads, vs_index, vs_norm
 
     def export_projected(self, rec):

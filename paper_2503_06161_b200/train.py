@@ -101,6 +101,8 @@ class TrainStep:
         self.optimizer = None
         self.schedules = None
         self.iteration = 0
+        self.stats = None      # ViewspaceGradStats on device when track_stats() is on
+        self.vs_norm = None
 
     def _bind(self, flat):
         """DeviceCloud / DeviceField / DeviceNet views into a flat buffer."""
@@ -198,7 +200,10 @@ class TrainStep:
                     self.d_feature.zero_()
             self.renderer.backward(self.snap, K, T, self.h, self.w, self.cfg, rec, d_color=self.d_color,
                                    d_depth=d_depth, d_feature=self.d_feature if dout else None,
-                                   grads=self.snap_grads, viewspace=False)
+                                   grads=self.snap_grads,
+                                   viewspace=self.vs_norm if self.stats is not None else False)
+            if self.stats is not None:  # training.py:514 grad_stats.add (dense, source order)
+                self.stats.add_dense(self.vs_norm)
             self.deformer.backward(self.cloud, field, self.net, t, self.snap_grads,
                                    cloud_grads=self.cloud_grads, net_grads=self.net_grads,
                                    plane_grads=self.plane_grads if self.net.enable_grid else None,
@@ -216,3 +221,75 @@ class TrainStep:
                 self.optimizer.check()
             self.iteration += 1
         return self.loss
+
+    # ------------------------------------------------------------------
+    # adaptive density control in the training loop (training.py:445-456)
+    # ------------------------------------------------------------------
+    def track_stats(self):
+        """Accumulate the view-space gradient statistics every step
+        (ViewspaceGradStats on device, reset by densify)."""
+        from .density import ViewspaceGradStats
+        k = len(self.cloud)
+        self.stats = ViewspaceGradStats.zeros(k, self.device)
+        self.vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device)
+        return self
+
+    def densify(self, cfg, extent, rng, prune_only=False):
+        """densify_and_prune / prune_only (gaussians.py:349-417) on the device
+        parameters: compacts every per-Gaussian parameter array and its Adam
+        moments in the reference's row order, keeps the network / plane /
+        decoder parameters, moments and every step count, rebuilds the flat
+        parameter / gradient / moment buffers for the new K and resets the
+        statistics.  Returns the reference's report dict."""
+        from .density import DeviceDensity, ViewspaceGradStats
+        from .parallel import PER_GAUSSIAN
+        if self.optimizer is None:
+            raise ValueError("attach_optimizer() first: density control remaps the Adam moments")
+        per = [n for n, _ in PER_GAUSSIAN if n in self.params.views]
+        old_specs, old_params, old_opt = self.specs, self.params, self.optimizer
+        extras = []
+        for n in per:
+            i = [sn for sn, _ in old_specs].index(n)
+            off, cnt = old_params.offsets[i], old_params.sizes[i]
+            shape = old_params.views[n].shape
+            extras += [old_opt.m[off:off + cnt].view(shape), old_opt.v[off:off + cnt].view(shape)]
+        stats = self.stats if self.stats is not None else ViewspaceGradStats.zeros(len(self.cloud), self.device)
+        out, new_stats, outs, rep = DeviceDensity(self.device).run(self.cloud, stats, cfg, extent, rng, prune_only,
+                                                                   extras)
+        k = len(out)
+        d, sh = out.feature_dim, out.sh_degree
+        field_specs = [(n, sh_) for n, sh_ in old_specs if n not in per]
+        new_specs = gradient_specs(k, d, sh, [], []) + field_specs
+        params = FlatGrads(new_specs, self.device)
+        opt = FlatAdam(new_specs, params.buffer, offsets=params.offsets)
+        moved = dict(zip([(n, t) for n in per for t in ("m", "v")], outs))
+        for i, (n, _) in enumerate(new_specs):
+            off, cnt = params.offsets[i], params.sizes[i]
+            if n in per:
+                src = getattr(out, n)
+                params.buffer[off:off + cnt].copy_(src.reshape(-1))
+                opt.m[off:off + cnt].copy_(moved[(n, "m")].reshape(-1))
+                opt.v[off:off + cnt].copy_(moved[(n, "v")].reshape(-1))
+            else:
+                j = [sn for sn, _ in old_specs].index(n)
+                o2, c2 = old_params.offsets[j], old_params.sizes[j]
+                params.buffer[off:off + cnt].copy_(old_params.buffer[o2:o2 + c2])
+                opt.m[off:off + cnt].copy_(old_opt.m[o2:o2 + c2])
+                opt.v[off:off + cnt].copy_(old_opt.v[o2:o2 + c2])
+        # step counts follow their arrays (AdamState per array, numerics.py:122-133)
+        old_steps = old_opt.steps.cpu().tolist()
+        name_to_step = {n: old_steps[i] for i, (n, _) in enumerate(old_specs)}
+        opt.steps.copy_(torch.tensor([name_to_step[n] for n, _ in new_specs], dtype=torch.int32))
+        self.specs, self.params, self.optimizer = new_specs, params, opt
+        self.cloud, self.field, self.net = self._bind(params)
+        if self.decoder is not None:
+            self.decoder = (params["decoder.weight"], params["decoder.bias"])
+        self.grads = FlatGrads(new_specs, self.device)
+        self.cloud_grads, self.plane_grads, self.net_grads = self._bind(self.grads)
+        self.snap = DeviceCloud.empty(k, d, 0, self.device)
+        self.snap_grads = DeviceCloud.empty(k, d, sh, self.device)
+        self.cache = None
+        if self.stats is not None:
+            self.stats = new_stats  # reset (densify) or compacted (prune_only), gaussians.py:397-415
+            self.vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device)
+        return rep

@@ -284,3 +284,79 @@ def test_checkpoint_round_trip_of_device_training_state(tmp_path):
     torch.cuda.synchronize()
     diff = (s1.params.buffer - s2.params.buffer).abs().max().item()
     assert diff < 1e-6, diff  # atomics in the backward: last-bit differences only
+
+
+def test_density_control_inside_the_training_step():
+    """TrainStep.track_stats + densify: the view-space statistics accumulate
+    on device every step, and densify compacts parameters and Adam moments in
+    the reference's row order (oracle density_control on the same pre-step
+    state), keeps the network / plane state, and the next step runs at the
+    new K."""
+    import torch
+    import paper_2503_06161_b200 as fs
+    from paper_2503_06161_b200 import device as dv
+    from paper_2503_06161_b200.density import DensityControlConfig
+    from paper_2503_06161_b200.numerics import LrSchedule
+    from paper_2503_06161_b200.train import TrainStep
+
+    rng = np.random.default_rng(11)
+    k, h, w, d = 3000, 48, 64, 8
+    a = random_cloud_arrays(rng, k, d, op_range=(0.001, 0.9), depth_range=(2.0, 4.0), xy=1.0,
+                            ls_range=(0.005, 0.2), sh_degree=1)
+    cloud = fs.GaussianCloud(**a)
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(8, 8, 8, 4), out_dim=64),
+                             fs.scene_aabb(cloud), rng, init="uniform")
+    net = fs.DeformationNet(64, fs.DeformationConfig(width=64, depth=1, feature_dim=d), rng, init="xavier",
+                            head_init="xavier")
+    step = TrainStep(dv.DeviceCloud.from_cloud(cloud), dv.DeviceField.from_field(field), dv.DeviceNet.from_net(net),
+                     h, w, fs.RasterConfig())
+    step.attach_optimizer({n: LrSchedule.constant(1e-3) for n in ("positions", "rotations", "log_scales",
+                                                                  "opacity_logits", "colors_raw", "features",
+                                                                  "grid", "net")})
+    step.track_stats()
+    K = pinhole(h, w, 50.0)
+    batch = [(0.3, K, np.eye(4), torch.rand(h, w, 3, device="cuda"), torch.randn(h, w, d, device="cuda"))]
+    for _ in range(2):
+        step.run(batch, check=True)
+    torch.cuda.synchronize()
+    counts = step.stats.count.cpu().numpy()
+    assert counts.max() == 2 and (counts > 0).mean() > 0.5  # visible Gaussians counted once per step
+    # oracle on the same pre-densify state
+    names = ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features")
+    pre = {n: getattr(step.cloud, n).cpu().numpy().astype(np.float64) for n in names}
+    pre["sh_rest"] = step.cloud.sh_rest.cpu().numpy().astype(np.float64)
+    spec_names = [sn for sn, _ in step.specs]
+    per = [n for n in ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "sh_rest", "features")]
+    extras = []
+    for n in per:
+        i = spec_names.index(n)
+        off, cnt = step.params.offsets[i], step.params.sizes[i]
+        shape = tuple(step.params.views[n].shape)
+        extras += [step.optimizer.m[off:off + cnt].cpu().numpy().astype(np.float64).reshape(shape),
+                   step.optimizer.v[off:off + cnt].cpu().numpy().astype(np.float64).reshape(shape)]
+    acc, cnt_ = step.stats.accum.cpu().numpy(), step.stats.count.cpu().numpy()
+    thr = float(np.percentile(acc / np.maximum(cnt_, 1), 70))
+    cfg = DensityControlConfig(grad_threshold=thr, percent_dense=0.05, prune_opacity=0.02)
+    net_before = step.params["net.trunk.0.weight"].clone()
+    rep = step.densify(cfg, 1.3, np.random.default_rng(5))
+    cl = type("C", (), dict(pre))()
+    zr = np.random.default_rng(5)
+    ro, _, _, rex, rc = O.density_control(cl, acc, cnt_, thr, 0.05, 0.02, 1.6, 1.3,
+                                          np.stack([zr.standard_normal((rep["split"], 3)) for _ in range(2)]),
+                                          extras=extras)
+    assert (rep["cloned"], rep["split"], rep["count"]) == (rc["clone"], rc["split"], len(ro["positions"]))
+    assert rep["cloned"] > 0 and rep["split"] > 0
+    for n in names + ("sh_rest",):
+        got = getattr(step.cloud, n).cpu().numpy().astype(np.float64).reshape(ro[n].shape)
+        tol = 1e-6 * max(1.0, np.abs(ro[n]).max()) if n in ("positions", "log_scales") else 0.0
+        assert np.abs(got - ro[n]).max() <= tol, n
+    for j, n in enumerate(per):
+        i = [sn for sn, _ in step.specs].index(n)
+        off, cnt = step.params.offsets[i], step.params.sizes[i]
+        np.testing.assert_array_equal(step.optimizer.m[off:off + cnt].cpu().numpy().astype(np.float64),
+                                      rex[2 * j].reshape(-1))
+    assert torch.equal(step.params["net.trunk.0.weight"], net_before)
+    assert not step.stats.accum.any() and len(step.stats.accum) == rep["count"]
+    step.run(batch, check=True)  # the next step at the new K
+    torch.cuda.synchronize()
+    assert len(step.cloud) == rep["count"] and torch.isfinite(step.params.buffer).all()
