@@ -329,7 +329,7 @@ extern "C" int fs4d_debug_blend_trace(unsigned long long* out) {
 }
 #endif
 
-template <int DC, int SUB>
+template <int DC, int SUB, bool FIRST>
 __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
 #ifdef FS4D_BLEND_TRACE
   const unsigned long long t_start = gtimer();
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   const int row = row0 + (threadIdx.x / kTile);
   const bool inside = col < a.W && row < a.H;
   const uint2 rg = a.ranges[tile];
-  const bool first = a.c0 == 0;
+  constexpr bool first = FIRST;  // the launch with c0 == 0 also composites colour, depth, alpha
   const float fc = (float)col, fr = (float)row;
   const int lane = threadIdx.x & 31;
   const int wrow0 = row0 + (threadIdx.x >> 5) * 2;  // this warp's two pixel rows
@@ -523,12 +523,21 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
 template <int SUB>
 static void launch_blend_sub(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
   const int grid = ntiles * SUB, nt = kTilePixels / SUB;
-  switch (dc) {
-    case 0: k_blend<0, SUB><<<grid, nt, 0, s>>>(a); break;
-    case 4: k_blend<4, SUB><<<grid, nt, 0, s>>>(a); break;
-    case 8: k_blend<8, SUB><<<grid, nt, 0, s>>>(a); break;
-    case 16: k_blend<16, SUB><<<grid, nt, 0, s>>>(a); break;
-    default: k_blend<32, SUB><<<grid, nt, 0, s>>>(a); break;
+  if (a.c0 == 0) {
+    switch (dc) {
+      case 0: k_blend<0, SUB, true><<<grid, nt, 0, s>>>(a); break;
+      case 4: k_blend<4, SUB, true><<<grid, nt, 0, s>>>(a); break;
+      case 8: k_blend<8, SUB, true><<<grid, nt, 0, s>>>(a); break;
+      case 16: k_blend<16, SUB, true><<<grid, nt, 0, s>>>(a); break;
+      default: k_blend<32, SUB, true><<<grid, nt, 0, s>>>(a); break;
+    }
+  } else {  // further feature-channel slices of a D > 32 map
+    switch (dc) {
+      case 4: k_blend<4, SUB, false><<<grid, nt, 0, s>>>(a); break;
+      case 8: k_blend<8, SUB, false><<<grid, nt, 0, s>>>(a); break;
+      case 16: k_blend<16, SUB, false><<<grid, nt, 0, s>>>(a); break;
+      default: k_blend<32, SUB, false><<<grid, nt, 0, s>>>(a); break;
+    }
   }
 }
 
