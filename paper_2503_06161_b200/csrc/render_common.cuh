@@ -31,6 +31,18 @@ __device__ __forceinline__ float4 unscaled_conic(const float4& cs) {
 __device__ __forceinline__ float gauss_power(const float4& cs, float dx, float dy) {
   return cs.x * dx * dx + cs.y * dx * dy + cs.z * dy * dy;
 }
+// 1/x to ~1 ulp (MUFU.RCP, no IEEE-division slow path).  The backward replay
+// recovers T_exc = T / (1 - alpha) with it; 1 - alpha lies in [0.01, 1).
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_sqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -74,8 +86,9 @@ template <int NR>
 __device__ __forceinline__ bool strip_hits(const int4& pr, const float2& mm, const float4& co, int r0, int c0,
                                            float alpha_skip) {
   if (co.w < alpha_skip) return false;
-  const float Q = fminf(kQSkip, 2.f * __logf(co.w / alpha_skip)) * 1.001f + 1e-3f;
-  const float inv_a = 1.f / co.x, schur = co.z - co.y * co.y * inv_a;
+  // approximate rcp / sqrt / log (~1e-6 relative): far inside the margins
+  const float Q = fminf(kQSkip, 2.f * __logf(co.w * fast_rcp(alpha_skip))) * 1.001f + 1e-3f;
+  const float inv_a = fast_rcp(co.x), schur = co.z - co.y * co.y * inv_a;
   const float xlo = (float)max(c0, pr.x) - 0.02f, xhi = (float)min(c0 + kTile - 1, pr.y) + 0.02f;
   bool hit = false;
 #pragma unroll
@@ -85,7 +98,7 @@ __device__ __forceinline__ bool strip_hits(const int4& pr, const float2& mm, con
     const float dy = (float)row - mm.y;
     const float qmin = schur * dy * dy;
     if (qmin > Q) continue;
-    const float h = sqrtf((Q - qmin) * inv_a) + 0.02f;
+    const float h = fast_sqrt((Q - qmin) * inv_a) + 0.02f;
     const float xc = mm.x - co.y * dy * inv_a;
     const float lo = fmaxf(xc - h, xlo), hi = fminf(xc + h, xhi);
     hit |= ceilf(lo) <= floorf(hi);
