@@ -496,7 +496,10 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
   // covariance (gaussians.py:187-194)
   const double q0 = Q[0], q1 = Q[1], q2 = Q[2], q3 = Q[3];
   const double qn = sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-  const double qu[4] = {q0 / qn, q1 / qn, q2 / qn, q3 / qn};
+  // one reciprocal per divisor (fp64; differs from true division by <= 1 ulp,
+  // far below the fp32 outputs' resolution) instead of an IEEE divide each
+  const double iqn = 1.0 / qn;
+  const double qu[4] = {q0 * iqn, q1 * iqn, q2 * iqn, q3 * iqn};
   const double qw = qu[0], qx = qu[1], qy = qu[2], qz = qu[3];
   double Rq[9];
   Rq[0] = 1 - 2 * (qy * qy + qz * qz);
@@ -518,8 +521,9 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
 
   // projection Jacobian and cov2d (rasterizer.py:141-152)
   const double fx = a.fx, fy = a.fy;
-  const double j00 = fx / z, j02 = -fx * x / (z * z);
-  const double j11 = fy / z, j12 = -fy * y / (z * z);
+  const double iz = 1.0 / z, iz2 = iz * iz;
+  const double j00 = fx * iz, j02 = -fx * x * iz2;
+  const double j11 = fy * iz, j12 = -fy * y * iz2;
   double M[6];
   for (int k = 0; k < 3; ++k) {
     M[k] = j00 * R[k] + j02 * R[6 + k];
@@ -533,7 +537,8 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
   const double cb = MS[0] * M[3] + MS[1] * M[4] + MS[2] * M[5];
   const double cc2 = MS[3] * M[3] + MS[4] * M[4] + MS[5] * M[5] + a.lowpass;
   const double det = ca * cc2 - cb * cb;
-  const double C00 = cc2 / det, C01 = -cb / det, C11 = ca / det;
+  const double idet = 1.0 / det;
+  const double C00 = cc2 * idet, C01 = -cb * idet, C11 = ca * idet;
 
   // d_cov2d = -C dConic C  (rasterizer.py:396), dConic symmetric with dxy off-diagonal
   // T1 = dConic C
@@ -559,12 +564,12 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
       dJ[3 * rr + k] = dM[3 * rr] * R[3 * k] + dM[3 * rr + 1] * R[3 * k + 1] + dM[3 * rr + 2] * R[3 * k + 2];
 
   // camera-space gradient (rasterizer.py:417-426)
-  const double z2 = z * z, z3 = z2 * z;
+  const double iz3 = iz2 * iz;
   double dcam[3];
-  dcam[0] = dJ[2] * (-fx / z2) + dmx * fx / z;
-  dcam[1] = dJ[5] * (-fy / z2) + dmy * fy / z;
-  dcam[2] = dJ[0] * (-fx / z2) + dJ[2] * (2.0 * fx * x / z3) + dJ[4] * (-fy / z2) + dJ[5] * (2.0 * fy * y / z3) +
-            dmx * (-fx * x / z2) + dmy * (-fy * y / z2) + ddep;
+  dcam[0] = dJ[2] * (-fx * iz2) + dmx * fx * iz;
+  dcam[1] = dJ[5] * (-fy * iz2) + dmy * fy * iz;
+  dcam[2] = dJ[0] * (-fx * iz2) + dJ[2] * (2.0 * fx * x * iz3) + dJ[4] * (-fy * iz2) + dJ[5] * (2.0 * fy * y * iz3) +
+            dmx * (-fx * x * iz2) + dmy * (-fy * y * iz2) + ddep;
   double dpos[3];
   for (int k = 0; k < 3; ++k) dpos[k] = dcam[0] * R[k] + dcam[1] * R[3 + k] + dcam[2] * R[6 + k];
 
@@ -601,26 +606,25 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
     double vx = X - a.campos[0], vy = Y - a.campos[1], vz = Z - a.campos[2];
     double dn = sqrt(vx * vx + vy * vy + vz * vz);
     dn = dn > 0 ? dn : 1.0;
-    const double ux = vx / dn, uy = vy / dn, uz = vz / dn;
-    double Yb[15], dY[15][3];
-    int nb = sh_basis<double>(a.sh_degree, ux, uy, uz, Yb, dY);
+    const double idn = 1.0 / dn;
+    const double ux = vx * idn, uy = vy * idn, uz = vz * idn;
     const float* S = sh_in;
     float* GS = sh_out;
     double ddir[3] = {0, 0, 0};
-    for (int k = 0; k < nb; ++k) {
+    sh_visit<double>(a.sh_degree, ux, uy, uz, [&](int k, double Yk, double dYx, double dYy, double dYz) {
       double gk = 0;
       for (int c = 0; c < 3; ++c) {
-        GS[3 * k + c] = (float)(Yb[k] * dcg[c]);
+        GS[3 * k + c] = (float)(Yk * dcg[c]);
         gk += S[3 * k + c] * dcg[c];
       }
-      ddir[0] += gk * dY[k][0];
-      ddir[1] += gk * dY[k][1];
-      ddir[2] += gk * dY[k][2];
-    }
+      ddir[0] += gk * dYx;
+      ddir[1] += gk * dYy;
+      ddir[2] += gk * dYz;
+    });
     const double dot = ddir[0] * ux + ddir[1] * uy + ddir[2] * uz;
-    dpos[0] += (ddir[0] - dot * ux) / dn;
-    dpos[1] += (ddir[1] - dot * uy) / dn;
-    dpos[2] += (ddir[2] - dot * uz) / dn;
+    dpos[0] += (ddir[0] - dot * ux) * idn;
+    dpos[1] += (ddir[1] - dot * uy) * idn;
+    dpos[2] += (ddir[2] - dot * uz) * idn;
   }
 
   const double o = sigmoid_db((double)a.c.opacity_logits[i]);
@@ -629,7 +633,7 @@ __device__ __forceinline__ void preprocess_bwd_one(const PreBwdArgs& a, int64_t 
     a.g.log_scales[3 * i + k] = (float)dls[k];
     a.g.colors_raw[3 * i + k] = (float)dcg[k];
   }
-  for (int k = 0; k < 4; ++k) a.g.rotations[4 * i + k] = (float)((dqu[k] - inner * qu[k]) / qn);
+  for (int k = 0; k < 4; ++k) a.g.rotations[4 * i + k] = (float)((dqu[k] - inner * qu[k]) * iqn);
   a.g.opacity_logits[i] = (float)(dop * o * (1.0 - o));
   for (int c = 0; c < a.D; ++c) a.g.features[(int64_t)a.D * i + c] = acc[10 + c];
   if (a.vs_index) a.vs_index[r] = (int32_t)i;

@@ -173,14 +173,12 @@ __device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i, cons
     double dx = X - a.campos[0], dy = Y - a.campos[1], dz = Z - a.campos[2];
     double dn = sqrt(dx * dx + dy * dy + dz * dz);
     dn = dn > 0 ? dn : 1.0;
-    double Yb[15];
-    int nb = sh_basis<double>(a.c.sh_degree, dx / dn, dy / dn, dz / dn, Yb, nullptr);
     const float* S = sh_row;
-    for (int k = 0; k < nb; ++k) {
-      col[0] += Yb[k] * S[3 * k + 0];
-      col[1] += Yb[k] * S[3 * k + 1];
-      col[2] += Yb[k] * S[3 * k + 2];
-    }
+    sh_visit<double>(a.c.sh_degree, dx / dn, dy / dn, dz / dn, [&](int k, double Yk, double, double, double) {
+      col[0] += Yk * S[3 * k + 0];
+      col[1] += Yk * S[3 * k + 1];
+      col[2] += Yk * S[3 * k + 2];
+    });
   }
   uint32_t gate = 0;
 #pragma unroll

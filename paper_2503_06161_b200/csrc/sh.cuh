@@ -28,74 +28,40 @@ struct ShConst {
   static constexpr T C3_6 = T(-0.5900435899266435);
 };
 
-// Y[k] for k = 1..(L+1)^2-1 (written to Y[0..n-1]) and, if dY != nullptr,
-// dY[k][3] = dY_k/d(x,y,z) treating (x,y,z) as free variables.
-template <typename T>
-__host__ __device__ inline int sh_basis(int degree, T x, T y, T z, T* Y, T (*dY)[3]) {
+// Calls f(k, Y_k, dY_k/dx, dY_k/dy, dY_k/dz) for k = 0..(L+1)^2-2 (basis
+// functions 1.. of the real SH, (x, y, z) treated as free variables), in
+// increasing k.  A visitor instead of Y[15] / dY[15][3] arrays: with a runtime
+// degree those arrays live in local memory (480 B per thread in the backward).
+template <typename T, typename F>
+__host__ __device__ __forceinline__ void sh_visit(int degree, T x, T y, T z, F&& f) {
   using C = ShConst<T>;
-  int n = 0;
+  const T o = T(0);
   if (degree >= 1) {
-    Y[0] = -C::C1 * y;
-    Y[1] = C::C1 * z;
-    Y[2] = -C::C1 * x;
-    if (dY) {
-      dY[0][0] = 0; dY[0][1] = -C::C1; dY[0][2] = 0;
-      dY[1][0] = 0; dY[1][1] = 0; dY[1][2] = C::C1;
-      dY[2][0] = -C::C1; dY[2][1] = 0; dY[2][2] = 0;
-    }
-    n = 3;
+    f(0, -C::C1 * y, o, -C::C1, o);
+    f(1, C::C1 * z, o, o, C::C1);
+    f(2, -C::C1 * x, -C::C1, o, o);
   }
   if (degree >= 2) {
-    T xx = x * x, yy = y * y, zz = z * z;
-    Y[3] = C::C2_0 * x * y;
-    Y[4] = C::C2_1 * y * z;
-    Y[5] = C::C2_2 * (T(2) * zz - xx - yy);
-    Y[6] = C::C2_3 * x * z;
-    Y[7] = C::C2_4 * (xx - yy);
-    if (dY) {
-      dY[3][0] = C::C2_0 * y; dY[3][1] = C::C2_0 * x; dY[3][2] = 0;
-      dY[4][0] = 0; dY[4][1] = C::C2_1 * z; dY[4][2] = C::C2_1 * y;
-      dY[5][0] = C::C2_2 * (-T(2) * x); dY[5][1] = C::C2_2 * (-T(2) * y); dY[5][2] = C::C2_2 * (T(4) * z);
-      dY[6][0] = C::C2_3 * z; dY[6][1] = 0; dY[6][2] = C::C2_3 * x;
-      dY[7][0] = C::C2_4 * (T(2) * x); dY[7][1] = C::C2_4 * (-T(2) * y); dY[7][2] = 0;
-    }
-    n = 8;
+    const T xx = x * x, yy = y * y, zz = z * z;
+    f(3, C::C2_0 * x * y, C::C2_0 * y, C::C2_0 * x, o);
+    f(4, C::C2_1 * y * z, o, C::C2_1 * z, C::C2_1 * y);
+    f(5, C::C2_2 * (T(2) * zz - xx - yy), C::C2_2 * (-T(2) * x), C::C2_2 * (-T(2) * y), C::C2_2 * (T(4) * z));
+    f(6, C::C2_3 * x * z, C::C2_3 * z, o, C::C2_3 * x);
+    f(7, C::C2_4 * (xx - yy), C::C2_4 * (T(2) * x), C::C2_4 * (-T(2) * y), o);
   }
   if (degree >= 3) {
-    T xx = x * x, yy = y * y, zz = z * z;
-    Y[8] = C::C3_0 * y * (T(3) * xx - yy);
-    Y[9] = C::C3_1 * x * y * z;
-    Y[10] = C::C3_2 * y * (T(4) * zz - xx - yy);
-    Y[11] = C::C3_3 * z * (T(2) * zz - T(3) * xx - T(3) * yy);
-    Y[12] = C::C3_4 * x * (T(4) * zz - xx - yy);
-    Y[13] = C::C3_5 * z * (xx - yy);
-    Y[14] = C::C3_6 * x * (xx - T(3) * yy);
-    if (dY) {
-      dY[8][0] = C::C3_0 * (T(6) * x * y);
-      dY[8][1] = C::C3_0 * (T(3) * xx - T(3) * yy);
-      dY[8][2] = 0;
-      dY[9][0] = C::C3_1 * y * z;
-      dY[9][1] = C::C3_1 * x * z;
-      dY[9][2] = C::C3_1 * x * y;
-      dY[10][0] = C::C3_2 * (-T(2) * x * y);
-      dY[10][1] = C::C3_2 * (T(4) * zz - xx - T(3) * yy);
-      dY[10][2] = C::C3_2 * (T(8) * y * z);
-      dY[11][0] = C::C3_3 * (-T(6) * x * z);
-      dY[11][1] = C::C3_3 * (-T(6) * y * z);
-      dY[11][2] = C::C3_3 * (T(6) * zz - T(3) * xx - T(3) * yy);
-      dY[12][0] = C::C3_4 * (T(4) * zz - T(3) * xx - yy);
-      dY[12][1] = C::C3_4 * (-T(2) * x * y);
-      dY[12][2] = C::C3_4 * (T(8) * x * z);
-      dY[13][0] = C::C3_5 * (T(2) * x * z);
-      dY[13][1] = C::C3_5 * (-T(2) * y * z);
-      dY[13][2] = C::C3_5 * (xx - yy);
-      dY[14][0] = C::C3_6 * (T(3) * xx - T(3) * yy);
-      dY[14][1] = C::C3_6 * (-T(6) * x * y);
-      dY[14][2] = 0;
-    }
-    n = 15;
+    const T xx = x * x, yy = y * y, zz = z * z;
+    f(8, C::C3_0 * y * (T(3) * xx - yy), C::C3_0 * (T(6) * x * y), C::C3_0 * (T(3) * xx - T(3) * yy), o);
+    f(9, C::C3_1 * x * y * z, C::C3_1 * y * z, C::C3_1 * x * z, C::C3_1 * x * y);
+    f(10, C::C3_2 * y * (T(4) * zz - xx - yy), C::C3_2 * (-T(2) * x * y), C::C3_2 * (T(4) * zz - xx - T(3) * yy),
+      C::C3_2 * (T(8) * y * z));
+    f(11, C::C3_3 * z * (T(2) * zz - T(3) * xx - T(3) * yy), C::C3_3 * (-T(6) * x * z), C::C3_3 * (-T(6) * y * z),
+      C::C3_3 * (T(6) * zz - T(3) * xx - T(3) * yy));
+    f(12, C::C3_4 * x * (T(4) * zz - xx - yy), C::C3_4 * (T(4) * zz - T(3) * xx - yy), C::C3_4 * (-T(2) * x * y),
+      C::C3_4 * (T(8) * x * z));
+    f(13, C::C3_5 * z * (xx - yy), C::C3_5 * (T(2) * x * z), C::C3_5 * (-T(2) * y * z), C::C3_5 * (xx - yy));
+    f(14, C::C3_6 * x * (xx - T(3) * yy), C::C3_6 * (T(3) * xx - T(3) * yy), C::C3_6 * (-T(6) * x * y), o);
   }
-  return n;
 }
 
 }  // namespace fs4d
