@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_photo_grads(const float* __restric
       terms[2] = (double)na;
       terms[3] = (double)nb;
     }
-    if (blockIdx.x == 0 && loss) *loss += lam_rgb * rgb + (dep ? lam_d * dterm : 0.0);
+    if (blockIdx.x == 0 && loss) atomicAdd(loss, lam_rgb * rgb + (dep ? lam_d * dterm : 0.0));  // lanes share it
   }
   __syncthreads();
   const float g_rgb = n_tot[0] ? (float)(lam_rgb / (double)n_tot[0]) : 0.f;

@@ -21,6 +21,7 @@ Loss modes:
 """
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -62,7 +63,7 @@ def _net_layer_specs(net):
 class TrainStep:
     def __init__(self, cloud, field, net, height, width, cfg, world=1, group=None, device="cuda",
                  loss_mode="raw", lambda_rgb=1.0, lambda_depth=0.0, lambda_feat=1.0, lambda_tv=0.0,
-                 decoder=None, locality=None):
+                 decoder=None, locality=None, lanes=None):
         self.cloud, self.field, self.net = cloud, field, net
         self.h, self.w, self.cfg = int(height), int(width), cfg
         self.world, self.group = int(world), group
@@ -70,8 +71,12 @@ class TrainStep:
         if loss_mode not in ("raw", "decoder"):
             raise ValueError(f"unknown loss mode {loss_mode!r}")
         self.loss_mode = loss_mode
-        import os
         self.locality = (os.environ.get("FS4D_TRAIN_LOCALITY", "0") == "1") if locality is None else bool(locality)
+        # pairs in flight: lane j runs pairs j, j+L, ... on its own stream with
+        # its own snapshot / record / image gradients / gradient buffer; the
+        # lane buffers are summed into self.grads before the all-reduce
+        self.n_lanes = max(1, int(os.environ.get("FS4D_TRAIN_LANES", "3") if lanes is None else lanes))
+        self._lanes = None
         self.lambda_rgb, self.lambda_depth = float(lambda_rgb), float(lambda_depth)
         self.lambda_feat, self.lambda_tv = float(lambda_feat), float(lambda_tv)
         self.decoder = decoder  # (weight [Ct,N], bias [Ct]) CUDA tensors for loss_mode="decoder"
@@ -152,6 +157,37 @@ class TrainStep:
     def current_lrs(self):
         return {k: lr_at_step(s, self.iteration) for k, s in self.schedules.items() if s is not None}
 
+    def _make_lanes(self):
+        from types import SimpleNamespace
+        k, d, sh = len(self.cloud), self.cloud.feature_dim, self.cloud.sh_degree
+        dout = self.d_feature.shape[2]
+        f = dict(dtype=torch.float32, device=self.device)
+        lanes = []
+        for j in range(self.n_lanes):
+            if j == 0:
+                ln = SimpleNamespace(grads=self.grads, cloud_grads=self.cloud_grads, plane_grads=self.plane_grads,
+                                     net_grads=self.net_grads, deformer=self.deformer, renderer=self.renderer,
+                                     snap=self.snap, snap_grads=self.snap_grads, images=self.images,
+                                     d_color=self.d_color, d_depth=self.d_depth, d_feature=self.d_feature,
+                                     decoder_loss=self.decoder_loss, vs_norm=self.vs_norm)
+            else:
+                g = FlatGrads(self.specs, self.device)
+                cg, pg, ng = self._bind(g)
+                ln = SimpleNamespace(grads=g, cloud_grads=cg, plane_grads=pg, net_grads=ng,
+                                     deformer=DeformEngine(self.device), renderer=Renderer(self.device),
+                                     snap=DeviceCloud.empty(k, d, 0, self.device),
+                                     snap_grads=DeviceCloud.empty(k, d, sh, self.device),
+                                     images=self.renderer.alloc_images(self.h, self.w, dout),
+                                     d_color=torch.empty(self.h, self.w, 3, **f), d_depth=torch.empty(self.h, self.w, **f),
+                                     d_feature=torch.empty(self.h, self.w, dout, **f),
+                                     decoder_loss=DecoderLoss(self.device),
+                                     vs_norm=None if self.vs_norm is None else torch.empty_like(self.vs_norm))
+            ln.cache, ln.photo_ws = None, None
+            ln.stream = torch.cuda.Stream(device=self.device) if self.n_lanes > 1 else None
+            lanes.append(ln)
+        self._lanes = lanes
+        return lanes
+
     def run(self, batch, check=False):
         """batch: list of (t, K, T, target_rgb [H,W,3], target_feat) CUDA
         tensors; loss_mode "decoder" additionally takes optional
@@ -168,46 +204,26 @@ class TrainStep:
             # Morton visiting order of this step's canonical positions for the
             # HexPlane gather / scatter (identical results, coherent caches)
             field = field.with_order(locality_order(self.cloud.positions, field.aabb, self.device))
+        lanes = self._lanes or self._make_lanes()
+        nl = len(lanes)
+        main = torch.cuda.current_stream()
+        if nl > 1:
+            ready = torch.cuda.Event()
+            ready.record(main)
+            for ln in lanes:
+                ln.stream.wait_event(ready)
+        stats_done = None  # the stats accumulation is a plain += : serialised across lanes
         for i, item in enumerate(batch):
-            t, K, T, tgt_rgb, tgt_feat = item[:5]
-            _, self.cache = self.deformer.forward(self.cloud, field, self.net, t, out=self.snap,
-                                                  with_cache=self.cache or True)
-            imgs, rec = self.renderer.forward(self.snap, K, T, self.h, self.w, self.cfg, images=self.images,
-                                              check=check)
-            d_depth = None
-            if self.loss_mode == "raw":
-                N.check(lib.fs4d_l1_loss_grad(_p(imgs["color"]), _p(tgt_rgb), _p(imgs["feature"]) if dout else None,
-                                              _p(tgt_feat) if dout else None, self.h, self.w, dout,
-                                              w * self.lambda_rgb, w * self.lambda_feat, _p(self.d_color),
-                                              _p(self.d_feature) if dout else None, _p(self.loss), _stream()))
-            else:
-                mask = item[5] if len(item) > 5 else None
-                tgt_depth = item[6] if len(item) > 6 else None
-                if tgt_depth is not None:
-                    d_depth = self.d_depth
-                if self.photo_ws is None:
-                    self.photo_ws = torch.empty(int(lib.fs4d_photometric_workspace_bytes(self.h, self.w)),
-                                                dtype=torch.uint8, device=self.device)
-                photometric_loss_grad(imgs["color"], tgt_rgb, mask, imgs["depth"] if d_depth is not None else None,
-                                      tgt_depth, imgs["alpha"], w * self.lambda_rgb, w * self.lambda_depth,
-                                      self.d_color, d_depth, loss=self.loss, workspace=self.photo_ws)
-                if dout and tgt_feat is not None and self.decoder is not None:
-                    dw = self.grads["decoder.weight"]
-                    db = self.grads["decoder.bias"]
-                    self.decoder_loss(self.decoder[0], self.decoder[1], imgs["feature"], tgt_feat,
-                                      w * self.lambda_feat, self.d_feature, dw, db, self.loss, accumulate=i > 0)
-                elif dout:
-                    self.d_feature.zero_()
-            self.renderer.backward(self.snap, K, T, self.h, self.w, self.cfg, rec, d_color=self.d_color,
-                                   d_depth=d_depth, d_feature=self.d_feature if dout else None,
-                                   grads=self.snap_grads,
-                                   viewspace=self.vs_norm if self.stats is not None else False)
-            if self.stats is not None:  # training.py:514 grad_stats.add (dense, source order)
-                self.stats.add_dense(self.vs_norm)
-            self.deformer.backward(self.cloud, field, self.net, t, self.snap_grads,
-                                   cloud_grads=self.cloud_grads, net_grads=self.net_grads,
-                                   plane_grads=self.plane_grads if self.net.enable_grid else None,
-                                   accumulate=i > 0, cache=self.cache)
+            ln = lanes[i % nl]
+            first = i < nl
+            with torch.cuda.stream(ln.stream if nl > 1 else main):
+                stats_done = self._run_pair(ln, item, field, w, dout, first, check, stats_done)
+        used = lanes[:min(nl, len(batch))]
+        if nl > 1:
+            for ln in used:
+                main.wait_stream(ln.stream)
+            for ln in used[1:]:
+                self.grads.buffer.add_(ln.grads.buffer)
         if self.lambda_tv > 0 and self.net.enable_grid:
             # d(lambda_tv * tv)/d(plane) once per iteration (training.py:523-529); 1/world per rank
             tv_loss_grad_device(self.field, self.plane_grads, self.lambda_tv / self.world, True, self.loss)
@@ -222,6 +238,52 @@ class TrainStep:
             self.iteration += 1
         return self.loss
 
+    def _run_pair(self, ln, item, field, w, dout, first, check, stats_done):
+        """One (view, t) pair on lane `ln` (the current stream): deform, render,
+        loss + image gradients, render backward, deform backward into the
+        lane's gradient buffer (overwritten by the lane's first pair)."""
+        lib = N.load()
+        t, K, T, tgt_rgb, tgt_feat = item[:5]
+        _, ln.cache = ln.deformer.forward(self.cloud, field, self.net, t, out=ln.snap, with_cache=ln.cache or True)
+        imgs, rec = ln.renderer.forward(ln.snap, K, T, self.h, self.w, self.cfg, images=ln.images, check=check)
+        d_depth = None
+        if self.loss_mode == "raw":
+            N.check(lib.fs4d_l1_loss_grad(_p(imgs["color"]), _p(tgt_rgb), _p(imgs["feature"]) if dout else None,
+                                          _p(tgt_feat) if dout else None, self.h, self.w, dout,
+                                          w * self.lambda_rgb, w * self.lambda_feat, _p(ln.d_color),
+                                          _p(ln.d_feature) if dout else None, _p(self.loss), _stream()))
+        else:
+            mask = item[5] if len(item) > 5 else None
+            tgt_depth = item[6] if len(item) > 6 else None
+            if tgt_depth is not None:
+                d_depth = ln.d_depth
+            if ln.photo_ws is None:
+                ln.photo_ws = torch.empty(int(lib.fs4d_photometric_workspace_bytes(self.h, self.w)),
+                                          dtype=torch.uint8, device=self.device)
+            photometric_loss_grad(imgs["color"], tgt_rgb, mask, imgs["depth"] if d_depth is not None else None,
+                                  tgt_depth, imgs["alpha"], w * self.lambda_rgb, w * self.lambda_depth,
+                                  ln.d_color, d_depth, loss=self.loss, workspace=ln.photo_ws)
+            if dout and tgt_feat is not None and self.decoder is not None:
+                ln.decoder_loss(self.decoder[0], self.decoder[1], imgs["feature"], tgt_feat, w * self.lambda_feat,
+                                ln.d_feature, ln.grads["decoder.weight"], ln.grads["decoder.bias"], self.loss,
+                                accumulate=not first)
+            elif dout:
+                ln.d_feature.zero_()
+        ln.renderer.backward(ln.snap, K, T, self.h, self.w, self.cfg, rec, d_color=ln.d_color, d_depth=d_depth,
+                             d_feature=ln.d_feature if dout else None, grads=ln.snap_grads,
+                             viewspace=ln.vs_norm if self.stats is not None else False)
+        if self.stats is not None:  # training.py:514 grad_stats.add (dense, source order)
+            cur = torch.cuda.current_stream()
+            if stats_done is not None:
+                cur.wait_event(stats_done)
+            self.stats.add_dense(ln.vs_norm)
+            stats_done = torch.cuda.Event()
+            stats_done.record(cur)
+        ln.deformer.backward(self.cloud, field, self.net, t, ln.snap_grads, cloud_grads=ln.cloud_grads,
+                             net_grads=ln.net_grads, plane_grads=ln.plane_grads if self.net.enable_grid else None,
+                             accumulate=not first, cache=ln.cache)
+        return stats_done
+
     # ------------------------------------------------------------------
     # adaptive density control in the training loop (training.py:445-456)
     # ------------------------------------------------------------------
@@ -232,6 +294,7 @@ class TrainStep:
         k = len(self.cloud)
         self.stats = ViewspaceGradStats.zeros(k, self.device)
         self.vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device)
+        self._lanes = None
         return self
 
     def densify(self, cfg, extent, rng, prune_only=False):
@@ -289,6 +352,7 @@ class TrainStep:
         self.snap = DeviceCloud.empty(k, d, 0, self.device)
         self.snap_grads = DeviceCloud.empty(k, d, sh, self.device)
         self.cache = None
+        self._lanes = None
         if self.stats is not None:
             self.stats = new_stats  # reset (densify) or compacted (prune_only), gaussians.py:397-415
             self.vs_norm = torch.empty(max(k, 1), dtype=torch.float32, device=self.device)
