@@ -464,13 +464,21 @@ def train_bench(args, rank, world, local):
     b.record(stream)
     torch.cuda.synchronize()
     ms = dist_max(a.elapsed_time(b), world)
+    # per-stage times from one serial step (one lane: with pairs in flight the
+    # stage events of concurrent streams would overlap)
+    lanes = step.n_lanes
+    step.n_lanes, step._lanes = 1, None
+    step.run(batch)
+    torch.cuda.synchronize()
     dv.profile_collect()
     dv.profile_enable(True)
     step.run(batch)
     torch.cuda.synchronize()
     prof = dv.profile_collect()
     dv.profile_enable(False)
-    return dict(ms=ms, prof=prof, loss=float(step.loss.item()), grad_floats=step.grads.numel, pairs=pairs)
+    step.n_lanes, step._lanes = lanes, None
+    return dict(ms=ms, prof=prof, loss=float(step.loss.item()), grad_floats=step.grads.numel, pairs=pairs,
+                lanes=lanes)
 
 
 def launches_per_frame():
@@ -529,7 +537,8 @@ def main():
                          "stage_ms_per_step": {s: round(ms, 4) for s, (ms, c) in r["prof"].items() if c},
                          "allreduce_floats": r["grad_floats"], "loss": r["loss"]})
             line["config"] = dict(base["config"], workload="configs[4]: configs[1] scene, 8 (view,t) pairs/GPU, "
-                                                           "L1 RGB + L1 feature", parallelism=f"dp{world}")
+                                                           "L1 RGB + L1 feature", parallelism=f"dp{world}",
+                                  pairs_in_flight=r["lanes"], stage_ms="one serial (1-lane) step")
             if args.workload == "fine":
                 line["config"]["workload"] = ("reference fine-stage iteration (training.py:489-535) on the configs[1] "
                                               "scene: 8 pairs/GPU, teacher 16ch at 160x128, TrainConfig defaults")

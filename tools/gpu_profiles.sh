@@ -9,7 +9,7 @@ timeout 600 python bench.py --workload fine --steps 5 --warmup 3 --no-cpu > gpur
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/ref.json 2> gpurun_out/ref.err; echo ref=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1; echo ncu=$?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/train_launches.csv python bench.py --workload train --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1; echo ncu_train=$?
-bash tools/ncu_full_render.sh; for k in; do
+bash tools/ncu_full_render.sh; bash tools/ncu_full_train.sh; for k in; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:"$k[<(]" -s 3 -c 1 -o gpurun_out/full_$k -f python bench.py --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
   echo "full $k rc=$?"
 done

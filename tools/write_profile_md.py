@@ -29,6 +29,8 @@ def main():
                                     text=True).stdout
     l1, l2 = run("launches", f"{P}/r1_launches_default.csv"), run("launches", f"{P}/r1_launches_train.csv")
     full = "\n".join(run("full", f"{G}/full_{k}.ncu-rep") for k in kernels)
+    train_kernels = ["k_blend_bwd2", "k_mlp_bwd_tc", "k_hexplane_bwd_c32", "k_preprocess_bwd"]
+    full_train = "\n".join(run("full", f"{G}/full_{k}.ncu-rep") for k in train_kernels)
     rf = b["roofline"]
     txt = f"""# Round 1 — committed-build profile (latest)
 
@@ -47,8 +49,8 @@ Per-kernel algorithmic GB/s: {json.dumps({k: round(v['achieved_gbs'], 1) for k, 
 MLP: {b['mlp']['tflops']:.1f} TFLOP/s useful (x3 issued as the bf16 split:
 {b['mlp']['frac_of_bf16_peak_issued']:.3f} of the bf16 peak).
 
-Training (configs[4], 8 pairs, fwd+bwd+all-reduce): {t['value']:.1f} steps/s ({t['ms_per_step']:.2f} ms/step);
-stage ms/step {json.dumps(t['stage_ms_per_step'])}.
+Training (configs[4], 8 pairs, fwd+bwd+all-reduce, {t['config'].get('pairs_in_flight', 1)} pairs in flight): {t['value']:.1f} steps/s ({t['ms_per_step']:.2f} ms/step);
+stage ms/step (one serial step) {json.dumps(t['stage_ms_per_step'])}.
 Fine-stage iteration (decoder + depth + TV + Adam): {f['value']:.1f} steps/s ({f['ms_per_step']:.2f} ms/step).
 
 ## Render launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`; serialised, cold cache: compare shares)
@@ -60,6 +62,10 @@ Fine-stage iteration (decoder + depth + TV + Adam): {f['value']:.1f} steps/s ({f
 ## `ncu --set full` of the top render kernels (one launch each, `-s 3 -c 1`)
 
 {full}
+
+## `ncu --set full` of the top training-step kernels (one launch each, `-s 2 -c 1`)
+
+{full_train}
 """
     open(f"{P}/r1_profile_latest.md", "w").write(txt)
     print(txt[:1800])
