@@ -500,19 +500,26 @@ __global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a
 constexpr int kHexC32Warps = 8;
 struct HexC32Args {
   HexBwdArgs h;
+  const float* rows;  // the frame's time rows (k_pack_tc), or null: bilinear time-plane gathers
   int toff[2][3];  // offsets (floats) of the time-plane accumulators inside a CTA's partial
   int tfloats;
   float* tpart;    // [grid][tfloats] per-CTA time-plane partials (global, zeroed by the host)
 };
 
 __device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 || q == 5; }
+// plane axes (hexplane.py:16) as compile-time values inside unrolled loops
+__device__ __forceinline__ constexpr int plane_axis0(int q) { return q < 3 ? 0 : (q < 5 ? 1 : 2); }
+__device__ __forceinline__ constexpr int plane_axis1(int q) { return q == 0 ? 1 : (q == 1 || q == 3 ? 2 : 3); }
 
 // Time planes: every Gaussian of a frame hits the same t row pair, so their
 // gradients collapse onto Ra spatial rows per plane.  They accumulate with
 // fire-and-forget red.global.add.v4 into a per-CTA partial (no cross-CTA
 // contention; a shared-memory float atomic is a CAS loop on sm_100), reduced
 // by k_time_partials afterwards.
-__global__ void __launch_bounds__(kHexC32Warps * 32, 1) k_hexplane_bwd_c32(HexC32Args A) {
+#ifndef FS4D_HEX_BWD_MINB
+#define FS4D_HEX_BWD_MINB 2  // measured: 1 -> 248 us, 2 -> 240 us (128 registers, small spill)
+#endif
+__global__ void __launch_bounds__(kHexC32Warps * 32, FS4D_HEX_BWD_MINB) k_hexplane_bwd_c32(HexC32Args A) {
   const HexBwdArgs& a = A.h;
   const TcPlan& p = a.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -552,7 +559,7 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 1) k_hexplane_bwd_c32(HexC3
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
           const int ra = p.res[l][q][0], rb = p.res[l][q][1];
-          const double u = c[c_axes_bwd[q][0]] * (ra - 1), v = c[c_axes_bwd[q][1]] * (rb - 1);
+          const double u = c[plane_axis0(q)] * (ra - 1), v = c[plane_axis1(q)] * (rb - 1);
           int i0 = (int)floor(u), j0 = (int)floor(v);
           i0 = min(max(i0, 0), ra - 2);
           j0 = min(max(j0, 0), rb - 2);
@@ -593,6 +600,23 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 1) k_hexplane_bwd_c32(HexC3
           cb[q] = cj;
           const int base = is_time_plane(q) ? (cj * rb + tj0[l]) * 32 : cj;
           const int rs = rb * 32;
+          const float f0 = w_a[q], f1 = w_b[q];
+          if (is_time_plane(q) && A.rows) {
+            // the frame's time row of this plane (the t lerp done once per
+            // frame by k_pack_tc, as in the forward gather): two float4 loads
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+            if (ok) {
+              const float* rp = A.rows + p.row_off[l][q == 2 ? 0 : (q == 4 ? 1 : 2)] + cj * 32 + ch;
+              r0 = __ldg(reinterpret_cast<const float4*>(rp));
+              r1 = __ldg(reinterpret_cast<const float4*>(rp + 32));
+            }
+            const float g0 = 1.f - f0;
+            s[q] = make_float4(g0 * r0.x + f0 * r1.x, g0 * r0.y + f0 * r1.y, g0 * r0.z + f0 * r1.z,
+                               g0 * r0.w + f0 * r1.w);
+            da[q] = make_float4(r1.x - r0.x, r1.y - r0.y, r1.z - r0.z, r1.w - r0.w);
+            db[q] = make_float4(0.f, 0.f, 0.f, 0.f);  // time axis: no position gradient
+            continue;
+          }
           float4 c00 = make_float4(0.f, 0.f, 0.f, 0.f), c01 = c00, c10 = c00, c11 = c00;
           if (ok) {
             const float* pl = p.planes[l][q] + base + ch;
@@ -601,7 +625,6 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 1) k_hexplane_bwd_c32(HexC3
             c10 = __ldg(reinterpret_cast<const float4*>(pl + rs));
             c11 = __ldg(reinterpret_cast<const float4*>(pl + rs + 32));
           }
-          const float f0 = w_a[q], f1 = w_b[q];
           const float w00 = (1.f - f0) * (1.f - f1), w10 = f0 * (1.f - f1), w01 = (1.f - f0) * f1, w11 = f0 * f1;
           s[q] = make_float4(w00 * c00.x + w10 * c10.x + w01 * c01.x + w11 * c11.x,
                              w00 * c00.y + w10 * c10.y + w01 * c01.y + w11 * c11.y,
@@ -652,8 +675,8 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, 1) k_hexplane_bwd_c32(HexC3
           }
           const float sa = cf.x * da[q].x + cf.y * da[q].y + cf.z * da[q].z + cf.w * da[q].w;
           const float sb = cf.x * db[q].x + cf.y * db[q].y + cf.z * db[q].z + cf.w * db[q].w;
-          dco[c_axes_bwd[q][0]] += sa * (float)(p.res[l][q][0] - 1);
-          if (c_axes_bwd[q][1] < 3) dco[c_axes_bwd[q][1]] += sb * (float)(p.res[l][q][1] - 1);
+          dco[plane_axis0(q)] += sa * (float)(p.res[l][q][0] - 1);
+          if (plane_axis1(q) < 3) dco[plane_axis1(q)] += sb * (float)(p.res[l][q][1] - 1);
         }
       }
 #pragma unroll
@@ -744,6 +767,7 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
     h.accumulate = accumulate;
     HexC32Args hc;
     hc.h = h;
+    hc.rows = p.rows_ok && !getenv("FS4D_NO_TIME_ROWS") ? reinterpret_cast<const float*>(blob + p.off_rows) : nullptr;
     int tf = 0;
     for (int l = 0; l < 2 && p.levels == 2; ++l)
       for (int qi = 0; qi < 3; ++qi) {
@@ -754,7 +778,8 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
     hc.tpart = wpart + (size_t)kNumSMs * kPartStride + 128;
     if (p.C == 32 && p.levels == 2 && tf <= kTimePartFloats && !getenv("FS4D_HEX_BWD_GENERIC")) {
       const int64_t nblk = ceil_div(ceil_div(K, 32), kHexC32Warps);
-      const int grid = (int)(nblk < kNumSMs ? nblk : kNumSMs);  // one 256-thread CTA per SM (242 registers)
+      const int nres = kNumSMs * FS4D_HEX_BWD_MINB;  // resident 256-thread CTAs
+      const int grid = (int)(nblk < nres ? nblk : nres);
       cudaMemsetAsync(hc.tpart, 0, (size_t)grid * tf * 4, s);
       k_hexplane_bwd_c32<<<grid, kHexC32Warps * 32, 0, s>>>(hc);
       TimeReduceArgs tr;
