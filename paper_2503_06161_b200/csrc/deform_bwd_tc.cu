@@ -507,9 +507,7 @@ struct HexC32Args {
 };
 
 __device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 || q == 5; }
-// plane axes (hexplane.py:16) as compile-time values inside unrolled loops
-__device__ __forceinline__ constexpr int plane_axis0(int q) { return q < 3 ? 0 : (q < 5 ? 1 : 2); }
-__device__ __forceinline__ constexpr int plane_axis1(int q) { return q == 0 ? 1 : (q == 1 || q == 3 ? 2 : 3); }
+
 
 // Time planes: every Gaussian of a frame hits the same t row pair, so their
 // gradients collapse onto Ra spatial rows per plane.  They accumulate with

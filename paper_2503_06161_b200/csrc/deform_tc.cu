@@ -23,7 +23,6 @@
 
 namespace fs4d {
 
-__constant__ int c_axes_tc[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};  // hexplane.py:16
 
 // ---------------------------------------------------------------------------
 // HexPlane latent
@@ -63,7 +62,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent(TcPlan p,
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const int ra = p.res[l][q][0], rb = p.res[l][q][1];
-        const double u = c[c_axes_tc[q][0]] * (ra - 1), v = c[c_axes_tc[q][1]] * (rb - 1);
+        const double u = c[plane_axis0(q)] * (ra - 1), v = c[plane_axis1(q)] * (rb - 1);
         int i0 = (int)floor(u), j0 = (int)floor(v);
         i0 = min(max(i0, 0), ra - 2);
         j0 = min(max(j0, 0), rb - 2);
@@ -122,7 +121,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPla
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const int ra = p.res[l][q][0], rb = p.res[l][q][1];
-        const double u = c[c_axes_tc[q][0]] * (ra - 1), v = c[c_axes_tc[q][1]] * (rb - 1);
+        const double u = c[plane_axis0(q)] * (ra - 1), v = c[plane_axis1(q)] * (rb - 1);
         int i0 = (int)floor(u), j0 = (int)floor(v);
         i0 = min(max(i0, 0), ra - 2);
         j0 = min(max(j0, 0), rb - 2);
@@ -194,14 +193,14 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPl
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const int ra = p.res[l][q][0], rb = p.res[l][q][1];
-        const double u = c[c_axes_tc[q][0]] * (ra - 1);
+        const double u = c[plane_axis0(q)] * (ra - 1);
         int i0 = (int)floor(u);
         i0 = min(max(i0, 0), ra - 2);
         if (q == 2 || q == 4 || q == 5) {
           s_base[warp][l * 6 + q][lane] = i0 * 32;
           s_f[warp][l * 6 + q][lane] = make_float2((float)(u - i0), 0.f);
         } else {
-          const double v = c[c_axes_tc[q][1]] * (rb - 1);
+          const double v = c[plane_axis1(q)] * (rb - 1);
           int j0 = (int)floor(v);
           j0 = min(max(j0, 0), rb - 2);
           s_base[warp][l * 6 + q][lane] = (i0 * rb + j0) * 32;
@@ -449,7 +448,7 @@ __device__ __forceinline__ void produce_latent(const TcArgs& a, int64_t tile, ui
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const int ra = p.res[l][q][0], rb = p.res[l][q][1];
-        const double u = c[c_axes_tc[q][0]] * (ra - 1), v = c[c_axes_tc[q][1]] * (rb - 1);
+        const double u = c[plane_axis0(q)] * (ra - 1), v = c[plane_axis1(q)] * (rb - 1);
         int i0 = (int)floor(u), j0 = (int)floor(v);
         i0 = min(max(i0, 0), ra - 2);
         j0 = min(max(j0, 0), rb - 2);

@@ -292,6 +292,11 @@ constexpr uint32_t kCacheMagic = 0xF54DCAC1u;
 // partial per CTA, [column][lane] then the bias tail.
 constexpr int kDwCols = 384;
 // per-CTA time-plane gradient partials of the HexPlane backward (deform_bwd_tc.cu)
+// plane axes (x,y),(x,z),(x,t),(y,z),(y,t),(z,t) (hexplane.py:16) as
+// compile-time values inside unrolled loops (a __constant__ table index makes
+// the coordinate array dynamically indexed, i.e. local memory)
+__host__ __device__ __forceinline__ constexpr int plane_axis0(int q) { return q < 3 ? 0 : (q < 5 ? 1 : 2); }
+__host__ __device__ __forceinline__ constexpr int plane_axis1(int q) { return q == 0 ? 1 : (q == 1 || q == 3 ? 2 : 3); }
 constexpr int kTimeParts = 2 * 148;
 constexpr int kTimePartFloats = 256 * 1024 / 4;  // upper bound of sum_l 3 * Ra * 32 (= kTimeRowBytes / 4)
 constexpr int kPartStride = kDwCols * kTcRows + 64;
