@@ -965,7 +965,7 @@ int tc_build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPla
 }
 
 int tc_pack(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p, uint8_t* blob, cudaStream_t s) {
-  static TcPackArgs pk;  // large: keep off the stack (host-side, filled per call)
+  static thread_local TcPackArgs pk;  // large: keep off the stack (host-side, filled per call; per host thread)
   int rc = build_plan(n, f, t, p, &pk);
   if (rc) return rc;
   pk.blob = blob;
