@@ -360,3 +360,48 @@ def test_density_control_inside_the_training_step():
     step.run(batch, check=True)  # the next step at the new K
     torch.cuda.synchronize()
     assert len(step.cloud) == rep["count"] and torch.isfinite(step.params.buffer).all()
+
+
+def test_pairs_in_flight_match_serial_step():
+    """TrainStep(lanes=L): pairs j, j+L, ... run on lane j's stream into the
+    lane's gradient buffer (overwritten by its first pair, accumulated by the
+    rest), summed before the reduce; view-space statistics serialised across
+    lanes.  Same gradients, loss and statistics as the serial step up to fp32
+    summation order."""
+    import torch
+    import paper_2503_06161_b200 as fs
+    from paper_2503_06161_b200 import device as dv
+    from paper_2503_06161_b200.train import TrainStep
+
+    rng = np.random.default_rng(5)
+    k, h, w, d = 3000, 48, 64, 8
+    a = random_cloud_arrays(rng, k, d, op_range=(0.05, 0.9), depth_range=(2.0, 4.0), xy=1.0,
+                            ls_range=(0.01, 0.1), sh_degree=1)
+    cloud = fs.GaussianCloud(**a)
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(8, 8, 8, 4), out_dim=64),
+                             fs.scene_aabb(cloud), rng, init="uniform")
+    net = fs.DeformationNet(64, fs.DeformationConfig(width=64, depth=1, feature_dim=d), rng, init="xavier",
+                            head_init="xavier")
+    K = pinhole(h, w, 50.0)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    batch = [(float(t), K, rigid_T(rng), torch.rand(h, w, 3, device="cuda", generator=gen),
+              torch.randn(h, w, d, device="cuda", generator=gen)) for t in np.linspace(0.05, 0.95, 7)]
+    out = {}
+    for lanes in (1, 2, 3):
+        step = TrainStep(dv.DeviceCloud.from_cloud(cloud), dv.DeviceField.from_field(field),
+                         dv.DeviceNet.from_net(net), h, w, fs.RasterConfig(), lanes=lanes)
+        step.track_stats()
+        for _ in range(2):  # the second run reuses the lanes and their caches
+            loss = float(step.run(batch, check=True).item())
+        torch.cuda.synchronize()
+        out[lanes] = (loss, step.grads.buffer.double().cpu().numpy(), step.stats.accum.cpu().numpy(),
+                      step.stats.count.cpu().numpy())
+    ref = out[1]
+    scale = np.abs(ref[1]).max()
+    for lanes in (2, 3):
+        loss, g, acc, cnt = out[lanes]
+        assert abs(loss - ref[0]) < 1e-9 * max(1.0, abs(ref[0]))
+        assert np.abs(g - ref[1]).max() < 1e-5 * scale, (lanes, np.abs(g - ref[1]).max(), scale)
+        np.testing.assert_array_equal(cnt, ref[3])
+        np.testing.assert_allclose(acc, ref[2], rtol=1e-5, atol=1e-9)
