@@ -595,7 +595,10 @@ def main():
         "work": {"visible": r["n_vis"], "pairs": r["n_pairs"]},
         "clocks": r["clocks"],
         "e2e": {"value": frames / (r["e2e_ms"] / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": r["h2d"],
-                "d2h_bytes_per_step": r["d2h"]},
+                "d2h_bytes_per_step": r["d2h"],
+                # the e2e bound: host link bytes per second (PCIe, both directions overlap)
+                "link_gbs": {"h2d": r["h2d"] * frames / (r["e2e_ms"] / 1000.0) / 1e9,
+                             "d2h": r["d2h"] * frames / (r["e2e_ms"] / 1000.0) / 1e9}},
         "gpu_launches": launches_per_frame() * r["steps"],
     })
     if rank == 0 and world == 1 and not args.no_cpu:
