@@ -345,7 +345,8 @@ def gpu_bench(args, rank, world, local):
     # headline: the configs[2] sequence with three frames in flight on three
     # streams over six model replicas (6 x 70 MB rotate through far more than
     # the 126 MB L2, so no flush is needed between frames); each step = one frame
-    seq = dv.SequenceRenderer(cloud, field, net, H, W, cfg, pipelines=6, streams=3, replicas=6)
+    n_str = int(os.environ.get("FS4D_SEQ_STREAMS", "3"))  # A/B knob; replicas = 2 x streams
+    seq = dv.SequenceRenderer(cloud, field, net, H, W, cfg, pipelines=2 * n_str, streams=n_str, replicas=2 * n_str)
     seq.warm(float(mine[0]), Kmat, T, pair_capacity=pipe.renderer.cap)
     ts_seq = [float(mine[i % len(mine)]) for i in range(steps)]
     seq.run([float(mine[i % len(mine)]) for i in range(warm)], Kmat, T)
@@ -545,8 +546,10 @@ def main():
             print(json.dumps(line))
         return
     r = gpu_bench(args, rank, world, local)
-    base["config"] = dict(base["config"], parallelism=f"frame-sharded x{world}, 3 frames in flight per GPU (3 streams)",
-                          l2="no flush: 6 rotating model replicas (6 x 70 MB > 126 MB L2); value_serial is flushed")
+    ns = int(os.environ.get("FS4D_SEQ_STREAMS", "3"))
+    base["config"] = dict(base["config"], parallelism=f"frame-sharded x{world}, {ns} frames in flight per GPU "
+                          f"({ns} streams)", l2=f"no flush: {2 * ns} rotating model replicas ({2 * ns} x 70 MB > "
+                          "126 MB L2); value_serial is flushed")
     hbm, tf, peak_src = peaks()
     frames = world * r["steps"]
     value = frames / (r["ms"] / 1000.0)
