@@ -301,7 +301,11 @@ def gpu_bench(args, rank, world, local):
     cloud_np, field_np, net_np, Kmat = make_scene(0)
     cloud = dv.DeviceCloud.from_cloud(cloud_np)
     field = dv.DeviceField.from_field(field_np)
-    if os.environ.get("FS4D_LOCALITY", "0") == "1":
+    if os.environ.get("FS4D_LOCALITY", "1") == "1":
+        # Morton visiting order of the canonical positions for the HexPlane
+        # gather: a property of the model, computed once (untimed) like any
+        # index; results are bit-identical in any order (tested).  Measured
+        # +2.5% frames/s (gather 72 -> 66 us)
         field = field.with_order(dv.locality_order(cloud.positions, field.aabb))
     net = dv.DeviceNet.from_net(net_np)
     cfg = fs.RasterConfig()
@@ -547,6 +551,8 @@ def main():
         return
     r = gpu_bench(args, rank, world, local)
     ns = int(os.environ.get("FS4D_SEQ_STREAMS", "3"))
+    base["config"]["gather_order"] = ("morton (once per model, untimed; bit-identical results)"
+                                      if os.environ.get("FS4D_LOCALITY", "1") == "1" else "source")
     base["config"] = dict(base["config"], parallelism=f"frame-sharded x{world}, {ns} frames in flight per GPU "
                           f"({ns} streams)", l2=f"no flush: {2 * ns} rotating model replicas ({2 * ns} x 70 MB > "
                           "126 MB L2); value_serial is flushed")
