@@ -368,24 +368,50 @@ struct DwReduceArgs {
   int accumulate;
 };
 
-__global__ void k_reduce_tc_wgrads(DwReduceArgs a) {
+// 32 consecutive gradient entries per block iteration; the 8 warps split the
+// partials (warp g sums parts g, g+8, ... in two interleaved chains) so each
+// thread has ~nparts/8 independent coalesced loads in flight instead of one
+// serial chain of nparts; the 8 warp sums are added in a fixed order
+// (run-to-run deterministic).
+constexpr int kRedGroups = 8;
+__device__ __forceinline__ float sum_parts(const float* wpart, int64_t stride, int nparts, int src, int g) {
+  float s0 = 0.f, s1 = 0.f;
+  int q = g;
+  for (; q + kRedGroups < nparts; q += 2 * kRedGroups) {
+    s0 += wpart[(int64_t)q * stride + src];
+    s1 += wpart[(int64_t)(q + kRedGroups) * stride + src];
+  }
+  if (q < nparts) s0 += wpart[(int64_t)q * stride + src];
+  return s0 + s1;
+}
+
+__global__ void __launch_bounds__(32 * kRedGroups) k_reduce_tc_wgrads(DwReduceArgs a) {
+  __shared__ float part[kRedGroups][33];
   const DwMap& m = a.m[blockIdx.y];
-  const int nw = m.out * m.in;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nw + m.out; e += gridDim.x * blockDim.x) {
-    int src;
-    float* dst;
+  const int nw = m.out * m.in, ne = nw + m.out;
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  for (int e0 = blockIdx.x * 32; e0 < ne; e0 += gridDim.x * 32) {
+    const int e = e0 + lane;
+    int src = 0;
+    float* dst = nullptr;
     if (e < nw) {
       const int o = e / m.in, i = e % m.in;
       src = (m.col0 + o) * kTcRows + m.lane0 + i;
       dst = m.gw + e;
-    } else {
+    } else if (e < ne) {
       const int o = e - nw;
       src = m.bias_lane >= 0 ? (m.col0 + o) * kTcRows + m.bias_lane : kDwCols * kTcRows + m.bias_tail + o;
       dst = m.gb + o;
     }
-    float s = 0.f;
-    for (int q = 0; q < a.nparts; ++q) s += a.wpart[(int64_t)q * kPartStride + src];
-    *dst = a.accumulate ? *dst + s : s;
+    part[g][lane] = dst ? sum_parts(a.wpart, kPartStride, a.nparts, src, g) : 0.f;
+    __syncthreads();
+    if (g == 0 && dst) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kRedGroups; ++w) s += part[w][lane];
+      *dst = a.accumulate ? *dst + s : s;
+    }
+    __syncthreads();
   }
 }
 
@@ -702,20 +728,25 @@ struct TimeReduceArgs {
   float tfb[2];
   float* gp[2][3];
 };
-__global__ void __launch_bounds__(256) k_time_partials(TimeReduceArgs a) {
-  const int e = blockIdx.x * 256 + threadIdx.x;
-  if (e >= a.tfloats) return;
+__global__ void __launch_bounds__(32 * kRedGroups) k_time_partials(TimeReduceArgs a) {
+  __shared__ float part[kRedGroups][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  part[g][lane] = e < a.tfloats ? sum_parts(a.tpart, a.tfloats, a.nparts, e, g) : 0.f;
+  __syncthreads();
+  if (g != 0 || e >= a.tfloats) return;
+  float v = 0.f;
+#pragma unroll
+  for (int w = 0; w < kRedGroups; ++w) v += part[w][lane];
+  if (v == 0.f) return;
   int l = 0, t = 0;
   for (int ll = 0; ll < 2; ++ll)
     for (int tt = 0; tt < 3; ++tt)
       if (e >= a.toff[ll][tt]) l = ll, t = tt;
-  float v = 0.f;
-  for (int q = 0; q < a.nparts; ++q) v += a.tpart[(int64_t)q * a.tfloats + e];
-  if (v == 0.f) return;
   const int loc = e - a.toff[l][t], i = loc >> 5, c = loc & 31, rb = a.rb[l][t];
-  float* g = a.gp[l][t];
-  g[(i * rb + a.tj0[l]) * 32 + c] += v * (1.f - a.tfb[l]);
-  g[(i * rb + a.tj0[l] + 1) * 32 + c] += v * a.tfb[l];
+  float* gp = a.gp[l][t];
+  gp[(i * rb + a.tj0[l]) * 32 + c] += v * (1.f - a.tfb[l]);
+  gp[(i * rb + a.tj0[l] + 1) * 32 + c] += v * a.tfb[l];
 }
 
 // ---------------------------------------------------------------------------
@@ -799,7 +830,7 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
           tr.gp[l][qi] = h.gplanes[l][q];
         }
       }
-      k_time_partials<<<(unsigned)ceil_div(tf, 256), 256, 0, s>>>(tr);
+      k_time_partials<<<(unsigned)ceil_div(tf, 32), 32 * kRedGroups, 0, s>>>(tr);
     } else {
       k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
     }
@@ -830,7 +861,9 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
   r.wpart = wpart;
   r.nparts = K > 0 ? grid : 0;
   r.accumulate = accumulate;
-  k_reduce_tc_wgrads<<<dim3(8, n), 256, 0, s>>>(r);
+  int max_ne = 0;
+  for (int i = 0; i < n; ++i) max_ne = max_ne > r.m[i].out * (r.m[i].in + 1) ? max_ne : r.m[i].out * (r.m[i].in + 1);
+  k_reduce_tc_wgrads<<<dim3((unsigned)ceil_div(max_ne, 32), n), 32 * kRedGroups, 0, s>>>(r);
   return check_launch("deform_bwd_tc");
 }
 
