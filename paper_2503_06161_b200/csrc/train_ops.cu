@@ -102,15 +102,22 @@ __global__ void __launch_bounds__(kThreads) k_photo_grads(const float* __restric
                                                          float* __restrict__ dd, double* __restrict__ terms,
                                                          double* __restrict__ loss) {
   __shared__ long long n_tot[2];
-  if (threadIdx.x == 0) {  // fixed-order reduction of the block partials: deterministic
-    double a = 0.0, b = 0.0;
-    long long na = 0, nb = 0;
-    for (int i = 0; i < n_part; ++i) {
-      a += part[i].sum_rgb;
-      b += part[i].sum_d;
-      na += part[i].n_rgb;
-      nb += part[i].n_d;
-    }
+  // fixed-order reduction of the block partials (thread t takes partials t,
+  // t + 256, ...; then the fixed block tree): deterministic, and parallel --
+  // one thread walking all partials was a serial chain of n_part loads
+  double a = 0.0, b = 0.0;
+  long long na = 0, nb = 0;
+  for (int i = threadIdx.x; i < n_part; i += kThreads) {
+    a += part[i].sum_rgb;
+    b += part[i].sum_d;
+    na += part[i].n_rgb;
+    nb += part[i].n_d;
+  }
+  a = block_sum_d(a);
+  b = block_sum_d(b);
+  na = block_sum_i(na);
+  nb = block_sum_i(nb);
+  if (threadIdx.x == 0) {
     n_tot[0] = na, n_tot[1] = nb;
     const double rgb = na ? a / (double)na : 0.0, dterm = nb ? b / (double)nb : 0.0;
     if (blockIdx.x == 0 && terms) {
@@ -428,6 +435,54 @@ __global__ void __launch_bounds__(kThreads) k_resize_adj(const float* __restrict
   }
 }
 
+// Same gather with one thread per (row a, input index i, chunk of CH channels):
+// the two monotone-range searches (fp64 axis positions, exactly those of
+// axis_lo) run once per thread instead of once per channel, and the channel
+// chunk moves as float4.  Per element the terms are added in the same order
+// as k_resize_adj, so the results are identical.  Needs C % 4 == 0 and
+// 16-byte aligned buffers.
+constexpr int kAdjChunk = 32;
+__global__ void __launch_bounds__(kThreads) k_resize_adj_v(const float* __restrict__ d_out, int A, int n_out, int C,
+                                                          float* __restrict__ d_in, int n_in) {
+  const int nch = (C + kAdjChunk - 1) / kAdjChunk;
+  const int64_t n = (int64_t)A * n_in * nch;
+  for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < n; t += (int64_t)gridDim.x * kThreads) {
+    const int ch = (int)(t % nch);
+    const int64_t r = t / nch;
+    const int i = (int)(r % n_in);
+    const int64_t a = r / n_in;
+    const int c0 = ch * kAdjChunk, cn = min(kAdjChunk, C - c0);
+    const float* src = d_out + a * (int64_t)n_out * C + c0;
+    float4 acc[kAdjChunk / 4];
+#pragma unroll
+    for (int q = 0; q < kAdjChunk / 4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto add = [&](int o, float w) {
+      const float4* row = reinterpret_cast<const float4*>(src + (int64_t)o * C);
+#pragma unroll
+      for (int q = 0; q < kAdjChunk / 4; ++q)
+        if (4 * q < cn) {
+          const float4 v = __ldg(row + q);
+          acc[q] = make_float4(acc[q].x + v.x * w, acc[q].y + v.y * w, acc[q].z + v.z * w, acc[q].w + v.w * w);
+        }
+    };
+    for (int o = axis_lower_bound(i, false, n_in, n_out); o < n_out; ++o) {
+      float f;
+      if (axis_lo(o, n_in, n_out, &f) != i) break;
+      add(o, 1.f - f);
+    }
+    for (int o = axis_lower_bound(i, true, n_in, n_out); o < n_out; ++o) {
+      float f;
+      const int lo = axis_lo(o, n_in, n_out, &f);
+      if (min(lo + 1, n_in - 1) != i) break;
+      add(o, f);
+    }
+    float4* dst = reinterpret_cast<float4*>(d_in + (a * n_in + i) * (int64_t)C + c0);
+#pragma unroll
+    for (int q = 0; q < kAdjChunk / 4; ++q)
+      if (4 * q < cn) dst[q] = acc[q];
+  }
+}
+
 static int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kThreads), kNumSMs * 8)); }
 
 int resize_bilinear(const float* in, int hi, int wi, int C, float* out, int ho, int wo, cudaStream_t s) {
@@ -444,6 +499,14 @@ int resize_bilinear_backward(const float* d_out, int ho, int wo, int C, float* d
   // semantic.py:107-123: columns first (d_rows [ho, wi, C]), then rows.
   int64_t n = (int64_t)ho * wi * C;
   if (n == 0 || (int64_t)hi * wi * C == 0) return FS4D_OK;
+  const bool vec = C % 4 == 0 && ((reinterpret_cast<uintptr_t>(d_out) | reinterpret_cast<uintptr_t>(d_in) |
+                                    reinterpret_cast<uintptr_t>(rows)) & 15) == 0;
+  if (vec) {
+    k_resize_adj_v<<<grid_for((int64_t)ho * wi * ceil_div(C, kAdjChunk)), kThreads, 0, s>>>(d_out, ho, wo, C, rows, wi);
+    k_resize_adj_v<<<grid_for((int64_t)hi * ceil_div((int64_t)wi * C, kAdjChunk)), kThreads, 0, s>>>(rows, 1, ho, wi * C,
+                                                                                                  d_in, hi);
+    return check_launch("resize_bilinear_backward");
+  }
   k_resize_adj<<<grid_for(n), kThreads, 0, s>>>(d_out, ho, wo, C, rows, wi);
   n = (int64_t)hi * wi * C;
   k_resize_adj<<<grid_for(n), kThreads, 0, s>>>(rows, 1, ho, wi * C, d_in, hi);
