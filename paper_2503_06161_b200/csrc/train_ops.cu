@@ -237,13 +237,23 @@ __global__ void __launch_bounds__(kThreads) k_adam_apply(const __grid_constant__
   const int s = adam_segment_of(T, blockIdx.x);
   const Fs4dAdamSegment& S = T.seg[s];
   if (threadIdx.x == 0) {
-    const int step = steps[s] + 1;  // AdamState.step_count += 1 (numerics.py:154)
-    s_coef[0] = (float)(1.0 - pow(S.beta1, (double)step));
-    s_coef[1] = (float)(1.0 - pow(S.beta2, (double)step));
+    // AdamState.step_count += 1 (numerics.py:154); beta^step by binary
+    // powering in fp64 (~2 log2(step) multiplies, a few hundred cycles, where
+    // the libm pow() call stalled every block for microseconds)
+    int e = steps[s] + 1;
+    double p1 = 1.0, p2 = 1.0, b1d = S.beta1, b2d = S.beta2;
+    while (e) {
+      if (e & 1) p1 *= b1d, p2 *= b2d;
+      b1d *= b1d;
+      b2d *= b2d;
+      e >>= 1;
+    }
+    s_coef[0] = (float)(1.0 / (1.0 - p1));
+    s_coef[1] = (float)(1.0 / (1.0 - p2));
   }
   __syncthreads();
   const float b1 = (float)S.beta1, b2 = (float)S.beta2, c1 = (float)(1.0 - S.beta1), c2 = (float)(1.0 - S.beta2);
-  const float bc1 = s_coef[0], bc2 = s_coef[1], lr = (float)S.lr, eps = (float)S.eps;
+  const float rbc1 = s_coef[0], rbc2 = s_coef[1], lr = (float)S.lr, eps = (float)S.eps;
   const int64_t lo = S.offset + (blockIdx.x - T.block_start[s]) * (int64_t)kAdamChunk;
   const int64_t hi = min(lo + kAdamChunk, S.offset + S.count);
 #pragma unroll 4
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(kThreads) k_adam_apply(const __grid_constant__
     const float vi = b2 * v[i] + c2 * gi * gi;
     m[i] = mi;
     v[i] = vi;
-    const float mh = mi / bc1, vh = vi / bc2;
+    const float mh = mi * rbc1, vh = vi * rbc2;
     p[i] = p[i] - lr * mh / (sqrtf(vh) + eps);
   }
   // the last block to finish advances every segment's step count
@@ -667,14 +677,32 @@ __global__ void __launch_bounds__(kThreads) k_decode_bwd(const float* __restrict
 }
 
 // fixed-order sum of the per-block partials into d_weight [Ct,N] / d_bias [Ct]
+// 32 accumulators per block; the 8 warps split the per-CTA partials (warp g
+// sums partials g, g+8, ...) and are combined in a fixed order: deterministic,
+// with ~nblk/8 independent loads per thread instead of a serial chain of nblk
 __global__ void __launch_bounds__(kThreads) k_decode_reduce(const float* __restrict__ partials, int nblk, int Ct,
                                                            int N, float* __restrict__ dw, float* __restrict__ db,
                                                            int accumulate) {
+  constexpr int G = kThreads / 32;
+  __shared__ float part[G][33];
   const int nacc = Ct * (N + 1);
-  const int e = blockIdx.x * kThreads + threadIdx.x;
-  if (e >= nacc) return;
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  float s0 = 0.f, s1 = 0.f;
+  if (e < nacc) {
+    int i = g;
+    for (; i + G < nblk; i += 2 * G) {
+      s0 += partials[(int64_t)i * nacc + e];
+      s1 += partials[(int64_t)(i + G) * nacc + e];
+    }
+    if (i < nblk) s0 += partials[(int64_t)i * nacc + e];
+  }
+  part[g][lane] = s0 + s1;
+  __syncthreads();
+  if (g != 0 || e >= nacc) return;
   float s = 0.f;
-  for (int i = 0; i < nblk; ++i) s += partials[(int64_t)i * nacc + e];
+#pragma unroll
+  for (int w = 0; w < G; ++w) s += part[w][lane];
   const int ct = e / (N + 1), n = e - ct * (N + 1);
   float* dst = n < N ? dw + ct * N + n : db + ct;
   *dst = accumulate ? *dst + s : s;
@@ -749,7 +777,7 @@ static int dec_backward_common(const DecShape& S, const float* d_out_or_teacher,
                                                      nullptr);
   }
   const int nacc = S.Ct * (S.N + 1);
-  k_decode_reduce<<<(unsigned)ceil_div(nacc, kThreads), kThreads, 0, s>>>(partials, grid, S.Ct, S.N, dw, db,
+  k_decode_reduce<<<(unsigned)ceil_div(nacc, 32), kThreads, 0, s>>>(partials, grid, S.Ct, S.N, dw, db,
                                                                           accumulate);
   if (int rc = check_launch("decoder backward")) return rc;
   return resize_bilinear_backward(d_res, S.ho, S.wo, S.N, d_rendered, S.hi, S.wi, rows, s);
