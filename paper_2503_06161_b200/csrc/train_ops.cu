@@ -256,15 +256,40 @@ __global__ void __launch_bounds__(kThreads) k_adam_apply(const __grid_constant__
   const float rbc1 = s_coef[0], rbc2 = s_coef[1], lr = (float)S.lr, eps = (float)S.eps;
   const int64_t lo = S.offset + (blockIdx.x - T.block_start[s]) * (int64_t)kAdamChunk;
   const int64_t hi = min(lo + kAdamChunk, S.offset + S.count);
-#pragma unroll 4
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
-    const float gi = g[i];
-    const float mi = b1 * m[i] + c1 * gi;
-    const float vi = b2 * v[i] + c2 * gi * gi;
+  auto upd = [&](float gi, float& mi, float& vi, float& pi) {
+    mi = b1 * mi + c1 * gi;
+    vi = b2 * vi + c2 * gi * gi;
+    const float mh = mi * rbc1, vh = vi * rbc2;
+    pi = pi - lr * mh / (sqrtf(vh) + eps);
+  };
+  // float4 body (segment offsets are 64-byte aligned by FlatGrads / FlatAdam;
+  // checked), scalar tail
+  int64_t i0 = lo;
+  if ((lo & 3) == 0 && ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                         reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0) {
+    const int64_t n4 = (hi - lo) >> 2;
+#pragma unroll 2
+    for (int64_t q = threadIdx.x; q < n4; q += kThreads) {
+      const int64_t i = lo + 4 * q;
+      const float4 gq = *reinterpret_cast<const float4*>(g + i);
+      float4 mq = *reinterpret_cast<const float4*>(m + i), vq = *reinterpret_cast<const float4*>(v + i);
+      float4 pq = *reinterpret_cast<const float4*>(p + i);
+      upd(gq.x, mq.x, vq.x, pq.x);
+      upd(gq.y, mq.y, vq.y, pq.y);
+      upd(gq.z, mq.z, vq.z, pq.z);
+      upd(gq.w, mq.w, vq.w, pq.w);
+      *reinterpret_cast<float4*>(m + i) = mq;
+      *reinterpret_cast<float4*>(v + i) = vq;
+      *reinterpret_cast<float4*>(p + i) = pq;
+    }
+    i0 = lo + 4 * n4;
+  }
+  for (int64_t i = i0 + threadIdx.x; i < hi; i += kThreads) {
+    float mi = m[i], vi = v[i], pi = p[i];
+    upd(g[i], mi, vi, pi);
     m[i] = mi;
     v[i] = vi;
-    const float mh = mi * rbc1, vh = vi * rbc2;
-    p[i] = p[i] - lr * mh / (sqrtf(vh) + eps);
+    p[i] = pi;
   }
   // the last block to finish advances every segment's step count
   __syncthreads();
