@@ -257,9 +257,15 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
 // Same replay with PX vertically adjacent pixels per thread (256/PX threads
 // per tile, a warp covers 2*PX pixel rows).  The per-Gaussian warp reduction
 // -- the kernel's dominant cost -- is then shared by PX times as many pixels.
-template <int DC, int PX>
-__global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
-  constexpr int NT = kTilePixels / PX;
+template <int SUBB>
+__device__ __forceinline__ int ty_sub_rows(int sub) { return sub * (kTile / SUBB); }
+
+// SUBB > 1 splits a tile's rows over SUBB CTAs (each replays the whole list
+// for its 16/SUBB rows): CTAs of one or two warps have no cross-warp batch
+// barrier to wait on, and more of them fit per SM.
+template <int DC, int PX, int SUBB>
+__global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs a) {
+  constexpr int NT = kTilePixels / PX / SUBB;
   constexpr int B = NT;  // Gaussians staged per batch
   constexpr int NF = DC > 0 ? DC : 1;
   __shared__ float2 s_xy[B];
@@ -273,10 +279,11 @@ __global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
   __shared__ __align__(16) float s_red[NT / 32][NROW * kRedRowStride];
   __shared__ int s_maxlast;
 
-  const int tile = a.tperm ? a.tperm[blockIdx.x] : blockIdx.x;
+  const int tile = a.tperm ? a.tperm[blockIdx.x / SUBB] : blockIdx.x / SUBB;
+  const int rsub = ty_sub_rows<SUBB>(blockIdx.x % SUBB);
   const int tx = tile % a.ntx, ty = tile / a.ntx;
   const int col = tx * kTile + (threadIdx.x & (kTile - 1));
-  const int row0 = ty * kTile + (threadIdx.x / kTile) * PX;
+  const int row0 = ty * kTile + rsub + (threadIdx.x / kTile) * PX;
   float* wred = s_red[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const uint2 rg = a.ranges[tile];
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kTilePixels / PX) k_blend_bwd2(BwdArgs a) {
   const int maxlast = s_maxlast;
   if (maxlast < (int)rg.x) return;
   const int wlast = __reduce_max_sync(0xffffffffu, mylast);
-  const int wrow0 = ty * kTile + (threadIdx.x >> 5) * 2 * PX;  // this warp's 2*PX pixel rows
+  const int wrow0 = ty * kTile + rsub + (threadIdx.x >> 5) * 2 * PX;  // this warp's 2*PX pixel rows
   const int tcol0 = tx * kTile;
 
   const int nv = a.nvals;
@@ -694,18 +701,35 @@ static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t 
       default: k_blend_bwd<64><<<ntiles, kTilePixels, 0, s>>>(a); break;
     }
   } else if (px == 2) {
-    switch (dc) {
-      case 0: k_blend_bwd2<0, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
-      case 4: k_blend_bwd2<4, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
-      case 8: k_blend_bwd2<8, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
-      default: k_blend_bwd2<16, 2><<<ntiles, kTilePixels / 2, 0, s>>>(a); break;
+    // CTAs per tile (FS4D_BLEND_BWD_SUB = 1, 2 or 4)
+    static const int subb = [] {
+      const char* e = getenv("FS4D_BLEND_BWD_SUB");
+      const int v = e ? atoi(e) : 2;  // measured (configs[4]): 1 -> 285 us, 2 -> 275 us, 4 -> 307 us
+      return v == 1 || v == 4 ? v : 2;
+    }();
+#define FS4D_BWD2(D, SB) k_blend_bwd2<D, 2, SB><<<ntiles * SB, kTilePixels / 2 / SB, 0, s>>>(a)
+#define FS4D_BWD2_DC(SB)            \
+  switch (dc) {                     \
+    case 0: FS4D_BWD2(0, SB); break;  \
+    case 4: FS4D_BWD2(4, SB); break;  \
+    case 8: FS4D_BWD2(8, SB); break;  \
+    default: FS4D_BWD2(16, SB); break; \
+  }
+    if (subb == 4) {
+      FS4D_BWD2_DC(4)
+    } else if (subb == 2) {
+      FS4D_BWD2_DC(2)
+    } else {
+      FS4D_BWD2_DC(1)
     }
+#undef FS4D_BWD2_DC
+#undef FS4D_BWD2
   } else {
     switch (dc) {
-      case 0: k_blend_bwd2<0, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
-      case 4: k_blend_bwd2<4, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
-      case 8: k_blend_bwd2<8, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
-      default: k_blend_bwd2<16, 4><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+      case 0: k_blend_bwd2<0, 4, 1><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+      case 4: k_blend_bwd2<4, 4, 1><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+      case 8: k_blend_bwd2<8, 4, 1><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
+      default: k_blend_bwd2<16, 4, 1><<<ntiles, kTilePixels / 4, 0, s>>>(a); break;
     }
   }
 }
