@@ -17,20 +17,28 @@ __global__ void __launch_bounds__(256) k_l1_loss_grad(const float* __restrict__ 
   __shared__ double red[8];
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  float part = 0.f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_rgb; i += stride) {
-    const float d = c[i] - ct[i];
-    dc[i] = g_rgb * sgn(d);
-    part += fabsf(d);
-  }
-  acc += (double)part * g_rgb;
-  part = 0.f;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_feat; i += stride) {
-    const float d = f[i] - ft[i];
-    df[i] = g_feat * sgn(d);
-    part += fabsf(d);
-  }
-  acc += (double)part * g_feat;
+  // float4 main part (16-byte aligned tensors), scalar tail
+  auto pass = [&](const float* x, const float* y, float* g, int64_t n, float gs) {
+    float part = 0.f;
+    int64_t n4 = 0;
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(g)) & 15) == 0) {
+      n4 = n >> 2;
+      for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
+        const float4 a = reinterpret_cast<const float4*>(x)[q], b = reinterpret_cast<const float4*>(y)[q];
+        const float d0 = a.x - b.x, d1 = a.y - b.y, d2 = a.z - b.z, d3 = a.w - b.w;
+        reinterpret_cast<float4*>(g)[q] = make_float4(gs * sgn(d0), gs * sgn(d1), gs * sgn(d2), gs * sgn(d3));
+        part += fabsf(d0) + fabsf(d1) + fabsf(d2) + fabsf(d3);
+      }
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const float d = x[i] - y[i];
+      g[i] = gs * sgn(d);
+      part += fabsf(d);
+    }
+    return (double)part * gs;
+  };
+  acc += pass(c, ct, dc, n_rgb, g_rgb);
+  if (n_feat > 0) acc += pass(f, ft, df, n_feat, g_feat);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
