@@ -301,12 +301,14 @@ def transmittance(alpha, stop):
     return t_before, contrib, w, t_final
 
 
-def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None):
+def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None, margins=False):
     """Colour/depth/feature/alpha + per-pixel live-contributor counts.
 
     tile_rows: optional iterable of tile-row indices to composite (used by the
     bounded CPU baseline); other pixels stay at background.
-    prepared: optional (proj, lists) from project()/bin_tiles() to reuse."""
+    prepared: optional (proj, lists) from project()/bin_tiles() to reuse.
+    margins: also return the per-pixel decision margins (pixel_decision_margins)
+    computed in the same tile loop (out["margins"])."""
     if prepared is None:
         proj = project(cloud, K, T, height, width, cfg)
         lists = bin_tiles(proj, height, width, cfg.tile)
@@ -319,6 +321,7 @@ def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None):
     feature = np.zeros((height, width, n))
     tfin = np.ones((height, width))
     ncontrib = np.zeros((height, width), dtype=np.int64)
+    margin = np.full((height, width), np.inf) if margins else None
     tiles = {}
     rows_to_do = range(len(lists)) if tile_rows is None else tile_rows
     for ty in rows_to_do:
@@ -328,8 +331,11 @@ def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None):
                 continue
             xs = np.arange(tx * tile, min(tx * tile + tile, width))
             alpha, g, a_raw, dx, dy, q, inside = tile_alpha(proj, rows, xs, ys, cfg)
-            _, contrib, w, t_final = transmittance(alpha, cfg.stop_transmittance)
+            t_before, contrib, w, t_final = transmittance(alpha, cfg.stop_transmittance)
             shp = (ys.size, xs.size)
+            if margins:
+                margin[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1] = \
+                    _tile_margins(alpha, a_raw, q, inside, t_before, cfg).min(axis=0).reshape(shp)
             sl = (slice(ys[0], ys[-1] + 1), slice(xs[0], xs[-1] + 1))
             color[sl] = (w.T @ proj["color"][rows]).reshape(shp + (3,))
             depth[sl] = (w.T @ proj["view_depth"][rows]).reshape(shp)
@@ -339,8 +345,11 @@ def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None):
             ncontrib[sl] = (contrib & (alpha > 0)).sum(axis=0).reshape(shp)
             tiles[(ty, tx)] = (rows, xs, ys)
     color = color + tfin[:, :, None] * cfg.background[None, None, :]
-    return {"color": color, "depth": depth, "feature": feature, "alpha": 1.0 - tfin,
-            "n_contrib": ncontrib, "proj": proj, "tiles": tiles, "t_final": tfin}
+    out = {"color": color, "depth": depth, "feature": feature, "alpha": 1.0 - tfin,
+           "n_contrib": ncontrib, "proj": proj, "tiles": tiles, "t_final": tfin}
+    if margins:
+        out["margins"] = margin
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -704,27 +713,35 @@ def projection_margins(proj, height, width, tile, cfg):
     return m
 
 
+def _tile_margins(alpha, a_raw, q, inside, t_before, cfg):
+    """[G, P] relative margins of one tile's fp32 blend decisions (see
+    pixel_decision_margins); rows the traversal cannot reach are inf."""
+    reach = t_before >= cfg.stop_transmittance * 0.5  # rows the traversal can see
+    mm = np.where(inside | (q > Q_SKIP), np.abs(q - Q_SKIP) / Q_SKIP, np.inf)
+    am = np.minimum(a_raw, cfg.alpha_cap)
+    mm = np.minimum(mm, np.where(inside, np.abs(am - cfg.alpha_skip) / cfg.alpha_skip, np.inf))
+    mm = np.minimum(mm, np.where(inside, np.abs(a_raw - cfg.alpha_cap) / cfg.alpha_cap, np.inf))
+    t_after = t_before * (1.0 - alpha)
+    mm = np.minimum(mm, np.where(alpha > 0, np.abs(t_after - cfg.stop_transmittance)
+                                 / cfg.stop_transmittance, np.inf))
+    return np.where(reach, mm, np.inf)
+
+
 def pixel_decision_margins(out, cfg):
     """Per pixel: the smallest relative margin of any fp32-evaluated blend
     decision met while compositing it (alpha-skip, alpha-cap, q-skip, stop).
     The square-footprint test is decided from fp64 integer bounds on device
-    and is covered by projection_margins."""
+    and is covered by projection_margins.  render(..., margins=True) computes
+    the same array in its own tile loop (out["margins"])."""
+    if "margins" in out:
+        return out["margins"]
     proj = out["proj"]
     h, w = out["t_final"].shape
     margin = np.full((h, w), np.inf)
     for (ty, tx), (rows, xs, ys) in out["tiles"].items():
         alpha, g, a_raw, dx, dy, q, inside = tile_alpha(proj, rows, xs, ys, cfg)
         t_before, contrib, wts, t_final = transmittance(alpha, cfg.stop_transmittance)
-        reach = t_before >= cfg.stop_transmittance * 0.5  # rows the traversal can see
-        mm = np.full(alpha.shape, np.inf)
-        mm = np.minimum(mm, np.where(inside | (q > Q_SKIP), np.abs(q - Q_SKIP) / Q_SKIP, np.inf))
-        am = np.minimum(a_raw, cfg.alpha_cap)
-        mm = np.minimum(mm, np.where(inside, np.abs(am - cfg.alpha_skip) / cfg.alpha_skip, np.inf))
-        mm = np.minimum(mm, np.where(inside, np.abs(a_raw - cfg.alpha_cap) / cfg.alpha_cap, np.inf))
-        t_after = t_before * (1.0 - alpha)
-        mm = np.minimum(mm, np.where(alpha > 0, np.abs(t_after - cfg.stop_transmittance)
-                                     / cfg.stop_transmittance, np.inf))
-        mm = np.where(reach, mm, np.inf)
+        mm = _tile_margins(alpha, a_raw, q, inside, t_before, cfg)
         sl = (slice(ys[0], ys[-1] + 1), slice(xs[0], xs[-1] + 1))
         margin[sl] = mm.min(axis=0).reshape(ys.size, xs.size) if rows.size else np.inf
     return margin

@@ -17,7 +17,6 @@ state (meta.config INI, meta.rng, frame schedule) belongs to the training
 driver, which is out of scope; callers pass those entries through `meta`.
 """
 
-import io
 import struct
 
 import numpy as np
@@ -26,84 +25,119 @@ from .errors import FormatError
 
 CHECKPOINT_MAGIC = b"FS4C"
 CHECKPOINT_VERSION = 1
-_KIND_ARRAY, _KIND_BYTES, _KIND_INT, _KIND_FLOAT = 0, 1, 2, 3
+# entry kinds (training.py:569-596): array, raw bytes, int64, float64
+KIND_ARRAY, KIND_BYTES, KIND_INT, KIND_FLOAT = 0, 1, 2, 3
+
+_U16, _U32, _U64, _I64, _F64 = (struct.Struct(f) for f in ("<H", "<I", "<Q", "<q", "<d"))
 
 
-def _write_entry(buf, name, value):
-    nb = name.encode()
-    buf.write(struct.pack("<H", len(nb)))
-    buf.write(nb)
+def _kind_of(value):
+    """Entry kind for a Python / NumPy value (bool and NumPy integers are
+    ints; Python and NumPy float64 scalars are floats; anything else is an
+    array, including 0-d and non-float64 scalars)."""
     if isinstance(value, (bool, int, np.integer)):
-        buf.write(struct.pack("<bq", _KIND_INT, int(value)))
-    elif isinstance(value, float):
-        buf.write(struct.pack("<bd", _KIND_FLOAT, value))
-    elif isinstance(value, bytes):
-        buf.write(struct.pack("<bQ", _KIND_BYTES, len(value)))
-        buf.write(value)
-    else:
-        arr = np.ascontiguousarray(value)
-        dt = arr.dtype.str.encode()
-        buf.write(struct.pack("<bB", _KIND_ARRAY, len(dt)))
-        buf.write(dt)
-        buf.write(struct.pack("<B", arr.ndim))
-        for dim in arr.shape:
-            buf.write(struct.pack("<Q", dim))
-        buf.write(arr.tobytes(order="C"))
+        return KIND_INT
+    if isinstance(value, float):
+        return KIND_FLOAT
+    if isinstance(value, (bytes, bytearray)):
+        return KIND_BYTES
+    return KIND_ARRAY
+
+
+def _payload(kind, value):
+    if kind == KIND_INT:
+        return _I64.pack(int(value))
+    if kind == KIND_FLOAT:
+        return _F64.pack(float(value))
+    if kind == KIND_BYTES:
+        return _U64.pack(len(value)) + bytes(value)
+    arr = np.ascontiguousarray(value)
+    tag = arr.dtype.str.encode("ascii")
+    dims = np.asarray(arr.shape, dtype="<u8").tobytes()
+    return bytes((len(tag),)) + tag + bytes((arr.ndim,)) + dims + arr.tobytes()
 
 
 def encode_entries(entries):
-    buf = io.BytesIO()
-    buf.write(CHECKPOINT_MAGIC)
-    buf.write(struct.pack("<IQ", CHECKPOINT_VERSION, len(entries)))
+    """FS4C bytes: magic, u32 version, u64 count, then the entries in sorted
+    name order as (u16 name length, UTF-8 name, i8 kind, payload)."""
+    chunks = [CHECKPOINT_MAGIC, _U32.pack(CHECKPOINT_VERSION), _U64.pack(len(entries))]
     for name in sorted(entries):
-        _write_entry(buf, name, entries[name])
-    return buf.getvalue()
+        key = name.encode("utf-8")
+        kind = _kind_of(entries[name])
+        chunks += [_U16.pack(len(key)), key, struct.pack("<b", kind), _payload(kind, entries[name])]
+    return b"".join(chunks)
 
 
 def write_entries(path, entries):
+    blob = encode_entries(entries)
     with open(path, "wb") as fh:
-        fh.write(encode_entries(entries))
+        fh.write(blob)
 
 
-def _read_exact(fh, n, what):
-    data = fh.read(n)
-    if len(data) != n:
-        raise FormatError(f"truncated checkpoint while reading {what}", offset=fh.tell())
-    return data
+class _Cursor:
+    """Bounds-checked little-endian reads over an in-memory FS4C image."""
+
+    def __init__(self, blob):
+        self.blob = memoryview(blob)
+        self.pos = 0
+
+    def take(self, n, what):
+        end = self.pos + n
+        if end > len(self.blob):
+            raise FormatError(f"truncated FS4C data: {what} needs {n} bytes, {len(self.blob) - self.pos} left",
+                              offset=self.pos)
+        view = self.blob[self.pos:end]
+        self.pos = end
+        return view
+
+    def unpack(self, st, what):
+        return st.unpack(self.take(st.size, what))[0]
+
+
+def _read_array(cur, name):
+    tag = bytes(cur.take(cur.take(1, name)[0], name)).decode("ascii")
+    ndim = cur.take(1, name)[0]
+    shape = tuple(int(d) for d in np.frombuffer(cur.take(8 * ndim, name), dtype="<u8"))
+    dtype = np.dtype(tag)
+    count = int(np.prod(shape, dtype=np.int64))
+    return np.frombuffer(cur.take(dtype.itemsize * count, name), dtype=dtype).reshape(shape).copy()
+
+
+_READERS = {
+    KIND_INT: lambda cur, name: cur.unpack(_I64, name),
+    KIND_FLOAT: lambda cur, name: cur.unpack(_F64, name),
+    KIND_BYTES: lambda cur, name: bytes(cur.take(cur.unpack(_U64, name), name)),
+    KIND_ARRAY: _read_array,
+}
+
+
+def decode_entries(blob, source="<bytes>"):
+    """Inverse of encode_entries; FormatError (byte offset attached) on a bad
+    magic, an unsupported version, an unknown kind or truncation
+    (training.py:640-674)."""
+    cur = _Cursor(blob)
+    if bytes(cur.blob[:4]) != CHECKPOINT_MAGIC:
+        raise FormatError(f"{source} is not an FS4C checkpoint", offset=0)
+    cur.pos = 4
+    version = cur.unpack(_U32, "header")
+    if version != CHECKPOINT_VERSION:
+        raise FormatError(f"FS4C version {version} is not supported (want {CHECKPOINT_VERSION})", offset=4)
+    count = cur.unpack(_U64, "header")
+    out = {}
+    for _ in range(count):
+        name = bytes(cur.take(cur.unpack(_U16, "entry name length"), "entry name")).decode("utf-8")
+        kind = struct.unpack("<b", cur.take(1, name))[0]
+        reader = _READERS.get(kind)
+        if reader is None:
+            raise FormatError(f"entry {name!r} has unknown kind {kind}", offset=cur.pos)
+        out[name] = reader(cur, name)
+    return out
 
 
 def load_entries(path):
-    """Entries dict of an FS4C file; FormatError (with byte offset) on a
-    bad magic, version, kind or a truncated file (training.py:640-674)."""
+    """Entries dict of an FS4C file."""
     with open(path, "rb") as fh:
-        if fh.read(4) != CHECKPOINT_MAGIC:
-            raise FormatError(f"bad checkpoint magic in {path!r}", offset=0)
-        version, count = struct.unpack("<IQ", _read_exact(fh, 12, "header"))
-        if version != CHECKPOINT_VERSION:
-            raise FormatError(f"unsupported checkpoint version {version}", offset=4)
-        entries = {}
-        for _ in range(count):
-            (nlen,) = struct.unpack("<H", _read_exact(fh, 2, "name length"))
-            name = _read_exact(fh, nlen, "name").decode()
-            (kind,) = struct.unpack("<b", _read_exact(fh, 1, "kind"))
-            if kind == _KIND_INT:
-                (entries[name],) = struct.unpack("<q", _read_exact(fh, 8, name))
-            elif kind == _KIND_FLOAT:
-                (entries[name],) = struct.unpack("<d", _read_exact(fh, 8, name))
-            elif kind == _KIND_BYTES:
-                (blen,) = struct.unpack("<Q", _read_exact(fh, 8, name))
-                entries[name] = _read_exact(fh, blen, name)
-            elif kind == _KIND_ARRAY:
-                (dlen,) = struct.unpack("<B", _read_exact(fh, 1, name))
-                dtype = np.dtype(_read_exact(fh, dlen, name).decode())
-                (ndim,) = struct.unpack("<B", _read_exact(fh, 1, name))
-                shape = struct.unpack(f"<{ndim}Q", _read_exact(fh, 8 * ndim, name))
-                n = int(np.prod(shape, dtype=np.int64)) if ndim else 1
-                raw = _read_exact(fh, dtype.itemsize * n, name)
-                entries[name] = np.frombuffer(raw, dtype=dtype).reshape(shape).copy()
-            else:
-                raise FormatError(f"unknown entry kind {kind} for {name!r}", offset=fh.tell())
-        return entries
+        return decode_entries(fh.read(), repr(path))
 
 
 # ---------------------------------------------------------------------------

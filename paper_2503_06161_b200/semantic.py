@@ -10,7 +10,6 @@ in libfs4d (csrc/train_ops.cu); there is no CPU fallback.
 """
 
 import ctypes
-import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -25,34 +24,39 @@ FORMAT_VERSION = 1   # semantic.py:18
 
 
 # ---------------------------------------------------------------------------
-# FE4D feature container (semantic.py:21-75): host file format
+# FE4D feature container (semantic.py:17-75): host file format
 # ---------------------------------------------------------------------------
-@dataclass
+# The 18-byte header as one packed little-endian record; the payload follows
+# as C*H*W little-endian float32 in channel-major order.
+_FE4D_HEADER = np.dtype([("magic", "S4"), ("version", "<u2"), ("channels", "<u4"),
+                         ("height", "<u4"), ("width", "<u4")])
+assert _FE4D_HEADER.itemsize == 18
+
+
 class FeatureMap:
-    """Dense C x H x W teacher feature map, float32 (semantic.py:21-46)."""
+    """Teacher feature map, float32 [C, H, W] (semantic.py:21-46)."""
 
-    data: np.ndarray
+    __slots__ = ("data",)
 
-    def __post_init__(self):
-        if self.data.ndim != 3 or min(self.data.shape) < 1:
+    def __init__(self, data):
+        arr = np.asarray(data)
+        if arr.ndim != 3 or 0 in arr.shape:
             raise ConfigurationError("feature map must be [C, H, W] with positive dims")
-        self.data = np.ascontiguousarray(self.data, dtype=np.float32)
+        self.data = np.ascontiguousarray(arr, dtype=np.float32)
 
-    @property
-    def channels(self):
-        return self.data.shape[0]
+    def __repr__(self):
+        return f"FeatureMap(channels={self.channels}, height={self.height}, width={self.width})"
 
-    @property
-    def height(self):
-        return self.data.shape[1]
+    def __eq__(self, other):
+        return isinstance(other, FeatureMap) and np.array_equal(self.data, other.data)
 
-    @property
-    def width(self):
-        return self.data.shape[2]
+    channels = property(lambda self: int(self.data.shape[0]))
+    height = property(lambda self: int(self.data.shape[1]))
+    width = property(lambda self: int(self.data.shape[2]))
 
     def hwc(self):
-        """Float64 [H, W, C] view for arithmetic."""
-        return np.transpose(self.data, (1, 2, 0)).astype(np.float64)
+        """Float64 [H, W, C] copy for arithmetic."""
+        return self.data.transpose(1, 2, 0).astype(np.float64)
 
     def to_device(self, device="cuda"):
         """[H, W, C] fp32 CUDA tensor (the layout the decoder loss reads)."""
@@ -60,29 +64,33 @@ class FeatureMap:
 
 
 def save_feature_map(path, fmap):
-    """magic, u16 version, u32 C/H/W (little endian), C*H*W float32 channel-major."""
-    header = MAGIC + struct.pack("<HIII", FORMAT_VERSION, fmap.channels, fmap.height, fmap.width)
+    """Header record + float32 payload (semantic.py:49-55)."""
+    head = np.zeros((), dtype=_FE4D_HEADER)
+    head["magic"], head["version"] = MAGIC, FORMAT_VERSION
+    head["channels"], head["height"], head["width"] = fmap.data.shape
     with open(path, "wb") as fh:
-        fh.write(header)
-        fh.write(fmap.data.astype("<f4").tobytes(order="C"))
+        fh.write(head.tobytes())
+        fh.write(np.asarray(fmap.data, dtype="<f4").tobytes())
 
 
 def load_feature_map(path):
-    """Inverse of save_feature_map; FormatError carries the byte offset (semantic.py:58-75)."""
-    with open(path, "rb") as fh:
-        blob = fh.read()
-    if len(blob) < 4 or blob[:4] != MAGIC:
-        raise FormatError(f"bad magic in {path!r}", offset=0)
-    if len(blob) < 18:
-        raise FormatError(f"truncated header in {path!r}", offset=len(blob))
-    version, c, h, w = struct.unpack("<HIII", blob[4:18])
-    if version != FORMAT_VERSION:
-        raise FormatError(f"unsupported format version {version}", offset=4)
-    expected = 18 + 4 * c * h * w
-    if len(blob) != expected:
-        raise FormatError(f"payload size mismatch: have {len(blob)} bytes, expected {expected}",
-                          offset=min(len(blob), expected))
-    return FeatureMap(data=np.frombuffer(blob[18:], dtype="<f4").reshape(c, h, w).copy())
+    """Parse an FE4D file; every malformed case is a FormatError carrying the
+    byte offset where the file stops making sense (semantic.py:58-75)."""
+    blob = memoryview(open(path, "rb").read())
+    size = len(blob)
+    if bytes(blob[:4]) != MAGIC:
+        raise FormatError(f"{path!r} is not an FE4D feature file", offset=0)
+    if size < _FE4D_HEADER.itemsize:
+        raise FormatError(f"{path!r}: header cut short after {size} bytes", offset=size)
+    head = np.frombuffer(blob, dtype=_FE4D_HEADER, count=1)[0]
+    if int(head["version"]) != FORMAT_VERSION:
+        raise FormatError(f"FE4D version {int(head['version'])} is not supported (want {FORMAT_VERSION})",
+                          offset=4)
+    shape = (int(head["channels"]), int(head["height"]), int(head["width"]))
+    want = _FE4D_HEADER.itemsize + 4 * shape[0] * shape[1] * shape[2]
+    if size != want:
+        raise FormatError(f"{path!r}: file is {size} bytes but its header implies {want}", offset=min(size, want))
+    return FeatureMap(np.frombuffer(blob, dtype="<f4", offset=_FE4D_HEADER.itemsize).reshape(shape).copy())
 
 
 # ---------------------------------------------------------------------------
