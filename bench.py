@@ -197,16 +197,64 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # distributed helpers
 # ---------------------------------------------------------------------------
+def torchrun_command(argv, n_gpus, port):
+    """The command bench.py re-executes itself under when asked for N > 1
+    GPUs without a torchrun environment: one rank per GPU on this node,
+    rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={int(n_gpus)}",
+            "--master-addr", "127.0.0.1", f"--master-port={int(port)}", os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def dist_setup(n_gpus):
+    """(rank, world, local rank).  Under torchrun the world comes from the
+    environment and must equal --gpus; NCCL over NVLink/NVSwitch carries the
+    barrier, the max-over-ranks timing and the training all-reduce."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != int(n_gpus):
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {n_gpus}")
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
+
+
+def comm_info(world):
+    """The collective backend the ranks actually run (the 'NCCL nranks' line)."""
+    if world == 1:
+        return {"backend": None, "nranks": 1}
+    import torch
+    import torch.distributed as dist
+    info = {"backend": dist.get_backend(), "nranks": dist.get_world_size()}
+    try:
+        v = torch.cuda.nccl.version()
+        info["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception:
+        pass
+    return info
+
+
+def dist_gather(x, world):
+    """Per-rank scalars gathered to every rank (list in rank order)."""
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [float(o.item()) for o in out]
 
 
 def dist_max(x, world):
@@ -361,7 +409,9 @@ def gpu_bench(args, rank, world, local):
         a_ev, b_ev = seq.run(ts_seq, Kmat, T)
         torch.cuda.synchronize()
     barrier(world)
-    ms_max = dist_max(a_ev.elapsed_time(b_ev), world)
+    ms_rank = a_ev.elapsed_time(b_ev)
+    ms_max = dist_max(ms_rank, world)
+    per_rank_ms = dist_gather(ms_rank, world)
     seq.raise_if_error()
 
     # per-stage timing pass (events around each stage on the launching stream)
@@ -395,7 +445,8 @@ def gpu_bench(args, rank, world, local):
         if int(st[0]) != 0:
             raise RuntimeError(f"device status {st[:5]} during the e2e region")
     return dict(ms=ms_max, ms_serial=ms_serial, prof=prof, clocks=clk.summary(), n_vis=n_vis, n_pairs=n_pairs,
-                e2e_ms=e2e_ms, h2d=sf.h2d_bytes(), d2h=sf.d2h_bytes(), steps=steps)
+                e2e_ms=e2e_ms, h2d=sf.h2d_bytes(), d2h=sf.d2h_bytes(), steps=steps, per_rank_ms=per_rank_ms,
+                comm=comm_info(world))
 
 
 def train_bench(args, rank, world, local):
@@ -469,6 +520,7 @@ def train_bench(args, rank, world, local):
     b.record(stream)
     torch.cuda.synchronize()
     ms = dist_max(a.elapsed_time(b), world)
+    per_rank_ms = dist_gather(a.elapsed_time(b), world)
     # per-stage times from one serial step (one lane: with pairs in flight the
     # stage events of concurrent streams would overlap)
     lanes = step.n_lanes
@@ -483,7 +535,7 @@ def train_bench(args, rank, world, local):
     dv.profile_enable(False)
     step.n_lanes, step._lanes = lanes, None
     return dict(ms=ms, prof=prof, loss=float(step.loss.item()), grad_floats=step.grads.numel, pairs=pairs,
-                lanes=lanes)
+                lanes=lanes, per_rank_ms=per_rank_ms, comm=comm_info(world))
 
 
 def launches_per_frame():
@@ -504,6 +556,10 @@ def main():
     ap.add_argument("--workload", default="render", choices=["render", "train", "fine"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute under torchrun (the driver launches
+        # it that way itself; this makes `python bench.py --gpus N` equivalent)
+        sys.exit(subprocess.call(torchrun_command(sys.argv[1:], args.gpus, _free_port())))
 
     rank, world, local = dist_setup(args.gpus)
     base = {"metric": METRIC, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -540,7 +596,8 @@ def main():
                          "ms_per_step": r["ms"] / args.steps,
                          "frames_per_s": world * r["pairs"] * args.steps / (r["ms"] / 1000.0),
                          "stage_ms_per_step": {s: round(ms, 4) for s, (ms, c) in r["prof"].items() if c},
-                         "allreduce_floats": r["grad_floats"], "loss": r["loss"]})
+                         "allreduce_floats": r["grad_floats"], "loss": r["loss"], "comm": r["comm"],
+                         "per_rank_steps_per_s": [args.steps / (m / 1000.0) for m in r["per_rank_ms"]]})
             line["config"] = dict(base["config"], workload="configs[4]: configs[1] scene, 8 (view,t) pairs/GPU, "
                                                            "L1 RGB + L1 feature", parallelism=f"dp{world}",
                                   pairs_in_flight=r["lanes"], stage_ms="one serial (1-lane) step")
@@ -609,6 +666,8 @@ def main():
                 "link_gbs": {"h2d": r["h2d"] * frames / (r["e2e_ms"] / 1000.0) / 1e9,
                              "d2h": r["d2h"] * frames / (r["e2e_ms"] / 1000.0) / 1e9}},
         "gpu_launches": launches_per_frame() * r["steps"],
+        "per_rank_frames_per_s": [r["steps"] / (m / 1000.0) for m in r["per_rank_ms"]],
+        "comm": r["comm"],
     })
     if rank == 0 and world == 1 and not args.no_cpu:
         c = cpu_reference(args.cpu_steps, 0)

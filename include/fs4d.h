@@ -205,6 +205,17 @@ const char* fs4d_build_info(void);
  * zero codes/counters, INT32_MAX in the first-index slots. */
 int fs4d_status_reset(int32_t* status, void* stream);
 
+/* Fold the status block `src` of a finished call into the accumulating block
+ * `dst`, stream-ordered (no host sync): the first error code and its words
+ * win, repeated capacity overflows keep the largest pair count.  With
+ * gate_adam != 0 an error in src also sets dst[FS4D_ST_ADAM_BAD_SEG] =
+ * FS4D_ADAM_GATED so that a following fs4d_adam_step with status = dst
+ * touches nothing -- a training step whose render failed (pair-buffer
+ * overflow, non-finite snapshot) never updates the parameters.  No reference
+ * counterpart (the reference raises synchronously, rasterizer.py:120-131). */
+#define FS4D_ADAM_GATED (-1)
+int fs4d_status_merge(const int32_t* src, int32_t* dst, int32_t gate_adam, void* stream);
+
 /* ---- optional per-stage timing ----
  * When enabled, every entry point brackets its stages with CUDA events
  * recorded on the launching stream; collect() waits on them, returns the
@@ -312,6 +323,49 @@ int fs4d_photometric_loss_grad(const float* color, const float* image, const uin
 int fs4d_l1(const float* pred, const float* target, int64_t n, double scale, float* grad,
             double* loss, void* stream);
 
+/* HexPlane query on its own (hexplane.query / query_with_cache,
+ * hexplane.py:113-142): latent [K, levels * channels] (level-major, the
+ * reference's concat order) of positions [K, 3] at time t (clipped to
+ * [0, 1]); coordinates and cells in fp64 as in deformation.  1..4 levels. */
+int fs4d_hexplane_query(const Fs4dHexPlane* field, const float* positions, int64_t K, double t, float* latent,
+                        void* stream);
+/* hexplane.query_backward (hexplane.py:145-187): plane_grads (same shapes as
+ * field; written, or added with accumulate != 0) receive d latent / d plane
+ * for the upstream d_latent [K, levels * channels]; d_positions [K, 3] (written
+ * or added) the position gradient, zero on every axis whose coordinate was
+ * clamped (outside the aabb, hexplane.py:186). */
+int fs4d_hexplane_query_backward(const Fs4dHexPlane* field, const float* positions, int64_t K, double t,
+                                 const float* d_latent, Fs4dHexPlane* plane_grads, float* d_positions,
+                                 int32_t accumulate, void* stream);
+
+/* One dense layer of numerics.mlp_forward / mlp_backward (numerics.py:56-105)
+ * for any shape (API helper; the deformation MLP itself runs fused on the
+ * tensor cores inside fs4d_deform_*): pre = x W^T + b, y = ReLU(pre) or pre,
+ * x [batch, in], W [out, in] (layer->relu selects the activation).  The
+ * backward writes dx = g W (dx may be NULL), dW = g^T x, db = sum_b g with
+ * g = dy * (pre > 0) for ReLU layers; dW / db are written, or added with
+ * accumulate != 0, and reduced over the batch in a fixed order
+ * (deterministic). */
+int fs4d_linear_forward(const float* x, int64_t batch, const Fs4dLinear* layer, float* pre, float* y, void* stream);
+size_t fs4d_linear_backward_workspace_bytes(int64_t batch, int32_t in_dim, int32_t out_dim);
+int fs4d_linear_backward(const float* x, const float* pre, int64_t batch, const Fs4dLinear* layer, const float* dy,
+                         float* dx, float* d_weight, float* d_bias, int32_t accumulate, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* rasterizer._tile_alphas (rasterizer.py:215-234) replayed from a render
+ * record: for the G Gaussians source_index[G] and the pixels
+ * [x0, x0+nx) x [y0, y0+ny) (row-major P = nx*ny), alpha / g2d / a_raw
+ * [G, P] exactly as the record's blend evaluated them (same footprint,
+ * q-skip, cap and skip decisions). */
+int fs4d_render_tile_alphas(const Fs4dRecordInfo* info, const void* workspace, size_t workspace_bytes,
+                            const Fs4dRasterConfig* cfg, const int32_t* source_index, int64_t G, int32_t x0,
+                            int32_t y0, int32_t nx, int32_t ny, float* alpha, float* g2d, float* a_raw, void* stream);
+/* rasterizer._composite_weights (rasterizer.py:244-261) of alpha [G, P]:
+ * t_exc, contrib (0/1 bytes), w [G, P] and t_final [P], front to back in
+ * fp32 with the blend's multiplication order. */
+int fs4d_composite_weights(const float* alpha, int64_t G, int64_t P, double stop, float* t_exc, uint8_t* contrib,
+                           float* w, float* t_final, void* stream);
+
 /* Adam over a flat parameter buffer (numerics.py:119-159 AdamState /
  * adam_step, applied per parameter array as training.py:431-442 does).
  * Every segment is one reference parameter array: [offset, offset+count) of
@@ -333,6 +387,15 @@ typedef struct Fs4dAdamSegment {
 int fs4d_adam_step(float* params, const float* grads, float* m, float* v, int32_t* step_counts,
                    const Fs4dAdamSegment* segments /* host array */, int32_t n_segments,
                    int32_t* status, void* stream);
+/* Same, stepping only the segments with active[i] != 0 (host array; NULL =
+ * all): the reference steps only the arrays present in its gradient dict
+ * (training.py:513-515 drops `features` without feature supervision,
+ * :519-529 adds grid.* only with the HexPlane enabled, :531 decoder.* only
+ * with the feature loss), so an inactive array keeps its parameters,
+ * moments and step count. */
+int fs4d_adam_step_masked(float* params, const float* grads, float* m, float* v, int32_t* step_counts,
+                          const Fs4dAdamSegment* segments /* host array */, const int32_t* active /* host */,
+                          int32_t n_segments, int32_t* status, void* stream);
 
 /* HexPlane total-variation regulariser (hexplane.py:190-222): with tv = sum
  * over planes of mean squared axis-adjacent differences, *loss (may be NULL)

@@ -321,7 +321,8 @@ def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None, margi
     feature = np.zeros((height, width, n))
     tfin = np.ones((height, width))
     ncontrib = np.zeros((height, width), dtype=np.int64)
-    margin = np.full((height, width), np.inf) if margins else None
+    margin_a = np.full((height, width), np.inf) if margins else None
+    margin_s = np.full((height, width), np.inf) if margins else None
     tiles = {}
     rows_to_do = range(len(lists)) if tile_rows is None else tile_rows
     for ty in rows_to_do:
@@ -334,8 +335,9 @@ def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None, margi
             t_before, contrib, w, t_final = transmittance(alpha, cfg.stop_transmittance)
             shp = (ys.size, xs.size)
             if margins:
-                margin[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1] = \
-                    _tile_margins(alpha, a_raw, q, inside, t_before, cfg).min(axis=0).reshape(shp)
+                a_m, s_m = _tile_margins(alpha, a_raw, q, inside, t_before, cfg, proj["opacity"][rows])
+                margin_a[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1] = a_m.min(axis=0).reshape(shp)
+                margin_s[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1] = s_m.min(axis=0).reshape(shp)
             sl = (slice(ys[0], ys[-1] + 1), slice(xs[0], xs[-1] + 1))
             color[sl] = (w.T @ proj["color"][rows]).reshape(shp + (3,))
             depth[sl] = (w.T @ proj["view_depth"][rows]).reshape(shp)
@@ -348,7 +350,8 @@ def render(cloud, K, T, height, width, cfg, tile_rows=None, prepared=None, margi
     out = {"color": color, "depth": depth, "feature": feature, "alpha": 1.0 - tfin,
            "n_contrib": ncontrib, "proj": proj, "tiles": tiles, "t_final": tfin}
     if margins:
-        out["margins"] = margin
+        out["alpha_margins"], out["stop_margins"] = margin_a, margin_s
+        out["margins"] = np.minimum(margin_a, margin_s)
     return out
 
 
@@ -713,38 +716,76 @@ def projection_margins(proj, height, width, tile, cfg):
     return m
 
 
-def _tile_margins(alpha, a_raw, q, inside, t_before, cfg):
+def _tile_margins(alpha, a_raw, q, inside, t_before, cfg, opac):
     """[G, P] relative margins of one tile's fp32 blend decisions (see
-    pixel_decision_margins); rows the traversal cannot reach are inf."""
+    pixel_decision_margins), split into (per-Gaussian alpha decisions:
+    q-skip, alpha-skip, alpha-cap; the stop rule |T_after - stop| / stop);
+    rows the traversal cannot reach are inf.  The q-skip test only decides
+    anything for opacities within 1e-4 of 1: at q = 2 ln 255 the raw alpha is
+    opacity/255, below the alpha-skip threshold either way."""
     reach = t_before >= cfg.stop_transmittance * 0.5  # rows the traversal can see
-    mm = np.where(inside | (q > Q_SKIP), np.abs(q - Q_SKIP) / Q_SKIP, np.inf)
+    q_matters = (opac * np.exp(-0.5 * Q_SKIP) >= cfg.alpha_skip * (1.0 - 1e-4))[:, None]
+    mm = np.where((inside | (q > Q_SKIP)) & q_matters, np.abs(q - Q_SKIP) / Q_SKIP, np.inf)
     am = np.minimum(a_raw, cfg.alpha_cap)
     mm = np.minimum(mm, np.where(inside, np.abs(am - cfg.alpha_skip) / cfg.alpha_skip, np.inf))
     mm = np.minimum(mm, np.where(inside, np.abs(a_raw - cfg.alpha_cap) / cfg.alpha_cap, np.inf))
     t_after = t_before * (1.0 - alpha)
-    mm = np.minimum(mm, np.where(alpha > 0, np.abs(t_after - cfg.stop_transmittance)
-                                 / cfg.stop_transmittance, np.inf))
-    return np.where(reach, mm, np.inf)
+    ms = np.where(alpha > 0, np.abs(t_after - cfg.stop_transmittance) / cfg.stop_transmittance, np.inf)
+    return np.where(reach, mm, np.inf), np.where(reach, ms, np.inf)
 
 
-def pixel_decision_margins(out, cfg):
+def pixel_decision_margins(out, cfg, split=False):
     """Per pixel: the smallest relative margin of any fp32-evaluated blend
     decision met while compositing it (alpha-skip, alpha-cap, q-skip, stop).
     The square-footprint test is decided from fp64 integer bounds on device
-    and is covered by projection_margins.  render(..., margins=True) computes
-    the same array in its own tile loop (out["margins"])."""
+    and is covered by projection_margins.  split=True returns (alpha
+    decisions, stop rule) separately: the stop rule compares a transmittance
+    that is a product over every earlier contributor, so its fp32 error grows
+    with the contributor count and callers may give it its own threshold.
+    render(..., margins=True) computes the same arrays in its own tile loop."""
     if "margins" in out:
-        return out["margins"]
+        return (out["alpha_margins"], out["stop_margins"]) if split else out["margins"]
     proj = out["proj"]
     h, w = out["t_final"].shape
-    margin = np.full((h, w), np.inf)
+    ma = np.full((h, w), np.inf)
+    ms = np.full((h, w), np.inf)
     for (ty, tx), (rows, xs, ys) in out["tiles"].items():
         alpha, g, a_raw, dx, dy, q, inside = tile_alpha(proj, rows, xs, ys, cfg)
         t_before, contrib, wts, t_final = transmittance(alpha, cfg.stop_transmittance)
-        mm = _tile_margins(alpha, a_raw, q, inside, t_before, cfg)
+        a_m, s_m = _tile_margins(alpha, a_raw, q, inside, t_before, cfg, proj["opacity"][rows])
         sl = (slice(ys[0], ys[-1] + 1), slice(xs[0], xs[-1] + 1))
-        margin[sl] = mm.min(axis=0).reshape(ys.size, xs.size) if rows.size else np.inf
-    return margin
+        if rows.size:
+            ma[sl] = a_m.min(axis=0).reshape(ys.size, xs.size)
+            ms[sl] = s_m.min(axis=0).reshape(ys.size, xs.size)
+    return (ma, ms) if split else np.minimum(ma, ms)
+
+
+def reached_rows(out, cfg, pixels, stop_pixels=None):
+    """Projected rows (bool [M]) whose backward sums include a term that an
+    ambiguous decision can change.  `pixels` (bool [H, W]): pixels with an
+    ambiguous alpha decision -- every Gaussian the traversal reaches there
+    with a non-zero or near-threshold alpha (a flipped alpha rescales the
+    transmittance of everything behind it).  `stop_pixels`: pixels whose only
+    ambiguity is the stop rule -- the flip adds or drops a contributor of
+    weight ~alpha * 1e-4, which moves the earlier contributors' terms there
+    by ~1e-4 relative, so only the Gaussians near the stop (T_before within
+    [stop/2, 2 stop]) are marked."""
+    proj = out["proj"]
+    hit = np.zeros(proj["source_index"].size, dtype=bool)
+    stop = cfg.stop_transmittance
+    sp = np.zeros_like(pixels) if stop_pixels is None else stop_pixels
+    for (ty, tx), (rows, xs, ys) in out["tiles"].items():
+        sub = pixels[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1].reshape(-1)
+        ssub = sp[ys[0]:ys[-1] + 1, xs[0]:xs[-1] + 1].reshape(-1)
+        if rows.size == 0 or not (sub.any() or ssub.any()):
+            continue
+        alpha, g, a_raw, dx, dy, q, inside = tile_alpha(proj, rows, xs, ys, cfg)
+        t_before, _, _, _ = transmittance(alpha, stop)
+        near = inside | (q <= Q_SKIP * 1.01)
+        reach = (t_before >= stop * 0.5) & near
+        tail = reach & (t_before <= stop * 2.0)
+        hit[rows[reach[:, sub].any(axis=1) | tail[:, ssub].any(axis=1)]] = True
+    return hit
 
 
 # ---------------------------------------------------------------------------

@@ -21,6 +21,7 @@ STATUS_WORDS = 32
 ST_CODE, ST_BAD_FIELDS, ST_N_VISIBLE, ST_PAIRS_LO, ST_PAIRS_HI = 0, 1, 2, 3, 4
 ST_BAD_INDEX, ST_DEGEN_INDEX = 8, 16
 ST_ADAM_BAD_SEG, ST_ADAM_BAD_COUNT = 17, 18
+ADAM_GATED = -1  # FS4D_ADAM_GATED: the Adam step was skipped because a gated-in call failed
 MAX_ADAM_SEGMENTS = 128
 
 FIELD_NAMES = ("positions", "rotations", "log_scales", "opacity_logits",
@@ -118,6 +119,7 @@ SIGNATURES = {
     "fs4d_last_error": (ctypes.c_char_p, []),
     "fs4d_build_info": (ctypes.c_char_p, []),
     "fs4d_status_reset": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_status_merge": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
     "fs4d_profile_enable": (ctypes.c_int, [ctypes.c_int]),
     "fs4d_profile_collect": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]),
@@ -136,6 +138,16 @@ SIGNATURES = {
                                        ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane),
                                        ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_hexplane_query": (ctypes.c_int, [ctypes.POINTER(HexPlane), _V, _I64, _D, _V, _V]),
+    "fs4d_hexplane_query_backward": (ctypes.c_int, [ctypes.POINTER(HexPlane), _V, _I64, _D, _V,
+                                                    ctypes.POINTER(HexPlane), _V, _I32, _V]),
+    "fs4d_linear_forward": (ctypes.c_int, [_V, _I64, ctypes.POINTER(Linear), _V, _V, _V]),
+    "fs4d_linear_backward_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "fs4d_linear_backward": (ctypes.c_int, [_V, _V, _I64, ctypes.POINTER(Linear), _V, _V, _V, _V, _I32, _V, _SZ,
+                                            _V]),
+    "fs4d_render_tile_alphas": (ctypes.c_int, [ctypes.POINTER(RecordInfo), _V, _SZ, ctypes.POINTER(RasterCfg), _V,
+                                               _I64, _I32, _I32, _I32, _I32, _V, _V, _V, _V]),
+    "fs4d_composite_weights": (ctypes.c_int, [_V, _I64, _I64, _D, _V, _V, _V, _V, _V]),
     "fs4d_l1_loss_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int32, ctypes.c_double, ctypes.c_double,
@@ -146,6 +158,8 @@ SIGNATURES = {
                                                   _V, _V, _SZ, _V]),
     "fs4d_l1": (ctypes.c_int, [_V, _V, _I64, _D, _V, _V, _V]),
     "fs4d_adam_step": (ctypes.c_int, [_V, _V, _V, _V, _V, ctypes.POINTER(AdamSegment), _I32, _V, _V]),
+    "fs4d_adam_step_masked": (ctypes.c_int, [_V, _V, _V, _V, _V, ctypes.POINTER(AdamSegment),
+                                             ctypes.POINTER(ctypes.c_int32), _I32, _V, _V]),
     "fs4d_tv_loss_grad": (ctypes.c_int, [ctypes.POINTER(HexPlane), ctypes.POINTER(HexPlane), _D, _I32, _V, _V]),
     "fs4d_resize_bilinear": (ctypes.c_int, [_V, _I32, _I32, _I32, _V, _I32, _I32, _V]),
     "fs4d_resize_workspace_bytes": (_SZ, [_I32, _I32, _I32]),

@@ -80,7 +80,18 @@ size_t photometric_workspace_bytes(int, int);
 int photometric_loss_grad(const float*, const float*, const uint8_t*, const float*, const float*, const float*, int,
                           int, double, double, float*, float*, double*, double*, void*, cudaStream_t);
 int l1(const float*, const float*, int64_t, double, float*, double*, cudaStream_t);
-int adam_step(float*, const float*, float*, float*, int32_t*, const Fs4dAdamSegment*, int, int32_t*, cudaStream_t);
+int adam_step(float*, const float*, float*, float*, int32_t*, const Fs4dAdamSegment*, int, const int32_t*, int32_t*,
+              cudaStream_t);
+int hexplane_query(const Fs4dHexPlane&, const float*, int64_t, double, float*, cudaStream_t);
+size_t linear_backward_workspace_bytes(int64_t, int, int);
+int linear_forward(const float*, int64_t, const Fs4dLinear&, float*, float*, cudaStream_t);
+int linear_backward(const float*, const float*, int64_t, const Fs4dLinear&, const float*, float*, float*, float*, int,
+                    void*, cudaStream_t);
+int render_tile_alphas(const RenderLayout&, void*, const int32_t*, int64_t, int, int, int, int, float, float, float*,
+                       float*, float*, cudaStream_t);
+int composite_weights(const float*, int64_t, int64_t, float, float*, uint8_t*, float*, float*, cudaStream_t);
+int hexplane_query_backward(const Fs4dHexPlane&, const float*, int64_t, double, const float*, Fs4dHexPlane&, float*, int,
+                            cudaStream_t);
 int tv_loss_grad(const Fs4dHexPlane&, Fs4dHexPlane*, double, int, double*, cudaStream_t);
 int resize_bilinear(const float*, int, int, int, float*, int, int, cudaStream_t);
 size_t resize_workspace_bytes(int, int, int);
@@ -151,6 +162,28 @@ __global__ void k_status_reset(int32_t* st) {
     st[i] = (i >= FS4D_ST_BAD_INDEX && i <= FS4D_ST_ADAM_BAD_SEG) ? 0x7FFFFFFF : 0;
 }
 
+// One thread: fold a finished call's status block into an accumulating one
+// (stream-ordered after the call, so no host sync).  The first error wins;
+// repeated capacity overflows keep the largest pair count; gate_adam makes
+// a later fs4d_adam_step on `dst` a no-op.
+__global__ void k_status_merge(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int gate_adam) {
+  const int code = src[FS4D_ST_CODE];
+  if (code == FS4D_OK) return;
+  if (dst[FS4D_ST_CODE] == FS4D_OK) {
+    for (int i = 0; i < FS4D_ST_ADAM_BAD_SEG; ++i) dst[i] = src[i];
+  } else if (code == FS4D_ERR_CAPACITY && dst[FS4D_ST_CODE] == FS4D_ERR_CAPACITY) {
+    const unsigned long long a = ((unsigned long long)(unsigned)src[FS4D_ST_PAIRS_HI] << 32) |
+                                 (unsigned)src[FS4D_ST_PAIRS_LO];
+    const unsigned long long b = ((unsigned long long)(unsigned)dst[FS4D_ST_PAIRS_HI] << 32) |
+                                 (unsigned)dst[FS4D_ST_PAIRS_LO];
+    if (a > b) {
+      dst[FS4D_ST_PAIRS_LO] = src[FS4D_ST_PAIRS_LO];
+      dst[FS4D_ST_PAIRS_HI] = src[FS4D_ST_PAIRS_HI];
+    }
+  }
+  if (gate_adam) dst[FS4D_ST_ADAM_BAD_SEG] = FS4D_ADAM_GATED;
+}
+
 }  // namespace fs4d
 
 using namespace fs4d;
@@ -199,6 +232,12 @@ int fs4d_status_reset(int32_t* status, void* stream) {
   return check_launch("status_reset");
 }
 
+int fs4d_status_merge(const int32_t* src, int32_t* dst, int32_t gate_adam, void* stream) {
+  if (!src || !dst) return fail(FS4D_ERR_CONFIG, "null status block");
+  k_status_merge<<<1, 1, 0, (cudaStream_t)stream>>>(src, dst, gate_adam);
+  return check_launch("status_merge");
+}
+
 size_t fs4d_deform_workspace_bytes(const Fs4dDeformNet* net, int64_t K) {
   if (!net) return 0;
   return deform_workspace_bytes(*net, K, nullptr);
@@ -233,6 +272,21 @@ int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4
     return fail(FS4D_ERR_CONTRACT, "gradient rows do not match the cloud");
   return deform_backward(*cloud, *field, *net, t, cache, cache_bytes, *snapshot_grads, *cloud_grads, *net_grads,
                          plane_grads, accumulate, workspace, workspace_bytes, status, (cudaStream_t)stream);
+}
+
+int fs4d_hexplane_query(const Fs4dHexPlane* field, const float* positions, int64_t K, double t, float* latent,
+                        void* stream) {
+  if (!field || K < 0 || (K > 0 && (!positions || !latent))) return fail(FS4D_ERR_CONFIG, "bad hexplane_query arguments");
+  return hexplane_query(*field, positions, K, t, latent, (cudaStream_t)stream);
+}
+
+int fs4d_hexplane_query_backward(const Fs4dHexPlane* field, const float* positions, int64_t K, double t,
+                                 const float* d_latent, Fs4dHexPlane* plane_grads, float* d_positions,
+                                 int32_t accumulate, void* stream) {
+  if (!field || !plane_grads || K < 0 || (K > 0 && (!positions || !d_latent || !d_positions)))
+    return fail(FS4D_ERR_CONFIG, "bad hexplane_query_backward arguments");
+  return hexplane_query_backward(*field, positions, K, t, d_latent, *plane_grads, d_positions, accumulate,
+                                 (cudaStream_t)stream);
 }
 
 int fs4d_l1_loss_grad(const float* color, const float* color_target, const float* feature,
@@ -271,14 +325,16 @@ int fs4d_l1(const float* pred, const float* target, int64_t n, double scale, flo
   return l1(pred, target, n, scale, grad, loss, (cudaStream_t)stream);
 }
 
-int fs4d_adam_step(float* params, const float* grads, float* m, float* v, int32_t* step_counts,
-                   const Fs4dAdamSegment* segments, int32_t n_segments, int32_t* status, void* stream) {
+int fs4d_adam_step_masked(float* params, const float* grads, float* m, float* v, int32_t* step_counts,
+                          const Fs4dAdamSegment* segments, const int32_t* active, int32_t n_segments,
+                          int32_t* status, void* stream) {
   if (n_segments < 0 || n_segments > FS4D_MAX_ADAM_SEGMENTS)
     return fail(FS4D_ERR_CONFIG, "adam segment count out of range");
   if (n_segments == 0) return FS4D_OK;
   if (!params || !grads || !m || !v || !step_counts || !segments || !status)
     return fail(FS4D_ERR_CONFIG, "null adam argument");
   for (int i = 0; i < n_segments; ++i) {
+    if (active && !active[i]) continue;
     const Fs4dAdamSegment& g = segments[i];
     // numerics.py:143-144: a non-positive learning rate is a configuration error
     if (!(g.lr > 0.0)) return fail(FS4D_ERR_CONFIG, "learning rate must be positive, got " + std::to_string(g.lr));
@@ -286,7 +342,12 @@ int fs4d_adam_step(float* params, const float* grads, float* m, float* v, int32_
     if (!(g.beta1 >= 0.0 && g.beta1 < 1.0) || !(g.beta2 >= 0.0 && g.beta2 < 1.0) || !(g.eps >= 0.0))
       return fail(FS4D_ERR_CONFIG, "bad adam hyper-parameters");
   }
-  return adam_step(params, grads, m, v, step_counts, segments, n_segments, status, (cudaStream_t)stream);
+  return adam_step(params, grads, m, v, step_counts, segments, n_segments, active, status, (cudaStream_t)stream);
+}
+
+int fs4d_adam_step(float* params, const float* grads, float* m, float* v, int32_t* step_counts,
+                   const Fs4dAdamSegment* segments, int32_t n_segments, int32_t* status, void* stream) {
+  return fs4d_adam_step_masked(params, grads, m, v, step_counts, segments, nullptr, n_segments, status, stream);
 }
 
 static int check_field(const Fs4dHexPlane* f) {
@@ -468,6 +529,56 @@ int fs4d_render_export_projected(const Fs4dRecordInfo* info, const void* workspa
   RenderLayout L = make_layout(*info);
   if (!workspace || workspace_bytes < L.total) return fail(FS4D_ERR_CONFIG, "render workspace too small");
   return render_export_projected(L, const_cast<void*>(workspace), *out, (cudaStream_t)stream);
+}
+
+static int check_linear(const Fs4dLinear* L) {
+  if (!L || !L->weight || !L->bias || L->in_dim <= 0 || L->out_dim <= 0)
+    return fail(FS4D_ERR_CONFIG, "bad linear layer");
+  return FS4D_OK;
+}
+
+int fs4d_linear_forward(const float* x, int64_t batch, const Fs4dLinear* layer, float* pre, float* y, void* stream) {
+  int rc = check_linear(layer);
+  if (rc) return rc;
+  if (batch < 0 || (batch > 0 && (!x || !pre || !y))) return fail(FS4D_ERR_CONFIG, "bad linear_forward arguments");
+  return linear_forward(x, batch, *layer, pre, y, (cudaStream_t)stream);
+}
+
+size_t fs4d_linear_backward_workspace_bytes(int64_t batch, int32_t in_dim, int32_t out_dim) {
+  if (batch < 0 || in_dim <= 0 || out_dim <= 0) return 0;
+  return linear_backward_workspace_bytes(batch, in_dim, out_dim);
+}
+
+int fs4d_linear_backward(const float* x, const float* pre, int64_t batch, const Fs4dLinear* layer, const float* dy,
+                         float* dx, float* d_weight, float* d_bias, int32_t accumulate, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  int rc = check_linear(layer);
+  if (rc) return rc;
+  if (batch < 0 || !d_weight || !d_bias || (batch > 0 && (!x || !pre || !dy)))
+    return fail(FS4D_ERR_CONFIG, "bad linear_backward arguments");
+  if (!workspace || workspace_bytes < linear_backward_workspace_bytes(batch, layer->in_dim, layer->out_dim))
+    return fail(FS4D_ERR_CONFIG, "linear_backward workspace too small");
+  return linear_backward(x, pre, batch, *layer, dy, dx, d_weight, d_bias, accumulate, workspace, (cudaStream_t)stream);
+}
+
+int fs4d_render_tile_alphas(const Fs4dRecordInfo* info, const void* workspace, size_t workspace_bytes,
+                            const Fs4dRasterConfig* cfg, const int32_t* source_index, int64_t G, int32_t x0,
+                            int32_t y0, int32_t nx, int32_t ny, float* alpha, float* g2d, float* a_raw, void* stream) {
+  if (!info || !cfg) return fail(FS4D_ERR_CONFIG, "null tile_alphas argument");
+  RenderLayout L = make_layout(*info);
+  if (!workspace || workspace_bytes < L.total) return fail(FS4D_ERR_CONFIG, "render workspace too small");
+  if (G < 0 || nx < 0 || ny < 0 || (G > 0 && (!source_index || !alpha || !g2d || !a_raw)))
+    return fail(FS4D_ERR_CONFIG, "bad tile_alphas arguments");
+  if (x0 < 0 || y0 < 0 || x0 + nx > L.W || y0 + ny > L.H) return fail(FS4D_ERR_CONFIG, "tile outside the image");
+  return render_tile_alphas(L, const_cast<void*>(workspace), source_index, G, x0, y0, nx, ny, (float)cfg->alpha_cap,
+                            (float)cfg->alpha_skip, alpha, g2d, a_raw, (cudaStream_t)stream);
+}
+
+int fs4d_composite_weights(const float* alpha, int64_t G, int64_t P, double stop, float* t_exc, uint8_t* contrib,
+                           float* w, float* t_final, void* stream) {
+  if (G < 0 || P < 0 || (P > 0 && !t_final) || (G * P > 0 && (!alpha || !t_exc || !contrib || !w)))
+    return fail(FS4D_ERR_CONFIG, "bad composite_weights arguments");
+  return composite_weights(alpha, G, P, (float)stop, t_exc, contrib, w, t_final, (cudaStream_t)stream);
 }
 
 int fs4d_render_export_tiles(const Fs4dRecordInfo* info, const void* workspace, size_t workspace_bytes,

@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a
       suf[5] = 1.f;
 #pragma unroll
       for (int q = 4; q >= 0; --q) suf[q] = suf[q + 1] * s[q + 1];
-      const float up = a.dlat[k * 64 + l * C + ch];
+      const float up = a.dlat[k * p.L + l * C + ch];
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const float coef = up * pre[q] * suf[q];
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a
   }
   if (lane < 3) {
     const float d = inside[lane] ? (float)((double)dco[lane] / p.span[lane]) : 0.f;
-    a.cg_pos[3 * k + lane] = (a.accumulate ? a.cg_pos[3 * k + lane] : 0.f) + a.g_pos[3 * k + lane] + d;
+    a.cg_pos[3 * k + lane] = (a.accumulate ? a.cg_pos[3 * k + lane] : 0.f) + (a.g_pos ? a.g_pos[3 * k + lane] : 0.f) + d;
   }
 }
 
@@ -752,6 +752,36 @@ __global__ void __launch_bounds__(32 * kRedGroups) k_time_partials(TimeReduceArg
 // ---------------------------------------------------------------------------
 // host driver (after deform_backward's pass-through and plane-gradient reset)
 // ---------------------------------------------------------------------------
+int tc_field_plan(const Fs4dHexPlane& f, double t, TcPlan& p);
+
+// hexplane.query_backward (hexplane.py:145-187): plane gradients (written,
+// or added with accumulate) and position gradients (zero on clamped axes).
+int hexplane_query_backward(const Fs4dHexPlane& f, const float* pos, int64_t K, double t, const float* dlat,
+                            Fs4dHexPlane& g, float* dpos, int accumulate, cudaStream_t s) {
+  TcPlan p;
+  int rc = tc_field_plan(f, t, p);
+  if (rc) return rc;
+  for (int l = 0; l < f.levels; ++l)
+    for (int q = 0; q < 6; ++q) {
+      if (!g.planes[l][q]) return fail(FS4D_ERR_CONFIG, "null plane gradient buffer");
+      if (!accumulate)
+        cudaMemsetAsync(g.planes[l][q], 0, (size_t)f.res[l][q][0] * f.res[l][q][1] * f.channels * 4, s);
+    }
+  if (K == 0) return FS4D_OK;
+  HexBwdArgs h;
+  h.p = p;
+  h.K = K;
+  h.pos = pos;
+  h.dlat = dlat;
+  h.g_pos = nullptr;
+  h.cg_pos = dpos;
+  for (int l = 0; l < FS4D_MAX_LEVELS; ++l)
+    for (int q = 0; q < 6; ++q) h.gplanes[l][q] = l < f.levels ? g.planes[l][q] : nullptr;
+  h.accumulate = accumulate;
+  k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
+  return check_launch("hexplane_query_backward");
+}
+
 int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
                        const uint8_t* cache, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
                        Fs4dHexPlane* pg, int accumulate, void* ws, int32_t* status, cudaStream_t s) {

@@ -960,6 +960,49 @@ extern "C" int fs4d_debug_mlp_trace(long long* out, int* n) {
 }
 #endif
 
+// Field-only plan: the standalone HexPlane query / query_backward
+// (hexplane.py:113-187) reuse the deformation's gather and scatter kernels
+// with latent rows of levels * channels floats.
+int tc_field_plan(const Fs4dHexPlane& f, double t, TcPlan& p) {
+  memset(&p, 0, sizeof(p));
+  if (f.levels < 1 || f.levels > kGatherMaxLevels)
+    return fail(FS4D_ERR_CONFIG, "hexplane query supports 1.." + std::to_string(kGatherMaxLevels) + " levels");
+  if (f.channels < 1) return fail(FS4D_ERR_CONFIG, "hexplane channels must be positive");
+  p.enable_grid = 1;
+  p.levels = f.levels;
+  p.C = f.channels;
+  p.L = f.levels * f.channels;
+  for (int l = 0; l < f.levels; ++l)
+    for (int q = 0; q < 6; ++q) {
+      p.res[l][q][0] = f.res[l][q][0];
+      p.res[l][q][1] = f.res[l][q][1];
+      p.planes[l][q] = f.planes[l][q];
+      if (f.res[l][q][0] < 2 || f.res[l][q][1] < 2) return fail(FS4D_ERR_CONFIG, "plane resolutions must be >= 2");
+      if (!f.planes[l][q]) return fail(FS4D_ERR_CONFIG, "null plane");
+    }
+  for (int a = 0; a < 3; ++a) {
+    p.lo[a] = f.aabb[a];
+    p.span[a] = f.aabb[3 + a] - f.aabb[a];
+    if (!(p.span[a] > 0.0)) return fail(FS4D_ERR_CONFIG, "aabb must have hi > lo");
+  }
+  p.order = f.order;
+  p.t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);  // hexplane.py:90
+  return FS4D_OK;
+}
+
+int hexplane_query(const Fs4dHexPlane& f, const float* pos, int64_t K, double t, float* latent, cudaStream_t s) {
+  TcPlan p;
+  int rc = tc_field_plan(f, t, p);
+  if (rc) return rc;
+  if (K == 0) return FS4D_OK;
+  const unsigned gblocks = (unsigned)ceil_div(K, kGatherWarps * 32);
+  if (p.C == 32 && p.levels == 2)
+    k_hexplane_latent_c32<2><<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, pos, latent);
+  else
+    k_hexplane_latent<<<gblocks, kGatherWarps * 32, 0, s>>>(p, K, pos, latent);
+  return check_launch("hexplane_query");
+}
+
 int tc_build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, TcPlan& p) {
   return build_plan(n, f, t, p, nullptr);
 }

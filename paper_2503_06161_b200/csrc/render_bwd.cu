@@ -20,7 +20,7 @@ struct BwdArgs {
   const uint2* ranges;
   const int32_t* tperm;  // tiles by decreasing pair count (from the forward record), or null
   const uint32_t* pvals;
-  const float2* xy;
+  const float4* xy;  // (u hi, v hi, u lo, v lo)
   const float4* conic_o;
   const int4* pix_rect;
   const float4* rgbz;
@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
   const uint2 rg = a.ranges[tile];
   if (rg.y <= rg.x) return;
   const int64_t pix = (int64_t)row * a.W + col;
-  const float fc = (float)col, fr = (float)row;
+  const float ox = (float)(tx * kTile), oy = (float)(ty * kTile);  // tile origin (tile_rel_mean)
+  const float fc = (float)(col - tx * kTile), fr = (float)(row - ty * kTile);
 
   float T = 1.f, Tfin = 1.f;
   int lastj = -1;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kTilePixels) k_blend_bwd(BwdArgs a) {
     if ((int)threadIdx.x < cnt) {
       const uint32_t g = a.pvals[bstart + threadIdx.x];
       s_g[threadIdx.x] = g;
-      s_xy[threadIdx.x] = a.xy[g];
+      s_xy[threadIdx.x] = tile_rel_mean(a.xy[g], ox, oy);
       s_co[threadIdx.x] = a.conic_o[g];
       s_pr[threadIdx.x] = a.pix_rect[g];
       s_rgbz[threadIdx.x] = a.rgbz[g];
@@ -288,7 +289,8 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
   const int lane = threadIdx.x & 31;
   const uint2 rg = a.ranges[tile];
   if (rg.y <= rg.x) return;
-  const float fc = (float)col;
+  const float ox = (float)(tx * kTile), oy = (float)(ty * kTile);  // tile origin (tile_rel_mean)
+  const float fc = (float)(col - tx * kTile);
 
   bool inside[PX];
   float T[PX], Tfin[PX], suffix[PX], vpix[PX], dc0[PX], dc1[PX], dc2[PX], dd[PX];
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
     if ((int)threadIdx.x < cnt) {
       const uint32_t g = a.pvals[bstart + threadIdx.x];
       s_g[threadIdx.x] = g;
-      s_xy[threadIdx.x] = a.xy[g];
+      s_xy[threadIdx.x] = tile_rel_mean(a.xy[g], ox, oy);
       const float4 cog = a.conic_o[g];
       s_co[threadIdx.x] = cog;
       s_cs[threadIdx.x] = scaled_conic(cog);
@@ -368,7 +370,10 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
         if (kk < cnt && bstart + kk <= (int64_t)wlast) {
           const int4 pr = s_pr[kk];
           hit = pr.w >= wrow0 && pr.z <= wrow0 + 2 * PX - 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
-          if (hit) hit = strip_hits<2 * PX>(pr, s_xy[kk], s_co[kk], wrow0, tcol0, a.alpha_skip);
+          if (hit) {
+            const float2 mr = s_xy[kk];
+            hit = strip_hits<2 * PX>(pr, make_float2(mr.x + ox, mr.y + oy), s_co[kk], wrow0, tcol0, a.alpha_skip);
+          }
         }
         bits = __ballot_sync(0xffffffffu, hit);
       }
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
           bool live = inside[p] && j <= (int64_t)lastj[p] &&
                       !(col < pr.x || col > pr.y || row < pr.z || row > pr.w);
           if (!live) continue;
-          const float dx = fc - mxy.x, dy = (float)row - mxy.y;
+          const float dx = fc - mxy.x, dy = (float)(row - ty * kTile) - mxy.y;
           const float pw = gauss_power(s_cs[k], dx, dy);
           if (pw < kPowSkip) continue;
           const float gv = fast_exp2(pw);
@@ -774,7 +779,7 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   b.ranges = at<uint2>(ws, L.ranges);
   b.tperm = L.ntiles <= 65536 ? at<int32_t>(ws, L.tperm) : nullptr;
   b.pvals = at<uint32_t>(ws, L.pvals0);
-  b.xy = at<float2>(ws, L.xy);
+  b.xy = at<float4>(ws, L.xy);
   b.conic_o = at<float4>(ws, L.conic_o);
   b.pix_rect = at<int4>(ws, L.pix_rect);
   b.rgbz = at<float4>(ws, L.rgbz);

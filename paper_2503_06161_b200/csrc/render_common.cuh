@@ -28,6 +28,14 @@ __device__ __forceinline__ float4 scaled_conic(const float4& co) {
 __device__ __forceinline__ float4 unscaled_conic(const float4& cs) {
   return make_float4(cs.x * (-2.f / kLog2e), cs.y * (-1.f / kLog2e), cs.z * (-2.f / kLog2e), cs.w);
 }
+// The projected mean is kept as fp32 hi + lo (u = hi + lo to ~1e-12 px) and
+// staged relative to the tile origin (ox, oy): the per-pair offsets
+// dx = (col - ox) - m.x are then exact to ~1e-6 px, where a single fp32 u
+// carries half an ulp of error (3e-5 px at u ~ 640) into every alpha.  The
+// forward blend, the backward replay and the tile-alpha replay all use it.
+__device__ __forceinline__ float2 tile_rel_mean(const float4& m, float ox, float oy) {
+  return make_float2((m.x - ox) + m.z, (m.y - oy) + m.w);
+}
 __device__ __forceinline__ float gauss_power(const float4& cs, float dx, float dy) {
   return cs.x * dx * dx + cs.y * dx * dy + cs.z * dy * dy;
 }
@@ -132,7 +140,7 @@ inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
     o = align_up(o + bytes, 256);
     return at;
   };
-  L.xy = take(K * 8);
+  L.xy = take(K * 16);
   L.conic_o = take(K * 16);
   L.pix_rect = take(K * 16);
   L.tile_rect = take(K * 16);

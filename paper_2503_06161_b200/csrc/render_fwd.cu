@@ -21,7 +21,7 @@ struct PreArgs {
   int H, W, ntx, nty;
   double z_near, lowpass;
   int with_features;
-  float2* xy;
+  float4* xy;  // (u hi, v hi, u lo, v lo)
   float4* conic_o;
   int4* pix_rect;
   int4* tile_rect;
@@ -197,7 +197,10 @@ __device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i, cons
   const int ty0 = (int)fmin(fmax(floor((v - radius) / kTile), 0.0), (double)(a.nty - 1));
   const int ty1 = (int)fmin(fmax(floor((v + radius) / kTile), 0.0), (double)(a.nty - 1));
 
-  a.xy[i] = make_float2((float)u, (float)v);
+  {
+    const float uh = (float)u, vh = (float)v;
+    a.xy[i] = make_float4(uh, vh, (float)(u - (double)uh), (float)(v - (double)vh));
+  }
   a.conic_o[i] = make_float4((float)c00r, (float)c01r, (float)c11r, opac);
   a.pix_rect[i] = make_int4(px0, px1, py0, py1);
   a.tile_rect[i] = make_int4(tx0, tx1, ty0, ty1);
@@ -287,7 +290,7 @@ struct BlendArgs {
   const uint2* ranges;
   const int32_t* tperm;  // tiles by decreasing pair count (launch order), or null
   const uint32_t* pvals;
-  const float2* xy;
+  const float4* xy;
   const float4* conic_o;
   const int4* pix_rect;
   const float4* rgbz;
@@ -352,10 +355,12 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   const bool inside = col < a.W && row < a.H;
   const uint2 rg = a.ranges[tile];
   constexpr bool first = FIRST;  // the launch with c0 == 0 also composites colour, depth, alpha
-  const float fc = (float)col, fr = (float)row;
   const int lane = threadIdx.x & 31;
   const int wrow0 = row0 + (threadIdx.x >> 5) * 2;  // this warp's two pixel rows
   const int tcol0 = tx * kTile;
+  // pixel and means relative to the tile origin (tile_rel_mean)
+  const float ox = (float)tcol0, oy = (float)(ty * kTile);
+  const float fc = (float)(col - tcol0), fr = (float)(row - ty * kTile);
 
   // accumulators as float2 pairs: every update is one FFMA2 (two fp32 FMAs,
   // bit-identical to the scalar FMAs) -- halves the blend's FMA issue slots
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
     const uint32_t j = b + threadIdx.x;
     if (j < rg.y) {
       const uint32_t g = a.pvals[j];
-      s_xy[threadIdx.x] = a.xy[g];
+      s_xy[threadIdx.x] = tile_rel_mean(a.xy[g], ox, oy);
       s_cs[threadIdx.x] = scaled_conic(a.conic_o[g]);
       s_pr[threadIdx.x] = a.pix_rect[g];
       s_rgbz[threadIdx.x] = a.rgbz[g];
@@ -408,7 +413,11 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
       if (kk < cnt) {
         const int4 pr = s_pr[kk];
         hit = pr.w >= wrow0 && pr.z <= wrow0 + 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
-        if (hit) hit = strip_hits<2>(pr, s_xy[kk], unscaled_conic(s_cs[kk]), wrow0, tcol0, a.alpha_skip);
+        if (hit) {
+          const float2 mr = s_xy[kk];
+          hit = strip_hits<2>(pr, make_float2(mr.x + ox, mr.y + oy), unscaled_conic(s_cs[kk]), wrow0, tcol0,
+                              a.alpha_skip);
+        }
       }
       const unsigned msk = __ballot_sync(0xffffffffu, hit);
       if (lane == 0) s_mask[wid][m] = msk;
@@ -577,7 +586,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   p.z_near = cfg.z_near;
   p.lowpass = cfg.lowpass;
   p.with_features = cfg.with_features;
-  p.xy = at<float2>(ws, L.xy);
+  p.xy = at<float4>(ws, L.xy);
   p.conic_o = at<float4>(ws, L.conic_o);
   p.pix_rect = at<int4>(ws, L.pix_rect);
   p.tile_rect = at<int4>(ws, L.tile_rect);
@@ -652,12 +661,13 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
 // record export (ProjectedGaussians / tile lists)
 // ---------------------------------------------------------------------------
 __global__ void k_export_projected(const uint32_t* __restrict__ order, const uint32_t* counters, int64_t K,
-                                   const float2* xy, const float4* conic_o, const float4* rgbz, const float4* cov_r,
+                                   const float4* xy, const float4* conic_o, const float4* rgbz, const float4* cov_r,
                                    const int4* tile_rect, Fs4dProjected o) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= (int64_t)counters[CNT_VISIBLE] || r >= K) return;
   const uint32_t i = order[r];
-  const float2 m = xy[i];
+  const float4 m4 = xy[i];
+  const float2 m = make_float2(m4.x + m4.z, m4.y + m4.w);
   const float4 co = conic_o[i], cz = rgbz[i], cv = cov_r[i];
   if (o.mean2d) { o.mean2d[2 * r] = m.x; o.mean2d[2 * r + 1] = m.y; }
   if (o.cov2d) { o.cov2d[3 * r] = cv.x; o.cov2d[3 * r + 1] = cv.y; o.cov2d[3 * r + 2] = cv.z; }
@@ -705,7 +715,7 @@ int render_export_projected(const RenderLayout& L, void* ws, Fs4dProjected& out,
   const uint32_t* dv = depth_order(L, ws, s);
   if (L.K > 0)
     k_export_projected<<<(unsigned)ceil_div(L.K, 256), 256, 0, s>>>(
-        dv, at<uint32_t>(ws, L.counters), L.K, at<float2>(ws, L.xy), at<float4>(ws, L.conic_o),
+        dv, at<uint32_t>(ws, L.counters), L.K, at<float4>(ws, L.xy), at<float4>(ws, L.conic_o),
         at<float4>(ws, L.rgbz), at<float4>(ws, L.cov_r), at<int4>(ws, L.tile_rect), out);
   return check_launch("render_export_projected");
 }

@@ -198,6 +198,7 @@ struct AdamTable {
   int n;
   int64_t block_start[FS4D_MAX_ADAM_SEGMENTS + 1];
   Fs4dAdamSegment seg[FS4D_MAX_ADAM_SEGMENTS];
+  int32_t slot[FS4D_MAX_ADAM_SEGMENTS];  // table entry -> caller's segment index (step count / status)
 };
 
 __device__ __forceinline__ int adam_segment_of(const AdamTable& T, int64_t b) {
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_adam_check(const __grid_constant__
   for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);
   if ((threadIdx.x & 31) == 0 && bad) {
     atomicAdd(&status[FS4D_ST_ADAM_BAD_COUNT], bad);
-    atomicMin(&status[FS4D_ST_ADAM_BAD_SEG], s);
+    atomicMin(&status[FS4D_ST_ADAM_BAD_SEG], T.slot[s]);
     raise_status(status, FS4D_ERR_NUMERIC);
   }
 }
@@ -232,7 +233,9 @@ __global__ void __launch_bounds__(kThreads) k_adam_apply(const __grid_constant__
                                                         const float* __restrict__ g, float* __restrict__ m,
                                                         float* __restrict__ v, int32_t* __restrict__ steps,
                                                         int32_t* __restrict__ status) {
-  if (status[FS4D_ST_ADAM_BAD_SEG] != 0x7FFFFFFF) return;  // non-finite gradient: nothing is touched
+  // non-finite gradient (or a failed render gated in by fs4d_status_merge):
+  // nothing is touched
+  if (status[FS4D_ST_ADAM_BAD_SEG] != 0x7FFFFFFF) return;
   __shared__ float s_coef[4];
   const int s = adam_segment_of(T, blockIdx.x);
   const Fs4dAdamSegment& S = T.seg[s];
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_adam_apply(const __grid_constant__
     // AdamState.step_count += 1 (numerics.py:154); beta^step by binary
     // powering in fp64 (~2 log2(step) multiplies, a few hundred cycles, where
     // the libm pow() call stalled every block for microseconds)
-    int e = steps[s] + 1;
+    int e = steps[T.slot[s]] + 1;
     double p1 = 1.0, p2 = 1.0, b1d = S.beta1, b2d = S.beta2;
     while (e) {
       if (e & 1) p1 *= b1d, p2 *= b2d;
@@ -297,23 +300,30 @@ __global__ void __launch_bounds__(kThreads) k_adam_apply(const __grid_constant__
     __threadfence();
     const unsigned ticket = atomicAdd((unsigned*)&status[kStAdamDone], 1u);
     if (ticket == gridDim.x - 1) {
-      for (int i = 0; i < T.n; ++i) steps[i] += 1;
+      for (int i = 0; i < T.n; ++i) steps[T.slot[i]] += 1;
       status[kStAdamDone] = 0;
     }
   }
 }
 
 int adam_step(float* p, const float* g, float* m, float* v, int32_t* steps, const Fs4dAdamSegment* segs, int n,
-              int32_t* status, cudaStream_t s) {
+              const int32_t* active, int32_t* status, cudaStream_t s) {
+  // inactive segments (arrays without a gradient this iteration,
+  // training.py:513-515) are left out of the table: neither their
+  // parameters, moments nor step counts change
   AdamTable T;
-  T.n = n;
   int64_t blocks = 0;
+  int nt = 0;
   for (int i = 0; i < n; ++i) {
-    T.seg[i] = segs[i];
-    T.block_start[i] = blocks;
+    if (active && !active[i]) continue;
+    T.seg[nt] = segs[i];
+    T.slot[nt] = i;
+    T.block_start[nt] = blocks;
     blocks += ceil_div(segs[i].count, kAdamChunk);
+    ++nt;
   }
-  T.block_start[n] = blocks;
+  T.n = nt;
+  T.block_start[nt] = blocks;
   if (blocks == 0) return FS4D_OK;
   if (blocks > 0x7FFFFFFF) return fail(FS4D_ERR_CONFIG, "adam buffer too large");
   k_adam_check<<<(unsigned)blocks, kThreads, 0, s>>>(T, g, status);

@@ -15,7 +15,7 @@ import numpy as np
 
 from .errors import ConfigurationError, ContractViolation
 from .gaussians import GaussianCloud
-from .numerics import linear_layer, mlp_params, set_mlp_params
+from .numerics import linear_layer, mlp_forward, mlp_params, set_mlp_params
 
 BRANCHES = ("position", "rotation", "scale", "opacity")
 BRANCH_DIMS = {"position": 3, "rotation": 4, "scale": 3, "opacity": 1}
@@ -67,6 +67,36 @@ class DeformationNet:
     def set_params(self, arrays):
         for prefix, stack in self.stacks():
             set_mlp_params(stack, prefix, arrays)
+
+
+# ---------------------------------------------------------------------------
+# the stacks one at a time (deformation.py:74-97), each layer on device via
+# numerics.mlp_forward; deform() runs them fused on the tensor cores
+# ---------------------------------------------------------------------------
+def decode_hidden(net, latent):
+    """Trunk output for latent [K, latent_dim]."""
+    h, _ = mlp_forward(net.trunk, latent)
+    return h
+
+
+def decode_branches(net, hidden):
+    """(deltas, feats): per branch, the head output and the extractor output."""
+    deltas, feats = {}, {}
+    for name in BRANCHES:
+        hg, _ = mlp_forward(net.extractors[name], hidden)
+        feats[name] = hg
+        deltas[name], _ = mlp_forward(net.heads[name], hg)
+    return deltas, feats
+
+
+def update_semantics(net, branch_feats, features):
+    """z' = z + F_feat([h_pos | h_rot | h_scale | h_opacity]); the features
+    object itself when the update is disabled."""
+    if not net.cfg.enable_feature_update:
+        return features
+    joint = np.concatenate([np.asarray(branch_feats[n], dtype=np.float64) for n in BRANCHES], axis=-1)
+    delta, _ = mlp_forward(net.feature_mlp, joint)
+    return features + delta
 
 
 def _device_parts(cloud, field, net):

@@ -1,15 +1,18 @@
-"""HexPlane field container (hexplane.py:16-92 API).
+"""HexPlane field (hexplane.py:16-222 API).
 
 Planes are stored channel-last [Ra, Rb, C] float64 on the host like the
-reference; the query (bilinear gather + six-plane product) and its backward
-run inside libfs4d's deform kernels (csrc/deform.cu).
+reference.  The query (bilinear gather + six-plane product) and its backward
+run in libfs4d: fused into the deformation kernels on the frame path, and on
+their own behind ``query`` / ``query_with_cache`` / ``query_backward``
+(fs4d_hexplane_query / fs4d_hexplane_query_backward), which keep the
+reference's signatures, NumPy in / out, and also accept fp32 CUDA tensors.
 """
 
 from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import ConfigurationError
+from .errors import ConfigurationError, ContractViolation
 
 PLANE_AXES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
 TIME_AXIS = 3
@@ -69,6 +72,20 @@ class HexPlaneField:
     def latent_dim(self):
         return self.channels * len(self.cfg.levels)
 
+    def normalized_coords(self, positions, t):
+        """(coords [K, 4], inside [K, 3]) of hexplane.py:84-92: spatial
+        coordinates (p - lo) / (hi - lo) clipped to [0, 1], inside = strictly
+        within (0, 1) per axis, t clipped to [0, 1].  A host helper of the
+        container (like scene_aabb); the kernels compute the same values in
+        fp64 per Gaussian."""
+        p = np.asarray(positions, dtype=np.float64)
+        lo, hi = self.aabb[0], self.aabb[1]
+        raw = (p - lo) / (hi - lo)
+        coords = np.empty((p.shape[0], 4))
+        coords[:, :3] = np.clip(raw, 0.0, 1.0)
+        coords[:, 3] = min(max(float(t), 0.0), 1.0)
+        return coords, (raw > 0.0) & (raw < 1.0)
+
     def param_arrays(self):
         return {f"grid.l{li}.p{pi}": plane
                 for li, level in enumerate(self.planes) for pi, plane in enumerate(level)}
@@ -76,6 +93,58 @@ class HexPlaneField:
     def set_param(self, name, arr):
         _, l, p = name.split(".")
         self.planes[int(l[1:])][int(p[1:])] = arr
+
+
+# ---------------------------------------------------------------------------
+# query / query_with_cache / query_backward (hexplane.py:113-187), on device
+# ---------------------------------------------------------------------------
+def query(field, positions, t):
+    """Latent [K, channels * levels] of `positions` at time t."""
+    f, _ = query_with_cache(field, positions, t)
+    return f
+
+
+def query_with_cache(field, positions, t):
+    """Latent plus the record query_backward needs (the device positions and
+    t: the backward re-selects every bilinear cell in fp64 instead of storing
+    them)."""
+    import torch
+
+    from . import _native as N
+    from .device import _p, _stream, as_device, to_host
+    dev, _ = _device_field(field)
+    pos, host = as_device(positions)
+    pos = pos.reshape(-1, 3)
+    k = int(pos.shape[0])
+    lat = torch.empty(k, dev.latent_dim, dtype=torch.float32, device=pos.device)
+    import ctypes
+    fs = dev.struct()
+    N.check(N.load().fs4d_hexplane_query(ctypes.byref(fs), _p(pos), k, float(t), _p(lat), _stream()))
+    cache = {"k": k, "t": float(t), "positions": pos, "field": dev, "host": host}
+    return to_host(lat, host), cache
+
+
+def query_backward(field, cache, dL_df):
+    """(plane_grads mirroring field.planes, dL/dpositions [K, 3]); position
+    gradients are zero on every clamped axis (hexplane.py:186)."""
+    import torch
+
+    from . import _native as N
+    from .device import _p, _stream, as_device, to_host
+    k = cache["k"]
+    dev = cache.get("field") or _device_field(field)[0]
+    up, _ = as_device(dL_df)
+    if tuple(up.shape) != (k, dev.latent_dim):
+        raise ContractViolation(f"dL_df shape {tuple(up.shape)} does not match ({k}, {dev.latent_dim})")
+    grads = dev.zeros_like()
+    dpos = torch.empty(k, 3, dtype=torch.float32, device=up.device)
+    import ctypes
+    gs, fs = grads.struct(), dev.struct()
+    N.check(N.load().fs4d_hexplane_query_backward(ctypes.byref(fs), _p(cache["positions"]), k, cache["t"], _p(up),
+                                                  ctypes.byref(gs), _p(dpos), 0, _stream()))
+    host = cache.get("host", True)
+    planes = grads.planes if not host else [[p.cpu().numpy().astype(np.float64) for p in lv] for lv in grads.planes]
+    return planes, to_host(dpos, host)
 
 
 # ---------------------------------------------------------------------------

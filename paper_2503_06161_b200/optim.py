@@ -74,21 +74,39 @@ class FlatAdam:
                 raise ConfigurationError(f"Adam segment {name} ends at {off}, buffer has {params.numel()}")
         self.names = [n for n, _ in self.specs]
 
-    def step(self, grads, lrs):
+    def step(self, grads, lrs, active=None, guards=()):
         """grads: flat fp32 CUDA buffer of the same layout; lrs: name -> lr or
-        schedule-key -> lr.  Stream-ordered; check() reads the status."""
+        schedule-key -> lr.  active: optional set of array names stepped this
+        iteration (the others keep parameters, moments and step counts,
+        training.py:513-531); default all.  guards: device status blocks of
+        this iteration's renders -- if any of them holds an error the whole
+        step is skipped on device (fs4d_status_merge).  The status block is
+        reset every step; stream-ordered, check() reads it."""
+        lib = N.load()
+        self.status.reset()
+        for g in guards:
+            N.check(lib.fs4d_status_merge(_p(g), _p(self.status.t), 1, _stream()))
+        mask = None
         for i, name in enumerate(self.names):
+            if active is not None and name not in active:
+                continue
             lr = lrs[name] if name in lrs else lrs[schedule_key(name)]
             self.segs[i].lr = float(lr)
-        N.check(N.load().fs4d_adam_step(_p(self.params), _p(grads), _p(self.m), _p(self.v), _p(self.steps),
-                                        self.segs, len(self.names), _p(self.status.t), _stream()))
+        if active is not None:
+            mask = (ctypes.c_int32 * max(len(self.names), 1))(*[int(n in active) for n in self.names])
+        N.check(lib.fs4d_adam_step_masked(_p(self.params), _p(grads), _p(self.m), _p(self.v), _p(self.steps),
+                                          self.segs, mask, len(self.names), _p(self.status.t), _stream()))
 
-    def check(self):
-        """Raise NumericalError (numerics.py:149-153) if a step saw a non-finite gradient."""
-        st = self.status.read()
+    def check(self, st=None):
+        """Raise if the last step did not apply: NumericalError
+        (numerics.py:149-153) for a non-finite gradient, or the gated render
+        error (capacity / numeric) that made it skip.  `st`: an already
+        read-back status block."""
+        st = self.status.read() if st is None else st
         if int(st[N.ST_CODE]) != 0:
             seg = int(st[N.ST_ADAM_BAD_SEG])
+            if seg == N.ADAM_GATED:
+                N.raise_device_status(st)
             name, shape = self.specs[seg] if 0 <= seg < len(self.specs) else ("?", ())
-            self.status.reset()
             raise NumericalError(f"param {name}: non-finite gradient ({int(st[N.ST_ADAM_BAD_COUNT])} entries) "
                                  f"for param of shape {shape}")

@@ -56,6 +56,23 @@ class ProjectedGaussians:
 
 
 @dataclass
+class TileRecord:
+    """Compositing state of one tile (rasterizer.py:64-78), replayed from the
+    device record: depth-ordered rows into ``proj`` with at least one live
+    pixel, and their [G, P] gated alpha, 2-d Gaussian and raw alpha values
+    exactly as the blend kernel evaluated them."""
+
+    rows: np.ndarray
+    alpha: np.ndarray
+    g2d: np.ndarray
+    a_raw: np.ndarray
+    x0: int
+    y0: int
+    xs: np.ndarray
+    ys: np.ndarray
+
+
+@dataclass
 class RasterRecord:
     """Device record replayed by the backward (rasterizer.py:81-91)."""
 
@@ -73,7 +90,29 @@ class RasterRecord:
     def proj(self):
         if self._proj is None:
             self._proj = _export_projected(self)
+            self._proj._record = self
         return self._proj
+
+    @property
+    def tiles(self):
+        """Flat list of TileRecord for every tile with a live row, in the
+        reference's row-major tile order (rasterizer.py:275-288), replayed on
+        the device from this record (fs4d_render_tile_alphas)."""
+        if getattr(self, "_tile_records", None) is None:
+            t = self.cfg.tile
+            recs = []
+            for ty, row in enumerate(self.tile_lists()):
+                ys = np.arange(ty * t, min(ty * t + t, self.height))
+                for tx, idx in enumerate(row):
+                    if idx.size == 0:
+                        continue
+                    xs = np.arange(tx * t, min(tx * t + t, self.width))
+                    rows, alpha, g2d, a_raw = _tile_alphas(self.proj, idx, xs, ys, self.cfg)
+                    if rows.size:
+                        recs.append(TileRecord(rows=rows, alpha=alpha, g2d=g2d, a_raw=a_raw, x0=int(xs[0]),
+                                               y0=int(ys[0]), xs=xs, ys=ys))
+            self._tile_records = recs
+        return self._tile_records
 
     def tile_lists(self):
         """tiles[ty][tx] -> rows into ``proj`` in depth order (bin_tiles layout)."""
@@ -98,39 +137,27 @@ class RenderOutput:
     n_contrib: np.ndarray = None   # live contributors per pixel (a19)
 
     def pixel_record(self, row, col):
-        """Contributing (source_index, alpha, weight) triples of one pixel,
-        replayed from the record's projected Gaussians (rasterizer.py:102-114)."""
+        """Contributing (source_index, alpha, weight) triples of one pixel
+        (rasterizer.py:102-114), replayed on the device from the render
+        record with the blend kernel's arithmetic (fs4d_render_tile_alphas +
+        fs4d_composite_weights), so they agree with ``n_contrib``."""
         rec = self.record
         t = rec.cfg.tile
-        rows = rec.tile_lists()[row // t][col // t]
+        idx = rec.tile_lists()[row // t][col // t]
+        empty = (np.empty(0, dtype=np.int64), np.empty(0), np.empty(0))
+        if idx.size == 0:
+            return empty
+        y0, x0 = (row // t) * t, (col // t) * t
+        xs = np.arange(x0, min(x0 + t, rec.width))
+        ys = np.arange(y0, min(y0 + t, rec.height))
+        rows, alpha, _, _ = _tile_alphas(rec.proj, idx, xs, ys, rec.cfg)
         if rows.size == 0:
-            return np.empty(0, dtype=np.int64), np.empty(0), np.empty(0)
-        proj = rec.proj
-        cfg = rec.cfg
-        src, alphas, weights = [], [], []
-        T = 1.0
-        q_skip = 2.0 * np.log(255.0)
-        for g in rows:
-            dx = col - proj.mean2d[g, 0]
-            dy = row - proj.mean2d[g, 1]
-            r = proj.radius[g]
-            if abs(dx) > r or abs(dy) > r:
-                continue
-            c = proj.conic[g]
-            q = c[0, 0] * dx * dx + (c[0, 1] + c[1, 0]) * dx * dy + c[1, 1] * dy * dy
-            if q > q_skip:
-                continue
-            a = min(proj.opacity[g] * np.exp(-0.5 * q), cfg.alpha_cap)
-            if a < cfg.alpha_skip:
-                continue
-            if T < cfg.stop_transmittance:
-                break
-            src.append(proj.source_index[g])
-            alphas.append(a)
-            weights.append(a * T)
-            T *= 1.0 - a
-        return (np.asarray(src, dtype=np.int64), np.asarray(alphas, dtype=np.float64),
-                np.asarray(weights, dtype=np.float64))
+            return empty
+        p = (row - y0) * xs.size + (col - x0)
+        _, contrib, w, _ = _composite_weights(alpha, rec.cfg.stop_transmittance)
+        a = alpha[:, p]
+        live = (a > 0) & contrib[:, p]
+        return rec.proj.source_index[rows[live]], a[live], w[live, p]
 
 
 @dataclass
@@ -191,6 +218,63 @@ def _export_projected(record):
         feature=np.asarray(feats, dtype=np.float64)[src, :n] if n else np.zeros((m, 0)),
         source_index=src,
     )
+
+
+def _tile_alphas(proj, idx, xs, ys, cfg):
+    """Gated alpha matrices of one tile, compressed to rows that touch it
+    (rasterizer.py:215-234): (rows, alpha, g2d, a_raw) with rows indexing into
+    ``proj``.  Replayed on the device from the render record ``proj`` came
+    from, with the blend kernel's own arithmetic; ``proj`` must come from
+    this package's project() / render()."""
+    import torch
+    import ctypes
+
+    from . import _native as N
+    from .device import _p, _stream, raster_struct
+    rec = getattr(proj, "_record", None)
+    if rec is None:
+        raise ContractViolation("_tile_alphas needs the ProjectedGaussians of a device project() / render() call")
+    idx = np.asarray(idx, dtype=np.int64).reshape(-1)
+    xs, ys = np.asarray(xs, dtype=np.int64), np.asarray(ys, dtype=np.int64)
+    nx, ny = int(xs.size), int(ys.size)
+    if (nx and not np.array_equal(xs, np.arange(xs[0], xs[0] + nx))) or \
+            (ny and not np.array_equal(ys, np.arange(ys[0], ys[0] + ny))):
+        raise ConfigurationError("tile pixel columns / rows must be contiguous ranges")
+    g = int(idx.size)
+    if g == 0 or nx == 0 or ny == 0:
+        z = np.zeros((0, nx * ny))
+        return idx[:0], z, z.copy(), z.copy()
+    dev = rec.device
+    src = torch.as_tensor(proj.source_index[idx].astype(np.int32), device="cuda")
+    f = dict(dtype=torch.float32, device="cuda")
+    alpha, g2d, a_raw = torch.empty(g, nx * ny, **f), torch.empty(g, nx * ny, **f), torch.empty(g, nx * ny, **f)
+    rc = raster_struct(rec.cfg if cfg is None else cfg)
+    N.check(N.load().fs4d_render_tile_alphas(ctypes.byref(dev.info), _p(dev.ws), dev.ws.numel(), ctypes.byref(rc),
+                                             _p(src), g, int(xs[0]), int(ys[0]), nx, ny, _p(alpha), _p(g2d),
+                                             _p(a_raw), _stream()))
+    alpha, g2d, a_raw = _host(alpha), _host(g2d), _host(a_raw)
+    keep = np.nonzero(alpha.max(axis=1) > 0.0)[0]
+    return idx[keep], alpha[keep], g2d[keep], a_raw[keep]
+
+
+def _composite_weights(alpha, stop):
+    """(t_exc, contrib, w, t_final) of a [G, P] alpha matrix
+    (rasterizer.py:244-261), front to back on the device in fp32 with the
+    blend kernel's multiplication order."""
+    import torch
+
+    from . import _native as N
+    from .device import _p, _stream, as_device
+    a, _ = as_device(np.atleast_2d(np.asarray(alpha, dtype=np.float64)) if not isinstance(alpha, torch.Tensor)
+                     else alpha)
+    g, p = int(a.shape[0]), int(a.shape[1])
+    f = dict(dtype=torch.float32, device=a.device)
+    t_exc, w = torch.empty(g, p, **f), torch.empty(g, p, **f)
+    contrib = torch.empty(g, p, dtype=torch.uint8, device=a.device)
+    t_final = torch.empty(p, **f)
+    N.check(N.load().fs4d_composite_weights(_p(a), g, p, float(stop), _p(t_exc), _p(contrib), _p(w), _p(t_final),
+                                            _stream()))
+    return _host(t_exc), contrib.cpu().numpy().astype(bool), _host(w), _host(t_final)
 
 
 def project(snapshot, frame, cfg):

@@ -20,6 +20,7 @@ Loss modes:
             against a teacher map (training.py:497-505) in one fused kernel.
 """
 
+import collections
 import ctypes
 import os
 
@@ -27,7 +28,9 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import DeformEngine, DeviceCloud, DeviceField, DeviceNet, Renderer, _p, _stream, locality_order
+from .device import (DeformEngine, DeviceCloud, DeviceField, DeviceNet, Renderer, StatusBlock, _p, _stream,
+                     locality_order)
+from .errors import NumericalError
 from .hexplane import tv_loss_grad_device
 from .numerics import lr_at_step
 from .optim import FlatAdam
@@ -108,6 +111,10 @@ class TrainStep:
         self.iteration = 0
         self.stats = None      # ViewspaceGradStats on device when track_stats() is on
         self.vs_norm = None
+        # asynchronous error reporting: every step copies its status blocks
+        # (one per lane + the Adam block) to pinned host memory; the next
+        # run() (or sync()) inspects them and raises
+        self._pending = collections.deque()
 
     def _bind(self, flat):
         """DeviceCloud / DeviceField / DeviceNet views into a flat buffer."""
@@ -183,17 +190,48 @@ class TrainStep:
                                      decoder_loss=DecoderLoss(self.device),
                                      vs_norm=None if self.vs_norm is None else torch.empty_like(self.vs_norm))
             ln.cache, ln.photo_ws = None, None
+            ln.step_status = StatusBlock(self.device)  # every render of this lane's pairs, merged
             ln.stream = torch.cuda.Stream(device=self.device) if self.n_lanes > 1 else None
             lanes.append(ln)
         self._lanes = lanes
         return lanes
+
+    def active_arrays(self, batch):
+        """Parameter arrays that receive a gradient this iteration -- the keys
+        of the reference's `grads` dict (training.py:509-531): `features`
+        only with feature supervision, grid.* only with the HexPlane,
+        net.feat.* only with the feature update, decoder.* only when the
+        decoder loss ran.  The others are left out of the Adam step."""
+        dout = self.d_feature.shape[2]
+        if self.loss_mode == "raw":
+            feature_on = dout > 0
+        else:
+            feature_on = dout > 0 and self.decoder is not None and any(
+                len(it) > 4 and it[4] is not None for it in batch)
+        act = set()
+        for name, _ in self.specs:
+            if name == "features" and not feature_on:
+                continue
+            if name.startswith("grid.") and not self.net.enable_grid:
+                continue
+            if name.startswith("net.feat.") and not self.net.enable_feature_update:
+                continue
+            if name.startswith("decoder.") and not feature_on:
+                continue
+            act.add(name)
+        return act
 
     def run(self, batch, check=False):
         """batch: list of (t, K, T, target_rgb [H,W,3], target_feat) CUDA
         tensors; loss_mode "decoder" additionally takes optional
         (mask uint8 [H,W] | None, target_depth [H,W] | None) as items 5-6 and
         target_feat is the teacher map [ho,wo,Ct].  Returns the device loss
-        (mean over pairs and ranks after the reduce)."""
+        (mean over pairs and ranks after the reduce).
+
+        check=False keeps the step asynchronous: device errors of THIS step
+        (tile-pair overflow, non-finite snapshot or gradient) skip its Adam
+        update on the device and are raised by the next run() or sync()."""
+        self._poll(block=False)
         lib = N.load()
         n = len(batch) * self.world
         w = 1.0 / n
@@ -207,6 +245,8 @@ class TrainStep:
         lanes = self._lanes or self._make_lanes()
         nl = len(lanes)
         main = torch.cuda.current_stream()
+        for ln in lanes:
+            ln.step_status.reset()
         if nl > 1:
             ready = torch.cuda.Event()
             ready.record(main)
@@ -232,11 +272,74 @@ class TrainStep:
             import torch.distributed as dist
             dist.all_reduce(self.loss, op=dist.ReduceOp.SUM, group=self.group)
         if self.optimizer is not None:
-            self.optimizer.step(self.grads.buffer, self.current_lrs())
-            if check:
-                self.optimizer.check()
+            self.optimizer.step(self.grads.buffer, self.current_lrs(), active=self.active_arrays(batch),
+                                guards=[ln.step_status.t for ln in used])
             self.iteration += 1
+        self._post_status(used)
+        if check:
+            self.sync()
         return self.loss
+
+    _MAX_PENDING = 2  # steps whose status may still be in flight before run() blocks on the oldest
+
+    def _post_status(self, used):
+        """Queue the D2H copy of this step's status blocks (pinned, async)."""
+        rows = len(used) + 1
+        host = torch.zeros((rows, N.STATUS_WORDS), dtype=torch.int32).pin_memory()
+        for j, ln in enumerate(used):
+            host[j].copy_(ln.step_status.t, non_blocking=True)
+        if self.optimizer is not None:
+            host[len(used)].copy_(self.optimizer.status.t, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._pending.append((ev, list(used), self.optimizer is not None, host))
+
+    def _poll(self, block):
+        """Inspect finished steps' status copies in order (all of them when
+        `block`, else the completed ones plus enough to keep at most
+        _MAX_PENDING in flight)."""
+        while self._pending:
+            ev = self._pending[0][0]
+            if not (block or ev.query() or len(self._pending) > self._MAX_PENDING):
+                break
+            ev.synchronize()
+            self._inspect(*self._pending.popleft()[1:])
+
+    def sync(self):
+        """Wait for every queued step's status and raise its device error,
+        if any: a tile-pair overflow grows that lane's pair buffer first (so
+        re-running the batch succeeds) and raises CapacityError; a
+        non-finite snapshot or gradient raises NumericalError.  Either way
+        that step's Adam update was skipped on the device, so its parameters,
+        moments and step counts stayed as they were and `iteration` is
+        rolled back by one."""
+        self._poll(block=True)
+
+    def _inspect(self, used, has_opt, host):
+        st = host.numpy()
+        failed = None
+        for j, ln in enumerate(used):
+            row = st[j]
+            code = int(row[N.ST_CODE])
+            if code == N.ERR_CAPACITY:
+                pairs = (int(row[N.ST_PAIRS_HI]) << 32) | (int(row[N.ST_PAIRS_LO]) & 0xFFFFFFFF)
+                ln.renderer.cap = max(int(ln.renderer.cap or 0), int(pairs * 1.25) + 1024)
+            if code != N.OK and failed is None:
+                failed = row.copy()
+        if has_opt and failed is None and int(st[len(used)][N.ST_CODE]) != N.OK:
+            failed = st[len(used)].copy()
+        if failed is None:
+            return
+        self._pending.clear()
+        if has_opt:
+            self.iteration -= 1
+            seg = int(failed[N.ST_ADAM_BAD_SEG])
+            if int(failed[N.ST_CODE]) == N.ERR_NUMERIC and seg not in (N.ADAM_GATED, 0x7FFFFFFF):
+                self.optimizer.check(failed)  # non-finite gradient: names the parameter array
+        try:
+            N.raise_device_status(failed)
+        except Exception as e:
+            raise type(e)(f"training step skipped on the device (parameters unchanged): {e}") from None
 
     def _run_pair(self, ln, item, field, w, dout, first, check, stats_done):
         """One (view, t) pair on lane `ln` (the current stream): deform, render,
@@ -246,6 +349,7 @@ class TrainStep:
         t, K, T, tgt_rgb, tgt_feat = item[:5]
         _, ln.cache = ln.deformer.forward(self.cloud, field, self.net, t, out=ln.snap, with_cache=ln.cache or True)
         imgs, rec = ln.renderer.forward(ln.snap, K, T, self.h, self.w, self.cfg, images=ln.images, check=check)
+        N.check(lib.fs4d_status_merge(_p(ln.renderer.status.t), _p(ln.step_status.t), 0, _stream()))
         d_depth = None
         if self.loss_mode == "raw":
             N.check(lib.fs4d_l1_loss_grad(_p(imgs["color"]), _p(tgt_rgb), _p(imgs["feature"]) if dout else None,
@@ -316,10 +420,26 @@ class TrainStep:
             off, cnt = old_params.offsets[i], old_params.sizes[i]
             shape = old_params.views[n].shape
             extras += [old_opt.m[off:off + cnt].view(shape), old_opt.v[off:off + cnt].view(shape)]
+        self.sync()
         stats = self.stats if self.stats is not None else ViewspaceGradStats.zeros(len(self.cloud), self.device)
+        if self.world > 1:
+            # every rank saw different (view, t) pairs: classify on the sums
+            # over all ranks, as a single process training on the union would
+            # (SURVEY §8(e)); the split samples must come from the same seeded
+            # rng on every rank (gaussians.py:380-383)
+            import torch.distributed as dist
+            dist.all_reduce(stats.accum, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(stats.count, op=dist.ReduceOp.SUM, group=self.group)
         out, new_stats, outs, rep = DeviceDensity(self.device).run(self.cloud, stats, cfg, extent, rng, prune_only,
                                                                    extras)
         k = len(out)
+        if self.world > 1:
+            import torch.distributed as dist
+            ks = torch.tensor([k, -k], dtype=torch.int64, device=self.device)
+            dist.all_reduce(ks, op=dist.ReduceOp.MAX, group=self.group)
+            if int(ks[0]) != k or -int(ks[1]) != k:
+                raise RuntimeError(f"density control diverged across ranks (K = {k} here, range "
+                                   f"[{-int(ks[1])}, {int(ks[0])}]): seed the split rng identically on every rank")
         d, sh = out.feature_dim, out.sh_degree
         field_specs = [(n, sh_) for n, sh_ in old_specs if n not in per]
         new_specs = gradient_specs(k, d, sh, [], []) + field_specs

@@ -329,8 +329,103 @@ def checkpoint_case(ref, seed=41):
     print("checkpoint", len(buf.getvalue()), "bytes")
 
 
+def hexplane_edge_case(ref, name, t, seed=47):
+    """HexPlane edge semantics (hexplane.py:84-110, 145-187; SURVEY Appendix A
+    #11/#13): Gaussians outside the aabb along every axis (clamped coords, no
+    dpos), Gaussians exactly on the lower and upper faces (raw = 0 / 1: the
+    c = 1 cell is i0 = R-2, fa = 1), and t at the ends of [0, 1] (and beyond,
+    clipped).  Stores the query, query_backward and the full deform /
+    deform_backward through the reference."""
+    H, D, G = ref["hexplane"], ref["deformation"], ref["gaussians"]
+    rng = np.random.default_rng(seed)
+    k, nf = 48, 8
+    arrs = cloud_arrays(rng, k, nf, (0.15, 0.3), (2.2, 3.8))
+    aabb = np.array([[-1.0, -1.0, 2.0], [1.0, 1.0, 4.0]])  # fp32-exact faces
+    pos = arrs["positions"].copy()
+    for i in range(12):                       # outside along each axis, both sides
+        ax, side = i % 3, (i // 3) % 2
+        pos[i, ax] = aabb[side, ax] + (0.25 + 0.1 * i) * (1 if side else -1)
+    for i in range(12, 18):                   # exactly on a face
+        ax, side = i % 3, (i // 3) % 2
+        pos[i, ax] = aabb[side, ax]
+    pos[18] = aabb[0]                         # both corners of the box
+    pos[19] = aabb[1]
+    pos[20] = aabb[1] + 0.5                   # outside on every axis
+    arrs["positions"] = f32(pos)
+    # 32 channels per plane and a width-64 depth-1 net: the shapes of the
+    # tensor-core deformation path (the configs[1] kernels)
+    field = H.HexPlaneField(H.HexPlaneConfig(levels=(1, 2), base_resolution=(6, 5, 7, 4), out_dim=64), aabb, rng)
+    for li, level in enumerate(field.planes):
+        for pi in range(len(level)):
+            field.planes[li][pi] = f32(0.8 + rng.normal(size=level[pi].shape) * 0.3)
+    net = D.DeformationNet(field.latent_dim, D.DeformationConfig(width=64, depth=1, feature_dim=nf), rng)
+    for prefix, stack in net.stacks():
+        for layer in stack:
+            layer.weight = f32(rng.normal(size=layer.weight.shape) * 0.15)
+            layer.bias = f32(rng.normal(size=layer.bias.shape) * 0.2)
+    cloud = G.GaussianCloud(**{k_: v.copy() for k_, v in arrs.items()})
+    lat, qcache = H.query_with_cache(field, cloud.positions, t)
+    d_lat = f32(rng.normal(size=lat.shape))
+    qpg, qdpos = H.query_backward(field, qcache, d_lat)
+    coords, inside = field.normalized_coords(cloud.positions, t)
+    snap, cache = D.deform_with_cache(cloud, field, net, t)
+    ups = {n_: f32(rng.normal(size=np.shape(getattr(cloud, n_))))
+           for n_ in ("positions", "rotations", "log_scales", "opacity_logits", "features")}
+
+    class Gr:
+        pass
+
+    gr = Gr()
+    for n_, v in ups.items():
+        setattr(gr, n_, v)
+    cg, ng, pg = D.deform_backward(cloud, field, net, cache, gr)
+    data = {f"cloud_{k_}": v for k_, v in arrs.items()}
+    data.update(aabb=aabb, t=t, width=64, depth=1, levels=np.asarray((1, 2)), base=np.asarray((6, 5, 7, 4)),
+                out_dim=64, feature_dim=nf, latent=lat, d_latent=d_lat, query_dpos=qdpos, coords=coords,
+                inside=inside)
+    for li, level in enumerate(field.planes):
+        for pi, pl in enumerate(level):
+            data[f"plane_{li}_{pi}"] = pl
+            data[f"qgplane_{li}_{pi}"] = qpg[li][pi]
+            data[f"gplane_{li}_{pi}"] = pg[li][pi]
+    for prefix, stack in net.stacks():
+        for i, layer in enumerate(stack):
+            data[f"w:{prefix}.{i}"] = layer.weight
+            data[f"b:{prefix}.{i}"] = layer.bias
+    for k_, v in ng.items():
+        data[f"g:{k_}"] = v
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        data[f"snap_{f}"] = getattr(snap, f)
+        data[f"up_{f}"] = ups[f]
+    data["cg_positions"] = cg["positions"]
+    np.savez_compressed(os.path.join(OUT, f"hexplane_{name}.npz"), **data)
+    print("hexplane", name, "outside", int((~inside).any(axis=1).sum()))
+
+
+def feature_map_case(ref, seed=43):
+    """An FE4D teacher-feature file written by the reference's own
+    save_feature_map (semantic.py:49-55)."""
+    S = ref["semantic"]
+    rng = np.random.default_rng(seed)
+    fmap = S.FeatureMap(rng.normal(size=(3, 5, 7)).astype(np.float32))
+    S.save_feature_map(os.path.join(OUT, "feature_map.feat"), fmap)
+    print("feature map", fmap.data.shape)
+
+
+def hexplane_edges(ref):
+    hexplane_edge_case(ref, "t0", 0.0)
+    hexplane_edge_case(ref, "t1", 1.0)
+    hexplane_edge_case(ref, "tclip", 1.3)
+
+
 def main():
     ref = load_reference()
+    if len(sys.argv) > 1 and sys.argv[1] == "feature_map":
+        feature_map_case(ref)
+        return
+    if len(sys.argv) > 1 and sys.argv[1] == "hexplane_edges":
+        hexplane_edges(ref)
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "checkpoint":
         checkpoint_case(ref)
         return
@@ -343,6 +438,8 @@ def main():
     train_ops_case(ref)
     density_case(ref)
     checkpoint_case(ref)
+    feature_map_case(ref)
+    hexplane_edges(ref)
     # the reference's own tiled-vs-naive scenes (test_rasterizer.py:168-183 sizes)
     render_case(ref, "s0", 0, 50, 32, 32, 4, 1.1 * 32, (0.1, 0.2, 0.3))
     render_case(ref, "s1", 1, 200, 64, 64, 16, 1.1 * 64, (0.1, 0.2, 0.3))

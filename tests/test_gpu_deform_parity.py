@@ -253,3 +253,60 @@ def test_locality_order_is_a_permutation_and_changes_nothing():
     torch.cuda.synchronize()
     for name in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
         assert torch.equal(getattr(s0, name), getattr(s1, name)), name
+
+
+@pytest.mark.parametrize("case", ["t0", "t1", "tclip"])
+def test_hexplane_edges_match_reference_golden(case):
+    """Outside-aabb Gaussians (clamped coordinates, no dpos), Gaussians on the
+    aabb faces (c = 1 -> i0 = R-2, fa = 1) and t = 0 / 1 / 1.3 (clipped),
+    through the tensor-core deformation path (32 channels, width 64): forward
+    and backward against reference goldens (make_golden.hexplane_edge_case;
+    hexplane.py:84-110, 186; SURVEY Appendix A #11/#13)."""
+    g = load_golden("hexplane_" + case)
+    cloud, field, net = build_parts(g)
+    t = float(g["t"])
+    snap, cache = fs().deform_with_cache(cloud, field, net, t)
+    assert cache["device"] is not None and cache["device"].nbytes > 0  # the cached tensor-core backward
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        close(getattr(snap, f), g[f"snap_{f}"], f)
+    gr = type("G", (), {f: g[f"up_{f}"] for f in ("positions", "rotations", "log_scales", "opacity_logits",
+                                                 "features")})()
+    cg, ng, pg = fs().deform_backward(cloud, field, net, cache, gr)
+    close(cg["positions"], g["cg_positions"], "cloud positions", rel=True)
+    outside = ~g["inside"]
+    # rows with every axis clamped get exactly the upstream position gradient
+    allout = outside.all(axis=1)
+    assert allout.any()
+    np.testing.assert_array_equal(cg["positions"][allout], np.asarray(g["up_positions"], np.float32)[allout])
+    for key in g:
+        if key.startswith("g:"):
+            close(ng[key[2:]], g[key], key, rel=True)
+    for l, level in enumerate(pg):
+        for p, arr in enumerate(level):
+            close(arr, g[f"gplane_{l}_{p}"], f"plane {l}/{p}", rel=True)
+
+
+@pytest.mark.parametrize("t", [0.0, 1.0])
+def test_config1_shapes_outside_aabb_and_time_ends_vs_oracle(t):
+    """configs[1] plane / MLP shapes with a shrunken aabb (about a third of the
+    Gaussians clamped on some axis) at t = 0 and t = 1: forward and backward
+    against the oracle, ambiguous ReLU gates excluded as above."""
+    cloud, field, net = config1_parts(k=20000, seed=11)
+    lo, hi = field.aabb
+    field.aabb = np.stack([lo + 0.12 * (hi - lo), hi - 0.12 * (hi - lo)])
+    _, inside = O.field_coords(field.aabb, cloud.positions, t)
+    assert 0.2 < (~inside).any(axis=1).mean() < 0.8
+    snap, cache = fs().deform_with_cache(cloud, field, net, t)
+    osnap, ocache = O.deform(cloud, field.planes, field.aabb, oracle_net(net), t)
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        close(getattr(snap, f), osnap[f], f)
+    ups, n_amb = gated_upstream(cloud, net, ocache, seed=12)
+    assert n_amb < 0.03 * len(cloud), n_amb
+    cg, ng, pg = fs().deform_backward(cloud, field, net, cache, type("G", (), ups)())
+    ocg, ong, opg = O.deform_backward(cloud, field.planes, field.aabb, oracle_net(net), ocache, ups)
+    close(cg["positions"], ocg["positions"], "positions", rel=True)
+    for k in ong:
+        close(ng[k], ong[k], k, rel=True)
+    for l in range(2):
+        for p in range(6):
+            close(pg[l][p], opg[l][p], f"plane {l}/{p}", rel=True)

@@ -1,0 +1,612 @@
+"""The reference's own test assertions, replayed through this package's
+drop-in API (the rebinding of INTEGRATION.md §2: every function below is the
+one a featsplat caller gets after the swap).
+
+Each test names the reference test it replays (/root/reference/pkg/tests/...,
+file:line).  The assertions are the reference's; tolerances are rescaled from
+float64 to the device's fp32 (1e-12 -> 1e-6 absolute / 1e-5 relative), and the
+finite-difference checks use fp32-sized steps (central differences with
+eps ~1e-3 and a 2% relative bound instead of eps 1e-6 and 0.1%).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import has_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+
+
+@pytest.fixture
+def fs():
+    import paper_2503_06161_b200 as m
+    return m
+
+
+AABB = np.array([[-1.0, -1.0, -1.0], [1.0, 1.0, 1.0]])
+
+
+def central_difference(f, arr, idx, eps=1e-3):
+    flat = arr.reshape(-1)
+    out = np.empty(len(idx))
+    for n, i in enumerate(idx):
+        old = flat[i]
+        flat[i] = old + eps
+        fp = f()
+        flat[i] = old - eps
+        fm = f()
+        flat[i] = old
+        out[n] = (fp - fm) / (2 * eps)
+    return out
+
+
+def fd_close(analytic, fd, rtol=2e-2, scale=None):
+    """|analytic - fd| <= rtol * max(|fd|, 0.05 * scale) element-wise, scale =
+    the largest |gradient| of the set (fp32 FD noise floor)."""
+    analytic, fd = np.asarray(analytic).reshape(-1), np.asarray(fd).reshape(-1)
+    scale = np.abs(fd).max(initial=0.0) if scale is None else scale
+    bound = rtol * np.maximum(np.abs(fd), 0.05 * scale) + 1e-7
+    return np.abs(analytic - fd) <= bound
+
+
+def random_cloud(fs, rng, k=20, n_feat=4, opacity_range=(0.1, 0.9), depth_range=(2.2, 3.8)):
+    """test conftest.py:26-37 shapes / distributions."""
+    return fs.GaussianCloud(
+        positions=np.column_stack([rng.uniform(-0.9, 0.9, k), rng.uniform(-0.9, 0.9, k),
+                                   rng.uniform(*depth_range, k)]),
+        rotations=rng.normal(size=(k, 4)), log_scales=np.log(rng.uniform(0.08, 0.35, size=(k, 3))),
+        opacity_logits=np.asarray(fs.logit(rng.uniform(*opacity_range, k))),
+        colors_raw=rng.uniform(0.1, 0.9, size=(k, 3)), features=rng.normal(size=(k, n_feat)))
+
+
+def simple_frame(fs, size=32, focal=None, time=0.0):
+    focal = focal if focal is not None else 1.1 * size
+    return fs.CameraFrame(K=np.array([[focal, 0, (size - 1) / 2], [0, focal, (size - 1) / 2], [0, 0, 1.0]]),
+                          T=np.eye(4), time=time, image=np.zeros((size, size, 3)), depth=np.zeros((size, size)),
+                          mask=np.ones((size, size), dtype=bool))
+
+
+def lone(fs, position, opacity, color, scale=0.5, feature=None):
+    feature = np.zeros(2) if feature is None else feature
+    return fs.GaussianCloud(positions=np.asarray([position], float), rotations=np.array([[1.0, 0, 0, 0]]),
+                            log_scales=np.log(np.full((1, 3), scale)),
+                            opacity_logits=np.asarray([float(fs.logit(opacity))]),
+                            colors_raw=np.asarray([color], float), features=np.asarray([feature], float))
+
+
+def stack(fs, *clouds):
+    return fs.GaussianCloud(*(np.concatenate([getattr(c, f) for c in clouds]) for f in
+                              ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features")))
+
+
+# ---------------------------------------------------------------------------
+# hexplane (test_hexplane.py:29-154)
+# ---------------------------------------------------------------------------
+def small_field(fs, rng, levels=(1, 2), base=(5, 6, 7, 4), out_dim=8, init=None):
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=levels, base_resolution=base, out_dim=out_dim), AABB, rng)
+    if init == "normal":
+        for level in field.planes:
+            for pi in range(len(level)):
+                level[pi] = rng.normal(size=level[pi].shape)
+    return field
+
+
+def test_hex_plane_shapes(fs, rng):  # test_hexplane.py:29-35
+    field = small_field(fs, rng, levels=(1, 3))
+    for mult, level in zip((1, 3), field.planes):
+        for plane, axes in zip(level, fs.PLANE_AXES):
+            assert plane.shape[:2] == tuple((4 if a == 3 else mult * (5, 6, 7)[a]) for a in axes)
+            assert plane.shape[2] == field.channels
+
+
+def test_hex_constant_ones_and_zero_plane(fs, rng):  # test_hexplane.py:38-54
+    field = small_field(fs, rng)
+    for level in field.planes:
+        for plane in level:
+            plane[:] = 1.0
+    f = fs.query(field, np.array([[0.1, -0.4, 0.7]]), 0.3)
+    np.testing.assert_allclose(f, np.ones((1, field.latent_dim)), atol=1e-6)
+    field = small_field(fs, rng, init="normal")
+    field.planes[1][2][:] = 0.0
+    f = fs.query(field, np.array([[0.2, 0.1, -0.3]]), 0.6)
+    c = field.channels
+    assert np.all(f[:, c:] == 0.0) and np.any(f[:, :c] != 0.0)
+
+
+def test_hex_query_at_cell_corner(fs, rng):  # test_hexplane.py:57-71
+    field = small_field(fs, rng, levels=(1,), base=(5, 5, 5, 4), out_dim=4, init="normal")
+    pos = AABB[0] + np.array([1 / 4, 2 / 4, 3 / 4]) * (AABB[1] - AABB[0])
+    f = fs.query(field, pos[None], 1.0 / 3.0)[0]
+    idx4 = {0: 1, 1: 2, 2: 3, 3: 1}
+    expect = np.ones(field.channels)
+    for plane, axes in zip(field.planes[0], fs.PLANE_AXES):
+        expect = expect * plane[idx4[axes[0]], idx4[axes[1]]]
+    np.testing.assert_allclose(f, expect, rtol=1e-5, atol=1e-6)
+
+
+def test_hex_query_deterministic_and_continuous(fs, rng):  # test_hexplane.py:74-84
+    field = small_field(fs, rng, init="normal")
+    pos = rng.uniform(-0.9, 0.9, size=(20, 3))
+    f1 = fs.query(field, pos, 0.4)
+    assert np.array_equal(f1, fs.query(field, pos, 0.4))
+    eps = 1e-3
+    for _ in range(10):
+        d = rng.normal(size=(20, 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        assert np.abs(fs.query(field, pos + eps * d, 0.4) - f1).max() < 100 * eps
+
+
+def test_hex_constant_grid_zero_position_gradient(fs, rng):  # test_hexplane.py:87-95
+    field = small_field(fs, rng)
+    for level in field.planes:
+        for plane in level:
+            plane[:] = 2.5
+    f, cache = fs.query_with_cache(field, np.array([[0.3, -0.2, 0.1]]), 0.5)
+    _, dpos = fs.query_backward(field, cache, np.ones_like(f))
+    np.testing.assert_allclose(dpos, 0.0, atol=1e-4)  # |f| = 2.5^6: fp32 cancellation noise
+
+
+def test_hex_single_plane_hand_product_rule(fs):  # test_hexplane.py:98-130
+    cfg = fs.HexPlaneConfig(levels=(1,), base_resolution=(3, 3, 3, 3), feat_dim=1, out_dim=0)
+    field = fs.HexPlaneField(cfg, AABB, np.random.default_rng(5))
+    for level in field.planes:
+        for pi in range(len(level)):
+            level[pi] = np.random.default_rng(10 + pi).uniform(0.5, 1.5, level[pi].shape)
+    pos, t = np.array([[0.37, -0.21, 0.55]]), 0.42
+    f, cache = fs.query_with_cache(field, pos, t)
+    plane_grads, _ = fs.query_backward(field, cache, np.array([[2.0]]))
+    coords, inside = field.normalized_coords(pos, t)
+    assert inside.all() and coords[0, 3] == t
+    vals = []
+    for plane, axes in zip(field.planes[0], fs.PLANE_AXES):
+        ra, rb = plane.shape[:2]
+        u, v = coords[0, axes[0]] * (ra - 1), coords[0, axes[1]] * (rb - 1)
+        i0, j0 = int(u), int(v)
+        fa, fb = u - i0, v - j0
+        vals.append(((1 - fa) * (1 - fb) * plane[i0, j0, 0] + fa * (1 - fb) * plane[i0 + 1, j0, 0]
+                     + (1 - fa) * fb * plane[i0, j0 + 1, 0] + fa * fb * plane[i0 + 1, j0 + 1, 0], (i0, j0, fa, fb)))
+    others = np.prod([v for i, (v, _) in enumerate(vals) if i != 0])
+    i0, j0, fa, fb = vals[0][1]
+    g = plane_grads[0][0]
+    for (di, dj), wgt in (((0, 0), (1 - fa) * (1 - fb)), ((1, 0), fa * (1 - fb)), ((0, 1), (1 - fa) * fb),
+                          ((1, 1), fa * fb)):
+        assert g[i0 + di, j0 + dj, 0] == pytest.approx(2.0 * others * wgt, rel=1e-5)
+
+
+def test_hex_query_backward_finite_differences(fs, rng):  # test_hexplane.py:133-154
+    field = small_field(fs, rng, init="normal")
+    pos = rng.uniform(-0.8, 0.8, size=(4, 3))
+    t = 0.43
+    up = rng.normal(size=(4, field.latent_dim))
+
+    def loss():
+        return float(np.sum(up * fs.query(field, pos, t)))
+
+    f, cache = fs.query_with_cache(field, pos, t)
+    plane_grads, dpos = fs.query_backward(field, cache, up)
+    ok = fd_close(dpos, central_difference(loss, pos, np.arange(pos.size)))
+    assert ok.all()
+    for li in range(2):
+        for pi in range(6):
+            arr = field.planes[li][pi]
+            idx = np.random.default_rng(li * 6 + pi).choice(arr.size, size=min(20, arr.size), replace=False)
+            assert fd_close(plane_grads[li][pi].reshape(-1)[idx], central_difference(loss, arr, idx),
+                            scale=np.abs(plane_grads[li][pi]).max()).all(), (li, pi)
+
+
+def test_hex_query_shape_contract(fs, rng):  # hexplane.py:151-155
+    field = small_field(fs, rng)
+    f, cache = fs.query_with_cache(field, rng.uniform(-0.5, 0.5, size=(3, 3)), 0.2)
+    with pytest.raises(fs.ContractViolation):
+        fs.query_backward(field, cache, np.zeros((2, field.latent_dim)))
+
+
+def test_tv_regulariser(fs, rng):  # test_hexplane.py:159-197
+    field = small_field(fs, rng)
+    for level in field.planes:
+        for plane in level:
+            plane[:] = 3.7
+    assert fs.tv_loss(field) == 0.0
+    cfg = fs.HexPlaneConfig(levels=(1,), base_resolution=(2, 2, 2, 2), feat_dim=1, out_dim=0)
+    f2 = fs.HexPlaneField(cfg, AABB, rng)
+    for pi in range(6):
+        f2.planes[0][pi] = np.zeros((2, 2, 1))
+    f2.planes[0][0] = np.array([[0.0, 1.0], [0.0, 1.0]])[:, :, None]
+    assert fs.tv_loss(f2) == pytest.approx(2.0 / 4.0, rel=1e-6)
+    assert fs.tv_loss(small_field(fs, rng, init="normal")) >= 0.0
+    f3 = small_field(fs, rng, levels=(1,), base=(3, 4, 3, 3), out_dim=4, init="normal")
+    grads = fs.tv_backward(f3, scale=1.0)
+    for pi in range(6):
+        arr = f3.planes[0][pi]
+        assert fd_close(grads[0][pi], central_difference(lambda: fs.tv_loss(f3), arr, np.arange(arr.size)),
+                        scale=np.abs(grads[0][pi]).max()).all()
+
+
+# ---------------------------------------------------------------------------
+# numerics (test_numerics.py:18-98)
+# ---------------------------------------------------------------------------
+def test_mlp_forward_closed_forms_and_contracts(fs, rng):  # test_numerics.py:18-51
+    from paper_2503_06161_b200.numerics import LinearLayer
+    from oracle import fs4d_oracle as O
+    y, _ = fs.mlp_forward([LinearLayer(np.eye(2), np.zeros(2), "none")], np.array([1.0, 2.0]))
+    np.testing.assert_array_equal(y, [1.0, 2.0])
+    y, _ = fs.mlp_forward([LinearLayer(np.zeros((2, 3)), np.array([3.0, 3.0]), "none")], np.array([5.0, -1.0, 0.5]))
+    np.testing.assert_array_equal(y, [3.0, 3.0])
+    layers = [fs.linear_layer(5, 7, "relu", rng), fs.linear_layer(7, 3, "none", rng)]
+    for layer in layers:
+        layer.bias = rng.normal(size=layer.bias.shape)
+    x = rng.normal(size=(6, 5))
+    y, _ = fs.mlp_forward(layers, x)
+    ref, _ = O.dense_stack([(l.weight, l.bias, l.activation == "relu") for l in layers], x)
+    np.testing.assert_allclose(y, ref, rtol=1e-5, atol=1e-6)
+    y2, _ = fs.mlp_forward(layers, x)
+    assert np.array_equal(y, y2)
+    with pytest.raises(fs.ConfigurationError):
+        fs.mlp_forward([LinearLayer(np.eye(2), np.zeros(2), "none")], np.zeros(3))
+
+
+def test_mlp_backward(fs, rng):  # test_numerics.py:54-98
+    from paper_2503_06161_b200.numerics import LinearLayer
+    layer = LinearLayer(np.eye(2), np.zeros(2), "none")
+    _, cache = fs.mlp_forward([layer], np.array([0.3, -0.7]))
+    dx, _ = fs.mlp_backward([layer], cache, np.array([1.0, 0.0]))
+    np.testing.assert_array_equal(dx, [1.0, 0.0])
+    layer = LinearLayer(np.eye(2), np.array([0.0, -5.0]), "relu")
+    _, cache = fs.mlp_forward([layer], np.array([1.0, 1.0]))
+    dx, grads = fs.mlp_backward([layer], cache, np.array([1.0, 1.0]))
+    np.testing.assert_array_equal(dx, [1.0, 0.0])
+    np.testing.assert_array_equal(grads[0][1], [1.0, 0.0])
+    layers = [fs.linear_layer(4, 6, "relu", rng), fs.linear_layer(6, 2, "none", rng)]
+    for layer in layers:
+        layer.bias = rng.normal(size=layer.bias.shape) * 0.5
+    x = rng.normal(size=(5, 4))
+    up = rng.normal(size=(5, 2))
+
+    def loss():
+        y, _ = fs.mlp_forward(layers, x)
+        return float(np.sum(up * y))
+
+    _, cache = fs.mlp_forward(layers, x)
+    dx, grads = fs.mlp_backward(layers, cache, up)
+    for arr, analytic in [(x, dx), (layers[0].weight, grads[0][0]), (layers[0].bias, grads[0][1]),
+                          (layers[1].weight, grads[1][0]), (layers[1].bias, grads[1][1])]:
+        assert fd_close(analytic, central_difference(loss, arr, np.arange(arr.size)),
+                        scale=np.abs(analytic).max()).all()
+    layers = [fs.linear_layer(4, 4, "relu", rng)]
+    _, cache = fs.mlp_forward(layers, np.zeros((2, 4)))
+    with pytest.raises(fs.ContractViolation):
+        fs.mlp_backward(layers + layers, cache, np.zeros((2, 4)))
+    with pytest.raises(fs.ContractViolation):
+        fs.mlp_backward(layers, cache, np.zeros((3, 4)))
+
+
+def test_mlp_large_batch_matches_oracle_and_is_deterministic(fs, rng):
+    """A 10k-row batch (several weight-gradient chunks): forward and backward
+    against the oracle's dense stack, bit-identical when repeated."""
+    from oracle import fs4d_oracle as O
+    layers = [fs.linear_layer(64, 64, "relu", rng), fs.linear_layer(64, 32, "relu", rng),
+              fs.linear_layer(32, 3, "none", rng)]
+    for layer in layers:
+        layer.weight = layer.weight.astype(np.float32).astype(np.float64)
+    x = rng.normal(size=(10000, 64)).astype(np.float32).astype(np.float64)
+    up = rng.normal(size=(10000, 3)).astype(np.float32).astype(np.float64)
+    y, cache = fs.mlp_forward(layers, x)
+    onet = [(l.weight, l.bias, l.activation == "relu") for l in layers]
+    ref, rec = O.dense_stack(onet, x)
+    np.testing.assert_allclose(y, ref, atol=1e-4 * np.abs(ref).max())
+    dx, grads = fs.mlp_backward(layers, cache, up)
+    odx, og = O.dense_stack_backward(onet, rec, up)
+    assert np.abs(dx - odx).max() < 1e-4 * np.abs(odx).max()
+    for (dw, db), (rw, rb) in zip(grads, og):
+        assert np.abs(dw - rw).max() < 1e-4 * np.abs(rw).max()
+        assert np.abs(db - rb).max() < 1e-4 * np.abs(rb).max()
+    dx2, grads2 = fs.mlp_backward(layers, cache, up)
+    assert np.array_equal(dx, dx2) and all(np.array_equal(a[0], b[0]) for a, b in zip(grads, grads2))
+
+
+# ---------------------------------------------------------------------------
+# rasterizer (test_rasterizer.py:39-283)
+# ---------------------------------------------------------------------------
+def test_projection_closed_forms(fs):  # test_rasterizer.py:39-78
+    f, d, s = 40.0, 4.0, 0.5
+    cfg = fs.RasterConfig()
+    proj = fs.project(lone(fs, [0.0, 0.0, d], 0.5, [0.5] * 3, scale=s), simple_frame(fs, 32, focal=f), cfg)
+    assert len(proj) == 1
+    np.testing.assert_allclose(proj.cov2d[0], (f * s / d) ** 2 * np.eye(2) + cfg.lowpass * np.eye(2), rtol=1e-6)
+    np.testing.assert_allclose(proj.mean2d[0], [15.5, 15.5], atol=1e-5)
+    assert proj.view_depth[0] == pytest.approx(d) and proj.radius[0] >= 1
+    assert len(fs.project(lone(fs, [0.0, 0.0, -2.0], 0.5, [0.5] * 3), simple_frame(fs, 16), cfg)) == 0
+    fr = simple_frame(fs, 64, focal=50.0)
+    near = fs.project(lone(fs, [0, 0, 2.0], 0.5, [0.5] * 3), fr, cfg)
+    far = fs.project(lone(fs, [0, 0, 4.0], 0.5, [0.5] * 3), fr, cfg)
+    assert (near.cov2d[0, 0, 0] - cfg.lowpass) / (far.cov2d[0, 0, 0] - cfg.lowpass) == pytest.approx(4.0, rel=1e-5)
+    cloud = stack(fs, lone(fs, [0.3, 0, 3.0], 0.4, [0.9, 0.1, 0.1]), lone(fs, [-0.3, 0, 3.0], 0.4, [0.1, 0.9, 0.1]),
+                  lone(fs, [0.0, 0, 2.0], 0.4, [0.1, 0.1, 0.9]))
+    assert fs.project(cloud, simple_frame(fs, 32), cfg).source_index.tolist() == [2, 0, 1]
+    bad = lone(fs, [0, 0, 3.0], 0.5, [0.5] * 3)
+    bad.positions[0, 1] = np.nan
+    with pytest.raises(fs.NumericalError, match="0"):
+        fs.project(bad, simple_frame(fs, 16), cfg)
+
+
+def test_binning(fs, rng):  # test_rasterizer.py:83-117
+    fr = simple_frame(fs, 64)
+    proj = fs.project(lone(fs, [-0.35, -0.35, 3.0], 0.5, [0.5] * 3, scale=0.08), fr, fs.RasterConfig())
+    tiles = fs.bin_tiles(proj, 64, 64, 16)
+    hit = [(ty, tx) for ty, row in enumerate(tiles) for tx, cell in enumerate(row) if cell.size]
+    assert 1 <= len(hit) <= 4
+    u, v = proj.mean2d[0]
+    assert (int(v) // 16, int(u) // 16) in hit
+    proj = fs.project(lone(fs, [0, 0, 2.5], 0.5, [0.5] * 3, scale=3.0), fr, fs.RasterConfig())
+    assert all(cell.size == 1 for row in fs.bin_tiles(proj, 64, 64, 16) for cell in row)
+    proj = fs.project(random_cloud(fs, rng, k=60), simple_frame(fs, 48), fs.RasterConfig())
+    union = set()
+    for row in fs.bin_tiles(proj, 48, 48, 16):
+        for cell in row:
+            assert len(set(cell.tolist())) == cell.size
+            union.update(cell.tolist())
+    assert union == set(range(len(proj)))
+
+
+def test_closed_form_blends_and_pixel_record(fs):  # test_rasterizer.py:122-163
+    fr = simple_frame(fs, 17)
+    out = fs.render(lone(fs, [0, 0, 3.0], 0.6, [1.0, 0, 0], scale=0.8), fr, fs.RasterConfig(with_features=False))
+    np.testing.assert_allclose(out.color[8, 8], [0.6, 0, 0], atol=1e-6)
+    assert out.alpha[8, 8] == pytest.approx(0.6, abs=1e-6) and out.depth[8, 8] == pytest.approx(1.8, abs=1e-5)
+    c1, c2 = np.array([1.0, 0, 0]), np.array([0, 1.0, 0])
+    out2 = fs.render(stack(fs, lone(fs, [0, 0, 2.0], 0.5, c1, 0.8), lone(fs, [0, 0, 4.0], 0.5, c2, 1.6)), fr,
+                     fs.RasterConfig(with_features=False))
+    np.testing.assert_allclose(out2.color[8, 8], 0.5 * c1 + 0.25 * c2, atol=1e-6)
+    assert out2.alpha[8, 8] == pytest.approx(0.75, abs=1e-6)
+    bg = np.array([0.2, 0.4, 0.6])
+    out3 = fs.render(lone(fs, [0, 0, 3.0], 0.6, [1.0, 0, 0], scale=0.8), fr,
+                     fs.RasterConfig(background=bg, with_features=False))
+    np.testing.assert_allclose(out3.color[8, 8], [0.6, 0, 0] + 0.4 * bg, atol=1e-6)
+    a = out3.alpha[0, 0]
+    np.testing.assert_allclose(out3.color[0, 0], a * np.array([1.0, 0, 0]) + (1 - a) * bg, atol=1e-6)
+    src, alphas, weights = out.pixel_record(8, 8)
+    assert src.tolist() == [0]
+    assert alphas[0] == pytest.approx(0.6, abs=1e-6) and weights[0] == pytest.approx(0.6, abs=1e-6)
+
+
+@pytest.mark.parametrize("seed,k,size,nf", [(0, 50, 32, 4), (1, 200, 64, 16), (2, 120, 48, 4), (3, 30, 33, 16)])
+def test_pixel_records_agree_with_contributor_counts(fs, seed, k, size, nf):
+    """test_rasterizer.py:168-183's scenes: every pixel's record (device
+    replay) has exactly n_contrib entries and its weights sum to the pixel's
+    alpha (conservation, rasterizer.py:244-261)."""
+    rng = np.random.default_rng(seed)
+    out = fs.render(random_cloud(fs, rng, k=k, n_feat=nf, opacity_range=(0.05, 0.98)), simple_frame(fs, size),
+                    fs.RasterConfig(background=np.array([0.1, 0.2, 0.3])))
+    for r in range(0, size, 3):
+        for c in range(0, size, 3):
+            src, al, w = out.pixel_record(r, c)
+            assert src.size == out.n_contrib[r, c]
+            assert abs(w.sum() - out.alpha[r, c]) < 1e-5
+
+
+def test_weight_conservation_inside_tiled_path(fs, rng):  # test_rasterizer.py:186-194
+    from paper_2503_06161_b200.rasterizer import _composite_weights, _tile_alphas
+    cfg = fs.RasterConfig()
+    out = fs.render(random_cloud(fs, rng, k=80, opacity_range=(0.1, 0.97)), simple_frame(fs, 32), cfg)
+    assert out.record.tiles, "expected populated tiles"
+    t_final_img = np.ones((32, 32))
+    for tr in out.record.tiles:
+        _, contrib, w, t_final = _composite_weights(tr.alpha, cfg.stop_transmittance)
+        np.testing.assert_allclose(w.sum(axis=0) + t_final, 1.0, atol=2e-6)
+        t_final_img[tr.y0:tr.y0 + tr.ys.size, tr.x0:tr.x0 + tr.xs.size] = t_final.reshape(tr.ys.size, tr.xs.size)
+        rows, alpha, _, _ = _tile_alphas(out.record.proj, tr.rows, tr.xs, tr.ys, cfg)
+        assert np.array_equal(rows, tr.rows) and np.array_equal(alpha, tr.alpha)
+    # the replayed transmittance is the blend kernel's, bit for bit
+    np.testing.assert_array_equal(1.0 - t_final_img, out.alpha)
+
+
+def test_render_invariants(fs, rng):  # test_rasterizer.py:199-228
+    z = np.array([0.7, -1.3, 2.0])
+    parts = [lone(fs, [0, 0, 2.0 + 0.2 * i], 0.985, [0.5] * 3, scale=1.2, feature=z) for i in range(4)]
+    out = fs.render(stack(fs, *parts), simple_frame(fs, 17), fs.RasterConfig())
+    assert out.record.proj.opacity.max() > 0.98
+    assert 1 - out.alpha[8, 8] < 1e-4
+    np.testing.assert_allclose(out.feature[8, 8], z, atol=1e-3)
+    near = lone(fs, [0, 0, 2.0], 0.999, [0.9, 0.1, 0.1], scale=1.0)
+    far = lone(fs, [0, 0, 5.0], 0.999, [0.1, 0.9, 0.1], scale=2.5)
+    out = fs.render(stack(fs, near, far), simple_frame(fs, 17), fs.RasterConfig(with_features=False))
+    assert abs(out.depth[8, 8] - 2.0) < 0.05
+    cloud = random_cloud(fs, rng, k=40)
+    a = fs.render(cloud, simple_frame(fs, 32), fs.RasterConfig())
+    b = fs.render(cloud, simple_frame(fs, 32), fs.RasterConfig())
+    for f in ("color", "depth", "feature", "alpha"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))
+
+
+def test_backward_closed_forms(fs, rng):  # test_rasterizer.py:233-256
+    cloud = random_cloud(fs, rng, k=10)
+    fr = simple_frame(fs, 24)
+    out = fs.render(cloud, fr, fs.RasterConfig())
+    g = fs.render_backward(cloud, fr, out)
+    for name in ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features"):
+        np.testing.assert_array_equal(getattr(g, name), 0.0)
+    fr = simple_frame(fs, 17)
+    cloud = lone(fs, [0.021, -0.013, 3.0], 0.47, [0.8, 0.3, 0.6], scale=0.7)
+    cfg = fs.RasterConfig(with_features=False)
+    out = fs.render(cloud, fr, cfg)
+    dC = np.zeros((17, 17, 3))
+    dC[8, 8, 0] = 1.0
+    g = fs.render_backward(cloud, fr, out, dC)
+    proj = fs.project(cloud, fr, cfg)
+    d = np.array([8.0, 8.0]) - proj.mean2d[0]
+    g2d = np.exp(-0.5 * (d @ proj.conic[0] @ d))
+    o = fs.sigmoid(cloud.opacity_logits)[0]
+    assert g.opacity_logits[0] == pytest.approx(cloud.colors_raw[0, 0] * o * (1 - o) * g2d, rel=1e-5)
+
+
+def test_full_scene_finite_difference_gradients(fs, rng):  # test_rasterizer.py:259-283
+    cloud = random_cloud(fs, rng, k=5, n_feat=3, opacity_range=(0.15, 0.3))
+    fr = simple_frame(fs, 24)
+    cfg = fs.RasterConfig()
+    up = {"c": rng.normal(size=(24, 24, 3)), "d": rng.normal(size=(24, 24)), "f": rng.normal(size=(24, 24, 3)),
+          "a": rng.normal(size=(24, 24))}
+
+    def loss():
+        o = fs.render(cloud, fr, cfg)
+        return float(np.sum(up["c"] * o.color) + np.sum(up["d"] * o.depth) + np.sum(up["f"] * o.feature)
+                     + np.sum(up["a"] * o.alpha))
+
+    out = fs.render(cloud, fr, cfg)
+    g = fs.render_backward(cloud, fr, out, up["c"], up["d"], up["f"], up["a"])
+    for name in ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features"):
+        arr = getattr(cloud, name)
+        analytic = getattr(g, name)
+        fd = central_difference(loss, arr, np.arange(arr.size), eps=1e-3)
+        assert fd_close(analytic, fd, rtol=5e-2, scale=np.abs(analytic).max()).mean() >= 0.9, name
+
+
+# ---------------------------------------------------------------------------
+# deformation (test_deformation.py:42-223)
+# ---------------------------------------------------------------------------
+DAABB = np.array([[-1.2, -1.2, 1.8], [1.2, 1.2, 4.2]])
+
+
+def make_parts(fs, rng, k=6, n_feat=5, width=16, depth=3, randomize=True):
+    cloud = random_cloud(fs, rng, k=k, n_feat=n_feat, opacity_range=(0.15, 0.3))
+    field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(4, 4, 4, 3), out_dim=8), DAABB, rng)
+    net = fs.DeformationNet(field.latent_dim, fs.DeformationConfig(width=width, depth=depth, feature_dim=n_feat), rng)
+    if randomize:
+        for level in field.planes:
+            for pi in range(len(level)):
+                level[pi] = 0.8 + rng.normal(size=level[pi].shape) * 0.3
+        for _, st in net.stacks():
+            for layer in st:
+                layer.weight = rng.normal(size=layer.weight.shape) * 0.2
+                layer.bias = rng.normal(size=layer.bias.shape) * 0.2
+    return cloud, field, net
+
+
+def test_deformation_stacks(fs, rng):  # test_deformation.py:42-106
+    from oracle import fs4d_oracle as O
+    net = fs.DeformationNet(64, fs.DeformationConfig(), rng)
+    assert net.trunk[0].in_dim == 64 and net.trunk[-1].out_dim == 64 and len(net.trunk) == 8
+    h = fs.decode_hidden(net, np.zeros((3, 64)))
+    assert h.shape == (3, 64)
+    deltas, feats = fs.decode_branches(net, h)
+    assert {k: v.shape[1] for k, v in deltas.items()} == {"position": 3, "rotation": 4, "scale": 3, "opacity": 1}
+    assert all(f.shape[1] == 32 for f in feats.values())
+    assert net.feature_mlp[0].in_dim == 128 and net.feature_mlp[1].out_dim == 128
+    net = fs.DeformationNet(8, fs.DeformationConfig(width=8, depth=2, feature_dim=4), rng)
+    for layer in net.trunk:
+        layer.weight[:] = 0.0
+        layer.bias[:] = 0.3
+    h = fs.decode_hidden(net, rng.normal(size=(5, 8)))
+    np.testing.assert_allclose(h, 0.3, atol=1e-7)
+    net = fs.DeformationNet(6, fs.DeformationConfig(width=8, depth=3, feature_dim=4), rng)
+    for layer in net.trunk:
+        layer.bias = rng.normal(size=layer.bias.shape) * 0.2
+    x = rng.normal(size=(4, 6))
+    ref, _ = O.dense_stack([(l.weight, l.bias, True) for l in net.trunk], x)
+    np.testing.assert_allclose(fs.decode_hidden(net, x), ref, rtol=1e-5, atol=1e-6)
+    net = fs.DeformationNet(8, fs.DeformationConfig(width=8, depth=2, feature_dim=4), rng)
+    deltas, _ = fs.decode_branches(net, rng.normal(size=(5, 8)))
+    for d in deltas.values():
+        np.testing.assert_array_equal(d, 0.0)
+    feats = {n: rng.normal(size=(5, 4)) for n in fs.BRANCHES}
+    z = rng.normal(size=(5, 4))
+    np.testing.assert_array_equal(fs.update_semantics(net, feats, z), z)
+    net.cfg.enable_feature_update = False
+    assert fs.update_semantics(net, feats, z) is z
+    net.cfg.enable_feature_update = True
+    net.feature_mlp[1].weight = rng.normal(size=net.feature_mlp[1].weight.shape)
+    feats = {n: rng.normal(size=(2, 4)) for n in fs.BRANCHES}
+    z = np.zeros((2, 4))
+    swapped = dict(feats)
+    swapped["position"], swapped["opacity"] = feats["opacity"], feats["position"]
+    assert not np.allclose(fs.update_semantics(net, feats, z), fs.update_semantics(net, swapped, z))
+
+
+def test_deform_identities(fs, rng):  # test_deformation.py:109-145, 218-223
+    cloud, field, net = make_parts(fs, rng, randomize=False)
+    snap = fs.deform(cloud, field, net, 0.5)
+    np.testing.assert_allclose(snap.positions, cloud.positions, atol=1e-6)
+    np.testing.assert_allclose(snap.opacities(), cloud.opacities(), atol=1e-6)
+    np.testing.assert_allclose(snap.features, cloud.features, atol=1e-6)
+    cloud, field, net = make_parts(fs, rng)
+    net.cfg.enable_grid = False
+    snap, cache = fs.deform_with_cache(cloud, field, net, 0.5)
+    assert cache["query"] is None
+    d = snap.positions - cloud.positions
+    assert np.allclose(d, d[0], atol=1e-6)
+    net.cfg.enable_grid = True
+    net.cfg.enable_feature_update = False
+    for t in (0.0, 0.33, 1.0):
+        assert fs.deform(cloud, field, net, t).features is cloud.features
+    cloud, field, net = make_parts(fs, rng, k=1, width=4, depth=1, randomize=False)
+    for level in field.planes:
+        for plane in level:
+            plane[:] = 1.0
+    net.trunk[0].weight = rng.normal(size=net.trunk[0].weight.shape)
+    net.trunk[0].bias = np.abs(rng.normal(size=4))
+    for name in fs.BRANCHES:
+        for layer in net.extractors[name]:
+            layer.weight[:] = 0.0
+            layer.bias[:] = 0.5
+        net.heads[name][0].weight[:] = 0.25
+    expect = np.full((1, 2), 0.5) @ np.full((3, 2), 0.25).T
+    np.testing.assert_allclose(fs.deform(cloud, field, net, 0.3).positions - cloud.positions, expect, atol=1e-5)
+
+
+def test_deform_backward_finite_differences(fs, rng):  # test_deformation.py:148-187
+    cloud, field, net = make_parts(fs, rng)
+    t = 0.61
+    ups = {n: rng.normal(size=getattr(cloud, n).shape) for n in ("positions", "rotations", "log_scales", "features")}
+    ups["opacity_logits"] = rng.normal(size=len(cloud))
+
+    def loss():
+        s = fs.deform(cloud, field, net, t)
+        return float(sum(np.sum(ups[n] * getattr(s, n)) for n in ups))
+
+    _, cache = fs.deform_with_cache(cloud, field, net, t)
+    cg, ng, pg = fs.deform_backward(cloud, field, net, cache, type("G", (), ups)())
+    for name, analytic in cg.items():
+        arr = getattr(cloud, name)
+        assert fd_close(analytic, central_difference(loss, arr, np.arange(arr.size)),
+                        scale=np.abs(analytic).max()).mean() >= 0.95, name
+    params = net.param_arrays()
+    for name, analytic in ng.items():
+        arr = params[name]
+        idx = np.random.default_rng(abs(hash(name)) % 2 ** 31).choice(arr.size, size=min(arr.size, 25), replace=False)
+        assert fd_close(analytic.reshape(-1)[idx], central_difference(loss, arr, idx),
+                        scale=np.abs(analytic).max()).mean() >= 0.9, name
+    for li, level in enumerate(pg):
+        for pi, g in enumerate(level):
+            arr = field.planes[li][pi]
+            idx = np.random.default_rng(li * 7 + pi).choice(arr.size, size=min(arr.size, 15), replace=False)
+            assert fd_close(g.reshape(-1)[idx], central_difference(loss, arr, idx),
+                            scale=np.abs(g).max()).mean() >= 0.9
+
+
+def test_end_to_end_render_gradient_through_deformation(fs, rng):  # test_deformation.py:190-215
+    cloud, field, net = make_parts(fs, rng, k=5)
+    fr = simple_frame(fs, 16)
+    t = 0.37
+    rcfg = fs.RasterConfig(with_features=True)
+    up_c = rng.normal(size=(16, 16, 3))
+
+    def loss():
+        return float(np.sum(up_c * fs.render(fs.deform(cloud, field, net, t), fr, rcfg).color))
+
+    snap, cache = fs.deform_with_cache(cloud, field, net, t)
+    out = fs.render(snap, fr, rcfg)
+    g = fs.render_backward(snap, fr, out, up_c)
+    _, ng, _ = fs.deform_backward(cloud, field, net, cache, g)
+    params = net.param_arrays()
+    for name, analytic in ng.items():
+        arr = params[name]
+        idx = np.random.default_rng(abs(hash(name)) % 2 ** 31).choice(arr.size, size=min(arr.size, 10), replace=False)
+        assert fd_close(analytic.reshape(-1)[idx], central_difference(loss, arr, idx),
+                        rtol=5e-2, scale=np.abs(analytic).max()).mean() >= 0.8, name

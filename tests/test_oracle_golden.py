@@ -101,3 +101,40 @@ def test_oracle_sh_degree0_reduces_to_reference_colour():
     cfg = O.RasterParams(background=g["background"])
     out = O.render(cloud, g["K"], g["T"], int(g["height"]), int(g["width"]), cfg)
     np.testing.assert_allclose(out["color"], g["color"], atol=1e-12)
+
+
+HEX_EDGE_CASES = ["t0", "t1", "tclip"]
+
+
+@pytest.mark.parametrize("case", HEX_EDGE_CASES)
+def test_oracle_hexplane_edges_match_reference(case):
+    """Outside-aabb / on-face Gaussians and t at (and past) the ends of [0, 1]
+    (hexplane.py:84-110, 145-187; make_golden.hexplane_edge_case)."""
+    g = load_golden("hexplane_" + case)
+    cloud = golden_cloud(g)
+    planes, net = _golden_planes(g), _golden_net(g)
+    t = float(g["t"])
+    coords, inside = O.field_coords(g["aabb"], cloud.positions, t)
+    np.testing.assert_array_equal(coords, g["coords"])
+    np.testing.assert_array_equal(inside, g["inside"])
+    assert (~inside).any(axis=1).sum() >= 20
+    lat = O.hexplane_query(planes, g["aabb"], cloud.positions, t)
+    np.testing.assert_allclose(lat, g["latent"], rtol=1e-12, atol=1e-14)
+    pg, dpos = O.hexplane_backward(planes, g["aabb"], cloud.positions, t, g["d_latent"])
+    np.testing.assert_allclose(dpos, g["query_dpos"], rtol=1e-10, atol=1e-12)
+    assert np.all(dpos[~inside] == 0.0)  # clamped coordinates pass no position gradient
+    for l, level in enumerate(pg):
+        for p, arr in enumerate(level):
+            np.testing.assert_allclose(arr, g[f"qgplane_{l}_{p}"], rtol=1e-10, atol=1e-12)
+    snap, cache = O.deform(cloud, planes, g["aabb"], net, t)
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        np.testing.assert_allclose(snap[f], g[f"snap_{f}"], rtol=1e-12, atol=1e-12, err_msg=f)
+    ups = {f: g[f"up_{f}"] for f in ("positions", "rotations", "log_scales", "opacity_logits", "features")}
+    cg, ng, pg = O.deform_backward(cloud, planes, g["aabb"], net, cache, ups)
+    np.testing.assert_allclose(cg["positions"], g["cg_positions"], rtol=1e-10, atol=1e-10)
+    for key in g:
+        if key.startswith("g:"):
+            np.testing.assert_allclose(ng[key[2:]], g[key], rtol=1e-10, atol=1e-10, err_msg=key)
+    for l, level in enumerate(pg):
+        for p, arr in enumerate(level):
+            np.testing.assert_allclose(arr, g[f"gplane_{l}_{p}"], rtol=1e-10, atol=1e-10)
