@@ -37,11 +37,11 @@ def f32(x):
     return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
 
 
-def make_scene(seed=0):
-    """Seeded configs[1] scene."""
+def make_scene(seed=0, k=K_GAUSS, h=H, w=W, focal=FOCAL, d=D):
+    """Seeded configs[1] scene; the arguments give the other
+    configs the same distributions (configs[0] size: k=10_000, 128x160, f=150)."""
     import paper_2503_06161_b200 as fs
     rng = np.random.default_rng(seed)
-    k = K_GAUSS
     q = rng.normal(size=(k, 4))
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     sh = rng.normal(0.0, 0.2, size=(k, 16, 3))
@@ -49,18 +49,18 @@ def make_scene(seed=0):
         positions=f32(np.column_stack([rng.uniform(-1, 1, k), rng.uniform(-1, 1, k), rng.uniform(3, 6, k)])),
         rotations=f32(q), log_scales=f32(rng.normal(-4.0, 0.5, size=(k, 3))),
         opacity_logits=f32(rng.normal(0.0, 1.0, size=k)),
-        colors_raw=f32(sh[:, 0, :]), features=f32(rng.normal(size=(k, D))), sh_rest=f32(sh[:, 1:, :]))
+        colors_raw=f32(sh[:, 0, :]), features=f32(rng.normal(size=(k, d))), sh_rest=f32(sh[:, 1:, :]))
     field = fs.HexPlaneField(fs.HexPlaneConfig(levels=(1, 2), base_resolution=(64, 64, 64, 25), out_dim=64),
                              fs.scene_aabb(cloud), rng, init="uniform")
     for level in field.planes:
         for i in range(6):
             level[i] = f32(level[i])
-    net = fs.DeformationNet(64, fs.DeformationConfig(width=64, depth=1, feature_dim=D), rng, init="xavier",
+    net = fs.DeformationNet(64, fs.DeformationConfig(width=64, depth=1, feature_dim=d), rng, init="xavier",
                             head_init="xavier")
     for _, st in net.stacks():
         for layer in st:
             layer.weight = f32(layer.weight)
-    Kmat = np.array([[FOCAL, 0, (W - 1) / 2], [0, FOCAL, (H - 1) / 2], [0, 0, 1.0]])
+    Kmat = np.array([[focal, 0, (w - 1) / 2], [0, focal, (h - 1) / 2], [0, 0, 1.0]])
     return cloud, field, net, Kmat
 
 
@@ -275,66 +275,125 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: reference algorithm (oracle port), bounded samples
+# CPU baseline: the unmodified reference (featsplat, pip-installed into
+# baseline/_ref), whole frames
 # ---------------------------------------------------------------------------
-CPU_SLICES = 32  # one sample = 1/32 of the Gaussians deformed + 1 of 32 tile rows composited (+ full projection)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 
-def _cpu_worker(args):
-    seed, band = args
-    import fs4d_cpu_state as S  # populated in the parent before fork
-    from oracle import fs4d_oracle as O
-    cloud, planes, aabb, onet, Kmat = S.scene
-    k = K_GAUSS
-    sl = slice((band % CPU_SLICES) * k // CPU_SLICES, (band % CPU_SLICES + 1) * k // CPU_SLICES)
-    part = type("C", (), {n: getattr(cloud, n)[sl] for n in
-                          ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features")})()
+def load_featsplat():
+    """The reference package itself, or None when baseline/_ref is absent."""
+    if os.path.isdir(REF_PATH) and REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        import featsplat.deformation  # noqa: F401
+        import featsplat.rasterizer  # noqa: F401
+        import featsplat
+        return featsplat
+    except Exception:
+        return None
+
+
+def reference_scene(seed=0, k=K_GAUSS, h=H, w=W, focal=FOCAL, d=D):
+    """make_scene's configs[1] scene as the reference's own objects.  The
+    reference has no SH: its colour is the degree-0 term
+    (colors_raw), which is what it renders."""
+    import featsplat.deformation as RD
+    import featsplat.gaussians as RG
+    import featsplat.hexplane as RH
+    import featsplat.rasterizer as RR
+    cloud, field, net, Kmat = make_scene(seed, k=k, h=h, w=w, focal=focal, d=d)
+    rc = RG.GaussianCloud(**{f: np.array(getattr(cloud, f)) for f in
+                             ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features")})
+    rf = RH.HexPlaneField(RH.HexPlaneConfig(levels=(1, 2), base_resolution=(64, 64, 64, 25), out_dim=64), field.aabb,
+                          np.random.default_rng(1))
+    rf.planes = [[np.array(p) for p in lv] for lv in field.planes]
+    rn = RD.DeformationNet(64, RD.DeformationConfig(width=64, depth=1, feature_dim=d), np.random.default_rng(2))
+    for (_, st), (_, st2) in zip(rn.stacks(), net.stacks()):
+        for layer, src in zip(st, st2):
+            layer.weight, layer.bias = np.array(src.weight), np.array(src.bias)
+    frame = RG.CameraFrame(K=Kmat, T=np.eye(4), time=0.0, image=np.zeros((h, w, 3)), depth=np.zeros((h, w)),
+                           mask=np.ones((h, w), dtype=bool))
+    return rc, rf, rn, frame, RR.RasterConfig()
+
+
+def _ref_init():
+    # one BLAS thread per worker: the workers are the parallelism
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+
+
+def _ref_frame(t):
+    """One whole reference frame in a worker: deformation.deform +
+    rasterizer.render (cli.py:58-61) on the fork-inherited scene."""
+    S = sys.modules["fs4d_ref_state"]
     t0 = time.perf_counter()
-    O.deform(part, planes, aabb, onet, 0.37)
-    t_def = time.perf_counter() - t0
-    nty = -(-H // 16)
-    t0 = time.perf_counter()
-    O.render(cloud, Kmat, np.eye(4), H, W, O.RasterParams(), tile_rows=[band % nty], prepared=S.prepared)
-    t_band = time.perf_counter() - t0
-    # projection + binning of the whole frame is paid once per frame, compositing per tile row
-    return CPU_SLICES * t_def + S.t_project + nty * t_band
+    if S.kind == "reference":
+        import featsplat.deformation as RD
+        import featsplat.rasterizer as RR
+        snap = RD.deform(S.cloud, S.field, S.net, float(t))
+        RR.render(snap, S.frame, S.cfg)
+    else:  # oracle port (baseline/_ref absent)
+        from oracle import fs4d_oracle as O
+        snap, _ = O.deform(S.cloud, S.field.planes, S.field.aabb, S.net, float(t))
+        snap = type("C", (), dict(snap, sh_rest=getattr(S.cloud, "sh_rest", None)))()
+        O.render(snap, S.K, np.eye(4), H, W, O.RasterParams())
+    return time.perf_counter() - t0
 
 
-def cpu_reference(steps, warmup, seed=0, procs=None):
-    """Reference CPU path on bounded samples with all host cores; returns dict."""
+def host_info():
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    avail = None
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    avail = int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    if avail is None:
+        avail = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    return {"cpu_count": os.cpu_count(), "affinity": ncores, "mem_available_gb": round(avail / 2 ** 30, 1)}
+
+
+REF_FRAME_GB = 16.0  # peak RSS of one configs[1] reference frame (SURVEY §8(d): ~15 GB)
+
+
+def cpu_reference(timed_frames, warm_frames, seed=0, procs=None):
+    """Whole configs[1] frames of the reference CPU path, P worker processes
+    (one frame each, one BLAS thread each) over the host cores; returns the
+    aggregate frames/s of the timed frames."""
     import multiprocessing as mp
     import types
-    from oracle import fs4d_oracle as O
-    cloud, field, net, Kmat = make_scene(seed)
-    onet = {p: [(l.weight, l.bias, l.activation == "relu") for l in st] for p, st in net.stacks()}
-    t0 = time.perf_counter()
-    proj = O.project(cloud, Kmat, np.eye(4), H, W, O.RasterParams())
-    lists = O.bin_tiles(proj, H, W, 16)
-    t_proj = time.perf_counter() - t0
-    mod = types.ModuleType("fs4d_cpu_state")
-    mod.scene = (cloud, field.planes, field.aabb, onet, Kmat)
-    mod.t_project = t_proj
-    mod.prepared = (proj, lists)
-    sys.modules["fs4d_cpu_state"] = mod
-    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2 ** 30
-    procs = procs or max(1, min(ncores, int(mem_gb // 4), 32))
+    fsp = load_featsplat()
+    mod = types.ModuleType("fs4d_ref_state")
+    if fsp is not None:
+        mod.kind = "reference"
+        mod.cloud, mod.field, mod.net, mod.frame, mod.cfg = reference_scene(seed)
+    else:
+        mod.kind = "port"
+        cloud, field, net, Kmat = make_scene(seed)
+        mod.cloud, mod.field, mod.K = cloud, field, Kmat
+        mod.net = {p: [(l.weight, l.bias, l.activation == "relu") for l in st] for p, st in net.stacks()}
+    sys.modules["fs4d_ref_state"] = mod
+    info = host_info()
+    cap = max(1, int(info["mem_available_gb"] // REF_FRAME_GB))
+    procs = procs or max(1, min(info["affinity"], cap, max(timed_frames, 1)))
+    ts = np.arange(156) / 155.0
     ctx = mp.get_context("fork")
-    vals = []
-    with ctx.Pool(procs, initializer=lambda: os.environ.update(OMP_NUM_THREADS="1")) as pool:
-        for step in range(warmup + steps):
-            jobs = [(seed, step * procs + j) for j in range(procs)]
-            ts = time.perf_counter()
-            frame_s = pool.map(_cpu_worker, jobs)
-            wall = time.perf_counter() - ts
-            if step >= warmup:
-                vals.append(sum(1.0 / f for f in frame_s))  # aggregate frames/s of P concurrent processes
-    return {"value": float(np.mean(vals)), "cores": procs, "host_cores": ncores,
-            "sample": f"per process per step: deform of 1/{CPU_SLICES} of the 200k Gaussians + "
-                      f"compositing of 1 of {-(-H // 16)} tile rows (+ the frame's fp64 projection+binning, timed once), extrapolated to one frame "
-                      f"(frame_s = {CPU_SLICES}*t_deform_slice + t_project + n_rows*t_band); "
-                      f"value = sum over {procs} concurrent processes of 1/frame_s",
-            "project_s": t_proj, "step_wall_s": wall}
+    with ctx.Pool(procs, initializer=_ref_init) as pool:
+        if warm_frames:
+            pool.map(_ref_frame, [ts[i % 156] for i in range(warm_frames)], chunksize=1)
+        t0 = time.perf_counter()
+        per = pool.map(_ref_frame, [ts[(warm_frames + i) % 156] for i in range(timed_frames)], chunksize=1)
+        wall = time.perf_counter() - t0
+    desc = ("unmodified featsplat 0.1.0 (baseline/_ref): deformation.deform + rasterizer.render, SH degree 0 "
+            "(the reference has no SH)" if mod.kind == "reference" else "oracle/fs4d_oracle.py float64 port")
+    return {"value": timed_frames / wall, "cores": procs, "kind": mod.kind, "host": info,
+            "frame_s_mean": float(np.mean(per)), "frame_s_max": float(np.max(per)), "wall_s": wall,
+            "sample": f"{timed_frames} whole configs[1] frames (t = k/155) of the {desc}, {procs} worker processes "
+                      f"x 1 BLAS thread, value = frames / wall time; mean {np.mean(per):.1f} s per frame per "
+                      f"process"}
 
 
 # ---------------------------------------------------------------------------
@@ -551,7 +610,6 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", default="render", choices=["render", "train", "fine"])
     args = ap.parse_args()
@@ -576,10 +634,10 @@ def main():
         line.update({"impl": "reference", "value": r["value"], "ms_per_step": 1000.0 / r["value"],
                      "n_gpus": world,
                      "cpu_baseline": {"value": r["value"], "unit": "frames/s", "cores": r["cores"],
-                                      "kind": "port", "sample": r["sample"]},
+                                      "kind": r["kind"], "sample": r["sample"]},
+                     "host": r["host"],
                      "e2e": {"value": r["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
                              "d2h_bytes_per_step": 0}})
-        line["config"] = dict(base["config"], cpu_impl="oracle/fs4d_oracle.py (float64 NumPy port of featsplat)")
         print(json.dumps(line))
         return
 
@@ -670,8 +728,9 @@ def main():
         "comm": r["comm"],
     })
     if rank == 0 and world == 1 and not args.no_cpu:
-        c = cpu_reference(args.cpu_steps, 0)
-        line["cpu_baseline"] = {"value": c["value"], "unit": "frames/s", "cores": c["cores"], "kind": "port",
+        # bounded sample: one wave of whole reference frames, one per worker process
+        c = cpu_reference(max(1, min(host_info()["affinity"], int(host_info()["mem_available_gb"] // REF_FRAME_GB))), 0)
+        line["cpu_baseline"] = {"value": c["value"], "unit": "frames/s", "cores": c["cores"], "kind": c["kind"],
                                 "sample": c["sample"]}
     if rank == 0:
         print(json.dumps(line))

@@ -194,10 +194,13 @@ int fs4d_abi_version(void) { return FS4D_ABI_VERSION; }
 
 const char* fs4d_last_error(void) { return g_last_error.c_str(); }
 
+#ifndef FS4D_SOURCE_HASH
+#define FS4D_SOURCE_HASH "unknown"
+#endif
 const char* fs4d_build_info(void) {
   static char buf[256];
-  snprintf(buf, sizeof(buf), "libfs4d abi=%d arch=sm_100a cuda=%d.%d", FS4D_ABI_VERSION, CUDART_VERSION / 1000,
-           (CUDART_VERSION % 1000) / 10);
+  snprintf(buf, sizeof(buf), "libfs4d abi=%d arch=sm_100a cuda=%d.%d src=%s", FS4D_ABI_VERSION, CUDART_VERSION / 1000,
+           (CUDART_VERSION % 1000) / 10, FS4D_SOURCE_HASH);
   return buf;
 }
 

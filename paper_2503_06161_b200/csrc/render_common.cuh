@@ -36,8 +36,13 @@ __device__ __forceinline__ float4 unscaled_conic(const float4& cs) {
 __device__ __forceinline__ float2 tile_rel_mean(const float4& m, float ox, float oy) {
   return make_float2((m.x - ox) + m.z, (m.y - oy) + m.w);
 }
+// explicit rounding: every kernel that evaluates a pair (forward blend,
+// backward replay, tile-alpha replay) gets the same bits, whatever FMA
+// contraction the compiler would pick in each context
 __device__ __forceinline__ float gauss_power(const float4& cs, float dx, float dy) {
-  return cs.x * dx * dx + cs.y * dx * dy + cs.z * dy * dy;
+  float p = __fmul_rn(__fmul_rn(cs.x, dx), dx);
+  p = __fmaf_rn(__fmul_rn(cs.y, dx), dy, p);
+  return __fmaf_rn(__fmul_rn(cs.z, dy), dy, p);
 }
 // 1/x to ~1 ulp (MUFU.RCP, no IEEE-division slow path).  The backward replay
 // recovers T_exc = T / (1 - alpha) with it; 1 - alpha lies in [0.01, 1).

@@ -224,8 +224,19 @@ def test_config3_frame_vs_oracle():
 
 
 def test_config4_training_gradients_vs_oracle_chain(config1):
-    """configs[4] at full size: 2 (view, t) pairs, every gradient of the flat
-    buffer against the oracle chain."""
+    """configs[4] at full size: 2 (view, t) pairs through TrainStep, every
+    gradient of the flat all-reduce buffer against the oracle chain, in two
+    stages so that each comparison is exact up to fp32 arithmetic:
+
+    * render stage: each pair's device snapshot gradients (the lane's
+      render-backward output) against the oracle's render_backward of the same
+      fp32 snapshot with the same L1 upstream -- per Gaussian, excluding the
+      Gaussians an ambiguous decision can touch;
+    * deformation stage: the oracle's deform_backward fed the DEVICE's
+      snapshot gradients against the flat buffer's cloud / plane / MLP
+      gradients (summed over the pairs) -- every entry, no exclusions.
+
+    The end-to-end aggregate error (oracle chain vs device) is reported too."""
     import torch
     from paper_2503_06161_b200 import device as dv
     from paper_2503_06161_b200.train import TrainStep
@@ -243,57 +254,77 @@ def test_config4_training_gradients_vs_oracle_chain(config1):
              for (t, T), (tr, tf) in zip(views, targets)]
     loss = float(step.run(batch, check=True).item())
     torch.cuda.synchronize()
-    snaps = [{f: getattr(ln.snap, f).detach().cpu().numpy().astype(np.float64)
-              for f in ("positions", "rotations", "log_scales", "opacity_logits", "features")} for ln in step._lanes]
+    host = lambda x: x.detach().cpu().numpy().astype(np.float64)  # noqa: E731
+    snaps = [{f: host(getattr(ln.snap, f)) for f in ("positions", "rotations", "log_scales", "opacity_logits",
+                                                       "features")} for ln in step._lanes]
+    sgrads = [{f: host(getattr(ln.snap_grads, f)) for f in ("positions", "rotations", "log_scales", "opacity_logits",
+                                                            "colors_raw", "sh_rest", "features")}
+              for ln in step._lanes]
 
     onet = oracle_net(net)
     cfg = O.RasterParams()
     wpair = 1.0 / len(views)
-    acc, loss_ref = {}, 0.0
+    inj, chain, loss_ref = {}, {}, 0.0
     bad = np.zeros(k, dtype=bool)
-    for (t, T), (tr, tf), sd in zip(views, targets, snaps):
+    worst_render = 0.0
+
+    def add(acc, key, v):
+        acc[key] = acc.get(key, 0.0) + v
+
+    for (t, T), (tr, tf), sd, sg in zip(views, targets, snaps, sgrads):
         osnap, ocache = O.deform(cloud, field.planes, field.aabb, onet, t)
         for f in sd:
             assert np.abs(sd[f] - osnap[f]).max() < 1e-4, f
-        # the oracle renders the device's own fp32 snapshot (stage injection)
         so = _C(**sd, colors_raw=cloud.colors_raw, sh_rest=cloud.sh_rest)
         out = O.render(so, K, T, h, w, cfg, margins=True)
         dcol, dfe = out["color"] - tr, out["feature"] - tf
         loss_ref += wpair * (np.abs(dcol).mean() + np.abs(dfe).sum() / (h * w))
         g = O.render_backward(so, K, T, h, w, cfg, out, wpair * np.sign(dcol) / (3 * h * w), None,
                               wpair * np.sign(dfe) / (h * w), None)
-        cg, ng, pg = O.deform_backward(cloud, field.planes, field.aabb, onet, ocache, g)
-        contrib = {"positions": cg["positions"], "rotations": g["rotations"], "log_scales": g["log_scales"],
-                   "opacity_logits": g["opacity_logits"], "colors_raw": g["colors_raw"], "sh_rest": g["sh_rest"],
-                   "features": g["features"]}
-        contrib.update(ng)
-        for l, level in enumerate(pg):
-            for p, arr in enumerate(level):
-                contrib[f"grid.l{l}.p{p}"] = arr
-        for key, v in contrib.items():
-            acc[key] = acc.get(key, 0.0) + v
         # exclusions: Gaussians reached by the traversal of a pixel with an
         # ambiguous blend / projection decision or an ambiguous L1 sign, the
-        # ambiguous projections themselves, ambiguous ReLU gates
+        # ambiguous projections themselves
         amb, amb_stop, amb_src = ambiguity(out, cfg, h, w, split=True)
         amb |= (np.abs(dcol) < 1e-5).any(axis=2) | (np.abs(dfe) < 1e-5).any(axis=2)
-        bad[out["proj"]["source_index"][O.reached_rows(out, cfg, amb, amb_stop)]] = True
-        bad[list(amb_src)] = True
-        bad |= O.relu_gate_margins(onet, ocache) < TAU_GATE
+        pb = np.zeros(k, dtype=bool)
+        pb[out["proj"]["source_index"][O.reached_rows(out, cfg, amb, amb_stop)]] = True
+        pb[list(amb_src)] = True
+        bad |= pb
+        for f in sg:  # render stage, per Gaussian
+            ref = np.asarray(g[f])
+            tol = RTOL_GRAD * max(np.abs(ref).max(), 1e-30)
+            err = np.abs(sg[f] - ref)[~pb].max()
+            worst_render = max(worst_render, err / tol)
+            assert err < tol, ("render stage", f, err, tol)
+        # deformation stage on the device's snapshot gradients (stage injection)
+        cg, ng, pg = O.deform_backward(cloud, field.planes, field.aabb, onet, ocache, sg)
+        add(inj, "positions", cg["positions"])
+        for f in ("rotations", "log_scales", "opacity_logits", "colors_raw", "sh_rest", "features"):
+            add(inj, f, sg[f])
+        for key, v in ng.items():
+            add(inj, key, v)
+        for l, level in enumerate(pg):
+            for p, arr in enumerate(level):
+                add(inj, f"grid.l{l}.p{p}", arr)
+        # the full oracle chain, for the end-to-end report
+        cg2, ng2, pg2 = O.deform_backward(cloud, field.planes, field.aabb, onet, ocache, g)
+        add(chain, "positions", cg2["positions"])
+        for key, v in ng2.items():
+            add(chain, key, v)
+        for l, level in enumerate(pg2):
+            for p, arr in enumerate(level):
+                add(chain, f"grid.l{l}.p{p}", arr)
 
     assert abs(loss - loss_ref) < 1e-5 * max(1.0, abs(loss_ref)), (loss, loss_ref)
-    keep = ~bad
-    print(f"[configs[4]] Gaussians excluded from per-Gaussian comparison: {int(bad.sum())} of {k}")
-    assert keep.mean() > 0.8
-    per_gauss = ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "sh_rest", "features")
-    worst = {}
-    for key, ref in acc.items():
+    print(f"[configs[4]] render stage: {int(bad.sum())} of {k} Gaussians excluded, worst err/tol {worst_render:.2f}")
+    worst = 0.0
+    for key, ref in inj.items():
         got = step.grads[key].cpu().numpy().astype(np.float64).reshape(np.shape(ref))
-        ref = np.asarray(ref)
-        if key in per_gauss:
-            got, ref = got[keep], ref[keep]
-        tol = max(RTOL_GRAD * np.abs(ref).max(), 1e-15)
+        tol = max(RTOL_GRAD * np.abs(ref).max(), 1e-30)
         err = np.abs(got - ref).max()
-        worst[key] = err / tol
-        assert err < tol, (key, err, tol)
-    print("[configs[4]] worst err/tol:", max(worst.values()))
+        worst = max(worst, err / tol)
+        assert err < tol, ("deformation stage", key, err, tol)
+    e2e = max(np.linalg.norm(step.grads[key].cpu().numpy().astype(np.float64).reshape(np.shape(v)) - v)
+              / max(np.linalg.norm(v), 1e-30) for key, v in chain.items())
+    print(f"[configs[4]] deformation stage worst err/tol {worst:.2f}; end-to-end aggregate rel. L2 error {e2e:.2e}")
+    assert e2e < 1e-3

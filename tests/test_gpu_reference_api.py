@@ -4,9 +4,15 @@ one a featsplat caller gets after the swap).
 
 Each test names the reference test it replays (/root/reference/pkg/tests/...,
 file:line).  The assertions are the reference's; tolerances are rescaled from
-float64 to the device's fp32 (1e-12 -> 1e-6 absolute / 1e-5 relative), and the
-finite-difference checks use fp32-sized steps (central differences with
-eps ~1e-3 and a 2% relative bound instead of eps 1e-6 and 0.1%).
+float64 to the device's fp32 (1e-12 -> 1e-6 absolute / 1e-5 relative).  The
+finite-difference checks keep the reference's step (1e-5) and bound (1e-3
+relative): the device's analytic gradient is compared with central
+differences of the float64 function -- the oracle's restatement of the
+reference (pinned to it by tests/test_oracle_golden.py), evaluated at the
+same fp32-representable inputs -- because the fp32 device function itself is
+not smooth at any step large enough to rise above its rounding (the square
+footprint and the alpha thresholds are discrete).  The relative error gets a
+floor of 5% of the tensor's largest gradient (fp32 accumulation).
 """
 
 import numpy as np
@@ -34,7 +40,11 @@ def fs():
 AABB = np.array([[-1.0, -1.0, -1.0], [1.0, 1.0, 1.0]])
 
 
-def central_difference(f, arr, idx, eps=1e-3):
+def f32(x):
+    return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def central_difference(f, arr, idx, eps=1e-5):
     flat = arr.reshape(-1)
     out = np.empty(len(idx))
     for n, i in enumerate(idx):
@@ -48,9 +58,10 @@ def central_difference(f, arr, idx, eps=1e-3):
     return out
 
 
-def fd_close(analytic, fd, rtol=2e-2, scale=None):
-    """|analytic - fd| <= rtol * max(|fd|, 0.05 * scale) element-wise, scale =
-    the largest |gradient| of the set (fp32 FD noise floor)."""
+def fd_close(analytic, fd, rtol=1e-3, scale=None):
+    """|analytic - fd| <= rtol * max(|fd|, 0.05 * scale) element-wise (the
+    reference's rel_err < 1e-3, oracles.py:143-146, with an fp32 floor), scale
+    = the largest |gradient| of the set."""
     analytic, fd = np.asarray(analytic).reshape(-1), np.asarray(fd).reshape(-1)
     scale = np.abs(fd).max(initial=0.0) if scale is None else scale
     bound = rtol * np.maximum(np.abs(fd), 0.05 * scale) + 1e-7
@@ -58,13 +69,13 @@ def fd_close(analytic, fd, rtol=2e-2, scale=None):
 
 
 def random_cloud(fs, rng, k=20, n_feat=4, opacity_range=(0.1, 0.9), depth_range=(2.2, 3.8)):
-    """test conftest.py:26-37 shapes / distributions."""
+    """test conftest.py:26-37 shapes / distributions (fp32-representable)."""
     return fs.GaussianCloud(
-        positions=np.column_stack([rng.uniform(-0.9, 0.9, k), rng.uniform(-0.9, 0.9, k),
-                                   rng.uniform(*depth_range, k)]),
-        rotations=rng.normal(size=(k, 4)), log_scales=np.log(rng.uniform(0.08, 0.35, size=(k, 3))),
-        opacity_logits=np.asarray(fs.logit(rng.uniform(*opacity_range, k))),
-        colors_raw=rng.uniform(0.1, 0.9, size=(k, 3)), features=rng.normal(size=(k, n_feat)))
+        positions=f32(np.column_stack([rng.uniform(-0.9, 0.9, k), rng.uniform(-0.9, 0.9, k),
+                                       rng.uniform(*depth_range, k)])),
+        rotations=f32(rng.normal(size=(k, 4))), log_scales=f32(np.log(rng.uniform(0.08, 0.35, size=(k, 3)))),
+        opacity_logits=f32(fs.logit(rng.uniform(*opacity_range, k))),
+        colors_raw=f32(rng.uniform(0.1, 0.9, size=(k, 3))), features=f32(rng.normal(size=(k, n_feat))))
 
 
 def simple_frame(fs, size=32, focal=None, time=0.0):
@@ -182,18 +193,21 @@ def test_hex_single_plane_hand_product_rule(fs):  # test_hexplane.py:98-130
 
 
 def test_hex_query_backward_finite_differences(fs, rng):  # test_hexplane.py:133-154
+    from oracle import fs4d_oracle as O
     field = small_field(fs, rng, init="normal")
-    pos = rng.uniform(-0.8, 0.8, size=(4, 3))
+    for level in field.planes:
+        for pi in range(6):
+            level[pi] = f32(level[pi])
+    pos = f32(rng.uniform(-0.8, 0.8, size=(4, 3)))
     t = 0.43
     up = rng.normal(size=(4, field.latent_dim))
 
     def loss():
-        return float(np.sum(up * fs.query(field, pos, t)))
+        return float(np.sum(up * O.hexplane_query(field.planes, field.aabb, pos, t)))
 
     f, cache = fs.query_with_cache(field, pos, t)
     plane_grads, dpos = fs.query_backward(field, cache, up)
-    ok = fd_close(dpos, central_difference(loss, pos, np.arange(pos.size)))
-    assert ok.all()
+    assert fd_close(dpos, central_difference(loss, pos, np.arange(pos.size)), scale=np.abs(dpos).max()).all()
     for li in range(2):
         for pi in range(6):
             arr = field.planes[li][pi]
@@ -222,12 +236,15 @@ def test_tv_regulariser(fs, rng):  # test_hexplane.py:159-197
     f2.planes[0][0] = np.array([[0.0, 1.0], [0.0, 1.0]])[:, :, None]
     assert fs.tv_loss(f2) == pytest.approx(2.0 / 4.0, rel=1e-6)
     assert fs.tv_loss(small_field(fs, rng, init="normal")) >= 0.0
+    from oracle import fs4d_oracle as O
     f3 = small_field(fs, rng, levels=(1,), base=(3, 4, 3, 3), out_dim=4, init="normal")
+    for pi in range(6):
+        f3.planes[0][pi] = f32(f3.planes[0][pi])
     grads = fs.tv_backward(f3, scale=1.0)
     for pi in range(6):
         arr = f3.planes[0][pi]
-        assert fd_close(grads[0][pi], central_difference(lambda: fs.tv_loss(f3), arr, np.arange(arr.size)),
-                        scale=np.abs(grads[0][pi]).max()).all()
+        fd = central_difference(lambda: O.total_variation(f3.planes)[0], arr, np.arange(arr.size))
+        assert fd_close(grads[0][pi], fd, scale=np.abs(grads[0][pi]).max()).all()
 
 
 # ---------------------------------------------------------------------------
@@ -264,14 +281,16 @@ def test_mlp_backward(fs, rng):  # test_numerics.py:54-98
     dx, grads = fs.mlp_backward([layer], cache, np.array([1.0, 1.0]))
     np.testing.assert_array_equal(dx, [1.0, 0.0])
     np.testing.assert_array_equal(grads[0][1], [1.0, 0.0])
+    from oracle import fs4d_oracle as O
     layers = [fs.linear_layer(4, 6, "relu", rng), fs.linear_layer(6, 2, "none", rng)]
     for layer in layers:
-        layer.bias = rng.normal(size=layer.bias.shape) * 0.5
-    x = rng.normal(size=(5, 4))
+        layer.weight = f32(layer.weight)
+        layer.bias = f32(rng.normal(size=layer.bias.shape) * 0.5)
+    x = f32(rng.normal(size=(5, 4)))
     up = rng.normal(size=(5, 2))
 
     def loss():
-        y, _ = fs.mlp_forward(layers, x)
+        y, _ = O.dense_stack([(l.weight, l.bias, l.activation == "relu") for l in layers], x)
         return float(np.sum(up * y))
 
     _, cache = fs.mlp_forward(layers, x)
@@ -448,6 +467,7 @@ def test_backward_closed_forms(fs, rng):  # test_rasterizer.py:233-256
 
 
 def test_full_scene_finite_difference_gradients(fs, rng):  # test_rasterizer.py:259-283
+    from oracle import fs4d_oracle as O
     cloud = random_cloud(fs, rng, k=5, n_feat=3, opacity_range=(0.15, 0.3))
     fr = simple_frame(fs, 24)
     cfg = fs.RasterConfig()
@@ -455,17 +475,17 @@ def test_full_scene_finite_difference_gradients(fs, rng):  # test_rasterizer.py:
           "a": rng.normal(size=(24, 24))}
 
     def loss():
-        o = fs.render(cloud, fr, cfg)
-        return float(np.sum(up["c"] * o.color) + np.sum(up["d"] * o.depth) + np.sum(up["f"] * o.feature)
-                     + np.sum(up["a"] * o.alpha))
+        o = O.render(cloud, fr.K, fr.T, 24, 24, O.RasterParams())
+        return float(np.sum(up["c"] * o["color"]) + np.sum(up["d"] * o["depth"]) + np.sum(up["f"] * o["feature"])
+                     + np.sum(up["a"] * o["alpha"]))
 
     out = fs.render(cloud, fr, cfg)
     g = fs.render_backward(cloud, fr, out, up["c"], up["d"], up["f"], up["a"])
     for name in ("positions", "rotations", "log_scales", "opacity_logits", "colors_raw", "features"):
         arr = getattr(cloud, name)
         analytic = getattr(g, name)
-        fd = central_difference(loss, arr, np.arange(arr.size), eps=1e-3)
-        assert fd_close(analytic, fd, rtol=5e-2, scale=np.abs(analytic).max()).mean() >= 0.9, name
+        fd = central_difference(loss, arr, np.arange(arr.size))
+        assert fd_close(analytic, fd, scale=np.abs(analytic).max()).all(), name
 
 
 # ---------------------------------------------------------------------------
@@ -481,12 +501,16 @@ def make_parts(fs, rng, k=6, n_feat=5, width=16, depth=3, randomize=True):
     if randomize:
         for level in field.planes:
             for pi in range(len(level)):
-                level[pi] = 0.8 + rng.normal(size=level[pi].shape) * 0.3
+                level[pi] = f32(0.8 + rng.normal(size=level[pi].shape) * 0.3)
         for _, st in net.stacks():
             for layer in st:
-                layer.weight = rng.normal(size=layer.weight.shape) * 0.2
-                layer.bias = rng.normal(size=layer.bias.shape) * 0.2
+                layer.weight = f32(rng.normal(size=layer.weight.shape) * 0.2)
+                layer.bias = f32(rng.normal(size=layer.bias.shape) * 0.2)
     return cloud, field, net
+
+
+def oracle_net(net):
+    return {p: [(l.weight, l.bias, l.activation == "relu") for l in st] for p, st in net.stacks()}
 
 
 def test_deformation_stacks(fs, rng):  # test_deformation.py:42-106
@@ -561,36 +585,37 @@ def test_deform_identities(fs, rng):  # test_deformation.py:109-145, 218-223
 
 
 def test_deform_backward_finite_differences(fs, rng):  # test_deformation.py:148-187
+    from oracle import fs4d_oracle as O
     cloud, field, net = make_parts(fs, rng)
     t = 0.61
     ups = {n: rng.normal(size=getattr(cloud, n).shape) for n in ("positions", "rotations", "log_scales", "features")}
     ups["opacity_logits"] = rng.normal(size=len(cloud))
 
     def loss():
-        s = fs.deform(cloud, field, net, t)
-        return float(sum(np.sum(ups[n] * getattr(s, n)) for n in ups))
+        s, _ = O.deform(cloud, field.planes, field.aabb, oracle_net(net), t)
+        return float(sum(np.sum(ups[n] * s[n]) for n in ups))
 
     _, cache = fs.deform_with_cache(cloud, field, net, t)
     cg, ng, pg = fs.deform_backward(cloud, field, net, cache, type("G", (), ups)())
     for name, analytic in cg.items():
         arr = getattr(cloud, name)
         assert fd_close(analytic, central_difference(loss, arr, np.arange(arr.size)),
-                        scale=np.abs(analytic).max()).mean() >= 0.95, name
+                        scale=np.abs(analytic).max()).all(), name
     params = net.param_arrays()
     for name, analytic in ng.items():
         arr = params[name]
         idx = np.random.default_rng(abs(hash(name)) % 2 ** 31).choice(arr.size, size=min(arr.size, 25), replace=False)
         assert fd_close(analytic.reshape(-1)[idx], central_difference(loss, arr, idx),
-                        scale=np.abs(analytic).max()).mean() >= 0.9, name
+                        scale=np.abs(analytic).max()).all(), name
     for li, level in enumerate(pg):
         for pi, g in enumerate(level):
             arr = field.planes[li][pi]
             idx = np.random.default_rng(li * 7 + pi).choice(arr.size, size=min(arr.size, 15), replace=False)
-            assert fd_close(g.reshape(-1)[idx], central_difference(loss, arr, idx),
-                            scale=np.abs(g).max()).mean() >= 0.9
+            assert fd_close(g.reshape(-1)[idx], central_difference(loss, arr, idx), scale=np.abs(g).max()).all()
 
 
 def test_end_to_end_render_gradient_through_deformation(fs, rng):  # test_deformation.py:190-215
+    from oracle import fs4d_oracle as O
     cloud, field, net = make_parts(fs, rng, k=5)
     fr = simple_frame(fs, 16)
     t = 0.37
@@ -598,7 +623,9 @@ def test_end_to_end_render_gradient_through_deformation(fs, rng):  # test_deform
     up_c = rng.normal(size=(16, 16, 3))
 
     def loss():
-        return float(np.sum(up_c * fs.render(fs.deform(cloud, field, net, t), fr, rcfg).color))
+        s, _ = O.deform(cloud, field.planes, field.aabb, oracle_net(net), t)
+        o = O.render(type("S", (), s)(), fr.K, fr.T, 16, 16, O.RasterParams())
+        return float(np.sum(up_c * o["color"]))
 
     snap, cache = fs.deform_with_cache(cloud, field, net, t)
     out = fs.render(snap, fr, rcfg)
@@ -609,4 +636,4 @@ def test_end_to_end_render_gradient_through_deformation(fs, rng):  # test_deform
         arr = params[name]
         idx = np.random.default_rng(abs(hash(name)) % 2 ** 31).choice(arr.size, size=min(arr.size, 10), replace=False)
         assert fd_close(analytic.reshape(-1)[idx], central_difference(loss, arr, idx),
-                        rtol=5e-2, scale=np.abs(analytic).max()).mean() >= 0.8, name
+                        scale=np.abs(analytic).max()).all(), name
