@@ -1,6 +1,23 @@
-// Tile binning without a global sort (bin_tiles, rasterizer.py:188-207, and the
-// stable depth argsort it relies on, rasterizer.py:163).
+// Tile binning (bin_tiles, rasterizer.py:188-207, and the stable depth argsort
+// it relies on, rasterizer.py:163).
 //
+// Default: depth-ordered emission -- no per-tile sort at all.
+//   depth_order       global stable depth order of the kept Gaussians (radix
+//                     sort on fp32 depth bits + exact fp64 tie fix-up,
+//                     render_fwd.cu) -- the reference's argsort itself
+//   k_depth_counts    blocks of 256 consecutive Gaussians in that order count
+//                     their pairs per tile WITHOUT atomics: per warp, one
+//                     ballot per tile column / row gives the lanes whose
+//                     rectangle covers it, X[tx] & Y[ty] the lanes covering a
+//                     tile, popc the count -> table [block][tile]
+//   k_depth_scan      per tile, exclusive prefix over the blocks + the tile
+//                     offset: the table becomes each block's first slot
+//   k_depth_emit      each lane writes its pairs at block base + earlier
+//                     warps' counts + popc(lanes before it covering the tile):
+//                     every tile list comes out in global depth order, written
+//                     once, with no atomics and no sort
+// Fallback (FS4D_BINNING=tilesort, or images with more than
+// kDepthMaxTileAxes tile rows + columns):
 //   (per-tile pair counts: fused into k_preprocess, render_fwd.cu)
 //   scan              tile offsets (device-wide exclusive scan)
 //   k_emit_partition  every (tile, Gaussian) pair lands in its tile's segment;
@@ -10,6 +27,10 @@
 //                     stable float64 argsort order — with a bitonic network in
 //                     shared memory (global memory for oversized tiles) and
 //                     writes the tile range and the sorted source indices.
+#include <limits.h>
+#include <stdlib.h>
+#include <string.h>
+
 #include "render_common.cuh"
 
 namespace fs4d {
@@ -333,6 +354,147 @@ __global__ void k_pairs_check2(uint32_t* counters, int64_t cap, int32_t* status)
   }
 }
 
+// ---------------------------------------------------------------------------
+// depth-ordered emission
+// ---------------------------------------------------------------------------
+constexpr int kDepthThreads = 256;                 // Gaussians per block (depth order)
+constexpr int kDepthWarps = kDepthThreads / 32;
+constexpr int kDepthMaxTileAxes = 1024;            // ntx + nty limit (mask table in shared memory)
+constexpr int kDepthMaxTilesSmem = 8192;           // emit stages the block's base row in shared memory
+
+// Per warp: masks[tx] = lanes whose tile rectangle covers column tx, and
+// masks[ntx + ty] = lanes covering row ty (one ballot per column / row of the
+// warp's bounding range; zero elsewhere).  A lane covers tile (tx, ty) iff it
+// is in both.
+__device__ __forceinline__ void warp_cover_masks(const int4& r, bool live, int ntx, int nty, uint32_t* masks) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < ntx + nty; i += 32) masks[i] = 0u;
+  int lo_x = live ? r.x : INT_MAX, hi_x = live ? r.y : -1, lo_y = live ? r.z : INT_MAX, hi_y = live ? r.w : -1;
+  lo_x = __reduce_min_sync(0xffffffffu, lo_x);
+  hi_x = __reduce_max_sync(0xffffffffu, hi_x);
+  lo_y = __reduce_min_sync(0xffffffffu, lo_y);
+  hi_y = __reduce_max_sync(0xffffffffu, hi_y);
+  __syncwarp();
+  for (int tx = lo_x; tx <= hi_x; ++tx) {
+    const uint32_t m = __ballot_sync(0xffffffffu, live && r.x <= tx && tx <= r.y);
+    if (lane == 0) masks[tx] = m;
+  }
+  for (int ty = lo_y; ty <= hi_y; ++ty) {
+    const uint32_t m = __ballot_sync(0xffffffffu, live && r.z <= ty && ty <= r.w);
+    if (lane == 0) masks[ntx + ty] = m;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kDepthThreads) k_depth_counts(const uint32_t* __restrict__ order,
+                                                                const uint32_t* __restrict__ counters, int64_t K,
+                                                                const int4* __restrict__ tile_rect, int ntx, int nty,
+                                                                uint32_t* __restrict__ table) {
+  extern __shared__ uint32_t s_masks[];  // [warps][ntx + nty]
+  const int warp = threadIdx.x >> 5;
+  const int64_t M = counters[CNT_VISIBLE];
+  const int64_t r = (int64_t)blockIdx.x * kDepthThreads + threadIdx.x;
+  const bool live = r < M && r < K;
+  const int4 rect = live ? tile_rect[order[r]] : make_int4(0, -1, 0, -1);
+  const int axes = ntx + nty;
+  warp_cover_masks(rect, live, ntx, nty, s_masks + warp * axes);
+  __syncthreads();
+  const int ntiles = ntx * nty;
+  uint32_t* row = table + (int64_t)blockIdx.x * ntiles;
+  for (int t = threadIdx.x; t < ntiles; t += kDepthThreads) {
+    const int ty = t / ntx, tx = t - ty * ntx;
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kDepthWarps; ++w) c += __popc(s_masks[w * axes + tx] & s_masks[w * axes + ntx + ty]);
+    row[t] = c;
+  }
+}
+
+// Column scan of table [nblk][ntiles]: table[b][t] <- toff[t] + sum_{b' < b}
+// table[b'][t].  A CTA owns 32 tiles (lane = tile: coalesced rows); its 32
+// warps split the blocks into 32 chunks, sum them, and rewrite their chunk
+// from the chunk's prefix.
+constexpr int kScanColWarps = 32;
+__global__ void __launch_bounds__(kScanColWarps * 32) k_depth_scan(uint32_t* __restrict__ table, int64_t nblk,
+                                                                   int ntiles, const uint64_t* __restrict__ toff) {
+  __shared__ uint32_t s_sum[kScanColWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int64_t per = (nblk + kScanColWarps - 1) / kScanColWarps;
+  const int64_t b0 = warp * per, b1 = min(nblk, b0 + per);
+  uint32_t sum = 0;
+  if (t < ntiles) {
+#pragma unroll 8
+    for (int64_t b = b0; b < b1; ++b) sum += table[b * ntiles + t];
+  }
+  s_sum[warp][lane] = sum;
+  __syncthreads();
+  if (t >= ntiles) return;
+  uint32_t run = (uint32_t)toff[t];
+  for (int w = 0; w < warp; ++w) run += s_sum[w][lane];
+#pragma unroll 8
+  for (int64_t b = b0; b < b1; ++b) {
+    uint32_t* cell = table + b * ntiles + t;
+    const uint32_t c = *cell;
+    *cell = run;
+    run += c;
+  }
+}
+
+__global__ void __launch_bounds__(kDepthThreads) k_depth_emit(const uint32_t* __restrict__ order,
+                                                              const uint32_t* __restrict__ counters, int64_t K,
+                                                              const int4* __restrict__ tile_rect, int ntx, int nty,
+                                                              const uint32_t* __restrict__ table, int64_t cap,
+                                                              uint32_t* __restrict__ pvals) {
+  extern __shared__ uint32_t s_dyn[];  // [warps][ntx + nty] masks, then the block's base row [ntiles]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t M = counters[CNT_VISIBLE];
+  const int64_t r = (int64_t)blockIdx.x * kDepthThreads + threadIdx.x;
+  const bool live = r < M && r < K;
+  const uint32_t g = live ? order[r] : 0u;
+  const int4 rect = live ? tile_rect[g] : make_int4(0, -1, 0, -1);
+  const int axes = ntx + nty, ntiles = ntx * nty;
+  uint32_t* masks = s_dyn;
+  warp_cover_masks(rect, live, ntx, nty, masks + warp * axes);
+  const uint32_t* row = table + (int64_t)blockIdx.x * ntiles;
+  uint32_t* base = s_dyn + kDepthWarps * axes;
+  const bool staged = ntiles <= kDepthMaxTilesSmem;
+  if (staged)
+    for (int t = threadIdx.x; t < ntiles; t += kDepthThreads) base[t] = row[t];
+  __syncthreads();
+  if (!live) return;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int ty = rect.z; ty <= rect.w; ++ty) {
+    uint32_t ym[kDepthWarps];
+#pragma unroll
+    for (int w = 0; w < kDepthWarps; ++w) ym[w] = masks[w * axes + ntx + ty];
+    for (int tx = rect.x; tx <= rect.y; ++tx) {
+      const int t = ty * ntx + tx;
+      uint32_t pos = staged ? base[t] : row[t];
+#pragma unroll
+      for (int w = 0; w < kDepthWarps; ++w)
+        if (w < warp) pos += __popc(masks[w * axes + tx] & ym[w]);
+      pos += __popc(masks[warp * axes + tx] & ym[warp] & lt);
+      if ((int64_t)pos < cap) pvals[pos] = g;
+    }
+  }
+}
+
+__global__ void k_tile_ranges_from_offsets(const uint64_t* __restrict__ toff, const uint32_t* __restrict__ tcnt,
+                                           int ntiles, int64_t cap, uint2* __restrict__ ranges) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  uint64_t a = toff[t], e = a + tcnt[t];
+  if (a > (uint64_t)cap) a = (uint64_t)cap;
+  if (e > (uint64_t)cap) e = (uint64_t)cap;
+  ranges[t] = make_uint2((uint32_t)a, (uint32_t)e);
+}
+
+bool depth_binning_ok(const RenderLayout& L) {
+  static const bool tilesort = getenv("FS4D_BINNING") && !strcmp(getenv("FS4D_BINNING"), "tilesort");
+  return !tilesort && L.ntx + L.nty <= kDepthMaxTileAxes && L.cap < (int64_t)0xFFFFFFFF;
+}
+
 // host: the whole binning stage (counts -> offsets -> partition -> per-tile sort)
 void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, const uint32_t* dkeys,
                       const double* z64, uint32_t* counters, int32_t* status, cudaStream_t s) {
@@ -348,6 +510,32 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
     exclusive_scan_u32_to_u64(tcnt, toff, L.ntiles, nullptr, reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64),
                               at<void>(ws, L.scratch), s);
     k_pairs_check2<<<1, 1, 0, s>>>(counters, L.cap, status);
+  }
+  if (depth_binning_ok(L)) {
+    const uint32_t* order = depth_order(L, ws, s, false);
+    const int64_t nblk = ceil_div(K > 0 ? K : 1, kDepthThreads);
+    uint32_t* table = at<uint32_t>(ws, L.dtable);
+    const int axes = L.ntx + L.nty;
+    const size_t smem_c = (size_t)kDepthWarps * axes * 4;
+    const size_t smem_e = smem_c + (L.ntiles <= kDepthMaxTilesSmem ? (size_t)L.ntiles * 4 : 0);
+    static size_t attr_c = 0, attr_e = 0;
+    if (smem_c > 48 * 1024 && smem_c > attr_c) {
+      cudaFuncSetAttribute(k_depth_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
+      attr_c = smem_c;
+    }
+    if (smem_e > 48 * 1024 && smem_e > attr_e) {
+      cudaFuncSetAttribute(k_depth_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+      attr_e = smem_e;
+    }
+    if (L.ntiles > 0) {
+      k_depth_counts<<<(unsigned)nblk, kDepthThreads, smem_c, s>>>(order, counters, K, tile_rect, L.ntx, L.nty, table);
+      k_depth_scan<<<(unsigned)ceil_div(L.ntiles, 32), kScanColWarps * 32, 0, s>>>(table, nblk, L.ntiles, toff);
+      k_depth_emit<<<(unsigned)nblk, kDepthThreads, smem_e, s>>>(order, counters, K, tile_rect, L.ntx, L.nty, table,
+                                                                 L.cap, at<uint32_t>(ws, L.pvals0));
+      k_tile_ranges_from_offsets<<<(unsigned)ceil_div(L.ntiles, 256), 256, 0, s>>>(toff, tcnt, L.ntiles, L.cap,
+                                                                                  at<uint2>(ws, L.ranges));
+    }
+    return;
   }
   unsigned long long* pkey = at<unsigned long long>(ws, L.pkey64);
   if (K > 0)

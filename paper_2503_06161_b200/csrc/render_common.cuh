@@ -69,6 +69,7 @@ struct RenderLayout {
   // per Gaussian (source-indexed): projected record, fp64 depth, depth-sort
   // keys/values (the global order is only materialised for export/backward)
   size_t xy, conic_o, pix_rect, tile_rect, rgbz, cov_r, z64, dkeys0, dkeys1, dvals0, dvals1, rank_of, clamp_mask;
+  size_t dtable;  // depth-ordered binning: per (256-Gaussian block, tile) counts / slots
   // tiles: counts, append cursors, segment offsets, [start, end) ranges
   size_t tcnt, tcur, toff64, ranges, tperm;
   // pairs: 64-bit (depth bits, source index) keys and the sorted source indices
@@ -165,6 +166,7 @@ inline RenderLayout make_layout(const Fs4dRecordInfo& info) {
   L.ranges = take(nt * 8);
   L.tperm = take(nt * 4);  // tiles by decreasing pair count (CTA launch order)
   L.pkey64 = take(cap * 8);
+  L.dtable = take((size_t)((K + 255) / 256) * nt * 4);
   L.pvals0 = take(cap * 4);
   L.tfinal = take(npix * 4);
   L.last = take(npix * 4);
@@ -186,6 +188,6 @@ __host__ __device__ inline T* at(void* base, size_t off) {
 void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, const uint32_t* dkeys,
                       const double* z64, uint32_t* counters, int32_t* status, cudaStream_t s);
 // render_fwd.cu: global stable depth order of the visible set (export / backward)
-const uint32_t* depth_order(const RenderLayout& L, void* ws, cudaStream_t s);
+const uint32_t* depth_order(const RenderLayout& L, void* ws, cudaStream_t s, bool with_rank = true);
 
 }  // namespace fs4d

