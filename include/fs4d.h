@@ -284,6 +284,23 @@ int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field,
                     int32_t accumulate,
                     void* workspace, size_t workspace_bytes,
                     int32_t* status, void* stream);
+/* Deterministic variant (fixed-order reductions): the
+ * HexPlane plane gradients accumulate in int64 fixed point -- one scale per
+ * plane, 2^(62 - ceil(log2 B)) with B = K * C * max|d latent| * the product of
+ * the other five planes' max |value| (a bound on the plane's total L1 mass),
+ * computed on device -- so integer adds make the scatter order irrelevant
+ * and the result bitwise reproducible (rounding unit ~B * 2^-62).  Every other
+ * output of the tensor-core backward is already produced in a fixed order.
+ * Needs the cached tensor-core path (width 64, depth 1, levels * channels =
+ * 64, feature_dim <= 16); det_workspace of
+ * fs4d_deform_bwd_det_workspace_bytes bytes. */
+int fs4d_deform_bwd_deterministic(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net,
+                                  double t, const void* cache, size_t cache_bytes,
+                                  const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads,
+                                  Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads, int32_t accumulate,
+                                  void* workspace, size_t workspace_bytes, void* det_workspace,
+                                  size_t det_workspace_bytes, int32_t* status, void* stream);
+size_t fs4d_deform_bwd_det_workspace_bytes(const Fs4dDeformNet* net, const Fs4dHexPlane* field);
 /* accumulate != 0 adds into every output instead of overwriting it (gradient
  * accumulation over the (view, t) pairs of a training step).  Non-NULL
  * cloud_grads fields other than positions receive the pass-through snapshot
@@ -322,6 +339,13 @@ int fs4d_photometric_loss_grad(const float* color, const float* image, const uin
  * (either output may be NULL).  feature_loss is scale = 1/(H*W). */
 int fs4d_l1(const float* pred, const float* target, int64_t n, double scale, float* grad,
             double* loss, void* stream);
+
+/* dst[i] (+)= srcs[0][i] + ... + srcs[n_src-1][i] in that order, one pass
+ * (accumulate != 0 adds to dst): the training step's per-lane gradient
+ * buffers summed before the all-reduce.  srcs is a host array of up to 8
+ * device pointers.  No reference counterpart (the reference has one lane). */
+int fs4d_sum_buffers(float* dst, const float* const* srcs, int32_t n_src, int64_t n, int32_t accumulate,
+                     void* stream);
 
 /* HexPlane query on its own (hexplane.query / query_with_cache,
  * hexplane.py:113-142): latent [K, levels * channels] (level-major, the
@@ -500,6 +524,19 @@ int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam,
                     const Fs4dImageGrads* upstream, Fs4dCloud* grads,
                     int32_t* viewspace_index, float* viewspace_norm,
                     int32_t* status, void* stream);
+
+/* Deterministic variant of fs4d_render_bwd: the blend backward writes one
+ * partial per (tile pair, row-split CTA) -- the CTA's warps added in a fixed
+ * order in shared memory -- and a gather sums each Gaussian's partials over
+ * its tiles in row-major order, instead of float atomics: gradients are
+ * bitwise reproducible run to run.  D <= 16 feature
+ * channels; det_workspace of fs4d_render_bwd_det_workspace_bytes bytes. */
+int fs4d_render_bwd_deterministic(const Fs4dCloud* snapshot, const Fs4dCamera* cam, const Fs4dRasterConfig* cfg,
+                                  const Fs4dRecordInfo* info, void* workspace, size_t workspace_bytes,
+                                  const Fs4dImageGrads* upstream, Fs4dCloud* grads, int32_t* viewspace_index,
+                                  float* viewspace_norm, void* det_workspace, size_t det_workspace_bytes,
+                                  int32_t* status, void* stream);
+size_t fs4d_render_bwd_det_workspace_bytes(const Fs4dRecordInfo* info);
 
 /* Read back a forward record: depth-sorted ProjectedGaussians (first M rows). */
 int fs4d_render_export_projected(const Fs4dRecordInfo* info, const void* workspace,

@@ -138,6 +138,7 @@ SIGNATURES = {
                                        ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane),
                                        ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_sum_buffers": (ctypes.c_int, [_V, ctypes.POINTER(ctypes.c_void_p), _I32, _I64, _I32, _V]),
     "fs4d_hexplane_query": (ctypes.c_int, [ctypes.POINTER(HexPlane), _V, _I64, _D, _V, _V]),
     "fs4d_hexplane_query_backward": (ctypes.c_int, [ctypes.POINTER(HexPlane), _V, _I64, _D, _V,
                                                     ctypes.POINTER(HexPlane), _V, _I32, _V]),
@@ -148,6 +149,15 @@ SIGNATURES = {
     "fs4d_render_tile_alphas": (ctypes.c_int, [ctypes.POINTER(RecordInfo), _V, _SZ, ctypes.POINTER(RasterCfg), _V,
                                                _I64, _I32, _I32, _I32, _I32, _V, _V, _V, _V]),
     "fs4d_composite_weights": (ctypes.c_int, [_V, _I64, _I64, _D, _V, _V, _V, _V, _V]),
+    "fs4d_deform_bwd_deterministic": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(HexPlane),
+                                                     ctypes.POINTER(DeformNet), ctypes.c_double,
+                                                     ctypes.c_void_p, ctypes.c_size_t,
+                                                     ctypes.POINTER(Cloud), ctypes.POINTER(Cloud),
+                                                     ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane),
+                                                     ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
+                                                     ctypes.c_void_p, ctypes.c_size_t,
+                                                     ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_deform_bwd_det_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane)]),
     "fs4d_l1_loss_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int32, ctypes.c_double, ctypes.c_double,
@@ -191,6 +201,13 @@ SIGNATURES = {
                                        ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ImageGrads),
                                        ctypes.POINTER(Cloud), ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_render_bwd_deterministic": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(Camera),
+                                                     ctypes.POINTER(RasterCfg), ctypes.POINTER(RecordInfo),
+                                                     ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ImageGrads),
+                                                     ctypes.POINTER(Cloud), ctypes.c_void_p, ctypes.c_void_p,
+                                                     ctypes.c_void_p, ctypes.c_size_t,
+                                                     ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_render_bwd_det_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(RecordInfo)]),
     "fs4d_render_export_projected": (ctypes.c_int, [ctypes.POINTER(RecordInfo), ctypes.c_void_p,
                                                     ctypes.c_size_t, ctypes.POINTER(Projected),
                                                     ctypes.c_void_p]),

@@ -63,7 +63,8 @@ void profile_mark(int stage, bool begin, cudaStream_t s) {
 int render_forward(const Fs4dCloud&, const Fs4dCamera&, const Fs4dRasterConfig&, const RenderLayout&, void*,
                    Fs4dImages&, int32_t*, cudaStream_t);
 int render_backward(const Fs4dCloud&, const Fs4dCamera&, const Fs4dRasterConfig&, const RenderLayout&, void*,
-                    const Fs4dImageGrads&, Fs4dCloud&, int32_t*, float*, cudaStream_t);
+                    const Fs4dImageGrads&, Fs4dCloud&, int32_t*, float*, void*, size_t, cudaStream_t);
+size_t render_bwd_det_bytes(const RenderLayout&);
 int render_export_projected(const RenderLayout&, void*, Fs4dProjected&, cudaStream_t);
 int render_export_tiles(const RenderLayout&, void*, int32_t*, int32_t*, int64_t, cudaStream_t);
 size_t deform_workspace_bytes(const Fs4dDeformNet& net, int64_t K, int* nparts_out);
@@ -71,8 +72,9 @@ size_t deform_cache_bytes(const Fs4dDeformNet& net, const Fs4dHexPlane& field, i
 int deform_forward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, Fs4dCloud&, void*, size_t,
                    void*, size_t, cudaStream_t);
 int deform_backward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, const void*, size_t,
-                    const Fs4dCloud&, Fs4dCloud&, Fs4dDeformNet&, Fs4dHexPlane*, int, void*, size_t, int32_t*,
-                    cudaStream_t);
+                    const Fs4dCloud&, Fs4dCloud&, Fs4dDeformNet&, Fs4dHexPlane*, int, void*, size_t, int32_t*, void*,
+                    size_t, cudaStream_t);
+size_t deform_backward_det_bytes(const Fs4dDeformNet&, const Fs4dHexPlane&);
 int l1_loss_grad(const float*, const float*, const float*, const float*, int, int, int, double, double, float*, float*,
                  double*, cudaStream_t);
 
@@ -83,6 +85,7 @@ int l1(const float*, const float*, int64_t, double, float*, double*, cudaStream_
 int adam_step(float*, const float*, float*, float*, int32_t*, const Fs4dAdamSegment*, int, const int32_t*, int32_t*,
               cudaStream_t);
 int hexplane_query(const Fs4dHexPlane&, const float*, int64_t, double, float*, cudaStream_t);
+int sum_buffers(float*, const float* const*, int, int64_t, int, cudaStream_t);
 size_t linear_backward_workspace_bytes(int64_t, int, int);
 int linear_forward(const float*, int64_t, const Fs4dLinear&, float*, float*, cudaStream_t);
 int linear_backward(const float*, const float*, int64_t, const Fs4dLinear&, const float*, float*, float*, float*, int,
@@ -274,7 +277,38 @@ int fs4d_deform_bwd(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4
   if (snapshot_grads->K != cloud->K || cloud_grads->K != cloud->K)
     return fail(FS4D_ERR_CONTRACT, "gradient rows do not match the cloud");
   return deform_backward(*cloud, *field, *net, t, cache, cache_bytes, *snapshot_grads, *cloud_grads, *net_grads,
-                         plane_grads, accumulate, workspace, workspace_bytes, status, (cudaStream_t)stream);
+                         plane_grads, accumulate, workspace, workspace_bytes, status, nullptr, 0,
+                         (cudaStream_t)stream);
+}
+
+int fs4d_deform_bwd_deterministic(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net, double t,
+                    const void* cache, size_t cache_bytes, const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads,
+                    Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads, int32_t accumulate, void* workspace,
+                    size_t workspace_bytes, void* det_workspace, size_t det_workspace_bytes,
+                                   int32_t* status, void* stream) {
+  if (!det_workspace) return fail(FS4D_ERR_CONFIG, "null deterministic workspace");
+  int rc = check_cloud(cloud, false);
+  if (rc) return rc;
+  if (!field || !net || !snapshot_grads || !cloud_grads || !net_grads)
+    return fail(FS4D_ERR_CONFIG, "null deform_bwd argument");
+  if (snapshot_grads->K != cloud->K || cloud_grads->K != cloud->K)
+    return fail(FS4D_ERR_CONTRACT, "gradient rows do not match the cloud");
+  return deform_backward(*cloud, *field, *net, t, cache, cache_bytes, *snapshot_grads, *cloud_grads, *net_grads,
+                         plane_grads, accumulate, workspace, workspace_bytes, status, det_workspace,
+                         det_workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t fs4d_deform_bwd_det_workspace_bytes(const Fs4dDeformNet* net, const Fs4dHexPlane* field) {
+  if (!net || !field) return 0;
+  return deform_backward_det_bytes(*net, *field);
+}
+
+int fs4d_sum_buffers(float* dst, const float* const* srcs, int32_t n_src, int64_t n, int32_t accumulate,
+                     void* stream) {
+  if (!dst || n < 0 || n_src < 0 || (n_src > 0 && !srcs)) return fail(FS4D_ERR_CONFIG, "bad sum_buffers arguments");
+  for (int j = 0; j < n_src; ++j)
+    if (!srcs[j]) return fail(FS4D_ERR_CONFIG, "null sum_buffers source");
+  return sum_buffers(dst, srcs, n_src, n, accumulate, (cudaStream_t)stream);
 }
 
 int fs4d_hexplane_query(const Fs4dHexPlane* field, const float* positions, int64_t K, double t, float* latent,
@@ -523,8 +557,36 @@ int fs4d_render_bwd(const Fs4dCloud* snapshot, const Fs4dCamera* cam, const Fs4d
     return fail(FS4D_ERR_CONFIG, "render backward supports at most 64 feature channels");
   RenderLayout L = make_layout(*info);
   return render_backward(*snapshot, *cam, *cfg, L, workspace, *upstream, *grads, viewspace_index, viewspace_norm,
-                         (cudaStream_t)stream);
+                         nullptr, 0, (cudaStream_t)stream);
 }
+
+int fs4d_render_bwd_deterministic(const Fs4dCloud* snapshot, const Fs4dCamera* cam, const Fs4dRasterConfig* cfg,
+                    const Fs4dRecordInfo* info, void* workspace, size_t workspace_bytes,
+                    const Fs4dImageGrads* upstream, Fs4dCloud* grads, int32_t* viewspace_index,
+                    float* viewspace_norm, void* det_workspace, size_t det_workspace_bytes,
+                                   int32_t* status, void* stream) {
+  (void)status;
+  int rc = check_cloud(snapshot, true);
+  if (rc) return rc;
+  if ((rc = check_camera(cam))) return rc;
+  if ((rc = check_record(info, snapshot, cam, cfg, workspace_bytes, workspace))) return rc;
+  if (!upstream || !grads) return fail(FS4D_ERR_CONFIG, "null backward argument");
+  if (viewspace_index && !viewspace_norm) return fail(FS4D_ERR_CONFIG, "viewspace_index without viewspace_norm");
+  if (grads->K != snapshot->K || grads->D != snapshot->D || grads->sh_degree != snapshot->sh_degree)
+    return fail(FS4D_ERR_CONFIG, "gradient buffers do not match the snapshot");
+  if (cfg->with_features && snapshot->D > 64)
+    return fail(FS4D_ERR_CONFIG, "render backward supports at most 64 feature channels");
+  RenderLayout L = make_layout(*info);
+  if (!det_workspace) return fail(FS4D_ERR_CONFIG, "null deterministic workspace");
+  return render_backward(*snapshot, *cam, *cfg, L, workspace, *upstream, *grads, viewspace_index, viewspace_norm,
+                         det_workspace, det_workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t fs4d_render_bwd_det_workspace_bytes(const Fs4dRecordInfo* info) {
+  if (!info) return 0;
+  return render_bwd_det_bytes(make_layout(*info));
+}
+
 
 int fs4d_render_export_projected(const Fs4dRecordInfo* info, const void* workspace, size_t workspace_bytes,
                                  Fs4dProjected* out, void* stream) {

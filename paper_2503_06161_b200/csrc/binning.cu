@@ -1,7 +1,7 @@
 // Tile binning (bin_tiles, rasterizer.py:188-207, and the stable depth argsort
 // it relies on, rasterizer.py:163).
 //
-// Default: depth-ordered emission -- no per-tile sort at all.
+// Option (FS4D_BINNING=depth): depth-ordered emission -- no per-tile sort.
 //   depth_order       global stable depth order of the kept Gaussians (radix
 //                     sort on fp32 depth bits + exact fp64 tie fix-up,
 //                     render_fwd.cu) -- the reference's argsort itself
@@ -16,8 +16,7 @@
 //                     warps' counts + popc(lanes before it covering the tile):
 //                     every tile list comes out in global depth order, written
 //                     once, with no atomics and no sort
-// Fallback (FS4D_BINNING=tilesort, or images with more than
-// kDepthMaxTileAxes tile rows + columns):
+// Default (per-tile sort):
 //   (per-tile pair counts: fused into k_preprocess, render_fwd.cu)
 //   scan              tile offsets (device-wide exclusive scan)
 //   k_emit_partition  every (tile, Gaussian) pair lands in its tile's segment;
@@ -490,9 +489,13 @@ __global__ void k_tile_ranges_from_offsets(const uint64_t* __restrict__ toff, co
   ranges[t] = make_uint2((uint32_t)a, (uint32_t)e);
 }
 
+// Opt-in (FS4D_BINNING=depth): measured on B200 at configs[1] the global
+// depth sort alone (4 radix passes over 200k keys) costs more than the
+// per-tile sort path it replaces (binning stage 157 vs 85 us), so the
+// per-tile sort stays the default.
 bool depth_binning_ok(const RenderLayout& L) {
-  static const bool tilesort = getenv("FS4D_BINNING") && !strcmp(getenv("FS4D_BINNING"), "tilesort");
-  return !tilesort && L.ntx + L.nty <= kDepthMaxTileAxes && L.cap < (int64_t)0xFFFFFFFF;
+  static const bool depth = getenv("FS4D_BINNING") && !strcmp(getenv("FS4D_BINNING"), "depth");
+  return depth && L.ntx + L.nty <= kDepthMaxTileAxes && L.cap < (int64_t)0xFFFFFFFF;
 }
 
 // host: the whole binning stage (counts -> offsets -> partition -> per-tile sort)

@@ -820,7 +820,9 @@ bool tc_bwd_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f);
 size_t tc_cache_bytes(const Fs4dDeformNet& n, const Fs4dHexPlane& f, int64_t K);
 int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
                        const uint8_t* cache, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
-                       Fs4dHexPlane* pg, int accumulate, void* ws, int32_t* status, cudaStream_t s);
+                       Fs4dHexPlane* pg, int accumulate, void* ws, int32_t* status, void* det_ws, size_t det_bytes,
+                       cudaStream_t s);
+size_t deform_bwd_det_bytes(const Fs4dHexPlane& f);
 
 static bool tc_enabled() { return !getenv("FS4D_NO_TC"); }
 
@@ -902,9 +904,15 @@ int deform_forward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4d
   return check_launch("deform_fwd");
 }
 
+size_t deform_backward_det_bytes(const Fs4dDeformNet& net, const Fs4dHexPlane& field) {
+  if (!tc_enabled() || !tc_bwd_ok(net, field)) return 0;
+  return deform_bwd_det_bytes(field);
+}
+
 int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
                     const void* cache, size_t cache_bytes, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
-                    Fs4dHexPlane* pg, int accumulate, void* ws, size_t ws_bytes, int32_t* status, cudaStream_t s) {
+                    Fs4dHexPlane* pg, int accumulate, void* ws, size_t ws_bytes, int32_t* status, void* det_ws,
+                    size_t det_bytes, cudaStream_t s) {
   DefArgs a;
   memset(&a, 0, sizeof(a));
   size_t smem = 0;
@@ -948,9 +956,14 @@ int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4
     if (blocks > 0) k_grad_passthrough<<<(unsigned)blocks, 256, 0, s>>>(pa);
   }
   const size_t cneed = deform_cache_bytes(net, field, cloud.K);
+  if (det_ws && !(cache && cneed))
+    return fail(FS4D_ERR_CONFIG,
+                "the deterministic deform backward needs the tensor-core path with its forward cache "
+                "(width 64, depth 1, levels * channels = 64, feature_dim <= 16)");
   if (cache && cneed) {
     if (cache_bytes < cneed) return fail(FS4D_ERR_CONFIG, "deform cache too small");
-    return deform_backward_tc(cloud, field, net, t, (const uint8_t*)cache, sg, cg, ng, pg, accumulate, ws, status, s);
+    return deform_backward_tc(cloud, field, net, t, (const uint8_t*)cache, sg, cg, ng, pg, accumulate, ws, status,
+                              det_ws, det_bytes, s);
   }
   const int64_t ntiles = ceil_div(cloud.K, a.TG);
   const int grid = (int)(ntiles < kNumSMs * 2 ? (ntiles > 0 ? ntiles : 1) : kNumSMs * 2);

@@ -428,10 +428,22 @@ struct HexBwdArgs {
   float* cg_pos;
   float* gplanes[FS4D_MAX_LEVELS][6];
   int accumulate;
+  // deterministic mode: int64 fixed-point accumulators per plane (integer
+  // adds commute, so the scatter order no longer matters) and the scale of
+  // each plane (det_scales)
+  unsigned long long* dacc[FS4D_MAX_LEVELS][6];
+  const double* dscale;
 };
+
+// v * scale rounded to an integer and added to a two's-complement int64 cell
+__device__ __forceinline__ void det_add(unsigned long long* cell, float v, double scale) {
+  const long long q = __double2ll_rn((double)v * scale);
+  if (q) atomicAdd(cell, (unsigned long long)q);
+}
 
 constexpr int kHexBwdWarps = 8;
 
+template <bool DET = false>
 __global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a) {
   const TcPlan& p = a.p;
   const int lane = threadIdx.x & 31;
@@ -488,11 +500,20 @@ __global__ void __launch_bounds__(kHexBwdWarps * 32) k_hexplane_bwd(HexBwdArgs a
       for (int q = 0; q < 6; ++q) {
         const float coef = up * pre[q] * suf[q];
         if (coef != 0.f) {
-          float* gp = a.gplanes[l][q] + base[q] + ch;
-          red_add(gp, coef * (1.f - fa[q]) * (1.f - fb[q]));
-          red_add(gp + rs[q], coef * fa[q] * (1.f - fb[q]));
-          red_add(gp + C, coef * (1.f - fa[q]) * fb[q]);
-          red_add(gp + rs[q] + C, coef * fa[q] * fb[q]);
+          if (DET) {
+            unsigned long long* gp = a.dacc[l][q] + base[q] + ch;
+            const double sc = a.dscale[l * 6 + q];
+            det_add(gp, coef * (1.f - fa[q]) * (1.f - fb[q]), sc);
+            det_add(gp + rs[q], coef * fa[q] * (1.f - fb[q]), sc);
+            det_add(gp + C, coef * (1.f - fa[q]) * fb[q], sc);
+            det_add(gp + rs[q] + C, coef * fa[q] * fb[q], sc);
+          } else {
+            float* gp = a.gplanes[l][q] + base[q] + ch;
+            red_add(gp, coef * (1.f - fa[q]) * (1.f - fb[q]));
+            red_add(gp + rs[q], coef * fa[q] * (1.f - fb[q]));
+            red_add(gp + C, coef * (1.f - fa[q]) * fb[q]);
+            red_add(gp + rs[q] + C, coef * fa[q] * fb[q]);
+          }
         }
         sa[q] += coef * d_a[q];
         sb[q] += coef * d_b[q];
@@ -530,9 +551,10 @@ struct HexC32Args {
   int toff[2][3];  // offsets (floats) of the time-plane accumulators inside a CTA's partial
   int tfloats;
   float* tpart;    // [grid][tfloats] per-CTA time-plane partials (global, zeroed by the host)
+  unsigned long long* tpart_i;  // deterministic mode: the same partials in int64 fixed point
 };
 
-__device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 || q == 5; }
+__host__ __device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 || q == 5; }
 
 
 // Time planes: every Gaussian of a frame hits the same t row pair, so their
@@ -543,11 +565,13 @@ __device__ __forceinline__ bool is_time_plane(int q) { return q == 2 || q == 4 |
 #ifndef FS4D_HEX_BWD_MINB
 #define FS4D_HEX_BWD_MINB 2  // measured: 1 -> 248 us, 2 -> 240 us (128 registers, small spill)
 #endif
+template <bool DET = false>
 __global__ void __launch_bounds__(kHexC32Warps * 32, FS4D_HEX_BWD_MINB) k_hexplane_bwd_c32(HexC32Args A) {
   const HexBwdArgs& a = A.h;
   const TcPlan& p = a.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* tacc = A.tpart + (int64_t)blockIdx.x * A.tfloats;
+  float* tacc = DET ? nullptr : A.tpart + (int64_t)blockIdx.x * A.tfloats;
+  unsigned long long* tacc_i = DET ? A.tpart_i + (int64_t)blockIdx.x * A.tfloats : nullptr;
   // the shared t cell of each level (hexplane.py:95-110 on the time axis)
   int tj0[2];
 #pragma unroll
@@ -683,7 +707,27 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, FS4D_HEX_BWD_MINB) k_hexpla
           const float4 cf = make_float4(up.x * pre[q].x * suf[q].x, up.y * pre[q].y * suf[q].y,
                                         up.z * pre[q].z * suf[q].z, up.w * pre[q].w * suf[q].w);
           const float f0 = w_a[q], f1 = w_b[q];
-          if (is_time_plane(q)) {
+          if (DET) {
+            const double sc = a.dscale[l * 6 + q];
+            auto add4 = [&](unsigned long long* c, float wgt) {
+              det_add(c, cf.x * wgt, sc);
+              det_add(c + 1, cf.y * wgt, sc);
+              det_add(c + 2, cf.z * wgt, sc);
+              det_add(c + 3, cf.w * wgt, sc);
+            };
+            if (is_time_plane(q)) {
+              unsigned long long* acc = tacc_i + A.toff[l][q == 2 ? 0 : (q == 4 ? 1 : 2)] + cb[q] * 32 + ch;
+              add4(acc, 1.f - f0);
+              add4(acc + 32, f0);
+            } else {
+              const int rs = p.res[l][q][1] * 32;
+              unsigned long long* gp = a.dacc[l][q] + cb[q] + ch;
+              add4(gp, (1.f - f0) * (1.f - f1));
+              add4(gp + rs, f0 * (1.f - f1));
+              add4(gp + 32, (1.f - f0) * f1);
+              add4(gp + rs + 32, f0 * f1);
+            }
+          } else if (is_time_plane(q)) {
             float* acc = tacc + A.toff[l][q == 2 ? 0 : (q == 4 ? 1 : 2)] + cb[q] * 32 + ch;
             const float g0 = 1.f - f0;
             red_add_v4(acc, cf.x * g0, cf.y * g0, cf.z * g0, cf.w * g0);
@@ -723,6 +767,8 @@ __global__ void __launch_bounds__(kHexC32Warps * 32, FS4D_HEX_BWD_MINB) k_hexpla
 // row onto the t rows j0 / j0 + 1 with the frame's t weights (hexplane.py:95-110).
 struct TimeReduceArgs {
   const float* tpart;
+  const unsigned long long* tpart_i;  // deterministic mode (int64 fixed point), or null
+  const double* dscale;
   int nparts, tfloats;
   int toff[2][3], ra[2][3], rb[2][3], tj0[2];
   float tfb[2];
@@ -730,23 +776,99 @@ struct TimeReduceArgs {
 };
 __global__ void __launch_bounds__(32 * kRedGroups) k_time_partials(TimeReduceArgs a) {
   __shared__ float part[kRedGroups][33];
+  __shared__ long long ipart[kRedGroups][33];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + lane;
-  part[g][lane] = e < a.tfloats ? sum_parts(a.tpart, a.tfloats, a.nparts, e, g) : 0.f;
+  if (a.tpart_i) {  // exact integer sums over the CTAs
+    long long acc = 0;
+    if (e < a.tfloats)
+      for (int q = g; q < a.nparts; q += kRedGroups) acc += (long long)a.tpart_i[(int64_t)q * a.tfloats + e];
+    ipart[g][lane] = acc;
+  } else {
+    part[g][lane] = e < a.tfloats ? sum_parts(a.tpart, a.tfloats, a.nparts, e, g) : 0.f;
+  }
   __syncthreads();
   if (g != 0 || e >= a.tfloats) return;
-  float v = 0.f;
-#pragma unroll
-  for (int w = 0; w < kRedGroups; ++w) v += part[w][lane];
-  if (v == 0.f) return;
   int l = 0, t = 0;
   for (int ll = 0; ll < 2; ++ll)
     for (int tt = 0; tt < 3; ++tt)
       if (e >= a.toff[ll][tt]) l = ll, t = tt;
+  float v = 0.f;
+  if (a.tpart_i) {
+    long long acc = 0;
+#pragma unroll
+    for (int w = 0; w < kRedGroups; ++w) acc += ipart[w][lane];
+    v = (float)((double)acc / a.dscale[l * 6 + (t == 0 ? 2 : (t == 1 ? 4 : 5))]);
+  } else {
+#pragma unroll
+    for (int w = 0; w < kRedGroups; ++w) v += part[w][lane];
+  }
+  if (v == 0.f) return;
   const int loc = e - a.toff[l][t], i = loc >> 5, c = loc & 31, rb = a.rb[l][t];
   float* gp = a.gp[l][t];
   gp[(i * rb + a.tj0[l]) * 32 + c] += v * (1.f - a.tfb[l]);
   gp[(i * rb + a.tj0[l] + 1) * 32 + c] += v * a.tfb[l];
+}
+
+// ---------------------------------------------------------------------------
+// deterministic mode: fixed-point scale per plane and the conversion back
+// ---------------------------------------------------------------------------
+// out[slot] = max |x| over a [rows, stride] block's columns [col0, col0+ncols)
+// (non-negative floats order as their bit patterns: an integer atomicMax,
+// independent of the order)
+__global__ void k_det_maxabs(const float* __restrict__ x, int64_t rows, int stride, int col0, int ncols,
+                             unsigned int* __restrict__ out) {
+  float m = 0.f;
+  const int64_t n = rows * ncols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float v = fabsf(x[(e / ncols) * stride + col0 + e % ncols]);
+    m = v > m ? v : m;  // NaN-safe: comparisons with NaN are false
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+// Plane (l, q): every Gaussian's coefficient is dlat * (product of the other
+// five interpolated planes), each interpolation a convex combination of the
+// plane's values, so the L1 mass the plane can receive is at most
+// B = K * C * max|dlat_l| * prod_{q' != q} max|plane_{l,q'}|.  With
+// scale = 2^(62 - ceil(log2 B)) every partial sum fits in int64 and the
+// rounding unit is ~B * 2^-62.
+__global__ void k_det_scales(const unsigned int* __restrict__ maxima, int levels, int64_t K, int C,
+                             double* __restrict__ scale) {
+  const int i = threadIdx.x;
+  if (i >= levels * 6) return;
+  const int l = i / 6, q = i % 6;
+  double b = (double)K * C * (double)__uint_as_float(maxima[l]);
+  for (int r = 0; r < 6; ++r)
+    if (r != q) b *= (double)__uint_as_float(maxima[levels + l * 6 + r]);
+  int e = 0;
+  if (b > 0.0 && isfinite(b)) {
+    frexp(b, &e);  // b <= 2^e
+    scale[i] = ldexp(1.0, 62 - e);
+  } else {
+    scale[i] = 1.0;
+  }
+}
+
+struct DetConvArgs {
+  const unsigned long long* acc[FS4D_MAX_LEVELS * 6];
+  float* dst[FS4D_MAX_LEVELS * 6];
+  int64_t n[FS4D_MAX_LEVELS * 6];
+  int64_t block_start[FS4D_MAX_LEVELS * 6 + 1];
+  int nplanes;
+  const double* scale;
+  int scale_idx[FS4D_MAX_LEVELS * 6];
+};
+
+// dst[i] += acc[i] / scale, plane by plane (block ranges per plane)
+__global__ void k_det_to_float(const __grid_constant__ DetConvArgs a) {
+  int pl = 0;
+  while (pl + 1 < a.nplanes && a.block_start[pl + 1] <= (int64_t)blockIdx.x) ++pl;
+  const int64_t i = ((int64_t)blockIdx.x - a.block_start[pl]) * blockDim.x + threadIdx.x;
+  if (i >= a.n[pl]) return;
+  const long long v = (long long)a.acc[pl][i];
+  if (v) a.dst[pl][i] += (float)((double)v / a.scale[a.scale_idx[pl]]);
 }
 
 // ---------------------------------------------------------------------------
@@ -769,6 +891,7 @@ int hexplane_query_backward(const Fs4dHexPlane& f, const float* pos, int64_t K, 
     }
   if (K == 0) return FS4D_OK;
   HexBwdArgs h;
+  memset(&h, 0, sizeof(h));
   h.p = p;
   h.K = K;
   h.pos = pos;
@@ -778,13 +901,31 @@ int hexplane_query_backward(const Fs4dHexPlane& f, const float* pos, int64_t K, 
   for (int l = 0; l < FS4D_MAX_LEVELS; ++l)
     for (int q = 0; q < 6; ++q) h.gplanes[l][q] = l < f.levels ? g.planes[l][q] : nullptr;
   h.accumulate = accumulate;
-  k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
+  k_hexplane_bwd<false><<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
   return check_launch("hexplane_query_backward");
+}
+
+static inline size_t det_align(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// deterministic-mode scratch of deform_backward_tc: maxima, scales, the int64
+// plane accumulators and the int64 per-CTA time partials
+size_t deform_bwd_det_bytes(const Fs4dHexPlane& f) {
+  size_t o = 256 + 512;  // maxima (u32) + scales (double)
+  int64_t tf = 0;        // time-plane partial floats of the 32-channel, 2-level kernel
+  for (int l = 0; l < f.levels; ++l)
+    for (int q = 0; q < 6; ++q) {
+      o += det_align((size_t)f.res[l][q][0] * f.res[l][q][1] * f.channels * 8, 256);
+      if (f.levels == 2 && f.channels == 32 && (q == 2 || q == 4 || q == 5)) tf += (int64_t)f.res[l][q][0] * 32;
+    }
+  return o + (size_t)kNumSMs * FS4D_HEX_BWD_MINB * (size_t)tf * 8;
 }
 
 int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
                        const uint8_t* cache, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
-                       Fs4dHexPlane* pg, int accumulate, void* ws, int32_t* status, cudaStream_t s) {
+                       Fs4dHexPlane* pg, int accumulate, void* ws, int32_t* status, void* det_ws,
+                       size_t det_bytes, cudaStream_t s) {
+  if (det_ws && det_bytes < deform_bwd_det_bytes(field))
+    return fail(FS4D_ERR_CONFIG, "deterministic deform workspace too small");
   TcPlan p;
   uint8_t* blob = (uint8_t*)ws;
   int rc = tc_pack(net, field, t, p, blob, s);
@@ -815,6 +956,7 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
     k_mlp_bwd_tc<<<grid, kBwdThreads, smem, s>>>(a);
 
     HexBwdArgs h;
+    memset(&h, 0, sizeof(h));
     h.p = p;
     h.K = K;
     h.pos = cloud.positions;
@@ -824,8 +966,40 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
     for (int l = 0; l < FS4D_MAX_LEVELS; ++l)
       for (int q = 0; q < 6; ++q) h.gplanes[l][q] = l < field.levels ? pg->planes[l][q] : nullptr;
     h.accumulate = accumulate;
+    const bool det = det_ws != nullptr;
+    unsigned long long* det_tpart = nullptr;
+    DetConvArgs dconv;
+    int64_t dblocks = 0;
+    if (det) {
+      // bounds -> scales -> zeroed int64 accumulators (all stream-ordered)
+      char* d = (char*)det_ws;
+      unsigned int* maxima = (unsigned int*)d;
+      double* scales = (double*)(d + 256);
+      cudaMemsetAsync(maxima, 0, 256, s);
+      for (int l = 0; l < p.levels; ++l) {
+        k_det_maxabs<<<kNumSMs * 2, 256, 0, s>>>(dlat, K, 64, l * p.C, p.C, maxima + l);
+        for (int q = 0; q < 6; ++q)
+          k_det_maxabs<<<kNumSMs, 256, 0, s>>>(field.planes[l][q], (int64_t)p.res[l][q][0] * p.res[l][q][1], p.C,
+                                                0, p.C, maxima + p.levels + l * 6 + q);
+      }
+      k_det_scales<<<1, 64, 0, s>>>(maxima, p.levels, K, p.C, scales);
+      h.dscale = scales;
+      size_t o = 256 + 512;
+      memset(&dconv, 0, sizeof(dconv));
+      dconv.scale = scales;
+      for (int l = 0; l < p.levels; ++l)
+        for (int q = 0; q < 6; ++q) {
+          const int64_t n = (int64_t)p.res[l][q][0] * p.res[l][q][1] * p.C;
+          h.dacc[l][q] = (unsigned long long*)(d + o);
+          o += det_align((size_t)n * 8, 256);
+          cudaMemsetAsync(h.dacc[l][q], 0, (size_t)n * 8, s);
+        }
+      det_tpart = (unsigned long long*)(d + o);
+      (void)dblocks;
+    }
     HexC32Args hc;
     hc.h = h;
+    hc.tpart_i = det_tpart;
     hc.rows = p.rows_ok && !getenv("FS4D_NO_TIME_ROWS") ? reinterpret_cast<const float*>(blob + p.off_rows) : nullptr;
     int tf = 0;
     for (int l = 0; l < 2 && p.levels == 2; ++l)
@@ -839,10 +1013,17 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
       const int64_t nblk = ceil_div(ceil_div(K, 32), kHexC32Warps);
       const int nres = kNumSMs * FS4D_HEX_BWD_MINB;  // resident 256-thread CTAs
       const int grid = (int)(nblk < nres ? nblk : nres);
-      cudaMemsetAsync(hc.tpart, 0, (size_t)grid * tf * 4, s);
-      k_hexplane_bwd_c32<<<grid, kHexC32Warps * 32, 0, s>>>(hc);
+      if (det) {
+        cudaMemsetAsync(hc.tpart_i, 0, (size_t)grid * tf * 8, s);
+        k_hexplane_bwd_c32<true><<<grid, kHexC32Warps * 32, 0, s>>>(hc);
+      } else {
+        cudaMemsetAsync(hc.tpart, 0, (size_t)grid * tf * 4, s);
+        k_hexplane_bwd_c32<false><<<grid, kHexC32Warps * 32, 0, s>>>(hc);
+      }
       TimeReduceArgs tr;
       tr.tpart = hc.tpart;
+      tr.tpart_i = det ? hc.tpart_i : nullptr;
+      tr.dscale = h.dscale;
       tr.nparts = grid;
       tr.tfloats = tf;
       for (int l = 0; l < 2; ++l) {
@@ -861,8 +1042,41 @@ int deform_backward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const 
         }
       }
       k_time_partials<<<(unsigned)ceil_div(tf, 32), 32 * kRedGroups, 0, s>>>(tr);
+      if (det) {  // spatial planes: int64 -> fp32 (the time planes went through k_time_partials)
+        int np = 0;
+        for (int l = 0; l < 2; ++l)
+          for (int q = 0; q < 6; ++q) {
+            if (is_time_plane(q)) continue;
+            dconv.acc[np] = h.dacc[l][q];
+            dconv.dst[np] = h.gplanes[l][q];
+            dconv.n[np] = (int64_t)p.res[l][q][0] * p.res[l][q][1] * 32;
+            dconv.scale_idx[np] = l * 6 + q;
+            dconv.block_start[np] = dblocks;
+            dblocks += ceil_div(dconv.n[np], 256);
+            ++np;
+          }
+        dconv.block_start[np] = dblocks;
+        dconv.nplanes = np;
+        k_det_to_float<<<(unsigned)dblocks, 256, 0, s>>>(dconv);
+      }
+    } else if (det) {
+      k_hexplane_bwd<true><<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
+      int np = 0;
+      for (int l = 0; l < p.levels; ++l)
+        for (int q = 0; q < 6; ++q) {
+          dconv.acc[np] = h.dacc[l][q];
+          dconv.dst[np] = h.gplanes[l][q];
+          dconv.n[np] = (int64_t)p.res[l][q][0] * p.res[l][q][1] * p.C;
+          dconv.scale_idx[np] = l * 6 + q;
+          dconv.block_start[np] = dblocks;
+          dblocks += ceil_div(dconv.n[np], 256);
+          ++np;
+        }
+      dconv.block_start[np] = dblocks;
+      dconv.nplanes = np;
+      k_det_to_float<<<(unsigned)dblocks, 256, 0, s>>>(dconv);
     } else {
-      k_hexplane_bwd<<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
+      k_hexplane_bwd<false><<<(unsigned)ceil_div(K, kHexBwdWarps), kHexBwdWarps * 32, 0, s>>>(h);
     }
   }
   DwReduceArgs r;

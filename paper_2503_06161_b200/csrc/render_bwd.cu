@@ -9,6 +9,7 @@
 #include <stdlib.h>
 
 #include "render_common.cuh"
+#include "scan_sort.cuh"
 #include "sh.cuh"
 
 namespace fs4d {
@@ -32,6 +33,7 @@ struct BwdArgs {
   const float* dF;
   const float* dA;
   float* accum;
+  float* part;  // deterministic mode: per (pair, row-split CTA) partial sums [cap][SUBB][nvals]
 };
 
 // Reduce v[0..31] over the warp; afterwards lane L holds the warp sum of v[L].
@@ -264,11 +266,17 @@ __device__ __forceinline__ int ty_sub_rows(int sub) { return sub * (kTile / SUBB
 // SUBB > 1 splits a tile's rows over SUBB CTAs (each replays the whole list
 // for its 16/SUBB rows): CTAs of one or two warps have no cross-warp batch
 // barrier to wait on, and more of them fit per SM.
-template <int DC, int PX, int SUBB>
+// DET: instead of red.global.add, every warp leaves its per-Gaussian sums in
+// shared memory, the CTA adds its warps in a fixed order at the end of each
+// staged batch and stores one partial per (pair, CTA) -- k_det_gather then
+// sums a Gaussian's partials in tile order: bitwise reproducible gradients.
+template <int DC, int PX, int SUBB, bool DET = false>
 __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs a) {
   constexpr int NT = kTilePixels / PX / SUBB;
   constexpr int B = NT;  // Gaussians staged per batch
   constexpr int NF = DC > 0 ? DC : 1;
+  constexpr int NVMAX = 10 + NF;
+  __shared__ float s_acc[DET ? (NT / 32) * B * NVMAX : 1];
   __shared__ float2 s_xy[B];
   __shared__ float4 s_co[B];
   __shared__ float4 s_cs[B];  // scaled conic (gauss_power), same evaluation as the forward
@@ -334,13 +342,20 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
   atomicMax(&s_maxlast, mylast);
   __syncthreads();
   const int maxlast = s_maxlast;
+  const int nv = a.nvals;
+  const uint32_t hi = (uint32_t)(maxlast + 1) < rg.y ? (uint32_t)(maxlast + 1) : rg.y;
+  const int sidx = blockIdx.x % SUBB;
+  if (DET) {  // pairs this CTA never stages (behind every pixel's last contributor): zero partials
+    const uint32_t z0 = maxlast < (int)rg.x ? rg.x : hi;
+    for (int64_t e = threadIdx.x; e < (int64_t)(rg.y - z0) * nv; e += NT)
+      a.part[((int64_t)(z0 + e / nv) * SUBB + sidx) * nv + e % nv] = 0.f;
+  }
   if (maxlast < (int)rg.x) return;
   const int wlast = __reduce_max_sync(0xffffffffu, mylast);
   const int wrow0 = ty * kTile + rsub + (threadIdx.x >> 5) * 2 * PX;  // this warp's 2*PX pixel rows
   const int tcol0 = tx * kTile;
+  float* wacc = DET ? s_acc + (threadIdx.x >> 5) * B * NVMAX : nullptr;
 
-  const int nv = a.nvals;
-  const uint32_t hi = (uint32_t)(maxlast + 1) < rg.y ? (uint32_t)(maxlast + 1) : rg.y;
   for (int64_t bend = hi; bend > (int64_t)rg.x; bend -= B) {
     const int64_t bstart = bend - B > (int64_t)rg.x ? bend - B : (int64_t)rg.x;
     const int cnt = (int)(bend - bstart);
@@ -361,6 +376,8 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
       }
     }
     __syncthreads();
+    if (DET)
+      for (int e = lane; e < cnt * NVMAX; e += 32) wacc[e] = 0.f;
 #pragma unroll 1
     for (int m = (cnt - 1) / 32; m >= 0; --m) {
       unsigned bits;
@@ -434,12 +451,73 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
           v[9] += -2.f * dq * (co.y * dx + co.z * dy);
         }
         if (!__any_sync(0xffffffffu, any)) continue;
-        float* dst = a.accum + (int64_t)s_g[k] * a.acc_stride;
         const float r = warp_smem_reduce<NROW>(v, wred, lane);
-        if (lane < nv && r != 0.f) red_add(dst + lane, r);
+        if (DET) {
+          if (lane < nv) wacc[k * NVMAX + lane] = r;
+        } else {
+          float* dst = a.accum + (int64_t)s_g[k] * a.acc_stride;
+          if (lane < nv && r != 0.f) red_add(dst + lane, r);
+        }
+      }
+    }
+    if (DET) {  // this batch's partials: warps added in index order, one store per (pair, CTA)
+      __syncthreads();
+      for (int e = threadIdx.x; e < cnt * nv; e += NT) {
+        const int k = e / nv, q = e - k * nv;
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) sum += s_acc[(w * B + k) * NVMAX + q];
+        a.part[((bstart + k) * SUBB + sidx) * nv + q] = sum;
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// deterministic mode: per-Gaussian pair slots and the ordered gather
+// ---------------------------------------------------------------------------
+__global__ void k_det_counts(const int4* __restrict__ tile_rect, int64_t K, uint32_t* __restrict__ cnt) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= K) return;
+  const int4 r = tile_rect[g];
+  cnt[g] = (r.y >= r.x && r.w >= r.z) ? (uint32_t)((r.y - r.x + 1) * (r.w - r.z + 1)) : 0u;
+}
+
+// slot[pfx[g] + i] = the pair index of Gaussian g in the i-th tile of its
+// rectangle (row-major): one CTA per tile walks the tile's list
+__global__ void k_det_slots(const uint2* __restrict__ ranges, const uint32_t* __restrict__ pvals, int ntx,
+                            const int4* __restrict__ tile_rect, const uint64_t* __restrict__ pfx, int64_t cap,
+                            uint32_t* __restrict__ slot) {
+  const int t = blockIdx.x;
+  const uint2 rg = ranges[t];
+  const int tx = t % ntx, ty = t / ntx;
+  for (uint32_t j = rg.x + threadIdx.x; j < rg.y; j += blockDim.x) {
+    const uint32_t g = pvals[j];
+    const int4 r = tile_rect[g];
+    const uint64_t q = pfx[g] + (uint64_t)((ty - r.z) * (r.y - r.x + 1) + (tx - r.x));
+    if (q < (uint64_t)cap) slot[q] = j;  // (an overflowed frame is reported by the forward's status)
+  }
+}
+
+// accum[g] = sum over g's tiles (row-major), then over the row-split CTAs, of
+// the partials -- a fixed order; one warp per Gaussian, lane = value
+__global__ void k_det_gather(const int4* __restrict__ tile_rect, int64_t K, const uint64_t* __restrict__ pfx,
+                             const uint32_t* __restrict__ slot, const float* __restrict__ part, int subb, int nv,
+                             int acc_stride, int64_t cap, float* __restrict__ accum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= K) return;
+  const int4 r = tile_rect[g];
+  if (!(r.y >= r.x && r.w >= r.z)) return;
+  const int n = (r.y - r.x + 1) * (r.w - r.z + 1);
+  const uint64_t b = pfx[g];
+  float acc = 0.f;
+  for (int i = 0; i < n && b + i < (uint64_t)cap; ++i) {
+    const uint32_t j = slot[b + i];
+    if (lane < nv && j < (uint64_t)cap)
+      for (int sidx = 0; sidx < subb; ++sidx) acc += part[((int64_t)j * subb + sidx) * nv + lane];
+  }
+  if (lane < nv) accum[g * acc_stride + lane] = acc;
 }
 
 struct PreBwdArgs {
@@ -689,6 +767,37 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdArgs a) {
   }
 }
 
+static int blend_bwd_subb() {
+  static const int subb = [] {
+    const char* e = getenv("FS4D_BLEND_BWD_SUB");
+    const int v = e ? atoi(e) : 2;  // measured (configs[4]): 1 -> 285 us, 2 -> 275 us, 4 -> 307 us
+    return v == 1 || v == 4 ? v : 2;
+  }();
+  return subb;
+}
+
+// the deterministic variant keeps a [warps][B][values] shared tile of warp
+// sums, which fits for 2 or 4 row-split CTAs per tile (not 1)
+static int det_subb() { return blend_bwd_subb() == 4 ? 4 : 2; }
+
+static void launch_blend_bwd_det(int dc, int ntiles, const BwdArgs& a, cudaStream_t s) {
+#define FS4D_BWD2D(D, SB) k_blend_bwd2<D, 2, SB, true><<<ntiles * SB, kTilePixels / 2 / SB, 0, s>>>(a)
+#define FS4D_BWD2D_DC(SB)             \
+  switch (dc) {                       \
+    case 0: FS4D_BWD2D(0, SB); break;  \
+    case 4: FS4D_BWD2D(4, SB); break;  \
+    case 8: FS4D_BWD2D(8, SB); break;  \
+    default: FS4D_BWD2D(16, SB); break; \
+  }
+  if (det_subb() == 4) {
+    FS4D_BWD2D_DC(4)
+  } else {
+    FS4D_BWD2D_DC(2)
+  }
+#undef FS4D_BWD2D_DC
+#undef FS4D_BWD2D
+}
+
 static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t s) {
   // pixels per thread of the replay (FS4D_BLEND_BWD_PX = 1, 2 or 4)
   static const int px = [] {
@@ -707,11 +816,7 @@ static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t 
     }
   } else if (px == 2) {
     // CTAs per tile (FS4D_BLEND_BWD_SUB = 1, 2 or 4)
-    static const int subb = [] {
-      const char* e = getenv("FS4D_BLEND_BWD_SUB");
-      const int v = e ? atoi(e) : 2;  // measured (configs[4]): 1 -> 285 us, 2 -> 275 us, 4 -> 307 us
-      return v == 1 || v == 4 ? v : 2;
-    }();
+    const int subb = blend_bwd_subb();
 #define FS4D_BWD2(D, SB) k_blend_bwd2<D, 2, SB><<<ntiles * SB, kTilePixels / 2 / SB, 0, s>>>(a)
 #define FS4D_BWD2_DC(SB)            \
   switch (dc) {                     \
@@ -739,11 +844,27 @@ static void launch_blend_bwd(int dc, int ntiles, const BwdArgs& a, cudaStream_t 
   }
 }
 
+// deterministic-mode scratch: partials, per-Gaussian slots and offsets
+size_t render_bwd_det_bytes(const RenderLayout& L) {
+  const int64_t K = L.K > 0 ? L.K : 1, cap = L.cap > 0 ? L.cap : 1;
+  const int nv = 10 + (L.D > 16 ? 16 : L.D);
+  size_t o = 0;
+  o = align_up(o + (size_t)cap * 4 /*subb*/ * nv * 4, 256);  // part (up to 4 row-split CTAs)
+  o = align_up(o + (size_t)cap * 4, 256);                     // slot
+  o = align_up(o + (size_t)K * 4, 256);                       // counts
+  o = align_up(o + (size_t)K * 8, 256);                       // offsets
+  return o + scan_scratch_bytes(K);
+}
+
 int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRasterConfig& cfg,
                     const RenderLayout& L, void* ws, const Fs4dImageGrads& up, Fs4dCloud& grads,
-                    int32_t* vs_index, float* vs_norm, cudaStream_t s) {
+                    int32_t* vs_index, float* vs_norm, void* det_ws, size_t det_bytes, cudaStream_t s) {
   const int64_t K = L.K;
   const int D = cfg.with_features ? L.D : 0;
+  if (det_ws) {
+    if (D > 16) return fail(FS4D_ERR_CONFIG, "the deterministic backward supports D <= 16 feature channels");
+    if (det_bytes < render_bwd_det_bytes(L)) return fail(FS4D_ERR_CONFIG, "deterministic workspace too small");
+  }
   float* accum = at<float>(ws, L.accum);
   cudaMemsetAsync(accum, 0, (size_t)K * L.acc_stride * 4, s);
   // Viewspace outputs requested: visit the visible rows in depth order (the
@@ -791,8 +912,32 @@ int render_backward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRast
   b.dF = D > 0 ? up.d_feature : nullptr;
   b.dA = up.d_alpha;
   b.accum = accum;
+  b.part = nullptr;
   int dc = D <= 0 ? 0 : D <= 4 ? 4 : D <= 8 ? 8 : D <= 16 ? 16 : D <= 32 ? 32 : 64;
-  if (L.ntiles > 0) {
+  if (L.ntiles > 0 && det_ws) {
+    StageTimer st(FS4D_STAGE_BLEND_BWD, s);
+    const int64_t cap = L.cap > 0 ? L.cap : 1;
+    char* d = (char*)det_ws;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+      void* at_ = d + o;
+      o = align_up(o + bytes, 256);
+      return at_;
+    };
+    b.part = (float*)take((size_t)cap * 4 * b.nvals * 4);
+    uint32_t* slot = (uint32_t*)take((size_t)cap * 4);
+    uint32_t* cnt = (uint32_t*)take((size_t)(K > 0 ? K : 1) * 4);
+    uint64_t* pfx = (uint64_t*)take((size_t)(K > 0 ? K : 1) * 8);
+    launch_blend_bwd_det(dc, L.ntiles, b, s);
+    if (K > 0) {
+      k_det_counts<<<(unsigned)ceil_div(K, 256), 256, 0, s>>>(at<int4>(ws, L.tile_rect), K, cnt);
+      exclusive_scan_u32_to_u64(cnt, pfx, K, nullptr, nullptr, d + o, s);
+      k_det_slots<<<L.ntiles, 256, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.pvals0), L.ntx,
+                                           at<int4>(ws, L.tile_rect), pfx, cap, slot);
+      k_det_gather<<<(unsigned)ceil_div(K, 8), 256, 0, s>>>(at<int4>(ws, L.tile_rect), K, pfx, slot, b.part,
+                                                            det_subb(), b.nvals, L.acc_stride, cap, accum);
+    }
+  } else if (L.ntiles > 0) {
     StageTimer st(FS4D_STAGE_BLEND_BWD, s);
     launch_blend_bwd(dc, L.ntiles, b, s);
   }

@@ -332,6 +332,62 @@ int adam_step(float* p, const float* g, float* m, float* v, int32_t* steps, cons
 }
 
 // ===========================================================================
+// dst = src[0] + src[1] + ... (fixed order): the training step's per-lane
+// gradient buffers summed in one pass (instead of one read-modify-write of
+// dst per lane)
+// ===========================================================================
+constexpr int kMaxSumSrc = 8;
+struct SumArgs {
+  const float* src[kMaxSumSrc];
+  int nsrc;
+  float* dst;
+  int64_t n;
+  int accumulate;
+};
+
+__global__ void __launch_bounds__(kThreads) k_sum_buffers(SumArgs a) {
+  const int64_t n4 = a.n >> 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(a.dst)) & 15) == 0;
+  bool svec = vec;
+  for (int j = 0; j < a.nsrc; ++j) svec = svec && ((reinterpret_cast<uintptr_t>(a.src[j]) & 15) == 0);
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  int64_t tail0 = 0;
+  if (svec) {
+    for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += stride) {
+      float4 acc = a.accumulate ? reinterpret_cast<const float4*>(a.dst)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < a.nsrc; ++j) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(a.src[j]) + q);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      reinterpret_cast<float4*>(a.dst)[q] = acc;
+    }
+    tail0 = n4 << 2;
+  }
+  for (int64_t i = tail0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; i < a.n; i += stride) {
+    float acc = a.accumulate ? a.dst[i] : 0.f;
+    for (int j = 0; j < a.nsrc; ++j) acc += a.src[j][i];
+    a.dst[i] = acc;
+  }
+}
+
+int sum_buffers(float* dst, const float* const* src, int nsrc, int64_t n, int accumulate, cudaStream_t s) {
+  if (nsrc < 0 || nsrc > kMaxSumSrc) return fail(FS4D_ERR_CONFIG, "sum_buffers: 0..8 sources");
+  if (n <= 0) return FS4D_OK;
+  SumArgs a;
+  for (int j = 0; j < nsrc; ++j) a.src[j] = src[j];
+  a.nsrc = nsrc;
+  a.dst = dst;
+  a.n = n;
+  a.accumulate = accumulate;
+  const int64_t blocks = std::min<int64_t>(ceil_div(ceil_div(n, 4), kThreads), kNumSMs * 8);
+  k_sum_buffers<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  return check_launch("sum_buffers");
+}
+
+// ===========================================================================
 // HexPlane total variation (hexplane.py:190-222)
 // ===========================================================================
 constexpr int kTvChunk = kThreads * 4;

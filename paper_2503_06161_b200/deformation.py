@@ -152,9 +152,11 @@ def _deform(cloud, field, net, t, want_cache):
     return snapshot, cache
 
 
-def deform_backward(cloud, field, net, cache, grads):
+def deform_backward(cloud, field, net, cache, grads, *, deterministic=False):
     """Pull snapshot gradients back to the cloud, the net and the grid
-    (deformation.py:139-183).  ``grads`` is duck-typed like the reference."""
+    (deformation.py:139-183).  ``grads`` is duck-typed like the reference.
+    deterministic=True (extension): fixed-point plane scatter, bitwise
+    reproducible (fs4d_deform_bwd_deterministic)."""
     import torch
     from .device import DeviceCloud
 
@@ -172,7 +174,8 @@ def deform_backward(cloud, field, net, cache, grads):
     feats = up("features", (k, d)) if net.cfg.enable_feature_update else torch.zeros(k, d, **f32)
     sg = DeviceCloud(up("positions", (k, 3)), up("rotations", (k, 4)), up("log_scales", (k, 3)),
                      up("opacity_logits", (k,)), torch.zeros(k, 3, **f32), feats)
-    gpos, ngrads, pgrads = _engine().backward(dc, df, dn, cache["t"], sg, cache=cache.get("device"))
+    gpos, ngrads, pgrads = _engine().backward(dc, df, dn, cache["t"], sg, cache=cache.get("device"),
+                                              deterministic=deterministic)
 
     cloud_grads = {
         "positions": _host(gpos).reshape(k, 3),

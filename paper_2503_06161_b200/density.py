@@ -51,14 +51,19 @@ class ViewspaceGradStats:
         return cls(accum=torch.zeros(k, **f), count=torch.zeros(k, **f))
 
     def add(self, indices, norms, n_dev=None):
-        if isinstance(self.accum, torch.Tensor):
-            idx = torch.as_tensor(indices, device=self.accum.device).to(torch.int32).contiguous()
-            nrm = torch.as_tensor(norms, device=self.accum.device).to(torch.float32).contiguous()
-            N.check(N.load().fs4d_grad_stats_add(_p(self.accum), _p(self.count), _p(idx), _p(nrm), idx.numel(),
-                                                 _p(n_dev), _stream()))
-        else:
-            np.add.at(self.accum, indices, norms)
-            np.add.at(self.count, indices, 1.0)
+        """accum[indices] += norms, count[indices] += 1 on the device
+        (fs4d_grad_stats_add); host (NumPy) statistics are staged through the
+        device and written back, so both forms run the same kernel."""
+        host = not isinstance(self.accum, torch.Tensor)
+        accum = torch.as_tensor(np.asarray(self.accum, np.float64), device="cuda") if host else self.accum
+        count = torch.as_tensor(np.asarray(self.count, np.float64), device="cuda") if host else self.count
+        idx = torch.as_tensor(np.asarray(indices) if host else indices, device=accum.device).to(torch.int32).contiguous()
+        nrm = torch.as_tensor(np.asarray(norms) if host else norms, device=accum.device).to(torch.float32).contiguous()
+        N.check(N.load().fs4d_grad_stats_add(_p(accum), _p(count), _p(idx), _p(nrm), idx.numel(), _p(n_dev),
+                                             _stream()))
+        if host:
+            self.accum = accum.cpu().numpy()
+            self.count = count.cpu().numpy()
 
     def add_dense(self, norms):
         """Accumulate render_backward's dense per-Gaussian norms (negative =

@@ -329,12 +329,13 @@ class DeformEngine:
         return (out, cache) if cache is not None else out
 
     def backward(self, cloud, field, net, t, snap_grads, cloud_grads=None, net_grads=None,
-                 plane_grads=None, accumulate=False, cache=None):
+                 plane_grads=None, accumulate=False, cache=None, deterministic=False):
         """deform_backward on device.  Without output buffers: returns
         (d_positions [K,3], net_grads DeviceNet, plane_grads DeviceField|None).
         With a DeviceCloud `cloud_grads` (+ net/plane grads) every cloud
         gradient is written (or added, accumulate=True) and the buffers are
-        returned."""
+        returned.  deterministic=True: fs4d_deform_bwd_deterministic
+        (fixed-point plane scatter, bitwise reproducible; needs `cache`)."""
         k = len(cloud)
         ngrads = net_grads if net_grads is not None else net.zeros_like()
         pgrads = plane_grads if plane_grads is not None else (field.zeros_like() if net.enable_grid else None)
@@ -353,11 +354,24 @@ class DeformEngine:
         if cache is not None and (cache.k != k or cache.t != float(t)):
             raise ContractViolation("deform cache was made for another (cloud, t)")
         cptr, cbytes = (cache.ptr(), cache.nbytes) if cache is not None else (None, 0)
-        N.check(N.load().fs4d_deform_bwd(ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns),
-                                         float(t), cptr, cbytes, ctypes.byref(sgs), ctypes.byref(cgs),
-                                         ctypes.byref(ngs),
-                                         ctypes.byref(pgs) if pgs is not None else None,
-                                         int(bool(accumulate)), _p(ws), ws.numel(), None, _stream()))
+        if deterministic:
+            lib = N.load()
+            need = int(lib.fs4d_deform_bwd_det_workspace_bytes(ctypes.byref(ns), ctypes.byref(fs)))
+            if need == 0:
+                raise ConfigurationError("the deterministic deform backward needs the tensor-core path (width 64, "
+                                         "depth 1, levels * channels = 64, feature_dim <= 16)")
+            if getattr(self, "det_ws", None) is None or self.det_ws.numel() < need:
+                self.det_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            N.check(lib.fs4d_deform_bwd_deterministic(
+                ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns), float(t), cptr, cbytes, ctypes.byref(sgs),
+                ctypes.byref(cgs), ctypes.byref(ngs), ctypes.byref(pgs) if pgs is not None else None,
+                int(bool(accumulate)), _p(ws), ws.numel(), _p(self.det_ws), self.det_ws.numel(), None, _stream()))
+        else:
+            N.check(N.load().fs4d_deform_bwd(ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns),
+                                             float(t), cptr, cbytes, ctypes.byref(sgs), ctypes.byref(cgs),
+                                             ctypes.byref(ngs),
+                                             ctypes.byref(pgs) if pgs is not None else None,
+                                             int(bool(accumulate)), _p(ws), ws.numel(), None, _stream()))
         return (cloud_grads if cloud_grads is not None else gpos), ngrads, pgrads
 
 
@@ -447,7 +461,7 @@ class Renderer:
         return images, rec
 
     def backward(self, cloud, K, T, height, width, cfg, rec, d_color=None, d_depth=None,
-                 d_feature=None, d_alpha=None, grads=None, viewspace=True):
+                 d_feature=None, d_alpha=None, grads=None, viewspace=True, deterministic=False):
         """render_backward on device.  viewspace=True: depth-ordered
         (index, norm) pairs like SnapshotGrads; False: none (and no global
         depth sort); "dense": norms per Gaussian ([K], -1 for culled, no depth
@@ -466,10 +480,20 @@ class Renderer:
         up = N.ImageGrads()
         up.d_color, up.d_depth = _p(d_color), _p(d_depth)
         up.d_feature, up.d_alpha = _p(d_feature), _p(d_alpha)
-        N.check(N.load().fs4d_render_bwd(ctypes.byref(cs), ctypes.byref(cam), ctypes.byref(rc),
-                                         ctypes.byref(rec.info), _p(rec.ws), rec.ws.numel(),
-                                         ctypes.byref(up), ctypes.byref(gs), _p(vs_index),
-                                         _p(vs_norm), None, _stream()))
+        if deterministic:  # fs4d_render_bwd_deterministic: ordered partials, no float atomics
+            lib = N.load()
+            need = max(int(lib.fs4d_render_bwd_det_workspace_bytes(ctypes.byref(rec.info))), 1)
+            if getattr(self, "det_ws", None) is None or self.det_ws.numel() < need:
+                self.det_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            N.check(lib.fs4d_render_bwd_deterministic(ctypes.byref(cs), ctypes.byref(cam), ctypes.byref(rc),
+                                                      ctypes.byref(rec.info), _p(rec.ws), rec.ws.numel(),
+                                                      ctypes.byref(up), ctypes.byref(gs), _p(vs_index), _p(vs_norm),
+                                                      _p(self.det_ws), self.det_ws.numel(), None, _stream()))
+        else:
+            N.check(N.load().fs4d_render_bwd(ctypes.byref(cs), ctypes.byref(cam), ctypes.byref(rc),
+                                             ctypes.byref(rec.info), _p(rec.ws), rec.ws.numel(),
+                                             ctypes.byref(up), ctypes.byref(gs), _p(vs_index),
+                                             _p(vs_norm), None, _stream()))
         if dense:
             return grads, None, vs_norm
         return grads, vs_index, vs_norm

@@ -311,8 +311,10 @@ def render(snapshot, frame, cfg):
 
 
 def render_backward(snapshot, frame, out, dL_dcolor=None, dL_ddepth=None, dL_dfeature=None,
-                    dL_dalpha=None):
-    """Gradients for every raw snapshot parameter (rasterizer.py:320-452)."""
+                    dL_dalpha=None, *, deterministic=False):
+    """Gradients for every raw snapshot parameter (rasterizer.py:320-452).
+    deterministic=True (extension): fixed-order reduction instead of float
+    atomics, bitwise reproducible (fs4d_render_bwd_deterministic)."""
     import torch
     from .device import DeviceCloud
 
@@ -333,7 +335,8 @@ def render_backward(snapshot, frame, out, dL_dcolor=None, dL_ddepth=None, dL_dfe
     grads, vs_index, vs_norm = rec.renderer.backward(
         dc, frame.K, frame.T, h, w, rec.cfg, rec.device,
         d_color=up(dL_dcolor, (h, w, 3)), d_depth=up(dL_ddepth, (h, w)),
-        d_feature=up(dL_dfeature, (h, w, n)) if n else None, d_alpha=up(dL_dalpha, (h, w)))
+        d_feature=up(dL_dfeature, (h, w, n)) if n else None, d_alpha=up(dL_dalpha, (h, w)),
+        deterministic=deterministic)
     k = len(snapshot)
     m = rec.device.n_visible
     sh = getattr(snapshot, "sh_rest", None)

@@ -66,7 +66,7 @@ def _net_layer_specs(net):
 class TrainStep:
     def __init__(self, cloud, field, net, height, width, cfg, world=1, group=None, device="cuda",
                  loss_mode="raw", lambda_rgb=1.0, lambda_depth=0.0, lambda_feat=1.0, lambda_tv=0.0,
-                 decoder=None, locality=None, lanes=None):
+                 decoder=None, locality=None, lanes=None, deterministic=False):
         self.cloud, self.field, self.net = cloud, field, net
         self.h, self.w, self.cfg = int(height), int(width), cfg
         self.world, self.group = int(world), group
@@ -74,6 +74,10 @@ class TrainStep:
         if loss_mode not in ("raw", "decoder"):
             raise ValueError(f"unknown loss mode {loss_mode!r}")
         self.loss_mode = loss_mode
+        # bitwise reproducible steps: ordered blend-backward partials, fixed-
+        # point plane scatter, one loss scalar per lane summed in lane order
+        # (the reference's resume test, test_training.py:282-299)
+        self.deterministic = bool(deterministic)
         self.locality = (os.environ.get("FS4D_TRAIN_LOCALITY", "0") == "1") if locality is None else bool(locality)
         # pairs in flight: lane j runs pairs j, j+L, ... on its own stream with
         # its own snapshot / record / image gradients / gradient buffer; the
@@ -191,6 +195,7 @@ class TrainStep:
                                      vs_norm=None if self.vs_norm is None else torch.empty_like(self.vs_norm))
             ln.cache, ln.photo_ws = None, None
             ln.step_status = StatusBlock(self.device)  # every render of this lane's pairs, merged
+            ln.loss = torch.zeros(1, dtype=torch.float64, device=self.device) if self.deterministic else self.loss
             ln.stream = torch.cuda.Stream(device=self.device) if self.n_lanes > 1 else None
             lanes.append(ln)
         self._lanes = lanes
@@ -247,6 +252,8 @@ class TrainStep:
         main = torch.cuda.current_stream()
         for ln in lanes:
             ln.step_status.reset()
+            if self.deterministic:
+                ln.loss.zero_()
         if nl > 1:
             ready = torch.cuda.Event()
             ready.record(main)
@@ -262,8 +269,13 @@ class TrainStep:
         if nl > 1:
             for ln in used:
                 main.wait_stream(ln.stream)
-            for ln in used[1:]:
-                self.grads.buffer.add_(ln.grads.buffer)
+            if len(used) > 1:  # lane 0's buffer += the other lanes', one pass
+                srcs = (ctypes.c_void_p * (len(used) - 1))(*[ln.grads.buffer.data_ptr() for ln in used[1:]])
+                N.check(lib.fs4d_sum_buffers(_p(self.grads.buffer), srcs, len(used) - 1, self.grads.numel, 1,
+                                             _stream()))
+        if self.deterministic:
+            for ln in used:  # the lanes' losses in lane order
+                self.loss.add_(ln.loss)
         if self.lambda_tv > 0 and self.net.enable_grid:
             # d(lambda_tv * tv)/d(plane) once per iteration (training.py:523-529); 1/world per rank
             tv_loss_grad_device(self.field, self.plane_grads, self.lambda_tv / self.world, True, self.loss)
@@ -355,7 +367,7 @@ class TrainStep:
             N.check(lib.fs4d_l1_loss_grad(_p(imgs["color"]), _p(tgt_rgb), _p(imgs["feature"]) if dout else None,
                                           _p(tgt_feat) if dout else None, self.h, self.w, dout,
                                           w * self.lambda_rgb, w * self.lambda_feat, _p(ln.d_color),
-                                          _p(ln.d_feature) if dout else None, _p(self.loss), _stream()))
+                                          _p(ln.d_feature) if dout else None, _p(ln.loss), _stream()))
         else:
             mask = item[5] if len(item) > 5 else None
             tgt_depth = item[6] if len(item) > 6 else None
@@ -366,16 +378,17 @@ class TrainStep:
                                           dtype=torch.uint8, device=self.device)
             photometric_loss_grad(imgs["color"], tgt_rgb, mask, imgs["depth"] if d_depth is not None else None,
                                   tgt_depth, imgs["alpha"], w * self.lambda_rgb, w * self.lambda_depth,
-                                  ln.d_color, d_depth, loss=self.loss, workspace=ln.photo_ws)
+                                  ln.d_color, d_depth, loss=ln.loss, workspace=ln.photo_ws)
             if dout and tgt_feat is not None and self.decoder is not None:
                 ln.decoder_loss(self.decoder[0], self.decoder[1], imgs["feature"], tgt_feat, w * self.lambda_feat,
-                                ln.d_feature, ln.grads["decoder.weight"], ln.grads["decoder.bias"], self.loss,
+                                ln.d_feature, ln.grads["decoder.weight"], ln.grads["decoder.bias"], ln.loss,
                                 accumulate=not first)
             elif dout:
                 ln.d_feature.zero_()
         ln.renderer.backward(ln.snap, K, T, self.h, self.w, self.cfg, rec, d_color=ln.d_color, d_depth=d_depth,
                              d_feature=ln.d_feature if dout else None, grads=ln.snap_grads,
-                             viewspace=ln.vs_norm if self.stats is not None else False)
+                             viewspace=ln.vs_norm if self.stats is not None else False,
+                             deterministic=self.deterministic)
         if self.stats is not None:  # training.py:514 grad_stats.add (dense, source order)
             cur = torch.cuda.current_stream()
             if stats_done is not None:
@@ -385,7 +398,7 @@ class TrainStep:
             stats_done.record(cur)
         ln.deformer.backward(self.cloud, field, self.net, t, ln.snap_grads, cloud_grads=ln.cloud_grads,
                              net_grads=ln.net_grads, plane_grads=ln.plane_grads if self.net.enable_grid else None,
-                             accumulate=not first, cache=ln.cache)
+                             accumulate=not first, cache=ln.cache, deterministic=self.deterministic)
         return stats_done
 
     # ------------------------------------------------------------------
