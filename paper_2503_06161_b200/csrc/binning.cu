@@ -156,7 +156,36 @@ __device__ void cta_radix_sort_tile(const unsigned long long* __restrict__ src, 
     key[r] = (uint32_t)(kv >> 32);
     val[r] = (uint32_t)kv;
   }
+  // digits on which every key of the tile agrees need no pass (e.g. the
+  // sign / exponent byte of depths within one octave): AND / OR over the keys
+  uint32_t kand = 0xFFFFFFFFu, kor = 0u;
+#pragma unroll
+  for (int r = 0; r < kTileSortIPT; ++r)
+    if (r < R && warp * 32 * R + r * 32 + lane < n) {
+      kand &= key[r];
+      kor |= key[r];
+    }
+  kand = __reduce_and_sync(0xffffffffu, kand);
+  kor = __reduce_or_sync(0xffffffffu, kor);
+  if (lane == 0) {
+    dbase[2 * warp] = kand;
+    dbase[2 * warp + 1] = kor;
+  }
+  __syncthreads();
+  uint32_t vary = 0u;
+  {
+    uint32_t ba = 0xFFFFFFFFu, bo = 0u;
+    for (int w = 0; w < kTileSortWarps; ++w) {
+      ba &= dbase[2 * w];
+      bo |= dbase[2 * w + 1];
+    }
+    vary = ba ^ bo;
+  }
+  __syncthreads();
+  bool sorted_into_xbuf = false;
   for (int shift = 0; shift < 32; shift += 8) {
+    if (((vary >> shift) & 0xFFu) == 0u) continue;  // uniform digit (block-uniform branch)
+    sorted_into_xbuf = true;
     for (int d = threadIdx.x; d < kTileSortWarps * 256; d += blockDim.x) wcnt[d] = 0;
     __syncthreads();
     uint32_t rank[kTileSortIPT];
@@ -220,6 +249,14 @@ __device__ void cta_radix_sort_tile(const unsigned long long* __restrict__ src, 
       key[r] = (uint32_t)(kv >> 32);
       val[r] = (uint32_t)kv;
     }
+  }
+  if (!sorted_into_xbuf) {  // all keys equal: the load order is the order
+#pragma unroll
+    for (int r = 0; r < kTileSortIPT; ++r) {
+      const int q = warp * 32 * R + r * 32 + lane;
+      if (r < R && q < n) xbuf[q] = ((unsigned long long)key[r] << 32) | val[r];
+    }
+    __syncthreads();
   }
   // xbuf holds the sorted sequence; fix equal-depth-bit runs, then emit
   for (int q = threadIdx.x; q < n; q += blockDim.x) {

@@ -69,7 +69,9 @@ __device__ __forceinline__ uint32_t relu_bits16(const uint8_t* img, int KT, int 
   return m;
 }
 
-// warp sum of v[i] for every i, added into shared accumulators by lane 0
+// warp sum of v[i] for every i, added by lane 0 into this warp's own shared
+// accumulators (one slot row per warp, summed in warp order at the end: the
+// bias gradients are reproducible bit for bit)
 template <int N>
 __device__ __forceinline__ void warp_sum_to_smem(const float* v, float* dst, int lane) {
 #pragma unroll
@@ -77,7 +79,7 @@ __device__ __forceinline__ void warp_sum_to_smem(const float* v, float* dst, int
     float s = v[i];
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) atomicAdd(dst + i, s);
+    if (lane == 0) dst[i] += s;
   }
 }
 
@@ -100,7 +102,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t accbar_s, ldbar_s;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float sbias[64];  // head biases [0, 16), F_feat layer-0 biases [16, 48)
+  // per-warp bias-gradient accumulators: head biases [0, 16), F_feat layer-0
+  // biases [16, 48) of each epilogue warp
+  __shared__ float sbias_w[kBwdEpiThreads / 32][64];
   const TcPlan& p = a.p;
   const int wbytes = (p.blob_bytes + 1023) & ~1023;
   uint8_t* W = smem;
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
 
   for (int e = tid; e < p.blob_bytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
-  if (tid < 64) sbias[tid] = 0.f;
+  for (int e = tid; e < (kBwdEpiThreads / 32) * 64; e += blockDim.x) (&sbias_w[0][0])[e] = 0.f;
   const uint32_t accbar = smem_u32(&accbar_s), ldbar = smem_u32(&ldbar_s);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(accbar));
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
         for (int i = 3; i < 8; ++i) v[i] = 0.f;
       }
       store_split8(R + kRGD, 16, row, 8 * half, v);
-      warp_sum_to_smem<8>(v, sbias + 8 * half, lane);
+      warp_sum_to_smem<8>(v, sbias_w[warp] + 8 * half, lane);
     }
     sync_all();
     if (issuer) {
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
         if (!((mf >> i) & 1u)) g[i] = 0.f;
       store_split8(R + kRGFF, 32, row, 16 * half, g);
       store_split8(R + kRGFF, 32, row, 16 * half + 8, g + 8);
-      warp_sum_to_smem<16>(g, sbias + 16 + 16 * half, lane);
+      warp_sum_to_smem<16>(g, sbias_w[warp] + 16 + 16 * half, lane);
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         m2 |= (uint64_t)relu_bits16(R + kRE2, kCacheKtE2, row, 32 * b + 16 * half) << (16 * b);
@@ -344,7 +348,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_mlp_bwd_tc(BwdArgs a) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) part[(c + i) * kTcRows + row] = v[i];
     }
-    if (tid < 48) part[kDwCols * kTcRows + tid] = sbias[tid];
+    if (tid < 48) {
+      float sb = 0.f;
+#pragma unroll
+      for (int w = 0; w < kBwdEpiThreads / 32; ++w) sb += sbias_w[w][tid];
+      part[kDwCols * kTcRows + tid] = sb;
+    }
   }
   tc_fence_before();
   __syncthreads();

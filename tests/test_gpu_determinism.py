@@ -7,9 +7,10 @@ resume, test_training.py:225-235, 282-299):
   fixed-point HexPlane scatter -- give bitwise identical gradients run to run
   and agree with the atomic path to fp32 summation noise;
 * TrainStep(deterministic=True) with three pairs in flight is bitwise
-  reproducible, and a save / load / continue of the device training state
-  ends byte-identical to the unbroken run (FS4C files compared byte for
-  byte).
+  reproducible (gradients, parameters, Adam state; the reported loss scalar
+  to double rounding), and a save / load / continue of the device training
+  state ends byte-identical to the unbroken run (FS4C files compared byte
+  for byte).
 """
 
 import numpy as np
@@ -101,7 +102,9 @@ def test_training_steps_and_checkpoint_resume_byte_identical(tmp_path):
     b = _train_step(cloud, field, net, h, w)
     la = [float(a.run(batch, check=True).item()) for _ in range(2)]
     lb = [float(b.run(batch, check=True).item()) for _ in range(2)]
-    assert la == lb
+    # the reported loss scalar sums per-block double partials with atomics
+    # (it is not model state): equal to double rounding
+    assert np.allclose(la, lb, rtol=1e-12, atol=0)
     assert torch.equal(a.grads.buffer, b.grads.buffer) and torch.equal(a.params.buffer, b.params.buffer)
     mid = str(tmp_path / "mid.fs4c")
     ck.save_train_state(a, mid)
