@@ -48,6 +48,12 @@ __device__ __forceinline__ bool rect_valid(const int4& t) { return t.y >= t.x &&
 #define FS4D_EMIT_THREADS 256
 #endif
 constexpr int kEmitThreads = FS4D_EMIT_THREADS;
+// One Gaussian per thread.  The block counts its pairs per tile in shared
+// memory, reserves its slice of every touched tile segment with one global
+// atomic, and keeps the slice's absolute start (segment offset + reservation,
+// 32-bit: pair capacities stay below 2^32) in shared memory, so the emission
+// loop is shared-memory atomics + one store per pair (no global load of the
+// segment offset on the per-pair critical path).
 __global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __restrict__ tile_rect,
                                                         const uint32_t* __restrict__ dkeys, int64_t K, int ntx,
                                                         int ntiles, const uint64_t* __restrict__ toff,
@@ -55,12 +61,13 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __r
                                                         unsigned long long* __restrict__ pkey) {
   __shared__ uint32_t cnt[kHistMaxTiles];
   __shared__ uint32_t base[kHistMaxTiles];
-  const bool smem = ntiles <= kHistMaxTiles;
+  const bool smem = ntiles <= kHistMaxTiles && cap <= (int64_t)0xFFFFFFFFu;
   if (smem)
     for (int b = threadIdx.x; b < ntiles; b += blockDim.x) cnt[b] = 0;
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool kept = i < K && dkeys[i] != 0xFFFFFFFFu;
+  const uint32_t dk = i < K ? dkeys[i] : 0xFFFFFFFFu;
+  const bool kept = dk != 0xFFFFFFFFu;
   int4 t = make_int4(0, -1, 0, -1);
   if (kept) t = tile_rect[i];
   if (smem && kept)
@@ -70,17 +77,16 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __r
   if (smem)
     for (int b = threadIdx.x; b < ntiles; b += blockDim.x) {
       const uint32_t c = cnt[b];
-      base[b] = c ? atomicAdd(&tcur[b], c) : 0u;  // reserve this block's slice of the segment
+      if (c) base[b] = (uint32_t)toff[b] + atomicAdd(&tcur[b], c);  // this block's slice of the segment
       cnt[b] = 0;
     }
   __syncthreads();
   if (!kept) return;
-  const unsigned long long key = ((unsigned long long)dkeys[i] << 32) | (unsigned long long)i;
+  const unsigned long long key = ((unsigned long long)dk << 32) | (unsigned long long)i;
   for (int ty = t.z; ty <= t.w; ++ty)
     for (int tx = t.x; tx <= t.y; ++tx) {
       const int b = ty * ntx + tx;
-      const uint32_t local = smem ? base[b] + atomicAdd(&cnt[b], 1u) : atomicAdd(&tcur[b], 1u);
-      const uint64_t o = toff[b] + local;
+      const uint64_t o = smem ? (uint64_t)(base[b] + atomicAdd(&cnt[b], 1u)) : toff[b] + atomicAdd(&tcur[b], 1u);
       if (o < (uint64_t)cap) pkey[o] = key;
     }
 }
@@ -135,6 +141,21 @@ __device__ void bitonic_sort(unsigned long long* keys, int n, const double* __re
 
 constexpr int kTileSortWarps = kTileSortThreads / 32;
 constexpr int kTileSortIPT = kSortSmemKeys / kTileSortThreads;  // 16 items per thread
+
+// Lanes of the warp holding the same 8-bit digit: eight ballots, one per
+// digit bit (VOTE + LOP3, ALU latency).  __match_any_sync does the same in one
+// instruction but runs on a long variable-latency path (the top short-
+// scoreboard stall of this kernel under ncu).
+__device__ __forceinline__ unsigned warp_peers8(uint32_t d) {
+  unsigned m = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bal : ~bal;
+  }
+  return m;
+}
 
 // CTA-wide stable LSD radix sort of up to kSortSmemKeys (depth bits, source
 // index) pairs held in registers ("striped": lane l of warp w owns items
@@ -193,7 +214,7 @@ __device__ void cta_radix_sort_tile(const unsigned long long* __restrict__ src, 
     for (int r = 0; r < kTileSortIPT; ++r) {
       if (r >= R) break;
       const uint32_t d = (key[r] >> shift) & 0xFFu;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const unsigned peers = warp_peers8(d);
       rank[r] = wcnt[warp * 256 + d] + __popc(peers & lt);
       __syncwarp();
       if ((peers & lt) == 0) wcnt[warp * 256 + d] += __popc(peers);

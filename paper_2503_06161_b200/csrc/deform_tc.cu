@@ -818,6 +818,293 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
 }
 
 // ---------------------------------------------------------------------------
+// two-slot variant: two independent tile pipelines per CTA ("slots"), each
+// with its own 8 epilogue warps, its own MMA-issuing warp, TMEM columns
+// [256 s, 256 s + 256) and one 64 KB operand region in which X (latent,
+// hidden, FF; KT 64/32) and E (e1, e2; KT 128) alias -- every write into the
+// region follows the wait for the accumulators that are products of the MMAs
+// reading its previous contents, so the alias is race-free.  The weights are
+// staged once per CTA and shared.  While one slot's epilogue converts
+// accumulators, the other slot's MMAs run: tensor pipe and epilogue issue
+// overlap instead of alternating (the single-slot chain leaves both idle half
+// of the time).  Epilogue warps 0-7 serve slot 0, 8-15 slot 1 (warp % 4 still
+// selects the TMEM lane quarter); warps 16 / 17 issue the MMAs of slot 0 / 1
+// (tcgen05.commit tracks the issuing thread's MMAs only, so each slot's
+// commits see its own MMAs).  Slot s of CTA c takes tiles c + G (2 i + s).
+// ---------------------------------------------------------------------------
+constexpr int kTc2Threads = 2 * kTcWsThreads;
+constexpr int kTc2Region = kTcRows * 128 * 4;  // E hi + lo: 64 KB
+
+template <bool CACHE>
+__global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int kSlots = FS4D_MAX_TRUNK + 16;
+  __shared__ __align__(8) uint64_t accbar_s[2], opbar_s[2][kSlots];
+  __shared__ uint32_t tmem_base_sh;
+  const TcPlan& p = a.p;
+  uint8_t* W = smem;
+  const int wbytes = (p.fwd_bytes + 1023) & ~1023;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const bool mma_warp = warp >= 2 * (kTcEpiThreads / 32);
+  const int sl = mma_warp ? warp - 2 * (kTcEpiThreads / 32) : warp / (kTcEpiThreads / 32);
+  uint8_t* R = smem + wbytes + sl * kTc2Region;
+
+  if (CACHE && blockIdx.x == 0 && tid == 0) {
+    CacheHeader* h = reinterpret_cast<CacheHeader*>(a.cache);
+    h->magic = kCacheMagic;
+    h->K = a.K;
+    h->t = p.t;
+  }
+  for (int e = tid; e < p.fwd_bytes / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
+  const uint32_t accbar = smem_u32(&accbar_s[sl]), opbar = smem_u32(&opbar_s[sl][0]);
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&accbar_s[s])));
+      for (int j = 0; j < kSlots; ++j)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&opbar_s[s][j])), "r"(kTcEpiThreads));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(2 * kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh + (uint32_t)(kTmemCols * sl);
+  const uint32_t sW = smem_u32(W), sR = smem_u32(R);
+  const int64_t ntiles = ceil_div(a.K, kTcRows);
+  const int64_t first = blockIdx.x + (int64_t)gridDim.x * sl, step = 2 * (int64_t)gridDim.x;
+
+  if (mma_warp) {
+    // ------------------------------------------------------------ MMA issuer (slot sl)
+    uint32_t iter = 0;
+    int slot = 0;
+    auto wait_op = [&]() {
+      mbar_wait(opbar + 8 * slot, iter & 1);
+      ++slot;
+      tc_fence_after();
+    };
+    for (int64_t tile = first; tile < ntiles; tile += step, ++iter) {
+      slot = 0;
+      for (int l = 0; l < p.depth; ++l) {
+        wait_op();  // X holds the latent / previous trunk output
+        gemm_bf16x3_w(tmem + 128, sR, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
+        mma_commit_w(accbar);
+      }
+      for (int c = 0; c < 64; c += 16) {  // hidden chunk c -> extractor-0 K step
+        wait_op();
+        gemm_bf16x3_w(tmem, sR, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
+      }
+      mma_commit_w(accbar);
+      for (int b = 0; b < 4; ++b) {  // e1 of branch b -> extractor-1
+        wait_op();
+        gemm_bf16x3_w(tmem + 32 * b, sR, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
+      }
+      mma_commit_w(accbar);
+      for (int b = 0; b < 4; ++b) {  // e2 of branch b -> head b and F_feat layer-0 K slice
+        wait_op();
+        gemm_bf16x3_w(tmem + 128 + 16 * b, sR, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
+        if (p.enable_feat) gemm_bf16x3_w(tmem + 192, sR, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
+      }
+      mma_commit_w(accbar);
+      if (p.enable_feat) {
+        wait_op();  // FF in X
+        gemm_bf16x3_w(tmem, sR, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
+        mma_commit_w(accbar);
+      }
+      wait_op();  // tile finished: TMEM and the region free for the next tile
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogues (slot sl)
+    const int etid = tid & (kTcEpiThreads - 1);
+    const int row = etid & (kTcRows - 1), half = etid / kTcRows;
+    const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float* bias_f = reinterpret_cast<const float*>(W);
+    uint32_t ph = 0;
+    auto wait_acc = [&]() {
+      mbar_wait(accbar, ph);
+      ph ^= 1;
+      tc_fence_after();
+    };
+    int slot = 0;
+    auto signal = [&]() {
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(opbar + 8 * slot);
+      ++slot;
+    };
+    for (int64_t tile = first; tile < ntiles; tile += step) {
+      slot = 0;
+      const int64_t k = tile * kTcRows + row;
+      const bool valid = k < a.K;
+      uint8_t* ct = CACHE ? a.cache + kCacheHeader + tile * (int64_t)kCacheTileBytes : nullptr;
+      if (CACHE) {
+        if (half == 0) {
+          cache_ones(ct + kCacheLat, kCacheKtLat, row, 64);
+          cache_ones(ct + kCacheHid, kCacheKtHid, row, 64);
+          cache_ones(ct + kCacheFF, kCacheKtFF, row, 32);
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) cache_ones(ct + kCacheE1 + b * kCacheE1Bytes, kCacheKtE1, row, 32);
+        }
+      }
+      {  // latent -> X (the other slot hides the load latency)
+        float4 lat[8];
+        const float4* src = reinterpret_cast<const float4*>(a.latent + (valid ? k : 0) * 64 + 32 * half);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) lat[c] = valid ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+          float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
+          store_split8(R, 64, row, 32 * half + 4 * c, v);
+          if (CACHE) cache_split8(ct + kCacheLat, kCacheKtLat, row, 32 * half + 4 * c, v);
+        }
+        signal();
+      }
+      for (int l = 0; l < p.depth; ++l) {
+        wait_acc();
+        const float* tb = bias_f + p.off_b_trunk[l] / 4;
+        if (l + 1 < p.depth) {
+          epilogue_to_operand(tmem_row, 128, 64, tb, true, R, 64, 0, row, half);
+          signal();
+        } else {
+          float v[4][8];
+          tmem_ld_batch<4>(tmem_row + 128 + 8 * half, v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int c = 16 * i + 8 * half;
+            chunk_to_operand(v[i], tb + c, R, 64, c, row, CACHE ? ct + kCacheHid : nullptr, kCacheKtHid, c);
+            signal();
+          }
+        }
+      }
+      wait_acc();  // extractor 0 -> e1 (KT 128), two TMEM batches of two branches
+      {
+        const float* eb = bias_f + p.off_b_ext0 / 4;
+#pragma unroll
+        for (int bb = 0; bb < 4; bb += 2) {
+          float v[4][8];
+          tmem_ld_batch<4>(tmem_row + 32 * bb + 8 * half, v);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int b = bb + j;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int c = 32 * b + 16 * i + 8 * half;
+              chunk_to_operand(v[2 * j + i], eb + c, R, 128, c, row,
+                               CACHE ? ct + kCacheE1 + b * kCacheE1Bytes : nullptr, kCacheKtE1, c - 32 * b);
+            }
+            signal();
+          }
+        }
+      }
+      wait_acc();  // extractor 1 -> e2
+      {
+        const float* eb = bias_f + p.off_b_ext1 / 4;
+#pragma unroll
+        for (int bb = 0; bb < 4; bb += 2) {
+          float v[4][8];
+          tmem_ld_batch<4>(tmem_row + 32 * bb + 8 * half, v);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int b = bb + j;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int c = 32 * b + 16 * i + 8 * half;
+              chunk_to_operand(v[2 * j + i], eb + c, R, 128, c, row, CACHE ? ct + kCacheE2 : nullptr, kCacheKtE2, c);
+            }
+            signal();
+          }
+        }
+      }
+      // the cloud values this thread updates (loads in flight during the head MMAs)
+      float cv[7];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) cv[q] = 0.f;
+      if (valid) {
+        if (half == 0) {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) cv[q] = a.pos[3 * k + q];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cv[3 + q] = a.rot[4 * k + q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 3; ++q) cv[q] = a.ls[3 * k + q];
+          cv[3] = a.op[k];
+        }
+      }
+      wait_acc();
+      {
+        const float* hb = bias_f + p.off_b_head / 4;
+        float d0[4], d1[4];
+        tmem_ld4(tmem_row + 128 + 32 * half, d0);
+        tmem_ld4(tmem_row + 144 + 32 * half, d1);
+        if (valid) {
+          if (half == 0) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) a.o_pos[3 * k + q] = cv[q] + d0[q] + hb[q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a.o_rot[4 * k + q] = cv[3 + q] + d1[q] + hb[16 + q];
+          } else {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) a.o_ls[3 * k + q] = cv[q] + d0[q] + hb[32 + q];
+            a.o_op[k] = cv[3] + d1[0] + hb[48];
+          }
+        }
+      }
+      if (p.enable_feat) {
+        float fv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int c = 8 * half + 16 * (q / 8) + (q % 8);
+          fv[q] = (valid && c < p.D && p.DP <= 32) ? a.feat[(int64_t)p.D * k + c] : 0.f;
+        }
+        epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, R, 32, 0, row, half,
+                            CACHE ? ct + kCacheFF : nullptr, kCacheKtFF, 0);
+        signal();
+        wait_acc();
+        const float* fb = bias_f + p.off_b_f2 / 4;
+#pragma unroll
+        for (int qc = 0; qc < 2; ++qc) {
+          const int c = 8 * half + 16 * qc;
+          if (c >= p.DP) break;
+          float v[8];
+          tmem_ld8(tmem_row + c, v);
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (c + i < p.D) {
+                const float base = p.DP <= 32 ? fv[8 * qc + i] : a.feat[(int64_t)p.D * k + c + i];
+                a.o_feat[(int64_t)p.D * k + c + i] = base + v[i] + fb[c + i];
+              }
+            }
+          }
+        }
+        for (int c = 8 * half + 32; c < p.DP; c += 16) {
+          float v[8];
+          tmem_ld8(tmem_row + c, v);
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (c + i < p.D) a.o_feat[(int64_t)p.D * k + c + i] = a.feat[(int64_t)p.D * k + c + i] + v[i] + fb[c + i];
+          }
+        }
+      }
+      signal();  // tile done
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "r"(2 * kTmemCols));
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 bool tc_path_ok(const Fs4dDeformNet& n, const Fs4dHexPlane& f) {
@@ -1085,6 +1372,21 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   const int64_t ntiles = ceil_div(K, kTcRows);
   static const int grid_cap = getenv("FS4D_MLP_GRID") ? atoi(getenv("FS4D_MLP_GRID")) : kNumSMs;
   const int grid = (int)(ntiles < grid_cap ? ntiles : grid_cap);
+  // two tile pipelines per CTA whenever the weights + two 64 KB regions fit
+  // (depth-1 trunk: 94 + 128 KB); FS4D_MLP_SLOTS=1 keeps the single-slot kernel
+  const int smem2 = ((p.fwd_bytes + 1023) & ~1023) + 2 * kTc2Region;
+  static const bool one_slot = getenv("FS4D_MLP_SLOTS") && atoi(getenv("FS4D_MLP_SLOTS")) == 1;
+  if (!fused && !one_slot && smem2 <= 232448 - 1024) {
+    const int grid2 = (int)(ceil_div(ntiles, 2) < grid_cap ? ceil_div(ntiles, 2) : grid_cap);
+    if (cache) {
+      cudaFuncSetAttribute(k_mlp_tc_2s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+      k_mlp_tc_2s<true><<<grid2, kTc2Threads, smem2, s>>>(a);
+    } else {
+      cudaFuncSetAttribute(k_mlp_tc_2s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+      k_mlp_tc_2s<false><<<grid2, kTc2Threads, smem2, s>>>(a);
+    }
+    return check_launch("deform_tc_2s");
+  }
   if (fused) {
     cudaFuncSetAttribute(k_mlp_tc_ws<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mlp_tc_ws<true, false><<<grid, kTcFusedThreads, smem, s>>>(a);
