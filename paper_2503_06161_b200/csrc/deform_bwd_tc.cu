@@ -44,16 +44,6 @@ constexpr int kRHid = 0, kRE1 = 36864, kRGE2 = 57344, kRGE1 = 73728;
 constexpr int kRLat = 36864, kRGH = 73728;
 constexpr int kRBytes = 118784 + 2048;  // + slack for M = 128 MN-major reads of narrower images
 
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-
 // ReLU gate of 16 consecutive columns c0.. of row r: bit i set iff value > 0
 __device__ __forceinline__ uint32_t relu_bits16(const uint8_t* img, int KT, int r, int c0) {
   const uint4 a = *reinterpret_cast<const uint4*>(img + core_off(r, c0, KT));

@@ -15,6 +15,8 @@
 //                      produces the next layer's A operand in place, and the
 //                      last epilogues add the raw-space deltas straight into
 //                      the snapshot (deformation.py:126-133).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <stdlib.h>
 #include <string.h>
@@ -166,11 +168,20 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPla
 // the per-frame time rows (k_pack_tc): 2 corner rows instead of 4 for half
 // of the planes, and those rows (72 KB at configs[1]) stay L1/L2-hot.  The
 // kernel is bound by L2->SM bytes, so this halves the time planes' share.
-template <int LEVELS>
+//
+// IMG: instead of fp32 rows, write each Gaussian's latent as bf16 hi / lo
+// (the tcgen05 A-operand split) in one 256-byte row [hi 64 x bf16 | lo 64 x
+// bf16]: every row is whole 32-byte sectors whatever the visiting order (the
+// core-matrix image itself interleaves row pairs in a sector, which under the
+// Morton order turns into partial-sector writes and ECC read-modify-writes),
+// and the MLP's epilogue threads move the rows into its operand image with
+// asynchronous 16-byte copies, never touching them in registers.
+template <int LEVELS, bool IMG = false>
 __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPlan p, int64_t K,
                                                                               const float* __restrict__ pos,
                                                                               const float* __restrict__ rows,
-                                                                              float* __restrict__ latent) {
+                                                                              float* __restrict__ latent,
+                                                                              uint8_t* __restrict__ img = nullptr) {
   __shared__ int s_base[kGatherWarps][LEVELS * 6][32];
   __shared__ float2 s_f[kGatherWarps][LEVELS * 6][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -209,6 +220,67 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPl
       }
   }
   __syncwarp();
+  if (IMG) {
+    // lane = (Gaussian j%8, 8-channel block): each lane ends with one 16-byte
+    // hi and one 16-byte lo chunk, and a warp's store covers 8 rows x 4 column
+    // blocks = four full 128-byte core-matrix rows (coalesced)
+    const int sub8 = lane >> 2, c8 = (lane & 3) * 8;
+    for (int j0 = 0; j0 < 32; j0 += 8) {
+      const int j = j0 + sub8;
+      const int64_t k = __shfl_sync(0xffffffffu, kg, j);
+#pragma unroll
+      for (int l = 0; l < LEVELS; ++l) {
+        float pr[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pr[i] = 1.f;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const float2 f = s_f[warp][l * 6 + q][j];
+          if (q == 2 || q == 4 || q == 5) {
+            const int tq = q == 2 ? 0 : (q == 4 ? 1 : 2);
+            const float* rp = rows + p.row_off[l][tq] + s_base[warp][l * 6 + q][j] + c8;
+            const float4 a0 = __ldg(reinterpret_cast<const float4*>(rp));
+            const float4 a1 = __ldg(reinterpret_cast<const float4*>(rp + 4));
+            const float4 c0 = __ldg(reinterpret_cast<const float4*>(rp + 32));
+            const float4 c1 = __ldg(reinterpret_cast<const float4*>(rp + 36));
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const float wa = 1.f - f.x;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pr[i] *= wa * av[i] + f.x * cv[i];
+          } else {
+            const int rs = p.res[l][q][1] * 32;
+            const float* pl = p.planes[l][q] + s_base[warp][l * 6 + q][j] + c8;
+            const float w00 = (1.f - f.x) * (1.f - f.y), w10 = f.x * (1.f - f.y);
+            const float w01 = (1.f - f.x) * f.y, w11 = f.x * f.y;
+            const float4 a0 = PLANE_LD(reinterpret_cast<const float4*>(pl));
+            const float4 a1 = PLANE_LD(reinterpret_cast<const float4*>(pl + 4));
+            const float4 b0 = PLANE_LD(reinterpret_cast<const float4*>(pl + 32));
+            const float4 b1 = PLANE_LD(reinterpret_cast<const float4*>(pl + 36));
+            const float4 c0 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs));
+            const float4 c1 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs + 4));
+            const float4 d0 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs + 32));
+            const float4 d1 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs + 36));
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+            // hexplane.py:105-106 order: (1-fa)(1-fb)p00 + fa(1-fb)p10 + (1-fa)fb p01 + fa fb p11
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pr[i] *= w00 * av[i] + w10 * cv[i] + w01 * bv[i] + w11 * dv[i];
+          }
+        }
+        if (k < K) {
+          uint4 h, lo;
+          split8(pr, h, lo);
+          uint8_t* row = img + k * 256 + (l * 32 + c8) * 2;
+          *reinterpret_cast<uint4*>(row) = h;
+          *reinterpret_cast<uint4*>(row + 128) = lo;
+        }
+      }
+    }
+    return;
+  }
   const int sub = lane >> 3, ch = (lane & 7) * 4;
   for (int j0 = 0; j0 < 32; j0 += 4) {
     const int j = j0 + sub;
@@ -329,6 +401,7 @@ struct TcArgs {
   TcPlan p;
   int64_t K;
   const float* latent;
+  const uint8_t* lat_img;  // two-slot kernel: [K][hi 64 | lo 64] bf16 latent rows (gather IMG output)
   const uint8_t* blob;
   const float* pos;
   const float* rot;
@@ -501,8 +574,9 @@ __device__ __forceinline__ void produce_latent(const TcArgs& a, int64_t tile, ui
 #ifdef FS4D_MLP_TRACE
 // debug timeline of CTA 0 (tools/mlp_trace.sh): clock64 << 4 | event
 // (MMA warp: 1 operand ready, 2 commit; epilogue thread 0: 3 acc ready, 4 signal)
-__device__ long long g_mlp_trace[2][512];
-__device__ int g_mlp_n[2];
+// (two-slot kernel: who = 2 * slot + {0 MMA, 1 epilogue})
+__device__ long long g_mlp_trace[4][512];
+__device__ int g_mlp_n[4];
 #define MLP_TRACE(who, ev)                                                           \
   if (blockIdx.x == 0) {                                                             \
     const int i_ = g_mlp_n[who]++;                                                   \
@@ -832,14 +906,122 @@ __global__ void __launch_bounds__(FUSED ? kTcFusedThreads : kTcWsThreads, 1) k_m
 // (tcgen05.commit tracks the issuing thread's MMAs only, so each slot's
 // commits see its own MMAs).  Slot s of CTA c takes tiles c + G (2 i + s).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+
 constexpr int kTc2Threads = 2 * kTcWsThreads;
+constexpr int kMaxDynSmemBytes = 232448 - 2048;  // 227 KB opt-in, less the kernel's static barriers
 constexpr int kTc2Region = kTcRows * 128 * 4;  // E hi + lo: 64 KB
+constexpr int kTc2Hand = FS4D_MAX_TRUNK + 16;  // operand hand-offs per tile (upper bound)
+
+struct Tc2Bars {
+  uint64_t acc[2], op[2][kTc2Hand], x[2], rfree[2];
+};
+
+// TMA: one 8-column block (16 bytes) of 128 latent rows -> 2 KB of shared
+// memory, rows contiguous: i.e. one K-adjacent column of core matrices
+__device__ __forceinline__ void tma_lat_block(uint32_t dst, const CUtensorMap* map, int c0, int row0, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(row0), "r"(bar)
+      : "memory");
+}
+
+// MMA issue of slot SL.  Everything the descriptors depend on is a compile-
+// time constant, a kernel parameter or a shared-memory symbol address
+// (TMEM: this CTA owns all 512 columns, so slot SL starts at column 256 SL;
+// the kernel checks the allocator agrees), so ptxas keeps the descriptor
+// arithmetic on the uniform datapath instead of moving every operand with
+// R2UR under the elected lane (measured ~100 cycles per MMA issue that way).
+template <int SL>
+__device__ __forceinline__ void mlp2_issue(const TcArgs& a, const CUtensorMap* tmap, Tc2Bars& bars,
+                                           const uint8_t* smem) {
+  const TcPlan& p = a.p;
+  const uint32_t tmem = (uint32_t)(kTmemCols * SL);
+  const uint32_t sW = smem_u32(smem);
+  const uint32_t sR = sW + (uint32_t)((p.fwd_bytes + 1023) & ~1023) + (uint32_t)(SL * kTc2Region);
+  const uint32_t accbar = smem_u32(&bars.acc[SL]), opbar = smem_u32(&bars.op[SL][0]);
+  const uint32_t xbar = smem_u32(&bars.x[SL]), rbar = smem_u32(&bars.rfree[SL]);
+  const bool leader = (threadIdx.x & 31) == 0;
+  const int64_t ntiles = ceil_div(a.K, kTcRows);
+  // the latent rows of tile t -> the region by TMA: 16 column blocks of
+  // [128 rows x 16 B] (8 hi, then 8 lo), i.e. the K-major no-swizzle operand
+  // with K-adjacent core matrices 2 KB apart (LBO 2048, SBO 128); rows past K
+  // are zero-filled by the TMA unit
+  auto load_x = [&](int64_t t) {
+    if (leader) {
+      mbar_expect_tx(xbar, kTcRows * 64 * 4);
+#pragma unroll 1
+      for (int cb = 0; cb < 16; ++cb) tma_lat_block(sR + 2048 * cb, tmap, 8 * cb, (int)(t * kTcRows), xbar);
+    }
+    __syncwarp();
+  };
+  if (blockIdx.x + (int64_t)gridDim.x * SL < ntiles) load_x(blockIdx.x + (int64_t)gridDim.x * SL);
+  const TcOpnd xA{sR, (uint32_t)(kTcRows * 64 * 2), 2048u, 128u, 4096u, false};
+  uint32_t iter = 0;
+  int slot = 0;
+  auto wait_op = [&]() {
+    mbar_wait(opbar + 8 * slot, iter & 1);
+    ++slot;
+    tc_fence_after();
+    if (leader) MLP_TRACE(2 * SL, 1);
+  };
+  auto commit = [&]() {
+    mma_commit_w(accbar);
+    if (leader) MLP_TRACE(2 * SL, 2);
+  };
+  for (int64_t tile = blockIdx.x + (int64_t)gridDim.x * SL; tile < ntiles; tile += 2 * (int64_t)gridDim.x, ++iter) {
+    slot = 0;
+    for (int l = 0; l < p.depth; ++l) {
+      if (l == 0) {  // the TMA-loaded latent (column-block-major image)
+        mbar_wait(xbar, iter & 1);
+        tc_fence_after();
+        gemm3_w(tmem + 128, xA, opnd_k(sW + p.off_trunk[0], 64, 64, 0), 64, 4, false);
+      } else {
+        wait_op();  // previous trunk output (64 columns, row-group-major)
+        gemm_bf16x3_w(tmem + 128, sR, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
+      }
+      commit();
+    }
+    for (int c = 0; c < 64; c += 16) {  // hidden chunk c -> extractor-0 K step
+      wait_op();
+      gemm_bf16x3_w(tmem, sR, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
+    }
+    commit();
+    for (int b = 0; b < 4; ++b) {  // e1 of branch b -> extractor-1
+      wait_op();
+      gemm_bf16x3_w(tmem + 32 * b, sR, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
+    }
+    commit();
+    for (int b = 0; b < 4; ++b) {  // e2 of branch b -> head b and F_feat layer-0 K slice
+      wait_op();
+      gemm_bf16x3_w(tmem + 128 + 16 * b, sR, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
+      if (p.enable_feat) gemm_bf16x3_w(tmem + 192, sR, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
+    }
+    commit();
+    if (p.enable_feat) {
+      wait_op();  // FF in X
+      gemm_bf16x3_w(tmem, sR, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
+      commit();
+    }
+    // the region is free once this tile's MMAs complete: start the next
+    // tile's latent load right then, while the epilogue still drains TMEM
+    mma_commit_w(rbar);
+    const int64_t next = tile + 2 * (int64_t)gridDim.x;
+    if (next < ntiles) {
+      mbar_wait(rbar, iter & 1);
+      load_x(next);
+    }
+    wait_op();  // tile finished: the epilogue is done with TMEM
+    __syncwarp();
+  }
+}
 
 template <bool CACHE>
-__global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a) {
+__global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int kSlots = FS4D_MAX_TRUNK + 16;
-  __shared__ __align__(8) uint64_t accbar_s[2], opbar_s[2][kSlots];
+  __shared__ __align__(8) Tc2Bars bars;
   __shared__ uint32_t tmem_base_sh;
   const TcPlan& p = a.p;
   uint8_t* W = smem;
@@ -857,12 +1039,14 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a) {
   }
   for (int e = tid; e < p.fwd_bytes / 16; e += blockDim.x)
     reinterpret_cast<uint4*>(W)[e] = __ldg(reinterpret_cast<const uint4*>(a.blob) + e);
-  const uint32_t accbar = smem_u32(&accbar_s[sl]), opbar = smem_u32(&opbar_s[sl][0]);
+  const uint32_t accbar = smem_u32(&bars.acc[sl]), opbar = smem_u32(&bars.op[sl][0]);
   if (tid == 0) {
     for (int s = 0; s < 2; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&accbar_s[s])));
-      for (int j = 0; j < kSlots; ++j)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&opbar_s[s][j])), "r"(kTcEpiThreads));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars.acc[s])));
+      for (int j = 0; j < kTc2Hand; ++j)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bars.op[s][j])), "r"(kTcEpiThreads / 32));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars.x[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars.rfree[s])));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -874,53 +1058,18 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_base_sh + (uint32_t)(kTmemCols * sl);
-  const uint32_t sW = smem_u32(W), sR = smem_u32(R);
   const int64_t ntiles = ceil_div(a.K, kTcRows);
   const int64_t first = blockIdx.x + (int64_t)gridDim.x * sl, step = 2 * (int64_t)gridDim.x;
 
+  if (tmem_base_sh != 0u) __trap();  // the issuers assume the CTA owns TMEM from column 0
   if (mma_warp) {
-    // ------------------------------------------------------------ MMA issuer (slot sl)
-    uint32_t iter = 0;
-    int slot = 0;
-    auto wait_op = [&]() {
-      mbar_wait(opbar + 8 * slot, iter & 1);
-      ++slot;
-      tc_fence_after();
-    };
-    for (int64_t tile = first; tile < ntiles; tile += step, ++iter) {
-      slot = 0;
-      for (int l = 0; l < p.depth; ++l) {
-        wait_op();  // X holds the latent / previous trunk output
-        gemm_bf16x3_w(tmem + 128, sR, 64, 0, sW + p.off_trunk[l], 64, 0, 64, 4, false);
-        mma_commit_w(accbar);
-      }
-      for (int c = 0; c < 64; c += 16) {  // hidden chunk c -> extractor-0 K step
-        wait_op();
-        gemm_bf16x3_w(tmem, sR, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
-      }
-      mma_commit_w(accbar);
-      for (int b = 0; b < 4; ++b) {  // e1 of branch b -> extractor-1
-        wait_op();
-        gemm_bf16x3_w(tmem + 32 * b, sR, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
-      }
-      mma_commit_w(accbar);
-      for (int b = 0; b < 4; ++b) {  // e2 of branch b -> head b and F_feat layer-0 K slice
-        wait_op();
-        gemm_bf16x3_w(tmem + 128 + 16 * b, sR, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
-        if (p.enable_feat) gemm_bf16x3_w(tmem + 192, sR, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
-      }
-      mma_commit_w(accbar);
-      if (p.enable_feat) {
-        wait_op();  // FF in X
-        gemm_bf16x3_w(tmem, sR, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
-        mma_commit_w(accbar);
-      }
-      wait_op();  // tile finished: TMEM and the region free for the next tile
-      __syncwarp();
-    }
+    if (sl == 0)
+      mlp2_issue<0>(a, &tmap, bars, smem);
+    else
+      mlp2_issue<1>(a, &tmap, bars, smem);
   } else {
     // ------------------------------------------------------------ epilogues (slot sl)
+    const uint32_t tmem = tmem_base_sh + (uint32_t)(kTmemCols * sl);
     const int etid = tid & (kTcEpiThreads - 1);
     const int row = etid & (kTcRows - 1), half = etid / kTcRows;
     const uint32_t tmem_row = tmem + ((uint32_t)((warp & 3) * 32) << 16);
@@ -930,14 +1079,28 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a) {
       mbar_wait(accbar, ph);
       ph ^= 1;
       tc_fence_after();
+      if (etid == 0) MLP_TRACE(2 * sl + 1, 3);
     };
     int slot = 0;
+    // one arrival per warp (count 8): each thread fences its own operand
+    // writes, __syncwarp orders the warp's writes before lane 0's release
+    // arrive -- 8 instead of 256 serialised arrivals on the barrier word
     auto signal = [&]() {
       fence_async_smem();
       tc_fence_before();
-      mbar_arrive(opbar + 8 * slot);
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(opbar + 8 * slot);
       ++slot;
+      if (etid == 0) MLP_TRACE(2 * sl + 1, 4);
     };
+    // desynchronise the slots: slot 1 starts once slot 0's first tile is
+    // half-way through its chain (its extractor-0 accumulators are ready), so
+    // one slot's exposed latencies overlap the other's work instead of both
+    // stalling together
+    if (sl == 1 && ntiles > 1) {
+      mbar_wait(smem_u32(&bars.acc[0]), 0);  // trunk of slot 0's first tile
+      mbar_wait(smem_u32(&bars.acc[0]), 1);  // extractor 0 of it
+    }
     for (int64_t tile = first; tile < ntiles; tile += step) {
       slot = 0;
       const int64_t k = tile * kTcRows + row;
@@ -953,21 +1116,36 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a) {
           for (int b = 0; b < 4; ++b) cache_ones(ct + kCacheE1 + b * kCacheE1Bytes, kCacheKtE1, row, 32);
         }
       }
-      {  // latent -> X (the other slot hides the load latency)
-        float4 lat[8];
-        const float4* src = reinterpret_cast<const float4*>(a.latent + (valid ? k : 0) * 64 + 32 * half);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) lat[c] = valid ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < 8; c += 2) {
-          float v[8] = {lat[c].x, lat[c].y, lat[c].z, lat[c].w, lat[c + 1].x, lat[c + 1].y, lat[c + 1].z, lat[c + 1].w};
-          store_split8(R, 64, row, 32 * half + 4 * c, v);
-          if (CACHE) cache_split8(ct + kCacheLat, kCacheKtLat, row, 32 * half + 4 * c, v);
+      // L2 prefetches (no registers held) of the cloud rows this thread
+      // updates at the end of the tile, so those loads hit L2 instead of
+      // exposing DRAM latency on the chain
+      if (valid) {
+        if (half == 0) {
+          prefetch_l2(a.pos + 3 * k);
+          prefetch_l2(a.rot + 4 * k);
+        } else {
+          prefetch_l2(a.ls + 3 * k);
+          prefetch_l2(a.op + k);
         }
-        signal();
+        if (p.enable_feat) prefetch_l2(a.feat + (int64_t)p.D * k);
       }
       for (int l = 0; l < p.depth; ++l) {
         wait_acc();
+        if (CACHE && l == 0) {
+          // the latent image into the cache (KT 72, row-group-major) from the
+          // TMA image (column-block-major); the slot's 256 epilogue threads
+          // meet at a named barrier before any of them overwrites the region
+          // with the hidden layer
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int c = 16 * i + 8 * half;
+            const int so = (c >> 3) * 2048 + row * 16, co = core_off(row, c, kCacheKtLat);
+            *reinterpret_cast<uint4*>(ct + kCacheLat + co) = *reinterpret_cast<const uint4*>(R + so);
+            *reinterpret_cast<uint4*>(ct + kCacheLat + kTcRows * kCacheKtLat * 2 + co) =
+                *reinterpret_cast<const uint4*>(R + kTcRows * 64 * 2 + so);
+          }
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + sl), "r"(kTcEpiThreads) : "memory");
+        }
         const float* tb = bias_f + p.off_b_trunk[l] / 4;
         if (l + 1 < p.depth) {
           epilogue_to_operand(tmem_row, 128, 64, tb, true, R, 64, 0, row, half);
@@ -1101,7 +1279,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "r"(2 * kTmemCols));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(0u), "r"(2 * kTmemCols));
 }
 
 // ---------------------------------------------------------------------------
@@ -1239,9 +1417,9 @@ static int build_plan(const Fs4dDeformNet& n, const Fs4dHexPlane& f, double t, T
 #ifdef FS4D_MLP_TRACE
 extern "C" int fs4d_debug_mlp_trace(long long* out, int* n) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_mlp_trace, sizeof(long long) * 1024);
-  cudaMemcpyFromSymbol(n, g_mlp_n, sizeof(int) * 2);
-  int z[2] = {0, 0};
+  cudaMemcpyFromSymbol(out, g_mlp_trace, sizeof(long long) * 2048);
+  cudaMemcpyFromSymbol(n, g_mlp_n, sizeof(int) * 4);
+  int z[4] = {0, 0, 0, 0};
   cudaMemcpyToSymbol(g_mlp_n, z, sizeof(z));
   return 0;
 }
@@ -1319,9 +1497,44 @@ size_t tc_workspace_bytes(const Fs4dDeformNet& n, int64_t K) {
   memset(&f, 0, sizeof(f));
   TcPlan p;
   build_plan(n, f, 0.0, p, nullptr);
-  // forward: latent [K, 64]; backward: d_latent [K, 64] + one weight-gradient partial per SM
-  return (size_t)p.ws_bytes + (size_t)K * 64 * 4 + (size_t)kNumSMs * kPartStride * 4 + 512 +
+  // forward: latent [K, 64] (fp32 rows, or per-tile operand images of the same
+  // size rounded up to whole tiles); backward: d_latent [K, 64] + one
+  // weight-gradient partial per SM
+  return (size_t)p.ws_bytes + (size_t)ceil_div(K, kTcRows) * kTcRows * 64 * 4 + (size_t)kNumSMs * kPartStride * 4 + 512 +
          (size_t)kTimeParts * kTimePartFloats * 4;
+}
+
+// 2-D tensor map over the [K][hi 64 | lo 64] bf16 latent rows: box of 8
+// elements (one 16-byte column block) x 128 rows.  The encode entry point comes
+// from the driver through the runtime (no -lcuda); maps are cached per
+// (address, K) since the workspace rarely moves.
+static int lat_tensor_map(const void* base, int64_t K, CUtensorMap* out) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(FS4D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  thread_local const void* last_base = nullptr;
+  thread_local int64_t last_K = -1;
+  thread_local CUtensorMap last;
+  if (base != last_base || K != last_K) {
+    const cuuint64_t dims[2] = {128, (cuuint64_t)K};
+    const cuuint64_t strides[1] = {256};
+    const cuuint32_t box[2] = {8, (cuuint32_t)kTcRows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&last, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FS4D_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    last_base = base;
+    last_K = K;
+  }
+  *out = last;
+  return FS4D_OK;
 }
 
 int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
@@ -1340,9 +1553,22 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   // occupancy.  It stays opt-in (FS4D_FUSED_GATHER=1).
   const bool fused = !cache && getenv("FS4D_FUSED_GATHER") && (!p.enable_grid || (p.C == 32 && p.levels == 2));
   const unsigned gblocks = (unsigned)ceil_div(K, kGatherWarps * 32);
+  const bool time_rows = p.rows_ok && !getenv("FS4D_NO_TIME_ROWS");
+  // two tile pipelines per CTA whenever the weights + two 64 KB regions fit
+  // (depth-1 trunk: 94 + 128 KB) and the gather can emit operand images;
+  // FS4D_MLP_SLOTS=1 keeps the single-slot kernel
+  const int smem2 = ((p.fwd_bytes + 1023) & ~1023) + 2 * kTc2Region;
+  static const bool one_slot = getenv("FS4D_MLP_SLOTS") && atoi(getenv("FS4D_MLP_SLOTS")) == 1;
+  const bool two_slot = !fused && !one_slot && time_rows && smem2 <= kMaxDynSmemBytes;
+  // two-slot path: bf16 hi|lo latent rows (256 B per Gaussian, the size of
+  // the fp32 rows) in the latent workspace
+  uint8_t* img = reinterpret_cast<uint8_t*>(latent);
   StageTimer st_gather(fused ? -1 : FS4D_STAGE_DEFORM_GATHER, s);
   if (!fused) {
-    if (p.rows_ok && !getenv("FS4D_NO_TIME_ROWS"))
+    if (two_slot)
+      k_hexplane_latent_c32t<2, true><<<gblocks, kGatherWarps * 32, 0, s>>>(
+          p, K, cloud.positions, reinterpret_cast<const float*>(blob + p.off_rows), nullptr, img);
+    else if (time_rows)
       k_hexplane_latent_c32t<2><<<gblocks, kGatherWarps * 32, 0, s>>>(
           p, K, cloud.positions, reinterpret_cast<const float*>(blob + p.off_rows), latent);
     else if (p.enable_grid && p.C == 32 && p.levels == 2)
@@ -1356,6 +1582,7 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   a.p = p;
   a.K = K;
   a.latent = latent;
+  a.lat_img = img;
   a.blob = blob;
   a.pos = cloud.positions;
   a.rot = cloud.rotations;
@@ -1372,18 +1599,17 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   const int64_t ntiles = ceil_div(K, kTcRows);
   static const int grid_cap = getenv("FS4D_MLP_GRID") ? atoi(getenv("FS4D_MLP_GRID")) : kNumSMs;
   const int grid = (int)(ntiles < grid_cap ? ntiles : grid_cap);
-  // two tile pipelines per CTA whenever the weights + two 64 KB regions fit
-  // (depth-1 trunk: 94 + 128 KB); FS4D_MLP_SLOTS=1 keeps the single-slot kernel
-  const int smem2 = ((p.fwd_bytes + 1023) & ~1023) + 2 * kTc2Region;
-  static const bool one_slot = getenv("FS4D_MLP_SLOTS") && atoi(getenv("FS4D_MLP_SLOTS")) == 1;
-  if (!fused && !one_slot && smem2 <= 232448 - 1024) {
+  if (two_slot) {
+    CUtensorMap tmap;
+    rc = lat_tensor_map(img, K, &tmap);
+    if (rc) return rc;
     const int grid2 = (int)(ceil_div(ntiles, 2) < grid_cap ? ceil_div(ntiles, 2) : grid_cap);
     if (cache) {
       cudaFuncSetAttribute(k_mlp_tc_2s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-      k_mlp_tc_2s<true><<<grid2, kTc2Threads, smem2, s>>>(a);
+      k_mlp_tc_2s<true><<<grid2, kTc2Threads, smem2, s>>>(a, tmap);
     } else {
       cudaFuncSetAttribute(k_mlp_tc_2s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-      k_mlp_tc_2s<false><<<grid2, kTc2Threads, smem2, s>>>(a);
+      k_mlp_tc_2s<false><<<grid2, kTc2Threads, smem2, s>>>(a, tmap);
     }
     return check_launch("deform_tc_2s");
   }

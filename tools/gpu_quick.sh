@@ -2,8 +2,8 @@
 # Quick GPU check after a kernel change: GPU tests (optionally a subset), render bench, launch list.
 # usage: bash tools/gpu_quick.sh [pytest -k expr]
 mkdir -p gpurun_out
-if [ -n "$1" ]; then K="-k $1"; else K=""; fi
-timeout 1200 python -m pytest tests -m gpu -x -q --timeout 900 $K > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
+KEXPR="${1:-}"
+timeout 1200 python -m pytest tests -m gpu -x -q --timeout 900 ${KEXPR:+-k "$KEXPR"} > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
 tail -3 gpurun_out/gpu_tests.log
 timeout 600 python bench.py --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
 python - <<'PY'

@@ -1,10 +1,11 @@
 #!/bin/bash
-# Debug timeline of the single-slot tcgen05 MLP (CTA 0): builds a traced
-# libfs4d.so in place on the GPU box, runs one configs[1] deform, prints events.
+# Debug timeline of the tcgen05 MLP (CTA 0, both slots of the two-slot kernel):
+# builds a traced libfs4d.so in place on the GPU box, runs one configs[1]
+# deform, prints events (who: S<slot> MMA / EPI).
 cd "$(dirname "$0")/.."
 nvcc -DFS4D_MLP_TRACE -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -shared \
   -o paper_2503_06161_b200/libfs4d.so paper_2503_06161_b200/csrc/*.cu || exit 1
-FS4D_MLP_ONE_SLOT=1 python - <<'PY'
+python - <<'PY'
 import ctypes, numpy as np, torch, sys
 sys.path.insert(0, ".")
 import bench
@@ -15,19 +16,19 @@ eng = dv.DeformEngine()
 for _ in range(3):
     eng.forward(c, f, n, 0.3)
 lib = N.load()
-buf = (ctypes.c_longlong * 1024)(); cnt = (ctypes.c_int * 2)()
+buf = (ctypes.c_longlong * 2048)(); cnt = (ctypes.c_int * 4)()
 lib.fs4d_debug_mlp_trace(buf, cnt)   # reset
 eng.forward(c, f, n, 0.3); torch.cuda.synchronize()
 lib.fs4d_debug_mlp_trace(buf, cnt)
 names = {1: "op-ready", 2: "commit", 3: "acc-ready", 4: "signal"}
 ev = []
-for who in range(2):
+for who in range(4):
     for i in range(min(cnt[who], 512)):
         v = buf[who * 512 + i]
         ev.append((v >> 4, who, names[v & 15]))
 ev.sort()
 t0 = ev[0][0]
-for t, who, nm in ev[:160]:
-    print(f"{t - t0:8d} {'MMA' if who == 0 else 'EPI'} {nm}")
-print("events", cnt[0], cnt[1], "span", ev[-1][0] - t0)
+for t, who, nm in ev[:400]:
+    print(f"{t - t0:8d} S{who // 2} {'MMA' if who % 2 == 0 else 'EPI'} {nm}")
+print("events", list(cnt), "span", ev[-1][0] - t0)
 PY
