@@ -1116,18 +1116,34 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __
           for (int b = 0; b < 4; ++b) cache_ones(ct + kCacheE1 + b * kCacheE1Bytes, kCacheKtE1, row, 32);
         }
       }
-      // L2 prefetches (no registers held) of the cloud rows this thread
-      // updates at the end of the tile, so those loads hit L2 instead of
-      // exposing DRAM latency on the chain
+      // the cloud values this thread updates at the end of the tile, loaded
+      // now so their latency hides behind the tile's MMA chain (and the other
+      // slot's work): position + rotation (half 0) or scales + opacity (half
+      // 1), and for D = 16 this thread's 8 feature channels as two float4
+      float cv[7];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) cv[q] = 0.f;
       if (valid) {
         if (half == 0) {
-          prefetch_l2(a.pos + 3 * k);
-          prefetch_l2(a.rot + 4 * k);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) cv[q] = __ldg(a.pos + 3 * k + q);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cv[3 + q] = __ldg(a.rot + 4 * k + q);
         } else {
-          prefetch_l2(a.ls + 3 * k);
-          prefetch_l2(a.op + k);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) cv[q] = __ldg(a.ls + 3 * k + q);
+          cv[3] = __ldg(a.op + k);
         }
-        if (p.enable_feat) prefetch_l2(a.feat + (int64_t)p.D * k);
+      }
+      const bool feat16 = p.enable_feat && p.D == 16 &&
+                          ((reinterpret_cast<uintptr_t>(a.feat) | reinterpret_cast<uintptr_t>(a.o_feat)) & 15) == 0;
+      float4 fq0 = make_float4(0.f, 0.f, 0.f, 0.f), fq1 = fq0;
+      if (feat16 && valid) {
+        const float4* fr = reinterpret_cast<const float4*>(a.feat + 16 * k + 8 * half);
+        fq0 = __ldg(fr);
+        fq1 = __ldg(fr + 1);
+      } else if (p.enable_feat && valid) {
+        prefetch_l2(a.feat + (int64_t)p.D * k);
       }
       for (int l = 0; l < p.depth; ++l) {
         wait_acc();
@@ -1200,22 +1216,6 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __
           }
         }
       }
-      // the cloud values this thread updates (loads in flight during the head MMAs)
-      float cv[7];
-#pragma unroll
-      for (int q = 0; q < 7; ++q) cv[q] = 0.f;
-      if (valid) {
-        if (half == 0) {
-#pragma unroll
-          for (int q = 0; q < 3; ++q) cv[q] = a.pos[3 * k + q];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) cv[3 + q] = a.rot[4 * k + q];
-        } else {
-#pragma unroll
-          for (int q = 0; q < 3; ++q) cv[q] = a.ls[3 * k + q];
-          cv[3] = a.op[k];
-        }
-      }
       wait_acc();
       {
         const float* hb = bias_f + p.off_b_head / 4;
@@ -1235,7 +1235,21 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __
           }
         }
       }
-      if (p.enable_feat) {
+      if (feat16) {
+        epilogue_to_operand(tmem_row, 192, 32, bias_f + p.off_b_f1 / 4, true, R, 32, 0, row, half,
+                            CACHE ? ct + kCacheFF : nullptr, kCacheKtFF, 0);
+        signal();
+        wait_acc();
+        const float* fb = bias_f + p.off_b_f2 / 4 + 8 * half;
+        float v[8];
+        tmem_ld8(tmem_row + 8 * half, v);
+        if (valid) {
+          const float4 b0 = *reinterpret_cast<const float4*>(fb), b1 = *reinterpret_cast<const float4*>(fb + 4);
+          float4* o = reinterpret_cast<float4*>(a.o_feat + 16 * k + 8 * half);
+          o[0] = make_float4(fq0.x + v[0] + b0.x, fq0.y + v[1] + b0.y, fq0.z + v[2] + b0.z, fq0.w + v[3] + b0.w);
+          o[1] = make_float4(fq1.x + v[4] + b1.x, fq1.y + v[5] + b1.y, fq1.z + v[6] + b1.z, fq1.w + v[7] + b1.w);
+        }
+      } else if (p.enable_feat) {
         float fv[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
