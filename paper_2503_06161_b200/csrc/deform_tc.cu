@@ -220,67 +220,6 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPl
       }
   }
   __syncwarp();
-  if (IMG) {
-    // lane = (Gaussian j%8, 8-channel block): each lane ends with one 16-byte
-    // hi and one 16-byte lo chunk, and a warp's store covers 8 rows x 4 column
-    // blocks = four full 128-byte core-matrix rows (coalesced)
-    const int sub8 = lane >> 2, c8 = (lane & 3) * 8;
-    for (int j0 = 0; j0 < 32; j0 += 8) {
-      const int j = j0 + sub8;
-      const int64_t k = __shfl_sync(0xffffffffu, kg, j);
-#pragma unroll
-      for (int l = 0; l < LEVELS; ++l) {
-        float pr[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) pr[i] = 1.f;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const float2 f = s_f[warp][l * 6 + q][j];
-          if (q == 2 || q == 4 || q == 5) {
-            const int tq = q == 2 ? 0 : (q == 4 ? 1 : 2);
-            const float* rp = rows + p.row_off[l][tq] + s_base[warp][l * 6 + q][j] + c8;
-            const float4 a0 = __ldg(reinterpret_cast<const float4*>(rp));
-            const float4 a1 = __ldg(reinterpret_cast<const float4*>(rp + 4));
-            const float4 c0 = __ldg(reinterpret_cast<const float4*>(rp + 32));
-            const float4 c1 = __ldg(reinterpret_cast<const float4*>(rp + 36));
-            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-            const float wa = 1.f - f.x;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) pr[i] *= wa * av[i] + f.x * cv[i];
-          } else {
-            const int rs = p.res[l][q][1] * 32;
-            const float* pl = p.planes[l][q] + s_base[warp][l * 6 + q][j] + c8;
-            const float w00 = (1.f - f.x) * (1.f - f.y), w10 = f.x * (1.f - f.y);
-            const float w01 = (1.f - f.x) * f.y, w11 = f.x * f.y;
-            const float4 a0 = PLANE_LD(reinterpret_cast<const float4*>(pl));
-            const float4 a1 = PLANE_LD(reinterpret_cast<const float4*>(pl + 4));
-            const float4 b0 = PLANE_LD(reinterpret_cast<const float4*>(pl + 32));
-            const float4 b1 = PLANE_LD(reinterpret_cast<const float4*>(pl + 36));
-            const float4 c0 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs));
-            const float4 c1 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs + 4));
-            const float4 d0 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs + 32));
-            const float4 d1 = PLANE_LD(reinterpret_cast<const float4*>(pl + rs + 36));
-            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-            const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-            const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-            // hexplane.py:105-106 order: (1-fa)(1-fb)p00 + fa(1-fb)p10 + (1-fa)fb p01 + fa fb p11
-#pragma unroll
-            for (int i = 0; i < 8; ++i) pr[i] *= w00 * av[i] + w10 * cv[i] + w01 * bv[i] + w11 * dv[i];
-          }
-        }
-        if (k < K) {
-          uint4 h, lo;
-          split8(pr, h, lo);
-          uint8_t* row = img + k * 256 + (l * 32 + c8) * 2;
-          *reinterpret_cast<uint4*>(row) = h;
-          *reinterpret_cast<uint4*>(row + 128) = lo;
-        }
-      }
-    }
-    return;
-  }
   const int sub = lane >> 3, ch = (lane & 7) * 4;
   for (int j0 = 0; j0 < 32; j0 += 4) {
     const int j = j0 + sub;
@@ -316,7 +255,20 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPl
           prod.w *= w00 * a.w + w10 * c.w + w01 * b.w + w11 * d.w;
         }
       }
-      if (k < K) *reinterpret_cast<float4*>(latent + k * 64 + l * 32 + ch) = prod;
+      if (k < K) {
+        if (IMG) {  // bf16 hi | lo row (8 lanes x 8 B = one 64 B run per level and half)
+          const uint32_t h01 = cvt_bf16x2(prod.x, prod.y), h23 = cvt_bf16x2(prod.z, prod.w);
+          const uint32_t l01 =
+              cvt_bf16x2(prod.x - __uint_as_float(h01 << 16), prod.y - __uint_as_float(h01 & 0xFFFF0000u));
+          const uint32_t l23 =
+              cvt_bf16x2(prod.z - __uint_as_float(h23 << 16), prod.w - __uint_as_float(h23 & 0xFFFF0000u));
+          uint8_t* rowp = img + k * 256 + (l * 32 + ch) * 2;
+          *reinterpret_cast<uint2*>(rowp) = make_uint2(h01, h23);
+          *reinterpret_cast<uint2*>(rowp + 128) = make_uint2(l01, l23);
+        } else {
+          *reinterpret_cast<float4*>(latent + k * 64 + l * 32 + ch) = prod;
+        }
+      }
     }
   }
 }
