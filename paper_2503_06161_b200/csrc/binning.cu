@@ -74,11 +74,25 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __r
     for (int ty = t.z; ty <= t.w; ++ty)
       for (int tx = t.x; tx <= t.y; ++tx) atomicAdd(&cnt[ty * ntx + tx], 1u);
   __syncthreads();
-  if (smem)
-    for (int b = threadIdx.x; b < ntiles; b += blockDim.x) {
-      const uint32_t c = cnt[b];
-      if (c) base[b] = (uint32_t)toff[b] + atomicAdd(&tcur[b], c);  // this block's slice of the segment
-      cnt[b] = 0;
+  if (smem)  // reserve this block's slice of every touched segment: four independent atomics in flight per thread
+    for (int b0 = threadIdx.x; b0 < ntiles; b0 += 4 * kEmitThreads) {
+      uint32_t c[4], r[4], o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int b = b0 + j * kEmitThreads;
+        c[j] = b < ntiles ? cnt[b] : 0u;
+        o[j] = c[j] ? (uint32_t)toff[b] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = c[j] ? atomicAdd(&tcur[b0 + j * kEmitThreads], c[j]) : 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int b = b0 + j * kEmitThreads;
+        if (b < ntiles) {
+          if (c[j]) base[b] = o[j] + r[j];
+          cnt[b] = 0;
+        }
+      }
     }
   __syncthreads();
   if (!kept) return;
@@ -300,12 +314,135 @@ __device__ void cta_radix_sort_tile(const unsigned long long* __restrict__ src, 
   for (int q = threadIdx.x; q < n; q += blockDim.x) out_vals[q] = (uint32_t)xbuf[q];
 }
 
+// CTA-wide sort of one tile's list by bucketing: each key goes to one of NB
+// buckets (NB ~ n, at most 4096) by a monotone map of its depth bits onto the
+// tile's [min, max] range, the buckets are laid out by one prefix sum, and the
+// few keys of each bucket are put in order by one thread (insertion sort on
+// (depth bits, exact fp64 depth, source index) -- the total order the
+// reference's stable float64 argsort produces).  One scatter instead of three
+// stable 8-bit LSD passes; the order inside a bucket before its sort (shared-
+// memory atomics) never matters because the final order is total.  Returns
+// false, having written nothing, when some bucket holds more than
+// kBucketMax keys (strongly clustered depths); the caller then runs the radix
+// sort.
+constexpr int kBucketMax = 64;
+constexpr int kBucketNB = kTileSortWarps * 256;  // bucket counters reuse the radix sort's warp counters
+
+__device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src, int n, const double* __restrict__ z64,
+                                     uint32_t* __restrict__ out_vals, unsigned long long* xbuf, uint32_t* cnt,
+                                     uint32_t* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int R = (n + kTileSortThreads - 1) / kTileSortThreads;
+  uint32_t key[kTileSortIPT], val[kTileSortIPT];
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll
+  for (int r = 0; r < kTileSortIPT; ++r) {
+    const int q = r * kTileSortThreads + threadIdx.x;
+    const unsigned long long kv = (r < R && q < n) ? src[q] : 0xFFFFFFFFFFFFFFFFull;
+    key[r] = (uint32_t)(kv >> 32);
+    val[r] = (uint32_t)kv;
+    if (r < R && q < n) {
+      kmin = min(kmin, key[r]);
+      kmax = max(kmax, key[r]);
+    }
+  }
+  int NB = 32;
+  while (NB < n && NB < kBucketNB) NB <<= 1;
+  for (int b = threadIdx.x; b < NB; b += kTileSortThreads) cnt[b] = 0;
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (lane == 0) {
+    red[2 * warp] = kmin;
+    red[2 * warp + 1] = kmax;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int w = 0; w < kTileSortWarps; ++w) {
+    kmin = min(kmin, red[2 * w]);
+    kmax = max(kmax, red[2 * w + 1]);
+  }
+  // monotone (non-decreasing) key -> bucket map: fp32 conversion and a
+  // positive scale preserve order, truncation keeps it weak
+  const float scale = (float)NB / ((float)(kmax - kmin) + 1.0f);
+#pragma unroll
+  for (int r = 0; r < kTileSortIPT; ++r) {
+    if (r >= R) break;
+    if (r * kTileSortThreads + (int)threadIdx.x < n) atomicAdd(&cnt[min(NB - 1, (int)((float)(key[r] - kmin) * scale))], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of the NB counters (E consecutive per thread) + the largest bucket
+  const int E = (NB + kTileSortThreads - 1) / kTileSortThreads;
+  const int b0 = threadIdx.x * E;
+  uint32_t c[kBucketNB / kTileSortThreads > 0 ? kBucketNB / kTileSortThreads : 1];
+  uint32_t tsum = 0, tmax = 0;
+#pragma unroll
+  for (int e = 0; e < (int)(sizeof(c) / sizeof(c[0])); ++e) {
+    c[e] = (e < E && b0 + e < NB) ? cnt[b0 + e] : 0u;
+    tsum += c[e];
+    tmax = max(tmax, c[e]);
+  }
+  uint32_t incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  tmax = __reduce_max_sync(0xffffffffu, tmax);
+  __syncthreads();  // everyone has read cnt / red
+  if (lane == 31) red[warp] = incl;
+  if (lane == 0) red[kTileSortWarps + warp] = tmax;
+  __syncthreads();
+  uint32_t wbase = 0, bmax = 0;
+#pragma unroll 4
+  for (int w = 0; w < kTileSortWarps; ++w) {
+    if (w < warp) wbase += red[w];
+    bmax = max(bmax, red[kTileSortWarps + w]);
+  }
+  if (bmax > (uint32_t)kBucketMax) return false;  // block-uniform
+  {
+    uint32_t run = wbase + incl - tsum;
+#pragma unroll
+    for (int e = 0; e < (int)(sizeof(c) / sizeof(c[0])); ++e)
+      if (e < E && b0 + e < NB) {
+        cnt[b0 + e] = run;
+        run += c[e];
+      }
+  }
+  __syncthreads();
+  // scatter through per-bucket cursors (the bucket starts); afterwards
+  // cnt[b] is the end of bucket b, i.e. the start of bucket b + 1
+#pragma unroll
+  for (int r = 0; r < kTileSortIPT; ++r) {
+    if (r >= R) break;
+    if (r * kTileSortThreads + (int)threadIdx.x < n) {
+      const int b = min(NB - 1, (int)((float)(key[r] - kmin) * scale));
+      xbuf[atomicAdd(&cnt[b], 1u)] = ((unsigned long long)key[r] << 32) | val[r];
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < NB; b += kTileSortThreads) {
+    const int s0 = b > 0 ? (int)cnt[b - 1] : 0, s1 = (int)cnt[b];
+    for (int a = s0 + 1; a < s1; ++a) {
+      const unsigned long long ka = xbuf[a];
+      int q = a - 1;
+      while (q >= s0 && key_less(ka, xbuf[q], z64)) {
+        xbuf[q + 1] = xbuf[q];
+        --q;
+      }
+      xbuf[q + 1] = ka;
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < n; q += kTileSortThreads) out_vals[q] = (uint32_t)xbuf[q];
+  return true;
+}
+
 __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long long* __restrict__ pkey,
                                                                 const uint64_t* __restrict__ toff,
                                                                 const uint32_t* __restrict__ tcnt, int ntiles,
                                                                 int64_t cap, const double* __restrict__ z64,
                                                                 uint32_t* __restrict__ pvals, uint2* __restrict__ ranges,
-                                                                const int32_t* __restrict__ tperm) {
+                                                                const int32_t* __restrict__ tperm, int radix_only) {
   extern __shared__ unsigned long long s_keys[];  // kSortSmemKeys exchange buffer (dynamic, 64 KB)
   __shared__ uint32_t wcnt[kTileSortWarps * 256];
   __shared__ uint32_t dbase[256];
@@ -318,7 +455,11 @@ __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long lo
   if (n == 0) return;
   unsigned long long* keys = pkey + off;
   if (n <= kSortSmemKeys) {
-    cta_radix_sort_tile(keys, n, z64, pvals + off, s_keys, wcnt, dbase);
+    static_assert(kTileSortThreads * kTileSortIPT >= kSortSmemKeys, "bucket sort covers the smem tile size");
+    if (radix_only || !cta_bucket_sort_tile(keys, n, z64, pvals + off, s_keys, wcnt, dbase)) {
+      __syncthreads();
+      cta_radix_sort_tile(keys, n, z64, pvals + off, s_keys, wcnt, dbase);
+    }
   } else {
     bitonic_sort(keys, n, z64);  // oversized tile: in place in global memory (L2-resident)
     for (int q = threadIdx.x; q < n; q += blockDim.x) pvals[off + q] = (uint32_t)keys[q];
@@ -602,6 +743,8 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
   if (K > 0)
     k_emit_partition<<<(unsigned)ceil_div(K, kEmitThreads), kEmitThreads, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles,
                                                                                 toff, tcur, L.cap, pkey);
+  // FS4D_TILE_SORT=radix: the three-pass LSD radix sort for every tile (A/B)
+  static const int radix_only = getenv("FS4D_TILE_SORT") && !strcmp(getenv("FS4D_TILE_SORT"), "radix");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmemKeys * 8);
@@ -613,7 +756,8 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
                                                                      at<uint2>(ws, L.ranges),
                                                                      L.ntiles <= 64 * kTileScanThreads
                                                                          ? at<int32_t>(ws, L.tperm)
-                                                                         : nullptr);
+                                                                         : nullptr,
+                                                                     radix_only);
 }
 
 }  // namespace fs4d
