@@ -34,7 +34,8 @@
 
 namespace fs4d {
 
-constexpr int kHistMaxTiles = 6144;   // shared-memory histogram capacity (24 KB)
+constexpr int kHistMaxTiles = 5888;   // shared-memory histogram capacity (23 KB; configs[3] has 5120 tiles)
+constexpr int kTileScanThreads = 1024;
 constexpr int kSortSmemKeys = 8192;   // per-tile keys sorted in shared memory (64 KB)
 #ifndef FS4D_TILE_SORT_THREADS
 #define FS4D_TILE_SORT_THREADS 512
@@ -44,8 +45,91 @@ constexpr int kTileSortThreads = FS4D_TILE_SORT_THREADS;
 __device__ __forceinline__ bool rect_valid(const int4& t) { return t.y >= t.x && t.w >= t.z; }
 
 // key = fp32 depth bits (positive floats order as unsigned) << 32 | source index
+// Body shared by k_tile_scan_check and the fused pair partition: every thread
+// of a kTileScanThreads block.  `base32` (shared memory, optional) receives
+// the offsets saturated at cap as 32-bit values; `toff` (global, optional) the
+// 64-bit offsets; `publish` also writes the densest-first tile order, the
+// pair total, the capacity check and the status words.
+struct TileScanSmem {
+  uint64_t wsum[kTileScanThreads / 32];
+  uint32_t bcnt[33], bcur[33];
+};
+
+__device__ void tile_scan_body(const uint32_t* __restrict__ tcnt, int ntiles, uint64_t* __restrict__ toff,
+                               uint32_t* base32, bool publish, uint32_t* counters, int64_t cap, int32_t* status,
+                               int32_t* __restrict__ tperm, TileScanSmem& sm) {
+  uint64_t* wsum = sm.wsum;
+  uint32_t* bcnt = sm.bcnt;
+  uint32_t* bcur = sm.bcur;
+  const int per = (ntiles + kTileScanThreads - 1) / kTileScanThreads;
+  const int b0 = threadIdx.x * per;
+  uint64_t local = 0;
+  for (int q = 0; q < per; ++q)
+    if (b0 + q < ntiles) local += tcnt[b0 + q];
+  // block-wide exclusive scan of the per-thread sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = wsum[lane];
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    wsum[lane] = wi - w;  // exclusive warp bases
+  }
+  __syncthreads();
+  uint64_t run = wsum[warp] + incl - local;
+  for (int q = 0; q < per; ++q)
+    if (b0 + q < ntiles) {
+      if (toff) toff[b0 + q] = run;
+      if (base32) base32[b0 + q] = (uint32_t)(run < (uint64_t)cap ? run : (uint64_t)cap);
+      run += tcnt[b0 + q];
+    }
+  if (!publish) return;
+  // launch order for the per-tile kernels: tiles by decreasing count (log2
+  // buckets, arbitrary order inside a bucket) so the longest tiles start in
+  // the first wave instead of the tail -- the order never affects results
+  if (tperm) {
+    if (threadIdx.x < 33) bcnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int q = 0; q < per; ++q)
+      if (b0 + q < ntiles) atomicAdd(&bcnt[32 - __clz(tcnt[b0 + q])], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t r = 0;
+      for (int b = 32; b >= 0; --b) {
+        bcur[b] = r;
+        r += bcnt[b];
+      }
+    }
+    __syncthreads();
+    for (int q = 0; q < per; ++q)
+      if (b0 + q < ntiles) tperm[atomicAdd(&bcur[32 - __clz(tcnt[b0 + q])], 1u)] = b0 + q;
+  }
+  if (threadIdx.x == kTileScanThreads - 1) {
+    const uint64_t total = run;
+    *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64) = total;
+    counters[CNT_PAIRS_CLAMPED] = (uint32_t)(total < (uint64_t)cap ? total : (uint64_t)cap);
+    if (status) {
+      status[FS4D_ST_N_VISIBLE] = (int32_t)counters[CNT_VISIBLE];
+      status[FS4D_ST_PAIRS_LO] = (int32_t)(total & 0xFFFFFFFFu);
+      status[FS4D_ST_PAIRS_HI] = (int32_t)(total >> 32);
+      if (total > (uint64_t)cap) raise_status(status, FS4D_ERR_CAPACITY);
+    }
+  }
+}
+
 #ifndef FS4D_EMIT_THREADS
-#define FS4D_EMIT_THREADS 256
+#define FS4D_EMIT_THREADS 1024
 #endif
 constexpr int kEmitThreads = FS4D_EMIT_THREADS;
 // One Gaussian per thread.  The block counts its pairs per tile in shared
@@ -54,16 +138,28 @@ constexpr int kEmitThreads = FS4D_EMIT_THREADS;
 // 32-bit: pair capacities stay below 2^32) in shared memory, so the emission
 // loop is shared-memory atomics + one store per pair (no global load of the
 // segment offset on the per-pair critical path).
+//
+// FUSED (kEmitThreads == kTileScanThreads, tiles fit in shared memory): the
+// tile-offset scan is done by every block into shared memory (1280 counts at
+// configs[1]: a few hundred cycles, in parallel) and published by block 0
+// (global offsets, densest-first order, pair total, status) -- one launch and
+// one serial single-block kernel fewer on the frame's critical path.
+template <bool FUSED>
 __global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __restrict__ tile_rect,
                                                         const uint32_t* __restrict__ dkeys, int64_t K, int ntx,
-                                                        int ntiles, const uint64_t* __restrict__ toff,
+                                                        int ntiles, uint64_t* __restrict__ toff,
                                                         uint32_t* __restrict__ tcur, int64_t cap,
-                                                        unsigned long long* __restrict__ pkey) {
+                                                        unsigned long long* __restrict__ pkey,
+                                                        const uint32_t* __restrict__ tcnt, uint32_t* counters,
+                                                        int32_t* status, int32_t* __restrict__ tperm) {
   __shared__ uint32_t cnt[kHistMaxTiles];
   __shared__ uint32_t base[kHistMaxTiles];
-  const bool smem = ntiles <= kHistMaxTiles && cap <= (int64_t)0xFFFFFFFFu;
+  __shared__ TileScanSmem scan_sm;
+  const bool smem = FUSED || (ntiles <= kHistMaxTiles && cap <= (int64_t)0xFFFFFFFFu);
   if (smem)
     for (int b = threadIdx.x; b < ntiles; b += blockDim.x) cnt[b] = 0;
+  if (FUSED) tile_scan_body(tcnt, ntiles, blockIdx.x == 0 ? toff : nullptr, base, blockIdx.x == 0, counters, cap,
+                            status, tperm, scan_sm);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t dk = i < K ? dkeys[i] : 0xFFFFFFFFu;
@@ -81,7 +177,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __r
       for (int j = 0; j < 4; ++j) {
         const int b = b0 + j * kEmitThreads;
         c[j] = b < ntiles ? cnt[b] : 0u;
-        o[j] = c[j] ? (uint32_t)toff[b] : 0u;
+        o[j] = c[j] ? (FUSED ? base[b] : (uint32_t)toff[b]) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) r[j] = c[j] ? atomicAdd(&tcur[b0 + j * kEmitThreads], c[j]) : 0u;
@@ -469,76 +565,12 @@ __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long lo
 // Tile offsets for up to a few tens of thousands of tiles in ONE block:
 // exclusive scan of the per-tile counts (u64 offsets), the pair total, and
 // the capacity check -- one launch instead of a 3-kernel device scan + check.
-constexpr int kTileScanThreads = 1024;
 __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan_check(const uint32_t* __restrict__ tcnt, int ntiles,
                                                                       uint64_t* __restrict__ toff, uint32_t* counters,
                                                                       int64_t cap, int32_t* status,
                                                                       int32_t* __restrict__ tperm) {
-  __shared__ uint64_t wsum[kTileScanThreads / 32];
-  __shared__ uint32_t bcnt[33], bcur[33];
-  const int per = (ntiles + kTileScanThreads - 1) / kTileScanThreads;
-  const int b0 = threadIdx.x * per;
-  uint64_t local = 0;
-  for (int q = 0; q < per; ++q)
-    if (b0 + q < ntiles) local += tcnt[b0 + q];
-  // block-wide exclusive scan of the per-thread sums
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    uint64_t w = wsum[lane];
-    uint64_t wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
-    }
-    wsum[lane] = wi - w;  // exclusive warp bases
-  }
-  __syncthreads();
-  uint64_t run = wsum[warp] + incl - local;
-  for (int q = 0; q < per; ++q)
-    if (b0 + q < ntiles) {
-      toff[b0 + q] = run;
-      run += tcnt[b0 + q];
-    }
-  // launch order for the per-tile kernels: tiles by decreasing count (log2
-  // buckets, arbitrary order inside a bucket) so the longest tiles start in
-  // the first wave instead of the tail -- the order never affects results
-  if (tperm) {
-    if (threadIdx.x < 33) bcnt[threadIdx.x] = 0;
-    __syncthreads();
-    for (int q = 0; q < per; ++q)
-      if (b0 + q < ntiles) atomicAdd(&bcnt[32 - __clz(tcnt[b0 + q])], 1u);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t r = 0;
-      for (int b = 32; b >= 0; --b) {
-        bcur[b] = r;
-        r += bcnt[b];
-      }
-    }
-    __syncthreads();
-    for (int q = 0; q < per; ++q)
-      if (b0 + q < ntiles) tperm[atomicAdd(&bcur[32 - __clz(tcnt[b0 + q])], 1u)] = b0 + q;
-  }
-  if (threadIdx.x == kTileScanThreads - 1) {
-    const uint64_t total = run;
-    *reinterpret_cast<uint64_t*>(counters + CNT_PAIRS64) = total;
-    counters[CNT_PAIRS_CLAMPED] = (uint32_t)(total < (uint64_t)cap ? total : (uint64_t)cap);
-    if (status) {
-      status[FS4D_ST_N_VISIBLE] = (int32_t)counters[CNT_VISIBLE];
-      status[FS4D_ST_PAIRS_LO] = (int32_t)(total & 0xFFFFFFFFu);
-      status[FS4D_ST_PAIRS_HI] = (int32_t)(total >> 32);
-      if (total > (uint64_t)cap) raise_status(status, FS4D_ERR_CAPACITY);
-    }
-  }
+  __shared__ TileScanSmem sm;
+  tile_scan_body(tcnt, ntiles, toff, nullptr, true, counters, cap, status, tperm, sm);
 }
 
 __global__ void k_pairs_check2(uint32_t* counters, int64_t cap, int32_t* status) {
@@ -705,7 +737,11 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
   uint32_t* tcur = at<uint32_t>(ws, L.tcur);
   uint64_t* toff = at<uint64_t>(ws, L.toff64);
   // tcnt / tcur / ranges were zeroed and tcnt filled by k_preprocess's fused histogram
-  if (L.ntiles <= 64 * kTileScanThreads) {
+  const bool fused_scan = K > 0 && kEmitThreads == kTileScanThreads && L.ntiles <= kHistMaxTiles &&
+                          L.cap <= (int64_t)0xFFFFFFFFu && !depth_binning_ok(L);
+  if (fused_scan) {
+    // (the pair partition below computes and publishes the tile offsets)
+  } else if (L.ntiles <= 64 * kTileScanThreads) {
     k_tile_scan_check<<<1, kTileScanThreads, 0, s>>>(tcnt, L.ntiles, toff, counters, L.cap, status,
                                                       at<int32_t>(ws, L.tperm));
   } else {
@@ -740,9 +776,13 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
     return;
   }
   unsigned long long* pkey = at<unsigned long long>(ws, L.pkey64);
-  if (K > 0)
-    k_emit_partition<<<(unsigned)ceil_div(K, kEmitThreads), kEmitThreads, 0, s>>>(tile_rect, dkeys, K, L.ntx, L.ntiles,
-                                                                                toff, tcur, L.cap, pkey);
+  if (fused_scan)
+    k_emit_partition<true><<<(unsigned)ceil_div(K, kEmitThreads), kEmitThreads, 0, s>>>(
+        tile_rect, dkeys, K, L.ntx, L.ntiles, toff, tcur, L.cap, pkey, tcnt, counters, status,
+        at<int32_t>(ws, L.tperm));
+  else if (K > 0)
+    k_emit_partition<false><<<(unsigned)ceil_div(K, kEmitThreads), kEmitThreads, 0, s>>>(
+        tile_rect, dkeys, K, L.ntx, L.ntiles, toff, tcur, L.cap, pkey, nullptr, nullptr, nullptr, nullptr);
   // FS4D_TILE_SORT=radix: the three-pass LSD radix sort for every tile (A/B)
   static const int radix_only = getenv("FS4D_TILE_SORT") && !strcmp(getenv("FS4D_TILE_SORT"), "radix");
   static bool attr = false;
