@@ -81,9 +81,12 @@ MLP_FLOPS = 2 * 21344 * K_GAUSS
 
 
 # stage (library profiler id) -> the single kernel it times (traffic lookup)
-STAGE_KERNEL = {"deform_gather": "k_hexplane_latent_c32t", "deform_mlp": "k_mlp_tc_ws", "preprocess": "k_preprocess",
+STAGE_KERNEL = {"deform_gather": "k_hexplane_latent_c32t", "deform_mlp": "k_mlp_tc_2s", "preprocess": "k_preprocess",
                 "blend": "k_blend"}
-TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r1_traffic.json")
+# per-kernel DRAM traffic + SM utilisation of one `ncu --set full` launch of
+# the current kernels (tools/ncu_traffic.py), the newest round's file first
+TRAFFIC_JSON = next((f for f in (os.path.join(ROOT, "profiles", n) for n in ("r2_traffic.json", "r1_traffic.json"))
+                     if os.path.exists(f)), os.path.join(ROOT, "profiles", "r2_traffic.json"))
 
 
 def stage_bytes(stage, n_visible, n_pairs):
@@ -599,9 +602,9 @@ def train_bench(args, rank, world, local):
 
 def launches_per_frame():
     """libfs4d kernels per frame: deform (pack, HexPlane latent, tcgen05 MLP) and
-    render (status reset, preprocess + fused tile histogram, single-block tile
-    scan + pair check, partition, per-tile sort, blend)."""
-    return 3 + (1 + 1 + 1 + 1 + 1 + 1)
+    render (status reset, preprocess + fused tile histogram, pair partition
+    with the fused tile-offset scan, per-tile sort, blend)."""
+    return 3 + (1 + 1 + 1 + 1 + 1)
 
 
 def main():
@@ -712,7 +715,7 @@ def main():
                            "achieved_gbs": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9,
                            "frac": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9 / hbm},
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items() if v},
-        "mlp": {"flops_per_frame": MLP_FLOPS, "kernel": "k_mlp_tc_ws (bf16x3 on tcgen05: 3x these flops issued)",
+        "mlp": {"flops_per_frame": MLP_FLOPS, "kernel": "k_mlp_tc_2s (bf16x3 on tcgen05: 3x these flops issued)",
                 "tflops": MLP_FLOPS / (stage_ms["deform_mlp"] / 1000.0) / 1e12 if stage_ms.get("deform_mlp") else None,
                 "peak_bf16_tflops": tf, "frac_of_bf16_peak_issued": 3 * MLP_FLOPS / (stage_ms["deform_mlp"] / 1000.0)
                 / 1e12 / tf if stage_ms.get("deform_mlp") else None},

@@ -1,5 +1,6 @@
-"""Write profiles/r1_profile_latest.md (+ copies of the bench JSON lines, launch
-lists and the traffic table) from a tools/gpu_profiles.sh run in gpurun_out/."""
+"""Write profiles/<round>_profile_latest.md (+ copies of the bench JSON lines,
+launch lists and the traffic table) from a tools/gpu_profiles.sh run in
+gpurun_out/.  usage: python tools/write_profile_md.py [round, default r2]"""
 import json
 import shutil
 import subprocess
@@ -7,6 +8,7 @@ import sys
 
 G = "gpurun_out"
 P = "profiles"
+R = sys.argv[1] if len(sys.argv) > 1 else "r2"
 
 
 def last_json(path):
@@ -16,23 +18,23 @@ def last_json(path):
 def main():
     b, t, f = last_json(f"{G}/bench.json"), last_json(f"{G}/train.json"), last_json(f"{G}/fine.json")
     r = last_json(f"{G}/ref.json")
-    for name, obj in (("r1_bench_default.json", b), ("r1_train_bench.json", t), ("r1_fine_bench.json", f),
-                      ("r1_reference_arm.json", r)):
+    for name, obj in ((f"{R}_bench_default.json", b), (f"{R}_train_bench.json", t), (f"{R}_fine_bench.json", f),
+                      (f"{R}_reference_arm.json", r)):
         with open(f"{P}/{name}", "w") as fh:
             fh.write(json.dumps(obj) + "\n")
-    shutil.copy(f"{G}/launches.csv", f"{P}/r1_launches_default.csv")
-    shutil.copy(f"{G}/train_launches.csv", f"{P}/r1_launches_train.csv")
-    kernels = ["k_blend", "k_mlp_tc_ws", "k_hexplane_latent_c32t", "k_preprocess", "k_tile_sort", "k_emit_partition"]
-    subprocess.run([sys.executable, "tools/ncu_traffic.py", f"{P}/r1_traffic.json"] +
+    shutil.copy(f"{G}/launches.csv", f"{P}/{R}_launches_default.csv")
+    shutil.copy(f"{G}/train_launches.csv", f"{P}/{R}_launches_train.csv")
+    kernels = ["k_blend", "k_mlp_tc_2s", "k_hexplane_latent_c32t", "k_preprocess", "k_tile_sort", "k_emit_partition"]
+    subprocess.run([sys.executable, "tools/ncu_traffic.py", f"{P}/{R}_traffic.json"] +
                    [f"{G}/full_{k}.ncu-rep" for k in kernels], check=True, capture_output=True)
     run = lambda *a: subprocess.run([sys.executable, "tools/ncu_summary.py", *a], capture_output=True,  # noqa: E731
                                     text=True).stdout
-    l1, l2 = run("launches", f"{P}/r1_launches_default.csv"), run("launches", f"{P}/r1_launches_train.csv")
+    l1, l2 = run("launches", f"{P}/{R}_launches_default.csv"), run("launches", f"{P}/{R}_launches_train.csv")
     full = "\n".join(run("full", f"{G}/full_{k}.ncu-rep") for k in kernels)
     train_kernels = ["k_blend_bwd2", "k_mlp_bwd_tc", "k_hexplane_bwd_c32", "k_preprocess_bwd"]
     full_train = "\n".join(run("full", f"{G}/full_{k}.ncu-rep") for k in train_kernels)
     rf = b["roofline"]
-    txt = f"""# Round 1 — committed-build profile (latest)
+    txt = f"""# Round {R[1:].lstrip("0")} — committed-build profile (latest)
 
 Bench (no profiler, `python bench.py`): **{b['value']:.1f} frames/s** whole-job (configs[2] sequence,
 {b['config']['parallelism']}; {b['config']['l2']}); one frame at a time with an L2 flush between
@@ -67,7 +69,7 @@ Fine-stage iteration (decoder + depth + TV + Adam): {f['value']:.1f} steps/s ({f
 
 {full_train}
 """
-    open(f"{P}/r1_profile_latest.md", "w").write(txt)
+    open(f"{P}/{R}_profile_latest.md", "w").write(txt)
     print(txt[:1800])
 
 
