@@ -862,6 +862,12 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
 }
 
+// operand hand-offs per group of this many chunks / branches (1, 2 or 4):
+// fewer, larger hand-offs when the other slot keeps the tensor pipe busy
+#ifndef FS4D_MLP_HAND
+#define FS4D_MLP_HAND 1
+#endif
+constexpr int kMlpHand = FS4D_MLP_HAND;
 constexpr int kTc2Threads = 2 * kTcWsThreads;
 constexpr int kMaxDynSmemBytes = 232448 - 2048;  // 227 KB opt-in, less the kernel's static barriers
 constexpr int kTc2Region = kTcRows * 128 * 4;  // E hi + lo: 64 KB
@@ -937,17 +943,17 @@ __device__ __forceinline__ void mlp2_issue(const TcArgs& a, const CUtensorMap* t
       commit();
     }
     for (int c = 0; c < 64; c += 16) {  // hidden chunk c -> extractor-0 K step
-      wait_op();
+      if ((c / 16) % kMlpHand == 0) wait_op();
       gemm_bf16x3_w(tmem, sR, 64, c, sW + p.off_ext0, 64, c, 128, 1, c > 0);
     }
     commit();
     for (int b = 0; b < 4; ++b) {  // e1 of branch b -> extractor-1
-      wait_op();
+      if (b % kMlpHand == 0) wait_op();
       gemm_bf16x3_w(tmem + 32 * b, sR, 128, 32 * b, sW + p.off_ext1[b], 32, 0, 32, 2, false);
     }
     commit();
     for (int b = 0; b < 4; ++b) {  // e2 of branch b -> head b and F_feat layer-0 K slice
-      wait_op();
+      if (b % kMlpHand == 0) wait_op();
       gemm_bf16x3_w(tmem + 128 + 16 * b, sR, 128, 32 * b, sW + p.off_head[b], 32, 0, 16, 2, false);
       if (p.enable_feat) gemm_bf16x3_w(tmem + 192, sR, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
     }
@@ -1125,7 +1131,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __
           for (int i = 0; i < 4; ++i) {
             const int c = 16 * i + 8 * half;
             chunk_to_operand(v[i], tb + c, R, 64, c, row, CACHE ? ct + kCacheHid : nullptr, kCacheKtHid, c);
-            signal();
+            if ((i + 1) % kMlpHand == 0) signal();
           }
         }
       }
@@ -1145,7 +1151,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __
               chunk_to_operand(v[2 * j + i], eb + c, R, 128, c, row,
                                CACHE ? ct + kCacheE1 + b * kCacheE1Bytes : nullptr, kCacheKtE1, c - 32 * b);
             }
-            signal();
+            if ((b + 1) % kMlpHand == 0) signal();
           }
         }
       }
@@ -1164,7 +1170,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __
               const int c = 32 * b + 16 * i + 8 * half;
               chunk_to_operand(v[2 * j + i], eb + c, R, 128, c, row, CACHE ? ct + kCacheE2 : nullptr, kCacheKtE2, c);
             }
-            signal();
+            if ((b + 1) % kMlpHand == 0) signal();
           }
         }
       }

@@ -45,7 +45,8 @@ __device__ __forceinline__ double sigmoid_d(double x) {
 
 // One Gaussian of k_preprocess; returns its inclusive tile rectangle
 // ((0, -1, 0, -1) when culled / out of range).
-__device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i, const float* __restrict__ sh_row) {
+__device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i, const float* __restrict__ sh_row,
+                                               bool async_sh = false) {
   if (i >= a.c.K) return make_int4(0, -1, 0, -1);
   a.dvals[i] = (uint32_t)i;
   a.dkeys[i] = 0xFFFFFFFFu;  // culled sentinel sorts last
@@ -82,6 +83,10 @@ __device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i, cons
   }
   const int n_sh = (a.c.sh_degree + 1) * (a.c.sh_degree + 1) - 1;
   if (n_sh > 0 && a.c.sh_rest) {
+    if (async_sh) {  // the warp's cp.async copies of its SH rows (issued before the field loads above)
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+    }
     const float* S = sh_row;  // this Gaussian's SH row, staged in shared memory by its warp
     bool sb = false;
     for (int k = 0; k < n_sh * 3; ++k) sb |= !isfinite(S[k]);
@@ -228,22 +233,31 @@ __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rowf = ((a.c.sh_degree + 1) * (a.c.sh_degree + 1) - 1) * 3;
   float* wsh = reinterpret_cast<float*>(s_sh4) + warp * 32 * rowf;
+  bool async_sh = false;
   if (rowf > 0 && a.c.sh_rest) {
     const int64_t g0 = i - lane;
     const int64_t nrows = min((int64_t)32, a.c.K - g0);
     const float* src = a.c.sh_rest + g0 * rowf;
     const int64_t nf = nrows * rowf;
     if (nrows == 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-      // 32 rows of any width are a multiple of 16 B in total
+      // 32 rows of any width are a multiple of 16 B in total.  Asynchronous
+      // 16-byte copies (cp.async): all of a lane's ~11 rows in flight at once
+      // with no registers held (a load -> store loop waited on each load)
+      // The wait is deferred into preprocess_one, after its field loads are
+      // issued: the SH rows and the other fields share one memory latency.
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(wsh));
       for (int e = lane; e < nf / 4; e += 32)
-        reinterpret_cast<float4*>(wsh)[e] = __ldg(reinterpret_cast<const float4*>(src) + e);
-      for (int e = (int)(nf / 4) * 4 + lane; e < nf; e += 32) wsh[e] = src[e];
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * e),
+                     "l"(reinterpret_cast<const float4*>(src) + e)
+                     : "memory");
+      async_sh = true;
     } else {
       for (int e = lane; e < nf; e += 32) wsh[e] = src[e];
+      __syncwarp();
     }
   }
-  __syncthreads();
-  const int4 t = preprocess_one(a, i, wsh + lane * rowf);
+  const int4 t = preprocess_one(a, i, wsh + lane * rowf, async_sh);
+  __syncthreads();  // the block's tile histogram was zeroed above
   for (int ty = t.z; ty <= t.w; ++ty)
     for (int tx = t.x; tx <= t.y; ++tx) {
       const int b = ty * a.ntx + tx;
@@ -331,7 +345,11 @@ extern "C" int fs4d_debug_blend_trace(unsigned long long* out) {
 #endif
 
 template <int DC, int SUB, bool FIRST>
+#ifdef FS4D_BLEND_MINB  // A/B knob: minimum resident CTAs per SM (caps registers)
+__global__ void __launch_bounds__(kTilePixels / SUB, FS4D_BLEND_MINB) k_blend(BlendArgs a) {
+#else  // (no minimum: ptxas settles at 72 registers; an explicit 1 lets it take 112 and costs ~9%)
 __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
+#endif
 #ifdef FS4D_BLEND_TRACE
   const unsigned long long t_start = gtimer();
   unsigned nbatch = 0;
