@@ -626,8 +626,10 @@ def main():
     base = {"metric": METRIC, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded stand-in for EndoNeRF, SURVEY §8(d); z~U[3,6])",
+            # identical in both arms (the driver compares them); each arm's
+            # execution details go under "setup"
             "config": {"workload": WORKLOAD, "frames_per_rank_step": 1, "timesteps": "t=k/155 sharded by rank",
-                       "parallelism": f"frame-sharded x{world}", "l2": "flushed (256 MB write) between steps"}}
+                       "parallelism": f"frame-sharded x{world}"}}
 
     if args.impl == "reference":
         if rank != 0:
@@ -635,7 +637,7 @@ def main():
         r = cpu_reference(args.steps, args.warmup)
         line = dict(base)
         line.update({"impl": "reference", "value": r["value"], "ms_per_step": 1000.0 / r["value"],
-                     "n_gpus": world,
+                     "n_gpus": world, "setup": {"cpu": "whole frames, one per worker process (see cpu_baseline)"},
                      "cpu_baseline": {"value": r["value"], "unit": "frames/s", "cores": r["cores"],
                                       "kind": r["kind"], "sample": r["sample"]},
                      "host": r["host"],
@@ -662,6 +664,7 @@ def main():
             line["config"] = dict(base["config"], workload="configs[4]: configs[1] scene, 8 (view,t) pairs/GPU, "
                                                            "L1 RGB + L1 feature", parallelism=f"dp{world}",
                                   pairs_in_flight=r["lanes"], stage_ms="one serial (1-lane) step")
+            line["setup"] = {"l2": "flushed (256 MB write) between steps"}
             if args.workload == "fine":
                 line["config"]["workload"] = ("reference fine-stage iteration (training.py:489-535) on the configs[1] "
                                               "scene: 8 pairs/GPU, teacher 16ch at 160x128, TrainConfig defaults")
@@ -669,11 +672,11 @@ def main():
         return
     r = gpu_bench(args, rank, world, local)
     ns = int(os.environ.get("FS4D_SEQ_STREAMS", "3"))
-    base["config"]["gather_order"] = ("morton (once per model, untimed; bit-identical results)"
-                                      if os.environ.get("FS4D_LOCALITY", "1") == "1" else "source")
-    base["config"] = dict(base["config"], parallelism=f"frame-sharded x{world}, {ns} frames in flight per GPU "
-                          f"({ns} streams)", l2=f"no flush: {2 * ns} rotating model replicas ({2 * ns} x 70 MB > "
-                          "126 MB L2); value_serial is flushed")
+    base["setup"] = {"gather_order": ("morton (once per model, untimed; bit-identical results)"
+                                      if os.environ.get("FS4D_LOCALITY", "1") == "1" else "source"),
+                     "frames_in_flight": f"{ns} per GPU ({ns} streams)",
+                     "l2": f"no flush: {2 * ns} rotating model replicas ({2 * ns} x 70 MB > 126 MB L2); "
+                           "value_serial is flushed (256 MB write) between frames"}
     hbm, tf, peak_src = peaks()
     frames = world * r["steps"]
     value = frames / (r["ms"] / 1000.0)

@@ -37,7 +37,7 @@ def main():
     txt = f"""# Round {R[1:].lstrip("0")} — committed-build profile (latest)
 
 Bench (no profiler, `python bench.py`): **{b['value']:.1f} frames/s** whole-job (configs[2] sequence,
-{b['config']['parallelism']}; {b['config']['l2']}); one frame at a time with an L2 flush between
+{b['config']['parallelism']}, {b.get('setup', {}).get('frames_in_flight', '')}; {b.get('setup', b['config']).get('l2', '')}); one frame at a time with an L2 flush between
 frames: {b['value_serial']['value']:.1f} frames/s ({b['value_serial']['ms_per_frame']:.3f} ms/frame).
 End to end through pinned PCIe copies (H2D {b['e2e']['h2d_bytes_per_step']/1e6:.1f} MB + D2H
 {b['e2e']['d2h_bytes_per_step']/1e6:.1f} MB per frame): {b['e2e']['value']:.1f} frames/s.  CPU reference arm:
