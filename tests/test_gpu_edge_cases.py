@@ -262,3 +262,52 @@ def test_sequence_renderer_frames_in_flight_match_serial_frames():
     for got, exp in zip(outs, ref):
         for key in exp:
             assert torch.equal(got[key], exp[key]), key
+
+
+@pytest.mark.parametrize("case", ["planes", "few_ties"])
+def test_tile_sort_clustered_depths_and_fp32_ties(case):
+    """Per-tile sort edge cases (binning.cu), seen by a camera tilted by
+    1e-7 rad so that equal fp32 depth keys still differ by ~1e-8 in fp64:
+    'planes' -- 3000 Gaussians on three depth planes only: the keys collide in
+    large runs, the bucket map degenerates and the radix fallback runs;
+    'few_ties' -- depths spread over [3, 6] except 40 Gaussians at exactly
+    4.0: the bucket sort itself resolves the fp32 ties.  Either way the tile
+    lists must follow the reference order exactly (fp64 depth, then source
+    index; rasterizer.py:163, 188-207)."""
+    from oracle import fs4d_oracle as O
+    rng = np.random.default_rng(11)
+    k = 3000
+    f32 = lambda a: np.asarray(a, np.float64).astype(np.float32).astype(np.float64)  # noqa: E731
+    q = rng.normal(size=(k, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    if case == "planes":
+        depths = rng.choice([3.0, 3.5, 4.0], k)
+    else:
+        depths = rng.uniform(3.0, 6.0, k)
+        depths[rng.choice(k, 40, replace=False)] = 4.0
+    cloud = fs().GaussianCloud(
+        positions=f32(np.column_stack([rng.uniform(-0.2, 0.2, k), rng.uniform(-0.2, 0.2, k), depths])),
+        rotations=f32(q), log_scales=f32(rng.normal(-4.0, 0.3, size=(k, 3))),
+        opacity_logits=f32(rng.normal(0.0, 1.0, size=k)), colors_raw=f32(rng.uniform(size=(k, 3))),
+        features=f32(rng.normal(size=(k, 4))))
+    eps = 1e-7
+    T = np.eye(4)
+    T[:3, :3] = [[np.cos(eps), 0, np.sin(eps)], [0, 1, 0], [-np.sin(eps), 0, np.cos(eps)]]
+    h = w = 64
+    fr = frame(h=h, w=w, focal=200.0, T=T)
+    out = fs().render(cloud, fr, fs().RasterConfig())
+    ocfg = O.RasterParams()
+    oproj = O.project(cloud, fr.K, T, h, w, ocfg)
+    z32 = oproj["view_depth"].astype(np.float32)
+    assert len(z32) - len(np.unique(z32)) > (1000 if case == "planes" else 30)  # the fp32 keys really collide
+    olists = O.bin_tiles(oproj, h, w, 16)
+    gproj = out.record.proj
+    glists = out.record.tile_lists()
+    longest = 0
+    for ty, row in enumerate(olists):
+        for tx, cell in enumerate(row):
+            osrc = oproj["source_index"][cell]
+            gsrc = gproj.source_index[glists[ty][tx]]
+            assert np.array_equal(gsrc, osrc), (ty, tx)
+            longest = max(longest, cell.size)
+    assert longest > 1000
