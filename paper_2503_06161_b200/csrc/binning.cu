@@ -34,8 +34,25 @@
 
 namespace fs4d {
 
+#ifdef FS4D_SORT_TRACE
+// debug timeline of the densest tile's CTA (tools/sort_trace.sh)
+__device__ long long g_sort_trace[32];  // [0, 16): the densest tile's CTA, [16, 32): CTA FS4D_SORT_TRACE2
+#ifndef FS4D_SORT_TRACE2
+#define FS4D_SORT_TRACE2 700
+#endif
+#define SORT_TRACE(i)                                                     \
+  if (trace_me && threadIdx.x == 0) g_sort_trace[(blockIdx.x ? 16 : 0) + (i)] = clock64();
+extern "C" int fs4d_debug_sort_trace(long long* out) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, g_sort_trace, sizeof(long long) * 32);
+}
+#else
+#define SORT_TRACE(i)
+#endif
+
 constexpr int kHistMaxTiles = 5888;   // shared-memory histogram capacity (23 KB; configs[3] has 5120 tiles)
 constexpr int kTileScanThreads = 1024;
+constexpr int kWarpTile = 32;           // tiles below this many pairs are sorted by one warp (k_tile_sort)
 constexpr int kSortSmemKeys = 8192;   // per-tile keys sorted in shared memory (64 KB)
 #ifndef FS4D_TILE_SORT_THREADS
 #define FS4D_TILE_SORT_THREADS 512
@@ -109,6 +126,7 @@ __device__ void tile_scan_body(const uint32_t* __restrict__ tcnt, int ntiles, ui
       for (int b = 32; b >= 0; --b) {
         bcur[b] = r;
         r += bcnt[b];
+        if (b == 32 - __clz(kWarpTile)) counters[CNT_BIG_TILES] = r;  // tiles of >= kWarpTile pairs come first
       }
     }
     __syncthreads();
@@ -201,10 +219,19 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __r
     }
 }
 
-// (depth bits, exact fp64 depth, source index) ordering
+// (depth bits, exact fp64 depth, source index) ordering.  The fp64 tie
+// break is out of line: inlined, the compiler hoists its two global z64 loads
+// above the (almost always taken) early return, and every comparison of the
+// per-bucket insertion sorts then waited on an L2 round trip (13k cycles of a
+// 25k-cycle dense-tile sort).
+__device__ __noinline__ bool key_less_tie(unsigned long long a, unsigned long long b, const double* __restrict__ z64);
 __device__ __forceinline__ bool key_less(unsigned long long a, unsigned long long b, const double* __restrict__ z64) {
   const uint32_t ha = (uint32_t)(a >> 32), hb = (uint32_t)(b >> 32);
   if (ha != hb) return ha < hb;
+  return key_less_tie(a, b, z64);
+}
+__device__ __noinline__ bool key_less_tie(unsigned long long a, unsigned long long b, const double* __restrict__ z64) {
+  const uint32_t ha = (uint32_t)(a >> 32);
   const uint32_t ia = (uint32_t)a, ib = (uint32_t)b;
   if (ia == ib) return false;
   if (ha == 0xFFFFFFFFu) return ia < ib;  // padding
@@ -426,7 +453,7 @@ constexpr int kBucketNB = kTileSortWarps * 256;  // bucket counters reuse the ra
 
 __device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src, int n, const double* __restrict__ z64,
                                      uint32_t* __restrict__ out_vals, unsigned long long* xbuf, uint32_t* cnt,
-                                     uint32_t* red) {
+                                     uint32_t* red, bool trace_me = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R = (n + kTileSortThreads - 1) / kTileSortThreads;
   uint32_t key[kTileSortIPT], val[kTileSortIPT];
@@ -452,6 +479,7 @@ __device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src,
     red[2 * warp + 1] = kmax;
   }
   __syncthreads();
+  SORT_TRACE(2)
 #pragma unroll 4
   for (int w = 0; w < kTileSortWarps; ++w) {
     kmin = min(kmin, red[2 * w]);
@@ -466,6 +494,7 @@ __device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src,
     if (r * kTileSortThreads + (int)threadIdx.x < n) atomicAdd(&cnt[min(NB - 1, (int)((float)(key[r] - kmin) * scale))], 1u);
   }
   __syncthreads();
+  SORT_TRACE(3)
   // exclusive scan of the NB counters (E consecutive per thread) + the largest bucket
   const int E = (NB + kTileSortThreads - 1) / kTileSortThreads;
   const int b0 = threadIdx.x * E;
@@ -484,16 +513,21 @@ __device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src,
     if (lane >= o) incl += y;
   }
   tmax = __reduce_max_sync(0xffffffffu, tmax);
-  __syncthreads();  // everyone has read cnt / red
+  __syncthreads();
+  SORT_TRACE(4)  // everyone has read cnt / red
   if (lane == 31) red[warp] = incl;
   if (lane == 0) red[kTileSortWarps + warp] = tmax;
   __syncthreads();
+  SORT_TRACE(5)
   uint32_t wbase = 0, bmax = 0;
 #pragma unroll 4
   for (int w = 0; w < kTileSortWarps; ++w) {
     if (w < warp) wbase += red[w];
     bmax = max(bmax, red[kTileSortWarps + w]);
   }
+#ifdef FS4D_SORT_TRACE
+  if (trace_me && threadIdx.x == 0) { const int o = blockIdx.x ? 16 : 0; g_sort_trace[o + 12] = bmax; g_sort_trace[o + 13] = NB; g_sort_trace[o + 14] = n; g_sort_trace[o + 15] = kmax - kmin; }
+#endif
   if (bmax > (uint32_t)kBucketMax) return false;  // block-uniform
   {
     uint32_t run = wbase + incl - tsum;
@@ -505,6 +539,7 @@ __device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src,
       }
   }
   __syncthreads();
+  SORT_TRACE(6)
   // scatter through per-bucket cursors (the bucket starts); afterwards
   // cnt[b] is the end of bucket b, i.e. the start of bucket b + 1
 #pragma unroll
@@ -516,6 +551,7 @@ __device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src,
     }
   }
   __syncthreads();
+  SORT_TRACE(7)
   for (int b = threadIdx.x; b < NB; b += kTileSortThreads) {
     const int s0 = b > 0 ? (int)cnt[b - 1] : 0, s1 = (int)cnt[b];
     for (int a = s0 + 1; a < s1; ++a) {
@@ -529,8 +565,40 @@ __device__ bool cta_bucket_sort_tile(const unsigned long long* __restrict__ src,
     }
   }
   __syncthreads();
+  SORT_TRACE(8)
   for (int q = threadIdx.x; q < n; q += kTileSortThreads) out_vals[q] = (uint32_t)xbuf[q];
+  SORT_TRACE(11)
   return true;
+}
+
+// One warp sorts a tile of n < kWarpTile = 32 pairs: a key per lane (+inf
+// padding), bitonic network over the lanes with shuffles, under the same
+// total order as the CTA sorts.
+__device__ __forceinline__ void warp_sort_small_tile(int tile, const unsigned long long* __restrict__ pkey,
+                                                     const uint64_t* __restrict__ toff,
+                                                     const uint32_t* __restrict__ tcnt, int64_t cap,
+                                                     const double* __restrict__ z64, uint32_t* __restrict__ pvals,
+                                                     uint2* __restrict__ ranges) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t off = toff[tile];
+  uint64_t end = off + tcnt[tile];
+  if (end > (uint64_t)cap) end = (uint64_t)cap;
+  const int n = off < end ? (int)(end - off) : 0;
+  if (lane == 0) ranges[tile] = make_uint2((uint32_t)off, (uint32_t)(off + n));
+  if (n == 0) return;  // warp-uniform
+  unsigned long long key = lane < n ? pkey[off + lane] : 0xFFFFFFFFFFFFFFFFull - (unsigned long long)lane;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      // the lower lane of an ascending pair keeps the smaller key
+      const bool other_less = key_less(other, key, z64);
+      if (lower == up ? other_less : !other_less) key = other;
+    }
+  }
+  if (lane < n) pvals[off + lane] = (uint32_t)key;
 }
 
 __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long long* __restrict__ pkey,
@@ -538,10 +606,27 @@ __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long lo
                                                                 const uint32_t* __restrict__ tcnt, int ntiles,
                                                                 int64_t cap, const double* __restrict__ z64,
                                                                 uint32_t* __restrict__ pvals, uint2* __restrict__ ranges,
-                                                                const int32_t* __restrict__ tperm, int radix_only) {
+                                                                const int32_t* __restrict__ tperm,
+                                                                const uint32_t* __restrict__ counters, int radix_only) {
   extern __shared__ unsigned long long s_keys[];  // kSortSmemKeys exchange buffer (dynamic, 64 KB)
   __shared__ uint32_t wcnt[kTileSortWarps * 256];
   __shared__ uint32_t dbase[256];
+#ifdef FS4D_SORT_TRACE
+  if (tperm && (blockIdx.x == 0 || blockIdx.x == FS4D_SORT_TRACE2) && threadIdx.x == 0)
+    g_sort_trace[blockIdx.x ? 16 : 0] = clock64();
+#endif
+  // Tiles of fewer than kWarpTile pairs (the end of the densest-first order,
+  // half the tiles of a configs[1] frame) are sorted one per WARP, 16 to a CTA,
+  // with a register bitonic network: a CTA-wide sort of a handful of keys cost
+  // ~6k cycles of fixed phases and barriers.
+  if (tperm) {
+    const int nbig = (int)counters[CNT_BIG_TILES];
+    if ((int)blockIdx.x >= nbig) {
+      const int pos = nbig + ((int)blockIdx.x - nbig) * kTileSortWarps + (int)(threadIdx.x >> 5);
+      if (pos < ntiles) warp_sort_small_tile(tperm[pos], pkey, toff, tcnt, cap, z64, pvals, ranges);
+      return;
+    }
+  }
   const int tile = tperm ? tperm[blockIdx.x] : blockIdx.x;
   const uint64_t off = toff[tile];
   uint64_t end = off + tcnt[tile];
@@ -552,7 +637,13 @@ __global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long lo
   unsigned long long* keys = pkey + off;
   if (n <= kSortSmemKeys) {
     static_assert(kTileSortThreads * kTileSortIPT >= kSortSmemKeys, "bucket sort covers the smem tile size");
-    if (radix_only || !cta_bucket_sort_tile(keys, n, z64, pvals + off, s_keys, wcnt, dbase)) {
+#ifdef FS4D_SORT_TRACE
+    const bool trace_me = tperm && (blockIdx.x == 0 || blockIdx.x == FS4D_SORT_TRACE2);
+    SORT_TRACE(1)
+#else
+    const bool trace_me = false;
+#endif
+    if (radix_only || !cta_bucket_sort_tile(keys, n, z64, pvals + off, s_keys, wcnt, dbase, trace_me)) {
       __syncthreads();
       cta_radix_sort_tile(keys, n, z64, pvals + off, s_keys, wcnt, dbase);
     }
@@ -797,7 +888,7 @@ void bin_tiles_device(const RenderLayout& L, void* ws, const int4* tile_rect, co
                                                                      L.ntiles <= 64 * kTileScanThreads
                                                                          ? at<int32_t>(ws, L.tperm)
                                                                          : nullptr,
-                                                                     radix_only);
+                                                                     counters, radix_only);
 }
 
 }  // namespace fs4d

@@ -84,7 +84,7 @@ struct RenderLayout {
 };
 
 // counters (uint32 words at layout.counters)
-enum { CNT_VISIBLE = 0, CNT_PAIRS64 = 2 /* u64 at words 2..3 */, CNT_PAIRS_CLAMPED = 4, CNT_WORDS = 8 };
+enum { CNT_VISIBLE = 0, CNT_PAIRS64 = 2 /* u64 at words 2..3 */, CNT_PAIRS_CLAMPED = 4, CNT_BIG_TILES = 5, CNT_WORDS = 8 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
