@@ -1575,7 +1575,13 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
     CUtensorMap tmap;
     rc = lat_tensor_map(img, K, &tmap);
     if (rc) return rc;
-    const int grid2 = (int)(ceil_div(ntiles, 2) < grid_cap ? ceil_div(ntiles, 2) : grid_cap);
+    // as few CTAs as keep the same number of tile rounds per slot: the
+    // makespan is ceil(ntiles / (2 grid)) rounds either way, and the SMs this
+    // frees run other frames' kernels (1563 tiles: 6 rounds on 131 CTAs
+    // instead of 148)
+    const int64_t rounds = ceil_div(ntiles, 2 * (int64_t)grid_cap);
+    const int64_t g2 = ceil_div(ntiles, 2 * rounds);
+    const int grid2 = (int)(g2 < grid_cap ? g2 : grid_cap);
     if (cache) {
       cudaFuncSetAttribute(k_mlp_tc_2s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
       k_mlp_tc_2s<true><<<grid2, kTc2Threads, smem2, s>>>(a, tmap);
