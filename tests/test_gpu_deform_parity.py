@@ -310,3 +310,21 @@ def test_config1_shapes_outside_aabb_and_time_ends_vs_oracle(t):
     for l in range(2):
         for p in range(6):
             close(pg[l][p], opg[l][p], f"plane {l}/{p}", rel=True)
+
+
+@pytest.mark.parametrize("k", [1, 127, 129, 383, 20000])
+def test_two_slot_forward_ragged_sizes_vs_oracle(k):
+    """The forward without cache (k_mlp_tc_2s: two tile pipelines per CTA, the
+    latent as TMA-loaded bf16 rows, rows past K zero-filled by the TMA unit):
+    one row, a short tile, a tile plus one row, an odd number of tiles (the
+    second slot of the last CTA idle) and a configs[1]-shaped batch, against
+    the oracle; and bitwise equal to deform_with_cache's forward (the cached
+    path writes the same snapshot)."""
+    cloud, field, net = config1_parts(k=k, seed=7)
+    t = 0.61
+    snap = fs().deform(cloud, field, net, t)
+    snap_c, _ = fs().deform_with_cache(cloud, field, net, t)
+    osnap, _ = O.deform(cloud, field.planes, field.aabb, oracle_net(net), t)
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "features"):
+        close(getattr(snap, f), osnap[f], f)
+        assert np.array_equal(np.asarray(getattr(snap, f)), np.asarray(getattr(snap_c, f))), f
