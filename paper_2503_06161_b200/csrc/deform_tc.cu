@@ -871,6 +871,7 @@ constexpr int kMlpHand = FS4D_MLP_HAND;
 constexpr int kTc2Threads = 2 * kTcWsThreads;
 constexpr int kMaxDynSmemBytes = 232448 - 2048;  // 227 KB opt-in, less the kernel's static barriers
 constexpr int kTc2Region = kTcRows * 128 * 4;  // E hi + lo: 64 KB
+constexpr int kTc2LatOff = kTc2Region / 2;      // the TMA latent image: upper 32 KB of the region
 constexpr int kTc2Hand = FS4D_MAX_TRUNK + 16;  // operand hand-offs per tile (upper bound)
 
 struct Tc2Bars {
@@ -903,20 +904,24 @@ __device__ __forceinline__ void mlp2_issue(const TcArgs& a, const CUtensorMap* t
   const uint32_t xbar = smem_u32(&bars.x[SL]), rbar = smem_u32(&bars.rfree[SL]);
   const bool leader = (threadIdx.x & 31) == 0;
   const int64_t ntiles = ceil_div(a.K, kTcRows);
-  // the latent rows of tile t -> the region by TMA: 16 column blocks of
-  // [128 rows x 16 B] (8 hi, then 8 lo), i.e. the K-major no-swizzle operand
-  // with K-adjacent core matrices 2 KB apart (LBO 2048, SBO 128); rows past K
-  // are zero-filled by the TMA unit
+  // the latent rows of tile t -> the upper half of the region by TMA: 16
+  // column blocks of [128 rows x 16 B] (8 hi, then 8 lo), i.e. the K-major
+  // no-swizzle operand with K-adjacent core matrices 2 KB apart (LBO 2048,
+  // SBO 128); rows past K are zero-filled by the TMA unit.  The upper half is
+  // free as soon as a tile's head / F_feat-0 MMAs have read e2 (FF, the last
+  // operand, lives in the lower 16 KB), so the next tile's latent streams in
+  // during the F_feat epilogue and the F_feat-1 MMAs.
+  const uint32_t sLat = sR + (uint32_t)kTc2LatOff;
   auto load_x = [&](int64_t t) {
     if (leader) {
       mbar_expect_tx(xbar, kTcRows * 64 * 4);
 #pragma unroll 1
-      for (int cb = 0; cb < 16; ++cb) tma_lat_block(sR + 2048 * cb, tmap, 8 * cb, (int)(t * kTcRows), xbar);
+      for (int cb = 0; cb < 16; ++cb) tma_lat_block(sLat + 2048 * cb, tmap, 8 * cb, (int)(t * kTcRows), xbar);
     }
     __syncwarp();
   };
   if (blockIdx.x + (int64_t)gridDim.x * SL < ntiles) load_x(blockIdx.x + (int64_t)gridDim.x * SL);
-  const TcOpnd xA{sR, (uint32_t)(kTcRows * 64 * 2), 2048u, 128u, 4096u, false};
+  const TcOpnd xA{sLat, (uint32_t)(kTcRows * 64 * 2), 2048u, 128u, 4096u, false};
   uint32_t iter = 0;
   int slot = 0;
   auto wait_op = [&]() {
@@ -958,18 +963,19 @@ __device__ __forceinline__ void mlp2_issue(const TcArgs& a, const CUtensorMap* t
       if (p.enable_feat) gemm_bf16x3_w(tmem + 192, sR, 128, 32 * b, sW + p.off_f1, 128, 32 * b, 32, 2, b > 0);
     }
     commit();
+    // e2 read: the upper half of the region is free once these MMAs complete
+    mma_commit_w(rbar);
+    {
+      const int64_t next = tile + 2 * (int64_t)gridDim.x;
+      if (next < ntiles) {
+        mbar_wait(rbar, iter & 1);
+        load_x(next);
+      }
+    }
     if (p.enable_feat) {
       wait_op();  // FF in X
       gemm_bf16x3_w(tmem, sR, 32, 0, sW + p.off_f2, 32, 0, p.DP, 2, false);
       commit();
-    }
-    // the region is free once this tile's MMAs complete: start the next
-    // tile's latent load right then, while the epilogue still drains TMEM
-    mma_commit_w(rbar);
-    const int64_t next = tile + 2 * (int64_t)gridDim.x;
-    if (next < ntiles) {
-      mbar_wait(rbar, iter & 1);
-      load_x(next);
     }
     wait_op();  // tile finished: the epilogue is done with TMEM
     __syncwarp();
@@ -1113,7 +1119,7 @@ __global__ void __launch_bounds__(kTc2Threads, 1) k_mlp_tc_2s(TcArgs a, const __
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int c = 16 * i + 8 * half;
-            const int so = (c >> 3) * 2048 + row * 16, co = core_off(row, c, kCacheKtLat);
+            const int so = kTc2LatOff + (c >> 3) * 2048 + row * 16, co = core_off(row, c, kCacheKtLat);
             *reinterpret_cast<uint4*>(ct + kCacheLat + co) = *reinterpret_cast<const uint4*>(R + so);
             *reinterpret_cast<uint4*>(ct + kCacheLat + kTcRows * kCacheKtLat * 2 + co) =
                 *reinterpret_cast<const uint4*>(R + kTcRows * 64 * 2 + so);
