@@ -78,6 +78,12 @@ MLP_PARAMS = 64 * 64 + 64 + 4 * (64 * 32 + 32 + 32 * 32 + 32) + (32 * 3 + 3 + 32
 FRAME_BYTES = K_GAUSS * 4 * (11 + D + 3 * (SH_DEG + 1) ** 2) + 4 * plane_floats() + 4 * MLP_PARAMS \
     + H * W * 4 * (3 + D + 1 + 1)
 MLP_FLOPS = 2 * 21344 * K_GAUSS
+# FP32 work of one evaluated (pixel, Gaussian) in the blend, following the
+# reference's per-entry arithmetic (rasterizer.py:215-261): offset 2, power
+# 8 (4 mul + 2 fma), opacity x exp 1, w = alpha T 1, 20 accumulated channels
+# (RGB, depth, D = 16 features) x 2, transmittance update 2; the exp2 runs on
+# the SFU and is not counted.  Evaluations per frame = sum of n_contrib.
+BLEND_FLOPS_PER_EVAL = 2 + 8 + 1 + 1 + 2 * (3 + 1 + D) + 2
 
 
 # stage (library profiler id) -> the single kernel it times (traffic lookup)
@@ -432,6 +438,7 @@ def gpu_bench(args, rank, world, local):
     st = pipe.renderer.status.read()
     n_vis = int(st[2])
     n_pairs = (int(st[4]) << 32) | (int(st[3]) & 0xFFFFFFFF)
+    n_eval = int(pipe.images["n_contrib"].sum().item())  # evaluated (pixel, Gaussian) entries of one frame
     pipe.renderer.cap = int(n_pairs * 1.5) + 4096
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
@@ -507,7 +514,7 @@ def gpu_bench(args, rank, world, local):
         if int(st[0]) != 0:
             raise RuntimeError(f"device status {st[:5]} during the e2e region")
     return dict(ms=ms_max, ms_serial=ms_serial, prof=prof, clocks=clk.summary(), n_vis=n_vis, n_pairs=n_pairs,
-                e2e_ms=e2e_ms, h2d=sf.h2d_bytes(), d2h=sf.d2h_bytes(), steps=steps, per_rank_ms=per_rank_ms,
+                e2e_ms=e2e_ms, n_eval=n_eval, h2d=sf.h2d_bytes(), d2h=sf.d2h_bytes(), steps=steps, per_rank_ms=per_rank_ms,
                 comm=comm_info(world))
 
 
@@ -598,6 +605,20 @@ def train_bench(args, rank, world, local):
     step.n_lanes, step._lanes = lanes, None
     return dict(ms=ms, prof=prof, loss=float(step.loss.item()), grad_floats=step.grads.numel, pairs=pairs,
                 lanes=lanes, per_rank_ms=per_rank_ms, comm=comm_info(world))
+
+
+def blend_fp32(r, stage_ms):
+    import torch
+    if not stage_ms.get("blend"):
+        return None
+    prop = torch.cuda.get_device_properties(0)
+    mhz = (r["clocks"] or {}).get("sm_max_mhz") or 1965.0
+    peak = prop.multi_processor_count * 128 * 2 * mhz * 1e6 / 1e12
+    flops = r["n_eval"] * BLEND_FLOPS_PER_EVAL
+    ach = flops / (stage_ms["blend"] / 1000.0) / 1e12
+    return {"bound": "fp32", "kernel": "k_blend", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+            "frac": ach / peak, "evals_per_frame": r["n_eval"], "flops_per_eval": BLEND_FLOPS_PER_EVAL,
+            "peak_source": f"{prop.multi_processor_count} SMs x 128 x 2 x {mhz:.0f} MHz"}
 
 
 def launches_per_frame():
@@ -714,6 +735,9 @@ def main():
                      # same ncu capture (percent of B200 peak)
                      "sm_utilisation_pct": utilisation},
         "kernels": kernels,
+        # secondary roofline: the blend is FP32-issue bound; peak =
+        # SMs x 128 FP32 lanes x 2 (FMA) x the max SM clock
+        "roofline_fp32": blend_fp32(r, stage_ms),
         "roofline_frame": {"bytes_per_frame": FRAME_BYTES,
                            "achieved_gbs": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9,
                            "frac": FRAME_BYTES / (r["ms"] / r["steps"] / 1000.0) / 1e9 / hbm},
