@@ -301,6 +301,20 @@ int fs4d_deform_bwd_deterministic(const Fs4dCloud* cloud, const Fs4dHexPlane* fi
                                   void* workspace, size_t workspace_bytes, void* det_workspace,
                                   size_t det_workspace_bytes, int32_t* status, void* stream);
 size_t fs4d_deform_bwd_det_workspace_bytes(const Fs4dDeformNet* net, const Fs4dHexPlane* field);
+/* fs4d_deform_bwd (det_workspace NULL) or fs4d_deform_bwd_deterministic
+ * (det_workspace non-NULL) that also records `passthrough_event` (a
+ * cudaEvent_t, may be NULL) on `stream` as soon as every cloud gradient
+ * except positions is written -- the pass-through rows of
+ * deformation.py:172-181 -- so a data-parallel caller can all-reduce those
+ * rows while the MLP and HexPlane backward still run (the gradient exchange
+ * of training.py:459-539 across ranks). */
+int fs4d_deform_bwd_split(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net,
+                          double t, const void* cache, size_t cache_bytes,
+                          const Fs4dCloud* snapshot_grads, Fs4dCloud* cloud_grads,
+                          Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads, int32_t accumulate,
+                          void* workspace, size_t workspace_bytes, void* det_workspace,
+                          size_t det_workspace_bytes, void* passthrough_event, int32_t* status,
+                          void* stream);
 /* accumulate != 0 adds into every output instead of overwriting it (gradient
  * accumulation over the (view, t) pairs of a training step).  Non-NULL
  * cloud_grads fields other than positions receive the pass-through snapshot

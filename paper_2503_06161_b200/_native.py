@@ -157,6 +157,14 @@ SIGNATURES = {
                                                      ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
                                                      ctypes.c_void_p, ctypes.c_size_t,
                                                      ctypes.c_void_p, ctypes.c_void_p]),
+    "fs4d_deform_bwd_split": (ctypes.c_int, [ctypes.POINTER(Cloud), ctypes.POINTER(HexPlane),
+                                             ctypes.POINTER(DeformNet), ctypes.c_double,
+                                             ctypes.c_void_p, ctypes.c_size_t,
+                                             ctypes.POINTER(Cloud), ctypes.POINTER(Cloud),
+                                             ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane),
+                                             ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
+                                             ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p]),
     "fs4d_deform_bwd_det_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(DeformNet), ctypes.POINTER(HexPlane)]),
     "fs4d_l1_loss_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,

@@ -73,7 +73,7 @@ int deform_forward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, 
                    void*, size_t, cudaStream_t);
 int deform_backward(const Fs4dCloud&, const Fs4dHexPlane&, const Fs4dDeformNet&, double, const void*, size_t,
                     const Fs4dCloud&, Fs4dCloud&, Fs4dDeformNet&, Fs4dHexPlane*, int, void*, size_t, int32_t*, void*,
-                    size_t, cudaStream_t);
+                    size_t, cudaStream_t, cudaEvent_t = nullptr);
 size_t deform_backward_det_bytes(const Fs4dDeformNet&, const Fs4dHexPlane&);
 int l1_loss_grad(const float*, const float*, const float*, const float*, int, int, int, double, double, float*, float*,
                  double*, cudaStream_t);
@@ -296,6 +296,23 @@ int fs4d_deform_bwd_deterministic(const Fs4dCloud* cloud, const Fs4dHexPlane* fi
   return deform_backward(*cloud, *field, *net, t, cache, cache_bytes, *snapshot_grads, *cloud_grads, *net_grads,
                          plane_grads, accumulate, workspace, workspace_bytes, status, det_workspace,
                          det_workspace_bytes, (cudaStream_t)stream);
+}
+
+int fs4d_deform_bwd_split(const Fs4dCloud* cloud, const Fs4dHexPlane* field, const Fs4dDeformNet* net, double t,
+                          const void* cache, size_t cache_bytes, const Fs4dCloud* snapshot_grads,
+                          Fs4dCloud* cloud_grads, Fs4dDeformNet* net_grads, Fs4dHexPlane* plane_grads,
+                          int32_t accumulate, void* workspace, size_t workspace_bytes, void* det_workspace,
+                          size_t det_workspace_bytes, void* passthrough_event, int32_t* status, void* stream) {
+  int rc = check_cloud(cloud, false);
+  if (rc) return rc;
+  if (!field || !net || !snapshot_grads || !cloud_grads || !net_grads)
+    return fail(FS4D_ERR_CONFIG, "null deform_bwd argument");
+  if (snapshot_grads->K != cloud->K || cloud_grads->K != cloud->K)
+    return fail(FS4D_ERR_CONTRACT, "gradient rows do not match the cloud");
+  return deform_backward(*cloud, *field, *net, t, cache, cache_bytes, *snapshot_grads, *cloud_grads, *net_grads,
+                         plane_grads, accumulate, workspace, workspace_bytes, status, det_workspace,
+                         det_workspace ? det_workspace_bytes : 0, (cudaStream_t)stream,
+                         (cudaEvent_t)passthrough_event);
 }
 
 size_t fs4d_deform_bwd_det_workspace_bytes(const Fs4dDeformNet* net, const Fs4dHexPlane* field) {

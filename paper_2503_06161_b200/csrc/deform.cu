@@ -912,7 +912,7 @@ size_t deform_backward_det_bytes(const Fs4dDeformNet& net, const Fs4dHexPlane& f
 int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4dDeformNet& net, double t,
                     const void* cache, size_t cache_bytes, const Fs4dCloud& sg, Fs4dCloud& cg, Fs4dDeformNet& ng,
                     Fs4dHexPlane* pg, int accumulate, void* ws, size_t ws_bytes, int32_t* status, void* det_ws,
-                    size_t det_bytes, cudaStream_t s) {
+                    size_t det_bytes, cudaStream_t s, cudaEvent_t pass_done) {
   DefArgs a;
   memset(&a, 0, sizeof(a));
   size_t smem = 0;
@@ -954,6 +954,10 @@ int deform_backward(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const Fs4
     pa.block_start[6] = blocks;
     pa.accumulate = accumulate;
     if (blocks > 0) k_grad_passthrough<<<(unsigned)blocks, 256, 0, s>>>(pa);
+    // every cloud gradient except positions is final here: a caller can start
+    // reducing those rows (all-reduce bucket) while the MLP / HexPlane
+    // backward below runs
+    if (pass_done) cudaEventRecord(pass_done, s);
   }
   const size_t cneed = deform_cache_bytes(net, field, cloud.K);
   if (det_ws && !(cache && cneed))

@@ -355,13 +355,20 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   unsigned nbatch = 0;
 #endif
   constexpr int NT = kTilePixels / SUB;  // threads = pixels = Gaussians per batch
-  __shared__ float2 s_xy[NT];
-  __shared__ float4 s_cs[NT];  // scaled conic (gauss_power)
-  __shared__ int4 s_pr[NT];
-  __shared__ float4 s_rgbz[NT];
-  // features channel-quad-major [DC/4][NT] float4: conflict-free staging
-  // stores, broadcast reads in the compositing loop
-  __shared__ __align__(16) float4 s_f4[DC > 0 ? NT * DC / 4 : 1];
+  // the staged batch as ONE shared array: 16-byte rows [3 + DC/4][NT] -- the
+  // scaled conic (gauss_power), the pixel rectangle, rgb + depth, then the
+  // feature quads (channel-quad-major: conflict-free staging stores,
+  // broadcast reads) -- and the tile-relative means (8 bytes each) after
+  // them.  Reads of Gaussian k are [k * 16 + constant] / [k * 8 + constant]
+  // off one base (with separate arrays ptxas rebuilt each array's
+  // shared-window address inside the compositing loop)
+  constexpr int kRows = 3 + (DC > 0 ? DC / 4 : 0);
+  __shared__ __align__(16) float4 s_g[kRows * NT + NT / 2];
+  float4* const s_cs = s_g;
+  int4* const s_pr = reinterpret_cast<int4*>(s_g + NT);
+  float4* const s_rgbz = s_g + 2 * NT;
+  float4* const s_f4 = s_g + 3 * NT;
+  float2* const s_xy = reinterpret_cast<float2*>(s_g + kRows * NT);
   // per-warp ballot masks of the staged batch (shared, not a local array)
   __shared__ unsigned s_mask[NT / 32][NT / 32];
 

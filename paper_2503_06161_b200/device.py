@@ -329,13 +329,16 @@ class DeformEngine:
         return (out, cache) if cache is not None else out
 
     def backward(self, cloud, field, net, t, snap_grads, cloud_grads=None, net_grads=None,
-                 plane_grads=None, accumulate=False, cache=None, deterministic=False):
+                 plane_grads=None, accumulate=False, cache=None, deterministic=False, pass_event=None):
         """deform_backward on device.  Without output buffers: returns
         (d_positions [K,3], net_grads DeviceNet, plane_grads DeviceField|None).
         With a DeviceCloud `cloud_grads` (+ net/plane grads) every cloud
         gradient is written (or added, accumulate=True) and the buffers are
         returned.  deterministic=True: fs4d_deform_bwd_deterministic
-        (fixed-point plane scatter, bitwise reproducible; needs `cache`)."""
+        (fixed-point plane scatter, bitwise reproducible; needs `cache`).
+        pass_event: a torch.cuda.Event recorded as soon as every cloud
+        gradient except positions is written (fs4d_deform_bwd_split), for an
+        all-reduce of those rows that overlaps the rest of the backward."""
         k = len(cloud)
         ngrads = net_grads if net_grads is not None else net.zeros_like()
         pgrads = plane_grads if plane_grads is not None else (field.zeros_like() if net.enable_grid else None)
@@ -354,6 +357,7 @@ class DeformEngine:
         if cache is not None and (cache.k != k or cache.t != float(t)):
             raise ContractViolation("deform cache was made for another (cloud, t)")
         cptr, cbytes = (cache.ptr(), cache.nbytes) if cache is not None else (None, 0)
+        det_ws = None
         if deterministic:
             lib = N.load()
             need = int(lib.fs4d_deform_bwd_det_workspace_bytes(ctypes.byref(ns), ctypes.byref(fs)))
@@ -362,6 +366,16 @@ class DeformEngine:
                                          "depth 1, levels * channels = 64, feature_dim <= 16)")
             if getattr(self, "det_ws", None) is None or self.det_ws.numel() < need:
                 self.det_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            det_ws = self.det_ws
+        if pass_event is not None:
+            pass_event.record()  # materialise the cudaEvent_t (torch creates it lazily)
+            N.check(N.load().fs4d_deform_bwd_split(
+                ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns), float(t), cptr, cbytes, ctypes.byref(sgs),
+                ctypes.byref(cgs), ctypes.byref(ngs), ctypes.byref(pgs) if pgs is not None else None,
+                int(bool(accumulate)), _p(ws), ws.numel(), _p(det_ws) if det_ws is not None else None,
+                det_ws.numel() if det_ws is not None else 0, ctypes.c_void_p(pass_event.cuda_event), None,
+                _stream()))
+        elif deterministic:
             N.check(lib.fs4d_deform_bwd_deterministic(
                 ctypes.byref(cs), ctypes.byref(fs), ctypes.byref(ns), float(t), cptr, cbytes, ctypes.byref(sgs),
                 ctypes.byref(cgs), ctypes.byref(ngs), ctypes.byref(pgs) if pgs is not None else None,

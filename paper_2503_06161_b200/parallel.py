@@ -69,6 +69,24 @@ class FlatGrads:
         self.buffer.zero_()
         return self
 
+    def span(self, first, last):
+        """[lo, hi) of the consecutive views first..last; hi is the next
+        view's (aligned) offset, or the end of the buffer."""
+        names = [n for n, _ in self.specs]
+        i, j = names.index(first), names.index(last)
+        if j < i:
+            raise ValueError("span: views out of order")
+        return self.offsets[i], (self.offsets[j + 1] if j + 1 < len(names) else self.numel)
+
+    def allreduce_sum_range(self, lo, hi, group=None, async_op=False):
+        """SUM over the group of buffer[lo:hi] (one gradient bucket).  Returns
+        the async work handle (async_op=True) or None; no-op when not
+        distributed or the range is empty."""
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1 and hi > lo:
+            return dist.all_reduce(self.buffer[lo:hi], op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+        return None
+
     def allreduce_sum(self, group=None):
         """In-place SUM over the process group (no-op when not distributed)."""
         import torch.distributed as dist

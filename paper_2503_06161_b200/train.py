@@ -84,6 +84,10 @@ class TrainStep:
         # lane buffers are summed into self.grads before the all-reduce
         self.n_lanes = max(1, int(os.environ.get("FS4D_TRAIN_LANES", "3") if lanes is None else lanes))
         self._lanes = None
+        # two-bucket gradient exchange overlapping the backward: always at
+        # world > 1; FS4D_OVERLAP_ALLREDUCE=1 also takes that path at world 1
+        self.overlap_allreduce = os.environ.get("FS4D_OVERLAP_ALLREDUCE", "0") == "1"
+        self._comm_stream = None
         self.lambda_rgb, self.lambda_depth = float(lambda_rgb), float(lambda_depth)
         self.lambda_feat, self.lambda_tv = float(lambda_feat), float(lambda_tv)
         self.decoder = decoder  # (weight [Ct,N], bias [Ct]) CUDA tensors for loss_mode="decoder"
@@ -201,6 +205,12 @@ class TrainStep:
         self._lanes = lanes
         return lanes
 
+    @property
+    def _early_span(self):
+        """Flat-buffer range of the pass-through cloud gradients (rotations ..
+        features): final after each lane's last pass-through kernel."""
+        return self.grads.span("rotations", "features")
+
     def active_arrays(self, batch):
         """Parameter arrays that receive a gradient this iteration -- the keys
         of the reference's `grads` dict (training.py:509-531): `features`
@@ -260,26 +270,62 @@ class TrainStep:
             for ln in lanes:
                 ln.stream.wait_event(ready)
         stats_done = None  # the stats accumulation is a plain += : serialised across lanes
+        used = lanes[:min(nl, len(batch))]
+        # gradient exchange in two buckets: the pass-through
+        # cloud rows (rotations .. features, ~80% of the buffer) are final once
+        # every lane's LAST pair has run its pass-through kernel, so their lane
+        # sum + all-reduce run on a side stream while those pairs' MLP and
+        # HexPlane backward still run; positions, planes, MLP and decoder
+        # follow after the backward.  Same sums in the same order: results are
+        # identical to one all-reduce of the whole buffer.
+        overlap = self.world > 1 or self.overlap_allreduce
+        last_pair = {i % nl: i for i in range(len(batch))}
+        pass_events = {}
         for i, item in enumerate(batch):
             ln = lanes[i % nl]
             first = i < nl
+            ev = None
+            if overlap and last_pair[i % nl] == i:
+                ev = pass_events[i % nl] = torch.cuda.Event()
             with torch.cuda.stream(ln.stream if nl > 1 else main):
-                stats_done = self._run_pair(ln, item, field, w, dout, first, check, stats_done)
-        used = lanes[:min(nl, len(batch))]
+                stats_done = self._run_pair(ln, item, field, w, dout, first, check, stats_done, pass_event=ev)
+        lo, hi = self._early_span if overlap else (0, 0)
+
+        def lane_sum(a, b):  # lane 0's buffer[a:b] += the other lanes', one pass
+            if len(used) > 1 and b > a:
+                srcs = (ctypes.c_void_p * (len(used) - 1))(*[ln.grads.buffer.data_ptr() + 4 * a for ln in used[1:]])
+                N.check(lib.fs4d_sum_buffers(self.grads.buffer.data_ptr() + 4 * a, srcs, len(used) - 1, b - a, 1,
+                                             _stream()))
+        early = None
+        if overlap:
+            if self._comm_stream is None:
+                self._comm_stream = torch.cuda.Stream(device=self.device)
+            comm = self._comm_stream
+            comm.wait_stream(main)  # buffers of the previous step
+            for ev in pass_events.values():
+                comm.wait_event(ev)
+            with torch.cuda.stream(comm):
+                lane_sum(lo, hi)
+                early = self.grads.allreduce_sum_range(lo, hi, self.group, async_op=True)
         if nl > 1:
             for ln in used:
                 main.wait_stream(ln.stream)
-            if len(used) > 1:  # lane 0's buffer += the other lanes', one pass
-                srcs = (ctypes.c_void_p * (len(used) - 1))(*[ln.grads.buffer.data_ptr() for ln in used[1:]])
-                N.check(lib.fs4d_sum_buffers(_p(self.grads.buffer), srcs, len(used) - 1, self.grads.numel, 1,
-                                             _stream()))
+            lane_sum(0, lo)
+            lane_sum(hi, self.grads.numel)
         if self.deterministic:
             for ln in used:  # the lanes' losses in lane order
                 self.loss.add_(ln.loss)
         if self.lambda_tv > 0 and self.net.enable_grid:
             # d(lambda_tv * tv)/d(plane) once per iteration (training.py:523-529); 1/world per rank
             tv_loss_grad_device(self.field, self.plane_grads, self.lambda_tv / self.world, True, self.loss)
-        self.grads.allreduce_sum(self.group)
+        if overlap:
+            self.grads.allreduce_sum_range(0, lo, self.group)
+            self.grads.allreduce_sum_range(hi, self.grads.numel, self.group)
+            if early is not None:
+                early.wait()  # the current (main) stream waits for the early bucket
+            main.wait_stream(self._comm_stream)
+        else:
+            self.grads.allreduce_sum(self.group)
         if self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(self.loss, op=dist.ReduceOp.SUM, group=self.group)
@@ -353,7 +399,7 @@ class TrainStep:
         except Exception as e:
             raise type(e)(f"training step skipped on the device (parameters unchanged): {e}") from None
 
-    def _run_pair(self, ln, item, field, w, dout, first, check, stats_done):
+    def _run_pair(self, ln, item, field, w, dout, first, check, stats_done, pass_event=None):
         """One (view, t) pair on lane `ln` (the current stream): deform, render,
         loss + image gradients, render backward, deform backward into the
         lane's gradient buffer (overwritten by the lane's first pair)."""
@@ -398,7 +444,8 @@ class TrainStep:
             stats_done.record(cur)
         ln.deformer.backward(self.cloud, field, self.net, t, ln.snap_grads, cloud_grads=ln.cloud_grads,
                              net_grads=ln.net_grads, plane_grads=ln.plane_grads if self.net.enable_grid else None,
-                             accumulate=not first, cache=ln.cache, deterministic=self.deterministic)
+                             accumulate=not first, cache=ln.cache, deterministic=self.deterministic,
+                             pass_event=pass_event)
         return stats_done
 
     # ------------------------------------------------------------------

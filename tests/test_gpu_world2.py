@@ -50,14 +50,15 @@ def _scene():
     return cloud, field, net, pairs
 
 
-def _train(pairs, world, group_ranks=None):
+def _train(pairs, world, group_ranks=None, lanes=1, overlap=False, deterministic=False):
     import torch
     import paper_2503_06161_b200 as fs
     from paper_2503_06161_b200 import device as dv
     from paper_2503_06161_b200.train import TrainStep
     cloud, field, net, _ = _scene()
     step = TrainStep(dv.DeviceCloud.from_cloud(cloud), dv.DeviceField.from_field(field), dv.DeviceNet.from_net(net),
-                     H, W, fs.RasterConfig(), world=world, lanes=1)
+                     H, W, fs.RasterConfig(), world=world, lanes=lanes, deterministic=deterministic)
+    step.overlap_allreduce = overlap
     K = pinhole(H, W, 50.0)
     batch = [(t, K, T, torch.as_tensor(tr, device="cuda"), torch.as_tensor(tf, device="cuda"))
              for t, T, tr, tf in pairs]
@@ -87,7 +88,9 @@ def _worker(rank, world, port, q):
     try:
         _, _, _, pairs = _scene()
         lo, hi = shard_range(len(pairs), world, rank)
-        loss, grads = _train(pairs[lo:hi], world)
+        # two lanes per rank: both gradient buckets (pass-through rows on
+        # the side stream, the rest after the backward) see a lane sum
+        loss, grads = _train(pairs[lo:hi], world, lanes=2)
         frames = _frames(shard_timesteps(N_FRAMES, world, rank))
         q.put((rank, loss, grads, frames))
     finally:
@@ -130,3 +133,15 @@ def test_world2_training_and_sequence_shards_match_world1():
     for a, b in zip(sharded, frames1):
         for key in b:
             np.testing.assert_array_equal(a[key], b[key], err_msg=key)
+
+
+def test_overlapped_allreduce_buckets_bitwise_equal_single_reduce():
+    """The two-bucket exchange (pass-through rows summed and reduced on a side
+    stream during the backward) performs the same sums in the same order as
+    the single post-backward reduce: world 1, three lanes, deterministic
+    backward (no float atomics), bitwise equal."""
+    _, _, _, pairs = _scene()
+    loss_a, grads_a = _train(pairs, 1, lanes=3, overlap=False, deterministic=True)
+    loss_b, grads_b = _train(pairs, 1, lanes=3, overlap=True, deterministic=True)
+    assert loss_a == loss_b
+    np.testing.assert_array_equal(grads_a, grads_b)

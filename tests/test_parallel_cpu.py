@@ -60,6 +60,23 @@ def _worker(rank, world, port, q):
         for name, _ in specs:
             fg[name].copy_(torch.full(fg[name].shape, float(rank + 1)) / world)
         fg.allreduce_sum()
+        # the two-bucket exchange of TrainStep (pass-through rows async, the
+        # rest after): the same sums as one all-reduce of the whole buffer
+        specs = gradient_specs(5, 4, 1, [[(3, 2, 2)] * 6], [("net.trunk.0.weight", (3, 2))])
+        fg = FlatGrads(specs, device="cpu")
+        for name, _ in specs:
+            fg[name].copy_(torch.full(fg[name].shape, float(rank + 1)) / world)
+        fg.allreduce_sum()
+        fb = FlatGrads(specs, device="cpu")
+        for name, _ in specs:
+            fb[name].copy_(torch.full(fb[name].shape, float(rank + 1)) / world)
+        lo, hi = fb.span("rotations", "features")
+        assert 0 < lo < hi < fb.numel
+        work = fb.allreduce_sum_range(lo, hi, async_op=True)
+        fb.allreduce_sum_range(0, lo)
+        fb.allreduce_sum_range(hi, fb.numel)
+        work.wait()
+        assert torch.equal(fb.buffer, fg.buffer)
         ts = shard_timesteps(156, world, rank)
         q.put((rank, {n: fg[n].clone().numpy() for n, _ in specs}, ts.tolist()))
     finally:
