@@ -277,13 +277,20 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
   constexpr int NF = DC > 0 ? DC : 1;
   constexpr int NVMAX = 10 + NF;
   __shared__ float s_acc[DET ? (NT / 32) * B * NVMAX : 1];
-  __shared__ float2 s_xy[B];
-  __shared__ float4 s_co[B];
-  __shared__ float4 s_cs[B];  // scaled conic (gauss_power), same evaluation as the forward
-  __shared__ int4 s_pr[B];
-  __shared__ float4 s_rgbz[B];
-  __shared__ uint32_t s_g[B];
-  __shared__ __align__(16) float s_f[DC > 0 ? B * DC : 1];
+  // the staged batch as ONE shared array (reads of Gaussian k off one base
+  // with immediate offsets, as in k_blend): 16-byte rows [4 + DC/4][B] --
+  // conic + opacity, scaled conic (gauss_power, same evaluation as the
+  // forward), pixel rectangle, rgb + depth, feature quads (channel-quad-
+  // major) -- then the tile-relative means (8 B) and the source indices
+  constexpr int kRows = 4 + (DC > 0 ? (DC + 3) / 4 : 0);
+  __shared__ __align__(16) float4 s_stage[kRows * B + B / 2 + B / 4];
+  float4* const s_co = s_stage;
+  float4* const s_cs = s_stage + B;
+  int4* const s_pr = reinterpret_cast<int4*>(s_stage + 2 * B);
+  float4* const s_rgbz = s_stage + 3 * B;
+  float4* const s_f4 = s_stage + 4 * B;
+  float2* const s_xy = reinterpret_cast<float2*>(s_stage + kRows * B);
+  uint32_t* const s_g = reinterpret_cast<uint32_t*>(s_stage + kRows * B + B / 2);
   constexpr int NROW = (10 + DC + 1) / 2;  // per-Gaussian values, in float2 rows
   __shared__ __align__(16) float s_red[NT / 32][NROW * kRedRowStride];
   __shared__ int s_maxlast;
@@ -371,8 +378,16 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
       s_rgbz[threadIdx.x] = a.rgbz[g];
       if (DC > 0) {
         const float* src = a.features + (int64_t)g * a.D;
-        float* dst = s_f + threadIdx.x * DC;
-        for (int c = 0; c < DC; ++c) dst[c] = c < a.D ? src[c] : 0.f;
+        if ((a.D & 3) == 0 && a.D >= DC) {
+#pragma unroll
+          for (int c = 0; c < DC; c += 4) s_f4[(c / 4) * B + threadIdx.x] = __ldg(reinterpret_cast<const float4*>(src + c));
+        } else {
+          for (int c = 0; c < DC; c += 4) {
+            float q[4];
+            for (int i = 0; i < 4; ++i) q[i] = c + i < a.D ? src[c + i] : 0.f;
+            s_f4[(c / 4) * B + threadIdx.x] = make_float4(q[0], q[1], q[2], q[3]);
+          }
+        }
       }
     }
     __syncthreads();
@@ -427,11 +442,18 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
           const float w = al * Texc;
           float uval = cz.x * dc0[p] + cz.y * dc1[p] + cz.z * dc2[p] + cz.w * dd[p];
           if (DC > 0) {
-            const float* f = s_f + k * DC;
 #pragma unroll
-            for (int c = 0; c < NF; ++c) {
-              uval += f[c] * df[p][c];
-              if (c < 22) v[10 + c] += w * df[p][c];
+            for (int c4 = 0; c4 < NF; c4 += 4) {
+              const float4 fq = s_f4[(c4 / 4) * B + k];
+              const float f[4] = {fq.x, fq.y, fq.z, fq.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int c = c4 + i;
+                if (c < NF) {
+                  uval += f[i] * df[p][c];
+                  if (c < 22) v[10 + c] += w * df[p][c];
+                }
+              }
             }
           }
           const float dal = uval * Texc - (suffix[p] + Tfin[p] * vpix[p]) * rom;

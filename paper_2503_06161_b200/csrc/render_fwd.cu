@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
 #pragma unroll
   for (int c = 0; c < (DC > 0 ? DC / 2 : 1); ++c) accf2[c] = make_float2(0.f, 0.f);
   int ncontrib = 0, last = -1;
-  bool done = !inside;
+  bool done = !inside || !(1.f >= a.stop);  // rasterizer.py:252: contrib needs T_exc >= stop
   const int nf = DC > 0 ? min(DC, a.D - a.c0) : 0;
   const bool vec_ok = DC >= 4 && nf == DC && (a.D & 3) == 0 && (a.c0 & 3) == 0;
 
@@ -484,11 +484,9 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
           }
 #pragma unroll
           for (int j = 0; j < BK; ++j) {
+            // (T < stop always sets done right after the update below, and
+            // done starts true when 1 < stop: no pre-check needed here)
             if (!live[j] || done) continue;
-            if (T < a.stop) {
-              done = true;
-              continue;
-            }
             const int k = kk[j];
             const float al = alv[j];
             const float w = al * T;
