@@ -223,9 +223,17 @@ __device__ __forceinline__ int4 preprocess_one(const PreArgs& a, int64_t i, cons
 // The warp's 32 SH rows ([K, n_sh, 3], 180 B each at SH3) are copied into
 // shared memory with coalesced 16 B loads first (a thread reading its own
 // row 180 B apart from its neighbours' was the kernel's load-issue cost).
+#ifdef FS4D_PRE_MINB  // A/B knob: minimum resident blocks per SM (caps registers)
+__global__ void __launch_bounds__(256, FS4D_PRE_MINB) k_preprocess(PreArgs a) {
+#else
 __global__ void __launch_bounds__(256) k_preprocess(PreArgs a) {
-  extern __shared__ float4 s_sh4[];  // [8 warps][32 rows * n_sh * 3 floats]
-  __shared__ uint32_t h[kHistTilesSmem];
+#endif
+  // dynamic shared memory: [8 warps][32 rows * n_sh * 3 floats] of SH rows,
+  // then the block's tile histogram sized to this frame's tile count (a
+  // fixed 24 KB array capped the kernel at 3 blocks per SM)
+  extern __shared__ float4 s_sh4[];
+  const int rowf_all = ((a.c.sh_degree + 1) * (a.c.sh_degree + 1) - 1) * 3;
+  uint32_t* h = reinterpret_cast<uint32_t*>(s_sh4) + 8 * 32 * rowf_all;
   const bool smem = a.ntx * a.nty <= kHistTilesSmem;
   if (smem)
     for (int b = threadIdx.x; b < a.ntx * a.nty; b += blockDim.x) h[b] = 0;
@@ -624,7 +632,9 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
   p.status = status;
   {
     StageTimer st(FS4D_STAGE_PREPROCESS, s);
-    const size_t sh_smem = (size_t)8 * 32 * (((snap.sh_degree + 1) * (snap.sh_degree + 1) - 1) * 3) * 4;
+    const int ntl = p.ntx * p.nty;
+    const size_t sh_smem = (size_t)8 * 32 * (((snap.sh_degree + 1) * (snap.sh_degree + 1) - 1) * 3) * 4 +
+                           (size_t)(ntl <= kHistTilesSmem ? ntl : 0) * 4;
     static size_t sh_attr = 0;
     if (sh_smem > sh_attr) {
       cudaFuncSetAttribute(k_preprocess, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_smem);
