@@ -305,6 +305,13 @@ __global__ void k_depth_tie_fixup(const uint32_t* __restrict__ keys, uint32_t* _
   }
 }
 
+// 16-byte global -> shared copy that bypasses registers (cp.async, L2 only)
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
+               "l"(src)
+               : "memory");
+}
+
 struct BlendArgs {
   int H, W, ntx, D, c0;
   float alpha_cap, alpha_skip, stop;
@@ -407,23 +414,29 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   const int nf = DC > 0 ? min(DC, a.D - a.c0) : 0;
   const bool vec_ok = DC >= 4 && nf == DC && (a.D & 3) == 0 && (a.c0 & 3) == 0;
 
+  // the next batch's Gaussian index is loaded one batch ahead (its latency
+  // hides behind this batch's compositing instead of preceding the record
+  // loads); the records that need no transform (pixel rectangle, rgb +
+  // depth, feature quads) go global -> shared with cp.async, no registers
+  uint32_t g_next = rg.x + threadIdx.x < rg.y ? a.pvals[rg.x + threadIdx.x] : 0u;
   for (uint32_t b = rg.x; b < rg.y; b += NT) {
     if (__syncthreads_count(done) == NT) break;
 #ifdef FS4D_BLEND_TRACE
     ++nbatch;
 #endif
     const uint32_t j = b + threadIdx.x;
+    const uint32_t g = g_next;
+    if (j + NT < rg.y) g_next = a.pvals[j + NT];
     if (j < rg.y) {
-      const uint32_t g = a.pvals[j];
+      cp_async16(s_pr + threadIdx.x, a.pix_rect + g);
+      cp_async16(s_rgbz + threadIdx.x, a.rgbz + g);
       s_xy[threadIdx.x] = tile_rel_mean(a.xy[g], ox, oy);
       s_cs[threadIdx.x] = scaled_conic(a.conic_o[g]);
-      s_pr[threadIdx.x] = a.pix_rect[g];
-      s_rgbz[threadIdx.x] = a.rgbz[g];
       if (DC > 0) {
         const float* src = a.features + (int64_t)g * a.D + a.c0;
         if (vec_ok) {
 #pragma unroll
-          for (int c = 0; c < DC; c += 4) s_f4[(c / 4) * NT + threadIdx.x] = __ldg(reinterpret_cast<const float4*>(src + c));
+          for (int c = 0; c < DC; c += 4) cp_async16(s_f4 + (c / 4) * NT + threadIdx.x, src + c);
         } else {
           for (int c = 0; c < DC; c += 4) {
             float v[4];
@@ -433,6 +446,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
         }
       }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const int cnt = min((uint32_t)NT, rg.y - b);
     // warp-level culling: one ballot per 32 staged Gaussians keeps those whose
