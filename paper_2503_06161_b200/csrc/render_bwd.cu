@@ -270,8 +270,14 @@ __device__ __forceinline__ int ty_sub_rows(int sub) { return sub * (kTile / SUBB
 // shared memory, the CTA adds its warps in a fixed order at the end of each
 // staged batch and stores one partial per (pair, CTA) -- k_det_gather then
 // sums a Gaussian's partials in tile order: bitwise reproducible gradients.
+// (an index prefetch + cp.async staging as in k_blend was measured equal at
+// 8 CTAs/SM and slower unconstrained: 142 registers, 2.44 vs 1.96 ms / step)
 template <int DC, int PX, int SUBB, bool DET = false>
+#ifdef FS4D_BWD_MINB  // A/B knob: minimum resident CTAs per SM (caps registers)
+__global__ void __launch_bounds__(kTilePixels / PX / SUBB, FS4D_BWD_MINB) k_blend_bwd2(BwdArgs a) {
+#else
 __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs a) {
+#endif
   constexpr int NT = kTilePixels / PX / SUBB;
   constexpr int B = NT;  // Gaussians staged per batch
   constexpr int NF = DC > 0 ? DC : 1;
