@@ -96,6 +96,35 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // Q gets a 1e-3 relative and the column interval a 0.02 pixel margin, far
 // above the fp32 rounding of either side, so no Gaussian the exact per-pixel
 // test accepts is ever culled: the pixel decisions stay exactly k_blend's.
+// The per-Gaussian constants of the strip cull below, computed once when the
+// Gaussian is staged instead of by every warp that tests it: (Q, 1/a,
+// c - b^2/a, b/a) of the conic (a, b, c) and opacity; Q < 0 marks a Gaussian
+// whose opacity is below alpha_skip (it hits nothing).
+__device__ __forceinline__ float4 strip_consts(const float4& co, float alpha_skip) {
+  if (co.w < alpha_skip) return make_float4(-1.f, 0.f, 0.f, 0.f);
+  const float Q = fminf(kQSkip, 2.f * __logf(co.w * fast_rcp(alpha_skip))) * 1.001f + 1e-3f;
+  const float inv_a = fast_rcp(co.x);
+  return make_float4(Q, inv_a, co.z - co.y * co.y * inv_a, co.y * inv_a);
+}
+template <int NR>
+__device__ __forceinline__ bool strip_hits_c(const int4& pr, const float2& mm, const float4& sc, int r0, int c0) {
+  const float xlo = (float)max(c0, pr.x) - 0.02f, xhi = (float)min(c0 + kTile - 1, pr.y) + 0.02f;
+  bool hit = false;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int row = r0 + r;
+    if (row < pr.z || row > pr.w) continue;
+    const float dy = (float)row - mm.y;
+    const float qmin = sc.z * dy * dy;
+    if (!(qmin <= sc.x)) continue;
+    const float h = fast_sqrt((sc.x - qmin) * sc.y) + 0.02f;
+    const float xc = mm.x - sc.w * dy;
+    const float lo = fmaxf(xc - h, xlo), hi = fminf(xc + h, xhi);
+    hit |= ceilf(lo) <= floorf(hi);
+  }
+  return hit;
+}
+
 template <int NR>
 __device__ __forceinline__ bool strip_hits(const int4& pr, const float2& mm, const float4& co, int r0, int c0,
                                            float alpha_skip) {

@@ -370,19 +370,20 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
   unsigned nbatch = 0;
 #endif
   constexpr int NT = kTilePixels / SUB;  // threads = pixels = Gaussians per batch
-  // the staged batch as ONE shared array: 16-byte rows [3 + DC/4][NT] -- the
-  // scaled conic (gauss_power), the pixel rectangle, rgb + depth, then the
+  // the staged batch as ONE shared array: 16-byte rows [4 + DC/4][NT] -- the
+  // scaled conic (gauss_power), the pixel rectangle, rgb + depth, the strip-cull constants, then the
   // feature quads (channel-quad-major: conflict-free staging stores,
   // broadcast reads) -- and the tile-relative means (8 bytes each) after
   // them.  Reads of Gaussian k are [k * 16 + constant] / [k * 8 + constant]
   // off one base (with separate arrays ptxas rebuilt each array's
   // shared-window address inside the compositing loop)
-  constexpr int kRows = 3 + (DC > 0 ? DC / 4 : 0);
+  constexpr int kRows = 4 + (DC > 0 ? DC / 4 : 0);
   __shared__ __align__(16) float4 s_g[kRows * NT + NT / 2];
   float4* const s_cs = s_g;
   int4* const s_pr = reinterpret_cast<int4*>(s_g + NT);
   float4* const s_rgbz = s_g + 2 * NT;
-  float4* const s_f4 = s_g + 3 * NT;
+  float4* const s_sc = s_g + 3 * NT;  // strip-cull constants (strip_consts)
+  float4* const s_f4 = s_g + 4 * NT;
   float2* const s_xy = reinterpret_cast<float2*>(s_g + kRows * NT);
   // per-warp ballot masks of the staged batch (shared, not a local array)
   __shared__ unsigned s_mask[NT / 32][NT / 32];
@@ -431,7 +432,9 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
       cp_async16(s_pr + threadIdx.x, a.pix_rect + g);
       cp_async16(s_rgbz + threadIdx.x, a.rgbz + g);
       s_xy[threadIdx.x] = tile_rel_mean(a.xy[g], ox, oy);
-      s_cs[threadIdx.x] = scaled_conic(a.conic_o[g]);
+      const float4 cog = a.conic_o[g];
+      s_cs[threadIdx.x] = scaled_conic(cog);
+      s_sc[threadIdx.x] = strip_consts(cog, a.alpha_skip);
       if (DC > 0) {
         const float* src = a.features + (int64_t)g * a.D + a.c0;
         if (vec_ok) {
@@ -462,8 +465,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
         hit = pr.w >= wrow0 && pr.z <= wrow0 + 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
         if (hit) {
           const float2 mr = s_xy[kk];
-          hit = strip_hits<2>(pr, make_float2(mr.x + ox, mr.y + oy), unscaled_conic(s_cs[kk]), wrow0, tcol0,
-                              a.alpha_skip);
+          hit = strip_hits_c<2>(pr, make_float2(mr.x + ox, mr.y + oy), s_sc[kk], wrow0, tcol0);
         }
       }
       const unsigned msk = __ballot_sync(0xffffffffu, hit);
@@ -584,21 +586,33 @@ static void launch_blend_sub(int dc, int ntiles, const BlendArgs& a, cudaStream_
       case 4: k_blend<4, SUB, true><<<grid, nt, 0, s>>>(a); break;
       case 8: k_blend<8, SUB, true><<<grid, nt, 0, s>>>(a); break;
       case 16: k_blend<16, SUB, true><<<grid, nt, 0, s>>>(a); break;
-      default: k_blend<32, SUB, true><<<grid, nt, 0, s>>>(a); break;
+      default:  // (SUB 1: 256 pixels per CTA, slices capped at 16 channels -- blend_max_dc)
+        if constexpr (SUB > 1) k_blend<32, SUB, true><<<grid, nt, 0, s>>>(a);
+        break;
     }
   } else {  // further feature-channel slices of a D > 32 map
     switch (dc) {
       case 4: k_blend<4, SUB, false><<<grid, nt, 0, s>>>(a); break;
       case 8: k_blend<8, SUB, false><<<grid, nt, 0, s>>>(a); break;
       case 16: k_blend<16, SUB, false><<<grid, nt, 0, s>>>(a); break;
-      default: k_blend<32, SUB, false><<<grid, nt, 0, s>>>(a); break;
+      default:
+        if constexpr (SUB > 1) k_blend<32, SUB, false><<<grid, nt, 0, s>>>(a);
+        break;
     }
   }
 }
 
+static int blend_sub() {
+  static const int sub = getenv("FS4D_BLEND_SUB") ? atoi(getenv("FS4D_BLEND_SUB")) : 2;
+  return sub;
+}
+// widest feature slice of one blend launch: the 256-thread variant (SUB 1)
+// stages 256 Gaussians per batch and fits 16 channels in 48 KB of shared memory
+static int blend_max_dc() { return blend_sub() == 1 ? 16 : 32; }
+
 static void launch_blend(int dc, int ntiles, const BlendArgs& a, cudaStream_t s) {
   // (two pixels per thread was measured slower: 157-165 vs 150 us)
-  static const int sub = getenv("FS4D_BLEND_SUB") ? atoi(getenv("FS4D_BLEND_SUB")) : 2;
+  const int sub = blend_sub();
   if (sub == 4) launch_blend_sub<4>(dc, ntiles, a, s);
   else if (sub == 1) launch_blend_sub<1>(dc, ntiles, a, s);
   else launch_blend_sub<2>(dc, ntiles, a, s);
@@ -695,7 +709,7 @@ int render_forward(const Fs4dCloud& snap, const Fs4dCamera& cam, const Fs4dRaste
     int c0 = 0;
     do {
       int rem = b.D - c0;
-      int dc = rem <= 0 ? 0 : rem <= 4 ? 4 : rem <= 8 ? 8 : rem <= 16 ? 16 : 32;
+      int dc = rem <= 0 ? 0 : rem <= 4 ? 4 : rem <= 8 ? 8 : rem <= 16 ? 16 : blend_max_dc();
       b.c0 = c0;
       launch_blend(dc, L.ntiles, b, s);
       c0 += dc;
