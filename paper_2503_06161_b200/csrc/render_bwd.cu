@@ -284,17 +284,19 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
   constexpr int NVMAX = 10 + NF;
   __shared__ float s_acc[DET ? (NT / 32) * B * NVMAX : 1];
   // the staged batch as ONE shared array (reads of Gaussian k off one base
-  // with immediate offsets, as in k_blend): 16-byte rows [4 + DC/4][B] --
+  // with immediate offsets, as in k_blend): 16-byte rows [5 + DC/4][B] --
   // conic + opacity, scaled conic (gauss_power, same evaluation as the
-  // forward), pixel rectangle, rgb + depth, feature quads (channel-quad-
+  // forward), pixel rectangle, rgb + depth, strip-cull constants (once per
+  // staged Gaussian, not per warp), feature quads (channel-quad-
   // major) -- then the tile-relative means (8 B) and the source indices
-  constexpr int kRows = 4 + (DC > 0 ? (DC + 3) / 4 : 0);
+  constexpr int kRows = 5 + (DC > 0 ? (DC + 3) / 4 : 0);
   __shared__ __align__(16) float4 s_stage[kRows * B + B / 2 + B / 4];
   float4* const s_co = s_stage;
   float4* const s_cs = s_stage + B;
   int4* const s_pr = reinterpret_cast<int4*>(s_stage + 2 * B);
   float4* const s_rgbz = s_stage + 3 * B;
-  float4* const s_f4 = s_stage + 4 * B;
+  float4* const s_sc = s_stage + 4 * B;  // strip-cull constants (strip_consts)
+  float4* const s_f4 = s_stage + 5 * B;
   float2* const s_xy = reinterpret_cast<float2*>(s_stage + kRows * B);
   uint32_t* const s_g = reinterpret_cast<uint32_t*>(s_stage + kRows * B + B / 2);
   constexpr int NROW = (10 + DC + 1) / 2;  // per-Gaussian values, in float2 rows
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
       const float4 cog = a.conic_o[g];
       s_co[threadIdx.x] = cog;
       s_cs[threadIdx.x] = scaled_conic(cog);
+      s_sc[threadIdx.x] = strip_consts(cog, a.alpha_skip);
       s_pr[threadIdx.x] = a.pix_rect[g];
       s_rgbz[threadIdx.x] = a.rgbz[g];
       if (DC > 0) {
@@ -410,7 +413,7 @@ __global__ void __launch_bounds__(kTilePixels / PX / SUBB) k_blend_bwd2(BwdArgs 
           hit = pr.w >= wrow0 && pr.z <= wrow0 + 2 * PX - 1 && pr.y >= tcol0 && pr.x <= tcol0 + kTile - 1;
           if (hit) {
             const float2 mr = s_xy[kk];
-            hit = strip_hits<2 * PX>(pr, make_float2(mr.x + ox, mr.y + oy), s_co[kk], wrow0, tcol0, a.alpha_skip);
+            hit = strip_hits_c<2 * PX>(pr, make_float2(mr.x + ox, mr.y + oy), s_sc[kk], wrow0, tcol0);
           }
         }
         bits = __ballot_sync(0xffffffffu, hit);
