@@ -15,6 +15,7 @@ reference API unchanged.
 """
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -653,7 +654,11 @@ class SequenceRenderer:
     rotation exceeds L2 and no cache flush is needed between frames)."""
 
     def __init__(self, cloud, field, net, height, width, cfg, pipelines=2, streams=2, replicas=1, device="cuda"):
-        self.streams = [torch.cuda.Stream(device=device) for _ in range(streams)]
+        # FS4D_SEQ_PRIO=1: stream i gets scheduling priority -i (clamped to the
+        # device range), so one frame leads and the others fill its gaps
+        prio = os.environ.get("FS4D_SEQ_PRIO", "0") == "1"
+        lo, hi = torch.cuda.Stream.priority_range() if prio else (0, 0)
+        self.streams = [torch.cuda.Stream(device=device, priority=max(hi, -i) if prio else 0) for i in range(streams)]
         self.pipes = []
         for p in range(pipelines):
             if replicas > 1 and p % replicas:
