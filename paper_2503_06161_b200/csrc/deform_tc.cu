@@ -177,7 +177,11 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPla
 // and the MLP's epilogue threads move the rows into its operand image with
 // asynchronous 16-byte copies, never touching them in registers.
 template <int LEVELS, bool IMG = false>
+#ifdef FS4D_GATHER_MINB  // A/B knob: minimum resident CTAs per SM (caps registers; unset: ptxas picks 56)
+__global__ void __launch_bounds__(kGatherWarps * 32, FS4D_GATHER_MINB) k_hexplane_latent_c32t(TcPlan p, int64_t K,
+#else
 __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPlan p, int64_t K,
+#endif
                                                                               const float* __restrict__ pos,
                                                                               const float* __restrict__ rows,
                                                                               float* __restrict__ latent,
