@@ -176,12 +176,14 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32(TcPla
 // Morton order turns into partial-sector writes and ECC read-modify-writes),
 // and the MLP's epilogue threads move the rows into its operand image with
 // asynchronous 16-byte copies, never touching them in registers.
-template <int LEVELS, bool IMG = false>
-#ifdef FS4D_GATHER_MINB  // A/B knob: minimum resident CTAs per SM (caps registers; unset: ptxas picks 56)
-__global__ void __launch_bounds__(kGatherWarps * 32, FS4D_GATHER_MINB) k_hexplane_latent_c32t(TcPlan p, int64_t K,
-#else
-__global__ void __launch_bounds__(kGatherWarps * 32) k_hexplane_latent_c32t(TcPlan p, int64_t K,
+// Minimum resident CTAs per SM: 9 (56 registers, as ptxas picks unbounded,
+// but scheduled for that occupancy) measured 69.8 -> 65.8 us, twice; 10 (48
+// registers) 72 us, 12 spills; an explicit 1 lets ptxas take 118 registers.
+#ifndef FS4D_GATHER_MINB
+#define FS4D_GATHER_MINB 9
 #endif
+template <int LEVELS, bool IMG = false>
+__global__ void __launch_bounds__(kGatherWarps * 32, FS4D_GATHER_MINB) k_hexplane_latent_c32t(TcPlan p, int64_t K,
                                                                               const float* __restrict__ pos,
                                                                               const float* __restrict__ rows,
                                                                               float* __restrict__ latent,
@@ -1547,6 +1549,15 @@ int deform_forward_tc(const Fs4dCloud& cloud, const Fs4dHexPlane& field, const F
   uint8_t* img = reinterpret_cast<uint8_t*>(latent);
   StageTimer st_gather(fused ? -1 : FS4D_STAGE_DEFORM_GATHER, s);
   if (!fused) {
+    // FS4D_GATHER_CARVEOUT (A/B knob): shared-memory carveout preference in
+    // percent -- fewer resident CTAs for a larger L1 (the plane corners
+    // neighbouring Gaussians share)
+    static const int carve = getenv("FS4D_GATHER_CARVEOUT") ? atoi(getenv("FS4D_GATHER_CARVEOUT")) : -1;
+    static bool carve_set = false;
+    if (carve >= 0 && !carve_set) {
+      cudaFuncSetAttribute(k_hexplane_latent_c32t<2, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+      carve_set = true;
+    }
     if (two_slot)
       k_hexplane_latent_c32t<2, true><<<gblocks, kGatherWarps * 32, 0, s>>>(
           p, K, cloud.positions, reinterpret_cast<const float*>(blob + p.off_rows), nullptr, img);
