@@ -164,7 +164,12 @@ constexpr int kEmitThreads = FS4D_EMIT_THREADS;
 // (global offsets, densest-first order, pair total, status) -- one launch and
 // one serial single-block kernel fewer on the frame's critical path.
 template <bool FUSED>
-__global__ void __launch_bounds__(kEmitThreads) k_emit_partition(const int4* __restrict__ tile_rect,
+#ifdef FS4D_EMIT_MINB  // A/B knob: minimum resident CTAs per SM
+__global__ void __launch_bounds__(kEmitThreads, FS4D_EMIT_MINB) k_emit_partition(
+#else
+__global__ void __launch_bounds__(kEmitThreads) k_emit_partition(
+#endif
+const int4* __restrict__ tile_rect,
                                                         const uint32_t* __restrict__ dkeys, int64_t K, int ntx,
                                                         int ntiles, uint64_t* __restrict__ toff,
                                                         uint32_t* __restrict__ tcur, int64_t cap,
@@ -602,7 +607,12 @@ __device__ __forceinline__ void warp_sort_small_tile(int tile, const unsigned lo
   if (lane < n) pvals[off + lane] = (uint32_t)key;
 }
 
-__global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(unsigned long long* __restrict__ pkey,
+#ifdef FS4D_SORT_MINB  // A/B knob: minimum resident CTAs per SM
+__global__ void __launch_bounds__(kTileSortThreads, FS4D_SORT_MINB) k_tile_sort(
+#else
+__global__ void __launch_bounds__(kTileSortThreads) k_tile_sort(
+#endif
+unsigned long long* __restrict__ pkey,
                                                                 const uint64_t* __restrict__ toff,
                                                                 const uint32_t* __restrict__ tcnt, int ntiles,
                                                                 int64_t cap, const double* __restrict__ z64,
