@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(kTilePixels / SUB) k_blend(BlendArgs a) {
         // (instruction-level parallelism across the smem loads and ex2), only
         // the compositing below is a serial chain -- same decisions, same order
 #ifndef FS4D_BLEND_BK
-#define FS4D_BLEND_BK 4  // measured blend stage: 2 -> 105 us, 4 -> 99 us, 8 -> 122 us
+#define FS4D_BLEND_BK 3  // measured blend stage (round 2, tools/gpu_final.sh): 3 -> 86.8 us, 4 -> 89.5, 5 -> 90.2, 6 -> 93.0
 #endif
         constexpr int BK = FS4D_BLEND_BK;
         while (bits) {
